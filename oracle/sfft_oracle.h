@@ -1,0 +1,106 @@
+/*
+ * sfft_oracle.h -- TEST INFRASTRUCTURE ONLY (not the product path).
+ *
+ * Plain, slow, literal CPU oracle of the multidimensional phase-shift sparse FFT
+ * (arXiv 1606.07407, Algorithm 2 "MultiPhaseshift").  Only
+ * tests/, __graft_entry__.smoke() and bench.py (cpu_baseline leg and
+ * --impl reference) may load this library.  It shares no code, header, table or
+ * constant generator with paper_1606_07407_b200/ and never calls it.
+ *
+ * Every value is double / int64; no -ffast-math.  Phases are reduced exactly in
+ * integers (reading R1 / SURVEY 8(c) C1): the sample point
+ * t = (h/p) e_m + (1/E) e_n (reduced, possibly tilted coordinates) gives each
+ * mode the phase  ((h * (v_m mod p)) mod p)/p + (v_n mod E)/E  in [0, 2).
+ */
+#ifndef SFFT_ORACLE_H
+#define SFFT_ORACLE_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Solver parameters (Algorithm 2 inputs "f, c, k, N, d, d1, d2, eps", PAPER.md:377,
+ * plus the readings of SURVEY 8(c) C3, C14, C15, C17-C19). */
+typedef struct {
+  int32_t d;
+  int32_t k;
+  int64_t N;
+  int32_t r;                 /* number of blocks of the partition */
+  const int32_t* blocks;     /* [r] d_1..d_r, sum = d */
+  int32_t n_tilts;
+  const int64_t* tilts;      /* [n_tilts][5]: axis0, axis1, base, height, hypo (Eq. (25)) */
+  int64_t E;                 /* 1/eps; 0 -> 2 * B * max(base+height) */
+  int32_t c;                 /* prime factor (5) */
+  double tol;                /* collision tolerance tau, default 1e-6 */
+  double bin_floor_rel;      /* |F_0[b]| < bin_floor_rel * p -> empty bin (C18), 1e-8 */
+  double prune_floor;        /* prune |a| < prune_floor (C17), 1e-8 */
+  double round_tol;          /* reject |x - round(x)| > round_tol (C14), 0.01 */
+  int32_t max_iter;          /* 1000 */
+  int32_t stall_limit;       /* 0 -> max(2r, 16) (C19) */
+  int32_t extra_checks;      /* bit0 range check, bit1 bin consistency (C15) */
+  int32_t n_primes;          /* explicit prime schedule p_i = primes[(i-1) mod n] */
+  const int64_t* primes;     /* NULL -> i-th prime >= max(2, c k*) (Alg. 2 l.8) */
+} oracle_params;
+
+enum { ORACLE_OK = 0, ORACLE_PARTIAL = 1, ORACLE_EINVAL = -1, ORACLE_EPRECISION = -2,
+       ORACLE_ECORRUPT = -4, ORACLE_ENOMEM = -6 };
+
+/* ---- index maps (Eqs. (19), (27), (31), (35), (36)) ---- */
+int oracle_unwrap_freq(int32_t d, int64_t N, int32_t r, const int32_t* blocks,
+                       const int32_t* w /*[d]*/, int64_t* u /*[r]*/);
+int oracle_wrap_freq(int32_t d, int64_t N, int32_t r, const int32_t* blocks,
+                     const int64_t* u /*[r]*/, int32_t* w /*[d]*/);
+void oracle_block_range(int64_t N, int32_t dq, int64_t* lo, int64_t* hi);
+void oracle_tilt_freq(int64_t base, int64_t height, int64_t w1, int64_t w2, int64_t* out /*[2]*/);
+int oracle_untilt_freq(int64_t base, int64_t height, int64_t hypo, int64_t v1, int64_t v2,
+                       int64_t* out /*[2]*/);
+/* time embedding Eq. (36): t[off_q + s] = N^s * t_red[q] */
+void oracle_unwrap_time(int32_t d, int64_t N, int32_t r, const int32_t* blocks,
+                        const double* t_red /*[r]*/, double* t /*[d]*/);
+
+/* ---- primes (Alg. 2 l.8) ---- */
+int64_t oracle_ith_prime_at_least(int64_t x, int32_t i);
+
+/* ---- plan-level derived quantities ---- */
+int oracle_prepare(const oracle_params* P, int64_t* E_out, int64_t* lo /*[r]*/, int64_t* hi /*[r]*/);
+/* v_j = T * unwrap(w_j): reduced (tilted) frequencies of k modes, v [k][r] */
+int oracle_project(const oracle_params* P, const int32_t* w /*[k][d]*/, int32_t k, int64_t* v /*[k][r]*/);
+
+/* ---- evaluation of f at a point (Eq. (9)) ---- */
+/* f(t) = sum_j a_j exp(2 pi i w_j . t) at a real point t in R^d, plain double arithmetic
+ * (used only to pin the exact-phase evaluation on tiny inputs). */
+void oracle_eval_point(int32_t d, int32_t K, const int32_t* w /*[K][d]*/, const double* a /*[K][2]*/,
+                       const double* t /*[d]*/, double* out /*[2]*/);
+/* One sample line (Eq. (41), Alg. 2 l.13-14): s[h] = sum_j c_j exp(2 pi i v_j . t_h),
+ * t_h = (h/p) e_m + (1/E) e_n  (n < 0: unshifted).  Exact integer phase reduction. */
+void oracle_sample_line(int32_t K, int32_t r, const int64_t* v /*[K][r]*/, const double* c /*[K][2]*/,
+                        int64_t p, int32_t m, int32_t n, int64_t E, double* s /*[p][2]*/);
+
+/* ---- DFT (Eq. (3)): F[b] = sum_h s[h] exp(-2 pi i h b / p), direct O(p^2) ---- */
+void oracle_dft(int64_t p, const double* s /*[p][2]*/, double* F /*[p][2]*/);
+
+/* ---- select + test + decode of one iteration (Alg. 2 l.18-32) ----
+ * F: [(r+1)][p][2], line 0 unshifted, line 1+n shifted along reduced axis n.
+ * Writes accepted bins in ascending b: acc_b [<=kstar], acc_v [<=kstar][r], acc_a [<=kstar][2].
+ * Returns the number of accepted bins; *n_cand receives the number of examined bins. */
+int32_t oracle_decode(const oracle_params* P, int64_t E, const int64_t* lo, const int64_t* hi,
+                      int64_t p, int32_t m, int32_t kstar, const double* F,
+                      int32_t* n_cand, int32_t* acc_b, int64_t* acc_v, double* acc_a);
+
+/* ---- the whole of Algorithm 2 for one signal ----
+ * out_w [k][d] int32 (canonical lexicographic order), out_a [k][2], out_count.
+ * trace [trace_cap][5] = (i, p, m, n_candidates, n_accepted) per iteration. */
+int oracle_solve(const oracle_params* P, const int32_t* w /*[k][d]*/, const double* a /*[k][2]*/,
+                 int32_t* out_w, double* out_a, int32_t* out_count, int64_t* out_samples,
+                 int32_t* out_iters, int32_t trace_cap, int64_t* trace);
+
+/* Independent signals spread over n_threads host threads (one solve per thread at a time). */
+int oracle_solve_batch(const oracle_params* P, int32_t batch, const int32_t* w, const double* a,
+                       int32_t* out_w, double* out_a, int32_t* out_count, int64_t* out_samples,
+                       int32_t* out_iters, int32_t* out_status, int32_t n_threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
