@@ -1,0 +1,186 @@
+/*
+ * sfft.h -- C ABI of the B200-native multidimensional phase-shift sparse FFT
+ * (arXiv 1606.07407, Algorithm 2 "MultiPhaseshift").
+ *
+ * Library: paper_1606_07407_b200/libsfft.so (CUDA, sm_100a).  Every step of the
+ * hot path runs in hand-written kernels; there is no CPU fallback.
+ *
+ * Conventions
+ *   - "device" pointers are CUDA device memory on the plan's device; "host"
+ *     pointers are ordinary (preferably pinned) host memory.
+ *   - complex numbers are interleaved (re, im) doubles.
+ *   - All calls are asynchronous on the plan's stream unless stated; they return
+ *     an sfft_status.  Nothing is thrown across the ABI.  On error
+ *     sfft_last_error(plan) holds a one-line message.
+ *   - A plan is bound to one device and one stream; it is not thread-safe.
+ */
+#ifndef SFFT_H
+#define SFFT_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define SFFT_API __attribute__((visibility("default")))
+#else
+#define SFFT_API
+#endif
+
+typedef enum {
+  SFFT_OK = 0,
+  SFFT_PARTIAL = 1,        /* max_iter or stall reached; outputs hold the current registry */
+  SFFT_EINVAL = -1,        /* invalid argument (d<1, N odd or <2, sum of blocks != d, k<1, bad tilt, 1/eps not an integer, ...) */
+  SFFT_EPRECISION = -2,    /* N^{d_q} > 2^40 or E > 2^42 (reading R1) */
+  SFFT_EDIM = -3,          /* signal batch larger than the plan's batch */
+  SFFT_ECORRUPT = -4,      /* untilt not integral / wrapped frequency outside the box (Alg. 3 l.39) */
+  SFFT_ECUDA = -5,
+  SFFT_ENOMEM = -6,
+  SFFT_ENCCL = -7,
+  SFFT_ENOTSUP = -8        /* prime larger than the FFT size table supports */
+} sfft_status;
+
+/* Eq. (25)/(27) tilt of the reduced-axis pair (axis0, axis1): sin = height/hypo, cos = base/hypo.
+ * Frequencies on the pair map to (base*u0 - height*u1, height*u0 + base*u1). */
+typedef struct {
+  int32_t axis0, axis1;
+  int64_t base, height, hypo;
+} sfft_tilt;
+
+/* Options; pass NULL to sfft_plan for the defaults in brackets. */
+typedef struct {
+  int32_t n_blocks;           /* partition d = d_1 + ... + d_r; 0 -> uniform largest d_1 | d with N^{d_1} <= 2^40 */
+  const int32_t* block_dims;  /* host [n_blocks] */
+  int32_t c;                  /* prime factor c of Alg. 2 l.8 [5, P:422] */
+  double tol;                 /* collision tolerance tau [1e-6] */
+  double bin_floor_rel;       /* empty-bin floor relative to p [1e-8] */
+  double prune_floor;         /* registry prune floor [1e-8] (Alg. 2 l.33) */
+  double round_tol;           /* max |x - round(x)| of a decoded coordinate [0.01] */
+  int32_t max_iter;           /* [1000] */
+  int32_t stall_limit;        /* [max(2r, 16)] */
+  int32_t batch;              /* max signals per execute [1] */
+  int32_t extra_checks;       /* bit0 range check, bit1 bin consistency [3] */
+  void* stream;               /* cudaStream_t [legacy default stream] */
+} sfft_options;
+
+/* Per-execute report (host struct). Aggregates over the batch. */
+typedef struct {
+  int64_t samples_used;        /* sum over signals of (r+1)*p per iteration (f evaluations) */
+  int64_t cmacs;               /* complex multiply-adds done by the exp-sum kernel */
+  int32_t iterations;          /* iterations of the batch loop */
+  int32_t n_ok, n_partial, n_error;
+  int32_t status;              /* worst status over the batch */
+  int32_t n_iter_logged;
+  int64_t primes[64];          /* prime of signal 0 per iteration */
+  int32_t accepted[64];        /* bins accepted for signal 0 per iteration */
+  int32_t kernel_launches;     /* kernels launched by this execute */
+} sfft_report;
+
+typedef struct sfft_plan_s sfft_plan_t;
+typedef struct sfft_signal_s sfft_signal_t;
+
+/*
+ * sfft_plan -- validate the problem and choose partition, E, prime table, FFT sizes
+ * and tile shapes (Eqs. (35)-(36) P:321-331).
+ *   d, N, k      dimension, per-axis bandwidth (omega in [-N/2, N/2)^d, N even >= 2), sparsity
+ *   primes       host [n_primes] explicit prime schedule p_i = primes[(i-1) mod n_primes], or NULL for
+ *                the paper's rule p_i = i-th prime >= max(2, c k*) (Alg. 2 l.8)
+ *   tilts        host [n_tilts] static tilts on disjoint reduced-axis pairs (Eq. (27)), or NULL
+ *   eps          shift; 0 -> 1/(2 B max(base+height)) with B = max_q N^{d_q}; else 1/eps must be an integer
+ *   opt          host, nullable
+ *   out          receives the plan.  The plan needs workspace: either call sfft_plan_set_workspace
+ *                with caller-owned device memory of sfft_plan_workspace_size() bytes, or the first
+ *                execute allocates it with cudaMalloc (owned by the plan).
+ */
+SFFT_API int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_primes,
+              const sfft_tilt* tilts, int32_t n_tilts, double eps, const sfft_options* opt,
+              sfft_plan_t** out);
+SFFT_API int sfft_plan_workspace_size(const sfft_plan_t* plan, size_t* bytes);
+/* dptr: device memory of >= workspace_size bytes, 256-byte aligned, owned by the caller, must
+ * outlive the plan. */
+SFFT_API int sfft_plan_set_workspace(sfft_plan_t* plan, void* dptr, size_t bytes);
+/* Query plan-derived values (host): E, r, number of lines L = r+1, p_max supported, tile shape. */
+SFFT_API int sfft_plan_info(const sfft_plan_t* plan, int64_t* E, int32_t* r, int32_t* L, int64_t* p_max,
+                   int32_t* tile_n);
+SFFT_API void sfft_plan_destroy(sfft_plan_t* plan);
+
+/*
+ * sfft_signal_expsum -- the exponential-sum signal f(t) = sum_j a_j e^{2 pi i omega_j . t}
+ * (Eq. (9)) of `batch` independent signals with k modes each.
+ *   freqs   device int32 [batch][k][d]
+ *   coeffs  device double [batch][k][2]
+ * The handle references (does not copy) the arrays: they must stay valid until the last
+ * sfft_execute using it has completed on the stream.  The product path reads them only to
+ * evaluate f at sample points (SURVEY 8(a) leak rule).
+ */
+SFFT_API int sfft_signal_expsum(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, const double* coeffs,
+                       sfft_signal_t** out);
+SFFT_API void sfft_signal_destroy(sfft_signal_t* sig);
+
+/*
+ * sfft_execute -- run Algorithm 2 to completion on every signal of the batch.
+ *   out_freqs   device int32 [batch][k][d]  recovered frequency vectors, canonical (lexicographic) order
+ *   out_coeffs  device double [batch][k][2]
+ *   out_count   device int32 [batch]        number of recovered modes (<= k)
+ *   out_status  device int32 [batch] or NULL  per-signal sfft_status
+ *   rep         host, nullable
+ * Returns SFFT_OK when every signal recovered k modes, SFFT_PARTIAL if some stalled / hit
+ * max_iter (outputs hold their registries), or an error.  Synchronises the plan's stream once
+ * per iteration (a 16-byte control read).
+ */
+SFFT_API int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs, double* out_coeffs,
+                 int32_t* out_count, int32_t* out_status, sfft_report* rep);
+
+/*
+ * sfft_solve_host -- end-to-end call with HOST buffers: copies the signal to the device, runs
+ * sfft_execute, copies the result back; returns after the result is on the host.
+ *   freqs host int32 [batch][k][d], coeffs host double [batch][k][2] (pinned for full speed);
+ *   out_* host, same shapes as sfft_execute.
+ */
+SFFT_API int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, const double* coeffs,
+                    int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
+                    sfft_report* rep);
+
+/* ---- stage entry points (teacher-forced parity of single steps; same kernels as execute) ---- */
+
+/*
+ * sfft_stage_expsum -- a3: lines of one iteration of ONE signal.
+ *   v      device int64 [r][K] reduced (tilted) frequencies of the K terms (column j = term j)
+ *   c      device double [K][2] term coefficients (signal a_j, registry -a_e)
+ *   p, m   prime and projection axis
+ *   s_out  device double [L][p][2]: line 0 unshifted, line 1+n shifted by 1/E along reduced axis n:
+ *          s_n[h] = sum_j c_j exp(2 pi i v_j . ((h/p) e_m + (1/E) e_n))   (Eq. (41), exact phase)
+ */
+SFFT_API int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const double* c, int64_t p,
+                      int32_t m, double* s_out);
+/*
+ * sfft_stage_pfft -- a4: n_lines unnormalised forward DFTs of length p (Eq. (3)), in place.
+ *   x      device double [n_lines][p][2]
+ */
+SFFT_API int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x);
+/*
+ * sfft_stage_decode -- a5+a6: select, collision-test and decode the bins of one iteration.
+ *   F      device double [L][p][2]
+ *   outputs (device): acc_b int32 [kstar], acc_v int64 [r][kstar], acc_a double [kstar][2],
+ *   counts int32 [2] = (n_candidates, n_accepted).  Accepted bins in ascending b.
+ */
+SFFT_API int sfft_stage_decode(sfft_plan_t* plan, int64_t p, int32_t m, int32_t kstar, const double* F,
+                      int32_t* acc_b, int64_t* acc_v, double* acc_a, int32_t* counts);
+/* a1 on its own: v [batch][r][k] (device int64) of a signal (unwrap Eq. (35) + tilt Eq. (27)). */
+SFFT_API int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int64_t* v_out);
+
+/* Multi-GPU: signal sharding needs no communicator; line sharding is NEXT. */
+SFFT_API int sfft_comm_init(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* nccl_unique_id,
+                   int32_t shard_mode);
+
+SFFT_API const char* sfft_strerror(int status);
+SFFT_API const char* sfft_last_error(const sfft_plan_t* plan);
+/* Library build identification (e.g. "sfft sm_100a <git>"). */
+SFFT_API const char* sfft_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

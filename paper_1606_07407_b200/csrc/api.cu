@@ -1,0 +1,673 @@
+// api.cu -- the C ABI (include/sfft.h): plan, workspace, the host-side
+// iteration driver of Algorithm 2 and the stage entry points.
+#include <algorithm>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <new>
+
+#include "sfft_internal.cuh"
+
+using namespace sfft;
+
+#ifndef SFFT_GIT
+#define SFFT_GIT "dev"
+#endif
+
+struct sfft_signal_s {
+  sfft_plan_t* plan;
+  int32_t batch;
+  const int32_t* freqs;
+  const double* coeffs;
+};
+
+namespace {
+
+struct FftSize {
+  int M;
+  std::vector<int8_t> radix;
+};
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+}  // namespace
+
+struct sfft_plan_s {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  // problem
+  int32_t d = 0, k = 0, r = 0, L = 0, Lp = 0, kk = 0, H = 0, batch = 1;
+  int64_t N = 0, E = 0;
+  std::vector<int32_t> blocks, block_off, axis_tilt;
+  std::vector<int64_t> lo, hi, tilts, sched;
+  // options
+  int32_t c = 5, max_iter = 1000, stall_limit = 0, extra = 3;
+  double tol = 1e-6, floor_rel = 1e-8, prune = 1e-8, round_tol = 0.01;
+  // tables
+  std::vector<int32_t> primes;
+  int32_t p_cap = 0;
+  int64_t p_stride = 0, M_stride = 0;
+  std::vector<FftSize> fft;
+  ExpsumShape shape{};
+  // workspace
+  size_t ws_bytes = 0;
+  void* ws = nullptr;
+  bool ws_owned = false;
+  bool tables_ready = false;
+  size_t off[64] = {0};
+  int32_t* h_ctrl = nullptr;   // pinned
+  std::string err;
+};
+
+namespace {
+
+enum Buf {
+  B_BLOCKS, B_BOFF, B_LO, B_HI, B_TILTS, B_AXT, B_SCHED, B_PRIMES, B_FFTM, B_FFTR, B_FFTN,
+  B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
+  B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
+  B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE,
+  B_COUNT
+};
+
+int fail(sfft_plan_t* P, int code, const char* fmt, ...) {
+  if (P) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    P->err = buf;
+  }
+  return code;
+}
+
+#define CUDA_TRY(P, call)                                                                         \
+  do {                                                                                            \
+    cudaError_t _e = (call);                                                                      \
+    if (_e != cudaSuccess) return fail((P), SFFT_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+  } while (0)
+
+bool is_7smooth(int x) {
+  for (int f : {2, 3, 5, 7})
+    while (x % f == 0) x /= f;
+  return x == 1;
+}
+
+FftSize radix_plan(int M) {
+  FftSize s;
+  s.M = M;
+  int e[8] = {0};
+  int x = M;
+  for (int f : {2, 3, 5, 7})
+    while (x % f == 0) { x /= f; ++e[f]; }
+  while (e[2] >= 3) { s.radix.push_back(8); e[2] -= 3; }
+  if (e[2] == 2) s.radix.push_back(4);
+  if (e[2] == 1) s.radix.push_back(2);
+  for (int i = 0; i < e[7]; ++i) s.radix.push_back(7);
+  for (int i = 0; i < e[5]; ++i) s.radix.push_back(5);
+  for (int i = 0; i < e[3]; ++i) s.radix.push_back(3);
+  return s;
+}
+
+size_t fft_smem_bytes(int M) { return 16 * ((size_t)M + 128 + (M + 127) / 128 + 2); }
+
+int64_t gcd64(int64_t a, int64_t b) {
+  a = a < 0 ? -a : a;
+  b = b < 0 ? -b : b;
+  while (b) { int64_t t = a % b; a = b; b = t; }
+  return a;
+}
+
+void layout(sfft_plan_t* P) {
+  const size_t S = (size_t)P->batch;
+  size_t sz[B_COUNT] = {0};
+  sz[B_BLOCKS] = 4 * (size_t)P->r;
+  sz[B_BOFF] = 4 * (size_t)P->r;
+  sz[B_LO] = 8 * (size_t)P->r;
+  sz[B_HI] = 8 * (size_t)P->r;
+  sz[B_TILTS] = 8 * std::max<size_t>(P->tilts.size(), 1);
+  sz[B_AXT] = 4 * (size_t)P->r;
+  sz[B_SCHED] = 8 * std::max<size_t>(P->sched.size(), 1);
+  sz[B_PRIMES] = 4 * P->primes.size();
+  sz[B_FFTM] = 4 * P->fft.size();
+  sz[B_FFTR] = (size_t)kMaxFftPasses * P->fft.size();
+  sz[B_FFTN] = 4 * P->fft.size();
+  sz[B_VALL] = 8 * S * P->r * P->kk;
+  sz[B_CALL] = 16 * S * P->kk * P->Lp;
+  sz[B_LINES] = 16 * S * P->L * P->p_stride;
+  sz[B_WTAB] = 16 * S * P->p_stride;
+  sz[B_CHIRP] = 16 * S * P->p_stride;
+  sz[B_V] = 16 * S * P->M_stride;
+  sz[B_AREG] = 16 * S * P->k;
+  sz[B_KHASH] = 8 * S * P->k;
+  sz[B_HTAB] = 4 * S * P->H;
+  sz[B_ACCV] = 8 * S * P->r * P->k;
+  sz[B_ACCA] = 16 * S * P->k;
+  sz[B_WTMP] = 4 * S * P->k * P->d;
+  for (int b : {B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS}) sz[b] = 4 * S;
+  sz[B_SAMPLES] = 8 * S;
+  sz[B_CMACS] = 8 * S;
+  sz[B_LOG] = 4 * 2 * kLogIters;
+  sz[B_CTRL] = 16;
+  sz[B_IN_F] = 4 * S * P->k * P->d;
+  sz[B_IN_C] = 16 * S * P->k;
+  sz[B_OUT_F] = 4 * S * P->k * P->d;
+  sz[B_OUT_C] = 16 * S * P->k;
+  sz[B_OUT_N] = 4 * S;
+  sz[B_OUT_S] = 4 * S;
+  sz[B_STAGE] = 64;
+  size_t o = 0;
+  for (int b = 0; b < B_COUNT; ++b) {
+    P->off[b] = o;
+    o = align_up(o + std::max<size_t>(sz[b], 16), 256);
+  }
+  P->ws_bytes = o;
+}
+
+template <typename T>
+T* ptr(const sfft_plan_t* P, int b) {
+  return reinterpret_cast<T*>(static_cast<char*>(P->ws) + P->off[b]);
+}
+
+DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
+  DevParams D;
+  memset(&D, 0, sizeof D);
+  D.d = P->d; D.k = P->k; D.r = P->r; D.L = P->L; D.Lp = P->Lp; D.kk = P->kk; D.H = P->H;
+  D.batch = batch;
+  D.N = P->N; D.E = P->E;
+  D.c = P->c; D.max_iter = P->max_iter; D.stall_limit = P->stall_limit; D.extra = P->extra;
+  D.n_sched = (int32_t)P->sched.size();
+  D.tol = P->tol; D.floor_rel = P->floor_rel; D.prune = P->prune; D.round_tol = P->round_tol;
+  D.n_tilts = (int32_t)(P->tilts.size() / 5);
+  D.p_cap = P->p_cap;
+  D.p_stride = P->p_stride; D.M_stride = P->M_stride;
+  D.block_dims = ptr<int32_t>(P, B_BLOCKS);
+  D.block_off = ptr<int32_t>(P, B_BOFF);
+  D.lo = ptr<int64_t>(P, B_LO);
+  D.hi = ptr<int64_t>(P, B_HI);
+  D.tilts = ptr<int64_t>(P, B_TILTS);
+  D.axis_tilt = ptr<int32_t>(P, B_AXT);
+  D.sched = ptr<int64_t>(P, B_SCHED);
+  D.primes = ptr<int32_t>(P, B_PRIMES);
+  D.n_primes = (int32_t)P->primes.size();
+  D.fft_M = ptr<int32_t>(P, B_FFTM);
+  D.fft_radix = ptr<int8_t>(P, B_FFTR);
+  D.fft_npass = ptr<int32_t>(P, B_FFTN);
+  D.n_fft = (int32_t)P->fft.size();
+  D.v_all = ptr<int64_t>(P, B_VALL);
+  D.C_all = ptr<double2>(P, B_CALL);
+  D.lines = ptr<double2>(P, B_LINES);
+  D.W_tab = ptr<double2>(P, B_WTAB);
+  D.chirp = ptr<double2>(P, B_CHIRP);
+  D.V = ptr<double2>(P, B_V);
+  D.a_reg = ptr<double2>(P, B_AREG);
+  D.key_hash = ptr<uint64_t>(P, B_KHASH);
+  D.htab = ptr<int32_t>(P, B_HTAB);
+  D.acc_v = ptr<int64_t>(P, B_ACCV);
+  D.acc_a = ptr<double2>(P, B_ACCA);
+  D.wtmp = ptr<int32_t>(P, B_WTMP);
+  D.st_status = ptr<int32_t>(P, B_STATUS);
+  D.st_nR = ptr<int32_t>(P, B_NR);
+  D.st_p = ptr<int32_t>(P, B_P);
+  D.st_m = ptr<int32_t>(P, B_M);
+  D.st_M = ptr<int32_t>(P, B_MI);
+  D.st_stall = ptr<int32_t>(P, B_STALL);
+  D.st_iters = ptr<int32_t>(P, B_ITERS);
+  D.st_samples = ptr<int64_t>(P, B_SAMPLES);
+  D.st_cmacs = ptr<int64_t>(P, B_CMACS);
+  D.st_log = ptr<int32_t>(P, B_LOG);
+  D.ctrl = ptr<int32_t>(P, B_CTRL);
+  return D;
+}
+
+int ensure_ready(sfft_plan_t* P) {
+  CUDA_TRY(P, cudaSetDevice(P->device));
+  if (!P->ws) {
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, P->ws_bytes);
+    if (e != cudaSuccess) return fail(P, SFFT_ENOMEM, "cudaMalloc(%zu): %s", P->ws_bytes, cudaGetErrorString(e));
+    P->ws = p;
+    P->ws_owned = true;
+    P->tables_ready = false;
+  }
+  if (!P->h_ctrl) CUDA_TRY(P, cudaMallocHost(&P->h_ctrl, 64));
+  if (!P->tables_ready) {
+    std::vector<int32_t> fm, fn;
+    std::vector<int8_t> fr(P->fft.size() * kMaxFftPasses, 0);
+    for (size_t i = 0; i < P->fft.size(); ++i) {
+      fm.push_back(P->fft[i].M);
+      fn.push_back((int32_t)P->fft[i].radix.size());
+      for (size_t j = 0; j < P->fft[i].radix.size(); ++j) fr[i * kMaxFftPasses + j] = P->fft[i].radix[j];
+    }
+    auto up = [&](int b, const void* src, size_t n) -> cudaError_t {
+      if (n == 0) return cudaSuccess;
+      return cudaMemcpyAsync(static_cast<char*>(P->ws) + P->off[b], src, n, cudaMemcpyHostToDevice, P->stream);
+    };
+    CUDA_TRY(P, up(B_BLOCKS, P->blocks.data(), 4 * P->blocks.size()));
+    CUDA_TRY(P, up(B_BOFF, P->block_off.data(), 4 * P->block_off.size()));
+    CUDA_TRY(P, up(B_LO, P->lo.data(), 8 * P->lo.size()));
+    CUDA_TRY(P, up(B_HI, P->hi.data(), 8 * P->hi.size()));
+    CUDA_TRY(P, up(B_TILTS, P->tilts.data(), 8 * P->tilts.size()));
+    CUDA_TRY(P, up(B_AXT, P->axis_tilt.data(), 4 * P->axis_tilt.size()));
+    CUDA_TRY(P, up(B_SCHED, P->sched.data(), 8 * P->sched.size()));
+    CUDA_TRY(P, up(B_PRIMES, P->primes.data(), 4 * P->primes.size()));
+    CUDA_TRY(P, up(B_FFTM, fm.data(), 4 * fm.size()));
+    CUDA_TRY(P, up(B_FFTR, fr.data(), fr.size()));
+    CUDA_TRY(P, up(B_FFTN, fn.data(), 4 * fn.size()));
+    CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+    P->tables_ready = true;
+  }
+  return SFFT_OK;
+}
+
+int fft_index_host(const sfft_plan_t* P, int p) {
+  const int need = 2 * p - 1;
+  for (size_t i = 0; i < P->fft.size(); ++i)
+    if (P->fft[i].M >= need) return (int)i;
+  return -1;
+}
+
+#define LAUNCH(P, call)                                                                          \
+  do {                                                                                           \
+    cudaError_t _e = (call);                                                                     \
+    if (_e != cudaSuccess) return fail((P), SFFT_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
+    ++launches;                                                                                  \
+  } while (0)
+
+}  // namespace
+
+extern "C" {
+
+const char* sfft_version(void) { return "sfft sm_100a " SFFT_GIT; }
+
+const char* sfft_strerror(int s) {
+  switch (s) {
+    case SFFT_OK: return "ok";
+    case SFFT_PARTIAL: return "partial result (stall or max_iter)";
+    case SFFT_EINVAL: return "invalid argument";
+    case SFFT_EPRECISION: return "precision budget exceeded (N^d_q > 2^40 or E > 2^42)";
+    case SFFT_EDIM: return "dimension / batch mismatch";
+    case SFFT_ECORRUPT: return "corrupt recovery (untilt or wrap failed)";
+    case SFFT_ECUDA: return "CUDA error";
+    case SFFT_ENOMEM: return "out of device memory";
+    case SFFT_ENCCL: return "NCCL error";
+    case SFFT_ENOTSUP: return "prime beyond the supported FFT size";
+  }
+  return "unknown status";
+}
+
+const char* sfft_last_error(const sfft_plan_t* plan) { return plan ? plan->err.c_str() : "null plan"; }
+
+int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_primes, const sfft_tilt* tilts,
+              int32_t n_tilts, double eps, const sfft_options* opt, sfft_plan_t** out) {
+  if (!out) return SFFT_EINVAL;
+  *out = nullptr;
+  std::unique_ptr<sfft_plan_t> P(new (std::nothrow) sfft_plan_t());
+  if (!P) return SFFT_ENOMEM;
+  if (d < 1 || k < 1 || N < 2 || (N % 2) != 0 || N > ((int64_t)1 << 31) || n_primes < 0 || n_tilts < 0)
+    return SFFT_EINVAL;
+  P->d = d; P->N = N; P->k = k;
+  if (opt) {
+    if (opt->c > 0) P->c = opt->c;
+    if (opt->tol > 0) P->tol = opt->tol;
+    if (opt->bin_floor_rel > 0) P->floor_rel = opt->bin_floor_rel;
+    if (opt->prune_floor > 0) P->prune = opt->prune_floor;
+    if (opt->round_tol > 0) P->round_tol = opt->round_tol;
+    if (opt->max_iter > 0) P->max_iter = opt->max_iter;
+    if (opt->stall_limit > 0) P->stall_limit = opt->stall_limit;
+    if (opt->batch > 0) P->batch = opt->batch;
+    if (opt->extra_checks >= 0) P->extra = opt->extra_checks & 3;
+    P->stream = (cudaStream_t)opt->stream;
+  }
+  // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
+  const double log2N = std::log2((double)N);
+  if (opt && opt->n_blocks > 0 && opt->block_dims) {
+    int32_t sum = 0;
+    for (int q = 0; q < opt->n_blocks; ++q) {
+      if (opt->block_dims[q] < 1) return SFFT_EINVAL;
+      P->blocks.push_back(opt->block_dims[q]);
+      sum += opt->block_dims[q];
+    }
+    if (sum != d) return SFFT_EINVAL;
+  } else {
+    int d1 = 1;
+    for (int t = 1; t <= d; ++t)
+      if (d % t == 0 && t * log2N <= 40.0 + 1e-9) d1 = t;
+    for (int q = 0; q < d / d1; ++q) P->blocks.push_back(d1);
+  }
+  P->r = (int32_t)P->blocks.size();
+  P->L = P->r + 1;
+  int64_t B = 1;
+  int32_t off = 0;
+  for (int q = 0; q < P->r; ++q) {
+    if (P->blocks[q] * log2N > 40.0 + 1e-9) return SFFT_EPRECISION;   // reading R1
+    int64_t b = 1;
+    for (int t = 0; t < P->blocks[q]; ++t) b *= N;
+    B = std::max(B, b);
+    P->block_off.push_back(off);
+    off += P->blocks[q];
+  }
+  // image interval of every block, tilts (Eq. (25)/(27)), E (reading R2)
+  std::vector<int64_t> blo(P->r), bhi(P->r);
+  for (int q = 0; q < P->r; ++q) {
+    int64_t geo = 0, pw = 1;
+    for (int t = 0; t < P->blocks[q]; ++t) { geo += pw; pw *= N; }
+    blo[q] = -(N / 2) * geo;
+    bhi[q] = (N / 2 - 1) * geo;
+  }
+  P->lo = blo;
+  P->hi = bhi;
+  P->axis_tilt.assign(P->r, -1);
+  int64_t scale = 1;
+  for (int t = 0; t < n_tilts; ++t) {
+    const sfft_tilt& T = tilts[t];
+    const int a0 = T.axis0, a1 = T.axis1;
+    if (a0 < 0 || a1 < 0 || a0 >= P->r || a1 >= P->r || a0 == a1) return SFFT_EINVAL;
+    if (P->axis_tilt[a0] >= 0 || P->axis_tilt[a1] >= 0) return SFFT_EINVAL;
+    const int64_t b = T.base, h = T.height, c = T.hypo;
+    if (b < 1 || h < 1 || b * b + h * h != c * c || gcd64(b, c) != 1 || gcd64(h, c) != 1) return SFFT_EINVAL;
+    P->axis_tilt[a0] = 2 * t;
+    P->axis_tilt[a1] = 2 * t + 1;
+    P->tilts.insert(P->tilts.end(), {(int64_t)a0, (int64_t)a1, b, h, c});
+    P->lo[a0] = b * blo[a0] - h * bhi[a1];
+    P->hi[a0] = b * bhi[a0] - h * blo[a1];
+    P->lo[a1] = h * blo[a0] + b * blo[a1];
+    P->hi[a1] = h * bhi[a0] + b * bhi[a1];
+    scale = std::max(scale, b + h);
+  }
+  if (eps == 0.0) {
+    P->E = 2 * B * scale;
+  } else {
+    if (!(eps > 0.0)) return SFFT_EINVAL;
+    const double Ed = std::nearbyint(1.0 / eps);
+    if (std::fabs(Ed * eps - 1.0) > 1e-12) return SFFT_EINVAL;
+    P->E = (int64_t)Ed;
+  }
+  if (P->E > ((int64_t)1 << 42)) return SFFT_EPRECISION;
+  for (int q = 0; q < P->r; ++q)
+    if (2 * P->hi[q] >= P->E || -2 * P->lo[q] > P->E) return SFFT_EINVAL;
+  if (P->stall_limit <= 0) P->stall_limit = std::max(2 * P->r, 16);
+  // device limits -> FFT sizes, p_cap, prime table
+  cudaError_t ce = cudaGetDevice(&P->device);
+  if (ce != cudaSuccess) return fail(nullptr, SFFT_ECUDA, "no device");
+  int smem_optin = 0;
+  ce = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, P->device);
+  if (ce != cudaSuccess) return SFFT_ECUDA;
+  int M_max = 0;
+  for (int M = 3; fft_smem_bytes(M) <= (size_t)smem_optin; ++M)
+    if (is_7smooth(M)) {
+      P->fft.push_back(radix_plan(M));
+      M_max = M;
+    }
+  P->p_cap = 0;
+  {
+    const int lim = (M_max + 1) / 2;
+    std::vector<char> comp(lim + 1, 0);
+    for (int x = 2; x <= lim; ++x) {
+      if (comp[x]) continue;
+      P->primes.push_back(x);
+      for (long y = (long)x * x; y <= lim; y += x) comp[y] = 1;
+    }
+    P->p_cap = P->primes.back();
+  }
+  if (primes && n_primes > 0) {
+    for (int i = 0; i < n_primes; ++i) {
+      if (primes[i] < 2 || primes[i] > P->p_cap) return SFFT_ENOTSUP;
+      P->sched.push_back(primes[i]);
+    }
+  } else {
+    // the first prime c k must be supported
+    int64_t first = 0;
+    for (int32_t x : P->primes)
+      if (x >= std::max<int64_t>(2, (int64_t)P->c * k)) { first = x; break; }
+    if (first == 0) return SFFT_ENOTSUP;
+  }
+  P->p_stride = align_up((size_t)P->p_cap, 32);
+  P->M_stride = align_up((size_t)M_max, 32);
+  P->kk = 2 * k;
+  P->H = 1;
+  while (P->H < 2 * k) P->H <<= 1;
+  P->shape = choose_expsum_shape(P->L);
+  P->Lp = P->shape.nt * P->shape.bn;
+  // shared-memory budgets of the other kernels
+  if (16 * ((size_t)P->p_stride + 2) + 2 * 16 * 16 * (size_t)P->shape.bn + 256 > (size_t)smem_optin) return SFFT_ENOTSUP;
+  if (8 * (size_t)P->p_stride + 4 * (2 * (size_t)P->p_stride + 2 * (size_t)k + 64) > (size_t)smem_optin)
+    return SFFT_ENOTSUP;
+  if (8 * (size_t)k > (size_t)smem_optin) return SFFT_ENOTSUP;
+  layout(P.get());
+  *out = P.release();
+  return SFFT_OK;
+}
+
+int sfft_plan_workspace_size(const sfft_plan_t* plan, size_t* bytes) {
+  if (!plan || !bytes) return SFFT_EINVAL;
+  *bytes = plan->ws_bytes;
+  return SFFT_OK;
+}
+
+int sfft_plan_set_workspace(sfft_plan_t* plan, void* dptr, size_t bytes) {
+  if (!plan || !dptr || bytes < plan->ws_bytes || ((uintptr_t)dptr & 255)) return SFFT_EINVAL;
+  if (plan->ws_owned) cudaFree(plan->ws);
+  plan->ws = dptr;
+  plan->ws_owned = false;
+  plan->tables_ready = false;
+  return SFFT_OK;
+}
+
+int sfft_plan_info(const sfft_plan_t* plan, int64_t* E, int32_t* r, int32_t* L, int64_t* p_max, int32_t* tile_n) {
+  if (!plan) return SFFT_EINVAL;
+  if (E) *E = plan->E;
+  if (r) *r = plan->r;
+  if (L) *L = plan->L;
+  if (p_max) *p_max = plan->p_cap;
+  if (tile_n) *tile_n = plan->shape.bn;
+  return SFFT_OK;
+}
+
+void sfft_plan_destroy(sfft_plan_t* plan) {
+  if (!plan) return;
+  if (plan->ws_owned && plan->ws) cudaFree(plan->ws);
+  if (plan->h_ctrl) cudaFreeHost(plan->h_ctrl);
+  delete plan;
+}
+
+int sfft_signal_expsum(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, const double* coeffs,
+                       sfft_signal_t** out) {
+  if (!plan || !out || !freqs || !coeffs) return SFFT_EINVAL;
+  if (batch < 1 || batch > plan->batch) return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch);
+  sfft_signal_t* s = new (std::nothrow) sfft_signal_t();
+  if (!s) return SFFT_ENOMEM;
+  s->plan = plan;
+  s->batch = batch;
+  s->freqs = freqs;
+  s->coeffs = coeffs;
+  *out = s;
+  return SFFT_OK;
+}
+
+void sfft_signal_destroy(sfft_signal_t* sig) { delete sig; }
+
+int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs, double* out_coeffs,
+                 int32_t* out_count, int32_t* out_status, sfft_report* rep) {
+  if (!plan || !sig || sig->plan != plan || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  cudaStream_t st = P->stream;
+  const int32_t batch = sig->batch;
+  DevParams D = dev_params(P, batch);
+  int launches = 0;
+  LAUNCH(P, launch_project(D, batch, sig->freqs, sig->coeffs, st));
+  launches += 1;   // init_state_kernel
+  int iter = 1;
+  int32_t last_iter = 0;
+  for (; iter <= P->max_iter; ++iter) {
+    LAUNCH(P, launch_setup(D, iter, st));
+    CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaStreamSynchronize(st));
+    const int n_active = P->h_ctrl[0], max_p = P->h_ctrl[1];
+    if (n_active == 0) break;
+    const int fi = fft_index_host(P, max_p);
+    if (fi < 0) return fail(P, SFFT_ENOTSUP, "p=%d beyond FFT table", max_p);
+    const int max_M = P->fft[fi].M;
+    LAUNCH(P, launch_fft_prep(D, batch, max_M, st));
+    LAUNCH(P, launch_expsum(D, P->shape, max_p, batch, st));
+    LAUNCH(P, launch_pfft(D, batch, P->L, max_M, st));
+    LAUNCH(P, launch_decode(D, iter, max_p, st));
+    last_iter = iter;
+  }
+  int32_t* ostat = out_status ? out_status : ptr<int32_t>(P, B_OUT_S);
+  LAUNCH(P, launch_wrap(D, batch, out_freqs, out_coeffs, out_count, ostat, st));
+  // report
+  std::vector<int32_t> hs(batch);
+  CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> hsamp(batch), hcm(batch);
+  std::vector<int32_t> hlog(2 * kLogIters);
+  if (rep) {
+    CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(P, cudaStreamSynchronize(st));
+  int worst = SFFT_OK, n_ok = 0, n_part = 0, n_err = 0;
+  for (int s = 0; s < batch; ++s) {
+    const int v = hs[s];
+    if (v == SFFT_OK) ++n_ok;
+    else if (v == SFFT_PARTIAL) { ++n_part; if (worst == SFFT_OK) worst = SFFT_PARTIAL; }
+    else { ++n_err; if (worst >= 0) worst = v; }
+  }
+  if (rep) {
+    memset(rep, 0, sizeof *rep);
+    for (int s = 0; s < batch; ++s) { rep->samples_used += hsamp[s]; rep->cmacs += hcm[s]; }
+    rep->iterations = last_iter;
+    rep->n_ok = n_ok; rep->n_partial = n_part; rep->n_error = n_err;
+    rep->status = worst;
+    rep->n_iter_logged = std::min(last_iter, kLogIters);
+    for (int i = 0; i < rep->n_iter_logged; ++i) { rep->primes[i] = hlog[2 * i]; rep->accepted[i] = hlog[2 * i + 1]; }
+    rep->kernel_launches = launches;
+  }
+  return worst;
+}
+
+int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, const double* coeffs,
+                    int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
+                    sfft_report* rep) {
+  if (!plan || !freqs || !coeffs || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
+  if (batch < 1 || batch > plan->batch) return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch);
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  const size_t nf = 4 * (size_t)batch * P->k * P->d, nc = 16 * (size_t)batch * P->k;
+  CUDA_TRY(P, cudaMemcpyAsync(ptr<int32_t>(P, B_IN_F), freqs, nf, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(P, cudaMemcpyAsync(ptr<double>(P, B_IN_C), coeffs, nc, cudaMemcpyHostToDevice, P->stream));
+  sfft_signal_t sig{P, batch, ptr<int32_t>(P, B_IN_F), ptr<double>(P, B_IN_C)};
+  const int st = sfft_execute(P, &sig, ptr<int32_t>(P, B_OUT_F), ptr<double>(P, B_OUT_C), ptr<int32_t>(P, B_OUT_N),
+                              ptr<int32_t>(P, B_OUT_S), rep);
+  if (st < 0 && st != SFFT_ENOTSUP && st != SFFT_ECORRUPT) return st;
+  CUDA_TRY(P, cudaMemcpyAsync(out_freqs, ptr<int32_t>(P, B_OUT_F), nf, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(P, cudaMemcpyAsync(out_coeffs, ptr<double>(P, B_OUT_C), nc, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(P, cudaMemcpyAsync(out_count, ptr<int32_t>(P, B_OUT_N), 4 * (size_t)batch, cudaMemcpyDeviceToHost, P->stream));
+  if (out_status)
+    CUDA_TRY(P, cudaMemcpyAsync(out_status, ptr<int32_t>(P, B_OUT_S), 4 * (size_t)batch, cudaMemcpyDeviceToHost, P->stream));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return st;
+}
+
+// ---------------------------------------------------------------- stage entry points
+static int set_signal0_state(sfft_plan_t* P, const DevParams& D, int p, int m, int nR) {
+  int32_t h[5] = {ST_RUN, nR, p, m, 0};
+  CUDA_TRY(P, cudaMemcpyAsync(D.st_status, &h[0], 4, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(P, cudaMemcpyAsync(D.st_nR, &h[1], 4, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(P, cudaMemcpyAsync(D.st_p, &h[2], 4, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(P, cudaMemcpyAsync(D.st_m, &h[3], 4, cudaMemcpyHostToDevice, P->stream));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return SFFT_OK;
+}
+
+int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const double* c, int64_t p, int32_t m,
+                      double* s_out) {
+  if (!plan || !v || !c || !s_out || K < 0 || K > plan->kk || m < 0 || m >= plan->r) return SFFT_EINVAL;
+  if (p < 2 || p > plan->p_cap) return SFFT_ENOTSUP;
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  DevParams D = dev_params(P, 1);
+  int launches = 0;
+  if (K > 0)
+    CUDA_TRY(P, cudaMemcpy2DAsync(D.v_all, 8 * (size_t)P->kk, v, 8 * (size_t)K, 8 * (size_t)K, P->r,
+                                  cudaMemcpyDeviceToDevice, P->stream));
+  LAUNCH(P, launch_line_coeffs(D, K, c, P->stream));
+  rc = set_signal0_state(P, D, (int)p, m, K - P->k);
+  if (rc) return rc;
+  const int fi = fft_index_host(P, (int)p);
+  LAUNCH(P, launch_fft_prep(D, 1, P->fft[fi].M, P->stream));
+  LAUNCH(P, launch_expsum(D, P->shape, (int)p, 1, P->stream));
+  CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
+                                cudaMemcpyDeviceToDevice, P->stream));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return SFFT_OK;
+}
+
+int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
+  if (!plan || !x || n_lines < 1) return SFFT_EINVAL;
+  if (p < 2 || p > plan->p_cap) return SFFT_ENOTSUP;
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  DevParams D = dev_params(P, 1);
+  D.lines = reinterpret_cast<double2*>(x);
+  D.p_stride = p;
+  D.L = n_lines;
+  int launches = 0;
+  rc = set_signal0_state(P, D, (int)p, 0, 0);
+  if (rc) return rc;
+  const int M = P->fft[fft_index_host(P, (int)p)].M;
+  LAUNCH(P, launch_fft_prep(D, 1, M, P->stream));
+  LAUNCH(P, launch_pfft(D, 1, n_lines, M, P->stream));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return SFFT_OK;
+}
+
+int sfft_stage_decode(sfft_plan_t* plan, int64_t p, int32_t m, int32_t kstar, const double* F, int32_t* acc_b,
+                      int64_t* acc_v, double* acc_a, int32_t* counts) {
+  if (!plan || !F || !acc_b || !acc_v || !acc_a || !counts || kstar < 1 || kstar > plan->k || m < 0 || m >= plan->r)
+    return SFFT_EINVAL;
+  if (p < 2 || p > plan->p_cap) return SFFT_ENOTSUP;
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  DevParams D = dev_params(P, 1);
+  D.lines = reinterpret_cast<double2*>(const_cast<double*>(F));
+  D.p_stride = p;
+  int launches = 0;
+  rc = set_signal0_state(P, D, (int)p, m, P->k - kstar);
+  if (rc) return rc;
+  LAUNCH(P, launch_stage_decode(D, kstar, acc_b, acc_v, acc_a, counts, P->stream));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return SFFT_OK;
+}
+
+int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int64_t* v_out) {
+  if (!plan || !sig || !v_out) return SFFT_EINVAL;
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  DevParams D = dev_params(P, sig->batch);
+  int launches = 0;
+  LAUNCH(P, launch_project(D, sig->batch, sig->freqs, sig->coeffs, P->stream));
+  CUDA_TRY(P, cudaMemcpy2DAsync(v_out, 8 * (size_t)P->k, D.v_all, 8 * (size_t)P->kk, 8 * (size_t)P->k,
+                                (size_t)sig->batch * P->r, cudaMemcpyDeviceToDevice, P->stream));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return SFFT_OK;
+}
+
+int sfft_comm_init(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* nccl_unique_id, int32_t shard_mode) {
+  (void)nccl_unique_id;
+  if (!plan || nranks < 1 || rank < 0 || rank >= nranks) return SFFT_EINVAL;
+  if (shard_mode == 0) return SFFT_OK;   // signal sharding: independent solves, no communicator
+  return fail(plan, SFFT_ENOTSUP, "line sharding (shard_mode 1) is not built yet");
+}
+
+}  // extern "C"

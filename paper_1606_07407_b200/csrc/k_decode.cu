@@ -1,0 +1,387 @@
+// k_decode.cu -- SURVEY 8(a) rows a2 (per-iteration setup), a5 (select), a6 (collision test +
+// decode) and a7 (registry update), Algorithm 2 l.6-10 and l.18-34.
+//
+// setup_kernel  : k* = k - |R|, p = i-th prime >= max(2, c k*) (l.8, reading R10), m = i mod r (R9)
+// decode_kernel : one CTA per signal.
+//   1. select   : bins b with |F_0[b]| >= 1e-8 p, ascending b; if more than k* the k* largest (R5)
+//   2. decode   : one warp per candidate, lanes over the r shifted lines:
+//                 Eq. (42) |F_n[b]| / |F_0[b]| within tau of 1 for every n (ballot),
+//                 Eq. (41) v_n = round(Arg(F_n conj F_0) E / 2 pi) with the R12/R13 rejections
+//   3. compact  : accepted candidates in ascending b (block prefix sum)
+//   4. registry : R[v] += F_0[b]/p (R14) through an open-addressing hash of the r-long key,
+//                 new entries appended in ascending-b order (deterministic), their C rows
+//                 (-a e^{2 pi i v_n / E}) written for the next iteration's residual; prune (R15)
+//   5. state    : |R|, stall counter (R16), samples (R18), status
+#include "sfft_internal.cuh"
+
+namespace sfft {
+
+// ------------------------------------------------------------------ setup
+__device__ int ith_prime_at_least(const DevParams& P, int x, int i) {
+  if (x < 2) x = 2;
+  int lo = 0, hi = P.n_primes;            // first index with primes[idx] >= x
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (P.primes[mid] >= x) hi = mid; else lo = mid + 1;
+  }
+  const int idx = lo + i - 1;
+  return idx < P.n_primes ? P.primes[idx] : -1;
+}
+
+__global__ void setup_kernel(DevParams P, int32_t iter) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int nR = P.st_nR[s];
+  const int kstar = P.k - nR;
+  int p;
+  if (P.n_sched > 0) p = (int)P.sched[(iter - 1) % P.n_sched];
+  else p = ith_prime_at_least(P, P.c * kstar, iter);
+  if (p < 2 || p > P.p_cap) {
+    P.st_status[s] = SFFT_ENOTSUP;
+    return;
+  }
+  P.st_p[s] = p;
+  P.st_m[s] = iter % P.r;
+  atomicAdd(&P.ctrl[0], 1);
+  atomicMax(&P.ctrl[1], p);
+  atomicMax(&P.ctrl[2], P.k + nR);
+}
+
+cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(P.ctrl, 0, sizeof(int32_t) * 4, st);
+  if (e != cudaSuccess) return e;
+  setup_kernel<<<(P.batch + 255) / 256, 256, 0, st>>>(P, iter);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ block helpers
+// exclusive prefix sum over the block; returns the exclusive value, *total gets the sum
+__device__ int block_excl_scan(int v, int* scratch, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) scratch[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int t = lane < nw ? scratch[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    if (lane < nw) scratch[lane] = t;       // inclusive warp-prefix
+  }
+  __syncthreads();
+  const int before = warp > 0 ? scratch[warp - 1] : 0;
+  *total = scratch[nw - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ double2 line_factor_d(int64_t v, int64_t E) {
+  const int64_t q = mod_pos64(v, E);
+  double s, c;
+  sincospi(2.0 * (double)q / (double)E, &s, &c);
+  return make_double2(c, s);
+}
+
+// ------------------------------------------------------------------ decode
+// dynamic smem: cand[p] int, flag[p] int, mag[p] double, accl[k] int, found[k] int, scratch[64] int
+size_t decode_smem_bytes(const DevParams& P, int32_t max_p) {
+  return sizeof(double) * (size_t)max_p + sizeof(int) * (2 * (size_t)max_p + 2 * (size_t)P.k + 64);
+}
+
+template <bool STAGE>
+__global__ void __launch_bounds__(kDecodeThreads)
+decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, int64_t* out_v,
+              double2* out_a, int32_t* out_counts) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.x;
+  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int p = P.st_p[s], m = P.st_m[s];
+  const int nR = P.st_nR[s];
+  const int kstar = STAGE ? kstar_stage : P.k - nR;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int r = P.r;
+
+  double* mag = reinterpret_cast<double*>(smem_raw);
+  int* cand = reinterpret_cast<int*>(mag + p);
+  int* flag = cand + p;
+  int* accl = flag + p;
+  int* found = accl + P.k;
+  int* scratch = found + P.k;
+
+  const double2* F = P.lines + (int64_t)s * P.L * P.p_stride;   // line n at F + n * p_stride
+  const double floor_abs = P.floor_rel * (double)p;
+
+  // ---- 1. select (ascending b) ----
+  const int chunk = (p + blockDim.x - 1) / blockDim.x;
+  const int b0 = tid * chunk, b1 = min(p, b0 + chunk);
+  int cnt = 0;
+  for (int b = b0; b < b1; ++b) {
+    const double2 f = F[b];
+    cnt += hypot(f.x, f.y) >= floor_abs;
+  }
+  int total;
+  int pos = block_excl_scan(cnt, scratch, &total);
+  for (int b = b0; b < b1; ++b) {
+    const double2 f = F[b];
+    const double mg = hypot(f.x, f.y);
+    if (mg >= floor_abs) { cand[pos] = b; mag[pos] = mg; ++pos; }
+  }
+  __syncthreads();
+  int nc = total;
+  if (nc > kstar) {
+    // keep the k* largest |F_0| (ties -> smaller b), preserve ascending order
+    for (int i = tid; i < nc; i += blockDim.x) {
+      const double mi = mag[i];
+      const int bi = cand[i];
+      int rank = 0;
+      for (int j = 0; j < nc; ++j) rank += (mag[j] > mi) || (mag[j] == mi && cand[j] < bi);
+      flag[i] = rank < kstar;
+    }
+    __syncthreads();
+    const int per = (nc + blockDim.x - 1) / blockDim.x;
+    const int i0 = tid * per, i1 = min(nc, i0 + per);
+    int c2 = 0;
+    int keep_b[32];
+    int nk = 0;
+    for (int i = i0; i < i1; ++i) c2 += flag[i];
+    int pos2 = block_excl_scan(c2, scratch, &total);
+    // stash own survivors in registers (per <= 14 since p <= 7168 and blockDim = 512)
+    for (int i = i0; i < i1 && nk < 32; ++i)
+      if (flag[i]) keep_b[nk++] = cand[i];
+    __syncthreads();
+    for (int t = 0; t < nk; ++t) cand[pos2 + t] = keep_b[t];
+    __syncthreads();
+    nc = total;
+  }
+
+  // ---- 2. collision test + decode, one warp per candidate ----
+  int64_t* accv = P.acc_v + (int64_t)s * r * P.k;       // [r][k], column = candidate index
+  const double twopi = 6.283185307179586476925286766559;
+  for (int ci = warp; ci < nc; ci += nwarps) {
+    const int b = cand[ci];
+    const double2 f0 = F[b];
+    const double mag0 = hypot(f0.x, f0.y);
+    bool ok = true;
+    for (int n = lane; n < r; n += 32) {
+      const double2 fn = F[(int64_t)(1 + n) * P.p_stride + b];
+      const double rho = hypot(fn.x, fn.y) / mag0;
+      ok = ok && (fabs(rho - 1.0) < P.tol);
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (ok) {
+      for (int n = lane; n < r; n += 32) {
+        const double2 fn = F[(int64_t)(1 + n) * P.p_stride + b];
+        // q = F_n conj(F_0), written without contraction to mirror the plain formula
+        const double qr = __dadd_rn(__dmul_rn(fn.x, f0.x), __dmul_rn(fn.y, f0.y));
+        const double qi = __dsub_rn(__dmul_rn(fn.y, f0.x), __dmul_rn(fn.x, f0.y));
+        const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)P.E), twopi);
+        const double xr = rint(x);
+        bool good = fabs(x - xr) <= P.round_tol;
+        const int64_t v = (int64_t)xr;
+        if (P.extra & 1) good = good && v >= P.lo[n] && v <= P.hi[n];
+        ok = ok && good;
+        accv[(int64_t)n * P.k + ci] = v;
+      }
+      ok = __all_sync(0xffffffffu, ok);
+      if (ok && (P.extra & 2)) {
+        __syncwarp();
+        const int64_t vm = accv[(int64_t)m * P.k + ci];
+        ok = mod_pos64(vm, p) == b;
+      }
+    }
+    if (lane == 0) flag[ci] = ok;
+  }
+  __syncthreads();
+
+  // ---- 3. accepted list in ascending b ----
+  {
+    const int per = (nc + blockDim.x - 1) / blockDim.x;
+    const int i0 = tid * per, i1 = min(nc, i0 + per);
+    int c3 = 0;
+    for (int i = i0; i < i1; ++i) c3 += flag[i];
+    int pos3 = block_excl_scan(c3, scratch, &total);
+    for (int i = i0; i < i1; ++i)
+      if (flag[i]) accl[pos3++] = i;
+    __syncthreads();
+  }
+  const int na = total;
+
+  if (STAGE) {
+    for (int t = tid; t < na; t += blockDim.x) {
+      const int ci = accl[t];
+      const int b = cand[ci];
+      out_b[t] = b;
+      const double2 f0 = F[b];
+      out_a[t] = make_double2(f0.x / (double)p, f0.y / (double)p);
+      for (int n = 0; n < r; ++n) out_v[(int64_t)n * kstar + t] = accv[(int64_t)n * P.k + ci];
+    }
+    if (tid == 0) { out_counts[0] = nc; out_counts[1] = na; }
+    return;
+  }
+
+  // ---- 4. registry update: R[v] += a ----
+  int64_t* vreg = P.v_all + (int64_t)s * r * P.kk + P.k;   // column e = registry entry e
+  double2* areg = P.a_reg + (int64_t)s * P.k;
+  uint64_t* khash = P.key_hash + (int64_t)s * P.k;
+  int* htab = P.htab + (int64_t)s * P.H;
+  const int Hm = P.H - 1;
+  for (int t = tid; t < na; t += blockDim.x) {
+    const int ci = accl[t];
+    uint64_t h = 0x9E3779B97F4A7C15ULL;
+    for (int n = 0; n < r; ++n) h = mix64(h ^ (uint64_t)accv[(int64_t)n * P.k + ci]);
+    int slot = (int)(h & (uint64_t)Hm);
+    int fe = -1;
+    for (;;) {
+      const int e1 = htab[slot];
+      if (e1 == 0) break;
+      const int e = e1 - 1;
+      if (khash[e] == h) {
+        bool eq = true;
+        for (int n = 0; n < r && eq; ++n) eq = vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+        if (eq) { fe = e; break; }
+      }
+      slot = (slot + 1) & Hm;
+    }
+    found[t] = fe;
+  }
+  __syncthreads();
+  int n_new;
+  {
+    const int per = (na + blockDim.x - 1) / blockDim.x;
+    const int t0 = tid * per, t1 = min(na, t0 + per);
+    int c4 = 0;
+    for (int t = t0; t < t1; ++t) c4 += found[t] < 0;
+    int rank = block_excl_scan(c4, scratch, &total);
+    n_new = total;
+    for (int t = t0; t < t1; ++t) {
+      const int ci = accl[t];
+      const int b = cand[ci];
+      const double2 f0 = F[b];
+      const double2 a = make_double2(f0.x / (double)p, f0.y / (double)p);    // Eq. (7): a = F_0 / p
+      if (found[t] >= 0) {
+        const int e = found[t];
+        areg[e] = make_double2(areg[e].x + a.x, areg[e].y + a.y);
+      } else {
+        const int e = nR + rank++;
+        uint64_t h = 0x9E3779B97F4A7C15ULL;
+        for (int n = 0; n < r; ++n) {
+          const int64_t v = accv[(int64_t)n * P.k + ci];
+          vreg[(int64_t)n * P.kk + e] = v;
+          h = mix64(h ^ (uint64_t)v);
+        }
+        areg[e] = a;
+        khash[e] = h;
+        int slot = (int)(h & (uint64_t)Hm);
+        while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+        found[t] = e;
+      }
+    }
+  }
+  __syncthreads();
+  const int nR_new = nR + n_new;
+
+  // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}
+  double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+  for (int64_t w = tid; w < (int64_t)na * P.Lp; w += blockDim.x) {
+    const int t = (int)(w / P.Lp), n = (int)(w % P.Lp);
+    const int e = found[t];
+    const double2 a = areg[e];
+    double2 c;
+    if (n == 0) c = make_double2(-a.x, -a.y);
+    else if (n < P.L) {
+      const double2 lf = line_factor_d(vreg[(int64_t)(n - 1) * P.kk + e], P.E);
+      c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+    } else c = make_double2(0.0, 0.0);
+    Creg[(int64_t)e * P.Lp + n] = c;
+  }
+  // prune test (only touched entries can have changed)
+  int small = 0;
+  for (int t = tid; t < na; t += blockDim.x) {
+    const double2 a = areg[found[t]];
+    small |= hypot(a.x, a.y) < P.prune;
+  }
+  const int any_small = __syncthreads_or(small);
+  int nR_final = nR_new;
+  if (any_small) {
+    // rare path: order-preserving compaction by warp 0, then rebuild the hash table
+    if (warp == 0) {
+      int wpos = 0;
+      for (int e = 0; e < nR_new; ++e) {
+        const double2 a = areg[e];
+        const bool keep = !(hypot(a.x, a.y) < P.prune);
+        if (keep) {
+          if (wpos != e) {
+            for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + wpos] = vreg[(int64_t)n * P.kk + e];
+            for (int n = lane; n < P.Lp; n += 32) Creg[(int64_t)wpos * P.Lp + n] = Creg[(int64_t)e * P.Lp + n];
+            if (lane == 0) { areg[wpos] = a; khash[wpos] = khash[e]; }
+          }
+          ++wpos;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) scratch[0] = wpos;
+    }
+    __syncthreads();
+    nR_final = scratch[0];
+    for (int i = tid; i < P.H; i += blockDim.x) htab[i] = 0;
+    __syncthreads();
+    for (int e = tid; e < nR_final; e += blockDim.x) {
+      int slot = (int)(khash[e] & (uint64_t)Hm);
+      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+    }
+    __syncthreads();
+  }
+
+  // ---- 5. state ----
+  if (tid == 0) {
+    const int K = P.k + nR;
+    P.st_nR[s] = nR_final;
+    const int stall = na == 0 ? P.st_stall[s] + 1 : 0;
+    P.st_stall[s] = stall;
+    P.st_samples[s] += (int64_t)P.L * p;
+    P.st_cmacs[s] += (int64_t)P.L * p * K;
+    P.st_iters[s] = iter;
+    if (s == 0 && iter <= kLogIters) {
+      P.st_log[2 * (iter - 1)] = p;
+      P.st_log[2 * (iter - 1) + 1] = na;
+    }
+    int st = ST_RUN;
+    if (nR_final >= P.k) st = SFFT_OK;
+    else if (stall >= P.stall_limit || iter >= P.max_iter) st = SFFT_PARTIAL;
+    P.st_status[s] = st;
+  }
+}
+
+cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, cudaStream_t st) {
+  const size_t smem = decode_smem_bytes(P, max_p);
+  cudaError_t e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  decode_kernel<false><<<P.batch, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,
+                                double* acc_a, int32_t* counts, cudaStream_t st) {
+  const int max_p = (int)P.p_stride;
+  const size_t smem = decode_smem_bytes(P, max_p);
+  cudaError_t e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  decode_kernel<true><<<1, kDecodeThreads, smem, st>>>(P, 0, kstar, acc_b, acc_v,
+                                                        reinterpret_cast<double2*>(acc_a), counts);
+  return cudaGetLastError();
+}
+
+}  // namespace sfft

@@ -1,0 +1,305 @@
+// k_fft.cu -- SURVEY 8(a) row a4: batched prime-length DFTs (Algorithm 2 l.16-17)
+//
+//   F_n[b] = sum_{h < p} s_n[h] e^{-2 pi i h b / p}     (unnormalised, so Eq. (3)'s factor p appears)
+//
+// p is prime (no Cooley-Tukey split), so each line is transformed with Bluestein's identity
+// hb = (h^2 + b^2 - (b-h)^2)/2:
+//   F[b] = w[b] * sum_h (s[h] w[h]) conj(w[b-h]),  w[n] = e^{-pi i (n^2 mod 2p)/p}  (exact index)
+// i.e. a cyclic convolution of length M >= 2p-1 done as DIF-FFT -> pointwise product with the
+// precomputed kernel spectrum -> DIT-inverse FFT.  M is 7-smooth (radices 2,3,4,5,7,8) and the
+// whole length-M work array lives in shared memory (M <= 14112 -> 221 KB).  The forward FFT is
+// in-place decimation in frequency (natural order in, digit-reversed out); the kernel spectrum
+// is produced by the same routine, so the pointwise product happens in digit-reversed order and
+// the in-place decimation-in-time inverse returns natural order: no permutation pass.
+// Twiddles e^{-2 pi i q/M} = T_hi[q >> 7] * T_lo[q & 127], two small tables in shared memory.
+#include "sfft_internal.cuh"
+
+namespace sfft {
+
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmulx(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cmulconj(double2 a, double2 b) {   // a * conj(b)
+  return make_double2(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+__device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ double2 mul_mi(double2 a) {
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// cos / sin of 2 pi k / R for the odd radices
+__device__ __constant__ double kCos3[3] = {1.0, -0.5, -0.5};
+__device__ __constant__ double kSin3[3] = {0.0, 0.86602540378443864676, -0.86602540378443864676};
+__device__ __constant__ double kCos5[5] = {1.0, 0.30901699437494742410, -0.80901699437494742410,
+                                           -0.80901699437494742410, 0.30901699437494742410};
+__device__ __constant__ double kSin5[5] = {0.0, 0.95105651629515357212, 0.58778525229247312917,
+                                           -0.58778525229247312917, -0.95105651629515357212};
+__device__ __constant__ double kCos7[7] = {1.0, 0.62348980185873353053, -0.22252093395631440429,
+                                           -0.90096886790241912624, -0.90096886790241912624,
+                                           -0.22252093395631440429, 0.62348980185873353053};
+__device__ __constant__ double kSin7[7] = {0.0, 0.78183148246802980871, 0.97492791218182360702,
+                                           0.43388373911755812048, -0.43388373911755812048,
+                                           -0.97492791218182360702, -0.78183148246802980871};
+
+// in-register DFT of size R; forward uses e^{-2 pi i nk/R}, inverse e^{+2 pi i nk/R}
+template <int R, bool INV>
+__device__ __forceinline__ void dft_small(double2 (&x)[R]) {
+  if constexpr (R == 2) {
+    const double2 a = x[0], b = x[1];
+    x[0] = cadd(a, b);
+    x[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    const double2 a0 = cadd(x[0], x[2]), a1 = csub(x[0], x[2]);
+    const double2 b0 = cadd(x[1], x[3]), b1 = mul_mi<INV>(csub(x[1], x[3]));
+    x[0] = cadd(a0, b0);
+    x[2] = csub(a0, b0);
+    x[1] = cadd(a1, b1);
+    x[3] = csub(a1, b1);
+  } else if constexpr (R == 8) {
+    const double h = 0.70710678118654752440;
+    double2 a[4], b[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) {
+      a[n] = cadd(x[n], x[n + 4]);
+      b[n] = csub(x[n], x[n + 4]);
+    }
+    // b[n] *= w8^n, w8 = e^{-+ 2 pi i / 8}
+    b[1] = INV ? make_double2(h * (b[1].x - b[1].y), h * (b[1].x + b[1].y))
+               : make_double2(h * (b[1].x + b[1].y), h * (b[1].y - b[1].x));
+    b[2] = mul_mi<INV>(b[2]);
+    b[3] = INV ? make_double2(-h * (b[3].x + b[3].y), h * (b[3].x - b[3].y))
+               : make_double2(h * (b[3].y - b[3].x), -h * (b[3].x + b[3].y));
+    dft_small<4, INV>(a);
+    dft_small<4, INV>(b);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      x[2 * k] = a[k];
+      x[2 * k + 1] = b[k];
+    }
+  } else {
+    // odd R: pair n with R-n
+    const double* C = (R == 3) ? kCos3 : (R == 5) ? kCos5 : kCos7;
+    const double* S = (R == 3) ? kSin3 : (R == 5) ? kSin5 : kSin7;
+    constexpr int H = (R - 1) / 2;
+    double2 sp[H], sm[H];
+    double2 y0 = x[0];
+#pragma unroll
+    for (int n = 1; n <= H; ++n) {
+      sp[n - 1] = cadd(x[n], x[R - n]);
+      sm[n - 1] = csub(x[n], x[R - n]);
+      y0 = cadd(y0, sp[n - 1]);
+    }
+    double2 out[R];
+    out[0] = y0;
+#pragma unroll
+    for (int k = 1; k <= H; ++k) {
+      double2 re = x[0], im = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int n = 1; n <= H; ++n) {
+        const int q = (n * k) % R;
+        re = make_double2(re.x + C[q] * sp[n - 1].x, re.y + C[q] * sp[n - 1].y);
+        im = make_double2(im.x + S[q] * sm[n - 1].x, im.y + S[q] * sm[n - 1].y);
+      }
+      // forward: y[k] = re - i im, y[R-k] = re + i im
+      const double2 mi = make_double2(im.y, -im.x);   // -i * im
+      out[k] = INV ? csub(re, mi) : cadd(re, mi);
+      out[R - k] = INV ? cadd(re, mi) : csub(re, mi);
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[k] = out[k];
+  }
+}
+
+struct Tw {
+  const double2* lo;
+  const double2* hi;
+  __device__ __forceinline__ double2 operator()(int q) const { return cmulx(hi[q >> 7], lo[q & 127]); }
+};
+
+template <int R>
+__device__ __forceinline__ void bfly_dif(double2* x, int base, int Q, int twstep, const Tw& tw) {
+  double2 v[R];
+#pragma unroll
+  for (int n = 0; n < R; ++n) v[n] = x[base + Q * n];
+  dft_small<R, false>(v);
+  x[base] = v[0];
+#pragma unroll
+  for (int k = 1; k < R; ++k) x[base + Q * k] = twstep ? cmulx(v[k], tw(twstep * k)) : v[k];
+}
+
+template <int R>
+__device__ __forceinline__ void bfly_dit(double2* x, int base, int Q, int twstep, const Tw& tw) {
+  double2 v[R];
+  v[0] = x[base];
+#pragma unroll
+  for (int k = 1; k < R; ++k) {
+    const double2 z = x[base + Q * k];
+    v[k] = twstep ? cmulconj(z, tw(twstep * k)) : z;
+  }
+  dft_small<R, true>(v);
+#pragma unroll
+  for (int n = 0; n < R; ++n) x[base + Q * n] = v[n];
+}
+
+template <bool INV>
+__device__ void fft_pass(double2* x, int M, int S, int R, const Tw& tw) {
+  const int Q = S / R;
+  const int nb = M / R;
+  const int mstep = M / S;
+  for (int bi = threadIdx.x; bi < nb; bi += blockDim.x) {
+    const int blk = bi / Q, n1 = bi - blk * Q;
+    const int base = blk * S + n1;
+    const int twstep = n1 * mstep;
+    switch (R) {
+      case 2: INV ? bfly_dit<2>(x, base, Q, twstep, tw) : bfly_dif<2>(x, base, Q, twstep, tw); break;
+      case 3: INV ? bfly_dit<3>(x, base, Q, twstep, tw) : bfly_dif<3>(x, base, Q, twstep, tw); break;
+      case 4: INV ? bfly_dit<4>(x, base, Q, twstep, tw) : bfly_dif<4>(x, base, Q, twstep, tw); break;
+      case 5: INV ? bfly_dit<5>(x, base, Q, twstep, tw) : bfly_dif<5>(x, base, Q, twstep, tw); break;
+      case 7: INV ? bfly_dit<7>(x, base, Q, twstep, tw) : bfly_dif<7>(x, base, Q, twstep, tw); break;
+      case 8: INV ? bfly_dit<8>(x, base, Q, twstep, tw) : bfly_dif<8>(x, base, Q, twstep, tw); break;
+    }
+  }
+  __syncthreads();
+}
+
+// forward DIF FFT, natural -> digit-reversed
+__device__ void fft_dif(double2* x, int M, const int8_t* radix, int npass, const Tw& tw) {
+  int S = M;
+  for (int ps = 0; ps < npass; ++ps) {
+    const int R = radix[ps];
+    fft_pass<false>(x, M, S, R, tw);
+    S /= R;
+  }
+}
+// inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
+__device__ void fft_dit(double2* x, int M, const int8_t* radix, int npass, const Tw& tw) {
+  int S = 1;
+  for (int ps = npass - 1; ps >= 0; --ps) {
+    const int R = radix[ps];
+    S *= R;
+    fft_pass<true>(x, M, S, R, tw);
+  }
+}
+
+__device__ int find_fft_index(const DevParams& P, int p) {
+  const int need = 2 * p - 1;
+  int lo = 0, hi = P.n_fft - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (P.fft_M[mid] >= need) hi = mid; else lo = mid + 1;
+  }
+  return lo;
+}
+
+// twiddle tables: T_lo[j] = e^{-2 pi i j / M}, T_hi[j] = e^{-2 pi i 128 j / M}
+__device__ void build_twiddles(double2* Tlo, double2* Thi, int M) {
+  const int nhi = (M + 127) / 128;
+  for (int j = threadIdx.x; j < 128 + nhi; j += blockDim.x) {
+    double s, c;
+    if (j < 128) {
+      sincospi(-2.0 * (double)j / (double)M, &s, &c);
+      Tlo[j] = make_double2(c, s);
+    } else {
+      const int jj = j - 128;
+      sincospi(-2.0 * (double)(128 * jj) / (double)M, &s, &c);
+      Thi[jj] = make_double2(c, s);
+    }
+  }
+}
+
+__device__ __forceinline__ double2 chirp_value(int64_t q, int64_t p) {
+  // e^{-pi i (q^2 mod 2p) / p}
+  const int64_t e = (q * q) % (2 * p);
+  double s, c;
+  sincospi((double)e / (double)p, &s, &c);
+  return make_double2(c, -s);
+}
+
+// per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
+__global__ void __launch_bounds__(kFftThreads) fft_prep_kernel(DevParams P) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.x;
+  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int p = P.st_p[s];
+  const int fi = find_fft_index(P, p);
+  const int M = P.fft_M[fi];
+  if (threadIdx.x == 0) P.st_M[s] = fi;
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* Tlo = x + M;
+  double2* Thi = Tlo + 128;
+  build_twiddles(Tlo, Thi, M);
+  double2* W = P.W_tab + (int64_t)s * P.p_stride;
+  double2* ch = P.chirp + (int64_t)s * P.p_stride;
+  for (int q = threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
+  __syncthreads();
+  for (int q = threadIdx.x; q < p; q += blockDim.x) {
+    double sn, cs;
+    sincospi(2.0 * (double)q / (double)p, &sn, &cs);   // e^{+2 pi i q/p}
+    W[q] = make_double2(cs, sn);
+    const double2 w = chirp_value(q, p);
+    ch[q] = w;
+    const double2 vq = make_double2(w.x, -w.y);        // conj(w[q]) = kernel value at +-q
+    x[q] = vq;
+    if (q > 0) x[M - q] = vq;
+  }
+  __syncthreads();
+  fft_dif(x, M, P.fft_radix + fi * kMaxFftPasses, P.fft_npass[fi], Tw{Tlo, Thi});
+  const double inv = 1.0 / (double)M;
+  double2* V = P.V + (int64_t)s * P.M_stride;
+  for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
+}
+
+// one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
+__global__ void __launch_bounds__(kFftThreads) pfft_kernel(DevParams P, int32_t n_lines) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int s = blockIdx.x / n_lines, n = blockIdx.x % n_lines;
+  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int p = P.st_p[s];
+  const int fi = P.st_M[s];
+  const int M = P.fft_M[fi];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* Tlo = x + M;
+  double2* Thi = Tlo + 128;
+  build_twiddles(Tlo, Thi, M);
+  const double2* ch = P.chirp + (int64_t)s * P.p_stride;
+  double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
+  for (int q = threadIdx.x; q < M; q += blockDim.x)
+    x[q] = q < p ? cmulx(line[q], ch[q]) : make_double2(0.0, 0.0);
+  __syncthreads();
+  const int8_t* rad = P.fft_radix + fi * kMaxFftPasses;
+  const int np = P.fft_npass[fi];
+  const Tw tw{Tlo, Thi};
+  fft_dif(x, M, rad, np, tw);
+  const double2* V = P.V + (int64_t)s * P.M_stride;
+  for (int q = threadIdx.x; q < M; q += blockDim.x) x[q] = cmulx(x[q], V[q]);
+  __syncthreads();
+  fft_dit(x, M, rad, np, tw);
+  for (int b = threadIdx.x; b < p; b += blockDim.x) line[b] = cmulx(x[b], ch[b]);
+}
+
+static size_t fft_smem(int max_M) {
+  return sizeof(double2) * ((size_t)max_M + 128 + (max_M + 127) / 128 + 2);
+}
+
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M, cudaStream_t st) {
+  const size_t smem = fft_smem(max_M);
+  cudaError_t e = cudaFuncSetAttribute(fft_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (n_signals > 0) fft_prep_kernel<<<n_signals, kFftThreads, smem, st>>>(P);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M, cudaStream_t st) {
+  const size_t smem = fft_smem(max_M);
+  cudaError_t e = cudaFuncSetAttribute(pfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const long grid = (long)n_signals * n_lines;
+  if (grid > 0) pfft_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(P, n_lines);
+  return cudaGetLastError();
+}
+
+}  // namespace sfft

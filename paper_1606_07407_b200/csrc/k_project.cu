@@ -1,0 +1,116 @@
+// k_project.cu -- SURVEY 8(a) row a1: reduced (tilted) frequencies and line coefficients.
+//
+//   v_{j,q} = sum_{t < d_q} omega_{j, off_q + t} N^t          (Eq. (35); powers 0..d_q-1)
+//   (v_{j,a0}, v_{j,a1}) <- (b v0 - h v1, h v0 + b v1)          (Eq. (27)) per tilt
+//   C[j][0]   = a_j                                            (unshifted line)
+//   C[j][1+n] = a_j e^{2 pi i (v_{j,n} mod E)/E}                (line shifted by eps = 1/E along axis n)
+//
+// These are the only d-long dot products of the method; they run once per solve.  The exact
+// integer reduction (v mod E) keeps the phase exact (reading R1).
+#include "sfft_internal.cuh"
+
+namespace sfft {
+
+__device__ __forceinline__ double2 line_factor(int64_t v, int64_t E) {
+  // e^{2 pi i (v mod E)/E} via sincospi of the exactly reduced rational 2 (v mod E) / E
+  const int64_t q = mod_pos64(v, E);
+  double s, c;
+  sincospi(2.0 * (double)q / (double)E, &s, &c);
+  return make_double2(c, s);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// one warp per (signal, term)
+__global__ void project_kernel(DevParams P, int32_t batch, const int32_t* __restrict__ freqs,
+                               const double2* __restrict__ coeffs) {
+  const int lane = threadIdx.x & 31;
+  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (gw >= (int64_t)batch * P.k) return;
+  const int s = (int)(gw / P.k), j = (int)(gw % P.k);
+  const int32_t* w = freqs + ((int64_t)s * P.k + j) * P.d;
+  int64_t* vs = P.v_all + (int64_t)s * P.r * P.kk;
+  for (int q = lane; q < P.r; q += 32) {
+    const int off = P.block_off[q], dq = P.block_dims[q];
+    int64_t acc = 0, pw = 1;
+    for (int t = 0; t < dq; ++t) {
+      acc += (int64_t)__ldg(w + off + t) * pw;
+      pw *= P.N;
+    }
+    vs[(int64_t)q * P.kk + j] = acc;
+  }
+  __syncwarp();
+  for (int t = lane; t < P.n_tilts; t += 32) {
+    const int64_t* T = P.tilts + 5 * t;
+    const int64_t a0 = T[0], a1 = T[1], b = T[2], h = T[3];
+    const int64_t u0 = vs[a0 * P.kk + j], u1 = vs[a1 * P.kk + j];
+    vs[a0 * P.kk + j] = b * u0 - h * u1;
+    vs[a1 * P.kk + j] = h * u0 + b * u1;
+  }
+  __syncwarp();
+  const double2 a = coeffs[(int64_t)s * P.k + j];
+  double2* Crow = P.C_all + ((int64_t)s * P.kk + j) * P.Lp;
+  for (int n = lane; n < P.Lp; n += 32) {
+    double2 c;
+    if (n == 0) c = a;
+    else if (n < P.L) c = cmul(a, line_factor(vs[(int64_t)(n - 1) * P.kk + j], P.E));
+    else c = make_double2(0.0, 0.0);
+    Crow[n] = c;
+  }
+}
+
+__global__ void init_state_kernel(DevParams P, int32_t batch) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= batch) return;
+  P.st_status[s] = ST_RUN;
+  P.st_nR[s] = 0;
+  P.st_p[s] = 0;
+  P.st_m[s] = 0;
+  P.st_M[s] = 0;
+  P.st_stall[s] = 0;
+  P.st_iters[s] = 0;
+  P.st_samples[s] = 0;
+  P.st_cmacs[s] = 0;
+}
+
+cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* freqs, const double* coeffs,
+                           cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(P.htab, 0, sizeof(int32_t) * (size_t)batch * P.H, st);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(P.st_log, 0, sizeof(int32_t) * 2 * kLogIters, st);
+  if (e != cudaSuccess) return e;
+  init_state_kernel<<<(batch + 255) / 256, 256, 0, st>>>(P, batch);
+  const int64_t warps = (int64_t)batch * P.k;
+  const int threads = 256;
+  const int64_t blocks = (warps * 32 + threads - 1) / threads;
+  project_kernel<<<(unsigned)blocks, threads, 0, st>>>(P, batch, freqs, reinterpret_cast<const double2*>(coeffs));
+  return cudaGetLastError();
+}
+
+// C rows of signal 0 for K arbitrary terms whose v already sits in v_all[0] (stage entry point).
+__global__ void line_coeffs_kernel(DevParams P, int32_t K, const double2* __restrict__ c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (j >= K) return;
+  const double2 a = c[j];
+  double2* Crow = P.C_all + j * P.Lp;
+  for (int n = lane; n < P.Lp; n += 32) {
+    double2 v;
+    if (n == 0) v = a;
+    else if (n < P.L) v = cmul(a, line_factor(P.v_all[(int64_t)(n - 1) * P.kk + j], P.E));
+    else v = make_double2(0.0, 0.0);
+    Crow[n] = v;
+  }
+}
+
+cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, cudaStream_t st) {
+  const int threads = 256;
+  const int64_t blocks = ((int64_t)K * 32 + threads - 1) / threads;
+  if (blocks > 0)
+    line_coeffs_kernel<<<(unsigned)blocks, threads, 0, st>>>(P, K, reinterpret_cast<const double2*>(c));
+  return cudaGetLastError();
+}
+
+}  // namespace sfft

@@ -1,0 +1,107 @@
+// sfft_internal.cuh -- shared declarations of the sm_100a implementation of the
+// multidimensional phase-shift sparse FFT (arXiv 1606.07407, Algorithm 2).
+// Nothing here is shared with oracle/ (test infrastructure); the two are independent.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sfft.h"
+
+namespace sfft {
+
+// ---- per-signal run state (device) -----------------------------------------------------
+enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK, 1 PARTIAL, <0 error)
+
+constexpr int kMaxFftPasses = 24;
+constexpr int kFftThreads = 512;
+constexpr int kDecodeThreads = 512;
+constexpr int kLogIters = 64;
+
+// Everything a kernel needs, passed by value (kernel parameter space).
+struct DevParams {
+  // problem
+  int32_t d, k, r, L, Lp;     // L = r + 1 lines, Lp = padded line count of C rows
+  int32_t kk;                  // term capacity per signal = 2k (k signal + k registry)
+  int32_t H;                   // hash table slots per signal (pow2 >= 2k)
+  int32_t batch;
+  int64_t N, E;
+  int32_t c, max_iter, stall_limit, extra, n_sched;
+  double tol, floor_rel, prune, round_tol;
+  int32_t n_tilts;
+  int32_t p_cap;               // largest prime the FFT size table supports
+  int64_t p_stride, M_stride;  // line stride (>= p_cap), Bluestein buffer stride (>= M_max)
+  // small tables (device)
+  const int32_t* block_dims;   // [r]
+  const int32_t* block_off;    // [r]
+  const int64_t* lo;           // [r] image interval of every (tilted) axis
+  const int64_t* hi;           // [r]
+  const int64_t* tilts;        // [n_tilts][5]
+  const int32_t* axis_tilt;    // [r] 2*tilt+slot of a tilted axis, -1 otherwise
+  const int64_t* sched;        // [n_sched] explicit primes or null
+  const int32_t* primes;       // sorted primes <= p_cap
+  int32_t n_primes;
+  const int32_t* fft_M;        // [n_fft] allowed Bluestein sizes, ascending
+  const int8_t* fft_radix;     // [n_fft][kMaxFftPasses]
+  const int32_t* fft_npass;    // [n_fft]
+  int32_t n_fft;
+  // buffers (device)
+  int64_t* v_all;              // [batch][r][kk]
+  double2* C_all;              // [batch][kk][Lp]
+  double2* lines;              // [batch][L][p_stride]
+  double2* W_tab;              // [batch][p_stride]   e^{+2 pi i q/p}
+  double2* chirp;              // [batch][p_stride]   e^{-pi i (q^2 mod 2p)/p}
+  double2* V;                  // [batch][M_stride]   DIF spectrum of the Bluestein kernel / M
+  double2* a_reg;              // [batch][k]
+  uint64_t* key_hash;          // [batch][k]
+  int32_t* htab;               // [batch][H]  entry index + 1, 0 = empty
+  int64_t* acc_v;              // [batch][r][k] scratch of decoded coordinates (per candidate)
+  double2* acc_a;              // [batch][k]
+  int32_t* wtmp;               // [batch][k][d] wrap scratch
+  // state (device)
+  int32_t* st_status;          // [batch]
+  int32_t* st_nR;              // [batch]
+  int32_t* st_p;               // [batch]
+  int32_t* st_m;               // [batch]
+  int32_t* st_M;               // [batch] Bluestein size index into fft tables
+  int32_t* st_stall;           // [batch]
+  int32_t* st_iters;           // [batch]
+  int64_t* st_samples;         // [batch]
+  int64_t* st_cmacs;           // [batch]
+  int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
+  int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
+};
+
+// ---- device helpers ----------------------------------------------------------------------
+__host__ __device__ inline int64_t mod_pos64(int64_t x, int64_t m) {
+  int64_t q = x % m;
+  return q < 0 ? q + m : q;
+}
+
+// ---- launchers (each .cu file) ----------------------------------------------------------
+// k_project.cu
+cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* freqs, const double* coeffs,
+                           cudaStream_t st);
+cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, cudaStream_t st);
+// k_decode.cu
+cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st);
+cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, cudaStream_t st);
+cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,
+                                double* acc_a, int32_t* counts, cudaStream_t st);
+size_t decode_smem_bytes(const DevParams& P, int32_t max_p);
+// k_expsum.cu
+struct ExpsumShape { int tn, wn, th, warps, bm, bn, nt; };
+ExpsumShape choose_expsum_shape(int L);
+cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
+                          cudaStream_t st);
+// k_fft.cu
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M, cudaStream_t st);
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M,
+                        cudaStream_t st);
+// k_wrap.cu
+cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freqs, double* out_coeffs,
+                        int32_t* out_count, int32_t* out_status, cudaStream_t st);
+
+}  // namespace sfft

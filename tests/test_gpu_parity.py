@@ -1,0 +1,291 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north star): recovered frequency sets bit-exact, coefficients within 1e-9
+relative (FP64).  Stage tests are teacher-forced: each kernel gets the oracle's exact inputs of
+one iteration.  Full-size configs compare with tests/golden/oracle_c*.npz (written by
+tests/golden/make_oracle_golden.py, which calls only oracle/).
+"""
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import workloads as W
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD_DIR = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def S():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1606_07407_b200 as S
+    from paper_1606_07407_b200 import build as b
+    b.build()
+    return S
+
+
+def _plan(S, c, blocks=None, **kw):
+    return S.sfft_plan(c.d, c.N, c.k, blocks=tuple(blocks or c.blocks), **kw)
+
+
+# ------------------------------------------------------------------ stage parity (teacher forced)
+@pytest.mark.parametrize("name,blocks,p,m", [("c2", (2, 1), 503, 1), ("c2", (1, 1, 1), 101, 2),
+                                             ("c1", (1, 1), 23, 1), ("c3", None, 1009, 7),
+                                             ("c5", None, 2503, 1)])
+def test_stage_expsum_vs_oracle(S, name, blocks, p, m):
+    """a3: every line of one iteration, with signal terms AND registry terms (negated coefficients)."""
+    c = W.CONFIGS[name]
+    blocks = blocks or c.blocks
+    w, a = W.make_signal(c, 2)
+    P = O.params_for(c, blocks=blocks)
+    E, _, _ = O.prepare(P)
+    v = O.project(P, w)
+    # registry: half of the modes with slightly wrong coefficients -> residual terms
+    nreg = c.k // 2
+    vv = np.concatenate([v, v[:nreg]])
+    cc = np.concatenate([a, -a[:nreg] * (1 + 1e-3)])
+    plan = _plan(S, c, blocks)
+    assert plan.E == E
+    got = S.sfft_stage_expsum(plan, torch.from_numpy(np.ascontiguousarray(vv.T)).cuda(),
+                              torch.from_numpy(cc).cuda(), p, m).cpu().numpy()
+    r = len(blocks)
+    scale = np.abs(cc).sum()
+    for n in [-1] + list(range(r)):
+        ref = O.sample_line(vv, cc, p, m, n, E)
+        err = np.abs(got[n + 1] - ref).max()
+        assert err <= 1e-12 * scale, (n, err, scale)
+
+
+@pytest.mark.parametrize("p", [2, 3, 5, 7, 11, 23, 101, 503, 1009, 2503, 5003])
+def test_stage_pfft_vs_oracle_dft(S, p):
+    """a4: Bluestein DFT of prime length against the oracle's direct O(p^2) DFT (and cuFFT)."""
+    c = W.CONFIGS["c2"]
+    plan = _plan(S, c)
+    rng = np.random.default_rng(p)
+    n_lines = 3
+    x = rng.standard_normal((n_lines, p)) + 1j * rng.standard_normal((n_lines, p))
+    xd = torch.from_numpy(x).cuda()
+    S.sfft_stage_pfft(plan, xd)
+    got = xd.cpu().numpy()
+    cufft = torch.fft.fft(torch.from_numpy(x).cuda(), dim=1).cpu().numpy()     # test-only third reference
+    for i in range(n_lines):
+        ref = O.dft(x[i])
+        scale = np.abs(ref).max()
+        assert np.abs(got[i] - ref).max() <= 1e-12 * scale * max(1.0, np.log2(p))
+        assert np.abs(got[i] - cufft[i]).max() <= 1e-12 * scale * max(1.0, np.log2(p))
+
+
+def test_stage_pfft_max_prime(S):
+    c = W.CONFIGS["c2"]
+    plan = _plan(S, c)
+    p = plan.p_max
+    assert p >= 5003
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((1, p)) + 1j * rng.standard_normal((1, p))
+    xd = torch.from_numpy(x).cuda()
+    S.sfft_stage_pfft(plan, xd)
+    ref = np.fft.fft(x[0])     # numpy (pinned to the oracle DFT by test_oracle_pins) for speed
+    assert np.abs(xd.cpu().numpy()[0] - ref).max() <= 1e-11 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("name,blocks,p", [("c2", (2, 1), 503), ("c2", (1, 1, 1), 503), ("c1", (1, 1), 23),
+                                           ("c4", None, 503), ("c3", None, 1009)])
+def test_stage_decode_vs_oracle(S, name, blocks, p):
+    """a5+a6: teacher-forced with the oracle's bins of iteration 1; accepted bins and decoded
+    coordinates exact, coefficients to rounding."""
+    c = W.CONFIGS[name]
+    blocks = blocks or c.blocks
+    w, a = W.make_signal(c, 0)
+    P = O.params_for(c, blocks=blocks)
+    E, lo, hi = O.prepare(P)
+    v = O.project(P, w)
+    r = len(blocks)
+    m = 1 % r
+    F = np.stack([O.dft(O.sample_line(v, a, p, m, n, E)) for n in [-1] + list(range(r))])
+    nc, ob, ov, oa = O.decode(P, E, lo, hi, p, m, c.k, F)
+    plan = _plan(S, c, blocks)
+    gnc, gb, gv, ga = S.sfft_stage_decode(plan, torch.from_numpy(F).cuda(), p, m, c.k)
+    assert gnc == nc
+    assert np.array_equal(gb.cpu().numpy(), ob)
+    assert np.array_equal(gv.cpu().numpy(), ov)
+    assert np.abs(ga.cpu().numpy() - oa).max() <= 1e-15 * np.abs(oa).max()
+    assert ob.size > 0.3 * min(p, c.k)
+
+
+@pytest.mark.parametrize("name,blocks,tilts", [("c2", (2, 1), ()), ("c4", None, ()), ("c3", None, ()),
+                                               ("c2", (1, 1, 1), [(0, 2, 3, 4, 5)])])
+def test_stage_project_vs_oracle(S, name, blocks, tilts):
+    """a1: reduced (tilted) frequencies bit-exact."""
+    c = W.CONFIGS[name]
+    blocks = blocks or c.blocks
+    w, a = W.make_batch(c, [0, 1, 2])
+    P = O.params_for(c, blocks=blocks, tilts=tilts)
+    plan = _plan(S, c, blocks, tilts=tilts, batch=3)
+    sig = S.sfft_signal_expsum(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    got = S.sfft_stage_project(plan, sig).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(got[i].T, O.project(P, w[i]))
+
+
+# ------------------------------------------------------------------ end-to-end parity
+def _check_against_oracle(res, i, ref_w, ref_a, ref_status=O.OK):
+    st = int(res.per_status[i])
+    assert st == ref_status, (i, st)
+    n = int(res.count[i])
+    gw = res.freqs[i, :n].cpu().numpy()
+    ga = res.coeffs[i, :n].cpu().numpy()
+    assert n == ref_w.shape[0] and np.array_equal(gw, ref_w), i
+    if n:
+        assert np.abs(ga - ref_a).max() <= 1e-9 * np.abs(ref_a).max(), i
+
+
+@pytest.mark.parametrize("blocks", [(1, 1), (2,)])
+def test_e2e_config1_batch_vs_live_oracle(S, blocks):
+    c = W.CONFIGS["c1"]
+    trials = list(range(100))
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, blocks, batch=len(trials))
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    assert res.status == S.SFFT_OK
+    for i in trials:
+        ref = O.solve(O.params_for(c, blocks=blocks), w[i], a[i])
+        _check_against_oracle(res, i, ref.w, ref.a)
+        # the input spectrum itself (P:426 exact recovery)
+        ws, as_ = W.canonical_sort(w[i], a[i])
+        assert np.array_equal(res.freqs[i].cpu().numpy(), ws)
+
+
+def _golden(name):
+    return np.load(os.path.join(GOLD_DIR, f"oracle_{name}.npz"))
+
+
+@pytest.mark.parametrize("name,tag,trials", [("c2", "primary", range(16)), ("c2", "alt", range(16)),
+                                             ("c4", "primary", range(4)), ("c4", "alt", [0]),
+                                             ("c3", "primary", range(4)), ("c3", "alt", [0]),
+                                             ("c5", "primary", range(4)), ("c5", "alt", [0])])
+def test_e2e_full_size_vs_golden_oracle(S, name, tag, trials):
+    """BASELINE sizes, the launch configuration bench.py times (one batched execute)."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    blocks = c.blocks if tag == "primary" else c.alt_blocks
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, blocks, batch=len(trials))
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for i, t in enumerate(trials):
+        key = f"{tag}_{t}"
+        st = int(g[key + "_status"])
+        assert int(res.per_status[i]) == st
+        n = int(res.count[i])
+        assert n == int(g[key + "_count"])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        ga = res.coeffs[i, :n].cpu().numpy()
+        ra = g[key + "_a"]
+        assert np.abs(ga - ra).max() <= 1e-9 * np.abs(ra).max(), key
+        ws, _ = W.canonical_sort(w[i], a[i])
+        assert np.array_equal(gw, ws)                         # exact recovery of the input
+    # iteration trace of signal 0 and the total sample count
+    tr = g[f"{tag}_{trials[0]}_trace"]
+    rep = res.report
+    assert [rep.primes[i] for i in range(min(len(tr), 64))] == tr[:64, 1].tolist()
+    assert [rep.accepted[i] for i in range(min(len(tr), 64))] == tr[:64, 4].tolist()
+    assert rep.samples_used == sum(int(g[f"{tag}_{t}_samples"]) for t in trials)
+
+
+def test_e2e_tilted_rectangle_and_fig2(S):
+    """Static tilt (Eq. (27)) recovers the axis-aligned worst case; explicit prime schedule."""
+    w = np.array([[[1, 1], [1, 2], [2, 1], [2, 2]]], np.int32)
+    a = np.exp(2j * np.pi * np.array([[0.1, 0.3, 0.6, 0.8]]))
+    plan = S.sfft_plan(2, 8, 4, blocks=(1, 1), tilts=[(0, 1, 3, 4, 5)])
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    ref = O.solve(O.Params(d=2, N=8, k=4, blocks=(1, 1), tilts=[(0, 1, 3, 4, 5)]), w[0], a[0])
+    _check_against_oracle(res, 0, ref.w, ref.a)
+    # untilted: stall -> PARTIAL, nothing recovered
+    plan = S.sfft_plan(2, 8, 4, blocks=(1, 1))
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    assert res.status == S.SFFT_PARTIAL and int(res.count[0]) == 0
+    # Fig. 2 with the prime schedule (11, 13)
+    w = np.array([[[1, 1], [2, 1], [1, 3]]], np.int32)
+    a = np.exp(2j * np.pi * np.array([[0.1, 0.4, 0.7]]))
+    plan = S.sfft_plan(2, 8, 3, blocks=(1, 1), primes=[11, 13])
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    ref = O.solve(O.Params(d=2, N=8, k=3, blocks=(1, 1), primes=[11, 13]), w[0], a[0])
+    _check_against_oracle(res, 0, ref.w, ref.a)
+    assert [res.report.accepted[i] for i in range(2)] == ref.trace[:, 4].tolist()
+
+
+def test_e2e_edge_cases(S):
+    """k = 1, d = 1 (r = 1, Alg. 1), full unwrap, non-uniform partition, ragged batch."""
+    cases = [W.custom_config(1, 1 << 20, 1, (1,), cfg=60), W.custom_config(1, 4096, 37, (1,), cfg=61),
+             W.custom_config(5, 64, 20, (3, 2), cfg=62), W.custom_config(4, 20, 2, (2, 2), cfg=63),
+             W.custom_config(7, 16, 50, (2, 2, 3), cfg=64)]
+    for c in cases:
+        trials = list(range(6))
+        w, a = W.make_batch(c, trials)
+        plan = _plan(S, c, batch=len(trials))
+        res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+        for i in trials:
+            ref = O.solve(O.params_for(c), w[i], a[i])
+            _check_against_oracle(res, i, ref.w, ref.a, ref.status)
+
+
+def test_e2e_paper_config_small(S):
+    """PAPER.md:422 (N=20, d1=5, d=100), non-power-of-two E = 2 * 20^5."""
+    c = W.paper_config(100, 16)
+    trials = list(range(4))
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, batch=len(trials))
+    assert plan.E == 2 * 20 ** 5
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for i in trials:
+        ref = O.solve(O.params_for(c), w[i], a[i])
+        _check_against_oracle(res, i, ref.w, ref.a)
+
+
+def test_determinism(S):
+    c = W.CONFIGS["c2"]
+    w, a = W.make_batch(c, range(8))
+    plan = _plan(S, c, batch=8)
+    r1 = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    f1, c1 = r1.freqs.clone(), r1.coeffs.clone()
+    r2 = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    assert torch.equal(f1, r2.freqs) and torch.equal(torch.view_as_real(c1), torch.view_as_real(r2.coeffs))
+
+
+def test_solve_host_matches_device(S):
+    c = W.CONFIGS["c2"]
+    w, a = W.make_batch(c, range(4))
+    plan = _plan(S, c, batch=4)
+    rd = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    fd, cd = rd.freqs.cpu(), rd.coeffs.cpu()
+    rh = S.sfft_solve_host(plan, torch.from_numpy(w).pin_memory(), torch.from_numpy(a).pin_memory())
+    assert torch.equal(fd, rh.freqs) and torch.equal(torch.view_as_real(cd), torch.view_as_real(rh.coeffs))
+
+
+def test_error_codes(S):
+    S.sfft_plan(3, 4096, 10, blocks=(3,))                   # N^3 = 2^36 is inside the budget
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(4, 4096, 10, blocks=(4,))               # N^4 = 2^48 > 2^40 (reading R1)
+    assert e.value.status == S.SFFT_EPRECISION
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(3, 63, 10)
+    assert e.value.status == S.SFFT_EINVAL
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(3, 64, 10, blocks=(1, 1))
+    assert e.value.status == S.SFFT_EINVAL
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(2, 64, 4, tilts=[(0, 1, 3, 4, 6)], blocks=(1, 1))
+    assert e.value.status == S.SFFT_EINVAL
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(3, 4096, 5000)                          # first prime 25013 > FFT table
+    assert e.value.status == S.SFFT_ENOTSUP
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(2, 64, 4, eps=1.0 / 3.5)
+    assert e.value.status == S.SFFT_EINVAL
