@@ -63,6 +63,7 @@ typedef struct {
   int32_t batch;              /* max signals per execute [1] */
   int32_t extra_checks;       /* bit0 range check, bit1 bin consistency [3] */
   void* stream;               /* cudaStream_t [legacy default stream] */
+  int32_t profile;            /* 1: time every kernel class with CUDA events on the stream [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */
@@ -76,6 +77,9 @@ typedef struct {
   int64_t primes[64];          /* prime of signal 0 per iteration */
   int32_t accepted[64];        /* bins accepted for signal 0 per iteration */
   int32_t kernel_launches;     /* kernels launched by this execute */
+  /* filled when sfft_options.profile = 1: device time per kernel class (CUDA events on the stream) */
+  int32_t n_expsum;            /* exp-sum launches */
+  float ms_expsum, ms_fft, ms_decode, ms_other;
 } sfft_report;
 
 typedef struct sfft_plan_s sfft_plan_t;

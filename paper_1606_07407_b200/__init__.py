@@ -40,7 +40,7 @@ class sfft_options(ctypes.Structure):
                 ("prune_floor", ctypes.c_double), ("round_tol", ctypes.c_double),
                 ("max_iter", ctypes.c_int32), ("stall_limit", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("extra_checks", ctypes.c_int32),
-                ("stream", ctypes.c_void_p)]
+                ("stream", ctypes.c_void_p), ("profile", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -49,7 +49,9 @@ class sfft_report(ctypes.Structure):
                 ("n_partial", ctypes.c_int32), ("n_error", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("n_iter_logged", ctypes.c_int32),
                 ("primes", ctypes.c_int64 * 64), ("accepted", ctypes.c_int32 * 64),
-                ("kernel_launches", ctypes.c_int32)]
+                ("kernel_launches", ctypes.c_int32), ("n_expsum", ctypes.c_int32),
+                ("ms_expsum", ctypes.c_float), ("ms_fft", ctypes.c_float), ("ms_decode", ctypes.c_float),
+                ("ms_other", ctypes.c_float)]
 
 
 class SfftError(RuntimeError):
@@ -156,7 +158,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               blocks: Optional[Sequence[int]] = None, batch: int = 1, c: int = 5, tol: float = 1e-6,
               bin_floor_rel: float = 1e-8, prune_floor: float = 1e-8, round_tol: float = 0.01,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
-              stream=None) -> Plan:
+              stream=None, profile: bool = False) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -170,6 +172,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.max_iter, opt.stall_limit, opt.batch, opt.extra_checks = max_iter, stall_limit, batch, extra_checks
     st = stream if stream is not None else torch.cuda.current_stream()
     opt.stream = ctypes.c_void_p(st.cuda_stream)
+    opt.profile = 1 if profile else 0
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)

@@ -4,6 +4,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <new>
@@ -32,10 +33,13 @@ struct FftSize {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
+constexpr size_t kPartBytes = (size_t)128 << 20;   // exp-sum partial lines of term-split iterations
+
 }  // namespace
 
 struct sfft_plan_s {
   int device = 0;
+  int n_sm = 148;
   cudaStream_t stream = nullptr;
   // problem
   int32_t d = 0, k = 0, r = 0, L = 0, Lp = 0, kk = 0, H = 0, batch = 1;
@@ -50,6 +54,9 @@ struct sfft_plan_s {
   int32_t p_cap = 0;
   int64_t p_stride = 0, M_stride = 0;
   std::vector<FftSize> fft;
+  std::vector<int32_t> tw_off;        // [n_fft][kMaxFftPasses]
+  std::vector<int4> tw_seg;           // (offset, S, R, 0) per (size, pass)
+  size_t tw_total = 0;
   ExpsumShape shape{};
   // workspace
   size_t ws_bytes = 0;
@@ -58,6 +65,8 @@ struct sfft_plan_s {
   bool tables_ready = false;
   size_t off[64] = {0};
   int32_t* h_ctrl = nullptr;   // pinned
+  bool profile = false;
+  std::vector<cudaEvent_t> events;
   std::string err;
 };
 
@@ -67,7 +76,7 @@ enum Buf {
   B_BLOCKS, B_BOFF, B_LO, B_HI, B_TILTS, B_AXT, B_SCHED, B_PRIMES, B_FFTM, B_FFTR, B_FFTN,
   B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
-  B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE,
+  B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG,
   B_COUNT
 };
 
@@ -111,7 +120,7 @@ FftSize radix_plan(int M) {
   return s;
 }
 
-size_t fft_smem_bytes(int M) { return 16 * ((size_t)M + 128 + (M + 127) / 128 + 2); }
+size_t fft_smem_bytes(int M) { return 16 * ((size_t)M + 2); }
 
 int64_t gcd64(int64_t a, int64_t b) {
   a = a < 0 ? -a : a;
@@ -158,6 +167,11 @@ void layout(sfft_plan_t* P) {
   sz[B_OUT_N] = 4 * S;
   sz[B_OUT_S] = 4 * S;
   sz[B_STAGE] = 64;
+  sz[B_ACTIVE] = 4 * S;
+  sz[B_PART] = kPartBytes;
+  sz[B_TWOFF] = 4 * (size_t)kMaxFftPasses * P->fft.size();
+  sz[B_TW] = 16 * P->tw_total;
+  sz[B_TWSEG] = 16 * P->tw_seg.size();
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -195,6 +209,8 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.fft_M = ptr<int32_t>(P, B_FFTM);
   D.fft_radix = ptr<int8_t>(P, B_FFTR);
   D.fft_npass = ptr<int32_t>(P, B_FFTN);
+  D.fft_tw_off = ptr<int32_t>(P, B_TWOFF);
+  D.fft_tw = ptr<double2>(P, B_TW);
   D.n_fft = (int32_t)P->fft.size();
   D.v_all = ptr<int64_t>(P, B_VALL);
   D.C_all = ptr<double2>(P, B_CALL);
@@ -219,6 +235,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_cmacs = ptr<int64_t>(P, B_CMACS);
   D.st_log = ptr<int32_t>(P, B_LOG);
   D.ctrl = ptr<int32_t>(P, B_CTRL);
+  D.active = ptr<int32_t>(P, B_ACTIVE);
   return D;
 }
 
@@ -256,6 +273,9 @@ int ensure_ready(sfft_plan_t* P) {
     CUDA_TRY(P, up(B_FFTM, fm.data(), 4 * fm.size()));
     CUDA_TRY(P, up(B_FFTR, fr.data(), fr.size()));
     CUDA_TRY(P, up(B_FFTN, fn.data(), 4 * fn.size()));
+    CUDA_TRY(P, up(B_TWOFF, P->tw_off.data(), 4 * P->tw_off.size()));
+    CUDA_TRY(P, up(B_TWSEG, P->tw_seg.data(), 16 * P->tw_seg.size()));
+    CUDA_TRY(P, launch_fft_twiddles(ptr<double2>(P, B_TW), ptr<int4>(P, B_TWSEG), (int)P->tw_seg.size(), P->stream));
     CUDA_TRY(P, cudaStreamSynchronize(P->stream));
     P->tables_ready = true;
   }
@@ -320,6 +340,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     if (opt->batch > 0) P->batch = opt->batch;
     if (opt->extra_checks >= 0) P->extra = opt->extra_checks & 3;
     P->stream = (cudaStream_t)opt->stream;
+    P->profile = opt->profile != 0;
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -395,12 +416,25 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   int smem_optin = 0;
   ce = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, P->device);
   if (ce != cudaSuccess) return SFFT_ECUDA;
+  cudaDeviceGetAttribute(&P->n_sm, cudaDevAttrMultiProcessorCount, P->device);
   int M_max = 0;
   for (int M = 3; fft_smem_bytes(M) <= (size_t)smem_optin; ++M)
     if (is_7smooth(M)) {
       P->fft.push_back(radix_plan(M));
       M_max = M;
     }
+  // per-pass twiddle table layout for every FFT size
+  P->tw_off.assign(P->fft.size() * kMaxFftPasses, 0);
+  for (size_t i = 0; i < P->fft.size(); ++i) {
+    int S = P->fft[i].M;
+    for (size_t ps = 0; ps < P->fft[i].radix.size(); ++ps) {
+      const int R = P->fft[i].radix[ps];
+      P->tw_off[i * kMaxFftPasses + ps] = (int32_t)P->tw_total;
+      P->tw_seg.push_back(make_int4((int)P->tw_total, S, R, 0));
+      P->tw_total += (size_t)(S / R) * (R - 1);
+      S /= R;
+    }
+  }
   P->p_cap = 0;
   {
     const int lim = (M_max + 1) / 2;
@@ -470,6 +504,7 @@ void sfft_plan_destroy(sfft_plan_t* plan) {
   if (!plan) return;
   if (plan->ws_owned && plan->ws) cudaFree(plan->ws);
   if (plan->h_ctrl) cudaFreeHost(plan->h_ctrl);
+  for (cudaEvent_t e : plan->events) cudaEventDestroy(e);
   delete plan;
 }
 
@@ -499,10 +534,23 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   const int32_t batch = sig->batch;
   DevParams D = dev_params(P, batch);
   int launches = 0;
+  // profiling: event marks on the stream, 5 per iteration (prep | expsum | pfft | decode)
+  size_t n_ev = 0;
+  auto mark = [&]() -> int {
+    if (!P->profile) return 0;
+    if (n_ev == P->events.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      P->events.push_back(e);
+    }
+    return cudaEventRecord(P->events[n_ev++], st) == cudaSuccess ? 0 : -1;
+  };
+  mark();
   LAUNCH(P, launch_project(D, batch, sig->freqs, sig->coeffs, st));
   launches += 1;   // init_state_kernel
   int iter = 1;
-  int32_t last_iter = 0;
+  int32_t last_iter = 0, n_expsum = 0;
+  std::vector<size_t> it_marks;
   for (; iter <= P->max_iter; ++iter) {
     LAUNCH(P, launch_setup(D, iter, st));
     CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
@@ -512,14 +560,32 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     const int fi = fft_index_host(P, max_p);
     if (fi < 0) return fail(P, SFFT_ENOTSUP, "p=%d beyond FFT table", max_p);
     const int max_M = P->fft[fi].M;
-    LAUNCH(P, launch_fft_prep(D, batch, max_M, st));
-    LAUNCH(P, launch_expsum(D, P->shape, max_p, batch, st));
-    LAUNCH(P, launch_pfft(D, batch, P->L, max_M, st));
-    LAUNCH(P, launch_decode(D, iter, max_p, st));
+    const int max_K = P->h_ctrl[2];
+    // term split when the (signal x h-tile x n-tile) grid cannot fill the GPU (late iterations)
+    int ksplit = 1;
+    {
+      const int blocks = expsum_blocks(P->shape, max_p, n_active);
+      const int target = 2 * P->n_sm;
+      const int chunks = (max_K + expsum_bk() - 1) / expsum_bk();
+      if (blocks < target) ksplit = std::min({(target + blocks - 1) / blocks, std::max(1, chunks / 2), 32});
+      while (ksplit > 1 && (size_t)ksplit * n_active * P->L * (size_t)max_p * 16 > kPartBytes) --ksplit;
+    }
+    if (P->profile) it_marks.push_back(n_ev);
+    mark();
+    LAUNCH(P, launch_fft_prep(D, n_active, max_M, st));
+    mark();
+    LAUNCH(P, launch_expsum(D, P->shape, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
+    ++n_expsum;
+    mark();
+    LAUNCH(P, launch_pfft(D, n_active, P->L, max_M, ksplit, ptr<double2>(P, B_PART), max_p, st));
+    mark();
+    LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
+    mark();
     last_iter = iter;
   }
   int32_t* ostat = out_status ? out_status : ptr<int32_t>(P, B_OUT_S);
   LAUNCH(P, launch_wrap(D, batch, out_freqs, out_coeffs, out_count, ostat, st));
+  mark();
   // report
   std::vector<int32_t> hs(batch);
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
@@ -547,6 +613,35 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     rep->n_iter_logged = std::min(last_iter, kLogIters);
     for (int i = 0; i < rep->n_iter_logged; ++i) { rep->primes[i] = hlog[2 * i]; rep->accepted[i] = hlog[2 * i + 1]; }
     rep->kernel_launches = launches;
+    rep->n_expsum = n_expsum;
+    if (P->profile && getenv("SFFT_DEBUG")) {
+      for (size_t it = 0; it < it_marks.size(); ++it) {
+        float a = 0, b = 0, c = 0, d = 0;
+        const size_t m0 = it_marks[it];
+        cudaEventElapsedTime(&a, P->events[m0], P->events[m0 + 1]);
+        cudaEventElapsedTime(&b, P->events[m0 + 1], P->events[m0 + 2]);
+        cudaEventElapsedTime(&c, P->events[m0 + 2], P->events[m0 + 3]);
+        cudaEventElapsedTime(&d, P->events[m0 + 3], P->events[m0 + 4]);
+        fprintf(stderr, "[sfft] iter %zu prep %.3f expsum %.3f pfft %.3f decode %.3f ms\n", it + 1, a, b, c, d);
+      }
+    }
+    if (P->profile && n_ev >= 2) {
+      auto el = [&](size_t a, size_t b) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, P->events[a], P->events[b]);
+        return ms;
+      };
+      float tot = el(0, n_ev - 1), fx = 0.f, ff = 0.f, fd = 0.f;
+      for (size_t m0 : it_marks) {
+        ff += el(m0, m0 + 1) + el(m0 + 2, m0 + 3);
+        fx += el(m0 + 1, m0 + 2);
+        fd += el(m0 + 3, m0 + 4);
+      }
+      rep->ms_expsum = fx;
+      rep->ms_fft = ff;
+      rep->ms_decode = fd;
+      rep->ms_other = tot - fx - ff - fd;
+    }
   }
   return worst;
 }
@@ -578,6 +673,7 @@ int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, cons
 // ---------------------------------------------------------------- stage entry points
 static int set_signal0_state(sfft_plan_t* P, const DevParams& D, int p, int m, int nR) {
   int32_t h[5] = {ST_RUN, nR, p, m, 0};
+  CUDA_TRY(P, cudaMemcpyAsync(D.active, &h[4], 4, cudaMemcpyHostToDevice, P->stream));
   CUDA_TRY(P, cudaMemcpyAsync(D.st_status, &h[0], 4, cudaMemcpyHostToDevice, P->stream));
   CUDA_TRY(P, cudaMemcpyAsync(D.st_nR, &h[1], 4, cudaMemcpyHostToDevice, P->stream));
   CUDA_TRY(P, cudaMemcpyAsync(D.st_p, &h[2], 4, cudaMemcpyHostToDevice, P->stream));
@@ -603,7 +699,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
   LAUNCH(P, launch_fft_prep(D, 1, P->fft[fi].M, P->stream));
-  LAUNCH(P, launch_expsum(D, P->shape, (int)p, 1, P->stream));
+  LAUNCH(P, launch_expsum(D, P->shape, (int)p, 1, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
                                 cudaMemcpyDeviceToDevice, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
@@ -625,7 +721,7 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   if (rc) return rc;
   const int M = P->fft[fft_index_host(P, (int)p)].M;
   LAUNCH(P, launch_fft_prep(D, 1, M, P->stream));
-  LAUNCH(P, launch_pfft(D, 1, n_lines, M, P->stream));
+  LAUNCH(P, launch_pfft(D, 1, n_lines, M, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }

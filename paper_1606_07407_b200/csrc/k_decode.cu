@@ -42,7 +42,7 @@ __global__ void setup_kernel(DevParams P, int32_t iter) {
   }
   P.st_p[s] = p;
   P.st_m[s] = iter % P.r;
-  atomicAdd(&P.ctrl[0], 1);
+  P.active[atomicAdd(&P.ctrl[0], 1)] = s;
   atomicMax(&P.ctrl[1], p);
   atomicMax(&P.ctrl[2], P.k + nR);
 }
@@ -106,8 +106,7 @@ __global__ void __launch_bounds__(kDecodeThreads)
 decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, int64_t* out_v,
               double2* out_a, int32_t* out_counts) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.x;
-  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int s = P.active[blockIdx.x];
   const int p = P.st_p[s], m = P.st_m[s];
   const int nR = P.st_nR[s];
   const int kstar = STAGE ? kstar_stage : P.k - nR;
@@ -365,11 +364,12 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   }
 }
 
-cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, cudaStream_t st) {
+cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st) {
   const size_t smem = decode_smem_bytes(P, max_p);
   cudaError_t e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  decode_kernel<false><<<P.batch, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
+  if (n_active > 0)
+    decode_kernel<false><<<n_active, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 

@@ -13,11 +13,15 @@
 // (32*TH) x TN, terms are staged through shared memory in chunks of BK with cp.async double
 // buffering.  One complex MAC = 4 DFMA; C values are warp-broadcast LDS.128, roots are
 // random-index LDS.128.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+
 #include "sfft_internal.cuh"
 
 namespace sfft {
 
-constexpr int kBK = 16;   // terms per staged chunk
+constexpr int kBK = 32;   // terms per staged chunk
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -30,18 +34,21 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 
 template <int TN, int TH, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
-expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles) {
+expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles, int32_t ksplit, double2* part,
+              int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int BN = TN * wn_count;
   const int WH = WARPS / wn_count;
   const int BM = 32 * TH * WH;
 
   int bid = blockIdx.x;
+  const int ks = bid % ksplit;
+  bid /= ksplit;
   const int nt = bid % n_ntiles;
   bid /= n_ntiles;
   const int ht = bid % n_htiles;
-  const int s = bid / n_htiles;
-  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int slot = bid / n_htiles;
+  const int s = P.active[slot];
   const int p = P.st_p[s];
   if (ht * BM >= p) return;
   const int m = P.st_m[s];
@@ -62,7 +69,9 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles)
 
   const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;     // column m of the term keys
   const double2* Cg = P.C_all + (int64_t)s * P.kk * P.Lp + (int64_t)nt * BN;
-  const int n_chunks = (K + kBK - 1) / kBK;
+  const int n_chunks_all = (K + kBK - 1) / kBK;
+  const int per = (n_chunks_all + ksplit - 1) / ksplit;
+  const int c_lo = ks * per, c_hi = min(n_chunks_all, c_lo + per);
 
   auto stage = [&](int buf, int chunk) {
     const int j0 = chunk * kBK;
@@ -92,11 +101,13 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles)
   const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;      // ceil(2^32 / p): x mod p for x < 2^32 / 64
   const int pp = p;
 
-  stage(0, 0);
-  cp_async_commit();
-  for (int ch = 0; ch < n_chunks; ++ch) {
-    const int buf = ch & 1;
-    if (ch + 1 < n_chunks) {
+  if (c_lo < c_hi) {
+    stage(0, c_lo);
+    cp_async_commit();
+  }
+  for (int ch = c_lo; ch < c_hi; ++ch) {
+    const int buf = (ch - c_lo) & 1;
+    if (ch + 1 < c_hi) {
       stage(buf ^ 1, ch + 1);
       cp_async_commit();
       cp_async_wait<1>();
@@ -137,7 +148,16 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles)
     __syncthreads();
   }
 
-  double2* out = P.lines + (int64_t)s * P.L * P.p_stride;
+  double2* out;
+  int64_t pstr;
+  if (ksplit == 1) {
+    out = P.lines + (int64_t)s * P.L * P.p_stride;
+    pstr = P.p_stride;
+  } else {
+    const int n_slots = gridDim.x / (ksplit * n_htiles * n_ntiles);
+    out = part + ((int64_t)ks * n_slots + slot) * P.L * (int64_t)p_part;
+    pstr = p_part;
+  }
   const int n_base = nt * BN + wn * TN;
 #pragma unroll
   for (int n = 0; n < TN; ++n) {
@@ -146,8 +166,179 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles)
 #pragma unroll
     for (int t = 0; t < TH; ++t) {
       const unsigned h = h0 + 32u * t;
-      if (h < (unsigned)p) out[(int64_t)nn * P.p_stride + h] = acc[t][n];
+      if (h < (unsigned)p) out[(int64_t)nn * pstr + h] = acc[t][n];
     }
+  }
+}
+
+// ---------------------------------------------------------------- FP64 tensor-core variant
+// Same contraction on the FP64 tensor pipe: mma.sync.m8n8k4 f64 (SASS DMMA), 4 real MMAs per
+// complex 8x8x4 block (Dr += Ar Br + Ai (-Bi), Di += Ar Bi + Ai Br).  Fragments (PTX ISA m8n8k4
+// .f64): A[m][k] m = lane>>2, k = lane&3; B[k][n] k = lane&3, n = lane>>2; D[m][n] m = lane>>2,
+// n = 2(lane&3)+{0,1}.  Rows m are samples h, columns n are lines, k are terms j: every lane
+// fetches ONE root W_p[(h u_j) mod p] per 8x4 A block and ONE line coefficient per 4x8 B block.
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+__device__ __forceinline__ double dneg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
+
+template <int MB, int NB, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t ksplit, double2* part, int32_t p_part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int BN = 8 * NB;
+  constexpr int BM = 8 * MB * WARPS;
+  constexpr int KS = kBK / 4;                                   // k-steps per staged chunk
+
+  int bid = blockIdx.x;
+  const int ks = bid % ksplit;
+  bid /= ksplit;
+  const int nt = bid % n_ntiles;
+  bid /= n_ntiles;
+  const int ht = bid % n_htiles;
+  const int slot = bid / n_htiles;                              // index into the active-signal list
+  const int s = P.active[slot];
+  const int p = P.st_p[s];
+  if (ht * BM >= p) return;
+  const int m = P.st_m[s];
+  const int K = P.k + P.st_nR[s];
+
+  double2* sW = reinterpret_cast<double2*>(smem_raw);
+  const int p_pad = (p + 1) & ~1;
+  double2* sC = sW + p_pad;                                    // [2][kBK][BN]
+  int2* sU = reinterpret_cast<int2*>(sC + 2 * kBK * BN);        // [2][kBK]  (u, (8u) mod p)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
+  for (int q = tid; q < p; q += WARPS * 32) sW[q] = Wg[q];
+
+  const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;
+  const double2* Cg = P.C_all + (int64_t)s * P.kk * P.Lp + (int64_t)nt * BN;
+  const int n_chunks_all = (K + kBK - 1) / kBK;
+  const int per = (n_chunks_all + ksplit - 1) / ksplit;
+  const int c_lo = ks * per, c_hi = min(n_chunks_all, c_lo + per);
+
+  auto stage = [&](int buf, int chunk) {
+    const int j0 = chunk * kBK;
+    double2* dst = sC + buf * kBK * BN;
+    for (int e = tid; e < kBK * BN; e += WARPS * 32) {
+      const int jj = e / BN, n = e - jj * BN;
+      const int j = j0 + jj;
+      const bool ok = j < K;
+      cp_async16(dst + e, ok ? (const void*)(Cg + (int64_t)j * P.Lp + n) : (const void*)Cg, ok);
+    }
+    if (tid < kBK) {
+      const int j = j0 + tid;
+      int u = 0;
+      if (j < K) u = (int)mod_pos64(vm[j], p);
+      sU[buf * kBK + tid] = make_int2(u, (int)(((int64_t)u * 8) % p));
+    }
+  };
+
+  double acc_r[MB][NB][2], acc_i[MB][NB][2];
+#pragma unroll
+  for (int a = 0; a < MB; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+      acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
+      acc_i[a][b][0] = acc_i[a][b][1] = 0.0;
+    }
+
+  const unsigned hrow = (unsigned)(ht * BM + warp * 8 * MB + (lane >> 2));
+  const int kl = lane & 3, nl = lane >> 2;
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;
+  const int pp = p;
+
+  // fragments of one k-step: MB roots (A) and NB line coefficients (B)
+  struct Frag { double2 tw[MB]; double2 cv[NB]; };
+  auto load_frag = [&](Frag& f, const double2* cb, const int2* ub, int kk) {
+    const int j = kk * 4 + kl;
+    const int2 ud = ub[j];
+    const unsigned x = hrow * (unsigned)ud.x;
+    int r = (int)(x - __umulhi(x, magic) * (unsigned)pp);
+    r += (r >> 31) & pp;
+#pragma unroll
+    for (int a = 0; a < MB; ++a) {
+      f.tw[a] = sW[r];
+      r += ud.y;
+      r -= (r >= pp) ? pp : 0;
+    }
+    const double2* crow = cb + j * BN + nl;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) f.cv[b] = crow[8 * b];
+  };
+  auto mma_frag = [&](const Frag& f) {
+    // two sweeps: the two MMAs into one accumulator are 2*MB*NB MMAs apart
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int a = 0; a < MB; ++a) {
+        dmma(acc_r[a][b][0], acc_r[a][b][1], f.tw[a].x, f.cv[b].x);
+        dmma(acc_i[a][b][0], acc_i[a][b][1], f.tw[a].x, f.cv[b].y);
+      }
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int a = 0; a < MB; ++a) {
+        dmma(acc_r[a][b][0], acc_r[a][b][1], f.tw[a].y, dneg(f.cv[b].y));
+        dmma(acc_i[a][b][0], acc_i[a][b][1], f.tw[a].y, f.cv[b].x);
+      }
+  };
+
+  if (c_lo < c_hi) {
+    stage(0, c_lo);
+    cp_async_commit();
+  }
+  for (int ch = c_lo; ch < c_hi; ++ch) {
+    const int buf = (ch - c_lo) & 1;
+    if (ch + 1 < c_hi) {
+      stage(buf ^ 1, ch + 1);
+      cp_async_commit();
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();
+    const double2* cb = sC + buf * kBK * BN;
+    const int2* ub = sU + buf * kBK;
+    Frag f0, f1;
+    load_frag(f0, cb, ub, 0);
+#pragma unroll
+    for (int kk = 0; kk < KS; kk += 2) {
+      load_frag(f1, cb, ub, kk + 1);              // software pipeline: next fragments in flight
+      mma_frag(f0);
+      if (kk + 2 < KS) load_frag(f0, cb, ub, kk + 2);
+      mma_frag(f1);
+    }
+    __syncthreads();
+  }
+
+  // epilogue: direct store (ksplit == 1) or a partial sum reduced in fixed order by the FFT load
+  double2* out;
+  int64_t pstr;
+  if (ksplit == 1) {
+    out = P.lines + (int64_t)s * P.L * P.p_stride;
+    pstr = P.p_stride;
+  } else {
+    const int n_slots = gridDim.x / (ksplit * n_htiles * n_ntiles);
+    out = part + ((int64_t)ks * n_slots + slot) * P.L * (int64_t)p_part;
+    pstr = p_part;
+  }
+#pragma unroll
+  for (int a = 0; a < MB; ++a) {
+    const unsigned h = (unsigned)(ht * BM + warp * 8 * MB + a * 8 + nl);
+    if (h >= (unsigned)p) continue;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int nn = nt * BN + b * 8 + 2 * kl + e;
+        if (nn < P.L) out[(int64_t)nn * pstr + h] = make_double2(acc_r[a][b][e], acc_i[a][b][e]);
+      }
   }
 }
 
@@ -155,54 +346,116 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles)
 static const int kTNs[] = {1, 2, 3, 4, 5, 6, 7, 8, 11, 13, 16};
 constexpr int kWarps = 8;
 constexpr int kTH = 2;
+constexpr int kDmmaMB = 2;
 
+// Throughput model: per (warp, term) the DFMA kernel spends 2 TH TN SM-cycles on the
+// FP64 pipe and ~8 TH + TN shared-memory wavefronts (random-index root loads, broadcast C loads);
+// the DMMA kernel is FP64-tensor bound (measured 37.1 vs 33.6 TFLOP/s) with padding to 8 lines.
 ExpsumShape choose_expsum_shape(int L) {
   ExpsumShape best{};
-  long best_pad = -1;
+  best.est = -1.0;
   for (int tn : kTNs)
     for (int wn : {1, 2, 4, 8}) {
       const int bn = tn * wn;
       const int nt = (L + bn - 1) / bn;
-      const long pad = (long)nt * bn;
-      bool better = best_pad < 0 || pad < best_pad || (pad == best_pad && tn > best.tn) ||
-                    (pad == best_pad && tn == best.tn && wn < best.wn);
-      if (better) {
-        best_pad = pad;
-        best.tn = tn; best.wn = wn; best.th = kTH; best.warps = kWarps;
-        best.bm = 32 * kTH * (kWarps / wn); best.bn = bn; best.nt = nt;
+      const double util = (double)L / ((double)nt * bn);
+      const double fp = 2.0 * kTH * tn, sm = 8.0 * kTH + tn;
+      const double est = 33.6 * util * fp / std::max(fp, sm);
+      if (est > best.est + 1e-9) {
+        best = ExpsumShape{0, tn, wn, kTH, kWarps, 32 * kTH * (kWarps / wn), bn, nt, 0, 0, est};
       }
     }
+  for (int nb = 1; nb <= 8; ++nb) {
+    const int bn = 8 * nb;
+    const int nt = (L + bn - 1) / bn;
+    const double util = (double)L / ((double)nt * bn);
+    const double est = 37.1 * util * (nb >= 2 ? 1.0 : 0.9);
+    if (est > best.est + 1e-9) best = ExpsumShape{1, 0, 0, 0, kWarps, 8 * kDmmaMB * kWarps, bn, nt, kDmmaMB, nb, est};
+  }
+  // tuning override: SFFT_EXPSUM=dfma:<tn>:<wn> | dmma:<nb> | dmma:<nb>:<mb>
+  if (const char* e = getenv("SFFT_EXPSUM")) {
+    int a = 0, b = 0;
+    if (sscanf(e, "dmma:%d:%d", &a, &b) == 2) {
+      const int bn = 8 * a, nt = (L + bn - 1) / bn;
+      const int warps = b == 1 ? 16 : 8;
+      best = ExpsumShape{1, 0, 0, 0, warps, 8 * b * warps, bn, nt, b, a, 0.0};
+    } else if (sscanf(e, "dfma:%d:%d", &a, &b) == 2) {
+      const int bn = a * b, nt = (L + bn - 1) / bn;
+      best = ExpsumShape{0, a, b, kTH, kWarps, 32 * kTH * (kWarps / b), bn, nt, 0, 0, 0.0};
+    } else if (sscanf(e, "dmma:%d", &a) == 1) {
+      const int bn = 8 * a, nt = (L + bn - 1) / bn;
+      best = ExpsumShape{1, 0, 0, 0, kWarps, 8 * kDmmaMB * kWarps, bn, nt, kDmmaMB, a, 0.0};
+    }
+  }
   return best;
+}
+
+static size_t expsum_smem(int max_p, int bn) {
+  return sizeof(double2) * (size_t)(((max_p + 1) & ~1) + 2 * kBK * bn) + sizeof(int) * 4 * kBK;
+}
+
+struct Split { int ksplit; double2* part; int p_part; };
+
+template <typename KernT, typename... Args>
+static cudaError_t launch_grid(KernT kern, const ExpsumShape& S, int32_t max_p, int32_t n_signals, const Split& sp,
+                               cudaStream_t st, Args... args) {
+  const size_t smem = expsum_smem(max_p, S.bn);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int n_htiles = (max_p + S.bm - 1) / S.bm;
+  const long grid = (long)n_signals * n_htiles * S.nt * sp.ksplit;
+  if (grid <= 0) return cudaSuccess;
+  kern<<<(unsigned)grid, S.warps * 32, smem, st>>>(args..., n_htiles, S.nt, sp.ksplit, sp.part, sp.p_part);
+  return cudaGetLastError();
 }
 
 template <int TN>
 static cudaError_t launch_tn(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
-                             cudaStream_t st) {
-  const int n_htiles = (max_p + S.bm - 1) / S.bm;
-  const size_t smem = sizeof(double2) * (size_t)(((max_p + 1) & ~1) + 2 * kBK * S.bn) + sizeof(int) * 4 * kBK;
-  auto kern = expsum_kernel<TN, kTH, kWarps>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const long grid = (long)n_signals * n_htiles * S.nt;
-  if (grid <= 0) return cudaSuccess;
-  kern<<<(unsigned)grid, kWarps * 32, smem, st>>>(P, S.wn, n_htiles, S.nt);
-  return cudaGetLastError();
+                             const Split& sp, cudaStream_t st) {
+  return launch_grid(expsum_kernel<TN, kTH, kWarps>, S, max_p, n_signals, sp, st, P, (int32_t)S.wn);
+}
+
+template <int NB>
+static cudaError_t launch_nb(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
+                             const Split& sp, cudaStream_t st) {
+  if (S.mb == 1) return launch_grid(expsum_dmma_kernel<1, NB, 16>, S, max_p, n_signals, sp, st, P);
+  return launch_grid(expsum_dmma_kernel<2, NB, 8>, S, max_p, n_signals, sp, st, P);
+}
+
+int expsum_bk() { return kBK; }
+
+int expsum_blocks(const ExpsumShape& S, int32_t max_p, int32_t n_signals) {
+  return n_signals * ((max_p + S.bm - 1) / S.bm) * S.nt;
 }
 
 cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
-                          cudaStream_t st) {
+                          int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st) {
+  const Split sp{ksplit, part, p_part};
+  if (S.kind == 1) {
+    switch (S.nb) {
+      case 1: return launch_nb<1>(P, S, max_p, n_signals, sp, st);
+      case 2: return launch_nb<2>(P, S, max_p, n_signals, sp, st);
+      case 3: return launch_nb<3>(P, S, max_p, n_signals, sp, st);
+      case 4: return launch_nb<4>(P, S, max_p, n_signals, sp, st);
+      case 5: return launch_nb<5>(P, S, max_p, n_signals, sp, st);
+      case 6: return launch_nb<6>(P, S, max_p, n_signals, sp, st);
+      case 7: return launch_nb<7>(P, S, max_p, n_signals, sp, st);
+      case 8: return launch_nb<8>(P, S, max_p, n_signals, sp, st);
+    }
+    return cudaErrorInvalidValue;
+  }
   switch (S.tn) {
-    case 1: return launch_tn<1>(P, S, max_p, n_signals, st);
-    case 2: return launch_tn<2>(P, S, max_p, n_signals, st);
-    case 3: return launch_tn<3>(P, S, max_p, n_signals, st);
-    case 4: return launch_tn<4>(P, S, max_p, n_signals, st);
-    case 5: return launch_tn<5>(P, S, max_p, n_signals, st);
-    case 6: return launch_tn<6>(P, S, max_p, n_signals, st);
-    case 7: return launch_tn<7>(P, S, max_p, n_signals, st);
-    case 8: return launch_tn<8>(P, S, max_p, n_signals, st);
-    case 11: return launch_tn<11>(P, S, max_p, n_signals, st);
-    case 13: return launch_tn<13>(P, S, max_p, n_signals, st);
-    case 16: return launch_tn<16>(P, S, max_p, n_signals, st);
+    case 1: return launch_tn<1>(P, S, max_p, n_signals, sp, st);
+    case 2: return launch_tn<2>(P, S, max_p, n_signals, sp, st);
+    case 3: return launch_tn<3>(P, S, max_p, n_signals, sp, st);
+    case 4: return launch_tn<4>(P, S, max_p, n_signals, sp, st);
+    case 5: return launch_tn<5>(P, S, max_p, n_signals, sp, st);
+    case 6: return launch_tn<6>(P, S, max_p, n_signals, sp, st);
+    case 7: return launch_tn<7>(P, S, max_p, n_signals, sp, st);
+    case 8: return launch_tn<8>(P, S, max_p, n_signals, sp, st);
+    case 11: return launch_tn<11>(P, S, max_p, n_signals, sp, st);
+    case 13: return launch_tn<13>(P, S, max_p, n_signals, sp, st);
+    case 16: return launch_tn<16>(P, S, max_p, n_signals, sp, st);
   }
   return cudaErrorInvalidValue;
 }

@@ -114,74 +114,81 @@ __device__ __forceinline__ void dft_small(double2 (&x)[R]) {
   }
 }
 
-struct Tw {
-  const double2* lo;
-  const double2* hi;
-  __device__ __forceinline__ double2 operator()(int q) const { return cmulx(hi[q >> 7], lo[q & 127]); }
-};
-
+// Per-pass twiddle table (precomputed once per plan for every FFT size, exact index):
+//   tw[n1 * (R-1) + (k-1)] = e^{-2 pi i n1 k / S},  n1 < Q = S/R, 1 <= k < R
+// consecutive lanes (consecutive n1) read consecutive 16-byte groups: coalesced, L1/L2 resident.
 template <int R>
-__device__ __forceinline__ void bfly_dif(double2* x, int base, int Q, int twstep, const Tw& tw) {
+__device__ __forceinline__ void bfly_dif(double2* x, int base, int Q, const double2* __restrict__ tw) {
   double2 v[R];
 #pragma unroll
   for (int n = 0; n < R; ++n) v[n] = x[base + Q * n];
+  double2 w[R - 1];
+#pragma unroll
+  for (int k = 0; k < R - 1; ++k) w[k] = __ldg(tw + k);
   dft_small<R, false>(v);
   x[base] = v[0];
 #pragma unroll
-  for (int k = 1; k < R; ++k) x[base + Q * k] = twstep ? cmulx(v[k], tw(twstep * k)) : v[k];
+  for (int k = 1; k < R; ++k) x[base + Q * k] = cmulx(v[k], w[k - 1]);
 }
 
 template <int R>
-__device__ __forceinline__ void bfly_dit(double2* x, int base, int Q, int twstep, const Tw& tw) {
+__device__ __forceinline__ void bfly_dit(double2* x, int base, int Q, const double2* __restrict__ tw) {
   double2 v[R];
+  double2 w[R - 1];
+#pragma unroll
+  for (int k = 0; k < R - 1; ++k) w[k] = __ldg(tw + k);
   v[0] = x[base];
 #pragma unroll
-  for (int k = 1; k < R; ++k) {
-    const double2 z = x[base + Q * k];
-    v[k] = twstep ? cmulconj(z, tw(twstep * k)) : z;
-  }
+  for (int k = 1; k < R; ++k) v[k] = cmulconj(x[base + Q * k], w[k - 1]);
   dft_small<R, true>(v);
 #pragma unroll
   for (int n = 0; n < R; ++n) x[base + Q * n] = v[n];
 }
 
 template <bool INV>
-__device__ void fft_pass(double2* x, int M, int S, int R, const Tw& tw) {
+__device__ void fft_pass(double2* x, int M, int S, int R, const double2* __restrict__ twp) {
   const int Q = S / R;
   const int nb = M / R;
-  const int mstep = M / S;
   for (int bi = threadIdx.x; bi < nb; bi += blockDim.x) {
     const int blk = bi / Q, n1 = bi - blk * Q;
     const int base = blk * S + n1;
-    const int twstep = n1 * mstep;
+    const double2* tw = twp + n1 * (R - 1);
     switch (R) {
-      case 2: INV ? bfly_dit<2>(x, base, Q, twstep, tw) : bfly_dif<2>(x, base, Q, twstep, tw); break;
-      case 3: INV ? bfly_dit<3>(x, base, Q, twstep, tw) : bfly_dif<3>(x, base, Q, twstep, tw); break;
-      case 4: INV ? bfly_dit<4>(x, base, Q, twstep, tw) : bfly_dif<4>(x, base, Q, twstep, tw); break;
-      case 5: INV ? bfly_dit<5>(x, base, Q, twstep, tw) : bfly_dif<5>(x, base, Q, twstep, tw); break;
-      case 7: INV ? bfly_dit<7>(x, base, Q, twstep, tw) : bfly_dif<7>(x, base, Q, twstep, tw); break;
-      case 8: INV ? bfly_dit<8>(x, base, Q, twstep, tw) : bfly_dif<8>(x, base, Q, twstep, tw); break;
+      case 2: INV ? bfly_dit<2>(x, base, Q, tw) : bfly_dif<2>(x, base, Q, tw); break;
+      case 3: INV ? bfly_dit<3>(x, base, Q, tw) : bfly_dif<3>(x, base, Q, tw); break;
+      case 4: INV ? bfly_dit<4>(x, base, Q, tw) : bfly_dif<4>(x, base, Q, tw); break;
+      case 5: INV ? bfly_dit<5>(x, base, Q, tw) : bfly_dif<5>(x, base, Q, tw); break;
+      case 7: INV ? bfly_dit<7>(x, base, Q, tw) : bfly_dif<7>(x, base, Q, tw); break;
+      case 8: INV ? bfly_dit<8>(x, base, Q, tw) : bfly_dif<8>(x, base, Q, tw); break;
     }
   }
   __syncthreads();
 }
 
 // forward DIF FFT, natural -> digit-reversed
-__device__ void fft_dif(double2* x, int M, const int8_t* radix, int npass, const Tw& tw) {
+__device__ void fft_dif(const DevParams& P, double2* x, int fi) {
+  const int M = P.fft_M[fi];
+  const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
+  const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
+  const int npass = P.fft_npass[fi];
   int S = M;
   for (int ps = 0; ps < npass; ++ps) {
     const int R = radix[ps];
-    fft_pass<false>(x, M, S, R, tw);
+    fft_pass<false>(x, M, S, R, P.fft_tw + off[ps]);
     S /= R;
   }
 }
 // inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
-__device__ void fft_dit(double2* x, int M, const int8_t* radix, int npass, const Tw& tw) {
+__device__ void fft_dit(const DevParams& P, double2* x, int fi) {
+  const int M = P.fft_M[fi];
+  const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
+  const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
+  const int npass = P.fft_npass[fi];
   int S = 1;
   for (int ps = npass - 1; ps >= 0; --ps) {
     const int R = radix[ps];
     S *= R;
-    fft_pass<true>(x, M, S, R, tw);
+    fft_pass<true>(x, M, S, R, P.fft_tw + off[ps]);
   }
 }
 
@@ -195,20 +202,22 @@ __device__ int find_fft_index(const DevParams& P, int p) {
   return lo;
 }
 
-// twiddle tables: T_lo[j] = e^{-2 pi i j / M}, T_hi[j] = e^{-2 pi i 128 j / M}
-__device__ void build_twiddles(double2* Tlo, double2* Thi, int M) {
-  const int nhi = (M + 127) / 128;
-  for (int j = threadIdx.x; j < 128 + nhi; j += blockDim.x) {
+// one segment of the per-pass twiddle tables: e^{-2 pi i n1 k / S} for n1 < S/R, 1 <= k < R
+__global__ void fft_twiddle_kernel(double2* __restrict__ tw, const int4* __restrict__ seg) {
+  const int4 g = seg[blockIdx.x];            // (offset, S, R, unused)
+  const int S = g.y, R = g.z, Q = S / R;
+  for (int e = threadIdx.x; e < Q * (R - 1); e += blockDim.x) {
+    const int n1 = e / (R - 1), k = e % (R - 1) + 1;
+    const int q = (n1 * k) % S;
     double s, c;
-    if (j < 128) {
-      sincospi(-2.0 * (double)j / (double)M, &s, &c);
-      Tlo[j] = make_double2(c, s);
-    } else {
-      const int jj = j - 128;
-      sincospi(-2.0 * (double)(128 * jj) / (double)M, &s, &c);
-      Thi[jj] = make_double2(c, s);
-    }
+    sincospi(-2.0 * (double)q / (double)S, &s, &c);
+    tw[g.x + e] = make_double2(c, s);
   }
+}
+
+cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st) {
+  if (n_seg > 0) fft_twiddle_kernel<<<n_seg, 256, 0, st>>>(tw, seg);
+  return cudaGetLastError();
 }
 
 __device__ __forceinline__ double2 chirp_value(int64_t q, int64_t p) {
@@ -222,16 +231,12 @@ __device__ __forceinline__ double2 chirp_value(int64_t q, int64_t p) {
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
 __global__ void __launch_bounds__(kFftThreads) fft_prep_kernel(DevParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.x;
-  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int s = P.active[blockIdx.x];
   const int p = P.st_p[s];
   const int fi = find_fft_index(P, p);
   const int M = P.fft_M[fi];
   if (threadIdx.x == 0) P.st_M[s] = fi;
   double2* x = reinterpret_cast<double2*>(smem_raw);
-  double2* Tlo = x + M;
-  double2* Thi = Tlo + 128;
-  build_twiddles(Tlo, Thi, M);
   double2* W = P.W_tab + (int64_t)s * P.p_stride;
   double2* ch = P.chirp + (int64_t)s * P.p_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
@@ -247,43 +252,78 @@ __global__ void __launch_bounds__(kFftThreads) fft_prep_kernel(DevParams P) {
     if (q > 0) x[M - q] = vq;
   }
   __syncthreads();
-  fft_dif(x, M, P.fft_radix + fi * kMaxFftPasses, P.fft_npass[fi], Tw{Tlo, Thi});
+  fft_dif(P, x, fi);
   const double inv = 1.0 / (double)M;
   double2* V = P.V + (int64_t)s * P.M_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
 }
 
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
-__global__ void __launch_bounds__(kFftThreads) pfft_kernel(DevParams P, int32_t n_lines) {
+__global__ void __launch_bounds__(kFftThreads)
+pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = blockIdx.x / n_lines, n = blockIdx.x % n_lines;
-  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
+  const int slot = blockIdx.x / n_lines, n = blockIdx.x % n_lines;
+  const int s = P.active[slot];
   const int p = P.st_p[s];
   const int fi = P.st_M[s];
   const int M = P.fft_M[fi];
   double2* x = reinterpret_cast<double2*>(smem_raw);
-  double2* Tlo = x + M;
-  double2* Thi = Tlo + 128;
-  build_twiddles(Tlo, Thi, M);
   const double2* ch = P.chirp + (int64_t)s * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
-  for (int q = threadIdx.x; q < M; q += blockDim.x)
-    x[q] = q < p ? cmulx(line[q], ch[q]) : make_double2(0.0, 0.0);
+  if (ksplit == 1) {
+    // 4 independent loads in flight per thread (latency-bound phase)
+    for (int q0 = threadIdx.x; q0 < M; q0 += 4 * blockDim.x) {
+      double2 a[4], c[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * blockDim.x;
+        a[u] = q < p ? line[q] : make_double2(0.0, 0.0);
+        c[u] = q < p ? ch[q] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < M) x[q] = cmulx(a[u], c[u]);
+      }
+    }
+  } else {
+    // sum the exp-sum partials over the term splits in fixed order (deterministic)
+    const int n_slots = gridDim.x / n_lines;
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+      double2 v = make_double2(0.0, 0.0);
+      if (q < p) {
+        for (int ks = 0; ks < ksplit; ++ks) {
+          const double2 t = part[(((int64_t)ks * n_slots + slot) * n_lines + n) * p_part + q];
+          v.x += t.x;
+          v.y += t.y;
+        }
+        v = cmulx(v, ch[q]);
+      }
+      x[q] = v;
+    }
+  }
   __syncthreads();
-  const int8_t* rad = P.fft_radix + fi * kMaxFftPasses;
-  const int np = P.fft_npass[fi];
-  const Tw tw{Tlo, Thi};
-  fft_dif(x, M, rad, np, tw);
+  fft_dif(P, x, fi);
   const double2* V = P.V + (int64_t)s * P.M_stride;
-  for (int q = threadIdx.x; q < M; q += blockDim.x) x[q] = cmulx(x[q], V[q]);
+  for (int q0 = threadIdx.x; q0 < M; q0 += 4 * blockDim.x) {
+    double2 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * blockDim.x;
+      v[u] = q < M ? V[q] : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int q = q0 + u * blockDim.x;
+      if (q < M) x[q] = cmulx(x[q], v[u]);
+    }
+  }
   __syncthreads();
-  fft_dit(x, M, rad, np, tw);
+  fft_dit(P, x, fi);
   for (int b = threadIdx.x; b < p; b += blockDim.x) line[b] = cmulx(x[b], ch[b]);
 }
 
-static size_t fft_smem(int max_M) {
-  return sizeof(double2) * ((size_t)max_M + 128 + (max_M + 127) / 128 + 2);
-}
+static size_t fft_smem(int max_M) { return sizeof(double2) * ((size_t)max_M + 2); }
 
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M, cudaStream_t st) {
   const size_t smem = fft_smem(max_M);
@@ -293,12 +333,13 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M
   return cudaGetLastError();
 }
 
-cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M, cudaStream_t st) {
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M, int32_t ksplit,
+                        const double2* part, int32_t p_part, cudaStream_t st) {
   const size_t smem = fft_smem(max_M);
   cudaError_t e = cudaFuncSetAttribute(pfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;
-  if (grid > 0) pfft_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(P, n_lines);
+  if (grid > 0) pfft_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(P, n_lines, ksplit, part, p_part);
   return cudaGetLastError();
 }
 

@@ -46,6 +46,8 @@ struct DevParams {
   const int32_t* fft_M;        // [n_fft] allowed Bluestein sizes, ascending
   const int8_t* fft_radix;     // [n_fft][kMaxFftPasses]
   const int32_t* fft_npass;    // [n_fft]
+  const int32_t* fft_tw_off;   // [n_fft][kMaxFftPasses] offsets of the per-pass twiddle tables
+  const double2* fft_tw;       // all per-pass twiddle tables
   int32_t n_fft;
   // buffers (device)
   int64_t* v_all;              // [batch][r][kk]
@@ -72,6 +74,7 @@ struct DevParams {
   int64_t* st_cmacs;           // [batch]
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
+  int32_t* active;             // [batch] indices of the signals still running this iteration
 };
 
 // ---- device helpers ----------------------------------------------------------------------
@@ -87,19 +90,26 @@ cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* fre
 cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, cudaStream_t st);
 // k_decode.cu
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st);
-cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, cudaStream_t st);
+cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st);
 cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,
                                 double* acc_a, int32_t* counts, cudaStream_t st);
 size_t decode_smem_bytes(const DevParams& P, int32_t max_p);
 // k_expsum.cu
-struct ExpsumShape { int tn, wn, th, warps, bm, bn, nt; };
+// kind 0: vector DFMA kernel (lanes along h, TN lines per thread)
+// kind 1: FP64 tensor-core kernel (mma.sync m8n8k4 f64 = DMMA; warp tile 8*MB h x 8*NB lines)
+struct ExpsumShape { int kind, tn, wn, th, warps, bm, bn, nt, mb, nb; double est; };
 ExpsumShape choose_expsum_shape(int L);
+int expsum_blocks(const ExpsumShape& S, int32_t max_p, int32_t n_signals);
+int expsum_bk();
+// ksplit > 1: terms split over ksplit CTAs; partial lines go to part[ks][slot][L][p_part] and are summed
+// in fixed ks order by the FFT load (deterministic, no atomics)
 cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
-                          cudaStream_t st);
+                          int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st);
 // k_fft.cu
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M, cudaStream_t st);
 cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M,
-                        cudaStream_t st);
+                        int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st);
+cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st);
 // k_wrap.cu
 cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freqs, double* out_coeffs,
                         int32_t* out_count, int32_t* out_status, cudaStream_t st);
