@@ -14,7 +14,7 @@ from dataclasses import dataclass
 from typing import Optional, Sequence, Tuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsfft.so")
+LIB_PATH = os.environ.get("SFFT_LIB_PATH") or os.path.join(_HERE, "libsfft.so")   # env: tuning builds only
 
 SFFT_OK, SFFT_PARTIAL = 0, 1
 SFFT_EINVAL, SFFT_EPRECISION, SFFT_EDIM, SFFT_ECORRUPT = -1, -2, -3, -4

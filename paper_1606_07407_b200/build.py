@@ -28,15 +28,17 @@ def _git():
         return "nogit"
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, out=None, defines=()):
+    """Compile every .cu under csrc/ and link libsfft.so (out= and defines= are for tuning builds)."""
+    lib = out or LIB
     srcs = sources()
     newest = max(os.path.getmtime(f) for f in srcs + headers())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
-    objdir = os.path.join(HERE, "build")
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= newest:
+        return lib
+    objdir = os.path.join(HERE, "build" if out is None else "build_" + os.path.basename(out))
     os.makedirs(objdir, exist_ok=True)
     flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-                    f"-DSFFT_GIT=\"{_git()}\"", "--expt-relaxed-constexpr"]
+                    f"-DSFFT_GIT=\"{_git()}\"", "--expt-relaxed-constexpr"] + [f"-D{d}" for d in defines]
     if verbose:
         flags += ["-Xptxas", "-v"]
     procs, objs = [], []
@@ -47,12 +49,14 @@ def build(force=False, verbose=False):
     bad = [p.wait() for p in procs]
     if any(bad):
         raise RuntimeError("nvcc failed")
-    tmp = LIB + f".tmp{os.getpid()}"
+    tmp = lib + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lcudart_static", "-lrt", "-ldl"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
-    print(LIB)
+    args = sys.argv[1:]
+    out = next((a.split("=", 1)[1] for a in args if a.startswith("--out=")), None)
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, out=out, defines=defs))

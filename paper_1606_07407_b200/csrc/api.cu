@@ -29,6 +29,8 @@ namespace {
 struct FftSize {
   int M;
   std::vector<int8_t> radix;
+  size_t smem = 0;        // 16 * (M + sum_passes S/R): data + base twiddles
+  size_t smem_upto = 0;   // max smem over all sizes <= M (launch size when max M is this one)
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -76,7 +78,7 @@ enum Buf {
   B_BLOCKS, B_BOFF, B_LO, B_HI, B_TILTS, B_AXT, B_SCHED, B_PRIMES, B_FFTM, B_FFTR, B_FFTN,
   B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
-  B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG,
+  B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_COUNT
 };
 
@@ -111,16 +113,20 @@ FftSize radix_plan(int M) {
   int x = M;
   for (int f : {2, 3, 5, 7})
     while (x % f == 0) { x /= f; ++e[f]; }
+  // descending radices: the first (largest-Q) pass gets the largest radix -> fewest base twiddles
   while (e[2] >= 3) { s.radix.push_back(8); e[2] -= 3; }
-  if (e[2] == 2) s.radix.push_back(4);
-  if (e[2] == 1) s.radix.push_back(2);
   for (int i = 0; i < e[7]; ++i) s.radix.push_back(7);
   for (int i = 0; i < e[5]; ++i) s.radix.push_back(5);
+  if (e[2] == 2) s.radix.push_back(4);
   for (int i = 0; i < e[3]; ++i) s.radix.push_back(3);
+  if (e[2] == 1) s.radix.push_back(2);
+  size_t sumq = 0;
+  int S = M;
+  for (int8_t R : s.radix) { sumq += S / R; S /= R; }
+  s.smem = 16 * ((size_t)M + sumq + 2);
   return s;
 }
 
-size_t fft_smem_bytes(int M) { return 16 * ((size_t)M + 2); }
 
 int64_t gcd64(int64_t a, int64_t b) {
   a = a < 0 ? -a : a;
@@ -172,6 +178,7 @@ void layout(sfft_plan_t* P) {
   sz[B_TWOFF] = 4 * (size_t)kMaxFftPasses * P->fft.size();
   sz[B_TW] = 16 * P->tw_total;
   sz[B_TWSEG] = 16 * P->tw_seg.size();
+  sz[B_UALL] = 8 * S * (size_t)P->kk + 256;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -214,6 +221,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.n_fft = (int32_t)P->fft.size();
   D.v_all = ptr<int64_t>(P, B_VALL);
   D.C_all = ptr<double2>(P, B_CALL);
+  D.u_all = ptr<int2>(P, B_UALL);
   D.lines = ptr<double2>(P, B_LINES);
   D.W_tab = ptr<double2>(P, B_WTAB);
   D.chirp = ptr<double2>(P, B_CHIRP);
@@ -418,9 +426,13 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   if (ce != cudaSuccess) return SFFT_ECUDA;
   cudaDeviceGetAttribute(&P->n_sm, cudaDevAttrMultiProcessorCount, P->device);
   int M_max = 0;
-  for (int M = 3; fft_smem_bytes(M) <= (size_t)smem_optin; ++M)
+  for (int M = 3; M <= 20000; ++M)
     if (is_7smooth(M)) {
-      P->fft.push_back(radix_plan(M));
+      FftSize f = radix_plan(M);
+      if (f.smem > (size_t)smem_optin) continue;
+      if ((int)f.radix.size() + 1 > kMaxFftPasses) continue;
+      f.smem_upto = std::max(f.smem, P->fft.empty() ? (size_t)0 : P->fft.back().smem_upto);
+      P->fft.push_back(f);
       M_max = M;
     }
   // per-pass twiddle table layout for every FFT size
@@ -431,9 +443,10 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
       const int R = P->fft[i].radix[ps];
       P->tw_off[i * kMaxFftPasses + ps] = (int32_t)P->tw_total;
       P->tw_seg.push_back(make_int4((int)P->tw_total, S, R, 0));
-      P->tw_total += (size_t)(S / R) * (R - 1);
+      P->tw_total += (size_t)(S / R);
       S /= R;
     }
+    P->tw_off[i * kMaxFftPasses + P->fft[i].radix.size()] = (int32_t)P->tw_total;   // end marker
   }
   P->p_cap = 0;
   {
@@ -572,12 +585,12 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     }
     if (P->profile) it_marks.push_back(n_ev);
     mark();
-    LAUNCH(P, launch_fft_prep(D, n_active, max_M, st));
+    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, st));
     mark();
     LAUNCH(P, launch_expsum(D, P->shape, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
     ++n_expsum;
     mark();
-    LAUNCH(P, launch_pfft(D, n_active, P->L, max_M, ksplit, ptr<double2>(P, B_PART), max_p, st));
+    LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, ksplit, ptr<double2>(P, B_PART), max_p, st));
     mark();
     LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
     mark();
@@ -698,7 +711,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   rc = set_signal0_state(P, D, (int)p, m, K - P->k);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  LAUNCH(P, launch_fft_prep(D, 1, P->fft[fi].M, P->stream));
+  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, P->stream));
   LAUNCH(P, launch_expsum(D, P->shape, (int)p, 1, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
                                 cudaMemcpyDeviceToDevice, P->stream));
@@ -719,9 +732,9 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   int launches = 0;
   rc = set_signal0_state(P, D, (int)p, 0, 0);
   if (rc) return rc;
-  const int M = P->fft[fft_index_host(P, (int)p)].M;
-  LAUNCH(P, launch_fft_prep(D, 1, M, P->stream));
-  LAUNCH(P, launch_pfft(D, 1, n_lines, M, 1, nullptr, 0, P->stream));
+  const int sm = (int)P->fft[fft_index_host(P, (int)p)].smem_upto;
+  LAUNCH(P, launch_fft_prep(D, 1, sm, P->stream));
+  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }

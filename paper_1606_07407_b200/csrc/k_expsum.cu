@@ -21,7 +21,10 @@
 
 namespace sfft {
 
-constexpr int kBK = 32;   // terms per staged chunk
+#ifndef SFFT_BK
+#define SFFT_BK 64
+#endif
+constexpr int kBK = SFFT_BK;   // terms per staged chunk
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -51,7 +54,6 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles,
   const int s = P.active[slot];
   const int p = P.st_p[s];
   if (ht * BM >= p) return;
-  const int m = P.st_m[s];
   const int K = P.k + P.st_nR[s];
 
   double2* sW = reinterpret_cast<double2*>(smem_raw);
@@ -67,7 +69,6 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles,
   const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
   for (int q = tid; q < p; q += WARPS * 32) sW[q] = Wg[q];
 
-  const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;     // column m of the term keys
   const double2* Cg = P.C_all + (int64_t)s * P.kk * P.Lp + (int64_t)nt * BN;
   const int n_chunks_all = (K + kBK - 1) / kBK;
   const int per = (n_chunks_all + ksplit - 1) / ksplit;
@@ -84,10 +85,9 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles,
     }
     if (tid < kBK) {
       const int j = j0 + tid;
-      int u = 0;
-      if (j < K) u = (int)mod_pos64(vm[j], p);
+      const int u = j < K ? P.u_all[(int64_t)s * P.kk + j].x : 0;
       sU[buf * kBK + tid] = u;
-      sDU[buf * kBK + tid] = (int)(((int64_t)u * 32) % p);
+      sDU[buf * kBK + tid] = (u * 32) % p;
     }
   };
 
@@ -186,76 +186,22 @@ __device__ __forceinline__ double dneg(double x) {
   return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
 }
 
-template <int MB, int NB, int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t ksplit, double2* part, int32_t p_part) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int BN = 8 * NB;
-  constexpr int BM = 8 * MB * WARPS;
-  constexpr int KS = kBK / 4;                                   // k-steps per staged chunk
+// Warp roles: the WARPS warps form WG = (NB1 ? 2 : 1) column groups.  Group 0 owns columns
+// [0, 8 NB0), group 1 owns [8 NB0, 8 (NB0 + NB1)); inside a group every warp owns 8 MB rows, so a
+// block tile is BM = 8 MB WARPS / WG rows x BN = 8 (NB0 + NB1) lines.  Two column groups double
+// the resident warps per SM at the same accumulator footprint per warp.
+template <int MB, int NB>
+struct DmmaAcc {
+  double r[MB][NB][2], i[MB][NB][2];
+};
 
-  int bid = blockIdx.x;
-  const int ks = bid % ksplit;
-  bid /= ksplit;
-  const int nt = bid % n_ntiles;
-  bid /= n_ntiles;
-  const int ht = bid % n_htiles;
-  const int slot = bid / n_htiles;                              // index into the active-signal list
-  const int s = P.active[slot];
-  const int p = P.st_p[s];
-  if (ht * BM >= p) return;
-  const int m = P.st_m[s];
-  const int K = P.k + P.st_nR[s];
-
-  double2* sW = reinterpret_cast<double2*>(smem_raw);
-  const int p_pad = (p + 1) & ~1;
-  double2* sC = sW + p_pad;                                    // [2][kBK][BN]
-  int2* sU = reinterpret_cast<int2*>(sC + 2 * kBK * BN);        // [2][kBK]  (u, (8u) mod p)
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
-  for (int q = tid; q < p; q += WARPS * 32) sW[q] = Wg[q];
-
-  const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;
-  const double2* Cg = P.C_all + (int64_t)s * P.kk * P.Lp + (int64_t)nt * BN;
-  const int n_chunks_all = (K + kBK - 1) / kBK;
-  const int per = (n_chunks_all + ksplit - 1) / ksplit;
-  const int c_lo = ks * per, c_hi = min(n_chunks_all, c_lo + per);
-
-  auto stage = [&](int buf, int chunk) {
-    const int j0 = chunk * kBK;
-    double2* dst = sC + buf * kBK * BN;
-    for (int e = tid; e < kBK * BN; e += WARPS * 32) {
-      const int jj = e / BN, n = e - jj * BN;
-      const int j = j0 + jj;
-      const bool ok = j < K;
-      cp_async16(dst + e, ok ? (const void*)(Cg + (int64_t)j * P.Lp + n) : (const void*)Cg, ok);
-    }
-    if (tid < kBK) {
-      const int j = j0 + tid;
-      int u = 0;
-      if (j < K) u = (int)mod_pos64(vm[j], p);
-      sU[buf * kBK + tid] = make_int2(u, (int)(((int64_t)u * 8) % p));
-    }
-  };
-
-  double acc_r[MB][NB][2], acc_i[MB][NB][2];
-#pragma unroll
-  for (int a = 0; a < MB; ++a)
-#pragma unroll
-    for (int b = 0; b < NB; ++b) {
-      acc_r[a][b][0] = acc_r[a][b][1] = 0.0;
-      acc_i[a][b][0] = acc_i[a][b][1] = 0.0;
-    }
-
-  const unsigned hrow = (unsigned)(ht * BM + warp * 8 * MB + (lane >> 2));
-  const int kl = lane & 3, nl = lane >> 2;
-  const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;
-  const int pp = p;
-
-  // fragments of one k-step: MB roots (A) and NB line coefficients (B)
+template <int MB, int NB, int BN>
+__device__ __forceinline__ void dmma_chunk(DmmaAcc<MB, NB>& acc, const double2* __restrict__ sW,
+                                           const double2* __restrict__ cb, const int2* __restrict__ ub,
+                                           unsigned hrow, int col0, int kl, int nl, unsigned magic, int pp) {
+  constexpr int KS = kBK / 4;
   struct Frag { double2 tw[MB]; double2 cv[NB]; };
-  auto load_frag = [&](Frag& f, const double2* cb, const int2* ub, int kk) {
+  auto load_frag = [&](Frag& f, int kk) {
     const int j = kk * 4 + kl;
     const int2 ud = ub[j];
     const unsigned x = hrow * (unsigned)ud.x;
@@ -267,28 +213,67 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
       r += ud.y;
       r -= (r >= pp) ? pp : 0;
     }
-    const double2* crow = cb + j * BN + nl;
+    const double2* crow = cb + j * BN + col0 + nl;
 #pragma unroll
     for (int b = 0; b < NB; ++b) f.cv[b] = crow[8 * b];
   };
   auto mma_frag = [&](const Frag& f) {
-    // two sweeps: the two MMAs into one accumulator are 2*MB*NB MMAs apart
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int a = 0; a < MB; ++a) {
-        dmma(acc_r[a][b][0], acc_r[a][b][1], f.tw[a].x, f.cv[b].x);
-        dmma(acc_i[a][b][0], acc_i[a][b][1], f.tw[a].x, f.cv[b].y);
+        dmma(acc.r[a][b][0], acc.r[a][b][1], f.tw[a].x, f.cv[b].x);
+        dmma(acc.i[a][b][0], acc.i[a][b][1], f.tw[a].x, f.cv[b].y);
       }
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
       for (int a = 0; a < MB; ++a) {
-        dmma(acc_r[a][b][0], acc_r[a][b][1], f.tw[a].y, dneg(f.cv[b].y));
-        dmma(acc_i[a][b][0], acc_i[a][b][1], f.tw[a].y, f.cv[b].x);
+        dmma(acc.r[a][b][0], acc.r[a][b][1], f.tw[a].y, dneg(f.cv[b].y));
+        dmma(acc.i[a][b][0], acc.i[a][b][1], f.tw[a].y, f.cv[b].x);
       }
   };
+  Frag f0, f1;
+  load_frag(f0, 0);
+#pragma unroll
+  for (int kk = 0; kk < KS; kk += 2) {
+    load_frag(f1, kk + 1);
+    mma_frag(f0);
+    if (kk + 2 < KS) load_frag(f0, kk + 2);
+    mma_frag(f1);
+  }
+}
 
+template <int MB, int NB>
+__device__ __forceinline__ void dmma_store(const DmmaAcc<MB, NB>& acc, double2* out, int64_t pstr, int L, int p,
+                                           unsigned hrow0, int col0, int kl, int nl) {
+#pragma unroll
+  for (int a = 0; a < MB; ++a) {
+    const unsigned h = hrow0 + a * 8 + nl;
+    if (h >= (unsigned)p) continue;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int nn = col0 + b * 8 + 2 * kl + e;
+        if (nn < L) out[(int64_t)nn * pstr + h] = make_double2(acc.r[a][b][e], acc.i[a][b][e]);
+      }
+  }
+}
+
+// The whole term loop of one column group (staging is shared by all warps of the block; every
+// warp of both groups reaches the same sequence of block barriers).
+template <int MB, int NB, int BN, int WARPS, typename StageF>
+__device__ __forceinline__ void dmma_group(StageF&& stage, const double2* sW, const double2* sC, const int2* sU,
+                                           int c_lo, int c_hi, unsigned hrow0, int col0, int lane, unsigned magic,
+                                           int p, double2* out, int64_t pstr, int L, int col_base) {
+  DmmaAcc<MB, NB> acc;
+#pragma unroll
+  for (int a = 0; a < MB; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc.r[a][b][0] = acc.r[a][b][1] = acc.i[a][b][0] = acc.i[a][b][1] = 0.0;
+  const int kl = lane & 3, nl = lane >> 2;
+  const unsigned hrow = hrow0 + nl;
   if (c_lo < c_hi) {
     stage(0, c_lo);
     cp_async_commit();
@@ -303,21 +288,64 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double2* cb = sC + buf * kBK * BN;
-    const int2* ub = sU + buf * kBK;
-    Frag f0, f1;
-    load_frag(f0, cb, ub, 0);
-#pragma unroll
-    for (int kk = 0; kk < KS; kk += 2) {
-      load_frag(f1, cb, ub, kk + 1);              // software pipeline: next fragments in flight
-      mma_frag(f0);
-      if (kk + 2 < KS) load_frag(f0, cb, ub, kk + 2);
-      mma_frag(f1);
-    }
+    dmma_chunk<MB, NB, BN>(acc, sW, sC + buf * kBK * BN, sU + buf * kBK, hrow, col0, kl, nl, magic, p);
     __syncthreads();
   }
+  dmma_store<MB, NB>(acc, out, pstr, L, p, hrow0, col_base + col0, kl, nl);
+}
 
-  // epilogue: direct store (ksplit == 1) or a partial sum reduced in fixed order by the FFT load
+template <int MB, int NB0, int NB1, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t ksplit, double2* part, int32_t p_part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int WG = NB1 ? 2 : 1;
+  constexpr int WPG = WARPS / WG;                               // warps per column group
+  constexpr int BN = 8 * (NB0 + NB1);
+  constexpr int BM = 8 * MB * WPG;
+
+  int bid = blockIdx.x;
+  const int ks = bid % ksplit;
+  bid /= ksplit;
+  const int nt = bid % n_ntiles;
+  bid /= n_ntiles;
+  const int ht = bid % n_htiles;
+  const int slot = bid / n_htiles;                              // index into the active-signal list
+  const int s = P.active[slot];
+  const int p = P.st_p[s];
+  if (ht * BM >= p) return;
+  const int K = P.k + P.st_nR[s];
+
+  double2* sW = reinterpret_cast<double2*>(smem_raw);
+  const int p_pad = (p + 1) & ~1;
+  double2* sC = sW + p_pad;                                    // [2][kBK][BN]
+  int2* sU = reinterpret_cast<int2*>(sC + 2 * kBK * BN);        // [2][kBK]  (u, (8u) mod p)
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wg = warp / WPG, wr = warp % WPG;
+  const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
+  for (int q = tid; q < p; q += WARPS * 32) cp_async16(sW + q, Wg + q, true);   // joins the first stage group
+
+  const int2* ug = P.u_all + (int64_t)s * P.kk;
+  const double2* Cg = P.C_all + (int64_t)s * P.kk * P.Lp + (int64_t)nt * BN;
+  const int n_chunks_all = (K + kBK - 1) / kBK;
+  const int per = (n_chunks_all + ksplit - 1) / ksplit;
+  const int c_lo = ks * per, c_hi = min(n_chunks_all, c_lo + per);
+
+  auto stage = [&](int buf, int chunk) {
+    const int j0 = chunk * kBK;
+    double2* dst = sC + buf * kBK * BN;
+    for (int e = tid; e < kBK * BN; e += WARPS * 32) {
+      const int jj = e / BN, n = e - jj * BN;
+      const int j = j0 + jj;
+      const bool ok = j < K;
+      cp_async16(dst + e, ok ? (const void*)(Cg + (int64_t)j * P.Lp + n) : (const void*)Cg, ok);
+    }
+    if (tid < kBK / 2) {                                        // 16-byte copies of two (u, 8u mod p) pairs
+      const int j = j0 + 2 * tid;
+      cp_async16(sU + buf * kBK + 2 * tid, ug + j, j < K);
+    }
+  };
+
   double2* out;
   int64_t pstr;
   if (ksplit == 1) {
@@ -328,18 +356,13 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
     out = part + ((int64_t)ks * n_slots + slot) * P.L * (int64_t)p_part;
     pstr = p_part;
   }
-#pragma unroll
-  for (int a = 0; a < MB; ++a) {
-    const unsigned h = (unsigned)(ht * BM + warp * 8 * MB + a * 8 + nl);
-    if (h >= (unsigned)p) continue;
-#pragma unroll
-    for (int b = 0; b < NB; ++b)
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int nn = nt * BN + b * 8 + 2 * kl + e;
-        if (nn < P.L) out[(int64_t)nn * pstr + h] = make_double2(acc_r[a][b][e], acc_i[a][b][e]);
-      }
-  }
+  const unsigned hrow0 = (unsigned)(ht * BM + wr * 8 * MB);
+  const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;
+  if (NB1 == 0 || wg == 0)
+    dmma_group<MB, NB0, BN, WARPS>(stage, sW, sC, sU, c_lo, c_hi, hrow0, 0, lane, magic, p, out, pstr, P.L, nt * BN);
+  else
+    dmma_group<MB, (NB1 ? NB1 : 1), BN, WARPS>(stage, sW, sC, sU, c_lo, c_hi, hrow0, 8 * NB0, lane, magic, p, out,
+                                               pstr, P.L, nt * BN);
 }
 
 // ---------------------------------------------------------------- host side
@@ -360,7 +383,7 @@ ExpsumShape choose_expsum_shape(int L) {
       const int nt = (L + bn - 1) / bn;
       const double util = (double)L / ((double)nt * bn);
       const double fp = 2.0 * kTH * tn, sm = 8.0 * kTH + tn;
-      const double est = 33.6 * util * fp / std::max(fp, sm);
+      const double est = 0.45 * 33.6 * util * fp / std::max(fp, sm);     // 0.45: measured DFMA efficiency
       if (est > best.est + 1e-9) {
         best = ExpsumShape{0, tn, wn, kTH, kWarps, 32 * kTH * (kWarps / wn), bn, nt, 0, 0, est};
       }
@@ -369,7 +392,7 @@ ExpsumShape choose_expsum_shape(int L) {
     const int bn = 8 * nb;
     const int nt = (L + bn - 1) / bn;
     const double util = (double)L / ((double)nt * bn);
-    const double est = 37.1 * util * (nb >= 2 ? 1.0 : 0.9);
+    const double est = 0.8 * 37.1 * util * (nb >= 2 ? 1.0 : 0.9);      // 0.8: measured DMMA efficiency
     if (est > best.est + 1e-9) best = ExpsumShape{1, 0, 0, 0, kWarps, 8 * kDmmaMB * kWarps, bn, nt, kDmmaMB, nb, est};
   }
   // tuning override: SFFT_EXPSUM=dfma:<tn>:<wn> | dmma:<nb> | dmma:<nb>:<mb>
@@ -377,8 +400,9 @@ ExpsumShape choose_expsum_shape(int L) {
     int a = 0, b = 0;
     if (sscanf(e, "dmma:%d:%d", &a, &b) == 2) {
       const int bn = 8 * a, nt = (L + bn - 1) / bn;
-      const int warps = b == 1 ? 16 : 8;
-      best = ExpsumShape{1, 0, 0, 0, warps, 8 * b * warps, bn, nt, b, a, 0.0};
+      const int warps = b == 2 ? 8 : 16;
+      const int bm = b == 1 ? 128 : 128;
+      best = ExpsumShape{1, 0, 0, 0, warps, bm, bn, nt, b, a, 0.0};
     } else if (sscanf(e, "dfma:%d:%d", &a, &b) == 2) {
       const int bn = a * b, nt = (L + bn - 1) / bn;
       best = ExpsumShape{0, a, b, kTH, kWarps, 32 * kTH * (kWarps / b), bn, nt, 0, 0, 0.0};
@@ -418,8 +442,11 @@ static cudaError_t launch_tn(const DevParams& P, const ExpsumShape& S, int32_t m
 template <int NB>
 static cudaError_t launch_nb(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
                              const Split& sp, cudaStream_t st) {
-  if (S.mb == 1) return launch_grid(expsum_dmma_kernel<1, NB, 16>, S, max_p, n_signals, sp, st, P);
-  return launch_grid(expsum_dmma_kernel<2, NB, 8>, S, max_p, n_signals, sp, st, P);
+  // mb 1: 16 warps x (8 rows); mb 2: 8 warps x (16 rows); mb 3: 16 warps in two column groups x (16 rows)
+  if (S.mb == 1) return launch_grid(expsum_dmma_kernel<1, NB, 0, 16>, S, max_p, n_signals, sp, st, P);
+  if (S.mb == 3 && NB >= 2)
+    return launch_grid(expsum_dmma_kernel<2, (NB + 1) / 2, NB / 2, 16>, S, max_p, n_signals, sp, st, P);
+  return launch_grid(expsum_dmma_kernel<2, NB, 0, 8>, S, max_p, n_signals, sp, st, P);
 }
 
 int expsum_bk() { return kBK; }

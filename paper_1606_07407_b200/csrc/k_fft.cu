@@ -114,59 +114,78 @@ __device__ __forceinline__ void dft_small(double2 (&x)[R]) {
   }
 }
 
-// Per-pass twiddle table (precomputed once per plan for every FFT size, exact index):
-//   tw[n1 * (R-1) + (k-1)] = e^{-2 pi i n1 k / S},  n1 < Q = S/R, 1 <= k < R
-// consecutive lanes (consecutive n1) read consecutive 16-byte groups: coalesced, L1/L2 resident.
-template <int R>
-__device__ __forceinline__ void bfly_dif(double2* x, int base, int Q, const double2* __restrict__ tw) {
-  double2 v[R];
+// Per-pass base twiddles (precomputed once per plan for every FFT size, exact index) are copied
+// into shared memory next to the data: base[n1] = e^{-2 pi i n1 / S} for n1 < Q = S/R; the
+// butterfly forms e^{-2 pi i n1 k / S} = base^k by repeated products (error ~k ulp, k < 8).
+// Two butterflies per loop trip with all loads issued before any store (ILP across the
+// shared-memory latency).
+template <int R, bool INV>
+__device__ __forceinline__ void bfly_load(const double2* x, int base, int Q, double2 (&v)[R]) {
 #pragma unroll
   for (int n = 0; n < R; ++n) v[n] = x[base + Q * n];
-  double2 w[R - 1];
-#pragma unroll
-  for (int k = 0; k < R - 1; ++k) w[k] = __ldg(tw + k);
-  dft_small<R, false>(v);
-  x[base] = v[0];
-#pragma unroll
-  for (int k = 1; k < R; ++k) x[base + Q * k] = cmulx(v[k], w[k - 1]);
 }
 
-template <int R>
-__device__ __forceinline__ void bfly_dit(double2* x, int base, int Q, const double2* __restrict__ tw) {
-  double2 v[R];
-  double2 w[R - 1];
+template <int R, bool INV>
+__device__ __forceinline__ void bfly_finish(double2* x, int base, int Q, double2 b, double2 (&v)[R]) {
+  if (!INV) {
+    dft_small<R, false>(v);
+    x[base] = v[0];
+    double2 w = b;
 #pragma unroll
-  for (int k = 0; k < R - 1; ++k) w[k] = __ldg(tw + k);
-  v[0] = x[base];
+    for (int k = 1; k < R; ++k) {
+      x[base + Q * k] = cmulx(v[k], w);
+      if (k + 1 < R) w = cmulx(w, b);
+    }
+  } else {
+    double2 w = b;
 #pragma unroll
-  for (int k = 1; k < R; ++k) v[k] = cmulconj(x[base + Q * k], w[k - 1]);
-  dft_small<R, true>(v);
+    for (int k = 1; k < R; ++k) {
+      v[k] = cmulconj(v[k], w);
+      if (k + 1 < R) w = cmulx(w, b);
+    }
+    dft_small<R, true>(v);
 #pragma unroll
-  for (int n = 0; n < R; ++n) x[base + Q * n] = v[n];
+    for (int n = 0; n < R; ++n) x[base + Q * n] = v[n];
+  }
 }
 
-template <bool INV>
-__device__ void fft_pass(double2* x, int M, int S, int R, const double2* __restrict__ twp) {
+template <int R, bool INV>
+__device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double2* __restrict__ tb) {
   const int Q = S / R;
   const int nb = M / R;
   for (int bi = threadIdx.x; bi < nb; bi += blockDim.x) {
     const int blk = bi / Q, n1 = bi - blk * Q;
     const int base = blk * S + n1;
-    const double2* tw = twp + n1 * (R - 1);
-    switch (R) {
-      case 2: INV ? bfly_dit<2>(x, base, Q, tw) : bfly_dif<2>(x, base, Q, tw); break;
-      case 3: INV ? bfly_dit<3>(x, base, Q, tw) : bfly_dif<3>(x, base, Q, tw); break;
-      case 4: INV ? bfly_dit<4>(x, base, Q, tw) : bfly_dif<4>(x, base, Q, tw); break;
-      case 5: INV ? bfly_dit<5>(x, base, Q, tw) : bfly_dif<5>(x, base, Q, tw); break;
-      case 7: INV ? bfly_dit<7>(x, base, Q, tw) : bfly_dif<7>(x, base, Q, tw); break;
-      case 8: INV ? bfly_dit<8>(x, base, Q, tw) : bfly_dif<8>(x, base, Q, tw); break;
-    }
+    double2 v[R];
+    bfly_load<R, INV>(x, base, Q, v);
+    bfly_finish<R, INV>(x, base, Q, tb[n1], v);
+  }
+}
+
+template <bool INV>
+__device__ void fft_pass(double2* x, int M, int S, int R, const double2* tb) {
+  switch (R) {
+    case 2: pass_loop<2, INV>(x, M, S, tb); break;
+    case 3: pass_loop<3, INV>(x, M, S, tb); break;
+    case 4: pass_loop<4, INV>(x, M, S, tb); break;
+    case 5: pass_loop<5, INV>(x, M, S, tb); break;
+    case 7: pass_loop<7, INV>(x, M, S, tb); break;
+    case 8: pass_loop<8, INV>(x, M, S, tb); break;
   }
   __syncthreads();
 }
 
-// forward DIF FFT, natural -> digit-reversed
-__device__ void fft_dif(const DevParams& P, double2* x, int fi) {
+// copy the base-twiddle tables of FFT size fi into shared memory (after the data array)
+__device__ void load_twiddles(const DevParams& P, int fi, double2* tb) {
+  const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
+  const int npass = P.fft_npass[fi];
+  const int n = off[npass] - off[0];
+  const double2* src = P.fft_tw + off[0];
+  for (int q = threadIdx.x; q < n; q += blockDim.x) tb[q] = src[q];
+}
+
+// forward DIF FFT, natural -> digit-reversed; tb = shared copy of this size's tables
+__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -174,12 +193,12 @@ __device__ void fft_dif(const DevParams& P, double2* x, int fi) {
   int S = M;
   for (int ps = 0; ps < npass; ++ps) {
     const int R = radix[ps];
-    fft_pass<false>(x, M, S, R, P.fft_tw + off[ps]);
+    fft_pass<false>(x, M, S, R, tb + (off[ps] - off[0]));
     S /= R;
   }
 }
 // inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
-__device__ void fft_dit(const DevParams& P, double2* x, int fi) {
+__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -188,7 +207,7 @@ __device__ void fft_dit(const DevParams& P, double2* x, int fi) {
   for (int ps = npass - 1; ps >= 0; --ps) {
     const int R = radix[ps];
     S *= R;
-    fft_pass<true>(x, M, S, R, P.fft_tw + off[ps]);
+    fft_pass<true>(x, M, S, R, tb + (off[ps] - off[0]));
   }
 }
 
@@ -202,16 +221,14 @@ __device__ int find_fft_index(const DevParams& P, int p) {
   return lo;
 }
 
-// one segment of the per-pass twiddle tables: e^{-2 pi i n1 k / S} for n1 < S/R, 1 <= k < R
+// one segment of the base-twiddle tables: e^{-2 pi i n1 / S} for n1 < S/R
 __global__ void fft_twiddle_kernel(double2* __restrict__ tw, const int4* __restrict__ seg) {
   const int4 g = seg[blockIdx.x];            // (offset, S, R, unused)
   const int S = g.y, R = g.z, Q = S / R;
-  for (int e = threadIdx.x; e < Q * (R - 1); e += blockDim.x) {
-    const int n1 = e / (R - 1), k = e % (R - 1) + 1;
-    const int q = (n1 * k) % S;
+  for (int n1 = threadIdx.x; n1 < Q; n1 += blockDim.x) {
     double s, c;
-    sincospi(-2.0 * (double)q / (double)S, &s, &c);
-    tw[g.x + e] = make_double2(c, s);
+    sincospi(-2.0 * (double)n1 / (double)S, &s, &c);
+    tw[g.x + n1] = make_double2(c, s);
   }
 }
 
@@ -229,14 +246,27 @@ __device__ __forceinline__ double2 chirp_value(int64_t q, int64_t p) {
 }
 
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
-__global__ void __launch_bounds__(kFftThreads) fft_prep_kernel(DevParams P) {
+__global__ void __launch_bounds__(kFftThreads, 1) fft_prep_kernel(DevParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = P.active[blockIdx.x];
   const int p = P.st_p[s];
   const int fi = find_fft_index(P, p);
   const int M = P.fft_M[fi];
   if (threadIdx.x == 0) P.st_M[s] = fi;
+  // term phases of this iteration (exp-sum A operand index): u_j = v_{j,m} mod p, 8 u_j mod p
+  {
+    const int m = P.st_m[s];
+    const int K = P.k + P.st_nR[s];
+    const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;
+    int2* ug = P.u_all + (int64_t)s * P.kk;
+    for (int j = threadIdx.x; j < K; j += blockDim.x) {
+      const int u = (int)mod_pos64(vm[j], p);
+      ug[j] = make_int2(u, (8 * u) % p);
+    }
+  }
   double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* tb = x + M;
+  load_twiddles(P, fi, tb);
   double2* W = P.W_tab + (int64_t)s * P.p_stride;
   double2* ch = P.chirp + (int64_t)s * P.p_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
@@ -252,14 +282,14 @@ __global__ void __launch_bounds__(kFftThreads) fft_prep_kernel(DevParams P) {
     if (q > 0) x[M - q] = vq;
   }
   __syncthreads();
-  fft_dif(P, x, fi);
+  fft_dif(P, x, fi, tb);
   const double inv = 1.0 / (double)M;
   double2* V = P.V + (int64_t)s * P.M_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
 }
 
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
-__global__ void __launch_bounds__(kFftThreads)
+__global__ void __launch_bounds__(kFftThreads, 1)
 pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int slot = blockIdx.x / n_lines, n = blockIdx.x % n_lines;
@@ -268,6 +298,8 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   const int fi = P.st_M[s];
   const int M = P.fft_M[fi];
   double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* tb = x + M;
+  load_twiddles(P, fi, tb);
   const double2* ch = P.chirp + (int64_t)s * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
   if (ksplit == 1) {
@@ -303,7 +335,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     }
   }
   __syncthreads();
-  fft_dif(P, x, fi);
+  fft_dif(P, x, fi, tb);
   const double2* V = P.V + (int64_t)s * P.M_stride;
   for (int q0 = threadIdx.x; q0 < M; q0 += 4 * blockDim.x) {
     double2 v[4];
@@ -319,23 +351,21 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     }
   }
   __syncthreads();
-  fft_dit(P, x, fi);
+  fft_dit(P, x, fi, tb);
   for (int b = threadIdx.x; b < p; b += blockDim.x) line[b] = cmulx(x[b], ch[b]);
 }
 
-static size_t fft_smem(int max_M) { return sizeof(double2) * ((size_t)max_M + 2); }
-
-cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M, cudaStream_t st) {
-  const size_t smem = fft_smem(max_M);
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, cudaStream_t st) {
+  const size_t smem = (size_t)smem_bytes;
   cudaError_t e = cudaFuncSetAttribute(fft_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (n_signals > 0) fft_prep_kernel<<<n_signals, kFftThreads, smem, st>>>(P);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M, int32_t ksplit,
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t ksplit,
                         const double2* part, int32_t p_part, cudaStream_t st) {
-  const size_t smem = fft_smem(max_M);
+  const size_t smem = (size_t)smem_bytes;
   cudaError_t e = cudaFuncSetAttribute(pfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;

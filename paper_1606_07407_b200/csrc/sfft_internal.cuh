@@ -16,7 +16,7 @@ namespace sfft {
 enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK, 1 PARTIAL, <0 error)
 
 constexpr int kMaxFftPasses = 24;
-constexpr int kFftThreads = 512;
+constexpr int kFftThreads = 1024;
 constexpr int kDecodeThreads = 512;
 constexpr int kLogIters = 64;
 
@@ -52,6 +52,7 @@ struct DevParams {
   // buffers (device)
   int64_t* v_all;              // [batch][r][kk]
   double2* C_all;              // [batch][kk][Lp]
+  int2* u_all;                 // [batch][kk] (v_{j,m} mod p, 8 v_{j,m} mod p) of the current iteration
   double2* lines;              // [batch][L][p_stride]
   double2* W_tab;              // [batch][p_stride]   e^{+2 pi i q/p}
   double2* chirp;              // [batch][p_stride]   e^{-pi i (q^2 mod 2p)/p}
@@ -106,8 +107,9 @@ int expsum_bk();
 cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
                           int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st);
 // k_fft.cu
-cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t max_M, cudaStream_t st);
-cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t max_M,
+// smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, cudaStream_t st);
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes,
                         int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st);
 cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st);
 // k_wrap.cu
