@@ -300,9 +300,13 @@ int fft_index_host(const sfft_plan_t* P, int p) {
 #define LAUNCH(P, call)                                                                          \
   do {                                                                                           \
     cudaError_t _e = (call);                                                                     \
+    if (_e == cudaSuccess && g_sync_launches) _e = cudaStreamSynchronize((P)->stream);           \
     if (_e != cudaSuccess) return fail((P), SFFT_ECUDA, "%s: %s", #call, cudaGetErrorString(_e)); \
     ++launches;                                                                                  \
   } while (0)
+
+// SFFT_SYNC=1: synchronise after every launch (debugging aid: pins errors to the launching call)
+const bool g_sync_launches = getenv("SFFT_SYNC") != nullptr;
 
 }  // namespace
 
@@ -585,12 +589,13 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     }
     if (P->profile) it_marks.push_back(n_ev);
     mark();
-    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, st));
+    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), st));
     mark();
     LAUNCH(P, launch_expsum(D, P->shape, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
     ++n_expsum;
     mark();
-    LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, ksplit, ptr<double2>(P, B_PART), max_p, st));
+    LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), ksplit,
+                          ptr<double2>(P, B_PART), max_p, st));
     mark();
     LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
     mark();
@@ -711,7 +716,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   rc = set_signal0_state(P, D, (int)p, m, K - P->k);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, P->stream));
+  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->stream));
   LAUNCH(P, launch_expsum(D, P->shape, (int)p, 1, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
                                 cudaMemcpyDeviceToDevice, P->stream));
@@ -732,9 +737,10 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   int launches = 0;
   rc = set_signal0_state(P, D, (int)p, 0, 0);
   if (rc) return rc;
-  const int sm = (int)P->fft[fft_index_host(P, (int)p)].smem_upto;
-  LAUNCH(P, launch_fft_prep(D, 1, sm, P->stream));
-  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, 1, nullptr, 0, P->stream));
+  const int fi = fft_index_host(P, (int)p);
+  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M);
+  LAUNCH(P, launch_fft_prep(D, 1, sm, th, P->stream));
+  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }

@@ -14,6 +14,7 @@
 // buffering.  One complex MAC = 4 DFMA; C values are warp-broadcast LDS.128, roots are
 // random-index LDS.128.
 #include <algorithm>
+#include <cassert>
 #include <cstdio>
 #include <cstdlib>
 
@@ -209,6 +210,9 @@ __device__ __forceinline__ void dmma_chunk(DmmaAcc<MB, NB>& acc, const double2* 
     r += (r >> 31) & pp;
 #pragma unroll
     for (int a = 0; a < MB; ++a) {
+#ifdef SFFT_BOUNDS
+      assert(r >= 0 && r < pp && ud.x >= 0 && ud.x < pp && ud.y >= 0 && ud.y < pp);
+#endif
       f.tw[a] = sW[r];
       r += ud.y;
       r -= (r >= pp) ? pp : 0;
@@ -291,6 +295,7 @@ __device__ __forceinline__ void dmma_group(StageF&& stage, const double2* sW, co
     dmma_chunk<MB, NB, BN>(acc, sW, sC + buf * kBK * BN, sU + buf * kBK, hrow, col0, kl, nl, magic, p);
     __syncthreads();
   }
+  cp_async_wait<0>();
   dmma_store<MB, NB>(acc, out, pstr, L, p, hrow0, col_base + col0, kl, nl);
 }
 
@@ -311,9 +316,15 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
   const int ht = bid % n_htiles;
   const int slot = bid / n_htiles;                              // index into the active-signal list
   const int s = P.active[slot];
+#ifdef SFFT_BOUNDS
+  assert(s >= 0 && s < P.batch);
+#endif
   const int p = P.st_p[s];
   if (ht * BM >= p) return;
   const int K = P.k + P.st_nR[s];
+#ifdef SFFT_BOUNDS
+  assert(p >= 2 && p <= P.p_cap && K >= 0 && K <= P.kk);
+#endif
 
   double2* sW = reinterpret_cast<double2*>(smem_raw);
   const int p_pad = (p + 1) & ~1;
@@ -342,7 +353,8 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
     }
     if (tid < kBK / 2) {                                        // 16-byte copies of two (u, 8u mod p) pairs
       const int j = j0 + 2 * tid;
-      cp_async16(sU + buf * kBK + 2 * tid, ug + j, j < K);
+      const bool ok = j < K;                                     // invalid: zero-fill from a safe address
+      cp_async16(sU + buf * kBK + 2 * tid, ok ? (const void*)(ug + j) : (const void*)ug, ok);
     }
   };
 

@@ -184,21 +184,57 @@ __device__ void load_twiddles(const DevParams& P, int fi, double2* tb) {
   for (int q = threadIdx.x; q < n; q += blockDim.x) tb[q] = src[q];
 }
 
+// Fused middle of the Bluestein convolution: the last DIF pass (S = R, Q = 1: contiguous groups of
+// R, unit twiddles), the pointwise product with the kernel spectrum V and the first DIT pass (the
+// same groups) in registers -- three shared-memory sweeps replaced by one.
+template <int R>
+__device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __restrict__ V) {
+  for (int g = threadIdx.x; g < M / R; g += blockDim.x) {
+    const int base = g * R;
+    double2 v[R], w[R];
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      v[k] = x[base + k];
+      w[k] = __ldg(V + base + k);
+    }
+    dft_small<R, false>(v);
+#pragma unroll
+    for (int k = 0; k < R; ++k) v[k] = cmulx(v[k], w[k]);
+    dft_small<R, true>(v);
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[base + k] = v[k];
+  }
+}
+
+__device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* __restrict__ V) {
+  const int M = P.fft_M[fi];
+  const int R = P.fft_radix[fi * kMaxFftPasses + P.fft_npass[fi] - 1];
+  switch (R) {
+    case 2: mid_loop<2>(x, M, V); break;
+    case 3: mid_loop<3>(x, M, V); break;
+    case 4: mid_loop<4>(x, M, V); break;
+    case 5: mid_loop<5>(x, M, V); break;
+    case 7: mid_loop<7>(x, M, V); break;
+    case 8: mid_loop<8>(x, M, V); break;
+  }
+  __syncthreads();
+}
+
 // forward DIF FFT, natural -> digit-reversed; tb = shared copy of this size's tables
-__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb) {
+__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
   const int npass = P.fft_npass[fi];
   int S = M;
-  for (int ps = 0; ps < npass; ++ps) {
+  for (int ps = 0; ps < npass - skip_last; ++ps) {
     const int R = radix[ps];
     fft_pass<false>(x, M, S, R, tb + (off[ps] - off[0]));
     S /= R;
   }
 }
 // inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
-__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb) {
+__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb, int skip_first = 0) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -207,6 +243,7 @@ __device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* t
   for (int ps = npass - 1; ps >= 0; --ps) {
     const int R = radix[ps];
     S *= R;
+    if (ps == npass - 1 && skip_first) continue;
     fft_pass<true>(x, M, S, R, tb + (off[ps] - off[0]));
   }
 }
@@ -263,6 +300,9 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_prep_kernel(DevParams P) {
       const int u = (int)mod_pos64(vm[j], p);
       ug[j] = make_int2(u, (8 * u) % p);
     }
+    // the exp-sum stages the phases in 16-byte pairs: the partner of the last term must be a valid
+    // index too (its line coefficients are zero-filled, its root index must stay inside the table)
+    if (threadIdx.x == 0 && (K & 1)) ug[K] = make_int2(0, 0);
   }
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* tb = x + M;
@@ -335,41 +375,27 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     }
   }
   __syncthreads();
-  fft_dif(P, x, fi, tb);
-  const double2* V = P.V + (int64_t)s * P.M_stride;
-  for (int q0 = threadIdx.x; q0 < M; q0 += 4 * blockDim.x) {
-    double2 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = q0 + u * blockDim.x;
-      v[u] = q < M ? V[q] : make_double2(0.0, 0.0);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int q = q0 + u * blockDim.x;
-      if (q < M) x[q] = cmulx(x[q], v[u]);
-    }
-  }
-  __syncthreads();
-  fft_dit(P, x, fi, tb);
+  fft_dif(P, x, fi, tb, 1);
+  fft_mid(P, x, fi, P.V + (int64_t)s * P.M_stride);
+  fft_dit(P, x, fi, tb, 1);
   for (int b = threadIdx.x; b < p; b += blockDim.x) line[b] = cmulx(x[b], ch[b]);
 }
 
-cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, cudaStream_t st) {
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, cudaStream_t st) {
   const size_t smem = (size_t)smem_bytes;
   cudaError_t e = cudaFuncSetAttribute(fft_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (n_signals > 0) fft_prep_kernel<<<n_signals, kFftThreads, smem, st>>>(P);
+  if (n_signals > 0) fft_prep_kernel<<<n_signals, threads, smem, st>>>(P);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t ksplit,
-                        const double2* part, int32_t p_part, cudaStream_t st) {
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads,
+                        int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st) {
   const size_t smem = (size_t)smem_bytes;
   cudaError_t e = cudaFuncSetAttribute(pfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;
-  if (grid > 0) pfft_kernel<<<(unsigned)grid, kFftThreads, smem, st>>>(P, n_lines, ksplit, part, p_part);
+  if (grid > 0) pfft_kernel<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part);
   return cudaGetLastError();
 }
 

@@ -108,8 +108,10 @@ cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_
                           int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st);
 // k_fft.cu
 // smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
-cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, cudaStream_t st);
-cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes,
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, cudaStream_t st);
+// threads per FFT CTA for a size (more CTAs per SM for small M)
+inline int fft_threads(int M) { int t = ((M / 6 + 31) / 32) * 32; return t < 128 ? 128 : (t > kFftThreads ? kFftThreads : t); }
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads,
                         int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st);
 cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st);
 // k_wrap.cu

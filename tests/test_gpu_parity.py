@@ -289,3 +289,24 @@ def test_error_codes(S):
     with pytest.raises(S.SfftError) as e:
         S.sfft_plan(2, 64, 4, eps=1.0 / 3.5)
     assert e.value.status == S.SFFT_EINVAL
+
+
+@pytest.mark.parametrize("name,trials", [("c2", range(8)), ("c3", range(2)), ("c5", range(2)), ("c4", range(2))])
+def test_e2e_poisoned_workspace(S, name, trials):
+    """Stale device memory must not leak into results: the plan workspace is filled with 0xFF bytes
+    (NaN doubles, -1 integers) before the first execute (catches reads of unwritten entries)."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, batch=len(trials))
+    plan.workspace.fill_(0xFF)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for i, t in enumerate(trials):
+        key = f"primary_{t}"
+        assert int(res.per_status[i]) == int(g[key + "_status"])
+        n = int(res.count[i])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        ra = g[key + "_a"]
+        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
