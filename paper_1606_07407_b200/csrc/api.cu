@@ -79,6 +79,7 @@ enum Buf {
   B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
+  B_WRAPS,
   B_COUNT
 };
 
@@ -179,6 +180,7 @@ void layout(sfft_plan_t* P) {
   sz[B_TW] = 16 * P->tw_total;
   sz[B_TWSEG] = 16 * P->tw_seg.size();
   sz[B_UALL] = 8 * S * (size_t)P->kk + 256;
+  sz[B_WRAPS] = 4 * S * ((size_t)P->k + 1);
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -602,7 +604,8 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     last_iter = iter;
   }
   int32_t* ostat = out_status ? out_status : ptr<int32_t>(P, B_OUT_S);
-  LAUNCH(P, launch_wrap(D, batch, out_freqs, out_coeffs, out_count, ostat, st));
+  LAUNCH(P, launch_wrap(D, batch, out_freqs, out_coeffs, out_count, ostat, ptr<int32_t>(P, B_WRAPS), st));
+  launches += 2;   // digits, rank, gather
   mark();
   // report
   std::vector<int32_t> hs(batch);

@@ -115,7 +115,8 @@ cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, 
                         int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st);
 cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st);
 // k_wrap.cu
+// scratch: device int32 [n_signals * (k + 1)]
 cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freqs, double* out_coeffs,
-                        int32_t* out_count, int32_t* out_status, cudaStream_t st);
+                        int32_t* out_count, int32_t* out_status, int32_t* scratch, cudaStream_t st);
 
 }  // namespace sfft
