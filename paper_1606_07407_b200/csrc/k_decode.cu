@@ -123,20 +123,21 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   const double2* F = P.lines + (int64_t)s * P.L * P.p_stride;   // line n at F + n * p_stride
   const double floor_abs = P.floor_rel * (double)p;
 
-  // ---- 1. select (ascending b) ----
-  const int chunk = (p + blockDim.x - 1) / blockDim.x;
-  const int b0 = tid * chunk, b1 = min(p, b0 + chunk);
-  int cnt = 0;
-  for (int b = b0; b < b1; ++b) {
-    const double2 f = F[b];
-    cnt += hypot(f.x, f.y) >= floor_abs;
-  }
-  int total;
-  int pos = block_excl_scan(cnt, scratch, &total);
-  for (int b = b0; b < b1; ++b) {
-    const double2 f = F[b];
-    const double mg = hypot(f.x, f.y);
-    if (mg >= floor_abs) { cand[pos] = b; mag[pos] = mg; ++pos; }
+  // ---- 1. select (ascending b): coalesced sweep, ballot + block prefix per 1024-bin round ----
+  int total = 0;
+  for (int b0 = 0; b0 < p; b0 += blockDim.x) {
+    const int b = b0 + tid;
+    double mg = 0.0;
+    bool fl = false;
+    if (b < p) {
+      const double2 f = F[b];
+      mg = hypot(f.x, f.y);
+      fl = mg >= floor_abs;
+    }
+    int round_total;
+    const int pos = block_excl_scan(fl ? 1 : 0, scratch, &round_total);
+    if (fl) { cand[total + pos] = b; mag[total + pos] = mg; }
+    total += round_total;
   }
   __syncthreads();
   int nc = total;
@@ -157,7 +158,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     int nk = 0;
     for (int i = i0; i < i1; ++i) c2 += flag[i];
     int pos2 = block_excl_scan(c2, scratch, &total);
-    // stash own survivors in registers (per <= 14 since p <= 7168 and blockDim = 512)
+    // stash own survivors in registers (per <= 7 since p <= 7168 and blockDim = 1024)
     for (int i = i0; i < i1 && nk < 32; ++i)
       if (flag[i]) keep_b[nk++] = cand[i];
     __syncthreads();
@@ -174,32 +175,45 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     const double2 f0 = F[b];
     const double mag0 = hypot(f0.x, f0.y);
     bool ok = true;
-    for (int n = lane; n < r; n += 32) {
-      const double2 fn = F[(int64_t)(1 + n) * P.p_stride + b];
-      const double rho = hypot(fn.x, fn.y) / mag0;
-      ok = ok && (fabs(rho - 1.0) < P.tol);
+    for (int n0 = 0; n0 < r; n0 += 128) {
+      // up to 4 shifted-line bins per lane, loaded once for both the test and the decode
+      double2 fv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int n = n0 + lane + 32 * i;
+        fv[i] = n < r ? F[(int64_t)(1 + n) * P.p_stride + b] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int n = n0 + lane + 32 * i;
+        if (n < r) {
+          const double rho = hypot(fv[i].x, fv[i].y) / mag0;     // Eq. (42)
+          ok = ok && (fabs(rho - 1.0) < P.tol);
+        }
+      }
+      if (!__all_sync(0xffffffffu, ok)) { ok = false; break; }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int n = n0 + lane + 32 * i;
+        if (n < r) {
+          // q = F_n conj(F_0), written without contraction to mirror the plain formula
+          const double qr = __dadd_rn(__dmul_rn(fv[i].x, f0.x), __dmul_rn(fv[i].y, f0.y));
+          const double qi = __dsub_rn(__dmul_rn(fv[i].y, f0.x), __dmul_rn(fv[i].x, f0.y));
+          const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)P.E), twopi);   // Eq. (41)
+          const double xr = rint(x);
+          bool good = fabs(x - xr) <= P.round_tol;
+          const int64_t v = (int64_t)xr;
+          if (P.extra & 1) good = good && v >= P.lo[n] && v <= P.hi[n];
+          ok = ok && good;
+          accv[(int64_t)n * P.k + ci] = v;
+        }
+      }
+      if (!__all_sync(0xffffffffu, ok)) { ok = false; break; }
     }
-    ok = __all_sync(0xffffffffu, ok);
-    if (ok) {
-      for (int n = lane; n < r; n += 32) {
-        const double2 fn = F[(int64_t)(1 + n) * P.p_stride + b];
-        // q = F_n conj(F_0), written without contraction to mirror the plain formula
-        const double qr = __dadd_rn(__dmul_rn(fn.x, f0.x), __dmul_rn(fn.y, f0.y));
-        const double qi = __dsub_rn(__dmul_rn(fn.y, f0.x), __dmul_rn(fn.x, f0.y));
-        const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)P.E), twopi);
-        const double xr = rint(x);
-        bool good = fabs(x - xr) <= P.round_tol;
-        const int64_t v = (int64_t)xr;
-        if (P.extra & 1) good = good && v >= P.lo[n] && v <= P.hi[n];
-        ok = ok && good;
-        accv[(int64_t)n * P.k + ci] = v;
-      }
-      ok = __all_sync(0xffffffffu, ok);
-      if (ok && (P.extra & 2)) {
-        __syncwarp();
-        const int64_t vm = accv[(int64_t)m * P.k + ci];
-        ok = mod_pos64(vm, p) == b;
-      }
+    if (ok && (P.extra & 2)) {
+      __syncwarp();
+      const int64_t vm = accv[(int64_t)m * P.k + ci];
+      ok = mod_pos64(vm, p) == b;
     }
     if (lane == 0) flag[ci] = ok;
   }

@@ -17,7 +17,7 @@ enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK,
 
 constexpr int kMaxFftPasses = 24;
 constexpr int kFftThreads = 1024;
-constexpr int kDecodeThreads = 512;
+constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
 
 // Everything a kernel needs, passed by value (kernel parameter space).
