@@ -582,9 +582,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     const int max_K = P->h_ctrl[2];
     // term split when the (signal x h-tile x n-tile) grid cannot fill the GPU (late iterations)
     int ksplit = 1;
+    const ExpsumShape shp = expsum_for_p(P->shape, max_p);
     {
-      const int blocks = expsum_blocks(P->shape, max_p, n_active);
-      const int target = 2 * P->n_sm;
+      const int blocks = expsum_blocks(shp, max_p, n_active);
+      const int target = 2 * P->n_sm * std::max(1, 8 / shp.warps);
       const int chunks = (max_K + expsum_bk() - 1) / expsum_bk();
       if (blocks < target) ksplit = std::min({(target + blocks - 1) / blocks, std::max(1, chunks / 2), 32});
       while (ksplit > 1 && (size_t)ksplit * n_active * P->L * (size_t)max_p * 16 > kPartBytes) --ksplit;
@@ -593,7 +594,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     mark();
     LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), st));
     mark();
-    LAUNCH(P, launch_expsum(D, P->shape, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
+    LAUNCH(P, launch_expsum(D, shp, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
     ++n_expsum;
     mark();
     LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), ksplit,
@@ -720,7 +721,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
   LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->stream));
-  LAUNCH(P, launch_expsum(D, P->shape, (int)p, 1, 1, nullptr, 0, P->stream));
+  LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, (int)p), (int)p, 1, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
                                 cudaMemcpyDeviceToDevice, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));

@@ -17,6 +17,7 @@
 #include <cassert>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "sfft_internal.cuh"
 
@@ -456,12 +457,25 @@ static cudaError_t launch_nb(const DevParams& P, const ExpsumShape& S, int32_t m
                              const Split& sp, cudaStream_t st) {
   // mb 1: 16 warps x (8 rows); mb 2: 8 warps x (16 rows); mb 3: 16 warps in two column groups x (16 rows)
   if (S.mb == 1) return launch_grid(expsum_dmma_kernel<1, NB, 0, 16>, S, max_p, n_signals, sp, st, P);
+  if (S.mb == 4) return launch_grid(expsum_dmma_kernel<1, NB, 0, 4>, S, max_p, n_signals, sp, st, P);   // 32 rows
+  if (S.mb == 5) return launch_grid(expsum_dmma_kernel<2, NB, 0, 4>, S, max_p, n_signals, sp, st, P);   // 64 rows
   if (S.mb == 3 && NB >= 2)
     return launch_grid(expsum_dmma_kernel<2, (NB + 1) / 2, NB / 2, 16>, S, max_p, n_signals, sp, st, P);
   return launch_grid(expsum_dmma_kernel<2, NB, 0, 8>, S, max_p, n_signals, sp, st, P);
 }
 
 int expsum_bk() { return kBK; }
+
+// Row tile for the iteration's largest prime: late iterations have p of a few tens to a few hundred,
+// where 128-row CTAs would leave most rows idle.
+ExpsumShape expsum_for_p(const ExpsumShape& S, int32_t max_p) {
+  const char* ov = getenv("SFFT_EXPSUM");
+  if (S.kind != 1 || S.mb != 2 || (ov && (!strncmp(ov, "dmma", 4) || !strncmp(ov, "dfma", 4)))) return S;
+  ExpsumShape r = S;
+  if (max_p <= 48) { r.mb = 4; r.warps = 4; r.bm = 32; }
+  else if (max_p <= 320) { r.mb = 5; r.warps = 4; r.bm = 64; }
+  return r;
+}
 
 int expsum_blocks(const ExpsumShape& S, int32_t max_p, int32_t n_signals) {
   return n_signals * ((max_p + S.bm - 1) / S.bm) * S.nt;

@@ -101,6 +101,7 @@ size_t decode_smem_bytes(const DevParams& P, int32_t max_p);
 struct ExpsumShape { int kind, tn, wn, th, warps, bm, bn, nt, mb, nb; double est; };
 ExpsumShape choose_expsum_shape(int L);
 int expsum_blocks(const ExpsumShape& S, int32_t max_p, int32_t n_signals);
+ExpsumShape expsum_for_p(const ExpsumShape& S, int32_t max_p);
 int expsum_bk();
 // ksplit > 1: terms split over ksplit CTAs; partial lines go to part[ks][slot][L][p_part] and are summed
 // in fixed ks order by the FFT load (deterministic, no atomics)
