@@ -35,7 +35,7 @@ struct FftSize {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-constexpr size_t kPartBytes = (size_t)128 << 20;   // exp-sum partial lines of term-split iterations
+constexpr size_t kPartBytes = (size_t)512 << 20;   // exp-sum partial lines of term-split iterations
 
 }  // namespace
 
@@ -584,11 +584,19 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     int ksplit = 1;
     const ExpsumShape shp = expsum_for_p(P->shape, max_p);
     {
+      // wave quantisation model: time ~ ceil(B ks / W) / ks, W = resident CTAs; a split costs ~3 %
+      // (partial lines written and re-read by the FFT)
       const int blocks = expsum_blocks(shp, max_p, n_active);
-      const int target = 2 * P->n_sm * std::max(1, 8 / shp.warps);
+      const int W = P->n_sm * expsum_occupancy(shp, max_p);
       const int chunks = (max_K + expsum_bk() - 1) / expsum_bk();
-      if (blocks < target) ksplit = std::min({(target + blocks - 1) / blocks, std::max(1, chunks / 2), 32});
-      while (ksplit > 1 && (size_t)ksplit * n_active * P->L * (size_t)max_p * 16 > kPartBytes) --ksplit;
+      const int ks_max = std::min(32, std::max(1, chunks / 2));
+      double best = 1e30;
+      for (int ks = 1; ks <= ks_max; ++ks) {
+        if (ks > 1 && (size_t)ks * n_active * P->L * (size_t)max_p * 16 > kPartBytes) break;
+        const double waves = std::ceil((double)blocks * ks / W);
+        const double t = waves / ks * (ks > 1 ? 1.03 : 1.0);
+        if (t < best - 1e-9) { best = t; ksplit = ks; }
+      }
     }
     if (P->profile) it_marks.push_back(n_ev);
     mark();

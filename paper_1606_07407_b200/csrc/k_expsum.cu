@@ -431,7 +431,7 @@ static size_t expsum_smem(int max_p, int bn) {
   return sizeof(double2) * (size_t)(((max_p + 1) & ~1) + 2 * kBK * bn) + sizeof(int) * 4 * kBK;
 }
 
-struct Split { int ksplit; double2* part; int p_part; };
+struct Split { int ksplit; double2* part; int p_part; int* occ_out; };   // occ_out: query only, no launch
 
 template <typename KernT, typename... Args>
 static cudaError_t launch_grid(KernT kern, const ExpsumShape& S, int32_t max_p, int32_t n_signals, const Split& sp,
@@ -439,6 +439,7 @@ static cudaError_t launch_grid(KernT kern, const ExpsumShape& S, int32_t max_p, 
   const size_t smem = expsum_smem(max_p, S.bn);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (sp.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(sp.occ_out, kern, S.warps * 32, smem);
   const int n_htiles = (max_p + S.bm - 1) / S.bm;
   const long grid = (long)n_signals * n_htiles * S.nt * sp.ksplit;
   if (grid <= 0) return cudaSuccess;
@@ -481,9 +482,17 @@ int expsum_blocks(const ExpsumShape& S, int32_t max_p, int32_t n_signals) {
   return n_signals * ((max_p + S.bm - 1) / S.bm) * S.nt;
 }
 
+int expsum_occupancy(const ExpsumShape& S, int32_t max_p) {
+  int occ = 1;
+  DevParams P;
+  memset(&P, 0, sizeof P);
+  if (launch_expsum(P, S, max_p, 1, 1, nullptr, 0, nullptr, &occ) != cudaSuccess) return 1;
+  return occ > 0 ? occ : 1;
+}
+
 cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
-                          int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st) {
-  const Split sp{ksplit, part, p_part};
+                          int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st, int* occ_out) {
+  const Split sp{ksplit, part, p_part, occ_out};
   if (S.kind == 1) {
     switch (S.nb) {
       case 1: return launch_nb<1>(P, S, max_p, n_signals, sp, st);

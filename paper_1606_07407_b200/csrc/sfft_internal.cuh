@@ -106,7 +106,8 @@ int expsum_bk();
 // ksplit > 1: terms split over ksplit CTAs; partial lines go to part[ks][slot][L][p_part] and are summed
 // in fixed ks order by the FFT load (deterministic, no atomics)
 cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
-                          int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st);
+                          int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st, int* occ_out = nullptr);
+int expsum_occupancy(const ExpsumShape& S, int32_t max_p);   // resident CTAs per SM
 // k_fft.cu
 // smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, cudaStream_t st);
