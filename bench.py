@@ -156,9 +156,10 @@ def main():
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_1606_07407_b200.shard import shard_indices
     cfg = W.CONFIGS[args.config]
     T = args.batch or cfg.trials
-    trials = list(range(rank * T, rank * T + T))       # each rank: its own shard of independent signals
+    trials = shard_indices(world * T, world, rank)     # each rank: its own shard of independent signals
     w_np, a_np = W.make_batch(cfg, trials)
     w_h = torch.from_numpy(w_np).pin_memory()
     a_h = torch.from_numpy(a_np).pin_memory()
@@ -249,6 +250,10 @@ def main():
     d2h = hout[0].numel() * 4 + hout[1].numel() * 8 + hout[2].numel() * 4 + hout[3].numel() * 4
     if args.e2e_steps:
         ok = ok and np.array_equal(hout[0].numpy(), ws)
+    ok_t = torch.tensor([1 if ok else 0], dtype=torch.int32, device="cuda")
+    if world > 1:
+        dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
+    ok = bool(ok_t.item())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

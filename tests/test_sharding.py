@@ -1,0 +1,71 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the signal-sharding host logic:
+contiguous shards, and the gather of per-rank results back to rank 0 in global trial order.
+The per-rank work is stood in for by a deterministic function of the trial index (no GPU here)."""
+import os
+import socket
+
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1606_07407_b200.shard import gather_to_rank0, shard_indices, shard_range
+
+
+def test_shard_range_partitions():
+    for n in (0, 1, 7, 100, 1024, 1025):
+        for world in (1, 2, 3, 8):
+            seen = []
+            for r in range(world):
+                lo, hi = shard_range(n, world, r)
+                assert 0 <= hi - lo <= -(-n // world)
+                seen += list(range(lo, hi))
+            assert seen == list(range(n))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fake_solve(trials, k, d):
+    """Stand-in for a rank's solves: outputs are a pure function of the trial index."""
+    t = torch.tensor(trials, dtype=torch.int64)
+    freqs = (t[:, None, None] * 1000 + torch.arange(k)[None, :, None] * 10 + torch.arange(d)[None, None, :]).to(torch.int32)
+    coeffs = torch.stack([t.double() + 0.5, -t.double()], -1)[:, None, :].expand(len(trials), k, 2).contiguous()
+    count = torch.full((len(trials),), k, dtype=torch.int32)
+    return freqs, coeffs, count
+
+
+def _worker(rank, world, port, n, k, d, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = shard_indices(n, world, rank)
+        outs = _fake_solve(mine, k, d)
+        got = gather_to_rank0(list(outs), n, world, rank)
+        if rank == 0:
+            ref = _fake_solve(list(range(n)), k, d)
+            ok = all(torch.equal(a, b) for a, b in zip(got, ref))
+            q.put(ok)
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [10, 7])
+def test_gather_world2_gloo(n):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, n, 3, 4, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=10) is True
