@@ -108,26 +108,30 @@ bool is_7smooth(int x) {
 }
 
 FftSize radix_plan(int M) {
+  // fewest passes with in-register radices {16,15,14,12,10,9,8,7,6,5,4,3,2} (DP over 2^a 3^b 5^c 7^d),
+  // then descending order: the first (largest-Q) pass gets the largest radix -> fewest base twiddles
+  // small sizes keep radices <= 8: with few butterflies per pass, wide radices idle most threads
+  static const int kRad[] = {16, 15, 14, 12, 10, 9, 8, 7, 6, 5, 4, 3, 2};
+  const int rmax = M >= kFftBigM ? 16 : 8;
   FftSize s;
   s.M = M;
-  int e[8] = {0};
-  int x = M;
-  for (int f : {2, 3, 5, 7})
-    while (x % f == 0) { x /= f; ++e[f]; }
-  // descending radices: the first (largest-Q) pass gets the largest radix -> fewest base twiddles
-  while (e[2] >= 3) { s.radix.push_back(8); e[2] -= 3; }
-  for (int i = 0; i < e[7]; ++i) s.radix.push_back(7);
-  for (int i = 0; i < e[5]; ++i) s.radix.push_back(5);
-  if (e[2] == 2) s.radix.push_back(4);
-  for (int i = 0; i < e[3]; ++i) s.radix.push_back(3);
-  if (e[2] == 1) s.radix.push_back(2);
+  std::vector<int> best(M + 1, 1 << 20), choice(M + 1, 0);
+  best[1] = 0;
+  for (int x = 2; x <= M; ++x) {
+    if (M % x) continue;
+    for (int R : kRad)
+      if (R <= rmax && x % R == 0 && best[x / R] + 1 < best[x]) { best[x] = best[x / R] + 1; choice[x] = R; }
+  }
+  std::vector<int> rs;
+  for (int x = M; x > 1; x /= choice[x]) rs.push_back(choice[x]);
+  std::sort(rs.begin(), rs.end(), [](int a, int b) { return a > b; });
+  for (int R : rs) s.radix.push_back((int8_t)R);
   size_t sumq = 0;
   int S = M;
   for (int8_t R : s.radix) { sumq += S / R; S /= R; }
   s.smem = 16 * ((size_t)M + sumq + 2);
   return s;
 }
-
 
 int64_t gcd64(int64_t a, int64_t b) {
   a = a < 0 ? -a : a;
@@ -600,12 +604,13 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     }
     if (P->profile) it_marks.push_back(n_ev);
     mark();
-    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), st));
+    const int big = max_M >= kFftBigM;
+    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, st));
     mark();
     LAUNCH(P, launch_expsum(D, shp, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
     ++n_expsum;
     mark();
-    LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), ksplit,
+    LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, ksplit,
                           ptr<double2>(P, B_PART), max_p, st));
     mark();
     LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
@@ -728,7 +733,8 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   rc = set_signal0_state(P, D, (int)p, m, K - P->k);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->stream));
+  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->fft[fi].M >= kFftBigM,
+                            P->stream));
   LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, (int)p), (int)p, 1, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
                                 cudaMemcpyDeviceToDevice, P->stream));
@@ -750,9 +756,9 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   rc = set_signal0_state(P, D, (int)p, 0, 0);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M);
-  LAUNCH(P, launch_fft_prep(D, 1, sm, th, P->stream));
-  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, 1, nullptr, 0, P->stream));
+  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M), big = P->fft[fi].M >= kFftBigM;
+  LAUNCH(P, launch_fft_prep(D, 1, sm, th, big, P->stream));
+  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, big, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }

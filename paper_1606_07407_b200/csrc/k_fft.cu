@@ -12,6 +12,7 @@
 // is produced by the same routine, so the pointwise product happens in digit-reversed order and
 // the in-place decimation-in-time inverse returns natural order: no permutation pass.
 // Twiddles e^{-2 pi i q/M} = T_hi[q >> 7] * T_lo[q & 127], two small tables in shared memory.
+#include "fft_consts.cuh"
 #include "sfft_internal.cuh"
 
 namespace sfft {
@@ -80,8 +81,8 @@ __device__ __forceinline__ void dft_small(double2 (&x)[R]) {
       x[2 * k] = a[k];
       x[2 * k + 1] = b[k];
     }
-  } else {
-    // odd R: pair n with R-n
+  } else if constexpr (R == 3 || R == 5 || R == 7) {
+    // odd prime R: pair n with R-n
     const double* C = (R == 3) ? kCos3 : (R == 5) ? kCos5 : kCos7;
     const double* S = (R == 3) ? kSin3 : (R == 5) ? kSin5 : kSin7;
     constexpr int H = (R - 1) / 2;
@@ -111,6 +112,44 @@ __device__ __forceinline__ void dft_small(double2 (&x)[R]) {
     }
 #pragma unroll
     for (int k = 0; k < R; ++k) x[k] = out[k];
+  } else {
+    // composite R = A B (in registers): n = B n1 + n2, k = k1 + A k2
+    //   t[n2][k1] = DFT_A over n1 of x[B n1 + n2], times w_R^(n2 k1); y[k1 + A k2] = DFT_B over n2
+    constexpr int A = (R == 16) ? 4 : (R == 12) ? 4 : (R == 9) ? 3 : (R == 15) ? 3 : (R == 6) ? 3 : (R == 10) ? 5 : 7;
+    constexpr int B = R / A;
+    const double* C = (R == 6) ? kCos6 : (R == 9) ? kCos9 : (R == 10) ? kCos10 : (R == 12) ? kCos12
+                    : (R == 14) ? kCos14 : (R == 15) ? kCos15 : kCos16;
+    const double* S = (R == 6) ? kSin6 : (R == 9) ? kSin9 : (R == 10) ? kSin10 : (R == 12) ? kSin12
+                    : (R == 14) ? kSin14 : (R == 15) ? kSin15 : kSin16;
+#pragma unroll
+    for (int n2 = 0; n2 < B; ++n2) {
+      double2 u[A];
+#pragma unroll
+      for (int n1 = 0; n1 < A; ++n1) u[n1] = x[B * n1 + n2];
+      dft_small<A, INV>(u);
+#pragma unroll
+      for (int k1 = 0; k1 < A; ++k1) {
+        const int q = (n2 * k1) % R;
+        double2 t = u[k1];
+        if (q != 0) {
+          const double c = C[q], s = INV ? S[q] : -S[q];      // e^{-+ 2 pi i q / R}
+          t = make_double2(t.x * c - t.y * s, t.x * s + t.y * c);
+        }
+        x[B * k1 + n2] = t;
+      }
+    }
+    double2 y[R];
+#pragma unroll
+    for (int k1 = 0; k1 < A; ++k1) {
+      double2 w[B];
+#pragma unroll
+      for (int n2 = 0; n2 < B; ++n2) w[n2] = x[B * k1 + n2];
+      dft_small<B, INV>(w);
+#pragma unroll
+      for (int k2 = 0; k2 < B; ++k2) y[k1 + A * k2] = w[k2];
+    }
+#pragma unroll
+    for (int k = 0; k < R; ++k) x[k] = y[k];
   }
 }
 
@@ -162,13 +201,25 @@ __device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double
   }
 }
 
-template <bool INV>
+template <bool INV, bool BIG>
 __device__ void fft_pass(double2* x, int M, int S, int R, const double2* tb) {
+  if constexpr (BIG) {
+    switch (R) {
+      case 6: pass_loop<6, INV>(x, M, S, tb); __syncthreads(); return;
+      case 9: pass_loop<9, INV>(x, M, S, tb); __syncthreads(); return;
+      case 10: pass_loop<10, INV>(x, M, S, tb); __syncthreads(); return;
+      case 12: pass_loop<12, INV>(x, M, S, tb); __syncthreads(); return;
+      case 14: pass_loop<14, INV>(x, M, S, tb); __syncthreads(); return;
+      case 15: pass_loop<15, INV>(x, M, S, tb); __syncthreads(); return;
+      case 16: pass_loop<16, INV>(x, M, S, tb); __syncthreads(); return;
+    }
+  }
   switch (R) {
     case 2: pass_loop<2, INV>(x, M, S, tb); break;
     case 3: pass_loop<3, INV>(x, M, S, tb); break;
     case 4: pass_loop<4, INV>(x, M, S, tb); break;
     case 5: pass_loop<5, INV>(x, M, S, tb); break;
+    case 6: pass_loop<6, INV>(x, M, S, tb); break;
     case 7: pass_loop<7, INV>(x, M, S, tb); break;
     case 8: pass_loop<8, INV>(x, M, S, tb); break;
   }
@@ -206,6 +257,7 @@ __device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __res
   }
 }
 
+template <bool BIG>
 __device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* __restrict__ V) {
   const int M = P.fft_M[fi];
   const int R = P.fft_radix[fi * kMaxFftPasses + P.fft_npass[fi] - 1];
@@ -214,13 +266,25 @@ __device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* _
     case 3: mid_loop<3>(x, M, V); break;
     case 4: mid_loop<4>(x, M, V); break;
     case 5: mid_loop<5>(x, M, V); break;
+    case 6: mid_loop<6>(x, M, V); break;
     case 7: mid_loop<7>(x, M, V); break;
     case 8: mid_loop<8>(x, M, V); break;
+  }
+  if constexpr (BIG) {
+    switch (R) {
+      case 9: mid_loop<9>(x, M, V); break;
+      case 10: mid_loop<10>(x, M, V); break;
+      case 12: mid_loop<12>(x, M, V); break;
+      case 14: mid_loop<14>(x, M, V); break;
+      case 15: mid_loop<15>(x, M, V); break;
+      case 16: mid_loop<16>(x, M, V); break;
+    }
   }
   __syncthreads();
 }
 
 // forward DIF FFT, natural -> digit-reversed; tb = shared copy of this size's tables
+template <bool BIG>
 __device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
@@ -229,11 +293,12 @@ __device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* t
   int S = M;
   for (int ps = 0; ps < npass - skip_last; ++ps) {
     const int R = radix[ps];
-    fft_pass<false>(x, M, S, R, tb + (off[ps] - off[0]));
+    fft_pass<false, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
     S /= R;
   }
 }
 // inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
+template <bool BIG>
 __device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb, int skip_first = 0) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
@@ -244,7 +309,7 @@ __device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* t
     const int R = radix[ps];
     S *= R;
     if (ps == npass - 1 && skip_first) continue;
-    fft_pass<true>(x, M, S, R, tb + (off[ps] - off[0]));
+    fft_pass<true, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
   }
 }
 
@@ -283,7 +348,10 @@ __device__ __forceinline__ double2 chirp_value(int64_t q, int64_t p) {
 }
 
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
-__global__ void __launch_bounds__(kFftThreads, 1) fft_prep_kernel(DevParams P) {
+// BIG: sizes >= 4096 whose plans use in-register radices up to 16 (512 threads, 128 registers);
+// small sizes use radices <= 8 with 64 registers so that several CTAs share an SM.
+template <bool BIG>
+__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(DevParams P) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = P.active[blockIdx.x];
   const int p = P.st_p[s];
@@ -322,14 +390,15 @@ __global__ void __launch_bounds__(kFftThreads, 1) fft_prep_kernel(DevParams P) {
     if (q > 0) x[M - q] = vq;
   }
   __syncthreads();
-  fft_dif(P, x, fi, tb);
+  fft_dif<BIG>(P, x, fi, tb);
   const double inv = 1.0 / (double)M;
   double2* V = P.V + (int64_t)s * P.M_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
 }
 
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
-__global__ void __launch_bounds__(kFftThreads, 1)
+template <bool BIG>
+__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4)
 pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int slot = blockIdx.x / n_lines, n = blockIdx.x % n_lines;
@@ -375,27 +444,30 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     }
   }
   __syncthreads();
-  fft_dif(P, x, fi, tb, 1);
-  fft_mid(P, x, fi, P.V + (int64_t)s * P.M_stride);
-  fft_dit(P, x, fi, tb, 1);
+  fft_dif<BIG>(P, x, fi, tb, 1);
+  fft_mid<BIG>(P, x, fi, P.V + (int64_t)s * P.M_stride);
+  fft_dit<BIG>(P, x, fi, tb, 1);
   for (int b = threadIdx.x; b < p; b += blockDim.x) line[b] = cmulx(x[b], ch[b]);
 }
 
-cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, cudaStream_t st) {
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
+                            cudaStream_t st) {
   const size_t smem = (size_t)smem_bytes;
-  cudaError_t e = cudaFuncSetAttribute(fft_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = big ? fft_prep_kernel<true> : fft_prep_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (n_signals > 0) fft_prep_kernel<<<n_signals, threads, smem, st>>>(P);
+  if (n_signals > 0) kern<<<n_signals, threads, smem, st>>>(P);
   return cudaGetLastError();
 }
 
 cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads,
-                        int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st) {
+                        int32_t big, int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st) {
   const size_t smem = (size_t)smem_bytes;
-  cudaError_t e = cudaFuncSetAttribute(pfft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = big ? pfft_kernel<true> : pfft_kernel<false>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;
-  if (grid > 0) pfft_kernel<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part);
+  if (grid > 0) kern<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part);
   return cudaGetLastError();
 }
 

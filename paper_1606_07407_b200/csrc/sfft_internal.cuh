@@ -16,7 +16,7 @@ namespace sfft {
 enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK, 1 PARTIAL, <0 error)
 
 constexpr int kMaxFftPasses = 24;
-constexpr int kFftThreads = 1024;
+constexpr int kFftThreads = 512;
 constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
 
@@ -110,10 +110,16 @@ cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_
 int expsum_occupancy(const ExpsumShape& S, int32_t max_p);   // resident CTAs per SM
 // k_fft.cu
 // smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
-cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, cudaStream_t st);
+cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
+                            cudaStream_t st);
 // threads per FFT CTA for a size (more CTAs per SM for small M)
-inline int fft_threads(int M) { int t = ((M / 6 + 31) / 32) * 32; return t < 128 ? 128 : (t > kFftThreads ? kFftThreads : t); }
-cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads,
+constexpr int kFftBigM = 4096;   // sizes >= this use radices up to 16 and the 512-thread variant
+inline int fft_threads(int M) {
+  const int cap = M >= kFftBigM ? 512 : 256;
+  int t = ((M / 6 + 31) / 32) * 32;
+  return t < 64 ? 64 : (t > cap ? cap : t);
+}
+cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads, int32_t big,
                         int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st);
 cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st);
 // k_wrap.cu
