@@ -64,6 +64,9 @@ typedef struct {
   int32_t extra_checks;       /* bit0 range check, bit1 bin consistency [3] */
   void* stream;               /* cudaStream_t [legacy default stream] */
   int32_t profile;            /* 1: time every kernel class with CUDA events on the stream [0] */
+  int32_t literal_residual;   /* 1: sample g (registry) on every line like f, K = k + |R| terms (Alg. 2 l.13-14
+                                 verbatim); 0: sample f only and subtract g's bins p*sum c_e directly (Eq. (3)),
+                                 same result up to rounding, O(|R| L) instead of O(p |R| L) [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */

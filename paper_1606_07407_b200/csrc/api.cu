@@ -68,6 +68,7 @@ struct sfft_plan_s {
   size_t off[64] = {0};
   int32_t* h_ctrl = nullptr;   // pinned
   bool profile = false;
+  int32_t literal = 0;
   std::vector<cudaEvent_t> events;
   std::string err;
 };
@@ -206,6 +207,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.N = P->N; D.E = P->E;
   D.c = P->c; D.max_iter = P->max_iter; D.stall_limit = P->stall_limit; D.extra = P->extra;
   D.n_sched = (int32_t)P->sched.size();
+  D.literal = P->literal;
   D.tol = P->tol; D.floor_rel = P->floor_rel; D.prune = P->prune; D.round_tol = P->round_tol;
   D.n_tilts = (int32_t)(P->tilts.size() / 5);
   D.p_cap = P->p_cap;
@@ -359,6 +361,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     if (opt->extra_checks >= 0) P->extra = opt->extra_checks & 3;
     P->stream = (cudaStream_t)opt->stream;
     P->profile = opt->profile != 0;
+    P->literal = opt->literal_residual != 0;
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -725,6 +728,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   if (rc) return rc;
   sfft_plan_t* P = plan;
   DevParams D = dev_params(P, 1);
+  D.literal = 1;                 // the stage sums exactly the K given terms
   int launches = 0;
   if (K > 0)
     CUDA_TRY(P, cudaMemcpy2DAsync(D.v_all, 8 * (size_t)P->kk, v, 8 * (size_t)K, 8 * (size_t)K, P->r,

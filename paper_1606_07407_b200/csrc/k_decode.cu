@@ -44,7 +44,7 @@ __global__ void setup_kernel(DevParams P, int32_t iter) {
   P.st_m[s] = iter % P.r;
   P.active[atomicAdd(&P.ctrl[0], 1)] = s;
   atomicMax(&P.ctrl[1], p);
-  atomicMax(&P.ctrl[2], P.k + nR);
+  atomicMax(&P.ctrl[2], P.k + (P.literal ? nR : 0));        // terms the exp-sum sums
 }
 
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st) {
@@ -120,8 +120,81 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   int* found = accl + P.k;
   int* scratch = found + P.k;
 
-  const double2* F = P.lines + (int64_t)s * P.L * P.p_stride;   // line n at F + n * p_stride
+  double2* Fw = P.lines + (int64_t)s * P.L * P.p_stride;        // line n at F + n * p_stride
+  const double2* F = Fw;
   const double floor_abs = P.floor_rel * (double)p;
+
+  // ---- 0. bin-domain residual (literal == 0): the lines hold DFT_p(f) only; add the registry's
+  //      bins p * sum_{e: v_{e,m} = b mod p} C_reg[e][n] (Eq. (3) applied to g, which is synthesised
+  //      from R, not sampled: reading R18).  Entries of a bin are summed in ascending e (stable
+  //      counting sort), so the result is deterministic.
+  if (!STAGE && !P.literal && nR > 0) {
+    int* cnt = cand;                                   // [p] entries per bin
+    int* pos = flag;                                   // [p] running end of each bin
+    int* order = accl;                                 // [nR] entries sorted by bin
+    const int2* ug = P.u_all + (int64_t)s * P.kk + P.k;
+    for (int b = tid; b < p; b += blockDim.x) cnt[b] = 0;
+    __syncthreads();
+    for (int e = tid; e < nR; e += blockDim.x) atomicAdd(&cnt[ug[e].x], 1);
+    __syncthreads();
+    {
+      const int per = (p + blockDim.x - 1) / blockDim.x;
+      const int b0 = tid * per, b1 = min(p, b0 + per);
+      int c0 = 0;
+      for (int b = b0; b < b1; ++b) c0 += cnt[b];
+      int tot;
+      int run = block_excl_scan(c0, scratch, &tot);
+      for (int b = b0; b < b1; ++b) { pos[b] = run; run += cnt[b]; }
+      __syncthreads();
+    }
+    if (warp == 0) {                                   // stable placement, 32 entries at a time
+      for (int e0 = 0; e0 < nR; e0 += 32) {
+        const int e = e0 + lane;
+        const int b = e < nR ? ug[e].x : -1 - lane;
+        const unsigned peers = __match_any_sync(0xffffffffu, b);
+        const int rank = __popc(peers & ((1u << lane) - 1u));
+        int base = 0;
+        if (e < nR) base = pos[b];
+        __syncwarp();
+        if (e < nR) {
+          order[base + rank] = e;
+          if (rank == __popc(peers) - 1) pos[b] = base + rank + 1;
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    const double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+    const double pd = (double)p;
+    // one warp per (bin, 32-line chunk): lanes along the lines -> coalesced reads of the C rows
+    const int nchunk = (P.L + 31) >> 5;
+    for (int task = warp; task < p * nchunk; task += nwarps) {
+      const int b = task / nchunk, n = (task - b * nchunk) * 32 + lane;
+      const int c = cnt[b];
+      if (!c) continue;
+      const int end = pos[b];
+      double2 acc = make_double2(0.0, 0.0);
+      if (n < P.L) {
+        int q = end - c;
+        for (; q + 4 <= end; q += 4) {
+          double2 v[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) v[u] = Creg[(int64_t)order[q + u] * P.Lp + n];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; }
+        }
+        for (; q < end; ++q) {
+          const double2 v = Creg[(int64_t)order[q] * P.Lp + n];
+          acc.x += v.x;
+          acc.y += v.y;
+        }
+        double2* Fn = Fw + (int64_t)n * P.p_stride;
+        const double2 f = Fn[b];
+        Fn[b] = make_double2(f.x + pd * acc.x, f.y + pd * acc.y);
+      }
+    }
+    __syncthreads();
+  }
 
   // ---- 1. select (ascending b): coalesced sweep, ballot + block prefix per 1024-bin round ----
   int total = 0;
@@ -360,7 +433,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
 
   // ---- 5. state ----
   if (tid == 0) {
-    const int K = P.k + nR;
+    const int K = P.k + (P.literal ? nR : 0);
     P.st_nR[s] = nR_final;
     const int stall = na == 0 ? P.st_stall[s] + 1 : 0;
     P.st_stall[s] = stall;

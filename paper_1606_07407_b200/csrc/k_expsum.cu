@@ -56,7 +56,7 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles,
   const int s = P.active[slot];
   const int p = P.st_p[s];
   if (ht * BM >= p) return;
-  const int K = P.k + P.st_nR[s];
+  const int K = P.k + (P.literal ? P.st_nR[s] : 0);      // bin-domain g: signal terms only
 
   double2* sW = reinterpret_cast<double2*>(smem_raw);
   const int p_pad = (p + 1) & ~1;
@@ -322,7 +322,7 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
 #endif
   const int p = P.st_p[s];
   if (ht * BM >= p) return;
-  const int K = P.k + P.st_nR[s];
+  const int K = P.k + (P.literal ? P.st_nR[s] : 0);      // bin-domain g: signal terms only
 #ifdef SFFT_BOUNDS
   assert(p >= 2 && p <= P.p_cap && K >= 0 && K <= P.kk);
 #endif

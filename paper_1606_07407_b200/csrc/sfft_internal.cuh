@@ -29,6 +29,7 @@ struct DevParams {
   int32_t batch;
   int64_t N, E;
   int32_t c, max_iter, stall_limit, extra, n_sched;
+  int32_t literal;             // 1: registry terms sampled with the signal (K = k + |R|); 0: bin-domain g
   double tol, floor_rel, prune, round_tol;
   int32_t n_tilts;
   int32_t p_cap;               // largest prime the FFT size table supports

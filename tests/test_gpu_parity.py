@@ -310,3 +310,28 @@ def test_e2e_poisoned_workspace(S, name, trials):
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ra = g[key + "_a"]
         assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+
+
+@pytest.mark.parametrize("name,trials", [("c2", range(8)), ("c3", range(2)), ("c5", range(2))])
+def test_e2e_literal_residual_mode(S, name, trials):
+    """literal_residual=1 samples g on every line exactly as Alg. 2 l.13-14 (K = k + |R|); the default
+    bin-domain subtraction must give the same frequency sets and coefficients (to rounding)."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    res = {}
+    for lit in (True, False):
+        plan = _plan(S, c, batch=len(trials), literal_residual=lit)
+        r = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+        res[lit] = (r.freqs.cpu().numpy().copy(), r.coeffs.cpu().numpy().copy(), r.count.cpu().numpy().copy(),
+                    [r.report.primes[i] for i in range(8)], [r.report.accepted[i] for i in range(8)])
+        for i, t in enumerate(trials):
+            key = f"primary_{t}"
+            n = int(r.count[i])
+            gw = np.ascontiguousarray(r.freqs[i, :n].cpu().numpy())
+            assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), (key, lit)
+            ra = g[key + "_a"]
+            assert np.abs(r.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), (key, lit)
+    assert np.array_equal(res[True][0], res[False][0]) and res[True][3:] == res[False][3:]
+    assert np.abs(res[True][1] - res[False][1]).max() <= 1e-12 * np.abs(res[True][1]).max()
