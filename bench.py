@@ -275,9 +275,10 @@ def main():
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
             "sample_evals_per_s": world * samples / (ms_max / 1e3),
             "verified_exact_recovery": ok,
-            "roofline": {"bound": "alu", "kernel": "expsum (FP64 DFMA)", "achieved": achieved,
+            "roofline": {"bound": "alu", "kernel": "expsum (FP64 tensor pipe: mma.sync f64 / DMMA)", "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                          "traffic": traffic,
+                         "traffic_note": "DRAM bytes of the iteration-1 launch (ncu --set full, profiles/expsum_ncu.json)",
                          "peak_source": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz; measured DMMA 37.1, DFMA 33.6 "
                                         "(profiles/r01_fp64_peak.log); MEASURED_PEAKS.json has no FP64 entry",
                          "algorithmic_flops_per_launch": 8.0 * cmacs / max(n_exp, 1),
