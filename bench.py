@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--expsum-path", type=int, default=0, choices=[0, 1, 2],
+                    help="0 auto (int8 limbs on tcgen05 when available), 1 FP64 tensor/vector, 2 int8 limbs")
     return ap.parse_args()
 
 
@@ -165,7 +167,8 @@ def main():
     a_h = torch.from_numpy(a_np).pin_memory()
     w_d, a_d = w_h.cuda(), a_h.cuda()
     stream = torch.cuda.current_stream()
-    plan = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, profile=True)
+    plan = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, profile=True,
+                        expsum_path=args.expsum_path)
     sig = S.sfft_signal_expsum(plan, w_d, a_d)
     outs = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32, device="cuda"),
             torch.empty((T, cfg.k, 2), dtype=torch.float64, device="cuda"),

@@ -67,6 +67,9 @@ typedef struct {
   int32_t literal_residual;   /* 1: sample g (registry) on every line like f, K = k + |R| terms (Alg. 2 l.13-14
                                  verbatim); 0: sample f only and subtract g's bins p*sum c_e directly (Eq. (3)),
                                  same result up to rounding, O(|R| L) instead of O(p |R| L) [0] */
+  int32_t expsum_path;        /* exp-sum arithmetic: 0 auto, 1 FP64 (DMMA / DFMA), 2 exact int8-limb products on
+                                 the tcgen05 tensor cores combined in FP64 (needs
+                                 literal_residual = 0 and E <= 2^36) [0: int8 limbs when available] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */

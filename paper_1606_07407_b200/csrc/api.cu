@@ -60,6 +60,10 @@ struct sfft_plan_s {
   std::vector<int4> tw_seg;           // (offset, S, R, 0) per (size, pass)
   size_t tw_total = 0;
   ExpsumShape shape{};
+  I8Config i8{};
+  bool i8_ok = false;          // int8-limb tensor-core exp-sum available for this plan
+  int32_t expsum_path = 0;     // sfft_options.expsum_path
+  int smem_optin = 0;
   // workspace
   size_t ws_bytes = 0;
   void* ws = nullptr;
@@ -80,7 +84,7 @@ enum Buf {
   B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
-  B_WRAPS,
+  B_WRAPS, B_I8B, B_I8SIG,
   B_COUNT
 };
 
@@ -186,6 +190,8 @@ void layout(sfft_plan_t* P) {
   sz[B_TWSEG] = 16 * P->tw_seg.size();
   sz[B_UALL] = 8 * S * (size_t)P->kk + 256;
   sz[B_WRAPS] = 4 * S * ((size_t)P->k + 1);
+  sz[B_I8B] = P->i8_ok ? i8_limb_bytes(P->i8, (int)S) : 0;
+  sz[B_I8SIG] = 8 * S;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -252,6 +258,12 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_log = ptr<int32_t>(P, B_LOG);
   D.ctrl = ptr<int32_t>(P, B_CTRL);
   D.active = ptr<int32_t>(P, B_ACTIVE);
+  if (P->i8_ok) {
+    D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
+    D.i8_K = P->k;
+    D.i8_B = ptr<int8_t>(P, B_I8B);
+    D.i8_sigma = ptr<double>(P, B_I8SIG);
+  }
   return D;
 }
 
@@ -313,6 +325,31 @@ int fft_index_host(const sfft_plan_t* P, int p) {
     ++launches;                                                                                  \
   } while (0)
 
+// int8-limb exp-sum for this iteration?  Needs the limb tables in shared memory; tiny primes (late
+// iterations) waste most of a 128-row MMA tile and stay on the FP64 kernels (SFFT_I8_MIN_P overrides).
+bool i8_use_for(const sfft_plan_t* P, int max_p) {
+  static const int min_p = getenv("SFFT_I8_MIN_P") ? atoi(getenv("SFFT_I8_MIN_P")) : 64;
+  if (P->expsum_path == 2) return i8_fits(P->i8, max_p, P->k, P->smem_optin);
+  return max_p >= min_p && i8_fits(P->i8, max_p, P->k, P->smem_optin);
+}
+
+// term split of the int8 kernel: same wave-quantisation model as the FP64 kernels, one CTA per SM
+int i8_ksplit(const sfft_plan_t* P, int max_p, int n_active) {
+  const int blocks = i8_blocks(P->i8, max_p, n_active);
+  const int W = P->n_sm;
+  const int steps = (P->k + 15) / 16;
+  const int ks_max = std::min(32, std::max(1, steps / 4));
+  int ksplit = 1;
+  double best = 1e30;
+  for (int ks = 1; ks <= ks_max; ++ks) {
+    if (ks > 1 && (size_t)ks * n_active * P->L * (size_t)max_p * 16 > kPartBytes) break;
+    const double waves = std::ceil((double)blocks * ks / W);
+    const double t = waves / ks * (ks > 1 ? 1.03 : 1.0) + 0.02 * ks;   // per-CTA prologue (tables)
+    if (t < best - 1e-9) { best = t; ksplit = ks; }
+  }
+  return ksplit;
+}
+
 // SFFT_SYNC=1: synchronise after every launch (debugging aid: pins errors to the launching call)
 const bool g_sync_launches = getenv("SFFT_SYNC") != nullptr;
 
@@ -362,6 +399,8 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->stream = (cudaStream_t)opt->stream;
     P->profile = opt->profile != 0;
     P->literal = opt->literal_residual != 0;
+    P->expsum_path = opt->expsum_path;
+    if (P->expsum_path < 0 || P->expsum_path > 2) return SFFT_EINVAL;
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -438,6 +477,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   ce = cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, P->device);
   if (ce != cudaSuccess) return SFFT_ECUDA;
   cudaDeviceGetAttribute(&P->n_sm, cudaDevAttrMultiProcessorCount, P->device);
+  P->smem_optin = smem_optin;
   int M_max = 0;
   for (int M = 3; M <= 20000; ++M)
     if (is_7smooth(M)) {
@@ -491,6 +531,9 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   while (P->H < 2 * k) P->H <<= 1;
   P->shape = choose_expsum_shape(P->L);
   P->Lp = P->shape.nt * P->shape.bn;
+  // int8-limb tensor-core exp-sum (bin-domain residual only: its B limbs are the fixed signal rows)
+  if (P->expsum_path != 1 && !P->literal) P->i8_ok = i8_configure(P->L, P->E, P->k, &P->i8);
+  if (P->expsum_path == 2 && !P->i8_ok) return SFFT_ENOTSUP;
   // shared-memory budgets of the other kernels
   if (16 * ((size_t)P->p_stride + 2) + 2 * 16 * 16 * (size_t)P->shape.bn + 256 > (size_t)smem_optin) return SFFT_ENOTSUP;
   if (8 * (size_t)P->p_stride + 4 * (2 * (size_t)P->p_stride + 2 * (size_t)k + 64) > (size_t)smem_optin)
@@ -574,6 +617,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   mark();
   LAUNCH(P, launch_project(D, batch, sig->freqs, sig->coeffs, st));
   launches += 1;   // init_state_kernel
+  if (P->i8_ok) {
+    LAUNCH(P, launch_i8_prepare(D, batch, P->k, st));
+    launches += 1;   // sigma + limbs
+  }
   int iter = 1;
   int32_t last_iter = 0, n_expsum = 0;
   std::vector<size_t> it_marks;
@@ -590,7 +637,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     // term split when the (signal x h-tile x n-tile) grid cannot fill the GPU (late iterations)
     int ksplit = 1;
     const ExpsumShape shp = expsum_for_p(P->shape, max_p);
-    {
+    const bool use_i8 = P->i8_ok && i8_use_for(P, max_p);
+    if (use_i8) {
+      ksplit = i8_ksplit(P, max_p, n_active);
+    } else {
       // wave quantisation model: time ~ ceil(B ks / W) / ks, W = resident CTAs; a split costs ~3 %
       // (partial lines written and re-read by the FFT)
       const int blocks = expsum_blocks(shp, max_p, n_active);
@@ -610,7 +660,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     const int big = max_M >= kFftBigM;
     LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, st));
     mark();
-    LAUNCH(P, launch_expsum(D, shp, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
+    if (use_i8)
+      LAUNCH(P, launch_expsum_i8(D, P->i8, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, P->smem_optin, st));
+    else
+      LAUNCH(P, launch_expsum(D, shp, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
     ++n_expsum;
     mark();
     LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, ksplit,
@@ -739,7 +792,13 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   const int fi = fft_index_host(P, (int)p);
   LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->fft[fi].M >= kFftBigM,
                             P->stream));
-  LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, (int)p), (int)p, 1, 1, nullptr, 0, P->stream));
+  if (P->i8_ok && i8_use_for(P, (int)p)) {
+    D.i8_K = K;
+    LAUNCH(P, launch_i8_prepare(D, 1, K, P->stream));
+    LAUNCH(P, launch_expsum_i8(D, P->i8, (int)p, 1, 1, nullptr, 0, P->smem_optin, P->stream));
+  } else {
+    LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, (int)p), (int)p, 1, 1, nullptr, 0, P->stream));
+  }
   CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
                                 cudaMemcpyDeviceToDevice, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));

@@ -77,6 +77,17 @@ struct DevParams {
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
   int32_t* active;             // [batch] indices of the signals still running this iteration
+  // int8-limb tensor-core exp-sum (k_expsum_i8.cu)
+  int32_t i8_S, i8_NT, i8_ntiles, i8_nks;   // limbs, output columns per tile, n-tiles, K-step capacity
+  int32_t i8_K;                // terms held in the B limbs (k for a solve, K for the stage entry point)
+  int8_t* i8_B;                // [batch][ntiles][nks][S][NT*32] B limbs in the UMMA K-major layout
+  double* i8_sigma;            // [batch] coefficient scale
+};
+
+// int8-limb exp-sum configuration (host)
+struct I8Config {
+  int S, NT, ntiles, nks, npass;
+  int wl[4], wh[4], a_base[4], nsa[4];   // per pass: weights [wl, wh], TMEM column of A slot 0, A slots
 };
 
 // ---- device helpers ----------------------------------------------------------------------
@@ -109,6 +120,15 @@ int expsum_bk();
 cudaError_t launch_expsum(const DevParams& P, const ExpsumShape& S, int32_t max_p, int32_t n_signals,
                           int32_t ksplit, double2* part, int32_t p_part, cudaStream_t st, int* occ_out = nullptr);
 int expsum_occupancy(const ExpsumShape& S, int32_t max_p);   // resident CTAs per SM
+// k_expsum_i8.cu
+int i8_limbs_for(int64_t E);
+bool i8_configure(int L, int64_t E, int k, I8Config* out);
+size_t i8_limb_bytes(const I8Config& c, int batch);
+bool i8_fits(const I8Config& c, int p, int k, int smem_optin);
+int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals);
+cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st);
+cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_p, int32_t n_signals, int32_t ksplit,
+                             double2* part, int32_t p_part, int smem_optin, cudaStream_t st);
 // k_fft.cu
 // smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,

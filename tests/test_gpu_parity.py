@@ -37,9 +37,11 @@ def _plan(S, c, blocks=None, **kw):
 # ------------------------------------------------------------------ stage parity (teacher forced)
 @pytest.mark.parametrize("name,blocks,p,m", [("c2", (2, 1), 503, 1), ("c2", (1, 1, 1), 101, 2),
                                              ("c1", (1, 1), 23, 1), ("c3", None, 1009, 7),
-                                             ("c5", None, 2503, 1)])
-def test_stage_expsum_vs_oracle(S, name, blocks, p, m):
-    """a3: every line of one iteration, with signal terms AND registry terms (negated coefficients)."""
+                                             ("c5", None, 2503, 1), ("c3", None, 5003, 3)])
+@pytest.mark.parametrize("path", [1, 2])
+def test_stage_expsum_vs_oracle(S, name, blocks, p, m, path):
+    """a3: every line of one iteration, with signal terms AND registry terms (negated coefficients);
+    path 1 = FP64 tensor/vector kernels, path 2 = exact int8-limb products on tcgen05."""
     c = W.CONFIGS[name]
     blocks = blocks or c.blocks
     w, a = W.make_signal(c, 2)
@@ -50,16 +52,25 @@ def test_stage_expsum_vs_oracle(S, name, blocks, p, m):
     nreg = c.k // 2
     vv = np.concatenate([v, v[:nreg]])
     cc = np.concatenate([a, -a[:nreg] * (1 + 1e-3)])
-    plan = _plan(S, c, blocks)
+    plan = _plan(S, c, blocks, expsum_path=path)
     assert plan.E == E
     got = S.sfft_stage_expsum(plan, torch.from_numpy(np.ascontiguousarray(vv.T)).cuda(),
                               torch.from_numpy(cc).cuda(), p, m).cpu().numpy()
     r = len(blocks)
     scale = np.abs(cc).sum()
+    if path == 2:
+        # int8 limbs: every root / coefficient component is held to 256^-S (rounding of the fixed-point
+        # value, <= 1.008 * 256^-S, plus the dropped limb products of weight >= S, <= (S + 1) * 256^-S)
+        # relative to 1 / sigma; 4 real products per complex term -> a worst-case bound per sample
+        nl = 5 if E <= 2 ** 28 else 6
+        sigma = np.abs(np.concatenate([cc.real, cc.imag])).max()
+        bound = len(cc) * 4 * (nl + 3) * 256.0 ** -nl * sigma
+    else:
+        bound = 1e-12 * scale
     for n in [-1] + list(range(r)):
         ref = O.sample_line(vv, cc, p, m, n, E)
         err = np.abs(got[n + 1] - ref).max()
-        assert err <= 1e-12 * scale, (n, err, scale)
+        assert err <= bound, (n, err, bound)
 
 
 @pytest.mark.parametrize("p", [2, 3, 5, 7, 11, 23, 101, 503, 1009, 2503, 5003])
@@ -322,7 +333,7 @@ def test_e2e_literal_residual_mode(S, name, trials):
     w, a = W.make_batch(c, trials)
     res = {}
     for lit in (True, False):
-        plan = _plan(S, c, batch=len(trials), literal_residual=lit)
+        plan = _plan(S, c, batch=len(trials), literal_residual=lit, expsum_path=1)   # FP64 on both sides
         r = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
         res[lit] = (r.freqs.cpu().numpy().copy(), r.coeffs.cpu().numpy().copy(), r.count.cpu().numpy().copy(),
                     [r.report.primes[i] for i in range(8)], [r.report.accepted[i] for i in range(8)])
