@@ -259,7 +259,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.ctrl = ptr<int32_t>(P, B_CTRL);
   D.active = ptr<int32_t>(P, B_ACTIVE);
   if (P->i8_ok) {
-    D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
+    D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
     D.i8_B = ptr<int8_t>(P, B_I8B);
     D.i8_sigma = ptr<double>(P, B_I8SIG);

@@ -26,10 +26,14 @@
 //     stages;
 //   * B limbs (line coefficients, precomputed once per solve in the UMMA K-major layout) stream
 //     through shared memory by 1-D bulk copies (TMA engine) on an mbarrier ring;
-//   * one thread issues tcgen05.mma.kind::i8 (A from TMEM, B from smem, s32 accumulators in TMEM),
-//     one accumulator per limb weight; weights that do not fit TMEM at once run in separate passes
-//     (highest weights first) whose FP64 partials are added in the epilogue;
-//   * the epilogue (same 4 warps) reads the accumulators with tcgen05.ld and writes complex128 lines.
+//   * one elected lane issues tcgen05.mma.kind::i8 (A from TMEM, B from smem, s32 accumulators in TMEM),
+//     one accumulator per limb weight: all S weights of an output tile live in TMEM at once, so the
+//     output columns are split into n-tiles of at most NT columns (S NT + slots <= 512 TMEM columns);
+//   * the epilogue (the generator warps) reads the accumulators with tcgen05.ld, sums the weights in FP64
+//     and writes complex128 lines;
+//   * the kernel is persistent (one CTA per SM walks a contiguous range of tiles, so the root table of a
+//     signal is built once per CTA) and a ring of full / empty mbarriers couples generators, the B
+//     producer and the MMA issuer.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -74,21 +78,28 @@ __device__ __forceinline__ void digits(int64_t X, int S, int (&d)[8]) {
   }
 }
 
-// One thread per (signal, n-tile, K step, output column, 4-byte K word): S words, one per limb.
+__host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT, int NT_last) {
+  return nt == ntiles - 1 ? NT_last : NT;
+}
+
+// B limbs of signal s, n-tile nt (width W), K step ks, limb t: 32 W bytes at
+//   i8_B + s * per_signal + nt * nks * S * NT * 32 + (ks * S + t) * W * 32,  per_signal = nks * S * 32 * cols
+// in the UMMA K-major layout: (column, K byte) -> (col / 8) 256 + (k / 16) 128 + (col % 8) 16 + k % 16.
+// One thread per (signal, padded output column, K step, 4-byte K word): S words, one per limb.
 __global__ void i8_limbs_kernel(DevParams P, int32_t K) {
-  const int NT = P.i8_NT, S = P.i8_S;
-  const int64_t per_step = (int64_t)NT * 8;                       // (column, K word) pairs
+  const int NT = P.i8_NT, S = P.i8_S, ntiles = P.i8_ntiles, nks = P.i8_nks;
+  const int cols = (ntiles - 1) * NT + P.i8_NT_last;
+  const int64_t per_sig = (int64_t)cols * nks * 8;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t steps_all = (int64_t)P.i8_ntiles * P.i8_nks;
-  const int64_t total = (int64_t)P.batch * steps_all * per_step;
-  if (g >= total) return;
-  const int e = (int)(g % per_step);
-  const int64_t st = g / per_step;                               // (signal, ntile, kstep)
-  const int ks = (int)(st % P.i8_nks);
-  const int nt = (int)((st / P.i8_nks) % P.i8_ntiles);
-  const int s = (int)(st / steps_all);
-  const int col = e >> 3, kw = e & 7;                            // output column, K word (4 K elements)
-  const int gc = nt * NT + col;
+  if (g >= (int64_t)P.batch * per_sig) return;
+  const int s = (int)(g / per_sig);
+  int64_t r = g % per_sig;
+  const int kw = (int)(r & 7);
+  r >>= 3;
+  const int ks = (int)(r % nks);
+  const int gc = (int)(r / nks);                                 // padded output column
+  const int nt = gc / NT, col = gc % NT;
+  const int W = i8_tile_width(nt, ntiles, NT, P.i8_NT_last);
   const int n = gc >> 1, im_out = gc & 1;
   const double q = 127.0 * ldexp(1.0, 8 * (S - 1)) / P.i8_sigma[s];
   int dg[4][8];
@@ -104,40 +115,38 @@ __global__ void i8_limbs_kernel(DevParams P, int32_t K) {
     }
     digits(llrint(v * q), S, dg[b]);
   }
-  int8_t* base = P.i8_B + ((((int64_t)s * P.i8_ntiles + nt) * P.i8_nks + ks) * S) * (int64_t)NT * 32;
+  int8_t* base = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)nt * nks * S * NT * 32 + (int64_t)ks * S * W * 32;
   const int off = (col >> 3) * 256 + (kw >> 2) * 128 + (col & 7) * 16 + (kw & 3) * 4;
   for (int t = 0; t < S; ++t) {
     const uint32_t w = (uint32_t)(uint8_t)dg[0][t] | ((uint32_t)(uint8_t)dg[1][t] << 8) |
                        ((uint32_t)(uint8_t)dg[2][t] << 16) | ((uint32_t)(uint8_t)dg[3][t] << 24);
-    *reinterpret_cast<uint32_t*>(base + (int64_t)t * NT * 32 + off) = w;
+    *reinterpret_cast<uint32_t*>(base + (int64_t)t * W * 32 + off) = w;
   }
 }
 
 // ------------------------------------------------------------------ the exp-sum kernel
 constexpr int kI8GenWarps = 8;        // 2 per TMEM lane quarter: warp g covers rows 32 (g % 4) .., terms 8 (g / 4) ..
-constexpr int kI8MaxAStages = 8;
+constexpr int kI8MaxSlots = 8;
 constexpr int kI8Threads = 32 * (kI8GenWarps + 2);   // + B producer warp + MMA warp
 constexpr int kI8ProdWarp = kI8GenWarps, kI8MmaWarp = kI8GenWarps + 1;
 
 struct I8Args {
-  int32_t n_htiles, ksplit, p_part, nsb, npass;
-  int32_t pass[4];            // wl | wh << 4 | nsa << 8 | a_base << 16 (TMEM column of A slot 0)
+  int32_t n_htiles, ksplit, p_part, n_slots;
+  int32_t nb;                 // B ring slots (shared memory)
+  int32_t nap;                // producer back-off (ns) while the B ring is full
+  int32_t gnap;               // generator back-off (ns) while waiting for a free A slot (0: spin)
   uint32_t b_stage_bytes;     // S * NT * 32
   uint32_t tab_off, u_off;    // smem offsets of the limb tables and the u list
-  int32_t dbg;                // tuning only (SFFT_I8_DBG): 1 conflict-free gathers, 2 no MMAs, 3 no A generation,
-                              // 4 MMAs only (no copies, no generation)
+  long long* prof;            // tuning only (SFFT_I8_PROF): per-CTA cycle counters
+  int32_t dbg;                // tuning only (SFFT_I8_DBG): 1 conflict-free gathers, 2 no MMAs, 3 no A generation
 };
-__device__ __forceinline__ int pass_wl(int v) { return v & 15; }
-__device__ __forceinline__ int pass_wh(int v) { return (v >> 4) & 15; }
-__device__ __forceinline__ int pass_nsa(int v) { return (v >> 8) & 255; }
-__device__ __forceinline__ int pass_abase(int v) { return v >> 16; }
 
-// 8 terms (4 TMEM columns per limb) of one K step for this thread's row h
+// 8 terms (4 TMEM columns per limb) of one K step for this thread's row h: gather the root limbs and pack
+// them into the TMEM word layout (4 K bytes per 32-bit column: re_j, im_j, re_j+1, im_j+1)
 template <int NL>
-__device__ __forceinline__ void gen_stage(uint32_t taddr, const int* __restrict__ sU, const uint2* __restrict__ sTlo,
-                                          const uint32_t* __restrict__ sThi, unsigned h, unsigned magic, int p,
-                                          int dbg) {
-  uint32_t w[NL][4];
+__device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int* __restrict__ sU,
+                                          const uint2* __restrict__ sTlo, const uint32_t* __restrict__ sThi, unsigned h,
+                                          unsigned magic, int p, int dbg) {
   unsigned q[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
@@ -166,240 +175,269 @@ __device__ __forceinline__ void gen_stage(uint32_t taddr, const int* __restrict_
       if constexpr (NL > 5) w[5][c] = __byte_perm(hi[2 * c], hi[2 * c + 1], 0x7632);
     }
   }
-#pragma unroll
-  for (int t = 0; t < NL; ++t) tc::tmem_st4(taddr + 8 * t, w[t]);
 }
 
-// All limb products of one K step for the weights [WL, WH] of a pass, fully unrolled: accumulator of
-// weight w at column (w - WL) NT, A limb s at a0 + 8 s, B limb t at descriptor bd0 + t * (NT * 32 / 16).
-template <int WL, int WH>
+// All S (S + 1) / 2 limb products of one K step, fully unrolled: accumulator of weight w at column w NT,
+// A limb s at a0 + 8 s, B limb t at descriptor bd0 + t * (NT * 32 / 16).
+template <int S>
 __device__ __forceinline__ void issue_stage(uint32_t tbase, uint32_t a0, uint64_t bd0, uint32_t nt_cols, uint32_t nt_desc,
                                             uint32_t idesc, bool first_k) {
 #pragma unroll
-  for (int w = WL; w <= WH; ++w)
+  for (int w = 0; w < S; ++w)
 #pragma unroll
     for (int sl = 0; sl <= w; ++sl)
-      tc::mma_i8_ts(tbase + (uint32_t)(w - WL) * nt_cols, a0 + 8 * sl, bd0 + (uint64_t)((w - sl) * nt_desc), idesc,
+      tc::mma_i8_ts(tbase + (uint32_t)w * nt_cols, a0 + 8 * sl, bd0 + (uint64_t)((w - sl) * nt_desc), idesc,
                     (!first_k || sl > 0) ? 1u : 0u);
 }
 
-__device__ __forceinline__ void issue_stage_rt(int wl, int wh, uint32_t tbase, uint32_t a0, uint64_t bd0,
-                                               uint32_t nt_cols, uint32_t nt_desc, uint32_t idesc, bool first_k) {
-#define SFFT_I8_CASE(a, b) \
-  case a * 8 + b: issue_stage<a, b>(tbase, a0, bd0, nt_cols, nt_desc, idesc, first_k); break;
-  switch (wl * 8 + wh) {
-    SFFT_I8_CASE(0, 0) SFFT_I8_CASE(0, 1) SFFT_I8_CASE(0, 2) SFFT_I8_CASE(0, 3) SFFT_I8_CASE(0, 4) SFFT_I8_CASE(0, 5)
-    SFFT_I8_CASE(1, 1) SFFT_I8_CASE(1, 2) SFFT_I8_CASE(1, 3) SFFT_I8_CASE(1, 4) SFFT_I8_CASE(1, 5)
-    SFFT_I8_CASE(2, 2) SFFT_I8_CASE(2, 3) SFFT_I8_CASE(2, 4) SFFT_I8_CASE(2, 5)
-    SFFT_I8_CASE(3, 3) SFFT_I8_CASE(3, 4) SFFT_I8_CASE(3, 5)
-    SFFT_I8_CASE(4, 4) SFFT_I8_CASE(4, 5)
-    SFFT_I8_CASE(5, 5)
-    default: break;
-  }
-#undef SFFT_I8_CASE
+// Tile t of the launch: (slot, h-tile, n-tile, term split) with the split index fastest.
+struct I8Tile { int slot, ht, nt, ks; };
+__device__ __forceinline__ I8Tile tile_of(int t, const I8Args& A, int ntiles) {
+  I8Tile r;
+  r.ks = t % A.ksplit;
+  t /= A.ksplit;
+  r.nt = t % ntiles;
+  t /= ntiles;
+  r.ht = t % A.n_htiles;
+  r.slot = t / A.n_htiles;
+  return r;
 }
 
-__global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I8Args A, double2* part) {
+// ring slots of a tile of width W: the S accumulators take S W columns, each slot S * 8 columns
+__device__ __forceinline__ int ring_slots(int W, int S) { return min(kI8MaxSlots, (512 - S * W) / (8 * S)); }
+
+// Persistent: CTA c owns the contiguous tile range [c T / G, (c + 1) T / G), so consecutive tiles share a
+// signal and the root limb table / phase list is rebuilt only when the signal changes.  Every role walks
+// the same tile sequence; the ring parities carry over from tile to tile (one bit per slot).  Two rings:
+//   A (TMEM, ring_slots(W, S) slots): afull[i] = 8 generator-warp arrivals, aempty[i] = one tcgen05.commit
+//   B (shared memory, A.nb slots, deep enough to cover the L2 latency of the bulk copies):
+//     bfull[i] = the producer's arrive.expect_tx + the bytes, bempty[i] = one tcgen05.commit
+// Generator warp 0 waits for bfull of the step before it arrives on afull, so the MMA issuer waits on one
+// barrier per step (every try_wait costs ~90 cycles even when the phase is complete, and the tensor
+// core's instruction queue is too shallow to hide two of them).
+template <int S, bool PROF>
+__global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I8Args A, double2* part, int32_t n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  uint64_t* bfull = reinterpret_cast<uint64_t*>(smem_raw);        // [4]
-  uint64_t* bempty = bfull + 4;                                      // [4]
-  uint64_t* afull = bfull + 8;                                       // [kI8MaxAStages]
-  uint64_t* aempty = afull + kI8MaxAStages;                          // [kI8MaxAStages]
-  uint64_t* accfull = aempty + kI8MaxAStages;
+  uint64_t* afull = reinterpret_cast<uint64_t*>(smem_raw);         // [kI8MaxSlots]
+  uint64_t* aempty = afull + kI8MaxSlots;
+  uint64_t* bfull = aempty + kI8MaxSlots;
+  uint64_t* bempty = bfull + kI8MaxSlots;
+  uint64_t* accfull = bempty + kI8MaxSlots;
   uint64_t* accempty = accfull + 1;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(accempty + 1);
-  int* spass = reinterpret_cast<int*>(tslot + 1);                   // [4]
   unsigned char* sB = smem_raw + 512;
   uint2* sTlo = reinterpret_cast<uint2*>(smem_raw + A.tab_off);
-  const int NT = P.i8_NT, S = P.i8_S;
-
-  int bid = blockIdx.x;
-  const int ks_i = bid % A.ksplit;
-  bid /= A.ksplit;
-  const int nt = bid % P.i8_ntiles;
-  bid /= P.i8_ntiles;
-  const int ht = bid % A.n_htiles;
-  const int slot = bid / A.n_htiles;
-  const int s = P.active[slot];
-  const int p = P.st_p[s];
-  if (ht * kI8Rows >= p) return;
-  const int K = P.i8_K;                                             // terms in the B limbs (bin-domain: k)
-  const int nks = (K + kI8StepTerms - 1) / kI8StepTerms;
-  const int per = (nks + A.ksplit - 1) / A.ksplit;
-  const int ks_lo = ks_i * per, ks_hi = min(nks, ks_lo + per);
-  const int nk = max(0, ks_hi - ks_lo);
-  uint32_t* sThi = reinterpret_cast<uint32_t*>(sTlo + p);
   int* sU = reinterpret_cast<int*>(smem_raw + A.u_off);
+  const int NT = P.i8_NT, ntiles = P.i8_ntiles, nks = P.i8_nks;
+  const int cols = (ntiles - 1) * NT + P.i8_NT_last;
+  const int K = P.i8_K;                                             // terms in the B limbs (bin-domain: k)
+  const int nkt = (K + kI8StepTerms - 1) / kI8StepTerms;             // K steps in use
+  const int per = (nkt + A.ksplit - 1) / A.ksplit;
+  const int t_lo = (int)((int64_t)blockIdx.x * n_tiles / gridDim.x);
+  const int t_hi = (int)((int64_t)(blockIdx.x + 1) * n_tiles / gridDim.x);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == kI8MmaWarp) tc::tmem_alloc<512>(tslot);
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) { tc::mbar_init(bfull + i, 1); tc::mbar_init(bempty + i, 1); }
-    for (int i = 0; i < kI8MaxAStages; ++i) { tc::mbar_init(afull + i, kI8GenWarps); tc::mbar_init(aempty + i, 1); }
+    for (int i = 0; i < kI8MaxSlots; ++i) {
+      tc::mbar_init(afull + i, kI8GenWarps);
+      tc::mbar_init(aempty + i, 1);
+      tc::mbar_init(bfull + i, 1);
+      tc::mbar_init(bempty + i, 1);
+    }
     tc::mbar_init(accfull, 1);
     tc::mbar_init(accempty, kI8GenWarps);
     tc::fence_mbar_init();
-  }
-  if (tid < 4) spass[tid] = A.pass[tid];
-  // root limb tables of this signal's prime (W_tab from the prep kernel) and the phase indices u_j
-  {
-    const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
-    const double qa = 127.0 * ldexp(1.0, 8 * (S - 1));
-    for (int q = tid; q < p; q += kI8Threads) {
-      const double2 w = Wg[q];
-      int dr[8], di[8];
-      digits(llrint(w.x * qa), S, dr);
-      digits(llrint(w.y * qa), S, di);
-      uint32_t e[6];
-#pragma unroll
-      for (int t = 0; t < 6; ++t) e[t] = t < S ? ((uint32_t)(uint8_t)dr[t] | ((uint32_t)(uint8_t)di[t] << 8)) : 0u;
-      sTlo[q] = make_uint2(e[0] | (e[1] << 16), e[2] | (e[3] << 16));
-      if (S > 4) sThi[q] = e[4] | (e[5] << 16);
-    }
-    const int2* ug = P.u_all + (int64_t)s * P.kk;
-    for (int i = tid; i < nk * kI8StepTerms; i += kI8Threads) {
-      const int j = ks_lo * kI8StepTerms + i;
-      sU[i] = j < K ? ug[j].x : 0;
-    }
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   const uint32_t tbase = *tslot;
 
-  if (warp < kI8GenWarps) {
-    // ---------------- A generators + epilogue: warp g owns TMEM lanes / rows 32 (g % 4) .., terms 8 (g / 4) ..
-    const int quarter = warp & 3, half = warp >> 2;
-    const int row = 32 * quarter + lane;
-    const unsigned h = (unsigned)(ht * kI8Rows + row);
-    const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;
-    const uint32_t lane_addr = tbase + ((uint32_t)(32 * quarter) << 16);
-    double2* out;
-    int64_t pstr;
-    if (A.ksplit == 1) {
-      out = P.lines + (int64_t)s * P.L * P.p_stride;
-      pstr = P.p_stride;
-    } else {
-      const int n_slots = gridDim.x / (A.ksplit * A.n_htiles * P.i8_ntiles);
-      out = part + ((int64_t)ks_i * n_slots + slot) * P.L * (int64_t)A.p_part;
-      pstr = A.p_part;
-    }
-    const double scale = P.i8_sigma[s] / (127.0 * 127.0);
-    uint32_t aphase = 0;                                           // parity bit per A slot
-    for (int ps = 0; ps < A.npass; ++ps) {
-      const int pv = spass[ps];
-      const int wl = pass_wl(pv), wh = pass_wh(pv), nsa = pass_nsa(pv), nl = wh + 1;
-      const uint32_t ta0 = lane_addr + pass_abase(pv) + 4 * half;
-      for (int kq = 0; kq < nk; ++kq) {
-        const int sa = kq % nsa;
-        tc::mbar_wait(aempty + sa, ((aphase >> sa) & 1) ^ 1);
-        aphase ^= 1u << sa;
-        const uint32_t ta = ta0 + sa * nl * 8;
-        const int* u8 = sU + kq * kI8StepTerms + 8 * half;
-        if (A.dbg != 3 && A.dbg != 4) switch (nl) {
-          case 1: gen_stage<1>(ta, u8, sTlo, sThi, h, magic, p, A.dbg); break;
-          case 2: gen_stage<2>(ta, u8, sTlo, sThi, h, magic, p, A.dbg); break;
-          case 3: gen_stage<3>(ta, u8, sTlo, sThi, h, magic, p, A.dbg); break;
-          case 4: gen_stage<4>(ta, u8, sTlo, sThi, h, magic, p, A.dbg); break;
-          case 5: gen_stage<5>(ta, u8, sTlo, sThi, h, magic, p, A.dbg); break;
-          default: gen_stage<6>(ta, u8, sTlo, sThi, h, magic, p, A.dbg); break;
+  uint32_t aring = 0, bring = 0;        // parity bit per ring slot (each role keeps its own copies)
+  int bpos = 0;                         // B ring position (producer / MMA)
+  int ntile_done = 0;                   // accfull / accempty parity
+  int cur_s = -1;
+  long long pr_a = 0, pr_b = 0, pr_e = 0, pr_t = 0;
+  const long long pr_start = clock64();
+  for (int t = t_lo; t < t_hi; ++t) {
+    const I8Tile tl = tile_of(t, A, ntiles);
+    const int s = P.active[tl.slot];
+    const int p = P.st_p[s];
+    if (tl.ht * kI8Rows >= p) continue;                            // uniform across the CTA
+    const int ks_lo = tl.ks * per, ks_hi = min(nkt, ks_lo + per);
+    const int nk = max(0, ks_hi - ks_lo);
+    if (nk == 0) continue;
+    const int W = i8_tile_width(tl.nt, ntiles, NT, P.i8_NT_last);
+    const int nsl = ring_slots(W, S);
+    uint32_t* sThi = reinterpret_cast<uint32_t*>(sTlo + p);
+    if (s != cur_s) {
+      const long long ct0 = PROF ? clock64() : 0;
+      // root limb table of this signal's prime (W_tab from the prep kernel) and all its phase indices u_j
+      __syncthreads();
+      const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
+      const double qa = 127.0 * ldexp(1.0, 8 * (S - 1));
+      for (int q0 = 0; q0 < p; q0 += 4 * kI8Threads) {
+        double2 wv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * kI8Threads + tid;
+          wv[u] = q < p ? Wg[q] : make_double2(0.0, 0.0);
         }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + u * kI8Threads + tid;
+          if (q >= p) break;
+          int dr[8], di[8];
+          digits(llrint(wv[u].x * qa), S, dr);
+          digits(llrint(wv[u].y * qa), S, di);
+          uint32_t e[6];
+#pragma unroll
+          for (int i = 0; i < 6; ++i) e[i] = i < S ? ((uint32_t)(uint8_t)dr[i] | ((uint32_t)(uint8_t)di[i] << 8)) : 0u;
+          sTlo[q] = make_uint2(e[0] | (e[1] << 16), e[2] | (e[3] << 16));
+          if (S > 4) sThi[q] = e[4] | (e[5] << 16);
+        }
+      }
+      const int2* ug = P.u_all + (int64_t)s * P.kk;
+      for (int i = tid; i < nkt * kI8StepTerms; i += kI8Threads) sU[i] = i < K ? ug[i].x : 0;
+      __syncthreads();
+      cur_s = s;
+      if (PROF) pr_t += clock64() - ct0;
+    }
+
+    if (warp < kI8GenWarps) {
+      // ---------------- A generators + epilogue: warp g owns TMEM lanes / rows 32 (g % 4) .., terms 8 (g / 4) ..
+      const int quarter = warp & 3, half = warp >> 2;
+      const int row = 32 * quarter + lane;
+      const unsigned h = (unsigned)(tl.ht * kI8Rows + row);
+      const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;
+      const uint32_t lane_addr = tbase + ((uint32_t)(32 * quarter) << 16);
+      const uint32_t ta0 = lane_addr + (uint32_t)(S * W) + 4 * half;
+      // software pipeline: the limbs of step kq + 1 are gathered while the tensor core works on step kq and
+      // before the slot they go to is free; only the TMEM store + arrive sit on the critical path
+      uint32_t w[S][4];
+      const int* ub = sU + ks_lo * kI8StepTerms + 8 * half;
+      if (A.dbg != 3) gen_limbs<S>(w, ub, sTlo, sThi, h, magic, p, A.dbg);
+      int sl = 0;
+      for (int kq = 0; kq < nk; ++kq, sl = (sl + 1 == nsl ? 0 : sl + 1)) {
+        if (warp == 0) {                                           // B of this step landed (MMA waits on afull only)
+          const int sb = bpos;
+          bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
+          tc::mbar_wait(bfull + sb, (bring >> sb) & 1);
+          bring ^= 1u << sb;
+        }
+        const long long c0 = PROF ? clock64() : 0;
+        if (A.gnap) {
+          while (!tc::mbar_try_wait(aempty + sl, ((aring >> sl) & 1) ^ 1)) __nanosleep(A.gnap);
+        } else {
+          tc::mbar_wait(aempty + sl, ((aring >> sl) & 1) ^ 1);
+        }
+        aring ^= 1u << sl;
+        if (PROF) pr_a += clock64() - c0;
+        const uint32_t ta = ta0 + sl * S * 8;
+#pragma unroll
+        for (int t = 0; t < S; ++t) tc::tmem_st4(ta + 8 * t, w[t]);
         tc::tmem_wait_st();
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(afull + sa);
+        if (lane == 0) tc::mbar_arrive(afull + sl);
+        if (kq + 1 < nk && A.dbg != 3) gen_limbs<S>(w, ub + (kq + 1) * kI8StepTerms, sTlo, sThi, h, magic, p, A.dbg);
       }
-      // epilogue of this pass: sum the weights in FP64 (lowest weight first) and add to the lines;
-      // the two warps of a lane quarter take alternate 16-column chunks
-      tc::mbar_wait(accfull, ps & 1);
+      // epilogue: sum the S weights in FP64 (lowest first); the two warps of a lane quarter take alternate
+      // 16-column chunks
+      double2* out;
+      int64_t pstr;
+      if (A.ksplit == 1) {
+        out = P.lines + (int64_t)s * P.L * P.p_stride;
+        pstr = P.p_stride;
+      } else {
+        out = part + ((int64_t)tl.ks * A.n_slots + tl.slot) * P.L * (int64_t)A.p_part;
+        pstr = A.p_part;
+      }
+      const double scale = P.i8_sigma[s] / (127.0 * 127.0);
+      const long long ce0 = PROF ? clock64() : 0;
+      tc::mbar_wait(accfull, ntile_done & 1);
       tc::fence_after_sync();
-      const bool first = ps == 0;
-      for (int c0 = 16 * half; c0 < NT; c0 += 32) {
+      const bool live = h < (unsigned)p;
+      for (int c0 = 16 * half; c0 < W; c0 += 32) {
+        int32_t v[16];
         double acc[16];
+        tc::tmem_ld16(lane_addr + (uint32_t)((S - 1) * W + c0), v);
+        tc::tmem_wait_ld();
+        const double f0 = ldexp(1.0, -8 * (S - 1));
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-        for (int w = wh; w >= wl; --w) {
-          int32_t v[16];
-          tc::tmem_ld16(lane_addr + (w - wl) * NT + c0, v);
+        for (int i = 0; i < 16; ++i) acc[i] = (double)v[i] * f0;
+        for (int w = S - 2; w >= 0; --w) {
+          tc::tmem_ld16(lane_addr + (uint32_t)(w * W + c0), v);
           tc::tmem_wait_ld();
           const double f = ldexp(1.0, -8 * w);
 #pragma unroll
           for (int i = 0; i < 16; ++i) acc[i] = fma((double)v[i], f, acc[i]);
         }
-        if (h < (unsigned)p) {
-          const int n0 = (nt * NT + c0) >> 1;
+        const int n0 = (tl.nt * NT + c0) >> 1;
+        if (live) {
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int nn = n0 + i;
-            if (nn < P.L) {
-              double2* o = out + (int64_t)nn * pstr + h;
-              double2 val = make_double2(acc[2 * i] * scale, acc[2 * i + 1] * scale);
-              if (!first) {
-                const double2 prev = *o;
-                val.x += prev.x;
-                val.y += prev.y;
-              }
-              *o = val;
-            }
-          }
+          for (int i = 0; i < 8; ++i)
+            if (n0 + i < P.L) out[(int64_t)(n0 + i) * pstr + h] = make_double2(acc[2 * i] * scale, acc[2 * i + 1] * scale);
         }
       }
+      if (PROF) pr_e += clock64() - ce0;
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(accempty);
-    }
-  } else if (warp == kI8ProdWarp) {
-    // ---------------- B producer: one elected lane streams the B limb tiles (backs off while the ring is full)
-    if (lane == 0 && nk > 0) {
-      const int8_t* Bg = P.i8_B + (((int64_t)s * P.i8_ntiles + nt) * P.i8_nks) * S * (int64_t)NT * 32;
-      int ib = 0;
-      for (int ps = 0; ps < A.npass; ++ps) {
-        const uint32_t bytes = (uint32_t)(pass_wh(spass[ps]) + 1) * NT * 32;
-        for (int kq = 0; kq < nk; ++kq, ++ib) {
-          const int sb = ib % A.nsb;
-          const uint32_t par = ((ib / A.nsb) & 1) ^ 1;
-          while (!tc::mbar_try_wait(bempty + sb, par)) __nanosleep(64);
-          if (A.dbg == 4) {
-            tc::mbar_arrive(bfull + sb);
-          } else {
-            tc::mbar_expect_tx(bfull + sb, bytes);
-            tc::bulk_g2s(sB + (size_t)sb * A.b_stage_bytes, Bg + (int64_t)(ks_lo + kq) * S * NT * 32, bytes, bfull + sb);
-          }
+    } else if (warp == kI8ProdWarp) {
+      // ---------------- B producer: one lane streams the B limb tiles (backs off while the ring is full)
+      const int8_t* Bg = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)tl.nt * nks * S * NT * 32;
+      const uint32_t bytes = (uint32_t)S * W * 32;
+      for (int kq = 0; kq < nk; ++kq) {
+        const int sb = bpos;
+        bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
+        const uint32_t par = ((bring >> sb) & 1) ^ 1;
+        bring ^= 1u << sb;
+        if (lane == 0) {
+          while (!tc::mbar_try_wait(bempty + sb, par)) __nanosleep(A.nap);
+          tc::mbar_expect_tx(bfull + sb, bytes);
+          tc::bulk_g2s(sB + (size_t)sb * A.b_stage_bytes, Bg + (int64_t)(ks_lo + kq) * S * W * 32, bytes, bfull + sb);
         }
       }
-    }
-  } else {
-    // ---------------- MMA issuer: the whole warp runs the loop (uniform descriptors), one elected lane issues
-    {
-      const uint32_t idesc = tc::idesc_i8(kI8Rows, NT);
-      int ib = 0;
-      uint32_t aphase = 0;
-      for (int ps = 0; ps < A.npass; ++ps) {
-        const int pv = spass[ps];
-        const int wl = pass_wl(pv), wh = pass_wh(pv), nsa = pass_nsa(pv), nl = wh + 1;
-        if (ps > 0) {
-          tc::mbar_wait(accempty, (ps - 1) & 1);
-          tc::fence_after_sync();
+    } else {
+      // ---------------- MMA issuer: the whole warp walks the ring, one elected lane issues
+      const uint32_t idesc = tc::idesc_i8(kI8Rows, W);
+      if (ntile_done > 0) {
+        const long long c0 = PROF ? clock64() : 0;
+        tc::mbar_wait(accempty, (ntile_done - 1) & 1);
+        if (PROF) pr_e += clock64() - c0;
+        tc::fence_after_sync();
+      }
+      const uint64_t bdesc0 = tc::sdesc_kmajor(tc::smem_u32(sB), 128, 256);
+      const uint32_t stage_desc = A.b_stage_bytes >> 4, a_slot0 = tbase + (uint32_t)(S * W);
+      int sl = 0;
+      for (int kq = 0; kq < nk; ++kq) {
+        const int sb = bpos;
+        bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
+        const long long c1 = PROF ? clock64() : 0;
+        tc::mbar_wait(afull + sl, (aring >> sl) & 1);      // implies bfull (generator warp 0 waited for it)
+        aring ^= 1u << sl;
+        if (PROF) pr_a += clock64() - c1;
+        tc::fence_after_sync();
+        if (tc::elect_one()) {
+          if (A.dbg != 2)
+            issue_stage<S>(tbase, a_slot0 + sl * S * 8, bdesc0 + (uint64_t)(sb * stage_desc), (uint32_t)W, (uint32_t)W * 2,
+                           idesc, kq == 0);
+          tc::mma_commit(bempty + sb);
+          tc::mma_commit(aempty + sl);
         }
-        for (int kq = 0; kq < nk; ++kq, ++ib) {
-          const int sb = ib % A.nsb, sa = kq % nsa;
-          tc::mbar_wait(bfull + sb, (ib / A.nsb) & 1);
-          tc::mbar_wait(afull + sa, (aphase >> sa) & 1);
-          aphase ^= 1u << sa;
-          tc::fence_after_sync();
-          const uint64_t bd0 = tc::sdesc_kmajor(tc::smem_u32(sB + (size_t)sb * A.b_stage_bytes), 128, 256);
-          const uint32_t a0 = tbase + pass_abase(pv) + sa * nl * 8;
-          if (tc::elect_one()) {
-            if (A.dbg != 2) issue_stage_rt(wl, wh, tbase, a0, bd0, (uint32_t)NT, (uint32_t)NT * 2, idesc, kq == 0);
-            tc::mma_commit(bempty + sb);
-            tc::mma_commit(aempty + sa);
-          }
-          __syncwarp();
-        }
-        if (tc::elect_one()) tc::mma_commit(accfull);
         __syncwarp();
+        sl = sl + 1 == nsl ? 0 : sl + 1;
       }
+      if (tc::elect_one()) tc::mma_commit(accfull);
+      __syncwarp();
     }
+    ++ntile_done;
+  }
+  if (PROF && lane == 0 && (warp == 0 || warp == kI8MmaWarp)) {
+    long long* o = A.prof + (blockIdx.x * 2 + (warp == 0 ? 0 : 1)) * 5;
+    o[0] = clock64() - pr_start; o[1] = pr_a; o[2] = pr_b; o[3] = pr_e; o[4] = pr_t;
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -418,47 +456,29 @@ int i8_limbs_for(int64_t E) {
   return 0;   // beyond what FP64 roots can feed: use the FP64 tensor (DMMA) path
 }
 
-// Passes over the limb weights: a pass [wl, wh] holds (wh - wl + 1) NT s32 accumulator columns and
-// nsa A slots of 8 (wh + 1) columns within the 512 TMEM columns; at least 3 A slots per pass so the
-// generators run ahead of the tensor core (the MMA completion -> slot free -> regenerate round trip).
-static bool i8_passes(int S, int NT, int min_slots, I8Config& c) {
-  c.npass = 0;
-  int wh = S - 1;
-  while (wh >= 0) {
-    int wl = wh;
-    auto fits = [&](int lo) { return (wh - lo + 1) * NT + min_slots * 8 * (wh + 1) <= 512; };
-    if (!fits(wl)) return false;
-    while (wl - 1 >= 0 && fits(wl - 1)) --wl;
-    if (c.npass == 4) return false;
-    const int acc = (wh - wl + 1) * NT;
-    c.wl[c.npass] = wl;
-    c.wh[c.npass] = wh;
-    c.a_base[c.npass] = acc;
-    c.nsa[c.npass] = std::min(8, (512 - acc) / (8 * (wh + 1)));
-    ++c.npass;
-    wh = wl - 1;
-  }
-  return true;
-}
-
+// n-tiles: widths NT (multiple of 16) except a narrower last one; every tile keeps its S accumulators plus
+// at least 2 ring slots (S * 8 columns each) in the 512 TMEM columns.  Cost model per (128 rows, 16 terms):
+// MMA cycles S (S + 1) / 2 * W / 2 per tile, A generation ~250 cycles per tile (overlapped) and a fixed
+// ~120 cycles of ring overhead per stage.
 bool i8_configure(int L, int64_t E, int k, I8Config* out) {
   I8Config c{};
   c.S = i8_limbs_for(E);
   if (c.S == 0 || getenv("SFFT_NO_I8")) return false;
   const int N2 = 2 * L;
+  const int prods = c.S * (c.S + 1) / 2;
+  const int nt_cap = ((512 - 2 * 8 * c.S) / c.S) / 16 * 16;
+  int force = getenv("SFFT_I8_NT") ? atoi(getenv("SFFT_I8_NT")) : 0;
   double best = 1e30;
-  for (int nt = (N2 + 255) / 256; nt <= (N2 + 15) / 16; ++nt) {
-    const int NT = ((N2 + nt - 1) / nt + 15) / 16 * 16;
-    if (NT > 256) continue;
-    I8Config t = c;
-    t.NT = NT;
-    t.ntiles = nt;
-    if (!i8_passes(c.S, NT, 3, t) && !i8_passes(c.S, NT, 2, t)) continue;
-    // cycles per (128 rows, 16 terms): MMA (products * NT / 2) vs A generation (~150 per pass) + epilogue
-    const int prods = c.S * (c.S + 1) / 2;
-    const double cost = nt * (std::max(prods * NT / 2.0, 150.0 * t.npass) + 40.0 * t.npass);
-    if (cost < best - 1e-9) { best = cost; c.NT = NT; c.ntiles = nt; c.npass = t.npass;
-      for (int i = 0; i < 4; ++i) { c.wl[i] = t.wl[i]; c.wh[i] = t.wh[i]; c.a_base[i] = t.a_base[i]; c.nsa[i] = t.nsa[i]; } }
+  for (int NT = 16; NT <= nt_cap; NT += 16) {
+    if (force && NT != force) continue;
+    const int nt = (N2 + NT - 1) / NT;
+    const int last = ((N2 - (nt - 1) * NT) + 15) / 16 * 16;
+    double cost = 0;
+    for (int i = 0; i < nt; ++i) {
+      const int W = i == nt - 1 ? last : NT;
+      cost += std::max(prods * W / 2.0, 250.0) + 120.0;
+    }
+    if (cost < best - 1e-9) { best = cost; c.NT = NT; c.ntiles = nt; c.NT_last = last; }
   }
   if (c.NT == 0) return false;
   c.nks = (2 * k + kI8StepTerms - 1) / kI8StepTerms;
@@ -467,24 +487,25 @@ bool i8_configure(int L, int64_t E, int k, I8Config* out) {
 }
 
 size_t i8_limb_bytes(const I8Config& c, int batch) {
-  return (size_t)batch * c.ntiles * c.nks * c.S * (size_t)c.NT * 32;
+  const int cols = (c.ntiles - 1) * c.NT + c.NT_last;
+  return (size_t)batch * c.nks * c.S * 32 * (size_t)cols;
 }
 
-static size_t i8_smem(const I8Config& c, int p, int nk_cta, int nsb, uint32_t* tab_off, uint32_t* u_off) {
-  size_t o = 512 + (size_t)nsb * c.S * c.NT * 32;
+static size_t i8_smem(const I8Config& c, int p, int nkt, int nb, uint32_t* tab_off, uint32_t* u_off) {
+  size_t o = 512 + (size_t)nb * c.S * c.NT * 32;
   o = (o + 15) & ~(size_t)15;
   *tab_off = (uint32_t)o;
   o += (size_t)p * 8 + (c.S > 4 ? (size_t)p * 4 : 0);
   o = (o + 15) & ~(size_t)15;
   *u_off = (uint32_t)o;
-  o += (size_t)nk_cta * kI8StepTerms * 4;
+  o += (size_t)nkt * kI8StepTerms * 4;
   return o;
 }
 
 bool i8_fits(const I8Config& c, int p, int k, int smem_optin) {
   uint32_t a, b;
-  const int nks = (k + kI8StepTerms - 1) / kI8StepTerms;
-  return i8_smem(c, p, nks, 2, &a, &b) <= (size_t)smem_optin;
+  const int nkt = (k + kI8StepTerms - 1) / kI8StepTerms;
+  return i8_smem(c, p, nkt, 2, &a, &b) <= (size_t)smem_optin;
 }
 
 int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
@@ -493,7 +514,8 @@ int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
 
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st) {
   i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);
-  const int64_t total = (int64_t)n_signals * P.i8_ntiles * P.i8_nks * P.i8_NT * 8;
+  const int cols = (P.i8_ntiles - 1) * P.i8_NT + P.i8_NT_last;
+  const int64_t total = (int64_t)n_signals * cols * P.i8_nks * 8;
   DevParams Q = P;
   Q.batch = n_signals;
   if (total > 0) i8_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, K);
@@ -506,26 +528,47 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   A.n_htiles = (max_p + kI8Rows - 1) / kI8Rows;
   A.ksplit = ksplit;
   A.p_part = p_part;
-  A.npass = c.npass;
+  A.n_slots = n_signals;
   A.dbg = getenv("SFFT_I8_DBG") ? atoi(getenv("SFFT_I8_DBG")) : 0;
-  for (int i = 0; i < c.npass; ++i) A.pass[i] = c.wl[i] | (c.wh[i] << 4) | (c.nsa[i] << 8) | (c.a_base[i] << 16);
+  A.nap = getenv("SFFT_I8_NAP") ? atoi(getenv("SFFT_I8_NAP")) : 256;
+  A.gnap = getenv("SFFT_I8_GNAP") ? atoi(getenv("SFFT_I8_GNAP")) : 0;
+  static long long* prof_buf = nullptr;
+  if (getenv("SFFT_I8_PROF")) {
+    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(long long) * 148 * 2 * 5);
+    cudaMemsetAsync(prof_buf, 0, sizeof(long long) * 148 * 2 * 5, st);
+    A.prof = prof_buf;
+  }
   A.b_stage_bytes = (uint32_t)c.S * c.NT * 32;
-  const int nks = (P.i8_K + kI8StepTerms - 1) / kI8StepTerms;
-  const int nk_cta = (nks + ksplit - 1) / ksplit;
-  int nsb = 4;
+  const int nkt = (P.i8_K + kI8StepTerms - 1) / kI8StepTerms;
   size_t smem = 0;
-  for (; nsb >= 2; --nsb) {
-    smem = i8_smem(c, max_p, nk_cta, nsb, &A.tab_off, &A.u_off);
+  for (A.nb = kI8MaxSlots; A.nb >= 2; --A.nb) {
+    smem = i8_smem(c, max_p, nkt, A.nb, &A.tab_off, &A.u_off);
     if (smem <= (size_t)smem_optin) break;
   }
-  if (nsb < 2) return cudaErrorInvalidValue;
-  A.nsb = nsb;
+  if (A.nb < 2) return cudaErrorInvalidValue;
   // one CTA per SM: the kernel allocates all 512 TMEM columns
   smem = std::max(smem, (size_t)120 * 1024);
-  cudaError_t e = cudaFuncSetAttribute(expsum_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = c.S == 5 ? (A.prof ? expsum_i8_kernel<5, true> : expsum_i8_kernel<5, false>)
+                       : (A.prof ? expsum_i8_kernel<6, true> : expsum_i8_kernel<6, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  const long grid = (long)n_signals * A.n_htiles * c.ntiles * ksplit;
-  if (grid > 0) expsum_i8_kernel<<<(unsigned)grid, kI8Threads, smem, st>>>(P, A, part);
+  const long tiles = (long)n_signals * A.n_htiles * c.ntiles * ksplit;
+  int n_sm = 148;
+  cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
+  const long grid = std::min<long>(tiles, n_sm);
+  if (grid > 0) kern<<<(unsigned)grid, kI8Threads, smem, st>>>(P, A, part, (int32_t)tiles);
+  if (A.prof && grid > 0) {
+    long long h[148 * 2 * 5];
+    cudaMemcpyAsync(h, A.prof, sizeof h, cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double g[5] = {0}, m[5] = {0};
+    for (int b = 0; b < grid; ++b)
+      for (int i = 0; i < 5; ++i) { g[i] += h[b * 10 + i]; m[i] += h[b * 10 + 5 + i]; }
+    fprintf(stderr, "[i8prof] p=%d tiles=%ld grid=%ld NT=%d/%d x%d | gen: total %.0f empty-wait %.0f epilogue %.0f "
+            "table %.0f | mma: total %.0f bfull-wait %.0f afull-wait %.0f accempty %.0f (cycles per CTA), nb %d\n", max_p,
+            tiles, grid, c.NT, c.NT_last, c.ntiles, g[0] / grid, g[1] / grid, g[3] / grid, g[4] / grid, m[0] / grid,
+            m[2] / grid, m[1] / grid, m[3] / grid, A.nb);
+  }
   return cudaGetLastError();
 }
 

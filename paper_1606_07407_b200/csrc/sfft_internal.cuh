@@ -78,7 +78,7 @@ struct DevParams {
   int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
   int32_t* active;             // [batch] indices of the signals still running this iteration
   // int8-limb tensor-core exp-sum (k_expsum_i8.cu)
-  int32_t i8_S, i8_NT, i8_ntiles, i8_nks;   // limbs, output columns per tile, n-tiles, K-step capacity
+  int32_t i8_S, i8_NT, i8_NT_last, i8_ntiles, i8_nks;   // limbs, n-tile width (last tile narrower), n-tiles, K-step capacity
   int32_t i8_K;                // terms held in the B limbs (k for a solve, K for the stage entry point)
   int8_t* i8_B;                // [batch][ntiles][nks][S][NT*32] B limbs in the UMMA K-major layout
   double* i8_sigma;            // [batch] coefficient scale
@@ -86,8 +86,7 @@ struct DevParams {
 
 // int8-limb exp-sum configuration (host)
 struct I8Config {
-  int S, NT, ntiles, nks, npass;
-  int wl[4], wh[4], a_base[4], nsa[4];   // per pass: weights [wl, wh], TMEM column of A slot 0, A slots
+  int S, NT, NT_last, ntiles, nks;
 };
 
 // ---- device helpers ----------------------------------------------------------------------
