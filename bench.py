@@ -28,6 +28,16 @@ import workloads as W  # noqa: E402
 
 FP64_PEAK_TFLOPS = 37.2          # 148 SMs x 64 FP64 FMA/clk x 2 flop x 1.965 GHz
 FP64_PEAK_MEASURED = 37.1        # tools/fp64_peak.cu, DMMA m8n8k4 (profiles/r01_fp64_peak.log)
+INT8_PER_BF16 = 2.0              # B200_PROFILING.md nominal dense ratio (4.5 POPS int8 / 2.25 PFLOP/s bf16)
+
+
+def measured_peaks():
+    """MEASURED_PEAKS.json (driver-written): HBM copy GB/s and cuBLAS bf16 TFLOP/s (burst / sustained)."""
+    try:
+        d = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        return d, "MEASURED_PEAKS.json"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback (B200_PROFILING.md)"
 METRIC = "recovered modes/s (d=100, N=65536, k=1000)"
 
 
@@ -220,14 +230,48 @@ def main():
     ms_oth = sum(r.ms_other for r in reps)
     n_exp = sum(r.n_expsum for r in reps)
     launches = sum(r.kernel_launches for r in reps)
-    achieved = 8.0 * cmacs / (ms_exp / 1e3) / 1e12
-    traffic = None
+    cm8 = sum(r.cmacs_i8 for r in reps)
+    ms8 = sum(r.ms_expsum_i8 for r in reps)
+    n8 = sum(r.n_expsum_i8 for r in reps)
+    limbs = reps[0].i8_limbs if reps else 0
+    peaks, peaks_src = measured_peaks()
+    traffic, traffic_kernel = None, ""
     tf = os.path.join(ROOT, "profiles", "expsum_ncu.json")
     if os.path.exists(tf):
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch")
+            tj = json.load(open(tf))
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_kernel = tj.get("kernel", "")
         except Exception:
             traffic = None
+    if n8 and ms8 > 0:
+        # int8-limb tensor-core exp-sum: per complex MAC of the method, 4 real MACs of the 2K x 2L
+        # real GEMM times S (S + 1) / 2 limb products, 2 ops per MAC -- unpadded rows p and columns 2L
+        ops = 2.0 * 4.0 * limbs * (limbs + 1) / 2.0 * cm8
+        peak = peaks.get("bf16_tflops_sustained", 1400.0) * INT8_PER_BF16
+        achieved = ops / (ms8 / 1e3) / 1e12
+        roofline = {"bound": "tensor", "kernel": f"expsum_i8 (tcgen05.mma.kind::i8, {limbs} limbs, A in TMEM)",
+                    "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                    "traffic": traffic if traffic is not None and "i8" in traffic_kernel else None,
+                    "unit_note": "int8 tera-ops/s (MAC = 2 ops)",
+                    "peak_source": f"{peaks_src} bf16_tflops_sustained x {INT8_PER_BF16} (nominal int8:bf16 ratio, "
+                                   "B200_PROFILING.md); kernel timed inside the step",
+                    "algorithmic_ops_per_launch": ops / n8, "avg_launch_ms": ms8 / n8,
+                    "fp64_equivalent": {"achieved_tflops": 8.0 * cm8 / (ms8 / 1e3) / 1e12,
+                                        "fp64_peak_tflops": FP64_PEAK_TFLOPS,
+                                        "ratio": 8.0 * cm8 / (ms8 / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                                        "note": "8 flop per complex MAC of the exp-sum vs the FP64 pipe peak"}}
+    else:
+        achieved = 8.0 * cmacs / (ms_exp / 1e3) / 1e12
+        roofline = {"bound": "alu", "kernel": "expsum (FP64 tensor pipe: mma.sync f64 / DMMA)", "achieved": achieved,
+                    "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                    "traffic": traffic if traffic is not None and "dmma" in traffic_kernel else None,
+                    "peak_source": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz; measured DMMA 37.1, DFMA 33.6 "
+                                   "(profiles/r01_fp64_peak.log); MEASURED_PEAKS.json has no FP64 entry",
+                    "algorithmic_flops_per_launch": 8.0 * cmacs / max(n_exp, 1),
+                    "avg_launch_ms": ms_exp / max(n_exp, 1)}
+    if roofline.get("traffic") is not None:
+        roofline["traffic_note"] = "DRAM bytes of the iteration-1 launch (ncu --set full, profiles/expsum_ncu.json)"
 
     # e2e: the public host-buffer call, H2D of the inputs and D2H of the result inside the timed region
     hout = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32).pin_memory(),
@@ -272,23 +316,17 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 per PAPER.md:424 recipe; no dataset exists for this metric)",
+            "expsum_path": "int8 limbs on tcgen05" if n8 else "fp64",
             "config": {"workload": f"{cfg.name}: d={cfg.d} N={cfg.N} k={cfg.k} |a|~U[1,10], partition (2^50), "
                                    f"r={plan.r}, E=2^{int(np.log2(plan.E))}",
                        "signals_per_gpu_per_step": T, "parallelism": f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
             "sample_evals_per_s": world * samples / (ms_max / 1e3),
             "verified_exact_recovery": ok,
-            "roofline": {"bound": "alu", "kernel": "expsum (FP64 tensor pipe: mma.sync f64 / DMMA)", "achieved": achieved,
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                         "traffic": traffic,
-                         "traffic_note": "DRAM bytes of the iteration-1 launch (ncu --set full, profiles/expsum_ncu.json)",
-                         "peak_source": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz; measured DMMA 37.1, DFMA 33.6 "
-                                        "(profiles/r01_fp64_peak.log); MEASURED_PEAKS.json has no FP64 entry",
-                         "algorithmic_flops_per_launch": 8.0 * cmacs / max(n_exp, 1),
-                         "avg_launch_ms": ms_exp / max(n_exp, 1)},
+            "roofline": roofline,
             "kernel_ms_per_step": {"expsum": ms_exp / args.steps, "fft": ms_fft / args.steps,
                                    "decode": ms_dec / args.steps, "other": ms_oth / args.steps},
-            "fft_hbm": {"achieved_gbs": 32.0 * samples / (ms_fft / 1e3) / 1e9, "peak_gbs": 6549.4,
+            "fft_hbm": {"achieved_gbs": 32.0 * samples / (ms_fft / 1e3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
                         "note": "32 B per sample (read s, write F); Bluestein work is FP64-bound"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "modes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},

@@ -86,6 +86,11 @@ typedef struct {
   /* filled when sfft_options.profile = 1: device time per kernel class (CUDA events on the stream) */
   int32_t n_expsum;            /* exp-sum launches */
   float ms_expsum, ms_fft, ms_decode, ms_other;
+  /* int8-limb tensor-core exp-sum (sfft_options.expsum_path): limbs S (0 = FP64 path only), launches, their
+     complex MACs (sum over signals of L p K) and, when profiling, their device time */
+  int32_t i8_limbs, n_expsum_i8;
+  int64_t cmacs_i8;
+  float ms_expsum_i8;
 } sfft_report;
 
 typedef struct sfft_plan_s sfft_plan_t;

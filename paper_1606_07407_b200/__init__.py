@@ -52,7 +52,8 @@ class sfft_report(ctypes.Structure):
                 ("primes", ctypes.c_int64 * 64), ("accepted", ctypes.c_int32 * 64),
                 ("kernel_launches", ctypes.c_int32), ("n_expsum", ctypes.c_int32),
                 ("ms_expsum", ctypes.c_float), ("ms_fft", ctypes.c_float), ("ms_decode", ctypes.c_float),
-                ("ms_other", ctypes.c_float)]
+                ("ms_other", ctypes.c_float), ("i8_limbs", ctypes.c_int32), ("n_expsum_i8", ctypes.c_int32),
+                ("cmacs_i8", ctypes.c_int64), ("ms_expsum_i8", ctypes.c_float)]
 
 
 class SfftError(RuntimeError):

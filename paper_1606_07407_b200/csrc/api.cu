@@ -84,7 +84,7 @@ enum Buf {
   B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
-  B_WRAPS, B_I8B, B_I8SIG,
+  B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_I8TLO, B_I8THI,
   B_COUNT
 };
 
@@ -192,6 +192,9 @@ void layout(sfft_plan_t* P) {
   sz[B_WRAPS] = 4 * S * ((size_t)P->k + 1);
   sz[B_I8B] = P->i8_ok ? i8_limb_bytes(P->i8, (int)S) : 0;
   sz[B_I8SIG] = 8 * S;
+  sz[B_CMACS8] = 8 * S;
+  sz[B_I8TLO] = P->i8_ok ? 8 * S * (P->p_stride + 8) : 0;
+  sz[B_I8THI] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -255,6 +258,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_iters = ptr<int32_t>(P, B_ITERS);
   D.st_samples = ptr<int64_t>(P, B_SAMPLES);
   D.st_cmacs = ptr<int64_t>(P, B_CMACS);
+  D.st_cmacs_i8 = ptr<int64_t>(P, B_CMACS8);
   D.st_log = ptr<int32_t>(P, B_LOG);
   D.ctrl = ptr<int32_t>(P, B_CTRL);
   D.active = ptr<int32_t>(P, B_ACTIVE);
@@ -263,6 +267,9 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_K = P->k;
     D.i8_B = ptr<int8_t>(P, B_I8B);
     D.i8_sigma = ptr<double>(P, B_I8SIG);
+    D.i8_tlo = ptr<uint2>(P, B_I8TLO);
+    D.i8_thi = ptr<uint32_t>(P, B_I8THI);
+    D.i8_tstride = P->p_stride + 8;
   }
   return D;
 }
@@ -622,8 +629,8 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     launches += 1;   // sigma + limbs
   }
   int iter = 1;
-  int32_t last_iter = 0, n_expsum = 0;
-  std::vector<size_t> it_marks;
+  int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
+  std::vector<size_t> it_marks, it_i8;
   for (; iter <= P->max_iter; ++iter) {
     LAUNCH(P, launch_setup(D, iter, st));
     CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
@@ -669,7 +676,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, ksplit,
                           ptr<double2>(P, B_PART), max_p, st));
     mark();
+    D.i8_iter = use_i8 ? 1 : 0;
     LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
+    D.i8_iter = 0;
+    if (use_i8) { ++n_expsum_i8; it_i8.push_back(it_marks.empty() ? 0 : it_marks.back()); }
     mark();
     last_iter = iter;
   }
@@ -680,11 +690,12 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   // report
   std::vector<int32_t> hs(batch);
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-  std::vector<int64_t> hsamp(batch), hcm(batch);
+  std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
   std::vector<int32_t> hlog(2 * kLogIters);
   if (rep) {
     CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
   }
   CUDA_TRY(P, cudaStreamSynchronize(st));
@@ -697,7 +708,9 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   }
   if (rep) {
     memset(rep, 0, sizeof *rep);
-    for (int s = 0; s < batch; ++s) { rep->samples_used += hsamp[s]; rep->cmacs += hcm[s]; }
+    for (int s = 0; s < batch; ++s) { rep->samples_used += hsamp[s]; rep->cmacs += hcm[s]; rep->cmacs_i8 += hcm8[s]; }
+    rep->i8_limbs = P->i8_ok ? P->i8.S : 0;
+    rep->n_expsum_i8 = n_expsum_i8;
     rep->iterations = last_iter;
     rep->n_ok = n_ok; rep->n_partial = n_part; rep->n_error = n_err;
     rep->status = worst;
@@ -729,6 +742,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
         fd += el(m0 + 3, m0 + 4);
       }
       rep->ms_expsum = fx;
+      for (size_t m0 : it_i8) rep->ms_expsum_i8 += el(m0 + 1, m0 + 2);
       rep->ms_fft = ff;
       rep->ms_decode = fd;
       rep->ms_other = tot - fx - ff - fd;

@@ -439,6 +439,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     P.st_stall[s] = stall;
     P.st_samples[s] += (int64_t)P.L * p;
     P.st_cmacs[s] += (int64_t)P.L * p * K;
+    if (P.i8_iter) P.st_cmacs_i8[s] += (int64_t)P.L * p * K;
     P.st_iters[s] = iter;
     if (s == 0 && iter <= kLogIters) {
       P.st_log[2 * (iter - 1)] = p;

@@ -69,14 +69,6 @@ __global__ void i8_sigma_kernel(DevParams P, int32_t K) {
   }
 }
 
-// balanced base-256 digits of X (|X| <= 127 * 256^(S-1)), most significant first
-__device__ __forceinline__ void digits(int64_t X, int S, int (&d)[8]) {
-  for (int t = S - 1; t >= 0; --t) {
-    const int64_t r = ((X + 128) & 255) - 128;
-    d[t] = (int)r;
-    X = (X - r) >> 8;
-  }
-}
 
 __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT, int NT_last) {
   return nt == ntiles - 1 ? NT_last : NT;
@@ -88,16 +80,17 @@ __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT
 // One thread per (signal, padded output column, K step, 4-byte K word): S words, one per limb.
 __global__ void i8_limbs_kernel(DevParams P, int32_t K) {
   const int NT = P.i8_NT, S = P.i8_S, ntiles = P.i8_ntiles, nks = P.i8_nks;
+  const int nkt = (K + kI8StepTerms - 1) / kI8StepTerms;        // steps in use (layout stride stays nks)
   const int cols = (ntiles - 1) * NT + P.i8_NT_last;
-  const int64_t per_sig = (int64_t)cols * nks * 8;
+  const int64_t per_sig = (int64_t)cols * nkt * 8;
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (int64_t)P.batch * per_sig) return;
   const int s = (int)(g / per_sig);
   int64_t r = g % per_sig;
   const int kw = (int)(r & 7);
   r >>= 3;
-  const int ks = (int)(r % nks);
-  const int gc = (int)(r / nks);                                 // padded output column
+  const int ks = (int)(r % nkt);
+  const int gc = (int)(r / nkt);                                 // padded output column
   const int nt = gc / NT, col = gc % NT;
   const int W = i8_tile_width(nt, ntiles, NT, P.i8_NT_last);
   const int n = gc >> 1, im_out = gc & 1;
@@ -113,7 +106,7 @@ __global__ void i8_limbs_kernel(DevParams P, int32_t K) {
       const bool a_im = kp & 1;                                   // row 2j+1 multiplies Im W
       v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
     }
-    digits(llrint(v * q), S, dg[b]);
+    i8_digits(llrint(v * q), S, dg[b]);
   }
   int8_t* base = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)nt * nks * S * NT * 32 + (int64_t)ks * S * W * 32;
   const int off = (col >> 3) * 256 + (kw >> 2) * 128 + (col & 7) * 16 + (kw & 3) * 4;
@@ -136,7 +129,8 @@ struct I8Args {
   int32_t nap;                // producer back-off (ns) while the B ring is full
   int32_t gnap;               // generator back-off (ns) while waiting for a free A slot (0: spin)
   uint32_t b_stage_bytes;     // S * NT * 32
-  uint32_t tab_off, u_off;    // smem offsets of the limb tables and the u list
+  uint32_t tab_off, thi_off, u_off;   // smem offsets of the limb tables and the phase list
+  int32_t chunk;              // consecutive tiles per CTA visit
   long long* prof;            // tuning only (SFFT_I8_PROF): per-CTA cycle counters
   int32_t dbg;                // tuning only (SFFT_I8_DBG): 1 conflict-free gathers, 2 no MMAs, 3 no A generation
 };
@@ -144,13 +138,13 @@ struct I8Args {
 // 8 terms (4 TMEM columns per limb) of one K step for this thread's row h: gather the root limbs and pack
 // them into the TMEM word layout (4 K bytes per 32-bit column: re_j, im_j, re_j+1, im_j+1)
 template <int NL>
-__device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int* __restrict__ sU,
+__device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int2* __restrict__ sU,
                                           const uint2* __restrict__ sTlo, const uint32_t* __restrict__ sThi, unsigned h,
                                           unsigned magic, int p, int dbg) {
   unsigned q[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const unsigned x = h * (unsigned)sU[e];
+    const unsigned x = h * (unsigned)sU[e].x;
     int r = (int)(x - __umulhi(x, magic) * (unsigned)p);
     r += (r >> 31) & p;
     q[e] = dbg == 1 ? (h + e) : (unsigned)r;
@@ -224,17 +218,17 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   uint64_t* bempty = bfull + kI8MaxSlots;
   uint64_t* accfull = bempty + kI8MaxSlots;
   uint64_t* accempty = accfull + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(accempty + 1);
+  uint64_t* tabbar = accempty + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tabbar + 1);
   unsigned char* sB = smem_raw + 512;
   uint2* sTlo = reinterpret_cast<uint2*>(smem_raw + A.tab_off);
-  int* sU = reinterpret_cast<int*>(smem_raw + A.u_off);
+  const uint32_t* sThi = reinterpret_cast<const uint32_t*>(smem_raw + A.thi_off);
+  int2* sU = reinterpret_cast<int2*>(smem_raw + A.u_off);
   const int NT = P.i8_NT, ntiles = P.i8_ntiles, nks = P.i8_nks;
   const int cols = (ntiles - 1) * NT + P.i8_NT_last;
   const int K = P.i8_K;                                             // terms in the B limbs (bin-domain: k)
   const int nkt = (K + kI8StepTerms - 1) / kI8StepTerms;             // K steps in use
   const int per = (nkt + A.ksplit - 1) / A.ksplit;
-  const int t_lo = (int)((int64_t)blockIdx.x * n_tiles / gridDim.x);
-  const int t_hi = (int)((int64_t)(blockIdx.x + 1) * n_tiles / gridDim.x);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (warp == kI8MmaWarp) tc::tmem_alloc<512>(tslot);
@@ -247,6 +241,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
     }
     tc::mbar_init(accfull, 1);
     tc::mbar_init(accempty, kI8GenWarps);
+    tc::mbar_init(tabbar, 1);
     tc::fence_mbar_init();
   }
   tc::fence_before_sync();
@@ -258,9 +253,16 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   int bpos = 0;                         // B ring position (producer / MMA)
   int ntile_done = 0;                   // accfull / accempty parity
   int cur_s = -1;
+  uint32_t tabphase = 0;
   long long pr_a = 0, pr_b = 0, pr_e = 0, pr_t = 0;
   const long long pr_start = clock64();
-  for (int t = t_lo; t < t_hi; ++t) {
+  // chunks of A.chunk consecutive tiles (same signal, mostly) dealt round robin: the CTAs sweep the signals
+  // together, so the B limbs of the few signals in flight stay in L2 while each CTA reuses its table
+  const int n_chunks = (n_tiles + A.chunk - 1) / A.chunk;
+  for (int t = 0, q = blockIdx.x, tq = 0; q < n_chunks; ) {
+    t = q * A.chunk + tq;
+    if (++tq == A.chunk || t + 1 >= n_tiles) { tq = 0; q += gridDim.x; }
+    if (t >= n_tiles) continue;
     const I8Tile tl = tile_of(t, A, ntiles);
     const int s = P.active[tl.slot];
     const int p = P.st_p[s];
@@ -270,37 +272,22 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
     if (nk == 0) continue;
     const int W = i8_tile_width(tl.nt, ntiles, NT, P.i8_NT_last);
     const int nsl = ring_slots(W, S);
-    uint32_t* sThi = reinterpret_cast<uint32_t*>(sTlo + p);
     if (s != cur_s) {
       const long long ct0 = PROF ? clock64() : 0;
-      // root limb table of this signal's prime (W_tab from the prep kernel) and all its phase indices u_j
+      // root limb table of this signal's prime (written by the prep kernel) and its phase indices u_j: three
+      // bulk copies once every warp is done with the previous signal's table
       __syncthreads();
-      const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
-      const double qa = 127.0 * ldexp(1.0, 8 * (S - 1));
-      for (int q0 = 0; q0 < p; q0 += 4 * kI8Threads) {
-        double2 wv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int q = q0 + u * kI8Threads + tid;
-          wv[u] = q < p ? Wg[q] : make_double2(0.0, 0.0);
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int q = q0 + u * kI8Threads + tid;
-          if (q >= p) break;
-          int dr[8], di[8];
-          digits(llrint(wv[u].x * qa), S, dr);
-          digits(llrint(wv[u].y * qa), S, di);
-          uint32_t e[6];
-#pragma unroll
-          for (int i = 0; i < 6; ++i) e[i] = i < S ? ((uint32_t)(uint8_t)dr[i] | ((uint32_t)(uint8_t)di[i] << 8)) : 0u;
-          sTlo[q] = make_uint2(e[0] | (e[1] << 16), e[2] | (e[3] << 16));
-          if (S > 4) sThi[q] = e[4] | (e[5] << 16);
-        }
+      if (tid == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t blo = ((uint32_t)p * 8 + 15) & ~15u, bhi = S > 4 ? (((uint32_t)p * 4 + 15) & ~15u) : 0u;
+        const uint32_t bu = ((uint32_t)min(nkt * kI8StepTerms, P.kk) * 8 + 15) & ~15u;
+        tc::mbar_expect_tx(tabbar, blo + bhi + bu);
+        tc::bulk_g2s(sTlo, P.i8_tlo + (int64_t)s * P.i8_tstride, blo, tabbar);
+        if (bhi) tc::bulk_g2s(smem_raw + A.thi_off, P.i8_thi + (int64_t)s * P.i8_tstride, bhi, tabbar);
+        tc::bulk_g2s(sU, P.u_all + (int64_t)s * P.kk, bu, tabbar);
       }
-      const int2* ug = P.u_all + (int64_t)s * P.kk;
-      for (int i = tid; i < nkt * kI8StepTerms; i += kI8Threads) sU[i] = i < K ? ug[i].x : 0;
-      __syncthreads();
+      tc::mbar_wait(tabbar, tabphase);
+      tabphase ^= 1;
       cur_s = s;
       if (PROF) pr_t += clock64() - ct0;
     }
@@ -316,7 +303,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       // software pipeline: the limbs of step kq + 1 are gathered while the tensor core works on step kq and
       // before the slot they go to is free; only the TMEM store + arrive sit on the critical path
       uint32_t w[S][4];
-      const int* ub = sU + ks_lo * kI8StepTerms + 8 * half;
+      const int2* ub = sU + ks_lo * kI8StepTerms + 8 * half;
       if (A.dbg != 3) gen_limbs<S>(w, ub, sTlo, sThi, h, magic, p, A.dbg);
       int sl = 0;
       for (int kq = 0; kq < nk; ++kq, sl = (sl + 1 == nsl ? 0 : sl + 1)) {
@@ -491,21 +478,23 @@ size_t i8_limb_bytes(const I8Config& c, int batch) {
   return (size_t)batch * c.nks * c.S * 32 * (size_t)cols;
 }
 
-static size_t i8_smem(const I8Config& c, int p, int nkt, int nb, uint32_t* tab_off, uint32_t* u_off) {
+static size_t i8_smem(const I8Config& c, int p, int nkt, int nb, uint32_t* tab_off, uint32_t* thi_off,
+                      uint32_t* u_off) {
   size_t o = 512 + (size_t)nb * c.S * c.NT * 32;
   o = (o + 15) & ~(size_t)15;
   *tab_off = (uint32_t)o;
-  o += (size_t)p * 8 + (c.S > 4 ? (size_t)p * 4 : 0);
-  o = (o + 15) & ~(size_t)15;
+  o += ((size_t)p * 8 + 15) & ~(size_t)15;
+  *thi_off = (uint32_t)o;
+  o += c.S > 4 ? (((size_t)p * 4 + 15) & ~(size_t)15) : 0;
   *u_off = (uint32_t)o;
-  o += (size_t)nkt * kI8StepTerms * 4;
+  o += (size_t)nkt * kI8StepTerms * 8 + 16;
   return o;
 }
 
 bool i8_fits(const I8Config& c, int p, int k, int smem_optin) {
-  uint32_t a, b;
+  uint32_t a, b, d;
   const int nkt = (k + kI8StepTerms - 1) / kI8StepTerms;
-  return i8_smem(c, p, nkt, 2, &a, &b) <= (size_t)smem_optin;
+  return i8_smem(c, p, nkt, 2, &a, &b, &d) <= (size_t)smem_optin;
 }
 
 int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
@@ -515,7 +504,7 @@ int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st) {
   i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);
   const int cols = (P.i8_ntiles - 1) * P.i8_NT + P.i8_NT_last;
-  const int64_t total = (int64_t)n_signals * cols * P.i8_nks * 8;
+  const int64_t total = (int64_t)n_signals * cols * ((K + kI8StepTerms - 1) / kI8StepTerms) * 8;
   DevParams Q = P;
   Q.batch = n_signals;
   if (total > 0) i8_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, K);
@@ -542,7 +531,7 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   const int nkt = (P.i8_K + kI8StepTerms - 1) / kI8StepTerms;
   size_t smem = 0;
   for (A.nb = kI8MaxSlots; A.nb >= 2; --A.nb) {
-    smem = i8_smem(c, max_p, nkt, A.nb, &A.tab_off, &A.u_off);
+    smem = i8_smem(c, max_p, nkt, A.nb, &A.tab_off, &A.thi_off, &A.u_off);
     if (smem <= (size_t)smem_optin) break;
   }
   if (A.nb < 2) return cudaErrorInvalidValue;
@@ -555,7 +544,8 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   const long tiles = (long)n_signals * A.n_htiles * c.ntiles * ksplit;
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-  const long grid = std::min<long>(tiles, n_sm);
+  A.chunk = getenv("SFFT_I8_CHUNK") ? std::max(1, atoi(getenv("SFFT_I8_CHUNK"))) : 4;
+  const long grid = std::min<long>((tiles + A.chunk - 1) / A.chunk, n_sm);
   if (grid > 0) kern<<<(unsigned)grid, kI8Threads, smem, st>>>(P, A, part, (int32_t)tiles);
   if (A.prof && grid > 0) {
     long long h[148 * 2 * 5];

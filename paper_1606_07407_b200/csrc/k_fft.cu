@@ -383,6 +383,13 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(
     double sn, cs;
     sincospi(2.0 * (double)q / (double)p, &sn, &cs);   // e^{+2 pi i q/p}
     W[q] = make_double2(cs, sn);
+    if (P.i8_S > 0) {                                      // root limb table of the int8-limb exp-sum
+      uint2 lo;
+      uint32_t hi;
+      i8_root_entry(cs, sn, P.i8_S, lo, hi);
+      P.i8_tlo[(int64_t)s * P.i8_tstride + q] = lo;
+      P.i8_thi[(int64_t)s * P.i8_tstride + q] = hi;
+    }
     const double2 w = chirp_value(q, p);
     ch[q] = w;
     const double2 vq = make_double2(w.x, -w.y);        // conj(w[q]) = kernel value at +-q

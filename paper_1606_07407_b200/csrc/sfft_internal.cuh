@@ -74,6 +74,8 @@ struct DevParams {
   int32_t* st_iters;           // [batch]
   int64_t* st_samples;         // [batch]
   int64_t* st_cmacs;           // [batch]
+  int64_t* st_cmacs_i8;        // [batch] cMACs of the iterations whose exp-sum ran on the int8-limb kernel
+  int32_t i8_iter;             // decode launch: this iteration's exp-sum used the int8-limb kernel
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
   int32_t* active;             // [batch] indices of the signals still running this iteration
@@ -82,7 +84,31 @@ struct DevParams {
   int32_t i8_K;                // terms held in the B limbs (k for a solve, K for the stage entry point)
   int8_t* i8_B;                // [batch][ntiles][nks][S][NT*32] B limbs in the UMMA K-major layout
   double* i8_sigma;            // [batch] coefficient scale
+  uint2* i8_tlo;               // [batch][i8_tstride] root limbs 0..3 of W_p[q] (16 bit each: re | im << 8)
+  uint32_t* i8_thi;            // [batch][i8_tstride] root limbs 4..5
+  int64_t i8_tstride;          // >= p_stride + 8 (bulk copies round the table up to 16 bytes)
 };
+
+// balanced base-256 digits of X (|X| <= 127 * 256^(S-1)), most significant first (k_expsum_i8.cu, k_fft.cu)
+__device__ __forceinline__ void i8_digits(int64_t X, int S, int (&d)[8]) {
+  for (int t = S - 1; t >= 0; --t) {
+    const int64_t r = ((X + 128) & 255) - 128;
+    d[t] = (int)r;
+    X = (X - r) >> 8;
+  }
+}
+// limb-table entry of the root (c, s) = e^{2 pi i q / p}: limb t of (re, im) as the 16-bit word re_t | im_t << 8
+__device__ __forceinline__ void i8_root_entry(double c, double s, int S, uint2& lo, uint32_t& hi) {
+  const double qa = 127.0 * ldexp(1.0, 8 * (S - 1));
+  int dr[8], di[8];
+  i8_digits(llrint(c * qa), S, dr);
+  i8_digits(llrint(s * qa), S, di);
+  uint32_t e[6];
+#pragma unroll
+  for (int i = 0; i < 6; ++i) e[i] = i < S ? ((uint32_t)(uint8_t)dr[i] | ((uint32_t)(uint8_t)di[i] << 8)) : 0u;
+  lo = make_uint2(e[0] | (e[1] << 16), e[2] | (e[3] << 16));
+  hi = e[4] | (e[5] << 16);
+}
 
 // int8-limb exp-sum configuration (host)
 struct I8Config {

@@ -9,6 +9,6 @@ if [ -n "$NCU" ]; then
   timeout 300 $CMD > gpurun_out/plain_${TAG}.log 2>&1 && \
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${TAG}.csv $CMD > gpurun_out/ncu_launches_${TAG}.log 2>&1
   echo "launches rc=$?"
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:expsum -s 0 -c 1 -o gpurun_out/expsum_${TAG} $CMD > gpurun_out/ncu_full_${TAG}.log 2>&1
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:${KREGEX:-expsum_i8} -s 0 -c 1 -o gpurun_out/expsum_${TAG} $CMD > gpurun_out/ncu_full_${TAG}.log 2>&1
   echo "full rc=$?"
 fi
