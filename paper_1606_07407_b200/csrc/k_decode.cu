@@ -240,57 +240,56 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     nc = total;
   }
 
-  // ---- 2. collision test + decode, one warp per candidate ----
+  // ---- 2. collision test + decode, flat over (candidate, shifted line) pairs ----
+  // Every pair is independent: thread t takes pairs t, t + blockDim, ... (4 in flight for latency hiding);
+  // a pair failing Eq. (42) or the rounding / range checks clears its candidate's flag (benign race: all
+  // writers store 0).  The decisions are those of a per-candidate loop: ok = AND over n of the same
+  // per-line tests.
   int64_t* accv = P.acc_v + (int64_t)s * r * P.k;       // [r][k], column = candidate index
   const double twopi = 6.283185307179586476925286766559;
-  for (int ci = warp; ci < nc; ci += nwarps) {
-    const int b = cand[ci];
-    const double2 f0 = F[b];
-    const double mag0 = hypot(f0.x, f0.y);
-    bool ok = true;
-    for (int n0 = 0; n0 < r; n0 += 128) {
-      // up to 4 shifted-line bins per lane, loaded once for both the test and the decode
-      double2 fv[4];
+  for (int ci = tid; ci < nc; ci += blockDim.x) flag[ci] = 1;
+  __syncthreads();
+  {
+    const int tot = nc * r;
+    for (int t0 = tid; t0 < tot; t0 += 4 * blockDim.x) {
+      double2 fv[4], f0[4];
+      int ci[4], n[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int n = n0 + lane + 32 * i;
-        fv[i] = n < r ? F[(int64_t)(1 + n) * P.p_stride + b] : make_double2(0.0, 0.0);
+      for (int u = 0; u < 4; ++u) {
+        const int t = t0 + u * blockDim.x;
+        ci[u] = t < tot ? t / r : 0;
+        n[u] = t < tot ? t - ci[u] * r : -1;
+        const int b = cand[ci[u]];
+        f0[u] = F[b];
+        fv[u] = n[u] >= 0 ? F[(int64_t)(1 + n[u]) * P.p_stride + b] : make_double2(0.0, 0.0);
       }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int n = n0 + lane + 32 * i;
-        if (n < r) {
-          const double rho = hypot(fv[i].x, fv[i].y) / mag0;     // Eq. (42)
-          ok = ok && (fabs(rho - 1.0) < P.tol);
-        }
-      }
-      if (!__all_sync(0xffffffffu, ok)) { ok = false; break; }
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int n = n0 + lane + 32 * i;
-        if (n < r) {
+      for (int u = 0; u < 4; ++u) {
+        if (n[u] < 0) continue;
+        const double mag0 = hypot(f0[u].x, f0[u].y);
+        const double rho = hypot(fv[u].x, fv[u].y) / mag0;      // Eq. (42)
+        bool good = fabs(rho - 1.0) < P.tol;
+        if (good) {
           // q = F_n conj(F_0), written without contraction to mirror the plain formula
-          const double qr = __dadd_rn(__dmul_rn(fv[i].x, f0.x), __dmul_rn(fv[i].y, f0.y));
-          const double qi = __dsub_rn(__dmul_rn(fv[i].y, f0.x), __dmul_rn(fv[i].x, f0.y));
+          const double qr = __dadd_rn(__dmul_rn(fv[u].x, f0[u].x), __dmul_rn(fv[u].y, f0[u].y));
+          const double qi = __dsub_rn(__dmul_rn(fv[u].y, f0[u].x), __dmul_rn(fv[u].x, f0[u].y));
           const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)P.E), twopi);   // Eq. (41)
           const double xr = rint(x);
-          bool good = fabs(x - xr) <= P.round_tol;
+          good = fabs(x - xr) <= P.round_tol;
           const int64_t v = (int64_t)xr;
-          if (P.extra & 1) good = good && v >= P.lo[n] && v <= P.hi[n];
-          ok = ok && good;
-          accv[(int64_t)n * P.k + ci] = v;
+          if (P.extra & 1) good = good && v >= P.lo[n[u]] && v <= P.hi[n[u]];
+          accv[(int64_t)n[u] * P.k + ci[u]] = v;
         }
+        if (!good) flag[ci[u]] = 0;
       }
-      if (!__all_sync(0xffffffffu, ok)) { ok = false; break; }
     }
-    if (ok && (P.extra & 2)) {
-      __syncwarp();
-      const int64_t vm = accv[(int64_t)m * P.k + ci];
-      ok = mod_pos64(vm, p) == b;
-    }
-    if (lane == 0) flag[ci] = ok;
   }
   __syncthreads();
+  if (P.extra & 2) {
+    for (int ci = tid; ci < nc; ci += blockDim.x)
+      if (flag[ci] && mod_pos64(accv[(int64_t)m * P.k + ci], p) != cand[ci]) flag[ci] = 0;
+    __syncthreads();
+  }
 
   // ---- 3. accepted list in ascending b ----
   {

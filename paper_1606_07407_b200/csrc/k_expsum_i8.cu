@@ -49,15 +49,15 @@ constexpr int kI8Rows = 128;          // MMA M
 constexpr int kI8StepTerms = 16;      // terms per K step (32 int8 K elements: re and im)
 
 // ------------------------------------------------------------------ B limbs (once per solve)
-// sigma[s] = max over terms j < K and lines n < L of max(|Re C|, |Im C|)
+// sigma[s] >= every |Re C[j][n]|, |Im C[j][n]|: the line factors have unit modulus, so |C[j][n]| = |C[j][0]|
+// up to a few ulp; sigma = (1 + 1e-12) max_j |C[j][0]| (column 0 is the unshifted line, C[j][0] = a_j)
 __global__ void i8_sigma_kernel(DevParams P, int32_t K) {
   const int s = blockIdx.x;
   const double2* Cs = P.C_all + (int64_t)s * P.kk * P.Lp;
   double m = 0.0;
-  for (int64_t e = threadIdx.x; e < (int64_t)K * P.L; e += blockDim.x) {
-    const int j = (int)(e / P.L), n = (int)(e % P.L);
-    const double2 c = Cs[(int64_t)j * P.Lp + n];
-    m = fmax(m, fmax(fabs(c.x), fabs(c.y)));
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const double2 c = Cs[(int64_t)j * P.Lp];
+    m = fmax(m, hypot(c.x, c.y));
   }
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   __shared__ double red[32];
@@ -65,10 +65,9 @@ __global__ void i8_sigma_kernel(DevParams P, int32_t K) {
   __syncthreads();
   if (threadIdx.x == 0) {
     for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
-    P.i8_sigma[s] = m > 0.0 ? m : 1.0;
+    P.i8_sigma[s] = m > 0.0 ? m * (1.0 + 1e-12) : 1.0;
   }
 }
-
 
 __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT, int NT_last) {
   return nt == ntiles - 1 ? NT_last : NT;
