@@ -48,6 +48,7 @@ class _Params(ctypes.Structure):
         ("max_iter", ctypes.c_int32), ("stall_limit", ctypes.c_int32),
         ("extra_checks", ctypes.c_int32),
         ("n_primes", ctypes.c_int32), ("primes", ctypes.POINTER(ctypes.c_int64)),
+        ("n_fallback", ctypes.c_int32),
     ]
 
 
@@ -76,6 +77,8 @@ def lib():
         L.oracle_decode.argtypes = [ctypes.POINTER(_Params), i64, vp, vp, i64, i32, i32, vp, vp, vp,
                                     vp, vp]
         L.oracle_decode.restype = i32
+        L.oracle_fallback_tilts.argtypes = [i32, i32, vp]
+        L.oracle_fallback_tilts.restype = i32
         L.oracle_solve.argtypes = [ctypes.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, i32, vp]
         L.oracle_solve_batch.argtypes = [ctypes.POINTER(_Params), i32, vp, vp, vp, vp, vp, vp, vp,
                                          vp, i32]
@@ -106,6 +109,7 @@ class Params:
     stall_limit: int = 0
     extra_checks: int = 3
     primes: Optional[Sequence[int]] = None
+    n_fallback: int = 0
     _keep: list = field(default_factory=list, repr=False)
 
     def c_struct(self) -> _Params:
@@ -126,6 +130,7 @@ class Params:
         s.max_iter, s.stall_limit, s.extra_checks = self.max_iter, self.stall_limit, self.extra_checks
         s.n_primes = 0 if primes is None else primes.size
         s.primes = None if primes is None else primes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
+        s.n_fallback = self.n_fallback
         return s
 
     @property
@@ -191,6 +196,13 @@ def ith_prime_at_least(x: int, i: int = 1) -> int:
 
 
 # ---------------------------------------------------------------- plan quantities
+def fallback_tilts(r: int, level: int):
+    """Tilts of stall-fallback level `level` >= 1 (reading R23): list of (axis0, axis1, base, height, hypo)."""
+    out = np.zeros((max(r // 2, 1), 5), np.int64)
+    n = lib().oracle_fallback_tilts(r, level, _p(out))
+    return [tuple(int(x) for x in row) for row in out[:n]]
+
+
 def prepare(P: Params) -> Tuple[int, np.ndarray, np.ndarray]:
     """(E, lo[r], hi[r]) or raises with the status code."""
     lo, hi = np.zeros(P.r, np.int64), np.zeros(P.r, np.int64)

@@ -408,6 +408,63 @@ static int row_cmp(const void* x, const void* y) {
   return 0;
 }
 
+/* ------------------------------------------------------------------------ */
+/* stall fallback ("apply the tilting method with several angles until */
+/* all k frequency pairs are found", Algorithm 3; reading R23)      */
+/* ------------------------------------------------------------------------ */
+
+static const int64_t kFallbackTriples[4][3] = {{3, 4, 5}, {5, 12, 13}, {8, 15, 17}, {7, 24, 25}};
+
+int32_t oracle_fallback_tilts(int32_t r, int32_t lvl, int64_t* out) {
+  if (lvl < 1 || lvl > 4) return 0;
+  const int64_t* T = kFallbackTriples[lvl - 1];
+  /* disjoint pairs (q, q + s): level 1 s = 1 from axis 0, level 2 s = 1 from axis 1 (r >= 3), level 3 s = 2,
+   * level 4 s = 3 -- for r <= 4 every axis pair is tilted at some level ("randomizing the order
+   * of the dimensions" in a fixed, reproducible form) */
+  const int32_t s = lvl <= 2 ? 1 : lvl - 1;
+  const int32_t off = (lvl == 2 && r >= 3) ? 1 : 0;
+  int32_t n = 0;
+  for (int32_t b = off; b < r; b += 2 * s)
+    for (int32_t i = 0; i < s && b + i + s < r; ++i, ++n) {
+      int64_t* o = out + 5 * n;
+      o[0] = b + i; o[1] = b + i + s; o[2] = T[0]; o[3] = T[1]; o[4] = T[2];   /* base, height, hypo */
+    }
+  return n;
+}
+
+/* one level of the schedule: level 0 = the caller's own tilts and E, level >= 1 = fallback tilts with the
+ * default E of that tilt (2 B (base + height), reading R2) */
+static int level_params(const oracle_params* P, int32_t lvl, oracle_params* out, int64_t* tbuf) {
+  *out = *P;
+  if (lvl == 0) return 1;
+  out->n_tilts = oracle_fallback_tilts(P->r, lvl, tbuf);
+  out->tilts = tbuf;
+  out->E = 0;
+  return out->n_tilts > 0;
+}
+
+/* untilt v (level tilts, last pair first as in the final wrap); 0 on success, -1 if not integral */
+static int untilt_all(const oracle_params* L, int64_t* u) {
+  for (int32_t t = L->n_tilts - 1; t >= 0; --t) {
+    const int64_t* T = L->tilts + 5 * t;
+    int64_t out[2];
+    if (oracle_untilt_freq(T[2], T[3], T[4], u[T[0]], u[T[1]], out)) return -1;
+    u[T[0]] = out[0];
+    u[T[1]] = out[1];
+  }
+  return 0;
+}
+
+static void tilt_all(const oracle_params* L, int64_t* u) {
+  for (int32_t t = 0; t < L->n_tilts; ++t) {
+    const int64_t* T = L->tilts + 5 * t;
+    int64_t out[2];
+    oracle_tilt_freq(T[2], T[3], u[T[0]], u[T[1]], out);
+    u[T[0]] = out[0];
+    u[T[1]] = out[1];
+  }
+}
+
 int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int32_t* out_w,
                  double* out_a, int32_t* out_count, int64_t* out_samples, int32_t* out_iters,
                  int32_t trace_cap, int64_t* trace) {
@@ -415,14 +472,19 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
   int64_t E;
   int64_t* lo = (int64_t*)malloc(sizeof(int64_t) * (size_t)r);
   int64_t* hi = (int64_t*)malloc(sizeof(int64_t) * (size_t)r);
-  int rc = oracle_prepare(P, &E, lo, hi);
-  if (rc) { free(lo); free(hi); return rc; }
+  /* level 0 = the caller's plan; a stall moves to the next fallback level (reading R23) */
+  int64_t* tbuf = (int64_t*)malloc(sizeof(int64_t) * 5 * (size_t)(r / 2 + 1));
+  oracle_params Lv;
+  int32_t lvl = 0;
+  level_params(P, 0, &Lv, tbuf);
+  int rc = oracle_prepare(&Lv, &E, lo, hi);
+  if (rc) { free(lo); free(hi); free(tbuf); return rc; }
   const int32_t stall_limit = P->stall_limit > 0 ? P->stall_limit : (2 * r > 16 ? 2 * r : 16);
 
   /* the signal: reduced frequencies of its modes (only used to evaluate f, Eq. (38)) */
   int64_t* vf = (int64_t*)malloc(sizeof(int64_t) * (size_t)k * r);
-  rc = oracle_project(P, w, k, vf);
-  if (rc) { free(lo); free(hi); free(vf); return rc; }
+  rc = oracle_project(&Lv, w, k, vf);
+  if (rc) { free(lo); free(hi); free(vf); free(tbuf); return rc; }
 
   registry_t R;
   R.n = 0; R.cap = k; R.r = r;
@@ -439,8 +501,8 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
   int64_t Fcap = 0;
 
   int64_t samples = 0;
-  int32_t i = 1, stall = 0, status = ORACLE_PARTIAL;
-  while (R.n < k && i <= P->max_iter) {                        /* Alg. 2 l.6 */
+  int32_t i = 1, it = 1, stall = 0, status = ORACLE_PARTIAL;   /* i: Alg. 2/3 counter of the level, it: total */
+  while (R.n < k && it <= P->max_iter) {                        /* Alg. 2 l.6 */
     int32_t kstar = k - R.n;                                  /* l.7 */
     int64_t p = (P->n_primes > 0 && P->primes)
                     ? P->primes[(i - 1) % P->n_primes]
@@ -503,13 +565,50 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
       ++keep;
     }
     R.n = keep;
-    if (trace && i <= trace_cap) {
-      int64_t* T = trace + (size_t)(i - 1) * 5;
-      T[0] = i; T[1] = p; T[2] = m; T[3] = ncand; T[4] = na;
+    if (trace && it <= trace_cap) {
+      int64_t* T = trace + (size_t)(it - 1) * 5;
+      T[0] = it; T[1] = p; T[2] = m; T[3] = ncand; T[4] = na;
     }
     stall = (na == 0) ? stall + 1 : 0;
     ++i;                                                        /* l.34 */
-    if (stall >= stall_limit) break;                            /* C19: fallback is NEXT */
+    ++it;
+    if (stall >= stall_limit && R.n < k) {
+      /* C19 / R23: no progress for stall_limit iterations -> the next tilt of the schedule (Alg. 3), keeping
+       * what was found: every entry is mapped to the new coordinates exactly (untilt, which must be
+       * integral, then tilt); entries that do not untilt exactly are dropped */
+      oracle_params Ln;
+      int64_t* tn = (int64_t*)malloc(sizeof(int64_t) * 5 * (size_t)(r / 2 + 1));
+      int64_t En;
+      if (lvl + 1 > P->n_fallback || lvl + 1 > 4 || !level_params(P, lvl + 1, &Ln, tn) ||
+          oracle_prepare(&Ln, &En, lo, hi) != ORACLE_OK) {
+        free(tn);
+        break;
+      }
+      int32_t keep = 0;
+      int64_t* u = (int64_t*)malloc(sizeof(int64_t) * (size_t)r);
+      for (int32_t e = 0; e < R.n; ++e) {
+        memcpy(u, R.v + (size_t)e * r, sizeof(int64_t) * (size_t)r);
+        if (untilt_all(&Lv, u)) continue;
+        tilt_all(&Ln, u);
+        memcpy(R.v + (size_t)keep * r, u, sizeof(int64_t) * (size_t)r);
+        R.a[2 * keep] = R.a[2 * e];
+        R.a[2 * keep + 1] = R.a[2 * e + 1];
+        ++keep;
+      }
+      free(u);
+      R.n = keep;
+      ++lvl;
+      memcpy(tbuf, tn, sizeof(int64_t) * 5 * (size_t)(r / 2 + 1));
+      free(tn);
+      Lv = Ln;
+      Lv.tilts = tbuf;
+      E = En;
+      oracle_project(&Lv, w, k, vf);                            /* the signal in the new coordinates */
+      i = 1;                                                    /* Alg. 3 l.5 */
+      stall = 0;
+    } else if (stall >= stall_limit) {
+      break;
+    }
   }
   if (R.n == k) status = ORACLE_OK;
 
@@ -520,14 +619,7 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
   int64_t* u = (int64_t*)malloc(sizeof(int64_t) * (size_t)r);
   for (int32_t e = 0; e < R.n && status >= 0; ++e) {
     memcpy(u, R.v + (size_t)e * r, sizeof(int64_t) * (size_t)r);
-    for (int32_t t = P->n_tilts - 1; t >= 0; --t) {
-      const int64_t* T = P->tilts + 5 * t;
-      int64_t out[2];
-      if (oracle_untilt_freq(T[2], T[3], T[4], u[T[0]], u[T[1]], out)) { status = ORACLE_ECORRUPT; break; }
-      u[T[0]] = out[0];
-      u[T[1]] = out[1];
-    }
-    if (status < 0) break;
+    if (untilt_all(&Lv, u)) { status = ORACLE_ECORRUPT; break; }
     if (oracle_wrap_freq(d, P->N, r, P->blocks, u, wt + (size_t)e * d)) { status = ORACLE_ECORRUPT; break; }
     refs[e].w = wt + (size_t)e * d;
     refs[e].d = d;
@@ -546,11 +638,11 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
   }
   *out_count = cnt;
   if (out_samples) *out_samples = samples;
-  if (out_iters) *out_iters = i - 1;
+  if (out_iters) *out_iters = it - 1;
 
   free(u); free(idx_of); free(refs); free(wt);
   free(F); free(acc_a); free(acc_v); free(acc_b); free(tc); free(tv);
-  free(R.a); free(R.v); free(vf); free(hi); free(lo);
+  free(R.a); free(R.v); free(vf); free(hi); free(lo); free(tbuf);
   return status;
 }
 

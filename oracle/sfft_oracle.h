@@ -41,7 +41,14 @@ typedef struct {
   int32_t extra_checks;      /* bit0 range check, bit1 bin consistency (C15) */
   int32_t n_primes;          /* explicit prime schedule p_i = primes[(i-1) mod n] */
   const int64_t* primes;     /* NULL -> i-th prime >= max(2, c k*) (Alg. 2 l.8) */
+  int32_t n_fallback;        /* stall fallback (reading R23): up to 4 tilt levels, Pythagorean triples
+                                (3,4,5), (5,12,13), (8,15,17), (7,24,25) on disjoint reduced-axis pairs */
 } oracle_params;
+
+/* Tilts of fallback level lvl in 1..4 (reading R23): triple lvl-1 of the schedule on disjoint reduced-axis
+ * pairs (q, q + s): level 1 (0,1),(2,3),...; level 2 (1,2),(3,4),... (r >= 3); level 3 stride 2 (0,2),(1,3),
+ * (4,6),...; level 4 stride 3.  Writes out [r/2][5]; returns the number of tilts (0 when r < 2). */
+int32_t oracle_fallback_tilts(int32_t r, int32_t lvl, int64_t* out);
 
 enum { ORACLE_OK = 0, ORACLE_PARTIAL = 1, ORACLE_EINVAL = -1, ORACLE_EPRECISION = -2,
        ORACLE_ECORRUPT = -4, ORACLE_ENOMEM = -6 };

@@ -408,3 +408,69 @@ def test_partial_when_sparsity_overstated():
     assert res.status == O.PARTIAL
     ws, _ = W.canonical_sort(w[:2], a[:2])
     assert (res.w == ws).all()
+
+
+# ------------------------------------------------------------------ stall fallback (reading R23)
+def test_fallback_tilt_schedule():
+    """Four Pythagorean triples (Eq. (25): b^2 + h^2 = c^2, gcd = 1) on disjoint reduced-axis pairs."""
+    assert O.fallback_tilts(1, 1) == []
+    assert O.fallback_tilts(2, 1) == [(0, 1, 3, 4, 5)]
+    assert O.fallback_tilts(2, 2) == [(0, 1, 5, 12, 13)]
+    assert O.fallback_tilts(3, 2) == [(1, 2, 5, 12, 13)]
+    assert O.fallback_tilts(3, 3) == [(0, 2, 8, 15, 17)]
+    assert O.fallback_tilts(5, 4) == [(0, 3, 7, 24, 25), (1, 4, 7, 24, 25)]
+    for r in range(2, 9):
+        pairs = set()
+        for lvl in range(1, 5):
+            ts = O.fallback_tilts(r, lvl)
+            axes = [x for t in ts for x in t[:2]]
+            assert len(axes) == len(set(axes))                        # disjoint pairs
+            for (a0, a1, b, h, c) in ts:
+                assert b * b + h * h == c * c and np.gcd(b, c) == 1 and np.gcd(h, c) == 1
+                pairs.add((a0, a1))
+        if r <= 4:                                                    # every axis pair tilted at some level
+            assert pairs == {(i, j) for i in range(r) for j in range(i + 1, r)}
+
+
+@pytest.mark.parametrize("d,N,k,blocks,structure", [(2, 16, 8, (1, 1), "rectangles"), (2, 16, 8, (1, 1), "rect_mix"),
+                                                    (3, 16, 16, (1, 1, 1), "rectangles"),
+                                                    (4, 8, 8, (2, 2), "rect_mix")])
+def test_stall_fallback_recovers_worst_case(d, N, k, blocks, structure):
+    """P:119 rectangles stall under parallel projection (PARTIAL without the fallback); with the fallback
+    (tilting after a stall, keeping what was found) the recovered set and coefficients equal the
+    brute-force dense d-dimensional DFT of f on the N^d grid."""
+    c = W.custom_config(d, N, k, blocks, structure=structure)
+    n_done = 0
+    for t in range(8):
+        try:
+            w, a = W.make_signal(c, t)
+        except AssertionError:
+            continue
+        r0 = O.solve(O.Params(d=d, N=N, k=k, blocks=blocks), w, a)
+        r4 = O.solve(O.Params(d=d, N=N, k=k, blocks=blocks, n_fallback=4), w, a)
+        wb, ab = _brute_force_modes(w, a, N)
+        assert r4.status == O.OK and np.array_equal(r4.w, wb) and np.abs(r4.a - ab).max() < 1e-11
+        if r0.status == O.PARTIAL:
+            # the trace shows the stall: stall_limit zero-accept iterations right before the switch
+            sl = max(2 * len(blocks), 16)
+            acc = r4.trace[:, 4]
+            runs = [len(x) for x in "".join("0" if v == 0 else "1" for v in acc).split("1")]
+            assert max(runs) >= sl
+            assert r4.samples > r0.samples
+        n_done += 1
+    assert n_done >= 5
+
+
+def test_stall_fallback_keeps_found_modes():
+    """Entries found before the switch are mapped exactly into the tilted coordinates: a mixed signal needs
+    fewer iterations after the switch than a solve that starts tilted from scratch would need for all k."""
+    c = W.custom_config(2, 64, 12, (1, 1), structure="rect_mix")
+    w, a = W.make_signal(c, 3)
+    r0 = O.solve(O.Params(d=2, N=64, k=12, blocks=(1, 1)), w, a)
+    assert r0.status == O.PARTIAL and 0 < r0.w.shape[0] < 12
+    r1 = O.solve(O.Params(d=2, N=64, k=12, blocks=(1, 1), n_fallback=1), w, a)
+    ws, as_ = W.canonical_sort(w, a)
+    assert r1.status == O.OK and np.array_equal(r1.w, ws) and np.abs(r1.a - as_).max() < 1e-12
+    # after the switch the first prime is the first prime >= c k* with k* = k - (modes kept), not c k
+    sw = r0.trace.shape[0]
+    assert r1.trace[sw, 1] == O.ith_prime_at_least(5 * (12 - r0.w.shape[0]), 1)

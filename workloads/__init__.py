@@ -43,7 +43,7 @@ class Config:
     alt_blocks: Tuple[int, ...]   # alternate partition exercised in parity tests
     trials: int                   # signals per batch (bench step)
     rho: str = "unit"             # "unit" or "uniform1_10"
-    structure: str = "uniform"    # "uniform", "collinear", "rectangles"
+    structure: str = "uniform"    # "uniform", "collinear", "rectangles", "rect_mix"
     groups: int = 0               # collinear groups (config 5)
 
     def seed(self, trial: int) -> int:
@@ -136,6 +136,20 @@ def _rectangle_rows(rng: np.random.Generator, N: int, k: int, d: int) -> np.ndar
     return w
 
 
+def _rect_mix_rows(rng: np.random.Generator, N: int, k: int, d: int) -> np.ndarray:
+    """k/2 modes in axis-aligned rectangles plus k/2 uniform distinct modes (stall-fallback tests)."""
+    kr = (k // 2) // 4 * 4
+    rect = _rectangle_rows(rng, N, kr, d)
+    rest = []
+    seen = {tuple(r) for r in rect}
+    while len(rest) < k - kr:
+        r = tuple(rng.integers(-N // 2, N // 2, size=d, dtype=np.int64))
+        if r not in seen:
+            seen.add(r)
+            rest.append(r)
+    return np.concatenate([rect, np.array(rest, np.int64).reshape(-1, d)])
+
+
 def make_signal(c: Config, trial: int = 0, seed: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray]:
     """Ground truth (omega int32 [k,d], a complex128 [k]) for one trial of config c."""
     s = c.seed(trial) if seed is None else seed
@@ -146,6 +160,8 @@ def make_signal(c: Config, trial: int = 0, seed: Optional[int] = None) -> Tuple[
         w = _collinear_rows(rng, c.N, c.k, c.d, c.groups)
     elif c.structure == "rectangles":
         w = _rectangle_rows(rng, c.N, c.k, c.d)
+    elif c.structure == "rect_mix":
+        w = _rect_mix_rows(rng, c.N, c.k, c.d)
     else:
         raise ValueError(c.structure)
     theta = rng.random(c.k)
