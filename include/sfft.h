@@ -70,6 +70,10 @@ typedef struct {
   int32_t expsum_path;        /* exp-sum arithmetic: 0 auto, 1 FP64 (DMMA / DFMA), 2 exact int8-limb products on
                                  the tcgen05 tensor cores combined in FP64 (needs
                                  literal_residual = 0 and E <= 2^36) [0: int8 limbs when available] */
+  int32_t fallback_tilts;     /* stall fallback (Algorithm 3; reading R23): after stall_limit
+                                 zero-accept iterations switch to the next of up to 4 tilt levels -- Pythagorean
+                                 triples (3,4,5), (5,12,13), (8,15,17), (7,24,25) on disjoint reduced-axis pairs --
+                                 keeping the modes found (mapped exactly); 0 = stop with PARTIAL [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */

@@ -572,7 +572,7 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
     stall = (na == 0) ? stall + 1 : 0;
     ++i;                                                        /* l.34 */
     ++it;
-    if (stall >= stall_limit && R.n < k) {
+    if (stall >= stall_limit && R.n < k && it <= P->max_iter) {
       /* C19 / R23: no progress for stall_limit iterations -> the next tilt of the schedule (Alg. 3), keeping
        * what was found: every entry is mapped to the new coordinates exactly (untilt, which must be
        * integral, then tilt); entries that do not untilt exactly are dropped */

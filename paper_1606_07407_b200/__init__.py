@@ -41,7 +41,8 @@ class sfft_options(ctypes.Structure):
                 ("max_iter", ctypes.c_int32), ("stall_limit", ctypes.c_int32),
                 ("batch", ctypes.c_int32), ("extra_checks", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("profile", ctypes.c_int32),
-                ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32)]
+                ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32),
+                ("fallback_tilts", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -161,7 +162,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               bin_floor_rel: float = 1e-8, prune_floor: float = 1e-8, round_tol: float = 0.01,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
               stream=None, profile: bool = False, literal_residual: bool = False,
-              expsum_path: int = 0) -> Plan:
+              expsum_path: int = 0, fallback_tilts: int = 0) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -178,6 +179,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.profile = 1 if profile else 0
     opt.literal_residual = 1 if literal_residual else 0
     opt.expsum_path = int(expsum_path)
+    opt.fallback_tilts = int(fallback_tilts)
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)

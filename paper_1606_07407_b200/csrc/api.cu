@@ -63,6 +63,10 @@ struct sfft_plan_s {
   I8Config i8{};
   bool i8_ok = false;          // int8-limb tensor-core exp-sum available for this plan
   int32_t expsum_path = 0;     // sfft_options.expsum_path
+  // stall fallback levels (reading R23): level 0 = the plan's own tilts / E
+  int32_t n_levels = 1, lvl_tmax = 1;
+  std::vector<int64_t> lvl_E, lvl_lo, lvl_hi, lvl_tilts;
+  std::vector<int32_t> lvl_nt, lvl_axt;
   int smem_optin = 0;
   // workspace
   size_t ws_bytes = 0;
@@ -84,7 +88,8 @@ enum Buf {
   B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
-  B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_I8TLO, B_I8THI,
+  B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
+  B_STRT, B_I8TLO, B_I8THI,
   B_COUNT
 };
 
@@ -193,6 +198,13 @@ void layout(sfft_plan_t* P) {
   sz[B_I8B] = P->i8_ok ? i8_limb_bytes(P->i8, (int)S) : 0;
   sz[B_I8SIG] = 8 * S;
   sz[B_CMACS8] = 8 * S;
+  sz[B_LVLE] = 8 * (size_t)P->n_levels;
+  sz[B_LVLLO] = 8 * (size_t)P->n_levels * P->r;
+  sz[B_LVLHI] = 8 * (size_t)P->n_levels * P->r;
+  sz[B_LVLT] = 8 * P->lvl_tilts.size();
+  sz[B_LVLNT] = 4 * (size_t)P->n_levels;
+  sz[B_LVLAXT] = 4 * (size_t)P->n_levels * P->r;
+  for (int b : {B_STLVL, B_STIL, B_STRT}) sz[b] = 4 * S;
   sz[B_I8TLO] = P->i8_ok ? 8 * S * (P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
   size_t o = 0;
@@ -262,6 +274,17 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_log = ptr<int32_t>(P, B_LOG);
   D.ctrl = ptr<int32_t>(P, B_CTRL);
   D.active = ptr<int32_t>(P, B_ACTIVE);
+  D.n_levels = P->n_levels;
+  D.lvl_tmax = P->lvl_tmax;
+  D.lvl_E = ptr<int64_t>(P, B_LVLE);
+  D.lvl_lo = ptr<int64_t>(P, B_LVLLO);
+  D.lvl_hi = ptr<int64_t>(P, B_LVLHI);
+  D.lvl_tilts = ptr<int64_t>(P, B_LVLT);
+  D.lvl_nt = ptr<int32_t>(P, B_LVLNT);
+  D.lvl_axt = ptr<int32_t>(P, B_LVLAXT);
+  D.st_lvl = ptr<int32_t>(P, B_STLVL);
+  D.st_il = ptr<int32_t>(P, B_STIL);
+  D.st_retilt = ptr<int32_t>(P, B_STRT);
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
@@ -310,6 +333,12 @@ int ensure_ready(sfft_plan_t* P) {
     CUDA_TRY(P, up(B_FFTN, fn.data(), 4 * fn.size()));
     CUDA_TRY(P, up(B_TWOFF, P->tw_off.data(), 4 * P->tw_off.size()));
     CUDA_TRY(P, up(B_TWSEG, P->tw_seg.data(), 16 * P->tw_seg.size()));
+    CUDA_TRY(P, up(B_LVLE, P->lvl_E.data(), 8 * P->lvl_E.size()));
+    CUDA_TRY(P, up(B_LVLLO, P->lvl_lo.data(), 8 * P->lvl_lo.size()));
+    CUDA_TRY(P, up(B_LVLHI, P->lvl_hi.data(), 8 * P->lvl_hi.size()));
+    CUDA_TRY(P, up(B_LVLT, P->lvl_tilts.data(), 8 * P->lvl_tilts.size()));
+    CUDA_TRY(P, up(B_LVLNT, P->lvl_nt.data(), 4 * P->lvl_nt.size()));
+    CUDA_TRY(P, up(B_LVLAXT, P->lvl_axt.data(), 4 * P->lvl_axt.size()));
     CUDA_TRY(P, launch_fft_twiddles(ptr<double2>(P, B_TW), ptr<int4>(P, B_TWSEG), (int)P->tw_seg.size(), P->stream));
     CUDA_TRY(P, cudaStreamSynchronize(P->stream));
     P->tables_ready = true;
@@ -408,6 +437,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->literal = opt->literal_residual != 0;
     P->expsum_path = opt->expsum_path;
     if (P->expsum_path < 0 || P->expsum_path > 2) return SFFT_EINVAL;
+    if (opt->fallback_tilts < 0 || opt->fallback_tilts > 4) return SFFT_EINVAL;
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -477,6 +507,57 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   for (int q = 0; q < P->r; ++q)
     if (2 * P->hi[q] >= P->E || -2 * P->lo[q] > P->E) return SFFT_EINVAL;
   if (P->stall_limit <= 0) P->stall_limit = std::max(2 * P->r, 16);
+  // fallback levels (reading R23): level 0 = this plan; level l >= 1 = Pythagorean triple l-1 on the disjoint
+  // reduced-axis pairs (q, q + s) -- s = 1 from axis 0 (l = 1), s = 1 from axis 1 (l = 2, r >= 3), s = 2 (l = 3),
+  // s = 3 (l = 4) -- with E = 2 B (base + height) (reading R2); the schedule stops at the first empty level
+  {
+    static const int64_t kTri[4][3] = {{3, 4, 5}, {5, 12, 13}, {8, 15, 17}, {7, 24, 25}};
+    const int n_fb = opt ? opt->fallback_tilts : 0;
+    std::vector<std::vector<int64_t>> lt(1, P->tilts);
+    std::vector<int64_t> lE(1, P->E);
+    for (int l = 1; l <= n_fb; ++l) {
+      const int64_t* T = kTri[l - 1];
+      const int st = l <= 2 ? 1 : l - 1;
+      const int off = (l == 2 && P->r >= 3) ? 1 : 0;
+      std::vector<int64_t> ts;
+      for (int b = off; b < P->r; b += 2 * st)
+        for (int i = 0; i < st && b + i + st < P->r; ++i) ts.insert(ts.end(), {b + i, b + i + st, T[0], T[1], T[2]});
+      if (ts.empty()) break;
+      const int64_t El = 2 * B * (T[0] + T[1]);
+      if (El > ((int64_t)1 << 42)) break;
+      lt.push_back(ts);
+      lE.push_back(El);
+    }
+    P->n_levels = (int32_t)lt.size();
+    size_t tmax = 1;
+    for (auto& t : lt) tmax = std::max(tmax, t.size() / 5);
+    P->lvl_tmax = (int32_t)tmax;
+    P->lvl_E = lE;
+    P->lvl_tilts.assign((size_t)P->n_levels * tmax * 5, 0);
+    P->lvl_nt.assign(P->n_levels, 0);
+    P->lvl_axt.assign((size_t)P->n_levels * P->r, -1);
+    P->lvl_lo.assign((size_t)P->n_levels * P->r, 0);
+    P->lvl_hi.assign((size_t)P->n_levels * P->r, 0);
+    for (int l = 0; l < P->n_levels; ++l) {
+      const std::vector<int64_t>& ts = lt[l];
+      P->lvl_nt[l] = (int32_t)(ts.size() / 5);
+      std::copy(ts.begin(), ts.end(), P->lvl_tilts.begin() + (size_t)l * tmax * 5);
+      int64_t* lo = P->lvl_lo.data() + (size_t)l * P->r;
+      int64_t* hi = P->lvl_hi.data() + (size_t)l * P->r;
+      int32_t* axt = P->lvl_axt.data() + (size_t)l * P->r;
+      for (int q = 0; q < P->r; ++q) { lo[q] = blo[q]; hi[q] = bhi[q]; }
+      for (size_t t = 0; t < ts.size() / 5; ++t) {
+        const int a0 = (int)ts[5 * t], a1 = (int)ts[5 * t + 1];
+        const int64_t b = ts[5 * t + 2], h = ts[5 * t + 3];
+        axt[a0] = 2 * (int)t;
+        axt[a1] = 2 * (int)t + 1;
+        lo[a0] = b * blo[a0] - h * bhi[a1];
+        hi[a0] = b * bhi[a0] - h * blo[a1];
+        lo[a1] = h * blo[a0] + b * blo[a1];
+        hi[a1] = h * bhi[a0] + b * bhi[a1];
+      }
+    }
+  }
   // device limits -> FFT sizes, p_cap, prime table
   cudaError_t ce = cudaGetDevice(&P->device);
   if (ce != cudaSuccess) return fail(nullptr, SFFT_ECUDA, "no device");
@@ -539,7 +620,8 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   P->shape = choose_expsum_shape(P->L);
   P->Lp = P->shape.nt * P->shape.bn;
   // int8-limb tensor-core exp-sum (bin-domain residual only: its B limbs are the fixed signal rows)
-  if (P->expsum_path != 1 && !P->literal) P->i8_ok = i8_configure(P->L, P->E, P->k, &P->i8);
+  if (P->expsum_path != 1 && !P->literal)
+    P->i8_ok = i8_configure(P->L, *std::max_element(P->lvl_E.begin(), P->lvl_E.end()), P->k, &P->i8);
   if (P->expsum_path == 2 && !P->i8_ok) return SFFT_ENOTSUP;
   // shared-memory budgets of the other kernels
   if (16 * ((size_t)P->p_stride + 2) + 2 * 16 * 16 * (size_t)P->shape.bn + 256 > (size_t)smem_optin) return SFFT_ENOTSUP;
@@ -679,6 +761,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     D.i8_iter = use_i8 ? 1 : 0;
     LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
     D.i8_iter = 0;
+    if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
+      LAUNCH(P, launch_retilt(D, batch, sig->freqs, st));
+      if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, batch, P->k, st, true));
+    }
     if (use_i8) { ++n_expsum_i8; it_i8.push_back(it_marks.empty() ? 0 : it_marks.back()); }
     mark();
     last_iter = iter;

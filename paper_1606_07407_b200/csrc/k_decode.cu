@@ -33,15 +33,18 @@ __global__ void setup_kernel(DevParams P, int32_t iter) {
   if (s >= P.batch || P.st_status[s] != ST_RUN) return;
   const int nR = P.st_nR[s];
   const int kstar = P.k - nR;
+  P.st_retilt[s] = 0;
+  const int il = P.st_il[s] + 1;                           // counter of the current level (= iter without a switch)
+  P.st_il[s] = il;
   int p;
-  if (P.n_sched > 0) p = (int)P.sched[(iter - 1) % P.n_sched];
-  else p = ith_prime_at_least(P, P.c * kstar, iter);
+  if (P.n_sched > 0) p = (int)P.sched[(il - 1) % P.n_sched];
+  else p = ith_prime_at_least(P, P.c * kstar, il);
   if (p < 2 || p > P.p_cap) {
     P.st_status[s] = SFFT_ENOTSUP;
     return;
   }
   P.st_p[s] = p;
-  P.st_m[s] = iter % P.r;
+  P.st_m[s] = il % P.r;
   P.active[atomicAdd(&P.ctrl[0], 1)] = s;
   atomicMax(&P.ctrl[1], p);
   atomicMax(&P.ctrl[2], P.k + (P.literal ? nR : 0));        // terms the exp-sum sums
@@ -112,6 +115,10 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   const int kstar = STAGE ? kstar_stage : P.k - nR;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
   const int r = P.r;
+  const int lvl = STAGE ? 0 : P.st_lvl[s];
+  const int64_t Ev = P.lvl_E[lvl];
+  const int64_t* lo_v = P.lvl_lo + (int64_t)lvl * r;
+  const int64_t* hi_v = P.lvl_hi + (int64_t)lvl * r;
 
   double* mag = reinterpret_cast<double*>(smem_raw);
   int* cand = reinterpret_cast<int*>(mag + p);
@@ -273,11 +280,11 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
           // q = F_n conj(F_0), written without contraction to mirror the plain formula
           const double qr = __dadd_rn(__dmul_rn(fv[u].x, f0[u].x), __dmul_rn(fv[u].y, f0[u].y));
           const double qi = __dsub_rn(__dmul_rn(fv[u].y, f0[u].x), __dmul_rn(fv[u].x, f0[u].y));
-          const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)P.E), twopi);   // Eq. (41)
+          const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)Ev), twopi);    // Eq. (41)
           const double xr = rint(x);
           good = fabs(x - xr) <= P.round_tol;
           const int64_t v = (int64_t)xr;
-          if (P.extra & 1) good = good && v >= P.lo[n[u]] && v <= P.hi[n[u]];
+          if (P.extra & 1) good = good && v >= lo_v[n[u]] && v <= hi_v[n[u]];
           accv[(int64_t)n[u] * P.k + ci[u]] = v;
         }
         if (!good) flag[ci[u]] = 0;
@@ -387,7 +394,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     double2 c;
     if (n == 0) c = make_double2(-a.x, -a.y);
     else if (n < P.L) {
-      const double2 lf = line_factor_d(vreg[(int64_t)(n - 1) * P.kk + e], P.E);
+      const double2 lf = line_factor_d(vreg[(int64_t)(n - 1) * P.kk + e], Ev);
       c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
     } else c = make_double2(0.0, 0.0);
     Creg[(int64_t)e * P.Lp + n] = c;
@@ -434,8 +441,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   if (tid == 0) {
     const int K = P.k + (P.literal ? nR : 0);
     P.st_nR[s] = nR_final;
-    const int stall = na == 0 ? P.st_stall[s] + 1 : 0;
-    P.st_stall[s] = stall;
+    int stall = na == 0 ? P.st_stall[s] + 1 : 0;
     P.st_samples[s] += (int64_t)P.L * p;
     P.st_cmacs[s] += (int64_t)P.L * p * K;
     if (P.i8_iter) P.st_cmacs_i8[s] += (int64_t)P.L * p * K;
@@ -445,10 +451,152 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
       P.st_log[2 * (iter - 1) + 1] = na;
     }
     int st = ST_RUN;
-    if (nR_final >= P.k) st = SFFT_OK;
-    else if (stall >= P.stall_limit || iter >= P.max_iter) st = SFFT_PARTIAL;
+    if (nR_final >= P.k) {
+      st = SFFT_OK;
+    } else if (stall >= P.stall_limit) {
+      // C19 / R23: no progress for stall_limit iterations -> next tilt level (Alg. 3) if another iteration may run
+      if (lvl + 1 < P.n_levels && iter < P.max_iter) {
+        P.st_lvl[s] = lvl + 1;
+        P.st_retilt[s] = 1;
+        stall = 0;
+      } else {
+        st = SFFT_PARTIAL;
+      }
+    } else if (iter >= P.max_iter) {
+      st = SFFT_PARTIAL;
+    }
+    P.st_stall[s] = stall;
     P.st_status[s] = st;
   }
+}
+
+// ------------------------------------------------------------------ stall fallback (reading R23)
+// One CTA per signal that switched level in the last decode: the signal terms are re-projected with the
+// new level's tilts (v_j = T unwrap(omega_j), Eq. (35) + Eq. (27)) and get new line factors (its E); every
+// registry entry is untilted with the old level (hypo^2 division, must be exact -- entries that are not
+// are dropped) and tilted with the new one, order preserved; hashes, the hash table and the registry C
+// rows are rebuilt.  The level-local iteration counter restarts (Alg. 3 l.5).
+__global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t* __restrict__ freqs) {
+  const int s = blockIdx.x;
+  if (!P.st_retilt[s]) return;
+  __shared__ int scratch[64];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int r = P.r, kk = P.kk;
+  const int lvl = P.st_lvl[s];
+  const int64_t E = P.lvl_E[lvl];
+  const int64_t* Tn = P.lvl_tilts + (int64_t)lvl * P.lvl_tmax * 5;
+  const int64_t* To = P.lvl_tilts + (int64_t)(lvl - 1) * P.lvl_tmax * 5;
+  const int ntn = P.lvl_nt[lvl], nto = P.lvl_nt[lvl - 1];
+  int64_t* vs = P.v_all + (int64_t)s * r * kk;
+  double2* Cs = P.C_all + (int64_t)s * kk * P.Lp;
+  // 1. signal terms (warp per term)
+  for (int j = warp; j < P.k; j += nwarps) {
+    const int32_t* w = freqs + ((int64_t)s * P.k + j) * P.d;
+    for (int q = lane; q < r; q += 32) {
+      const int off = P.block_off[q], dq = P.block_dims[q];
+      int64_t acc = 0, pw = 1;
+      for (int t = 0; t < dq; ++t) {
+        acc += (int64_t)__ldg(w + off + t) * pw;
+        pw *= P.N;
+      }
+      vs[(int64_t)q * kk + j] = acc;
+    }
+    __syncwarp();
+    for (int t = lane; t < ntn; t += 32) {
+      const int64_t* T = Tn + 5 * t;
+      const int64_t u0 = vs[T[0] * kk + j], u1 = vs[T[1] * kk + j];
+      vs[T[0] * kk + j] = T[2] * u0 - T[3] * u1;
+      vs[T[1] * kk + j] = T[3] * u0 + T[2] * u1;
+    }
+    __syncwarp();
+    const double2 a = Cs[(int64_t)j * P.Lp];                       // column 0 = a_j
+    for (int n = 1 + lane; n < P.L; n += 32) {
+      const double2 lf = line_factor_d(vs[(int64_t)(n - 1) * kk + j], E);
+      Cs[(int64_t)j * P.Lp + n] = make_double2(a.x * lf.x - a.y * lf.y, a.x * lf.y + a.y * lf.x);
+    }
+  }
+  // 2. registry entries (warp per entry): old untilt (exact) then new tilt, into the acc_v scratch
+  const int nR = P.st_nR[s];
+  int64_t* vreg = vs + P.k;                                        // column e = entry e
+  int64_t* sv = P.acc_v + (int64_t)s * r * P.k;                     // [r][k]
+  double2* areg = P.a_reg + (int64_t)s * P.k;
+  double2* sa = P.acc_a + (int64_t)s * P.k;
+  int* keep = reinterpret_cast<int*>(P.wtmp + (int64_t)s * P.k * P.d);   // [k] (wrap scratch, unused until the end)
+  for (int e = warp; e < nR; e += nwarps) {
+    for (int q = lane; q < r; q += 32) sv[(int64_t)q * P.k + e] = vreg[(int64_t)q * kk + e];
+    __syncwarp();
+    int bad = 0;
+    for (int t = lane; t < nto; t += 32) {
+      const int64_t* T = To + 5 * t;
+      const int64_t v0 = sv[T[0] * P.k + e], v1 = sv[T[1] * P.k + e];
+      const int64_t b = T[2], h = T[3], c2 = T[4] * T[4];
+      const int64_t n0 = b * v0 + h * v1, n1 = -h * v0 + b * v1;
+      if (n0 % c2 != 0 || n1 % c2 != 0) bad = 1;
+      else { sv[T[0] * P.k + e] = n0 / c2; sv[T[1] * P.k + e] = n1 / c2; }
+    }
+    __syncwarp();
+    for (int t = lane; t < ntn; t += 32) {
+      const int64_t* T = Tn + 5 * t;
+      const int64_t u0 = sv[T[0] * P.k + e], u1 = sv[T[1] * P.k + e];
+      sv[T[0] * P.k + e] = T[2] * u0 - T[3] * u1;
+      sv[T[1] * P.k + e] = T[3] * u0 + T[2] * u1;
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) { keep[e] = !bad; sa[e] = areg[e]; }
+  }
+  __syncthreads();
+  // 3. order-preserving compaction (block scan over chunks of the entries)
+  int total = 0;
+  {
+    const int per = (nR + blockDim.x - 1) / blockDim.x;
+    const int e0 = tid * per, e1 = min(nR, e0 + per);
+    int c = 0;
+    for (int e = e0; e < e1; ++e) c += keep[e];
+    int pos = block_excl_scan(c, scratch, &total);
+    for (int e = e0; e < e1; ++e) {
+      if (!keep[e]) continue;
+      uint64_t h = 0x9E3779B97F4A7C15ULL;
+      for (int n = 0; n < r; ++n) {
+        const int64_t v = sv[(int64_t)n * P.k + e];
+        vreg[(int64_t)n * kk + pos] = v;
+        h = mix64(h ^ (uint64_t)v);
+      }
+      areg[pos] = sa[e];
+      P.key_hash[(int64_t)s * P.k + pos] = h;
+      ++pos;
+    }
+  }
+  __syncthreads();
+  // 4. hash table and registry C rows (-a_e e^{2 pi i v_{e,n} / E})
+  int* htab = P.htab + (int64_t)s * P.H;
+  const int Hm = P.H - 1;
+  for (int i = tid; i < P.H; i += blockDim.x) htab[i] = 0;
+  __syncthreads();
+  for (int e = tid; e < total; e += blockDim.x) {
+    int slot = (int)(P.key_hash[(int64_t)s * P.k + e] & (uint64_t)Hm);
+    while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+  }
+  double2* Creg = Cs + (int64_t)P.k * P.Lp;
+  for (int64_t w = tid; w < (int64_t)total * P.Lp; w += blockDim.x) {
+    const int e = (int)(w / P.Lp), n = (int)(w % P.Lp);
+    const double2 a = areg[e];
+    double2 c;
+    if (n == 0) c = make_double2(-a.x, -a.y);
+    else if (n < P.L) {
+      const double2 lf = line_factor_d(vreg[(int64_t)(n - 1) * kk + e], E);
+      c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+    } else c = make_double2(0.0, 0.0);
+    Creg[(int64_t)e * P.Lp + n] = c;
+  }
+  if (tid == 0) {
+    P.st_nR[s] = total;
+    P.st_il[s] = 0;
+  }
+}
+
+cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freqs, cudaStream_t st) {
+  if (P.n_levels > 1 && batch > 0) retilt_kernel<<<batch, 1024, 0, st>>>(P, freqs);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st) {

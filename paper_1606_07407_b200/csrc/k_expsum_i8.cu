@@ -77,7 +77,7 @@ __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT
 //   i8_B + s * per_signal + nt * nks * S * NT * 32 + (ks * S + t) * W * 32,  per_signal = nks * S * 32 * cols
 // in the UMMA K-major layout: (column, K byte) -> (col / 8) 256 + (k / 16) 128 + (col % 8) 16 + k % 16.
 // One thread per (signal, padded output column, K step, 4-byte K word): S words, one per limb.
-__global__ void i8_limbs_kernel(DevParams P, int32_t K) {
+__global__ void i8_limbs_kernel(DevParams P, int32_t K, int32_t only_retilted) {
   const int NT = P.i8_NT, S = P.i8_S, ntiles = P.i8_ntiles, nks = P.i8_nks;
   const int nkt = (K + kI8StepTerms - 1) / kI8StepTerms;        // steps in use (layout stride stays nks)
   const int cols = (ntiles - 1) * NT + P.i8_NT_last;
@@ -85,6 +85,7 @@ __global__ void i8_limbs_kernel(DevParams P, int32_t K) {
   const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (g >= (int64_t)P.batch * per_sig) return;
   const int s = (int)(g / per_sig);
+  if (only_retilted && !P.st_retilt[s]) return;
   int64_t r = g % per_sig;
   const int kw = (int)(r & 7);
   r >>= 3;
@@ -500,13 +501,13 @@ int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
   return n_signals * ((max_p + kI8Rows - 1) / kI8Rows) * c.ntiles;
 }
 
-cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st) {
-  i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);
+cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st, bool only_retilted) {
+  if (!only_retilted) i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);   // |a_j| do not change on a retilt
   const int cols = (P.i8_ntiles - 1) * P.i8_NT + P.i8_NT_last;
   const int64_t total = (int64_t)n_signals * cols * ((K + kI8StepTerms - 1) / kI8StepTerms) * 8;
   DevParams Q = P;
   Q.batch = n_signals;
-  if (total > 0) i8_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, K);
+  if (total > 0) i8_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, K, only_retilted ? 1 : 0);
   return cudaGetLastError();
 }
 

@@ -74,6 +74,9 @@ __global__ void init_state_kernel(DevParams P, int32_t batch) {
   P.st_samples[s] = 0;
   P.st_cmacs[s] = 0;
   P.st_cmacs_i8[s] = 0;
+  P.st_lvl[s] = 0;
+  P.st_il[s] = 0;
+  P.st_retilt[s] = 0;
 }
 
 cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* freqs, const double* coeffs,

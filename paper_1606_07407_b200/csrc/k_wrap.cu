@@ -28,11 +28,14 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad) {
   const int64_t N = P.N, h2 = N / 2;
   const double invN = 1.0 / (double)N;
   int err = 0;
+  const int lvl = P.st_lvl[s];
+  const int32_t* axt = P.lvl_axt + (int64_t)lvl * P.r;
+  const int64_t* tl = P.lvl_tilts + (int64_t)lvl * P.lvl_tmax * 5;
   for (int q = lane; q < P.r; q += 32) {
     int64_t u = vreg[(int64_t)q * P.kk + e];
-    const int at = P.axis_tilt[q];
+    const int at = axt[q];
     if (at >= 0) {
-      const int64_t* T = P.tilts + 5 * (at >> 1);
+      const int64_t* T = tl + 5 * (at >> 1);
       const int64_t v0 = vreg[T[0] * P.kk + e], v1 = vreg[T[1] * P.kk + e];
       const int64_t b = T[2], h = T[3], c2 = T[4] * T[4];
       const int64_t num = (at & 1) ? (-h * v0 + b * v1) : (b * v0 + h * v1);

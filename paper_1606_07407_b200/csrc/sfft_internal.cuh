@@ -79,6 +79,17 @@ struct DevParams {
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
   int32_t* active;             // [batch] indices of the signals still running this iteration
+  // stall fallback (reading R23): level 0 = the plan's own tilts and E, levels 1.. = fallback tilts
+  int32_t n_levels, lvl_tmax;  // levels, tilt slots per level
+  const int64_t* lvl_E;        // [n_levels]
+  const int64_t* lvl_lo;       // [n_levels][r] decodable image of every axis
+  const int64_t* lvl_hi;       // [n_levels][r]
+  const int64_t* lvl_tilts;    // [n_levels][lvl_tmax][5] (axis0, axis1, base, height, hypo)
+  const int32_t* lvl_nt;       // [n_levels] tilts per level
+  const int32_t* lvl_axt;      // [n_levels][r] 2*tilt+slot of a tilted axis, -1 otherwise
+  int32_t* st_lvl;             // [batch] current level
+  int32_t* st_il;              // [batch] iteration counter of the current level (Alg. 3 l.5)
+  int32_t* st_retilt;          // [batch] 1: switched level in the last decode, re-project before the next setup
   // int8-limb tensor-core exp-sum (k_expsum_i8.cu)
   int32_t i8_S, i8_NT, i8_NT_last, i8_ntiles, i8_nks;   // limbs, n-tile width (last tile narrower), n-tiles, K-step capacity
   int32_t i8_K;                // terms held in the B limbs (k for a solve, K for the stage entry point)
@@ -129,6 +140,8 @@ cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, c
 // k_decode.cu
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st);
 cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st);
+// re-projection of the signals that switched fallback level (reading R23); freqs = the execute's input
+cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freqs, cudaStream_t st);
 cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,
                                 double* acc_a, int32_t* counts, cudaStream_t st);
 size_t decode_smem_bytes(const DevParams& P, int32_t max_p);
@@ -151,7 +164,8 @@ bool i8_configure(int L, int64_t E, int k, I8Config* out);
 size_t i8_limb_bytes(const I8Config& c, int batch);
 bool i8_fits(const I8Config& c, int p, int k, int smem_optin);
 int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals);
-cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st);
+cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st,
+                              bool only_retilted = false);
 cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_p, int32_t n_signals, int32_t ksplit,
                              double2* part, int32_t p_part, int smem_optin, cudaStream_t st);
 // k_fft.cu

@@ -346,3 +346,46 @@ def test_e2e_literal_residual_mode(S, name, trials):
             assert np.abs(r.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), (key, lit)
     assert np.array_equal(res[True][0], res[False][0]) and res[True][3:] == res[False][3:]
     assert np.abs(res[True][1] - res[False][1]).max() <= 1e-12 * np.abs(res[True][1]).max()
+
+
+# ------------------------------------------------------------------ stall fallback (reading R23)
+@pytest.mark.parametrize("d,N,k,blocks,structure,n_fb,trials", [
+    (2, 16, 8, (1, 1), "rectangles", 4, 12), (2, 64, 12, (1, 1), "rect_mix", 1, 12),
+    (3, 16, 16, (1, 1, 1), "rect_mix", 4, 8), (4, 16, 8, (1, 1, 1, 1), "rectangles", 4, 8),
+    (4, 8, 8, (2, 2), "rect_mix", 2, 8), (2, 16, 8, (1, 1), "rectangles", 0, 4)])
+@pytest.mark.parametrize("path", [0, 1])
+def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trials, path):
+    """Worst-case rectangles stall; the tilt fallback (Alg. 3 after a stall) recovers them.
+    Batched execute (signals switch levels independently) against the oracle with the same schedule:
+    statuses, sets bit-exact, coefficients <= 1e-9, per-signal sample totals."""
+    c = W.custom_config(d, N, k, blocks, structure=structure)
+    ws, as_, used = [], [], []
+    for t in range(trials * 2):
+        try:
+            w, a = W.make_signal(c, t)
+        except AssertionError:
+            continue
+        ws.append(w)
+        as_.append(a)
+        used.append(t)
+        if len(used) == trials:
+            break
+    w = np.stack(ws).astype(np.int32)
+    a = np.stack(as_)
+    plan = _plan(S, c, batch=len(used), fallback_tilts=n_fb, expsum_path=path)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    P = O.params_for(c, n_fallback=n_fb)
+    samples = 0
+    for i in range(len(used)):
+        ref = O.solve(P, w[i], a[i])
+        samples += ref.samples
+        assert int(res.per_status[i]) == ref.status, (i, int(res.per_status[i]), ref.status)
+        n = int(res.count[i])
+        assert n == ref.w.shape[0]
+        assert np.array_equal(res.freqs[i, :n].cpu().numpy(), ref.w), i
+        if n:
+            assert np.abs(res.coeffs[i, :n].cpu().numpy() - ref.a).max() <= 1e-9 * np.abs(ref.a).max()
+        if n_fb and ref.status == O.OK:
+            wc, _ = W.canonical_sort(w[i], a[i])
+            assert np.array_equal(ref.w, wc)
+    assert res.report.samples_used == samples
