@@ -73,7 +73,7 @@ struct sfft_plan_s {
   void* ws = nullptr;
   bool ws_owned = false;
   bool tables_ready = false;
-  size_t off[64] = {0};
+  size_t off[128] = {0};        // workspace offsets, indexed by Buf (static_assert below)
   int32_t* h_ctrl = nullptr;   // pinned
   bool profile = false;
   int32_t literal = 0;
@@ -89,9 +89,10 @@ enum Buf {
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
-  B_STRT, B_I8TLO, B_I8THI,
+  B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_I8TLO, B_I8THI,
   B_COUNT
 };
+static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
 
 int fail(sfft_plan_t* P, int code, const char* fmt, ...) {
   if (P) {
@@ -205,6 +206,10 @@ void layout(sfft_plan_t* P) {
   sz[B_LVLNT] = 4 * (size_t)P->n_levels;
   sz[B_LVLAXT] = 4 * (size_t)P->n_levels * P->r;
   for (int b : {B_STLVL, B_STIL, B_STRT}) sz[b] = 4 * S;
+  sz[B_I8PW] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
+  sz[B_I8DLOG] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
+  sz[B_I8ELOG] = P->i8_ok ? 4 * S * align_up((size_t)P->kk + 16, 4) : 0;
+  sz[B_I8CHL] = P->i8_ok ? 16 * S * (P->p_stride + 8) : 0;
   sz[B_I8TLO] = P->i8_ok ? 8 * S * (P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
   size_t o = 0;
@@ -293,12 +298,22 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_tlo = ptr<uint2>(P, B_I8TLO);
     D.i8_thi = ptr<uint32_t>(P, B_I8THI);
     D.i8_tstride = P->p_stride + 8;
+    D.i8_pw = ptr<int32_t>(P, B_I8PW);
+    D.i8_dlog = ptr<int32_t>(P, B_I8DLOG);
+    D.i8_elog = ptr<int32_t>(P, B_I8ELOG);
+    D.i8_estride = (int32_t)align_up((size_t)P->kk + 16, 4);   // rows 16-byte aligned for the bulk copies
+    D.i8_chl = ptr<double2>(P, B_I8CHL);
   }
   return D;
 }
 
 int ensure_ready(sfft_plan_t* P) {
   CUDA_TRY(P, cudaSetDevice(P->device));
+  {
+    const cudaError_t pending = cudaGetLastError();   // a stale error of another library must not be reported as ours
+    if (pending != cudaSuccess && getenv("SFFT_DEBUG"))
+      fprintf(stderr, "[sfft] cleared pending CUDA error before plan setup: %s\n", cudaGetErrorString(pending));
+  }
   if (!P->ws) {
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, P->ws_bytes);
@@ -755,8 +770,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
       LAUNCH(P, launch_expsum(D, shp, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
     ++n_expsum;
     mark();
+    D.lines_log = use_i8 ? 1 : 0;
     LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, ksplit,
                           ptr<double2>(P, B_PART), max_p, st));
+    D.lines_log = 0;
     mark();
     D.i8_iter = use_i8 ? 1 : 0;
     LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
@@ -896,11 +913,12 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
     D.i8_K = K;
     LAUNCH(P, launch_i8_prepare(D, 1, K, P->stream));
     LAUNCH(P, launch_expsum_i8(D, P->i8, (int)p, 1, 1, nullptr, 0, P->smem_optin, P->stream));
+    LAUNCH(P, launch_i8_unpermute(D, (int)p, s_out, P->stream));     // discrete-log row order -> natural
   } else {
     LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, (int)p), (int)p, 1, 1, nullptr, 0, P->stream));
+    CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
+                                  cudaMemcpyDeviceToDevice, P->stream));
   }
-  CUDA_TRY(P, cudaMemcpy2DAsync(s_out, 16 * (size_t)p, D.lines, 16 * (size_t)P->p_stride, 16 * (size_t)p, P->L,
-                                cudaMemcpyDeviceToDevice, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }

@@ -137,17 +137,21 @@ struct I8Args {
 
 // 8 terms (4 TMEM columns per limb) of one K step for this thread's row h: gather the root limbs and pack
 // them into the TMEM word layout (4 K bytes per 32-bit column: re_j, im_j, re_j+1, im_j+1)
+// 8 terms (4 TMEM columns per limb) of one K step for this thread's row f (discrete-log order, reading R22):
+// the root of (f, j) is table entry (f + e_j) mod (p - 1) (entry p - 1 = W_p[0] for h = 0 or u_j = 0), so the
+// 32 lanes of a warp (consecutive f) read consecutive entries -- conflict-free shared-memory gathers.
 template <int NL>
-__device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int2* __restrict__ sU,
-                                          const uint2* __restrict__ sTlo, const uint32_t* __restrict__ sThi, unsigned h,
-                                          unsigned magic, int p, int dbg) {
-  unsigned q[8];
+__device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int* __restrict__ sE,
+                                          const uint2* __restrict__ sTlo, const uint32_t* __restrict__ sThi, int f,
+                                          int n1, int dbg) {
+  int q[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
-    const unsigned x = h * (unsigned)sU[e].x;
-    int r = (int)(x - __umulhi(x, magic) * (unsigned)p);
-    r += (r >> 31) & p;
-    q[e] = dbg == 1 ? (h + e) : (unsigned)r;
+    const int ej = sE[e];
+    int x = f + ej;
+    x -= x >= n1 ? n1 : 0;
+    q[e] = (f >= n1 || ej < 0 || ej >= n1) ? n1 : x;       // padding terms may hold any value: stay in the table
+    if (dbg == 1) q[e] = f < n1 ? f : n1;
   }
   uint2 lo[8];
 #pragma unroll
@@ -223,7 +227,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   unsigned char* sB = smem_raw + 512;
   uint2* sTlo = reinterpret_cast<uint2*>(smem_raw + A.tab_off);
   const uint32_t* sThi = reinterpret_cast<const uint32_t*>(smem_raw + A.thi_off);
-  int2* sU = reinterpret_cast<int2*>(smem_raw + A.u_off);
+  int* sU = reinterpret_cast<int*>(smem_raw + A.u_off);         // e_j of the signal's terms
   const int NT = P.i8_NT, ntiles = P.i8_ntiles, nks = P.i8_nks;
   const int cols = (ntiles - 1) * NT + P.i8_NT_last;
   const int K = P.i8_K;                                             // terms in the B limbs (bin-domain: k)
@@ -280,11 +284,11 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         const uint32_t blo = ((uint32_t)p * 8 + 15) & ~15u, bhi = S > 4 ? (((uint32_t)p * 4 + 15) & ~15u) : 0u;
-        const uint32_t bu = ((uint32_t)min(nkt * kI8StepTerms, P.kk) * 8 + 15) & ~15u;
+        const uint32_t bu = ((uint32_t)nkt * kI8StepTerms * 4 + 15) & ~15u;     // i8_elog rows hold kk + 16
         tc::mbar_expect_tx(tabbar, blo + bhi + bu);
         tc::bulk_g2s(sTlo, P.i8_tlo + (int64_t)s * P.i8_tstride, blo, tabbar);
         if (bhi) tc::bulk_g2s(smem_raw + A.thi_off, P.i8_thi + (int64_t)s * P.i8_tstride, bhi, tabbar);
-        tc::bulk_g2s(sU, P.u_all + (int64_t)s * P.kk, bu, tabbar);
+        tc::bulk_g2s(sU, P.i8_elog + (int64_t)s * P.i8_estride, bu, tabbar);
       }
       tc::mbar_wait(tabbar, tabphase);
       tabphase ^= 1;
@@ -296,15 +300,14 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       // ---------------- A generators + epilogue: warp g owns TMEM lanes / rows 32 (g % 4) .., terms 8 (g / 4) ..
       const int quarter = warp & 3, half = warp >> 2;
       const int row = 32 * quarter + lane;
-      const unsigned h = (unsigned)(tl.ht * kI8Rows + row);
-      const unsigned magic = 0xFFFFFFFFu / (unsigned)p + 1u;
+      const unsigned h = (unsigned)(tl.ht * kI8Rows + row);        // row f of the discrete-log order
       const uint32_t lane_addr = tbase + ((uint32_t)(32 * quarter) << 16);
       const uint32_t ta0 = lane_addr + (uint32_t)(S * W) + 4 * half;
       // software pipeline: the limbs of step kq + 1 are gathered while the tensor core works on step kq and
       // before the slot they go to is free; only the TMEM store + arrive sit on the critical path
       uint32_t w[S][4];
-      const int2* ub = sU + ks_lo * kI8StepTerms + 8 * half;
-      if (A.dbg != 3) gen_limbs<S>(w, ub, sTlo, sThi, h, magic, p, A.dbg);
+      const int* ub = sU + ks_lo * kI8StepTerms + 8 * half;
+      if (A.dbg != 3) gen_limbs<S>(w, ub, sTlo, sThi, (int)h, p - 1, A.dbg);
       int sl = 0;
       for (int kq = 0; kq < nk; ++kq, sl = (sl + 1 == nsl ? 0 : sl + 1)) {
         if (warp == 0) {                                           // B of this step landed (MMA waits on afull only)
@@ -328,7 +331,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(afull + sl);
-        if (kq + 1 < nk && A.dbg != 3) gen_limbs<S>(w, ub + (kq + 1) * kI8StepTerms, sTlo, sThi, h, magic, p, A.dbg);
+        if (kq + 1 < nk && A.dbg != 3) gen_limbs<S>(w, ub + (kq + 1) * kI8StepTerms, sTlo, sThi, (int)h, p - 1, A.dbg);
       }
       // epilogue: sum the S weights in FP64 (lowest first); the two warps of a lane quarter take alternate
       // 16-column chunks
@@ -487,7 +490,7 @@ static size_t i8_smem(const I8Config& c, int p, int nkt, int nb, uint32_t* tab_o
   *thi_off = (uint32_t)o;
   o += c.S > 4 ? (((size_t)p * 4 + 15) & ~(size_t)15) : 0;
   *u_off = (uint32_t)o;
-  o += (size_t)nkt * kI8StepTerms * 8 + 16;
+  o += (size_t)nkt * kI8StepTerms * 4 + 16;
   return o;
 }
 
@@ -508,6 +511,20 @@ cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, 
   DevParams Q = P;
   Q.batch = n_signals;
   if (total > 0) i8_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, K, only_retilted ? 1 : 0);
+  return cudaGetLastError();
+}
+
+// stage entry point: lines of signal 0 from discrete-log order back to natural order, out [L][p]
+__global__ void i8_unpermute_kernel(DevParams P, int32_t p, double2* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)P.L * p) return;
+  const int n = (int)(i / p), f = (int)(i % p);
+  out[(int64_t)n * p + P.i8_pw[f]] = P.lines[(int64_t)n * P.p_stride + f];
+}
+
+cudaError_t launch_i8_unpermute(const DevParams& P, int32_t p, double* out, cudaStream_t st) {
+  const int64_t tot = (int64_t)P.L * p;
+  if (tot > 0) i8_unpermute_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(P, p, reinterpret_cast<double2*>(out));
   return cudaGetLastError();
 }
 

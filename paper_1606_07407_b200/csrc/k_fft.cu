@@ -347,6 +347,78 @@ __device__ __forceinline__ double2 chirp_value(int64_t q, int64_t p) {
   return make_double2(c, -s);
 }
 
+// ---- discrete-log row order of the int8-limb exp-sum (reading R22) ----
+__device__ __forceinline__ uint32_t mulmod32(uint32_t a, uint32_t b, uint32_t p) { return (uint32_t)(((uint64_t)a * b) % p); }
+__device__ uint32_t powmod32(uint32_t g, uint32_t e, uint32_t p) {
+  uint32_t r = 1 % p;
+  while (e) {
+    if (e & 1) r = mulmod32(r, g, p);
+    g = mulmod32(g, g, p);
+    e >>= 1;
+  }
+  return r;
+}
+// smallest primitive root of the prime p: g^((p-1)/q) != 1 for every prime factor q of p - 1
+__device__ uint32_t primitive_root(uint32_t p) {
+  if (p == 2) return 1;
+  uint32_t f[16];
+  int nf = 0;
+  uint32_t n = p - 1;
+  for (uint32_t q = 2; q * q <= n; ++q)
+    if (n % q == 0) {
+      f[nf++] = q;
+      while (n % q == 0) n /= q;
+    }
+  if (n > 1) f[nf++] = n;
+  for (uint32_t g = 2; g < p; ++g) {
+    bool ok = true;
+    for (int i = 0; i < nf && ok; ++i) ok = powmod32(g, (p - 1) / f[i], p) != 1;
+    if (ok) return g;
+  }
+  return 1;
+}
+// T[f] = limbs of W_p[g^f] (f < p-1), T[p-1] = limbs of W_p[0]; pw[f]; dlog; e_j of the iteration's terms
+__device__ void i8_log_tables(const DevParams& P, int s, int p) {
+  __shared__ uint32_t s_g;
+  if (threadIdx.x == 0) s_g = primitive_root((uint32_t)p);
+  __syncthreads();
+  const uint32_t g = s_g, n1 = (uint32_t)p - 1;
+  const int64_t base = (int64_t)s * P.i8_tstride;
+  const uint32_t per = (n1 + blockDim.x - 1) / blockDim.x;
+  const uint32_t f0 = threadIdx.x * per;
+  uint32_t x = f0 < n1 ? powmod32(g, f0, (uint32_t)p) : 0;
+  for (uint32_t f = f0; f < n1 && f < f0 + per; ++f) {
+    P.i8_pw[base + f] = (int32_t)x;
+    P.i8_dlog[base + x] = (int32_t)f;
+    P.i8_chl[base + f] = chirp_value(x, p);
+    double sn, cs;
+    sincospi(2.0 * (double)x / (double)p, &sn, &cs);   // W_p[x] = e^{+2 pi i x / p}, exact rational argument
+    uint2 lo;
+    uint32_t hi;
+    i8_root_entry(cs, sn, P.i8_S, lo, hi);
+    P.i8_tlo[base + f] = lo;
+    P.i8_thi[base + f] = hi;
+    x = mulmod32(x, g, (uint32_t)p);
+  }
+  if (threadIdx.x == 0) {
+    uint2 lo;
+    uint32_t hi;
+    i8_root_entry(1.0, 0.0, P.i8_S, lo, hi);
+    P.i8_pw[base + n1] = 0;
+    P.i8_chl[base + n1] = chirp_value(0, p);
+    P.i8_tlo[base + n1] = lo;
+    P.i8_thi[base + n1] = hi;
+  }
+  __syncthreads();
+  const int K = P.k + P.st_nR[s];
+  const int2* ug = P.u_all + (int64_t)s * P.kk;
+  int32_t* eg = P.i8_elog + (int64_t)s * P.i8_estride;
+  for (int j = threadIdx.x; j < K; j += blockDim.x) {
+    const int u = ug[j].x;
+    eg[j] = u ? P.i8_dlog[base + u] : -1;
+  }
+}
+
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
 // BIG: sizes >= 4096 whose plans use in-register radices up to 16 (512 threads, 128 registers);
 // small sizes use radices <= 8 with 64 registers so that several CTAs share an SM.
@@ -383,19 +455,13 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(
     double sn, cs;
     sincospi(2.0 * (double)q / (double)p, &sn, &cs);   // e^{+2 pi i q/p}
     W[q] = make_double2(cs, sn);
-    if (P.i8_S > 0) {                                      // root limb table of the int8-limb exp-sum
-      uint2 lo;
-      uint32_t hi;
-      i8_root_entry(cs, sn, P.i8_S, lo, hi);
-      P.i8_tlo[(int64_t)s * P.i8_tstride + q] = lo;
-      P.i8_thi[(int64_t)s * P.i8_tstride + q] = hi;
-    }
     const double2 w = chirp_value(q, p);
     ch[q] = w;
     const double2 vq = make_double2(w.x, -w.y);        // conj(w[q]) = kernel value at +-q
     x[q] = vq;
     if (q > 0) x[M - q] = vq;
   }
+  if (P.i8_S > 0) i8_log_tables(P, s, p);
   __syncthreads();
   fft_dif<BIG>(P, x, fi, tb);
   const double inv = 1.0 / (double)M;
@@ -418,7 +484,39 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   load_twiddles(P, fi, tb);
   const double2* ch = P.chirp + (int64_t)s * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
-  if (ksplit == 1) {
+  if (P.lines_log) {
+    // the int8 exp-sum wrote the samples in discrete-log order: position f holds h = pw[f]
+    const int32_t* pw = P.i8_pw + (int64_t)s * P.i8_tstride;
+    const double2* chl = P.i8_chl + (int64_t)s * P.i8_tstride;
+    const int n_slots = gridDim.x / n_lines;
+    for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
+    if (ksplit == 1) {
+      for (int f0 = threadIdx.x; f0 < p; f0 += 4 * blockDim.x) {   // coalesced loads, 4 in flight
+        double2 v[4], c[4];
+        int h[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int f = f0 + u * blockDim.x;
+          v[u] = f < p ? line[f] : make_double2(0.0, 0.0);
+          c[u] = f < p ? chl[f] : make_double2(0.0, 0.0);
+          h[u] = f < p ? pw[f] : -1;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (h[u] >= 0) x[h[u]] = cmulx(v[u], c[u]);
+      }
+    } else {
+      for (int f = threadIdx.x; f < p; f += blockDim.x) {
+        double2 v = make_double2(0.0, 0.0);
+        for (int ks = 0; ks < ksplit; ++ks) {
+          const double2 t = part[(((int64_t)ks * n_slots + slot) * n_lines + n) * p_part + f];
+          v.x += t.x;
+          v.y += t.y;
+        }
+        x[pw[f]] = cmulx(v, chl[f]);
+      }
+    }
+  } else if (ksplit == 1) {
     // 4 independent loads in flight per thread (latency-bound phase)
     for (int q0 = threadIdx.x; q0 < M; q0 += 4 * blockDim.x) {
       double2 a[4], c[4];

@@ -95,8 +95,17 @@ struct DevParams {
   int32_t i8_K;                // terms held in the B limbs (k for a solve, K for the stage entry point)
   int8_t* i8_B;                // [batch][ntiles][nks][S][NT*32] B limbs in the UMMA K-major layout
   double* i8_sigma;            // [batch] coefficient scale
-  uint2* i8_tlo;               // [batch][i8_tstride] root limbs 0..3 of W_p[q] (16 bit each: re | im << 8)
-  uint32_t* i8_thi;            // [batch][i8_tstride] root limbs 4..5
+  // rows in discrete-log order (reading R22): f < p-1 is the sample h = g^f mod p (g a primitive root of p),
+  // f = p-1 is h = 0; term j enters as its discrete log e_j = log_g(u_j) (-1 when u_j = 0), so the root of
+  // (f, j) is entry (f + e_j) mod (p-1) of the table T[f] = W_p[g^f] (T[p-1] = W_p[0] = 1)
+  uint2* i8_tlo;               // [batch][i8_tstride] T[f] limbs 0..3 (16 bit each: re | im << 8)
+  uint32_t* i8_thi;            // [batch][i8_tstride] T[f] limbs 4..5
+  int32_t* i8_pw;              // [batch][i8_tstride] h of row f: g^f mod p (f < p-1), 0 (f = p-1)
+  double2* i8_chl;             // [batch][i8_tstride] Bluestein chirp in row order: chirp[pw[f]]
+  int32_t* i8_dlog;            // [batch][i8_tstride] scratch: log_g(x)
+  int32_t* i8_elog;            // [batch][i8_estride] e_j of the iteration's terms
+  int32_t i8_estride;          // >= kk + 16, multiple of 4
+  int32_t lines_log;           // launch flag: the lines hold samples in discrete-log order (int8 exp-sum)
   int64_t i8_tstride;          // >= p_stride + 8 (bulk copies round the table up to 16 bytes)
 };
 
@@ -166,6 +175,7 @@ bool i8_fits(const I8Config& c, int p, int k, int smem_optin);
 int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals);
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st,
                               bool only_retilted = false);
+cudaError_t launch_i8_unpermute(const DevParams& P, int32_t p, double* out, cudaStream_t st);
 cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_p, int32_t n_signals, int32_t ksplit,
                              double2* part, int32_t p_part, int smem_optin, cudaStream_t st);
 // k_fft.cu
