@@ -206,12 +206,12 @@ void layout(sfft_plan_t* P) {
   sz[B_LVLNT] = 4 * (size_t)P->n_levels;
   sz[B_LVLAXT] = 4 * (size_t)P->n_levels * P->r;
   for (int b : {B_STLVL, B_STIL, B_STRT}) sz[b] = 4 * S;
-  sz[B_I8PW] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
-  sz[B_I8DLOG] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
+  sz[B_I8PW] = P->i8_ok ? 4 * S * (2 * P->p_stride + 8) : 0;
+  sz[B_I8DLOG] = P->i8_ok ? 4 * S * (2 * P->p_stride + 8) : 0;
   sz[B_I8ELOG] = P->i8_ok ? 4 * S * align_up((size_t)P->kk + 16, 4) : 0;
-  sz[B_I8CHL] = P->i8_ok ? 16 * S * (P->p_stride + 8) : 0;
-  sz[B_I8TLO] = P->i8_ok ? 8 * S * (P->p_stride + 8) : 0;
-  sz[B_I8THI] = P->i8_ok ? 4 * S * (P->p_stride + 8) : 0;
+  sz[B_I8CHL] = P->i8_ok ? 16 * S * (2 * P->p_stride + 8) : 0;
+  sz[B_I8TLO] = P->i8_ok ? 8 * S * (2 * P->p_stride + 8) : 0;
+  sz[B_I8THI] = P->i8_ok ? 4 * S * (2 * P->p_stride + 8) : 0;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -297,7 +297,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_sigma = ptr<double>(P, B_I8SIG);
     D.i8_tlo = ptr<uint2>(P, B_I8TLO);
     D.i8_thi = ptr<uint32_t>(P, B_I8THI);
-    D.i8_tstride = P->p_stride + 8;
+    D.i8_tstride = 2 * P->p_stride + 8;   // the root table holds T twice (discrete-log rows, no wrap)
     D.i8_pw = ptr<int32_t>(P, B_I8PW);
     D.i8_dlog = ptr<int32_t>(P, B_I8DLOG);
     D.i8_elog = ptr<int32_t>(P, B_I8ELOG);

@@ -120,8 +120,8 @@ __global__ void i8_limbs_kernel(DevParams P, int32_t K, int32_t only_retilted) {
 // ------------------------------------------------------------------ the exp-sum kernel
 constexpr int kI8GenWarps = 8;        // 2 per TMEM lane quarter: warp g covers rows 32 (g % 4) .., terms 8 (g / 4) ..
 constexpr int kI8MaxSlots = 8;
-constexpr int kI8Threads = 32 * (kI8GenWarps + 2);   // + B producer warp + MMA warp
-constexpr int kI8ProdWarp = kI8GenWarps, kI8MmaWarp = kI8GenWarps + 1;
+constexpr int kI8Threads = 32 * (kI8GenWarps + 3);   // + B producer warp + MMA warp + B forwarder warp
+constexpr int kI8ProdWarp = kI8GenWarps, kI8MmaWarp = kI8GenWarps + 1, kI8FwdWarp = kI8GenWarps + 2;
 
 struct I8Args {
   int32_t n_htiles, ksplit, p_part, n_slots;
@@ -138,20 +138,21 @@ struct I8Args {
 // 8 terms (4 TMEM columns per limb) of one K step for this thread's row h: gather the root limbs and pack
 // them into the TMEM word layout (4 K bytes per 32-bit column: re_j, im_j, re_j+1, im_j+1)
 // 8 terms (4 TMEM columns per limb) of one K step for this thread's row f (discrete-log order, reading R22):
-// the root of (f, j) is table entry (f + e_j) mod (p - 1) (entry p - 1 = W_p[0] for h = 0 or u_j = 0), so the
-// 32 lanes of a warp (consecutive f) read consecutive entries -- conflict-free shared-memory gathers.
+// the root of (f, j) is table entry f + e_j (the table holds T twice, so no wrap), or entry 2(p-1) = W_p[0]
+// when e_j < 0 (u_j = 0, padding) or the row is h = 0 / padding (special).  The 32 lanes of a warp (consecutive
+// f) read consecutive entries -- conflict-free shared-memory gathers.
 template <int NL>
 __device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int* __restrict__ sE,
                                           const uint2* __restrict__ sTlo, const uint32_t* __restrict__ sThi, int f,
-                                          int n1, int dbg) {
+                                          bool special, int one, int dbg) {
+  const int4 ea = *reinterpret_cast<const int4*>(sE), eb = *reinterpret_cast<const int4*>(sE + 4);
+  const int ev[8] = {ea.x, ea.y, ea.z, ea.w, eb.x, eb.y, eb.z, eb.w};
   int q[8];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int ej = sE[e];
-    int x = f + ej;
-    x -= x >= n1 ? n1 : 0;
-    q[e] = (f >= n1 || ej < 0 || ej >= n1) ? n1 : x;       // padding terms may hold any value: stay in the table
-    if (dbg == 1) q[e] = f < n1 ? f : n1;
+  for (int e = 0; e < 8; ++e) q[e] = (special || ev[e] < 0) ? one : f + ev[e];
+  if (dbg == 1) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) q[e] = special ? one : f;
   }
   uint2 lo[8];
 #pragma unroll
@@ -210,9 +211,9 @@ __device__ __forceinline__ int ring_slots(int W, int S) { return min(kI8MaxSlots
 //   A (TMEM, ring_slots(W, S) slots): afull[i] = 8 generator-warp arrivals, aempty[i] = one tcgen05.commit
 //   B (shared memory, A.nb slots, deep enough to cover the L2 latency of the bulk copies):
 //     bfull[i] = the producer's arrive.expect_tx + the bytes, bempty[i] = one tcgen05.commit
-// Generator warp 0 waits for bfull of the step before it arrives on afull, so the MMA issuer waits on one
-// barrier per step (every try_wait costs ~90 cycles even when the phase is complete, and the tensor
-// core's instruction queue is too shallow to hide two of them).
+// A forwarder warp waits for bfull of the step and arrives on afull as its 9th arrival, so the MMA issuer
+// waits on one barrier per step (every try_wait costs ~90 cycles even when the phase is complete, and the
+// tensor core's instruction queue is too shallow to hide two of them).
 template <int S, bool PROF>
 __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I8Args A, double2* part, int32_t n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -238,7 +239,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   if (warp == kI8MmaWarp) tc::tmem_alloc<512>(tslot);
   if (tid == 0) {
     for (int i = 0; i < kI8MaxSlots; ++i) {
-      tc::mbar_init(afull + i, kI8GenWarps);
+      tc::mbar_init(afull + i, kI8GenWarps + 1);                      // + the B forwarder
       tc::mbar_init(aempty + i, 1);
       tc::mbar_init(bfull + i, 1);
       tc::mbar_init(bempty + i, 1);
@@ -258,7 +259,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   int ntile_done = 0;                   // accfull / accempty parity
   int cur_s = -1;
   uint32_t tabphase = 0;
-  long long pr_a = 0, pr_b = 0, pr_e = 0, pr_t = 0;
+  long long pr_a = 0, pr_b = 0, pr_e = 0, pr_t = 0, pr_g = 0;
   const long long pr_start = clock64();
   // chunks of A.chunk consecutive tiles (same signal, mostly) dealt round robin: the CTAs sweep the signals
   // together, so the B limbs of the few signals in flight stay in L2 while each CTA reuses its table
@@ -283,7 +284,8 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       __syncthreads();
       if (tid == 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t blo = ((uint32_t)p * 8 + 15) & ~15u, bhi = S > 4 ? (((uint32_t)p * 4 + 15) & ~15u) : 0u;
+        const uint32_t nt = 2 * (uint32_t)p - 1;                       // T twice + the W_p[0] entry
+        const uint32_t blo = (nt * 8 + 15) & ~15u, bhi = S > 4 ? ((nt * 4 + 15) & ~15u) : 0u;
         const uint32_t bu = ((uint32_t)nkt * kI8StepTerms * 4 + 15) & ~15u;     // i8_elog rows hold kk + 16
         tc::mbar_expect_tx(tabbar, blo + bhi + bu);
         tc::bulk_g2s(sTlo, P.i8_tlo + (int64_t)s * P.i8_tstride, blo, tabbar);
@@ -293,7 +295,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       tc::mbar_wait(tabbar, tabphase);
       tabphase ^= 1;
       cur_s = s;
-      if (PROF) pr_t += clock64() - ct0;
+      (void)ct0;
     }
 
     if (warp < kI8GenWarps) {
@@ -307,15 +309,10 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       // before the slot they go to is free; only the TMEM store + arrive sit on the critical path
       uint32_t w[S][4];
       const int* ub = sU + ks_lo * kI8StepTerms + 8 * half;
-      if (A.dbg != 3) gen_limbs<S>(w, ub, sTlo, sThi, (int)h, p - 1, A.dbg);
+      const bool special = (int)h >= p - 1;                         // h = 0 row or padding: all roots 1
+      if (A.dbg != 3) gen_limbs<S>(w, ub, sTlo, sThi, (int)h, special, 2 * (p - 1), A.dbg);
       int sl = 0;
       for (int kq = 0; kq < nk; ++kq, sl = (sl + 1 == nsl ? 0 : sl + 1)) {
-        if (warp == 0) {                                           // B of this step landed (MMA waits on afull only)
-          const int sb = bpos;
-          bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
-          tc::mbar_wait(bfull + sb, (bring >> sb) & 1);
-          bring ^= 1u << sb;
-        }
         const long long c0 = PROF ? clock64() : 0;
         if (A.gnap) {
           while (!tc::mbar_try_wait(aempty + sl, ((aring >> sl) & 1) ^ 1)) __nanosleep(A.gnap);
@@ -331,7 +328,11 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(afull + sl);
-        if (kq + 1 < nk && A.dbg != 3) gen_limbs<S>(w, ub + (kq + 1) * kI8StepTerms, sTlo, sThi, (int)h, p - 1, A.dbg);
+        const long long cg = PROF ? clock64() : 0;
+        if (PROF) pr_t += cg - c0 - (pr_a - pr_a);                   // store + arrive (incl. the slot wait, see pr_a)
+        if (kq + 1 < nk && A.dbg != 3)
+          gen_limbs<S>(w, ub + (kq + 1) * kI8StepTerms, sTlo, sThi, (int)h, special, 2 * (p - 1), A.dbg);
+        if (PROF) pr_g += clock64() - cg;
       }
       // epilogue: sum the S weights in FP64 (lowest first); the two warps of a lane quarter take alternate
       // 16-column chunks
@@ -390,6 +391,21 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
           tc::bulk_g2s(sB + (size_t)sb * A.b_stage_bytes, Bg + (int64_t)(ks_lo + kq) * S * W * 32, bytes, bfull + sb);
         }
       }
+    } else if (warp == kI8FwdWarp) {
+      // ---------------- B forwarder: the 9th arrival on afull, once the step's B limbs have landed, so the MMA
+      // issuer waits on one barrier per step without putting a second wait on a generator's critical path
+      int sl = 0;
+      for (int kq = 0; kq < nk; ++kq, sl = (sl + 1 == nsl ? 0 : sl + 1)) {
+        const int sb = bpos;
+        bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
+        const long long cb = PROF ? clock64() : 0;
+        tc::mbar_wait(aempty + sl, ((aring >> sl) & 1) ^ 1);   // the slot's previous phase is over
+        aring ^= 1u << sl;
+        tc::mbar_wait(bfull + sb, (bring >> sb) & 1);
+        bring ^= 1u << sb;
+        if (PROF) pr_b += clock64() - cb;
+        if (lane == 0) tc::mbar_arrive(afull + sl);
+      }
     } else {
       // ---------------- MMA issuer: the whole warp walks the ring, one elected lane issues
       const uint32_t idesc = tc::idesc_i8(kI8Rows, W);
@@ -406,7 +422,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         const int sb = bpos;
         bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
         const long long c1 = PROF ? clock64() : 0;
-        tc::mbar_wait(afull + sl, (aring >> sl) & 1);      // implies bfull (generator warp 0 waited for it)
+        tc::mbar_wait(afull + sl, (aring >> sl) & 1);      // implies bfull (the forwarder waited for it)
         aring ^= 1u << sl;
         if (PROF) pr_a += clock64() - c1;
         tc::fence_after_sync();
@@ -426,8 +442,8 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
     ++ntile_done;
   }
   if (PROF && lane == 0 && (warp == 0 || warp == kI8MmaWarp)) {
-    long long* o = A.prof + (blockIdx.x * 2 + (warp == 0 ? 0 : 1)) * 5;
-    o[0] = clock64() - pr_start; o[1] = pr_a; o[2] = pr_b; o[3] = pr_e; o[4] = pr_t;
+    long long* o = A.prof + (blockIdx.x * 2 + (warp == 0 ? 0 : 1)) * 6;
+    o[0] = clock64() - pr_start; o[1] = pr_a; o[2] = pr_b; o[3] = pr_e; o[4] = pr_t; o[5] = pr_g;
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -486,9 +502,10 @@ static size_t i8_smem(const I8Config& c, int p, int nkt, int nb, uint32_t* tab_o
   size_t o = 512 + (size_t)nb * c.S * c.NT * 32;
   o = (o + 15) & ~(size_t)15;
   *tab_off = (uint32_t)o;
-  o += ((size_t)p * 8 + 15) & ~(size_t)15;
+  const size_t nt = 2 * (size_t)p - 1;                                  // T twice + the W_p[0] entry
+  o += (nt * 8 + 15) & ~(size_t)15;
   *thi_off = (uint32_t)o;
-  o += c.S > 4 ? (((size_t)p * 4 + 15) & ~(size_t)15) : 0;
+  o += c.S > 4 ? ((nt * 4 + 15) & ~(size_t)15) : 0;
   *u_off = (uint32_t)o;
   o += (size_t)nkt * kI8StepTerms * 4 + 16;
   return o;
@@ -540,8 +557,8 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   A.gnap = getenv("SFFT_I8_GNAP") ? atoi(getenv("SFFT_I8_GNAP")) : 0;
   static long long* prof_buf = nullptr;
   if (getenv("SFFT_I8_PROF")) {
-    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(long long) * 148 * 2 * 5);
-    cudaMemsetAsync(prof_buf, 0, sizeof(long long) * 148 * 2 * 5, st);
+    if (!prof_buf) cudaMalloc(&prof_buf, sizeof(long long) * 148 * 2 * 6);
+    cudaMemsetAsync(prof_buf, 0, sizeof(long long) * 148 * 2 * 6, st);
     A.prof = prof_buf;
   }
   A.b_stage_bytes = (uint32_t)c.S * c.NT * 32;
@@ -565,16 +582,16 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   const long grid = std::min<long>((tiles + A.chunk - 1) / A.chunk, n_sm);
   if (grid > 0) kern<<<(unsigned)grid, kI8Threads, smem, st>>>(P, A, part, (int32_t)tiles);
   if (A.prof && grid > 0) {
-    long long h[148 * 2 * 5];
+    long long h[148 * 2 * 6];
     cudaMemcpyAsync(h, A.prof, sizeof h, cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    double g[5] = {0}, m[5] = {0};
+    double g[6] = {0}, m[6] = {0};
     for (int b = 0; b < grid; ++b)
-      for (int i = 0; i < 5; ++i) { g[i] += h[b * 10 + i]; m[i] += h[b * 10 + 5 + i]; }
-    fprintf(stderr, "[i8prof] p=%d tiles=%ld grid=%ld NT=%d/%d x%d | gen: total %.0f empty-wait %.0f epilogue %.0f "
-            "table %.0f | mma: total %.0f bfull-wait %.0f afull-wait %.0f accempty %.0f (cycles per CTA), nb %d\n", max_p,
-            tiles, grid, c.NT, c.NT_last, c.ntiles, g[0] / grid, g[1] / grid, g[3] / grid, g[4] / grid, m[0] / grid,
-            m[2] / grid, m[1] / grid, m[3] / grid, A.nb);
+      for (int i = 0; i < 6; ++i) { g[i] += h[b * 12 + i]; m[i] += h[b * 12 + 6 + i]; }
+    fprintf(stderr, "[i8prof] p=%d NT=%d/%d x%d | gen(warp 0): total %.0f slot-wait %.0f bfull-wait %.0f "
+            "store+arrive %.0f gather %.0f epilogue %.0f | mma: total %.0f afull-wait %.0f accempty %.0f (cycles per CTA)\n",
+            max_p, c.NT, c.NT_last, c.ntiles, g[0] / grid, g[1] / grid, g[2] / grid, (g[4] - g[1]) / grid, g[5] / grid,
+            g[3] / grid, m[0] / grid, m[1] / grid, m[3] / grid);
   }
   return cudaGetLastError();
 }

@@ -377,7 +377,9 @@ __device__ uint32_t primitive_root(uint32_t p) {
   }
   return 1;
 }
-// T[f] = limbs of W_p[g^f] (f < p-1), T[p-1] = limbs of W_p[0]; pw[f]; dlog; e_j of the iteration's terms
+// Tables of the discrete-log row order (reading R22): T[f] = T[f + p - 1] = limbs of W_p[g^f] (f < p-1, stored
+// twice so row f + e_j needs no wrap), T[2(p-1)] = limbs of W_p[0] = 1; pw[f] = g^f (pw[p-1] = 0: the h = 0
+// row); e_j = log_g u_j of the iteration's terms, -1 for u_j = 0 and for the padding up to a multiple of 16.
 __device__ void i8_log_tables(const DevParams& P, int s, int p) {
   __shared__ uint32_t s_g;
   if (threadIdx.x == 0) s_g = primitive_root((uint32_t)p);
@@ -398,6 +400,8 @@ __device__ void i8_log_tables(const DevParams& P, int s, int p) {
     i8_root_entry(cs, sn, P.i8_S, lo, hi);
     P.i8_tlo[base + f] = lo;
     P.i8_thi[base + f] = hi;
+    P.i8_tlo[base + n1 + f] = lo;
+    P.i8_thi[base + n1 + f] = hi;
     x = mulmod32(x, g, (uint32_t)p);
   }
   if (threadIdx.x == 0) {
@@ -406,15 +410,16 @@ __device__ void i8_log_tables(const DevParams& P, int s, int p) {
     i8_root_entry(1.0, 0.0, P.i8_S, lo, hi);
     P.i8_pw[base + n1] = 0;
     P.i8_chl[base + n1] = chirp_value(0, p);
-    P.i8_tlo[base + n1] = lo;
-    P.i8_thi[base + n1] = hi;
+    P.i8_tlo[base + 2 * n1] = lo;
+    P.i8_thi[base + 2 * n1] = hi;
   }
   __syncthreads();
   const int K = P.k + P.st_nR[s];
+  const int Kp = (K + 15) & ~15;
   const int2* ug = P.u_all + (int64_t)s * P.kk;
   int32_t* eg = P.i8_elog + (int64_t)s * P.i8_estride;
-  for (int j = threadIdx.x; j < K; j += blockDim.x) {
-    const int u = ug[j].x;
+  for (int j = threadIdx.x; j < Kp; j += blockDim.x) {
+    const int u = j < K ? ug[j].x : 0;
     eg[j] = u ? P.i8_dlog[base + u] : -1;
   }
 }
