@@ -65,6 +65,8 @@ struct sfft_plan_s {
   int32_t expsum_path = 0;     // sfft_options.expsum_path
   // stall fallback levels (reading R23): level 0 = the plan's own tilts / E
   int32_t n_levels = 1, lvl_tmax = 1;
+  int32_t n_tslots = 0;          // per-prime table cache slots (+1 reserved for the stage entry points)
+  int32_t epoch = 0;             // iteration counter across executes (table cache LRU stamp)
   std::vector<int64_t> lvl_E, lvl_lo, lvl_hi, lvl_tilts;
   std::vector<int32_t> lvl_nt, lvl_axt;
   int smem_optin = 0;
@@ -89,7 +91,7 @@ enum Buf {
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
-  B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_I8TLO, B_I8THI,
+  B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -168,9 +170,10 @@ void layout(sfft_plan_t* P) {
   sz[B_VALL] = 8 * S * P->r * P->kk;
   sz[B_CALL] = 16 * S * P->kk * P->Lp;
   sz[B_LINES] = 16 * S * P->L * P->p_stride;
-  sz[B_WTAB] = 16 * S * P->p_stride;
-  sz[B_CHIRP] = 16 * S * P->p_stride;
-  sz[B_V] = 16 * S * P->M_stride;
+  const size_t T = (size_t)P->n_tslots + 1;          // table slots (per prime), not per signal
+  sz[B_WTAB] = 16 * T * P->p_stride;
+  sz[B_CHIRP] = 16 * T * P->p_stride;
+  sz[B_V] = 16 * T * P->M_stride;
   sz[B_AREG] = 16 * S * P->k;
   sz[B_KHASH] = 8 * S * P->k;
   sz[B_HTAB] = 4 * S * P->H;
@@ -206,12 +209,16 @@ void layout(sfft_plan_t* P) {
   sz[B_LVLNT] = 4 * (size_t)P->n_levels;
   sz[B_LVLAXT] = 4 * (size_t)P->n_levels * P->r;
   for (int b : {B_STLVL, B_STIL, B_STRT}) sz[b] = 4 * S;
-  sz[B_I8PW] = P->i8_ok ? 4 * S * (2 * P->p_stride + 8) : 0;
-  sz[B_I8DLOG] = P->i8_ok ? 4 * S * (2 * P->p_stride + 8) : 0;
+  sz[B_I8PW] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_I8DLOG] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
   sz[B_I8ELOG] = P->i8_ok ? 4 * S * align_up((size_t)P->kk + 16, 4) : 0;
-  sz[B_I8CHL] = P->i8_ok ? 16 * S * (2 * P->p_stride + 8) : 0;
-  sz[B_I8TLO] = P->i8_ok ? 8 * S * (2 * P->p_stride + 8) : 0;
-  sz[B_I8THI] = P->i8_ok ? 4 * S * (2 * P->p_stride + 8) : 0;
+  sz[B_I8CHL] = P->i8_ok ? 16 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_STSLOT] = 4 * S;
+  sz[B_SLOTP] = 4 * T;
+  sz[B_SLOTE] = 4 * T;
+  sz[B_FILL] = 4 * T;
+  sz[B_I8TLO] = P->i8_ok ? 8 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -290,6 +297,11 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_lvl = ptr<int32_t>(P, B_STLVL);
   D.st_il = ptr<int32_t>(P, B_STIL);
   D.st_retilt = ptr<int32_t>(P, B_STRT);
+  D.n_tslots = P->n_tslots;
+  D.st_slot = ptr<int32_t>(P, B_STSLOT);
+  D.slot_p = ptr<int32_t>(P, B_SLOTP);
+  D.slot_epoch = ptr<int32_t>(P, B_SLOTE);
+  D.fill = ptr<int32_t>(P, B_FILL);
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
@@ -355,6 +367,9 @@ int ensure_ready(sfft_plan_t* P) {
     CUDA_TRY(P, up(B_LVLNT, P->lvl_nt.data(), 4 * P->lvl_nt.size()));
     CUDA_TRY(P, up(B_LVLAXT, P->lvl_axt.data(), 4 * P->lvl_axt.size()));
     CUDA_TRY(P, launch_fft_twiddles(ptr<double2>(P, B_TW), ptr<int4>(P, B_TWSEG), (int)P->tw_seg.size(), P->stream));
+    // empty per-prime table cache (slot_p = 0, slot_epoch = -1)
+    CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SLOTP), 0, 4 * ((size_t)P->n_tslots + 1), P->stream));
+    CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SLOTE), 0xFF, 4 * ((size_t)P->n_tslots + 1), P->stream));
     CUDA_TRY(P, cudaStreamSynchronize(P->stream));
     P->tables_ready = true;
   }
@@ -643,6 +658,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   if (8 * (size_t)P->p_stride + 4 * (2 * (size_t)P->p_stride + 2 * (size_t)k + 64) > (size_t)smem_optin)
     return SFFT_ENOTSUP;
   if (8 * (size_t)k > (size_t)smem_optin) return SFFT_ENOTSUP;
+  P->n_tslots = P->batch + 16;    // at most batch primes are live per iteration; the rest keeps recent primes
   layout(P.get());
   *out = P.release();
   return SFFT_OK;
@@ -762,7 +778,8 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     if (P->profile) it_marks.push_back(n_ev);
     mark();
     const int big = max_M >= kFftBigM;
-    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, st));
+    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, st, ++P->epoch));
+    launches += 2;   // tables_assign, terms
     mark();
     if (use_i8)
       LAUNCH(P, launch_expsum_i8(D, P->i8, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, P->smem_optin, st));
@@ -881,6 +898,8 @@ int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, cons
 // ---------------------------------------------------------------- stage entry points
 static int set_signal0_state(sfft_plan_t* P, const DevParams& D, int p, int m, int nR) {
   int32_t h[5] = {ST_RUN, nR, p, m, 0};
+  const int32_t stage_slot = P->n_tslots;             // reserved table slot of the stage entry points
+  CUDA_TRY(P, cudaMemcpyAsync(D.st_slot, &stage_slot, 4, cudaMemcpyHostToDevice, P->stream));
   CUDA_TRY(P, cudaMemcpyAsync(D.active, &h[4], 4, cudaMemcpyHostToDevice, P->stream));
   CUDA_TRY(P, cudaMemcpyAsync(D.st_status, &h[0], 4, cudaMemcpyHostToDevice, P->stream));
   CUDA_TRY(P, cudaMemcpyAsync(D.st_nR, &h[1], 4, cudaMemcpyHostToDevice, P->stream));
@@ -908,7 +927,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
   LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->fft[fi].M >= kFftBigM,
-                            P->stream));
+                            P->stream, 0, true));
   if (P->i8_ok && i8_use_for(P, (int)p)) {
     D.i8_K = K;
     LAUNCH(P, launch_i8_prepare(D, 1, K, P->stream));
@@ -938,7 +957,7 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
   const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M), big = P->fft[fi].M >= kFftBigM;
-  LAUNCH(P, launch_fft_prep(D, 1, sm, th, big, P->stream));
+  LAUNCH(P, launch_fft_prep(D, 1, sm, th, big, P->stream, 0, true));
   LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, big, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;

@@ -68,7 +68,7 @@ expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles,
   const int wn = warp % wn_count, wh = warp / wn_count;
 
   // root table of this signal's prime (computed by the prep kernel)
-  const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
+  const double2* Wg = P.W_tab + (int64_t)P.st_slot[s] * P.p_stride;
   for (int q = tid; q < p; q += WARPS * 32) sW[q] = Wg[q];
 
   const double2* Cg = P.C_all + (int64_t)s * P.kk * P.Lp + (int64_t)nt * BN;
@@ -334,7 +334,7 @@ expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t kspl
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wg = warp / WPG, wr = warp % WPG;
-  const double2* Wg = P.W_tab + (int64_t)s * P.p_stride;
+  const double2* Wg = P.W_tab + (int64_t)P.st_slot[s] * P.p_stride;
   for (int q = tid; q < p; q += WARPS * 32) cp_async16(sW + q, Wg + q, true);   // joins the first stage group
 
   const int2* ug = P.u_all + (int64_t)s * P.kk;

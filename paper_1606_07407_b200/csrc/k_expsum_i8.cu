@@ -288,8 +288,9 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         const uint32_t blo = (nt * 8 + 15) & ~15u, bhi = S > 4 ? ((nt * 4 + 15) & ~15u) : 0u;
         const uint32_t bu = ((uint32_t)nkt * kI8StepTerms * 4 + 15) & ~15u;     // i8_elog rows hold kk + 16
         tc::mbar_expect_tx(tabbar, blo + bhi + bu);
-        tc::bulk_g2s(sTlo, P.i8_tlo + (int64_t)s * P.i8_tstride, blo, tabbar);
-        if (bhi) tc::bulk_g2s(smem_raw + A.thi_off, P.i8_thi + (int64_t)s * P.i8_tstride, bhi, tabbar);
+        const int64_t tab0 = (int64_t)P.st_slot[s] * P.i8_tstride;     // the signal's table slot
+        tc::bulk_g2s(sTlo, P.i8_tlo + tab0, blo, tabbar);
+        if (bhi) tc::bulk_g2s(smem_raw + A.thi_off, P.i8_thi + tab0, bhi, tabbar);
         tc::bulk_g2s(sU, P.i8_elog + (int64_t)s * P.i8_estride, bu, tabbar);
       }
       tc::mbar_wait(tabbar, tabphase);
@@ -536,7 +537,7 @@ __global__ void i8_unpermute_kernel(DevParams P, int32_t p, double2* __restrict_
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= (int64_t)P.L * p) return;
   const int n = (int)(i / p), f = (int)(i % p);
-  out[(int64_t)n * p + P.i8_pw[f]] = P.lines[(int64_t)n * P.p_stride + f];
+  out[(int64_t)n * p + P.i8_pw[(int64_t)P.st_slot[0] * P.i8_tstride + f]] = P.lines[(int64_t)n * P.p_stride + f];
 }
 
 cudaError_t launch_i8_unpermute(const DevParams& P, int32_t p, double* out, cudaStream_t st) {

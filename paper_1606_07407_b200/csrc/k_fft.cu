@@ -380,12 +380,12 @@ __device__ uint32_t primitive_root(uint32_t p) {
 // Tables of the discrete-log row order (reading R22): T[f] = T[f + p - 1] = limbs of W_p[g^f] (f < p-1, stored
 // twice so row f + e_j needs no wrap), T[2(p-1)] = limbs of W_p[0] = 1; pw[f] = g^f (pw[p-1] = 0: the h = 0
 // row); e_j = log_g u_j of the iteration's terms, -1 for u_j = 0 and for the padding up to a multiple of 16.
-__device__ void i8_log_tables(const DevParams& P, int s, int p) {
+__device__ void i8_log_tables(const DevParams& P, int slot, int p) {
   __shared__ uint32_t s_g;
   if (threadIdx.x == 0) s_g = primitive_root((uint32_t)p);
   __syncthreads();
   const uint32_t g = s_g, n1 = (uint32_t)p - 1;
-  const int64_t base = (int64_t)s * P.i8_tstride;
+  const int64_t base = (int64_t)slot * P.i8_tstride;
   const uint32_t per = (n1 + blockDim.x - 1) / blockDim.x;
   const uint32_t f0 = threadIdx.x * per;
   uint32_t x = f0 < n1 ? powmod32(g, f0, (uint32_t)p) : 0;
@@ -413,47 +413,122 @@ __device__ void i8_log_tables(const DevParams& P, int s, int p) {
     P.i8_tlo[base + 2 * n1] = lo;
     P.i8_thi[base + 2 * n1] = hi;
   }
+}
+
+// ---- table cache: slot assignment (one CTA) ----
+// Hits reuse their slot; the distinct missing primes get slots not used in this epoch (at most n_active slots
+// are in use, the cache has n_active + 16 or more), which are queued in fill[] for tables_fill.
+__global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_t epoch) {
+  extern __shared__ int sm[];
+  int* sp = sm;                                      // [n_tslots] primes of the slots
+  int* hkey = sp + P.n_tslots;                       // [2048] hash of missing primes
+  int* hidx = hkey + 2048;                           // [2048] their rank
+  __shared__ int n_miss, n_free;
+  const int n_active = P.ctrl[0];
+  const int C = P.n_tslots;
+  for (int i = threadIdx.x; i < C; i += blockDim.x) sp[i] = P.slot_p[i];
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) hkey[i] = 0;
+  if (threadIdx.x == 0) { n_miss = 0; n_free = 0; }
   __syncthreads();
-  const int K = P.k + P.st_nR[s];
-  const int Kp = (K + 15) & ~15;
-  const int2* ug = P.u_all + (int64_t)s * P.kk;
-  int32_t* eg = P.i8_elog + (int64_t)s * P.i8_estride;
-  for (int j = threadIdx.x; j < Kp; j += blockDim.x) {
-    const int u = j < K ? ug[j].x : 0;
-    eg[j] = u ? P.i8_dlog[base + u] : -1;
+  for (int a = threadIdx.x; a < n_active; a += blockDim.x) {
+    const int s = P.active[a];
+    const int p = P.st_p[s];
+    int hit = -1;
+    for (int i = 0; i < C; ++i)
+      if (sp[i] == p) { hit = i; break; }
+    if (hit >= 0) {
+      P.st_slot[s] = hit;
+      P.slot_epoch[hit] = epoch;
+    } else {
+      int h = (p * 40503) & 2047;
+      for (;;) {
+        const int old = atomicCAS(&hkey[h], 0, p);
+        if (old == 0) { hidx[h] = atomicAdd(&n_miss, 1); break; }
+        if (old == p) break;
+        h = (h + 1) & 2047;
+      }
+    }
   }
+  __syncthreads();
+  // slots free for this epoch, in index order (warp 0, deterministic)
+  if (threadIdx.x < 32) {
+    int base = 0;
+    for (int i0 = 0; i0 < C; i0 += 32) {
+      const int i = i0 + threadIdx.x;
+      const bool fr = i < C && P.slot_epoch[i] != epoch;
+      const unsigned b = __ballot_sync(0xffffffffu, fr);
+      if (fr) {
+        const int r = base + __popc(b & ((1u << threadIdx.x) - 1u));
+        if (r < n_miss) P.fill[r] = i;
+      }
+      base += __popc(b);
+    }
+    if (threadIdx.x == 0) n_free = base;
+  }
+  __syncthreads();
+  for (int h = threadIdx.x; h < 2048; h += blockDim.x) {
+    const int p = hkey[h];
+    if (p == 0 || hidx[h] >= n_free) continue;
+    const int slot = P.fill[hidx[h]];
+    P.slot_p[slot] = p;
+    P.slot_epoch[slot] = epoch;
+    sp[slot] = p;
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < n_active; a += blockDim.x) {
+    const int s = P.active[a];
+    const int p = P.st_p[s];
+    for (int i = 0; i < C; ++i)
+      if (sp[i] == p) { P.st_slot[s] = i; break; }
+  }
+  if (threadIdx.x == 0) P.ctrl[3] = min(n_miss, n_free);
+}
+
+// ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
+__global__ void terms_kernel(DevParams P) {
+  const int s = P.active[blockIdx.x];
+  const int p = P.st_p[s];
+  if (threadIdx.x == 0) P.st_M[s] = find_fft_index(P, p);
+  const int m = P.st_m[s];
+  const int K = P.k + P.st_nR[s];
+  const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;
+  int2* ug = P.u_all + (int64_t)s * P.kk;
+  const int Kp = (K + 15) & ~15;
+  const int64_t base = (int64_t)P.st_slot[s] * P.i8_tstride;
+  int32_t* eg = P.i8_S > 0 ? P.i8_elog + (int64_t)s * P.i8_estride : nullptr;
+  for (int j = threadIdx.x; j < (eg ? Kp : K); j += blockDim.x) {
+    const int u = j < K ? (int)mod_pos64(vm[j], p) : 0;
+    if (j < K) ug[j] = make_int2(u, (8 * u) % p);
+    // e_j: -1 for u_j = 0 and for the padding up to a multiple of 16 (reading R22)
+    if (eg) eg[j] = u ? P.i8_dlog[base + u] : -1;
+  }
+  // the FP64 exp-sum stages the phases in 16-byte pairs: the partner of the last term must be a valid index
+  if (threadIdx.x == 0 && (K & 1)) ug[K] = make_int2(0, 0);
 }
 
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
 // BIG: sizes >= 4096 whose plans use in-register radices up to 16 (512 threads, 128 registers);
 // small sizes use radices <= 8 with 64 registers so that several CTAs share an SM.
 template <bool BIG>
-__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(DevParams P) {
+__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(DevParams P, int32_t direct) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int s = P.active[blockIdx.x];
-  const int p = P.st_p[s];
+  int slot, p;
+  if (direct) {
+    const int s = P.active[blockIdx.x];
+    slot = P.st_slot[s];
+    p = P.st_p[s];
+  } else {
+    if ((int)blockIdx.x >= P.ctrl[3]) return;
+    slot = P.fill[blockIdx.x];
+    p = P.slot_p[slot];
+  }
   const int fi = find_fft_index(P, p);
   const int M = P.fft_M[fi];
-  if (threadIdx.x == 0) P.st_M[s] = fi;
-  // term phases of this iteration (exp-sum A operand index): u_j = v_{j,m} mod p, 8 u_j mod p
-  {
-    const int m = P.st_m[s];
-    const int K = P.k + P.st_nR[s];
-    const int64_t* vm = P.v_all + ((int64_t)s * P.r + m) * P.kk;
-    int2* ug = P.u_all + (int64_t)s * P.kk;
-    for (int j = threadIdx.x; j < K; j += blockDim.x) {
-      const int u = (int)mod_pos64(vm[j], p);
-      ug[j] = make_int2(u, (8 * u) % p);
-    }
-    // the exp-sum stages the phases in 16-byte pairs: the partner of the last term must be a valid
-    // index too (its line coefficients are zero-filled, its root index must stay inside the table)
-    if (threadIdx.x == 0 && (K & 1)) ug[K] = make_int2(0, 0);
-  }
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* tb = x + M;
   load_twiddles(P, fi, tb);
-  double2* W = P.W_tab + (int64_t)s * P.p_stride;
-  double2* ch = P.chirp + (int64_t)s * P.p_stride;
+  double2* W = P.W_tab + (int64_t)slot * P.p_stride;
+  double2* ch = P.chirp + (int64_t)slot * P.p_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
   __syncthreads();
   for (int q = threadIdx.x; q < p; q += blockDim.x) {
@@ -466,11 +541,11 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(
     x[q] = vq;
     if (q > 0) x[M - q] = vq;
   }
-  if (P.i8_S > 0) i8_log_tables(P, s, p);
+  if (P.i8_S > 0) i8_log_tables(P, slot, p);
   __syncthreads();
   fft_dif<BIG>(P, x, fi, tb);
   const double inv = 1.0 / (double)M;
-  double2* V = P.V + (int64_t)s * P.M_stride;
+  double2* V = P.V + (int64_t)slot * P.M_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
 }
 
@@ -487,12 +562,13 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* tb = x + M;
   load_twiddles(P, fi, tb);
-  const double2* ch = P.chirp + (int64_t)s * P.p_stride;
+  const int tslot = P.st_slot[s];                     // table slot of the signal's prime
+  const double2* ch = P.chirp + (int64_t)tslot * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
   if (P.lines_log) {
     // the int8 exp-sum wrote the samples in discrete-log order: position f holds h = pw[f]
-    const int32_t* pw = P.i8_pw + (int64_t)s * P.i8_tstride;
-    const double2* chl = P.i8_chl + (int64_t)s * P.i8_tstride;
+    const int32_t* pw = P.i8_pw + (int64_t)tslot * P.i8_tstride;
+    const double2* chl = P.i8_chl + (int64_t)tslot * P.i8_tstride;
     const int n_slots = gridDim.x / n_lines;
     for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
     if (ksplit == 1) {
@@ -555,18 +631,39 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   }
   __syncthreads();
   fft_dif<BIG>(P, x, fi, tb, 1);
-  fft_mid<BIG>(P, x, fi, P.V + (int64_t)s * P.M_stride);
+  fft_mid<BIG>(P, x, fi, P.V + (int64_t)tslot * P.M_stride);
   fft_dit<BIG>(P, x, fi, tb, 1);
-  for (int b = threadIdx.x; b < p; b += blockDim.x) line[b] = cmulx(x[b], ch[b]);
+  // F[b] = w[b] * (conv)[b]: 4 chirp loads in flight per thread (the chirp is L2-resident, latency-bound)
+  for (int b0 = threadIdx.x; b0 < p; b0 += 4 * blockDim.x) {
+    double2 c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = b0 + u * blockDim.x;
+      c[u] = b < p ? __ldg(ch + b) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = b0 + u * blockDim.x;
+      if (b < p) line[b] = cmulx(x[b], c[u]);
+    }
+  }
 }
 
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
-                            cudaStream_t st) {
+                            cudaStream_t st, int32_t epoch, bool direct) {
+  if (n_signals <= 0) return cudaSuccess;
+  if (!direct) {
+    const size_t sm = sizeof(int) * ((size_t)P.n_tslots + 4096);
+    cudaError_t e = cudaFuncSetAttribute(tables_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    tables_assign_kernel<<<1, 1024, sm, st>>>(P, epoch);
+  }
   const size_t smem = (size_t)smem_bytes;
   auto kern = big ? fft_prep_kernel<true> : fft_prep_kernel<false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (n_signals > 0) kern<<<n_signals, threads, smem, st>>>(P);
+  kern<<<n_signals, threads, smem, st>>>(P, direct ? 1 : 0);
+  terms_kernel<<<n_signals, 256, 0, st>>>(P);
   return cudaGetLastError();
 }
 

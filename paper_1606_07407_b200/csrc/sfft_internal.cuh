@@ -79,6 +79,13 @@ struct DevParams {
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
   int32_t* active;             // [batch] indices of the signals still running this iteration
+  // per-prime tables (W_tab, chirp, V, int8 root tables) live in a cache of slots keyed by p: they depend on p
+  // only, like FFT twiddles; slot n_tslots is reserved for the stage entry points
+  int32_t n_tslots;
+  int32_t* st_slot;            // [batch] slot of the signal's current prime
+  int32_t* slot_p;             // [n_tslots] prime held by the slot, 0 = empty
+  int32_t* slot_epoch;         // [n_tslots] last iteration epoch that used the slot
+  int32_t* fill;               // [n_tslots] slots to (re)compute this iteration, count in ctrl[3]
   // stall fallback (reading R23): level 0 = the plan's own tilts and E, levels 1.. = fallback tilts
   int32_t n_levels, lvl_tmax;  // levels, tilt slots per level
   const int64_t* lvl_E;        // [n_levels]
@@ -180,8 +187,11 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
                              double2* part, int32_t p_part, int smem_optin, cudaStream_t st);
 // k_fft.cu
 // smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
+// per iteration: assign table slots to the active signals' primes (fills counted in ctrl[3]), compute the
+// tables of new primes (grid n_signals, CTAs beyond the fill count exit; direct = stage entry point: fill the
+// slot of every listed signal), then the per-signal term phases u_j / e_j and FFT size index
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
-                            cudaStream_t st);
+                            cudaStream_t st, int32_t epoch, bool direct = false);
 // threads per FFT CTA for a size (more CTAs per SM for small M)
 constexpr int kFftBigM = 4096;   // sizes >= this use radices up to 16 and the 512-thread variant
 inline int fft_threads(int M) {
