@@ -76,45 +76,46 @@ __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT
 // B limbs of signal s, n-tile nt (width W), K step ks, limb t: 32 W bytes at
 //   i8_B + s * per_signal + nt * nks * S * NT * 32 + (ks * S + t) * W * 32,  per_signal = nks * S * 32 * cols
 // in the UMMA K-major layout: (column, K byte) -> (col / 8) 256 + (k / 16) 128 + (col % 8) 16 + k % 16.
-// One thread per (signal, padded output column, K step, 4-byte K word): S words, one per limb.
-__global__ void i8_limbs_kernel(DevParams P, int32_t K, int32_t only_retilted) {
+// One CTA per (signal, n-tile, K step): the 16 terms x W/2 lines of C are read coalesced into shared
+// memory, every (column, K byte) value is split into its S digits in shared memory, and the S limb tiles
+// (contiguous in global memory) are written with 16-byte stores.
+__global__ void __launch_bounds__(256) i8_limbs_kernel(DevParams P, int32_t K, int32_t only_retilted) {
+  __shared__ double2 cv[kI8StepTerms][48];                      // [term][line of the tile] (W <= 96)
+  __shared__ __align__(16) uint8_t tiles[6 * 96 * 32];           // [limb][W * 32]
   const int NT = P.i8_NT, S = P.i8_S, ntiles = P.i8_ntiles, nks = P.i8_nks;
   const int nkt = (K + kI8StepTerms - 1) / kI8StepTerms;        // steps in use (layout stride stays nks)
   const int cols = (ntiles - 1) * NT + P.i8_NT_last;
-  const int64_t per_sig = (int64_t)cols * nkt * 8;
-  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (g >= (int64_t)P.batch * per_sig) return;
-  const int s = (int)(g / per_sig);
+  int b = blockIdx.x;
+  const int ks = b % nkt;
+  b /= nkt;
+  const int nt = b % ntiles;
+  const int s = b / ntiles;
   if (only_retilted && !P.st_retilt[s]) return;
-  int64_t r = g % per_sig;
-  const int kw = (int)(r & 7);
-  r >>= 3;
-  const int ks = (int)(r % nkt);
-  const int gc = (int)(r / nkt);                                 // padded output column
-  const int nt = gc / NT, col = gc % NT;
   const int W = i8_tile_width(nt, ntiles, NT, P.i8_NT_last);
-  const int n = gc >> 1, im_out = gc & 1;
+  const int n0 = (nt * NT) >> 1, nl = W >> 1;                     // lines of the tile
+  const double2* Cs = P.C_all + (int64_t)s * P.kk * P.Lp;
+  for (int i = threadIdx.x; i < kI8StepTerms * nl; i += blockDim.x) {
+    const int jj = i / nl, l = i - jj * nl;
+    const int j = ks * kI8StepTerms + jj, n = n0 + l;
+    cv[jj][l] = (j < K && n < P.L) ? Cs[(int64_t)j * P.Lp + n] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
   const double q = 127.0 * ldexp(1.0, 8 * (S - 1)) / P.i8_sigma[s];
-  int dg[4][8];
-#pragma unroll
-  for (int b = 0; b < 4; ++b) {
-    const int kp = 4 * kw + b;                                   // K element in the step
-    const int j = ks * kI8StepTerms + (kp >> 1);
-    double v = 0.0;
-    if (j < K && n < P.L) {
-      const double2 c = P.C_all[((int64_t)s * P.kk + j) * P.Lp + n];
-      const bool a_im = kp & 1;                                   // row 2j+1 multiplies Im W
-      v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
-    }
-    i8_digits(llrint(v * q), S, dg[b]);
+  for (int i = threadIdx.x; i < W * 32; i += blockDim.x) {
+    const int col = i >> 5, kp = i & 31;                          // output column, K byte of the step
+    const double2 c = cv[kp >> 1][col >> 1];
+    const bool a_im = kp & 1, im_out = col & 1;                   // row 2j+1 multiplies Im W; column 2n+1 is Im s_n
+    const double v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
+    int dg[8];
+    i8_digits(llrint(v * q), S, dg);
+    const int off = (col >> 3) * 256 + (kp >> 4) * 128 + (col & 7) * 16 + (kp & 15);
+    for (int t = 0; t < S; ++t) tiles[t * W * 32 + off] = (uint8_t)dg[t];
   }
+  __syncthreads();
   int8_t* base = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)nt * nks * S * NT * 32 + (int64_t)ks * S * W * 32;
-  const int off = (col >> 3) * 256 + (kw >> 2) * 128 + (col & 7) * 16 + (kw & 3) * 4;
-  for (int t = 0; t < S; ++t) {
-    const uint32_t w = (uint32_t)(uint8_t)dg[0][t] | ((uint32_t)(uint8_t)dg[1][t] << 8) |
-                       ((uint32_t)(uint8_t)dg[2][t] << 16) | ((uint32_t)(uint8_t)dg[3][t] << 24);
-    *reinterpret_cast<uint32_t*>(base + (int64_t)t * W * 32 + off) = w;
-  }
+  const int4* src = reinterpret_cast<const int4*>(tiles);
+  int4* dst = reinterpret_cast<int4*>(base);
+  for (int i = threadIdx.x; i < S * W * 2; i += blockDim.x) dst[i] = src[i];
 }
 
 // ------------------------------------------------------------------ the exp-sum kernel
@@ -473,7 +474,7 @@ bool i8_configure(int L, int64_t E, int k, I8Config* out) {
   if (c.S == 0 || getenv("SFFT_NO_I8")) return false;
   const int N2 = 2 * L;
   const int prods = c.S * (c.S + 1) / 2;
-  const int nt_cap = ((512 - 2 * 8 * c.S) / c.S) / 16 * 16;
+  const int nt_cap = std::min(96, ((512 - 2 * 8 * c.S) / c.S) / 16 * 16);   // 96: limbs kernel staging
   int force = getenv("SFFT_I8_NT") ? atoi(getenv("SFFT_I8_NT")) : 0;
   double best = 1e30;
   for (int NT = 16; NT <= nt_cap; NT += 16) {
@@ -524,11 +525,8 @@ int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
 
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st, bool only_retilted) {
   if (!only_retilted) i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);   // |a_j| do not change on a retilt
-  const int cols = (P.i8_ntiles - 1) * P.i8_NT + P.i8_NT_last;
-  const int64_t total = (int64_t)n_signals * cols * ((K + kI8StepTerms - 1) / kI8StepTerms) * 8;
-  DevParams Q = P;
-  Q.batch = n_signals;
-  if (total > 0) i8_limbs_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(Q, K, only_retilted ? 1 : 0);
+  const int64_t ctas = (int64_t)n_signals * P.i8_ntiles * ((K + kI8StepTerms - 1) / kI8StepTerms);
+  if (ctas > 0) i8_limbs_kernel<<<(unsigned)ctas, 256, 0, st>>>(P, K, only_retilted ? 1 : 0);
   return cudaGetLastError();
 }
 

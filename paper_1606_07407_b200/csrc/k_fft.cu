@@ -450,20 +450,26 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
     }
   }
   __syncthreads();
-  // slots free for this epoch, in index order (warp 0, deterministic)
+  // victims for the missing primes: least recently used first (empty slots have epoch -1), ties -> lower index;
+  // warp 0 picks them one by one (deterministic; n_miss is 0 in the steady state)
   if (threadIdx.x < 32) {
-    int base = 0;
-    for (int i0 = 0; i0 < C; i0 += 32) {
-      const int i = i0 + threadIdx.x;
-      const bool fr = i < C && P.slot_epoch[i] != epoch;
-      const unsigned b = __ballot_sync(0xffffffffu, fr);
-      if (fr) {
-        const int r = base + __popc(b & ((1u << threadIdx.x) - 1u));
-        if (r < n_miss) P.fill[r] = i;
+    int* ep = hidx + 2048;                                     // [n_tslots] epochs, chosen slots marked
+    for (int i = threadIdx.x; i < C; i += 32) ep[i] = P.slot_epoch[i];
+    __syncwarp();
+    int got = 0;
+    for (; got < n_miss; ++got) {
+      int best = 0x7fffffff, bi = -1;
+      for (int i = threadIdx.x; i < C; i += 32)
+        if (ep[i] != epoch && ep[i] < best) { best = ep[i]; bi = i; }
+      for (int o = 16; o; o >>= 1) {
+        const int ob = __shfl_xor_sync(0xffffffffu, best, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob < best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) { best = ob; bi = oi; }
       }
-      base += __popc(b);
+      if (bi < 0) break;
+      if (threadIdx.x == 0) { P.fill[got] = bi; ep[bi] = epoch; }
+      __syncwarp();
     }
-    if (threadIdx.x == 0) n_free = base;
+    if (threadIdx.x == 0) n_free = got;
   }
   __syncthreads();
   for (int h = threadIdx.x; h < 2048; h += blockDim.x) {
@@ -653,7 +659,7 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
                             cudaStream_t st, int32_t epoch, bool direct) {
   if (n_signals <= 0) return cudaSuccess;
   if (!direct) {
-    const size_t sm = sizeof(int) * ((size_t)P.n_tslots + 4096);
+    const size_t sm = sizeof(int) * (2 * (size_t)P.n_tslots + 4096);
     cudaError_t e = cudaFuncSetAttribute(tables_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
     tables_assign_kernel<<<1, 1024, sm, st>>>(P, epoch);
