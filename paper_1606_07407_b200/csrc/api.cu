@@ -652,6 +652,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   // int8-limb tensor-core exp-sum (bin-domain residual only: its B limbs are the fixed signal rows)
   if (P->expsum_path != 1 && !P->literal)
     P->i8_ok = i8_configure(P->L, *std::max_element(P->lvl_E.begin(), P->lvl_E.end()), P->k, &P->i8);
+  if (P->i8_ok && P->i8.small_l && P->expsum_path == 0) P->i8_ok = false;
   if (P->expsum_path == 2 && !P->i8_ok) return SFFT_ENOTSUP;
   // shared-memory budgets of the other kernels
   if (16 * ((size_t)P->p_stride + 2) + 2 * 16 * 16 * (size_t)P->shape.bn + 256 > (size_t)smem_optin) return SFFT_ENOTSUP;

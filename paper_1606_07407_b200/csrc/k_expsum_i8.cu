@@ -473,6 +473,9 @@ bool i8_configure(int L, int64_t E, int k, I8Config* out) {
   c.S = i8_limbs_for(E);
   if (c.S == 0 || getenv("SFFT_NO_I8")) return false;
   const int N2 = 2 * L;
+  // very few lines (2L <= 16): one N = 16 MMA per limb product is mostly padding and the A generation
+  // dominates; the FP64 kernels are faster there (measured on C2, L = 3) unless forced (expsum_path = 2)
+  if (N2 <= 16 && !getenv("SFFT_I8_SMALL_L")) c.small_l = 1;
   const int prods = c.S * (c.S + 1) / 2;
   const int nt_cap = std::min(96, ((512 - 2 * 8 * c.S) / c.S) / 16 * 16);   // 96: limbs kernel staging
   int force = getenv("SFFT_I8_NT") ? atoi(getenv("SFFT_I8_NT")) : 0;

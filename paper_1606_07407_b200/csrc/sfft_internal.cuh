@@ -140,6 +140,7 @@ __device__ __forceinline__ void i8_root_entry(double c, double s, int S, uint2& 
 // int8-limb exp-sum configuration (host)
 struct I8Config {
   int S, NT, NT_last, ntiles, nks;
+  int small_l;   // 1: auto mode prefers the FP64 kernels (2L <= 16)
 };
 
 // ---- device helpers ----------------------------------------------------------------------
@@ -193,7 +194,10 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
                             cudaStream_t st, int32_t epoch, bool direct = false);
 // threads per FFT CTA for a size (more CTAs per SM for small M)
-constexpr int kFftBigM = 4096;   // sizes >= this use radices up to 16 and the 512-thread variant
+#ifndef SFFT_FFT_BIGM
+#define SFFT_FFT_BIGM 8192
+#endif
+constexpr int kFftBigM = SFFT_FFT_BIGM;   // sizes >= this use radices up to 16 and the 512-thread variant (one CTA per SM); smaller sizes run two CTAs per SM
 inline int fft_threads(int M) {
   const int cap = M >= kFftBigM ? 512 : 256;
   int t = ((M / 6 + 31) / 32) * 32;
