@@ -305,6 +305,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
+    D.i8_pair = P->i8.pair;
     D.i8_B = ptr<int8_t>(P, B_I8B);
     D.i8_sigma = ptr<double>(P, B_I8SIG);
     D.i8_tlo = ptr<uint2>(P, B_I8TLO);
@@ -402,7 +403,7 @@ bool i8_use_for(const sfft_plan_t* P, int max_p) {
 // term split of the int8 kernel: same wave-quantisation model as the FP64 kernels, one CTA per SM
 int i8_ksplit(const sfft_plan_t* P, int max_p, int n_active) {
   const int blocks = i8_blocks(P->i8, max_p, n_active);
-  const int W = P->n_sm;
+  const int W = P->i8.pair ? P->n_sm / 2 : P->n_sm;                     // persistent units (CTA pairs)
   const int steps = (P->k + 15) / 16;
   const int ks_max = std::min(32, std::max(1, steps / 4));
   int ksplit = 1;

@@ -108,8 +108,10 @@ __global__ void __launch_bounds__(256) i8_limbs_kernel(DevParams P, int32_t K, i
     const double v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
     int dg[8];
     i8_digits(llrint(v * q), S, dg);
-    const int off = (col >> 3) * 256 + (kp >> 4) * 128 + (col & 7) * 16 + (kp & 15);
-    for (int t = 0; t < S; ++t) tiles[t * W * 32 + off] = (uint8_t)dg[t];
+    // CTA pairs: column halves [0, W/2) and [W/2, W) are separate K-major tiles (one per CTA of the pair)
+    const int hw = P.i8_pair ? W / 2 : W, half = col / hw, cc = col - half * hw;
+    const int off = half * S * hw * 32 + (cc >> 3) * 256 + (kp >> 4) * 128 + (cc & 7) * 16 + (kp & 15);
+    for (int t = 0; t < S; ++t) tiles[t * hw * 32 + off] = (uint8_t)dg[t];
   }
   __syncthreads();
   int8_t* base = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)nt * nks * S * NT * 32 + (int64_t)ks * S * W * 32;
@@ -129,6 +131,7 @@ struct I8Args {
   int32_t nb;                 // B ring slots (shared memory)
   int32_t nap;                // producer back-off (ns) while the B ring is full
   int32_t gnap;               // generator back-off (ns) while waiting for a free A slot (0: spin)
+  int32_t relaxed;            // tuning only (SFFT_I8_RELAXED=-1): release semantics for every cross-CTA arrival
   uint32_t b_stage_bytes;     // S * NT * 32
   uint32_t tab_off, thi_off, u_off;   // smem offsets of the limb tables and the phase list
   int32_t chunk;              // consecutive tiles per CTA visit
@@ -179,15 +182,20 @@ __device__ __forceinline__ void gen_limbs(uint32_t (&w)[NL][4], const int* __res
 
 // All S (S + 1) / 2 limb products of one K step, fully unrolled: accumulator of weight w at column w NT,
 // A limb s at a0 + 8 s, B limb t at descriptor bd0 + t * (NT * 32 / 16).
-template <int S>
+template <int S, bool PAIR>
 __device__ __forceinline__ void issue_stage(uint32_t tbase, uint32_t a0, uint64_t bd0, uint32_t nt_cols, uint32_t nt_desc,
                                             uint32_t idesc, bool first_k) {
 #pragma unroll
   for (int w = 0; w < S; ++w)
 #pragma unroll
-    for (int sl = 0; sl <= w; ++sl)
-      tc::mma_i8_ts(tbase + (uint32_t)w * nt_cols, a0 + 8 * sl, bd0 + (uint64_t)((w - sl) * nt_desc), idesc,
-                    (!first_k || sl > 0) ? 1u : 0u);
+    for (int sl = 0; sl <= w; ++sl) {
+      if constexpr (PAIR)
+        tc::mma_i8_ts2(tbase + (uint32_t)w * nt_cols, a0 + 8 * sl, bd0 + (uint64_t)((w - sl) * nt_desc), idesc,
+                       (!first_k || sl > 0) ? 1u : 0u);
+      else
+        tc::mma_i8_ts(tbase + (uint32_t)w * nt_cols, a0 + 8 * sl, bd0 + (uint64_t)((w - sl) * nt_desc), idesc,
+                      (!first_k || sl > 0) ? 1u : 0u);
+    }
 }
 
 // Tile t of the launch: (slot, h-tile, n-tile, term split) with the split index fastest.
@@ -215,7 +223,12 @@ __device__ __forceinline__ int ring_slots(int W, int S) { return min(kI8MaxSlots
 // A forwarder warp waits for bfull of the step and arrives on afull as its 9th arrival, so the MMA issuer
 // waits on one barrier per step (every try_wait costs ~90 cycles even when the phase is complete, and the
 // tensor core's instruction queue is too shallow to hide two of them).
-template <int S, bool PROF>
+// PAIR: clusters of 2 CTAs on one TPC run tcgen05.mma.cta_group::2 over M = 256 rows (128 per CTA): each CTA
+// generates its own rows' A limbs in its own TMEM and streams half of the B columns (W/2 per tile) into its own
+// shared memory, so the tensor cores' shared-memory B reads and the B copies per SM halve.  The leader CTA
+// (rank 0) issues; the peer's generator / forwarder / epilogue warps arrive on the leader's afull / accempty
+// barriers through the cluster window; the commits are multicast to both CTAs.
+template <int S, bool PROF, bool PAIR>
 __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I8Args A, double2* part, int32_t n_tiles) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* afull = reinterpret_cast<uint64_t*>(smem_raw);         // [kI8MaxSlots]
@@ -237,23 +250,53 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   const int per = (nkt + A.ksplit - 1) / A.ksplit;
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (warp == kI8MmaWarp) tc::tmem_alloc<512>(tslot);
+  const uint32_t rank = PAIR ? tc::cluster_rank() : 0u;
+  const int cid = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;       // pair (cluster) index
+  const int ncl = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  constexpr int kRowsTile = PAIR ? 2 * kI8Rows : kI8Rows;
+  if (warp == kI8MmaWarp) {
+    if (PAIR) tc::tmem_alloc2<512>(tslot);
+    else tc::tmem_alloc<512>(tslot);
+  }
   if (tid == 0) {
     for (int i = 0; i < kI8MaxSlots; ++i) {
-      tc::mbar_init(afull + i, kI8GenWarps + 1);                      // + the B forwarder
+      tc::mbar_init(afull + i, (PAIR ? 2 : 1) * (kI8GenWarps + 1));   // generators + the B forwarder (of both CTAs)
       tc::mbar_init(aempty + i, 1);
       tc::mbar_init(bfull + i, 1);
       tc::mbar_init(bempty + i, 1);
     }
     tc::mbar_init(accfull, 1);
-    tc::mbar_init(accempty, kI8GenWarps);
+    tc::mbar_init(accempty, (PAIR ? 2 : 1) * kI8GenWarps);
     tc::mbar_init(tabbar, 1);
     tc::fence_mbar_init();
   }
   tc::fence_before_sync();
   __syncthreads();
+  if (PAIR) tc::cluster_sync();                                        // barriers of both CTAs initialised
   tc::fence_after_sync();
   const uint32_t tbase = *tslot;
+  // the leader's afull / accempty as seen from this CTA (cluster window), for the peer's arrivals
+  const uint32_t afull_l = PAIR ? tc::mapa(afull, 0) : 0u, accempty_l = PAIR ? tc::mapa(accempty, 0) : 0u;
+  // Peer arrivals of the generators / epilogue only signal completed TMEM stores / loads (tcgen05.wait::st /
+  // ::ld, then tcgen05.fence::before_thread_sync), so they are relaxed (a release at cluster scope costs
+  // ~500 cycles per arrival); the forwarder's arrival publishes the peer's B half (TMA-written shared
+  // memory) and keeps release semantics.
+  auto arrive_afull = [&](int sl, bool publishes_smem) {
+    if (PAIR && rank != 0) {
+      if (publishes_smem || A.relaxed < 0) tc::mbar_arrive_cluster(afull_l + 8u * (uint32_t)sl);
+      else tc::mbar_arrive_cluster_relaxed(afull_l + 8u * (uint32_t)sl);
+    } else {
+      tc::mbar_arrive(afull + sl);
+    }
+  };
+  auto arrive_accempty = [&]() {
+    if (PAIR && rank != 0) {
+      if (A.relaxed < 0) tc::mbar_arrive_cluster(accempty_l);
+      else tc::mbar_arrive_cluster_relaxed(accempty_l);
+    } else {
+      tc::mbar_arrive(accempty);
+    }
+  };
 
   uint32_t aring = 0, bring = 0;        // parity bit per ring slot (each role keeps its own copies)
   int bpos = 0;                         // B ring position (producer / MMA)
@@ -265,14 +308,14 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   // chunks of A.chunk consecutive tiles (same signal, mostly) dealt round robin: the CTAs sweep the signals
   // together, so the B limbs of the few signals in flight stay in L2 while each CTA reuses its table
   const int n_chunks = (n_tiles + A.chunk - 1) / A.chunk;
-  for (int t = 0, q = blockIdx.x, tq = 0; q < n_chunks; ) {
+  for (int t = 0, q = cid, tq = 0; q < n_chunks; ) {
     t = q * A.chunk + tq;
-    if (++tq == A.chunk || t + 1 >= n_tiles) { tq = 0; q += gridDim.x; }
+    if (++tq == A.chunk || t + 1 >= n_tiles) { tq = 0; q += ncl; }
     if (t >= n_tiles) continue;
     const I8Tile tl = tile_of(t, A, ntiles);
     const int s = P.active[tl.slot];
     const int p = P.st_p[s];
-    if (tl.ht * kI8Rows >= p) continue;                            // uniform across the CTA
+    if (tl.ht * kRowsTile >= p) continue;                          // uniform across the CTA (pair)
     const int ks_lo = tl.ks * per, ks_hi = min(nkt, ks_lo + per);
     const int nk = max(0, ks_hi - ks_lo);
     if (nk == 0) continue;
@@ -304,7 +347,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       // ---------------- A generators + epilogue: warp g owns TMEM lanes / rows 32 (g % 4) .., terms 8 (g / 4) ..
       const int quarter = warp & 3, half = warp >> 2;
       const int row = 32 * quarter + lane;
-      const unsigned h = (unsigned)(tl.ht * kI8Rows + row);        // row f of the discrete-log order
+      const unsigned h = (unsigned)(tl.ht * kRowsTile + (int)rank * kI8Rows + row);   // row f (discrete-log order)
       const uint32_t lane_addr = tbase + ((uint32_t)(32 * quarter) << 16);
       const uint32_t ta0 = lane_addr + (uint32_t)(S * W) + 4 * half;
       // software pipeline: the limbs of step kq + 1 are gathered while the tensor core works on step kq and
@@ -329,7 +372,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         tc::tmem_wait_st();
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(afull + sl);
+        if (lane == 0) arrive_afull(sl, false);
         const long long cg = PROF ? clock64() : 0;
         if (PROF) pr_t += cg - c0 - (pr_a - pr_a);                   // store + arrive (incl. the slot wait, see pr_a)
         if (kq + 1 < nk && A.dbg != 3)
@@ -377,11 +420,12 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
       if (PROF) pr_e += clock64() - ce0;
       tc::fence_before_sync();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(accempty);
+      if (lane == 0) arrive_accempty();
     } else if (warp == kI8ProdWarp) {
       // ---------------- B producer: one lane streams the B limb tiles (backs off while the ring is full)
-      const int8_t* Bg = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)tl.nt * nks * S * NT * 32;
-      const uint32_t bytes = (uint32_t)S * W * 32;
+      // PAIR: this CTA's half of the columns, [rank W/2, (rank + 1) W/2), stored after the other half
+      const uint32_t bytes = (uint32_t)S * (PAIR ? W / 2 : W) * 32;
+      const int8_t* Bg = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)tl.nt * nks * S * NT * 32 + rank * bytes;
       for (int kq = 0; kq < nk; ++kq) {
         const int sb = bpos;
         bpos = bpos + 1 == A.nb ? 0 : bpos + 1;
@@ -390,7 +434,8 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         if (lane == 0) {
           while (!tc::mbar_try_wait(bempty + sb, par)) __nanosleep(A.nap);
           tc::mbar_expect_tx(bfull + sb, bytes);
-          tc::bulk_g2s(sB + (size_t)sb * A.b_stage_bytes, Bg + (int64_t)(ks_lo + kq) * S * W * 32, bytes, bfull + sb);
+          tc::bulk_g2s(sB + (size_t)sb * A.b_stage_bytes, Bg + (int64_t)(ks_lo + kq) * S * W * 32, bytes,
+                       bfull + sb);
         }
       }
     } else if (warp == kI8FwdWarp) {
@@ -406,11 +451,11 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         tc::mbar_wait(bfull + sb, (bring >> sb) & 1);
         bring ^= 1u << sb;
         if (PROF) pr_b += clock64() - cb;
-        if (lane == 0) tc::mbar_arrive(afull + sl);
+        if (lane == 0) arrive_afull(sl, true);
       }
-    } else {
+    } else if (!PAIR || rank == 0) {
       // ---------------- MMA issuer: the whole warp walks the ring, one elected lane issues
-      const uint32_t idesc = tc::idesc_i8(kI8Rows, W);
+      const uint32_t idesc = tc::idesc_i8(kRowsTile, W);
       if (ntile_done > 0) {
         const long long c0 = PROF ? clock64() : 0;
         tc::mbar_wait(accempty, (ntile_done - 1) & 1);
@@ -430,15 +475,23 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
         tc::fence_after_sync();
         if (tc::elect_one()) {
           if (A.dbg != 2)
-            issue_stage<S>(tbase, a_slot0 + sl * S * 8, bdesc0 + (uint64_t)(sb * stage_desc), (uint32_t)W, (uint32_t)W * 2,
-                           idesc, kq == 0);
-          tc::mma_commit(bempty + sb);
-          tc::mma_commit(aempty + sl);
+            issue_stage<S, PAIR>(tbase, a_slot0 + sl * S * 8, bdesc0 + (uint64_t)(sb * stage_desc), (uint32_t)W,
+                                 (uint32_t)(PAIR ? W : W * 2), idesc, kq == 0);
+          if (PAIR) {
+            tc::mma_commit2(bempty + sb);
+            tc::mma_commit2(aempty + sl);
+          } else {
+            tc::mma_commit(bempty + sb);
+            tc::mma_commit(aempty + sl);
+          }
         }
         __syncwarp();
         sl = sl + 1 == nsl ? 0 : sl + 1;
       }
-      if (tc::elect_one()) tc::mma_commit(accfull);
+      if (tc::elect_one()) {
+        if (PAIR) tc::mma_commit2(accfull);
+        else tc::mma_commit(accfull);
+      }
       __syncwarp();
     }
     ++ntile_done;
@@ -449,9 +502,11 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   }
   tc::fence_before_sync();
   __syncthreads();
+  if (PAIR) tc::cluster_sync();                                        // the peer's MMAs read this CTA's TMEM
   if (warp == kI8MmaWarp) {
     tc::fence_after_sync();
-    tc::tmem_dealloc<512>(tbase);
+    if (PAIR) tc::tmem_dealloc2<512>(tbase);
+    else tc::tmem_dealloc<512>(tbase);
   }
 }
 
@@ -493,6 +548,10 @@ bool i8_configure(int L, int64_t E, int k, I8Config* out) {
   }
   if (c.NT == 0) return false;
   c.nks = (2 * k + kI8StepTerms - 1) / kI8StepTerms;
+  // CTA pairs (cta_group::2) are exact (parity-tested) but not the default: the peer CTA's arrivals on the
+  // leader's barriers cost ~500 cycles each with release semantics, which the two A slots of a 64-column tile
+  // cannot hide (measured: 2.38 ms vs 1.93 ms for the C3 iteration-1 exp-sum); SFFT_I8_PAIR=1 enables them.
+  c.pair = (c.NT_last >= 32 && c.NT >= 32 && getenv("SFFT_I8_PAIR") && atoi(getenv("SFFT_I8_PAIR")) == 1) ? 1 : 0;
   *out = c;
   return true;
 }
@@ -523,7 +582,8 @@ bool i8_fits(const I8Config& c, int p, int k, int smem_optin) {
 }
 
 int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
-  return n_signals * ((max_p + kI8Rows - 1) / kI8Rows) * c.ntiles;
+  const int rows = c.pair ? 2 * kI8Rows : kI8Rows;                      // tiles of one persistent unit (CTA or pair)
+  return n_signals * ((max_p + rows - 1) / rows) * c.ntiles;
 }
 
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st, bool only_retilted) {
@@ -557,6 +617,7 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   A.dbg = getenv("SFFT_I8_DBG") ? atoi(getenv("SFFT_I8_DBG")) : 0;
   A.nap = getenv("SFFT_I8_NAP") ? atoi(getenv("SFFT_I8_NAP")) : 256;
   A.gnap = getenv("SFFT_I8_GNAP") ? atoi(getenv("SFFT_I8_GNAP")) : 0;
+  A.relaxed = getenv("SFFT_I8_RELAXED") ? atoi(getenv("SFFT_I8_RELAXED")) : 0;
   static long long* prof_buf = nullptr;
   if (getenv("SFFT_I8_PROF")) {
     if (!prof_buf) cudaMalloc(&prof_buf, sizeof(long long) * 148 * 2 * 6);
@@ -573,16 +634,39 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   if (A.nb < 2) return cudaErrorInvalidValue;
   // one CTA per SM: the kernel allocates all 512 TMEM columns
   smem = std::max(smem, (size_t)120 * 1024);
-  auto kern = c.S == 5 ? (A.prof ? expsum_i8_kernel<5, true> : expsum_i8_kernel<5, false>)
-                       : (A.prof ? expsum_i8_kernel<6, true> : expsum_i8_kernel<6, false>);
+  const bool pair = P.i8_pair != 0;
+  void (*kern)(DevParams, I8Args, double2*, int32_t);
+  if (pair) kern = c.S == 5 ? (A.prof ? expsum_i8_kernel<5, true, true> : expsum_i8_kernel<5, false, true>)
+                            : (A.prof ? expsum_i8_kernel<6, true, true> : expsum_i8_kernel<6, false, true>);
+  else kern = c.S == 5 ? (A.prof ? expsum_i8_kernel<5, true, false> : expsum_i8_kernel<5, false, false>)
+                       : (A.prof ? expsum_i8_kernel<6, true, false> : expsum_i8_kernel<6, false, false>);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  if (pair) {
+    A.n_htiles = (max_p + 2 * kI8Rows - 1) / (2 * kI8Rows);            // 256-row tiles of the pair
+  }
   const long tiles = (long)n_signals * A.n_htiles * c.ntiles * ksplit;
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
   A.chunk = getenv("SFFT_I8_CHUNK") ? std::max(1, atoi(getenv("SFFT_I8_CHUNK"))) : 4;
-  const long grid = std::min<long>((tiles + A.chunk - 1) / A.chunk, n_sm);
-  if (grid > 0) kern<<<(unsigned)grid, kI8Threads, smem, st>>>(P, A, part, (int32_t)tiles);
+  const long units = pair ? n_sm / 2 : n_sm;                            // persistent CTAs (pairs)
+  const long grid = std::min<long>((tiles + A.chunk - 1) / A.chunk, units) * (pair ? 2 : 1);
+  if (grid > 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kI8Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = pair ? 2 : 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, P, A, part, (int32_t)tiles);
+    if (e != cudaSuccess) return e;
+  }
   if (A.prof && grid > 0) {
     long long h[148 * 2 * 6];
     cudaMemcpyAsync(h, A.prof, sizeof h, cudaMemcpyDeviceToHost, st);

@@ -100,6 +100,7 @@ struct DevParams {
   // int8-limb tensor-core exp-sum (k_expsum_i8.cu)
   int32_t i8_S, i8_NT, i8_NT_last, i8_ntiles, i8_nks;   // limbs, n-tile width (last tile narrower), n-tiles, K-step capacity
   int32_t i8_K;                // terms held in the B limbs (k for a solve, K for the stage entry point)
+  int32_t i8_pair;             // 1: CTA pairs (cta_group::2, M = 256); B limbs stored as two column halves
   int8_t* i8_B;                // [batch][ntiles][nks][S][NT*32] B limbs in the UMMA K-major layout
   double* i8_sigma;            // [batch] coefficient scale
   // rows in discrete-log order (reading R22): f < p-1 is the sample h = g^f mod p (g a primitive root of p),
@@ -141,6 +142,7 @@ __device__ __forceinline__ void i8_root_entry(double c, double s, int S, uint2& 
 struct I8Config {
   int S, NT, NT_last, ntiles, nks;
   int small_l;   // 1: auto mode prefers the FP64 kernels (2L <= 16)
+  int pair;      // 1: CTA-pair kernel (every tile width >= 32)
 };
 
 // ---- device helpers ----------------------------------------------------------------------

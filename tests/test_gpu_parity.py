@@ -389,3 +389,25 @@ def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trial
             wc, _ = W.canonical_sort(w[i], a[i])
             assert np.array_equal(ref.w, wc)
     assert res.report.samples_used == samples
+
+
+def test_e2e_cta_pair_mode(S):
+    """The CTA-pair (tcgen05.mma.cta_group::2, M = 256) variant of the int8 exp-sum (opt-in, SFFT_I8_PAIR=1)
+    gives the same sets and coefficients as the oracle (full size, C3 and C5 seeds)."""
+    import subprocess, sys
+    code = ("import numpy as np, torch, hashlib, oracle as O, workloads as W, paper_1606_07407_b200 as S\n"
+            "for name, tr in (('c3', [0, 1]), ('c5', [0])):\n"
+            "    c = W.CONFIGS[name]; g = np.load('tests/golden/oracle_%s.npz' % name)\n"
+            "    w, a = W.make_batch(c, tr)\n"
+            "    plan = S.sfft_plan(c.d, c.N, c.k, blocks=c.blocks, batch=len(tr))\n"
+            "    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())\n"
+            "    for i, t in enumerate(tr):\n"
+            "        k = 'primary_%d' % t; n = int(res.count[i])\n"
+            "        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())\n"
+            "        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[k + '_w_sha256'])\n"
+            "        ra = g[k + '_a']; assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max()\n"
+            "print('pair ok')\n")
+    env = dict(os.environ, SFFT_I8_PAIR="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+                         cwd=os.path.dirname(GOLD_DIR.rstrip("/")).rsplit("/tests", 1)[0])
+    assert out.returncode == 0 and "pair ok" in out.stdout, out.stderr[-2000:]
