@@ -52,6 +52,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--shard", default="signals", choices=["signals", "lines"],
+                    help="signals: independent signal shards per rank (weak scaling, default); lines: every rank "
+                         "solves the same signals and owns a shard of the shifted lines (strong scaling, NCCL "
+                         "record all-gather per iteration, SURVEY 8(e))")
     ap.add_argument("--expsum-path", type=int, default=0, choices=[0, 1, 2],
                     help="0 auto (int8 limbs on tcgen05 when available), 1 FP64 tensor/vector, 2 int8 limbs")
     return ap.parse_args()
@@ -171,14 +175,23 @@ def main():
     from paper_1606_07407_b200.shard import shard_indices
     cfg = W.CONFIGS[args.config]
     T = args.batch or cfg.trials
-    trials = shard_indices(world * T, world, rank)     # each rank: its own shard of independent signals
+    lines = args.shard == "lines"
+    mult = 1 if lines else world                        # signal sets solved per step across the job
+    # signal shards: each rank its own independent signals; line shards: every rank the same signals
+    trials = list(range(T)) if lines else shard_indices(world * T, world, rank)
     w_np, a_np = W.make_batch(cfg, trials)
     w_h = torch.from_numpy(w_np).pin_memory()
     a_h = torch.from_numpy(a_np).pin_memory()
     w_d, a_d = w_h.cuda(), a_h.cuda()
     stream = torch.cuda.current_stream()
     plan = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, profile=True,
-                        expsum_path=args.expsum_path)
+                        expsum_path=args.expsum_path, line_shards=world if lines else 0,
+                        line_rank=rank if lines else 0)
+    if lines:
+        if world > 1:
+            S.comm_init_line_shards(plan)
+        else:
+            S.sfft_comm_init(plan, 1, 0, shard_mode=1, unique_id=S.sfft_comm_unique_id())
     sig = S.sfft_signal_expsum(plan, w_d, a_d)
     outs = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32, device="cuda"),
             torch.empty((T, cfg.k, 2), dtype=torch.float64, device="cuda"),
@@ -220,7 +233,7 @@ def main():
         dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
     ms_max = float(t_max.item())
     ms_step = ms_max / args.steps
-    modes_total = world * T * cfg.k * args.steps
+    modes_total = mult * T * cfg.k * args.steps
     value = modes_total / (ms_max / 1e3)
     samples = sum(r.samples_used for r in reps)
     cmacs = sum(r.cmacs for r in reps)
@@ -292,7 +305,7 @@ def main():
     e_t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-    e2e_value = world * T * cfg.k * args.e2e_steps / (float(e_t.item()) / 1e3) if args.e2e_steps else None
+    e2e_value = mult * T * cfg.k * args.e2e_steps / (float(e_t.item()) / 1e3) if args.e2e_steps else None
     h2d = w_h.numel() * 4 + a_h.numel() * 16
     d2h = hout[0].numel() * 4 + hout[1].numel() * 8 + hout[2].numel() * 4 + hout[3].numel() * 4
     if args.e2e_steps:
@@ -313,15 +326,17 @@ def main():
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "modes/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong" if lines else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64 per PAPER.md:424 recipe; no dataset exists for this metric)",
             "expsum_path": "int8 limbs on tcgen05" if n8 else "fp64",
             "config": {"workload": f"{cfg.name}: d={cfg.d} N={cfg.N} k={cfg.k} |a|~U[1,10], partition (2^50), "
                                    f"r={plan.r}, E=2^{int(np.log2(plan.E))}",
-                       "signals_per_gpu_per_step": T, "parallelism": f"signal shards x{world}",
+                       "signals_per_gpu_per_step": T,
+                       "parallelism": f"line shards x{world} (NCCL record all-gather)" if lines else f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
-            "sample_evals_per_s": world * samples / (ms_max / 1e3),
+            "sample_evals_per_s": mult * samples / (ms_max / 1e3),
             "verified_exact_recovery": ok,
             "roofline": roofline,
             "kernel_ms_per_step": {"expsum": ms_exp / args.steps, "fft": ms_fft / args.steps,

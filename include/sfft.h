@@ -74,6 +74,12 @@ typedef struct {
                                  zero-accept iterations switch to the next of up to 4 tilt levels -- Pythagorean
                                  triples (3,4,5), (5,12,13), (8,15,17), (7,24,25) on disjoint reduced-axis pairs --
                                  keeping the modes found (mapped exactly); 0 = stop with PARTIAL [0] */
+  int32_t line_shards;        /* line sharding: 0 = this plan holds every line [0]; G >= 1 = the
+                                 plan is shard line_rank of G: it computes line 0 and the shifted lines of reduced
+                                 axes [lo, hi) (contiguous, sizes differ by at most one, shard 0 the largest), and
+                                 its decode exchanges per-candidate records with the other shards every iteration
+                                 (sfft_comm_init, or sfft_execute_group on one device).  1 <= G <= r. */
+  int32_t line_rank;          /* shard index of this plan, 0 <= line_rank < line_shards [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */
@@ -120,7 +126,8 @@ SFFT_API int sfft_plan_workspace_size(const sfft_plan_t* plan, size_t* bytes);
 /* dptr: device memory of >= workspace_size bytes, 256-byte aligned, owned by the caller, must
  * outlive the plan. */
 SFFT_API int sfft_plan_set_workspace(sfft_plan_t* plan, void* dptr, size_t bytes);
-/* Query plan-derived values (host): E, r, number of lines L = r+1, p_max supported, tile shape. */
+/* Query plan-derived values (host): E, r, number of lines L this plan computes (r+1, or 1 + its shard's
+ * axes when line-sharded), p_max supported, tile shape. */
 SFFT_API int sfft_plan_info(const sfft_plan_t* plan, int64_t* E, int32_t* r, int32_t* L, int64_t* p_max,
                    int32_t* tile_n);
 SFFT_API void sfft_plan_destroy(sfft_plan_t* plan);
@@ -190,9 +197,37 @@ SFFT_API int sfft_stage_decode(sfft_plan_t* plan, int64_t p, int32_t m, int32_t 
 /* a1 on its own: v [batch][r][k] (device int64) of a signal (unwrap Eq. (35) + tilt Eq. (27)). */
 SFFT_API int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int64_t* v_out);
 
-/* Multi-GPU: signal sharding needs no communicator; line sharding is NEXT. */
+/*
+ * Multi-GPU.  Signal sharding (shard_mode 0) runs independent solves per rank and needs
+ * no communicator (sfft_comm_init returns SFFT_OK and does nothing).  Line sharding (shard_mode 1):
+ * the plan must have been created with line_shards = nranks, line_rank = rank; every iteration each
+ * rank computes line 0 (redundantly, bitwise identical on all ranks) and its own shifted lines, tests
+ * and decodes the candidates of line 0 on them, all-gathers the per-candidate records (pass flag over
+ * its lines, decoded coordinates of its axes: batch * ((k+1)/2 + (Lmax-1) k) int64 words per rank) with
+ * ncclAllGather on the plan's stream, and applies the identical registry update (Alg. 2 l.20-33).
+ *   nccl_unique_id  host, 128 bytes from sfft_comm_unique_id on rank 0, broadcast by the caller
+ * NCCL is loaded at run time (dlopen "libnccl.so.2": the copy already in the process, e.g. torch's,
+ * else the system one); without it the call fails with SFFT_ENCCL.  All ranks must call it together
+ * (ncclCommInitRank is collective).  The communicator is destroyed with the plan.
+ */
 SFFT_API int sfft_comm_init(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* nccl_unique_id,
                    int32_t shard_mode);
+/* Reduced axes [lo, hi) of line shard g of G over r axes (host, no device needed): contiguous, sizes
+ * differ by at most one, shard 0 the largest.  The shard computes line 0 and lines 1+lo .. hi. */
+SFFT_API int sfft_line_shard_range(int32_t r, int32_t G, int32_t g, int32_t* lo, int32_t* hi);
+/* 128-byte NCCL unique id (ncclGetUniqueId) into host memory `out` (rank 0 of a line-sharded job). */
+SFFT_API int sfft_comm_unique_id(void* out);
+/*
+ * sfft_execute_group -- the line-sharded solve of plans[0..n_plans) (line_shards = n_plans, line_rank g
+ * = plans[g]) on ONE device: the shards' phases run one after another on plans[0]'s stream and the
+ * record all-gather is a device copy into every shard's receive buffer.  Same kernels and records as the
+ * multi-GPU path; used to prove the sharded protocol against the unsharded path on one GPU.  Every plan
+ * needs a signal of the same arrays (sfft_signal_expsum on each plan).  Outputs are plan 0's; the call
+ * fails with SFFT_ECORRUPT if the shards' registries are not bitwise identical at the end.
+ */
+SFFT_API int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* sigs, int32_t n_plans,
+                       int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
+                       sfft_report* rep);
 
 SFFT_API const char* sfft_strerror(int status);
 SFFT_API const char* sfft_last_error(const sfft_plan_t* plan);

@@ -25,7 +25,9 @@ EXPORTS = (
     "sfft_plan", "sfft_plan_workspace_size", "sfft_plan_set_workspace", "sfft_plan_info",
     "sfft_plan_destroy", "sfft_signal_expsum", "sfft_signal_destroy", "sfft_execute",
     "sfft_solve_host", "sfft_stage_expsum", "sfft_stage_pfft", "sfft_stage_decode",
-    "sfft_stage_project", "sfft_comm_init", "sfft_strerror", "sfft_last_error", "sfft_version",
+    "sfft_stage_project", "sfft_comm_init", "sfft_comm_unique_id", "sfft_execute_group",
+    "sfft_line_shard_range", "sfft_strerror",
+    "sfft_last_error", "sfft_version",
 )
 
 
@@ -42,7 +44,8 @@ class sfft_options(ctypes.Structure):
                 ("batch", ctypes.c_int32), ("extra_checks", ctypes.c_int32),
                 ("stream", ctypes.c_void_p), ("profile", ctypes.c_int32),
                 ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32),
-                ("fallback_tilts", ctypes.c_int32)]
+                ("fallback_tilts", ctypes.c_int32), ("line_shards", ctypes.c_int32),
+                ("line_rank", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -91,6 +94,9 @@ def lib() -> ctypes.CDLL:
         L.sfft_stage_decode.argtypes = [vp, i64, i32, i32, vp, vp, vp, vp, vp]
         L.sfft_stage_project.argtypes = [vp, vp, vp]
         L.sfft_comm_init.argtypes = [vp, i32, i32, vp, i32]
+        L.sfft_comm_unique_id.argtypes = [vp]
+        L.sfft_line_shard_range.argtypes = [i32, i32, i32, vp, vp]
+        L.sfft_execute_group.argtypes = [vp, vp, i32, vp, vp, vp, vp, vp]
         L.sfft_strerror.argtypes = [ctypes.c_int]
         L.sfft_strerror.restype = ctypes.c_char_p
         L.sfft_last_error.argtypes = [vp]
@@ -162,7 +168,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               bin_floor_rel: float = 1e-8, prune_floor: float = 1e-8, round_tol: float = 0.01,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
               stream=None, profile: bool = False, literal_residual: bool = False,
-              expsum_path: int = 0, fallback_tilts: int = 0) -> Plan:
+              expsum_path: int = 0, fallback_tilts: int = 0, line_shards: int = 0, line_rank: int = 0) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -180,6 +186,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.literal_residual = 1 if literal_residual else 0
     opt.expsum_path = int(expsum_path)
     opt.fallback_tilts = int(fallback_tilts)
+    opt.line_shards, opt.line_rank = int(line_shards), int(line_rank)
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)
@@ -332,6 +339,50 @@ def sfft_stage_project(plan: Plan, sig: Signal):
 def sfft_comm_init(plan: Plan, nranks: int, rank: int, shard_mode: int = 0, unique_id: bytes = b""):
     buf = ctypes.create_string_buffer(unique_id, 128) if unique_id else None
     return _check(lib().sfft_comm_init(plan.handle, nranks, rank, buf, shard_mode), plan.handle)
+
+
+def sfft_line_shard_range(r: int, G: int, g: int) -> Tuple[int, int]:
+    """Reduced axes [lo, hi) of line shard g of G (host call, no device needed)."""
+    lo, hi = ctypes.c_int32(), ctypes.c_int32()
+    _check(lib().sfft_line_shard_range(r, G, g, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def sfft_comm_unique_id() -> bytes:
+    """128-byte NCCL unique id (rank 0 of a line-sharded job; broadcast it with torch.distributed)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().sfft_comm_unique_id(buf))
+    return buf.raw
+
+
+def sfft_execute_group(plans: Sequence[Plan], sigs: Sequence[Signal], out=None) -> Result:
+    """Line-sharded solve of len(plans) shards on ONE device (include/sfft.h sfft_execute_group)."""
+    torch = _torch()
+    n = len(plans)
+    B, p0 = sigs[0].batch, plans[0]
+    if out is None:
+        out = (torch.empty((B, p0.k, p0.d), dtype=torch.int32, device="cuda"),
+               torch.empty((B, p0.k, 2), dtype=torch.float64, device="cuda"),
+               torch.empty((B,), dtype=torch.int32, device="cuda"),
+               torch.empty((B,), dtype=torch.int32, device="cuda"))
+    of, oc, on, os_ = out
+    hp = (ctypes.c_void_p * n)(*[p.handle for p in plans])
+    hs = (ctypes.c_void_p * n)(*[s.handle for s in sigs])
+    rep = sfft_report()
+    rc = lib().sfft_execute_group(hp, hs, n, ctypes.c_void_p(of.data_ptr()), ctypes.c_void_p(oc.data_ptr()),
+                                  ctypes.c_void_p(on.data_ptr()), ctypes.c_void_p(os_.data_ptr()), ctypes.byref(rep))
+    _check(rc, p0.handle, ok=(SFFT_OK, SFFT_PARTIAL, SFFT_ENOTSUP))
+    return Result(rc, of, torch.view_as_complex(oc), on, os_, rep)
+
+
+def comm_init_line_shards(plan: Plan, group=None) -> None:
+    """Line sharding over a torch.distributed group: rank 0 draws the NCCL id, the group broadcasts it
+    (broadcast_object_list), every rank initialises the plan's communicator (collective)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [sfft_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    sfft_comm_init(plan, world, rank, shard_mode=1, unique_id=obj[0])
 
 
 def solve(plan: Plan, freqs, coeffs):

@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
+#include <functional>
 #include <memory>
 #include <new>
 
@@ -81,6 +83,12 @@ struct sfft_plan_s {
   int32_t literal = 0;
   std::vector<cudaEvent_t> events;
   std::string err;
+  // line sharding: shard line_g of line_G (0 = unsharded) holds line 0 and the shifted lines of
+  // reduced axes [line_lo, line_lo + L - 1); tile shapes / term split follow shard 0's line count L_ref so
+  // that line 0 is computed identically on every shard
+  int32_t line_G = 0, line_g = 0, line_lo = 0, L_ref = 0;
+  int32_t rec_words = 0, rec_fw = 0;
+  void* nccl_comm = nullptr;   // ncclComm_t of sfft_comm_init (shard_mode 1)
 };
 
 namespace {
@@ -92,6 +100,7 @@ enum Buf {
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
+  B_RSEND, B_RRECV, B_RCAND, B_RNC,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -219,6 +228,11 @@ void layout(sfft_plan_t* P) {
   sz[B_FILL] = 4 * T;
   sz[B_I8TLO] = P->i8_ok ? 8 * T * (2 * P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
+  const size_t G = (size_t)std::max(P->line_G, 0);
+  sz[B_RSEND] = G ? 8 * S * (size_t)P->rec_words : 0;
+  sz[B_RRECV] = G ? 8 * G * S * (size_t)P->rec_words : 0;
+  sz[B_RCAND] = G ? 4 * S * (size_t)P->k : 0;
+  sz[B_RNC] = G ? 4 * S : 0;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -317,6 +331,18 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_estride = (int32_t)align_up((size_t)P->kk + 16, 4);   // rows 16-byte aligned for the bulk copies
     D.i8_chl = ptr<double2>(P, B_I8CHL);
   }
+  D.line_lo = P->line_lo;
+  D.line_G = std::max(P->line_G, 1);
+  D.line_g = P->line_g;
+  D.line_split = P->line_G > 0;
+  D.rec_words = P->rec_words;
+  D.rec_fw = P->rec_fw;
+  if (P->line_G > 0) {
+    D.rec_send = ptr<int64_t>(P, B_RSEND);
+    D.rec_recv = ptr<int64_t>(P, B_RRECV);
+    D.rec_cand = ptr<int32_t>(P, B_RCAND);
+    D.rec_nc = ptr<int32_t>(P, B_RNC);
+  }
   return D;
 }
 
@@ -409,7 +435,7 @@ int i8_ksplit(const sfft_plan_t* P, int max_p, int n_active) {
   int ksplit = 1;
   double best = 1e30;
   for (int ks = 1; ks <= ks_max; ++ks) {
-    if (ks > 1 && (size_t)ks * n_active * P->L * (size_t)max_p * 16 > kPartBytes) break;
+    if (ks > 1 && (size_t)ks * n_active * P->L_ref * (size_t)max_p * 16 > kPartBytes) break;
     const double waves = std::ceil((double)blocks * ks / W);
     const double t = waves / ks * (ks > 1 ? 1.03 : 1.0) + 0.02 * ks;   // per-CTA prologue (tables)
     if (t < best - 1e-9) { best = t; ksplit = ks; }
@@ -419,6 +445,179 @@ int i8_ksplit(const sfft_plan_t* P, int max_p, int n_active) {
 
 // SFFT_SYNC=1: synchronise after every launch (debugging aid: pins errors to the launching call)
 const bool g_sync_launches = getenv("SFFT_SYNC") != nullptr;
+
+// ---------------------------------------------------------------- the iteration driver (Alg. 2)
+// One iteration = setup (host reads n_active / max p) | front: table prep, exp-sum (a3), pfft (a4), decode
+// (a5-a7; its local phase when line-sharded) | [record all-gather] | back: decode commit, fallback retilt.
+struct IterPlan {
+  int n_active = 0, max_p = 0, fi = 0, max_M = 0, ksplit = 1, big = 0;
+  bool use_i8 = false;
+};
+
+// a1 (projection, term rows) and the int8 limbs of the signal terms, once per solve
+int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& launches) {
+  cudaStream_t st = P->stream;
+  LAUNCH(P, launch_project(D, sig->batch, sig->freqs, sig->coeffs, st));
+  launches += 1;   // init_state_kernel
+  if (P->i8_ok) {
+    LAUNCH(P, launch_i8_prepare(D, sig->batch, P->k, st));
+    launches += 1;   // sigma + limbs
+  }
+  return SFFT_OK;
+}
+
+int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launches) {
+  cudaStream_t st = P->stream;
+  LAUNCH(P, launch_setup(D, iter, st));
+  CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(P, cudaStreamSynchronize(st));
+  it->n_active = P->h_ctrl[0];
+  it->max_p = P->h_ctrl[1];
+  if (it->n_active == 0) return SFFT_OK;
+  it->fi = fft_index_host(P, it->max_p);
+  if (it->fi < 0) return fail(P, SFFT_ENOTSUP, "p=%d beyond FFT table", it->max_p);
+  it->max_M = P->fft[it->fi].M;
+  const int max_K = P->h_ctrl[2];
+  // term split when the (signal x h-tile x n-tile) grid cannot fill the GPU (late iterations); computed
+  // from shard 0's line count so that every line shard sums line 0 in the same order
+  const ExpsumShape shp = expsum_for_p(P->shape, it->max_p);
+  it->use_i8 = P->i8_ok && i8_use_for(P, it->max_p);
+  it->ksplit = 1;
+  if (it->use_i8) {
+    it->ksplit = i8_ksplit(P, it->max_p, it->n_active);
+  } else {
+    // wave quantisation model: time ~ ceil(B ks / W) / ks, W = resident CTAs; a split costs ~3 %
+    // (partial lines written and re-read by the FFT)
+    const int blocks = expsum_blocks(shp, it->max_p, it->n_active);
+    const int W = P->n_sm * expsum_occupancy(shp, it->max_p);
+    const int chunks = (max_K + expsum_bk() - 1) / expsum_bk();
+    const int ks_max = std::min(32, std::max(1, chunks / 2));
+    double best = 1e30;
+    for (int ks = 1; ks <= ks_max; ++ks) {
+      if (ks > 1 && (size_t)ks * it->n_active * P->L_ref * (size_t)it->max_p * 16 > kPartBytes) break;
+      const double waves = std::ceil((double)blocks * ks / W);
+      const double t = waves / ks * (ks > 1 ? 1.03 : 1.0);
+      if (t < best - 1e-9) { best = t; it->ksplit = ks; }
+    }
+  }
+  it->big = it->max_M >= kFftBigM;
+  return SFFT_OK;
+}
+
+int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& launches,
+               const std::function<int()>& mark) {
+  cudaStream_t st = P->stream;
+  LAUNCH(P, launch_fft_prep(D, it.n_active, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M), it.big, st, ++P->epoch));
+  launches += 2;   // tables_assign, terms
+  mark();
+  if (it.use_i8)
+    LAUNCH(P, launch_expsum_i8(D, P->i8, it.max_p, it.n_active, it.ksplit, ptr<double2>(P, B_PART), it.max_p,
+                               P->smem_optin, st));
+  else
+    LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, it.max_p), it.max_p, it.n_active, it.ksplit,
+                            ptr<double2>(P, B_PART), it.max_p, st));
+  mark();
+  D.lines_log = it.use_i8 ? 1 : 0;
+  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M), it.big, it.ksplit,
+                        ptr<double2>(P, B_PART), it.max_p, st));
+  D.lines_log = 0;
+  mark();
+  D.i8_iter = it.use_i8 ? 1 : 0;
+  LAUNCH(P, launch_decode(D, iter, it.max_p, it.n_active, st, P->line_G > 0 ? 1 : 0));
+  D.i8_iter = 0;
+  return SFFT_OK;
+}
+
+int iter_back(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, const sfft_signal_t* sig, int& launches) {
+  cudaStream_t st = P->stream;
+  if (P->line_G > 0) {
+    D.i8_iter = it.use_i8 ? 1 : 0;
+    LAUNCH(P, launch_decode(D, iter, it.max_p, it.n_active, st, 2));
+    D.i8_iter = 0;
+  }
+  if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
+    LAUNCH(P, launch_retilt(D, sig->batch, sig->freqs, st));
+    if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch, P->k, st, true));
+  }
+  return SFFT_OK;
+}
+
+// per-signal status -> worst status; the host report (samples, cMACs, trace of signal 0)
+int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_t* ostat, sfft_report* rep,
+                 int32_t last_iter, int launches, int32_t n_expsum, int32_t n_expsum_i8, int* worst_out) {
+  cudaStream_t st = P->stream;
+  std::vector<int32_t> hs(batch);
+  CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
+  std::vector<int32_t> hlog(2 * kLogIters);
+  if (rep) {
+    CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(P, cudaStreamSynchronize(st));
+  int worst = SFFT_OK, n_ok = 0, n_part = 0, n_err = 0;
+  for (int s = 0; s < batch; ++s) {
+    const int v = hs[s];
+    if (v == SFFT_OK) ++n_ok;
+    else if (v == SFFT_PARTIAL) { ++n_part; if (worst == SFFT_OK) worst = SFFT_PARTIAL; }
+    else { ++n_err; if (worst >= 0) worst = v; }
+  }
+  *worst_out = worst;
+  if (rep) {
+    memset(rep, 0, sizeof *rep);
+    for (int s = 0; s < batch; ++s) { rep->samples_used += hsamp[s]; rep->cmacs += hcm[s]; rep->cmacs_i8 += hcm8[s]; }
+    rep->i8_limbs = P->i8_ok ? P->i8.S : 0;
+    rep->n_expsum_i8 = n_expsum_i8;
+    rep->iterations = last_iter;
+    rep->n_ok = n_ok; rep->n_partial = n_part; rep->n_error = n_err;
+    rep->status = worst;
+    rep->n_iter_logged = std::min(last_iter, kLogIters);
+    for (int i = 0; i < rep->n_iter_logged; ++i) { rep->primes[i] = hlog[2 * i]; rep->accepted[i] = hlog[2 * i + 1]; }
+    rep->kernel_launches = launches;
+    rep->n_expsum = n_expsum;
+  }
+  return SFFT_OK;
+}
+
+// ---------------------------------------------------------------- NCCL (line sharding), loaded at run time
+// Only the five entry points the record all-gather needs; types as in nccl.h (ABI-stable since 2.x).
+struct NcclUid { char internal[128]; };
+struct NcclApi {
+  bool ok = false;
+  int (*get_unique_id)(NcclUid*) = nullptr;
+  int (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
+  int (*all_gather)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  const char* (*get_error_string)(int) = nullptr;
+};
+constexpr int kNcclInt64 = 4;   // ncclInt64
+
+const NcclApi& nccl_api() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);   // the copy already loaded (torch)
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<int (*)(NcclUid*)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<int (*)(void**, int, NcclUid, int)>(dlsym(h, "ncclCommInitRank"));
+    a.all_gather = reinterpret_cast<int (*)(const void*, void*, size_t, int, void*, cudaStream_t)>(dlsym(h, "ncclAllGather"));
+    a.comm_destroy = reinterpret_cast<int (*)(void*)>(dlsym(h, "ncclCommDestroy"));
+    a.get_error_string = reinterpret_cast<const char* (*)(int)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.all_gather && a.comm_destroy && a.get_error_string;
+    return a;
+  }();
+  return api;
+}
+
+int nccl_allgather(sfft_plan_t* P, const int64_t* send, int64_t* recv, size_t words) {
+  const NcclApi& n = nccl_api();
+  const int r = n.all_gather(send, recv, words, kNcclInt64, P->nccl_comm, P->stream);
+  if (r != 0) return fail(P, SFFT_ENCCL, "ncclAllGather: %s", n.get_error_string(r));
+  return SFFT_OK;
+}
 
 }  // namespace
 
@@ -469,6 +668,10 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->expsum_path = opt->expsum_path;
     if (P->expsum_path < 0 || P->expsum_path > 2) return SFFT_EINVAL;
     if (opt->fallback_tilts < 0 || opt->fallback_tilts > 4) return SFFT_EINVAL;
+    if (opt->line_shards < 0 || (opt->line_shards > 0 && (opt->line_rank < 0 || opt->line_rank >= opt->line_shards)))
+      return SFFT_EINVAL;
+    P->line_G = opt->line_shards;
+    P->line_g = opt->line_shards > 0 ? opt->line_rank : 0;
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -488,6 +691,18 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   }
   P->r = (int32_t)P->blocks.size();
   P->L = P->r + 1;
+  P->L_ref = P->L;
+  if (P->line_G > 0) {
+    if (P->line_G > P->r) return SFFT_EINVAL;                 // every shard owns at least one shifted line
+    int lo, hi, lo0, hi0;
+    line_shard_range(P->r, P->line_G, P->line_g, &lo, &hi);
+    line_shard_range(P->r, P->line_G, 0, &lo0, &hi0);
+    P->line_lo = lo;
+    P->L = 1 + (hi - lo);
+    P->L_ref = 1 + (hi0 - lo0);
+    P->rec_fw = (k + 1) / 2;
+    P->rec_words = P->rec_fw + (P->L_ref - 1) * k;
+  }
   int64_t B = 1;
   int32_t off = 0;
   for (int q = 0; q < P->r; ++q) {
@@ -648,11 +863,11 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   P->kk = 2 * k;
   P->H = 1;
   while (P->H < 2 * k) P->H <<= 1;
-  P->shape = choose_expsum_shape(P->L);
+  P->shape = choose_expsum_shape(P->L_ref);
   P->Lp = P->shape.nt * P->shape.bn;
   // int8-limb tensor-core exp-sum (bin-domain residual only: its B limbs are the fixed signal rows)
   if (P->expsum_path != 1 && !P->literal)
-    P->i8_ok = i8_configure(P->L, *std::max_element(P->lvl_E.begin(), P->lvl_E.end()), P->k, &P->i8);
+    P->i8_ok = i8_configure(P->L_ref, *std::max_element(P->lvl_E.begin(), P->lvl_E.end()), P->k, &P->i8);
   if (P->i8_ok && P->i8.small_l && P->expsum_path == 0) P->i8_ok = false;
   if (P->expsum_path == 2 && !P->i8_ok) return SFFT_ENOTSUP;
   // shared-memory budgets of the other kernels
@@ -693,6 +908,7 @@ int sfft_plan_info(const sfft_plan_t* plan, int64_t* E, int32_t* r, int32_t* L, 
 
 void sfft_plan_destroy(sfft_plan_t* plan) {
   if (!plan) return;
+  if (plan->nccl_comm && nccl_api().ok) nccl_api().comm_destroy(plan->nccl_comm);
   if (plan->ws_owned && plan->ws) cudaFree(plan->ws);
   if (plan->h_ctrl) cudaFreeHost(plan->h_ctrl);
   for (cudaEvent_t e : plan->events) cudaEventDestroy(e);
@@ -718,6 +934,8 @@ void sfft_signal_destroy(sfft_signal_t* sig) { delete sig; }
 int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs, double* out_coeffs,
                  int32_t* out_count, int32_t* out_status, sfft_report* rep) {
   if (!plan || !sig || sig->plan != plan || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
+  if (plan->line_G > 1 && !plan->nccl_comm)
+    return fail(plan, SFFT_EINVAL, "line-sharded plan (%d shards) needs sfft_comm_init or sfft_execute_group", plan->line_G);
   int rc = ensure_ready(plan);
   if (rc) return rc;
   sfft_plan_t* P = plan;
@@ -737,71 +955,30 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     return cudaEventRecord(P->events[n_ev++], st) == cudaSuccess ? 0 : -1;
   };
   mark();
-  LAUNCH(P, launch_project(D, batch, sig->freqs, sig->coeffs, st));
-  launches += 1;   // init_state_kernel
-  if (P->i8_ok) {
-    LAUNCH(P, launch_i8_prepare(D, batch, P->k, st));
-    launches += 1;   // sigma + limbs
-  }
+  if ((rc = solve_begin(P, D, sig, launches))) return rc;
   int iter = 1;
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
   std::vector<size_t> it_marks, it_i8;
   for (; iter <= P->max_iter; ++iter) {
-    LAUNCH(P, launch_setup(D, iter, st));
-    CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaStreamSynchronize(st));
-    const int n_active = P->h_ctrl[0], max_p = P->h_ctrl[1];
-    if (n_active == 0) break;
-    const int fi = fft_index_host(P, max_p);
-    if (fi < 0) return fail(P, SFFT_ENOTSUP, "p=%d beyond FFT table", max_p);
-    const int max_M = P->fft[fi].M;
-    const int max_K = P->h_ctrl[2];
-    // term split when the (signal x h-tile x n-tile) grid cannot fill the GPU (late iterations)
-    int ksplit = 1;
-    const ExpsumShape shp = expsum_for_p(P->shape, max_p);
-    const bool use_i8 = P->i8_ok && i8_use_for(P, max_p);
-    if (use_i8) {
-      ksplit = i8_ksplit(P, max_p, n_active);
-    } else {
-      // wave quantisation model: time ~ ceil(B ks / W) / ks, W = resident CTAs; a split costs ~3 %
-      // (partial lines written and re-read by the FFT)
-      const int blocks = expsum_blocks(shp, max_p, n_active);
-      const int W = P->n_sm * expsum_occupancy(shp, max_p);
-      const int chunks = (max_K + expsum_bk() - 1) / expsum_bk();
-      const int ks_max = std::min(32, std::max(1, chunks / 2));
-      double best = 1e30;
-      for (int ks = 1; ks <= ks_max; ++ks) {
-        if (ks > 1 && (size_t)ks * n_active * P->L * (size_t)max_p * 16 > kPartBytes) break;
-        const double waves = std::ceil((double)blocks * ks / W);
-        const double t = waves / ks * (ks > 1 ? 1.03 : 1.0);
-        if (t < best - 1e-9) { best = t; ksplit = ks; }
-      }
-    }
+    IterPlan it;
+    if ((rc = iter_setup(P, D, iter, &it, launches))) return rc;
+    if (it.n_active == 0) break;
     if (P->profile) it_marks.push_back(n_ev);
     mark();
-    const int big = max_M >= kFftBigM;
-    LAUNCH(P, launch_fft_prep(D, n_active, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, st, ++P->epoch));
-    launches += 2;   // tables_assign, terms
-    mark();
-    if (use_i8)
-      LAUNCH(P, launch_expsum_i8(D, P->i8, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, P->smem_optin, st));
-    else
-      LAUNCH(P, launch_expsum(D, shp, max_p, n_active, ksplit, ptr<double2>(P, B_PART), max_p, st));
-    ++n_expsum;
-    mark();
-    D.lines_log = use_i8 ? 1 : 0;
-    LAUNCH(P, launch_pfft(D, n_active, P->L, (int)P->fft[fi].smem_upto, fft_threads(max_M), big, ksplit,
-                          ptr<double2>(P, B_PART), max_p, st));
-    D.lines_log = 0;
-    mark();
-    D.i8_iter = use_i8 ? 1 : 0;
-    LAUNCH(P, launch_decode(D, iter, max_p, n_active, st));
-    D.i8_iter = 0;
-    if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
-      LAUNCH(P, launch_retilt(D, batch, sig->freqs, st));
-      if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, batch, P->k, st, true));
+    if ((rc = iter_front(P, D, iter, it, launches, mark))) return rc;
+    if (P->line_G > 0) {
+      // line sharding: all-gather of this shard's records (one rank: a device copy), then the commit
+      const size_t words = (size_t)batch * P->rec_words;
+      if (P->nccl_comm) {
+        if ((rc = nccl_allgather(P, ptr<int64_t>(P, B_RSEND), ptr<int64_t>(P, B_RRECV), words))) return rc;
+      } else {
+        CUDA_TRY(P, cudaMemcpyAsync(ptr<int64_t>(P, B_RRECV), ptr<int64_t>(P, B_RSEND), 8 * words,
+                                    cudaMemcpyDeviceToDevice, st));
+      }
     }
-    if (use_i8) { ++n_expsum_i8; it_i8.push_back(it_marks.empty() ? 0 : it_marks.back()); }
+    if ((rc = iter_back(P, D, iter, it, sig, launches))) return rc;
+    ++n_expsum;
+    if (it.use_i8) { ++n_expsum_i8; it_i8.push_back(it_marks.empty() ? 0 : it_marks.back()); }
     mark();
     last_iter = iter;
   }
@@ -809,65 +986,125 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   LAUNCH(P, launch_wrap(D, batch, out_freqs, out_coeffs, out_count, ostat, ptr<int32_t>(P, B_WRAPS), st));
   launches += 2;   // digits, rank, gather
   mark();
-  // report
-  std::vector<int32_t> hs(batch);
-  CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-  std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
-  std::vector<int32_t> hlog(2 * kLogIters);
-  if (rep) {
-    CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
+  int worst = 0;
+  if ((rc = solve_report(P, D, batch, ostat, rep, last_iter, launches, n_expsum, n_expsum_i8, &worst))) return rc;
+  if (rep && P->profile && getenv("SFFT_DEBUG")) {
+    for (size_t it = 0; it < it_marks.size(); ++it) {
+      float a = 0, b = 0, c = 0, d = 0;
+      const size_t m0 = it_marks[it];
+      cudaEventElapsedTime(&a, P->events[m0], P->events[m0 + 1]);
+      cudaEventElapsedTime(&b, P->events[m0 + 1], P->events[m0 + 2]);
+      cudaEventElapsedTime(&c, P->events[m0 + 2], P->events[m0 + 3]);
+      cudaEventElapsedTime(&d, P->events[m0 + 3], P->events[m0 + 4]);
+      fprintf(stderr, "[sfft] iter %zu prep %.3f expsum %.3f pfft %.3f decode %.3f ms\n", it + 1, a, b, c, d);
+    }
   }
-  CUDA_TRY(P, cudaStreamSynchronize(st));
-  int worst = SFFT_OK, n_ok = 0, n_part = 0, n_err = 0;
-  for (int s = 0; s < batch; ++s) {
-    const int v = hs[s];
-    if (v == SFFT_OK) ++n_ok;
-    else if (v == SFFT_PARTIAL) { ++n_part; if (worst == SFFT_OK) worst = SFFT_PARTIAL; }
-    else { ++n_err; if (worst >= 0) worst = v; }
+  if (rep && P->profile && n_ev >= 2) {
+    auto el = [&](size_t a, size_t b) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, P->events[a], P->events[b]);
+      return ms;
+    };
+    float tot = el(0, n_ev - 1), fx = 0.f, ff = 0.f, fd = 0.f;
+    for (size_t m0 : it_marks) {
+      ff += el(m0, m0 + 1) + el(m0 + 2, m0 + 3);
+      fx += el(m0 + 1, m0 + 2);
+      fd += el(m0 + 3, m0 + 4);
+    }
+    rep->ms_expsum = fx;
+    for (size_t m0 : it_i8) rep->ms_expsum_i8 += el(m0 + 1, m0 + 2);
+    rep->ms_fft = ff;
+    rep->ms_decode = fd;
+    rep->ms_other = tot - fx - ff - fd;
   }
-  if (rep) {
-    memset(rep, 0, sizeof *rep);
-    for (int s = 0; s < batch; ++s) { rep->samples_used += hsamp[s]; rep->cmacs += hcm[s]; rep->cmacs_i8 += hcm8[s]; }
-    rep->i8_limbs = P->i8_ok ? P->i8.S : 0;
-    rep->n_expsum_i8 = n_expsum_i8;
-    rep->iterations = last_iter;
-    rep->n_ok = n_ok; rep->n_partial = n_part; rep->n_error = n_err;
-    rep->status = worst;
-    rep->n_iter_logged = std::min(last_iter, kLogIters);
-    for (int i = 0; i < rep->n_iter_logged; ++i) { rep->primes[i] = hlog[2 * i]; rep->accepted[i] = hlog[2 * i + 1]; }
-    rep->kernel_launches = launches;
-    rep->n_expsum = n_expsum;
-    if (P->profile && getenv("SFFT_DEBUG")) {
-      for (size_t it = 0; it < it_marks.size(); ++it) {
-        float a = 0, b = 0, c = 0, d = 0;
-        const size_t m0 = it_marks[it];
-        cudaEventElapsedTime(&a, P->events[m0], P->events[m0 + 1]);
-        cudaEventElapsedTime(&b, P->events[m0 + 1], P->events[m0 + 2]);
-        cudaEventElapsedTime(&c, P->events[m0 + 2], P->events[m0 + 3]);
-        cudaEventElapsedTime(&d, P->events[m0 + 3], P->events[m0 + 4]);
-        fprintf(stderr, "[sfft] iter %zu prep %.3f expsum %.3f pfft %.3f decode %.3f ms\n", it + 1, a, b, c, d);
+  return worst;
+}
+
+int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* sigs, int32_t n_plans,
+                       int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
+                       sfft_report* rep) {
+  if (!plans || !sigs || n_plans < 1 || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
+  sfft_plan_t* P0 = plans[0];
+  if (!P0) return SFFT_EINVAL;
+  const int G = n_plans;
+  for (int g = 0; g < G; ++g) {
+    sfft_plan_t* P = plans[g];
+    if (!P || !sigs[g] || sigs[g]->plan != P) return SFFT_EINVAL;
+    if (P->line_G != G || P->line_g != g) return fail(P0, SFFT_EINVAL, "plan %d is not line shard %d of %d", g, g, G);
+    if (P->stream != P0->stream || P->device != P0->device) return fail(P0, SFFT_EINVAL, "shards must share device and stream");
+    if (P->k != P0->k || P->r != P0->r || P->d != P0->d || sigs[g]->batch != sigs[0]->batch) return SFFT_EINVAL;
+    const int rc = ensure_ready(P);
+    if (rc) return rc;
+  }
+  cudaStream_t st = P0->stream;
+  const int32_t batch = sigs[0]->batch;
+  std::vector<DevParams> D(G);
+  int launches = 0, rc;
+  auto nomark = []() -> int { return 0; };
+  for (int g = 0; g < G; ++g) {
+    D[g] = dev_params(plans[g], batch);
+    if ((rc = solve_begin(plans[g], D[g], sigs[g], launches))) return rc;
+  }
+  int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
+  const size_t words = (size_t)batch * P0->rec_words;
+  for (int iter = 1; iter <= P0->max_iter; ++iter) {
+    std::vector<IterPlan> it(G);
+    for (int g = 0; g < G; ++g) {
+      if ((rc = iter_setup(plans[g], D[g], iter, &it[g], launches))) return rc;
+      if (it[g].n_active != it[0].n_active || it[g].max_p != it[0].max_p)
+        return fail(P0, SFFT_ECORRUPT, "line shards diverged at iteration %d", iter);
+    }
+    if (it[0].n_active == 0) break;
+    for (int g = 0; g < G; ++g)
+      if ((rc = iter_front(plans[g], D[g], iter, it[g], launches, nomark))) return rc;
+    for (int g = 0; g < G; ++g)          // the all-gather: shard g's records into slot g of every shard
+      for (int h = 0; h < G; ++h)
+        CUDA_TRY(P0, cudaMemcpyAsync(ptr<int64_t>(plans[h], B_RRECV) + (size_t)g * words, ptr<int64_t>(plans[g], B_RSEND),
+                                     8 * words, cudaMemcpyDeviceToDevice, st));
+    for (int g = 0; g < G; ++g)
+      if ((rc = iter_back(plans[g], D[g], iter, it[g], sigs[g], launches))) return rc;
+    ++n_expsum;
+    if (it[0].use_i8) ++n_expsum_i8;
+    last_iter = iter;
+  }
+  // the shards' registries must be bitwise identical (same F_0, same records, same update order)
+  {
+    std::vector<int32_t> nR0(batch), nRg(batch);
+    CUDA_TRY(P0, cudaMemcpyAsync(nR0.data(), D[0].st_nR, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    const size_t va = 8 * (size_t)batch * P0->r * P0->kk, aa = 16 * (size_t)batch * P0->k;
+    std::vector<char> v0(va), a0(aa), vg(va), ag(aa);
+    CUDA_TRY(P0, cudaMemcpyAsync(v0.data(), D[0].v_all, va, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P0, cudaMemcpyAsync(a0.data(), D[0].a_reg, aa, cudaMemcpyDeviceToHost, st));
+    for (int g = 1; g < G; ++g) {
+      CUDA_TRY(P0, cudaMemcpyAsync(nRg.data(), D[g].st_nR, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(P0, cudaMemcpyAsync(vg.data(), D[g].v_all, va, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(P0, cudaMemcpyAsync(ag.data(), D[g].a_reg, aa, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(P0, cudaStreamSynchronize(st));
+      for (int s = 0; s < batch; ++s) {
+        if (nRg[s] != nR0[s]) return fail(P0, SFFT_ECORRUPT, "shard %d signal %d: |R| %d vs %d", g, s, nRg[s], nR0[s]);
+        for (int q = 0; q < P0->r; ++q) {
+          const size_t o = 8 * (((size_t)s * P0->r + q) * P0->kk + P0->k);
+          if (memcmp(v0.data() + o, vg.data() + o, 8 * (size_t)nR0[s]))
+            return fail(P0, SFFT_ECORRUPT, "shard %d signal %d: registry keys differ", g, s);
+        }
+        if (memcmp(a0.data() + 16 * (size_t)s * P0->k, ag.data() + 16 * (size_t)s * P0->k, 16 * (size_t)nR0[s]))
+          return fail(P0, SFFT_ECORRUPT, "shard %d signal %d: registry coefficients differ", g, s);
       }
     }
-    if (P->profile && n_ev >= 2) {
-      auto el = [&](size_t a, size_t b) {
-        float ms = 0.f;
-        cudaEventElapsedTime(&ms, P->events[a], P->events[b]);
-        return ms;
-      };
-      float tot = el(0, n_ev - 1), fx = 0.f, ff = 0.f, fd = 0.f;
-      for (size_t m0 : it_marks) {
-        ff += el(m0, m0 + 1) + el(m0 + 2, m0 + 3);
-        fx += el(m0 + 1, m0 + 2);
-        fd += el(m0 + 3, m0 + 4);
-      }
-      rep->ms_expsum = fx;
-      for (size_t m0 : it_i8) rep->ms_expsum_i8 += el(m0 + 1, m0 + 2);
-      rep->ms_fft = ff;
-      rep->ms_decode = fd;
-      rep->ms_other = tot - fx - ff - fd;
+  }
+  sfft_plan_t* P = P0;
+  int32_t* ostat = out_status ? out_status : ptr<int32_t>(P, B_OUT_S);
+  LAUNCH(P, launch_wrap(D[0], batch, out_freqs, out_coeffs, out_count, ostat, ptr<int32_t>(P, B_WRAPS), st));
+  launches += 2;
+  int worst = 0;
+  if ((rc = solve_report(P, D[0], batch, ostat, rep, last_iter, launches, n_expsum, n_expsum_i8, &worst))) return rc;
+  if (rep) {            // exp-sum work of every shard
+    for (int g = 1; g < G; ++g) {
+      std::vector<int64_t> hcm(batch), hcm8(batch);
+      CUDA_TRY(P0, cudaMemcpyAsync(hcm.data(), D[g].st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(P0, cudaMemcpyAsync(hcm8.data(), D[g].st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(P0, cudaStreamSynchronize(st));
+      for (int s = 0; s < batch; ++s) { rep->cmacs += hcm[s]; rep->cmacs_i8 += hcm8[s]; }
     }
   }
   return worst;
@@ -998,11 +1235,43 @@ int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int64_t* v_o
   return SFFT_OK;
 }
 
+int sfft_line_shard_range(int32_t r, int32_t G, int32_t g, int32_t* lo, int32_t* hi) {
+  if (!lo || !hi || r < 1 || G < 1 || G > r || g < 0 || g >= G) return SFFT_EINVAL;
+  int a, b;
+  line_shard_range(r, G, g, &a, &b);
+  *lo = a;
+  *hi = b;
+  return SFFT_OK;
+}
+
+int sfft_comm_unique_id(void* out) {
+  if (!out) return SFFT_EINVAL;
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return SFFT_ENCCL;
+  NcclUid id;
+  if (n.get_unique_id(&id) != 0) return SFFT_ENCCL;
+  memcpy(out, id.internal, sizeof id.internal);
+  return SFFT_OK;
+}
+
 int sfft_comm_init(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* nccl_unique_id, int32_t shard_mode) {
-  (void)nccl_unique_id;
   if (!plan || nranks < 1 || rank < 0 || rank >= nranks) return SFFT_EINVAL;
   if (shard_mode == 0) return SFFT_OK;   // signal sharding: independent solves, no communicator
-  return fail(plan, SFFT_ENOTSUP, "line sharding (shard_mode 1) is not built yet");
+  if (shard_mode != 1 || !nccl_unique_id) return SFFT_EINVAL;
+  if (plan->line_G != nranks || plan->line_g != rank)
+    return fail(plan, SFFT_EINVAL, "plan is line shard %d of %d, communicator rank %d of %d", plan->line_g,
+                plan->line_G, rank, nranks);
+  if (plan->nccl_comm) return fail(plan, SFFT_EINVAL, "communicator already initialised");
+  const NcclApi& n = nccl_api();
+  if (!n.ok) return fail(plan, SFFT_ENCCL, "libnccl.so.2 not loadable");
+  CUDA_TRY(plan, cudaSetDevice(plan->device));
+  NcclUid id;
+  memcpy(id.internal, nccl_unique_id, sizeof id.internal);
+  void* comm = nullptr;
+  const int r = n.comm_init_rank(&comm, nranks, id, rank);
+  if (r != 0) return fail(plan, SFFT_ENCCL, "ncclCommInitRank: %s", n.get_error_string(r));
+  plan->nccl_comm = comm;
+  return SFFT_OK;
 }
 
 }  // extern "C"

@@ -104,7 +104,14 @@ size_t decode_smem_bytes(const DevParams& P, int32_t max_p) {
   return sizeof(double) * (size_t)max_p + sizeof(int) * (2 * (size_t)max_p + 2 * (size_t)P.k + 64);
 }
 
-template <bool STAGE>
+// MODE 0: the whole decode.  Line sharding splits it: MODE 1 (local) runs steps 0-2 on this
+// shard's lines and writes the per-candidate record (pass flag over the local lines, decoded coordinates of
+// the local axes); MODE 2 (commit), after the all-gather, ANDs the flags of every shard, unpacks the
+// coordinates and runs steps 2b-5.  Line 0 is local to every shard and computed by the same kernels, so the
+// candidate list and F_0 are bitwise identical on all shards and every shard applies the same registry update.
+enum { kDecFull = 0, kDecLocal = 1, kDecCommit = 2 };
+
+template <bool STAGE, int MODE>
 __global__ void __launch_bounds__(kDecodeThreads)
 decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, int64_t* out_v,
               double2* out_a, int32_t* out_counts) {
@@ -128,6 +135,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   int* scratch = found + P.k;
 
   double2* Fw = P.lines + (int64_t)s * P.L * P.p_stride;        // line n at F + n * p_stride
+  int64_t* accv = P.acc_v + (int64_t)s * r * P.k;               // [r][k], column = candidate index
   const double2* F = Fw;
   const double floor_abs = P.floor_rel * (double)p;
 
@@ -135,6 +143,8 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   //      bins p * sum_{e: v_{e,m} = b mod p} C_reg[e][n] (Eq. (3) applied to g, which is synthesised
   //      from R, not sampled: reading R18).  Entries of a bin are summed in ascending e (stable
   //      counting sort), so the result is deterministic.
+  int nc = 0, total = 0;
+  if (MODE != kDecCommit) {
   if (!STAGE && !P.literal && nR > 0) {
     int* cnt = cand;                                   // [p] entries per bin
     int* pos = flag;                                   // [p] running end of each bin
@@ -204,7 +214,6 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   }
 
   // ---- 1. select (ascending b): coalesced sweep, ballot + block prefix per 1024-bin round ----
-  int total = 0;
   for (int b0 = 0; b0 < p; b0 += blockDim.x) {
     const int b = b0 + tid;
     double mg = 0.0;
@@ -220,7 +229,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     total += round_total;
   }
   __syncthreads();
-  int nc = total;
+  nc = total;
   if (nc > kstar) {
     // keep the k* largest |F_0| (ties -> smaller b), preserve ascending order
     for (int i = tid; i < nc; i += blockDim.x) {
@@ -252,20 +261,21 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   // a pair failing Eq. (42) or the rounding / range checks clears its candidate's flag (benign race: all
   // writers store 0).  The decisions are those of a per-candidate loop: ok = AND over n of the same
   // per-line tests.
-  int64_t* accv = P.acc_v + (int64_t)s * r * P.k;       // [r][k], column = candidate index
   const double twopi = 6.283185307179586476925286766559;
   for (int ci = tid; ci < nc; ci += blockDim.x) flag[ci] = 1;
   __syncthreads();
   {
-    const int tot = nc * r;
+    const int nl = P.L - 1;                               // local shifted lines (= r unsharded)
+    int64_t* sendv = MODE == kDecLocal ? P.rec_send + (int64_t)s * P.rec_words + P.rec_fw : nullptr;
+    const int tot = nc * nl;
     for (int t0 = tid; t0 < tot; t0 += 4 * blockDim.x) {
       double2 fv[4], f0[4];
       int ci[4], n[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int t = t0 + u * blockDim.x;
-        ci[u] = t < tot ? t / r : 0;
-        n[u] = t < tot ? t - ci[u] * r : -1;
+        ci[u] = t < tot ? t / nl : 0;
+        n[u] = t < tot ? t - ci[u] * nl : -1;
         const int b = cand[ci[u]];
         f0[u] = F[b];
         fv[u] = n[u] >= 0 ? F[(int64_t)(1 + n[u]) * P.p_stride + b] : make_double2(0.0, 0.0);
@@ -284,14 +294,47 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
           const double xr = rint(x);
           good = fabs(x - xr) <= P.round_tol;
           const int64_t v = (int64_t)xr;
-          if (P.extra & 1) good = good && v >= lo_v[n[u]] && v <= hi_v[n[u]];
-          accv[(int64_t)n[u] * P.k + ci[u]] = v;
+          const int ng = P.line_lo + n[u];                 // reduced axis of the line
+          if (P.extra & 1) good = good && v >= lo_v[ng] && v <= hi_v[ng];
+          if (MODE == kDecLocal) sendv[(int64_t)n[u] * P.k + ci[u]] = v;
+          else accv[(int64_t)ng * P.k + ci[u]] = v;
         }
         if (!good) flag[ci[u]] = 0;
       }
     }
   }
   __syncthreads();
+  if (MODE == kDecLocal) {
+    int32_t* sendf = reinterpret_cast<int32_t*>(P.rec_send + (int64_t)s * P.rec_words);
+    for (int ci = tid; ci < nc; ci += blockDim.x) {
+      sendf[ci] = flag[ci];
+      P.rec_cand[(int64_t)s * P.k + ci] = cand[ci];
+    }
+    if (tid == 0) P.rec_nc[s] = nc;
+    return;
+  }
+  } else {
+    // ---- commit: candidates of the local phase, flags ANDed over the shards, coordinates unpacked ----
+    nc = P.rec_nc[s];
+    for (int ci = tid; ci < nc; ci += blockDim.x) {
+      cand[ci] = P.rec_cand[(int64_t)s * P.k + ci];
+      int f = 1;
+      for (int g = 0; g < P.line_G; ++g)
+        f &= reinterpret_cast<const int32_t*>(P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words)[ci];
+      flag[ci] = f;
+    }
+    __syncthreads();
+    for (int g = 0; g < P.line_G; ++g) {
+      int glo, ghi;
+      line_shard_range(r, P.line_G, g, &glo, &ghi);
+      const int64_t* rv = P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words + P.rec_fw;
+      for (int t = tid; t < (ghi - glo) * nc; t += blockDim.x) {
+        const int nn = t / nc, ci = t - nn * nc;
+        if (flag[ci]) accv[(int64_t)(glo + nn) * P.k + ci] = rv[(int64_t)nn * P.k + ci];
+      }
+    }
+    __syncthreads();
+  }
   if (P.extra & 2) {
     for (int ci = tid; ci < nc; ci += blockDim.x)
       if (flag[ci] && mod_pos64(accv[(int64_t)m * P.k + ci], p) != cand[ci]) flag[ci] = 0;
@@ -394,7 +437,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     double2 c;
     if (n == 0) c = make_double2(-a.x, -a.y);
     else if (n < P.L) {
-      const double2 lf = line_factor_d(vreg[(int64_t)(n - 1) * P.kk + e], Ev);
+      const double2 lf = line_factor_d(vreg[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
       c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
     } else c = make_double2(0.0, 0.0);
     Creg[(int64_t)e * P.Lp + n] = c;
@@ -442,7 +485,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     const int K = P.k + (P.literal ? nR : 0);
     P.st_nR[s] = nR_final;
     int stall = na == 0 ? P.st_stall[s] + 1 : 0;
-    P.st_samples[s] += (int64_t)P.L * p;
+    P.st_samples[s] += (int64_t)(r + 1) * p;              // f evaluations of all shards (reading C22)
     P.st_cmacs[s] += (int64_t)P.L * p * K;
     if (P.i8_iter) P.st_cmacs_i8[s] += (int64_t)P.L * p * K;
     P.st_iters[s] = iter;
@@ -511,7 +554,7 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
     __syncwarp();
     const double2 a = Cs[(int64_t)j * P.Lp];                       // column 0 = a_j
     for (int n = 1 + lane; n < P.L; n += 32) {
-      const double2 lf = line_factor_d(vs[(int64_t)(n - 1) * kk + j], E);
+      const double2 lf = line_factor_d(vs[(int64_t)(P.line_lo + n - 1) * kk + j], E);
       Cs[(int64_t)j * P.Lp + n] = make_double2(a.x * lf.x - a.y * lf.y, a.x * lf.y + a.y * lf.x);
     }
   }
@@ -583,7 +626,7 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
     double2 c;
     if (n == 0) c = make_double2(-a.x, -a.y);
     else if (n < P.L) {
-      const double2 lf = line_factor_d(vreg[(int64_t)(n - 1) * kk + e], E);
+      const double2 lf = line_factor_d(vreg[(int64_t)(P.line_lo + n - 1) * kk + e], E);
       c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
     } else c = make_double2(0.0, 0.0);
     Creg[(int64_t)e * P.Lp + n] = c;
@@ -599,12 +642,13 @@ cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freq
   return cudaGetLastError();
 }
 
-cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st) {
+cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st, int mode) {
   const size_t smem = decode_smem_bytes(P, max_p);
-  cudaError_t e = cudaFuncSetAttribute(decode_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = mode == kDecLocal ? decode_kernel<false, kDecLocal>
+            : mode == kDecCommit ? decode_kernel<false, kDecCommit> : decode_kernel<false, kDecFull>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (n_active > 0)
-    decode_kernel<false><<<n_active, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
+  if (n_active > 0) kern<<<n_active, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -612,9 +656,9 @@ cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_
                                 double* acc_a, int32_t* counts, cudaStream_t st) {
   const int max_p = (int)P.p_stride;
   const size_t smem = decode_smem_bytes(P, max_p);
-  cudaError_t e = cudaFuncSetAttribute(decode_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(decode_kernel<true, kDecFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  decode_kernel<true><<<1, kDecodeThreads, smem, st>>>(P, 0, kstar, acc_b, acc_v,
+  decode_kernel<true, kDecFull><<<1, kDecodeThreads, smem, st>>>(P, 0, kstar, acc_b, acc_v,
                                                         reinterpret_cast<double2*>(acc_a), counts);
   return cudaGetLastError();
 }

@@ -55,7 +55,7 @@ __global__ void project_kernel(DevParams P, int32_t batch, const int32_t* __rest
   for (int n = lane; n < P.Lp; n += 32) {
     double2 c;
     if (n == 0) c = a;
-    else if (n < P.L) c = cmul(a, line_factor(vs[(int64_t)(n - 1) * P.kk + j], P.E));
+    else if (n < P.L) c = cmul(a, line_factor(vs[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
     else c = make_double2(0.0, 0.0);
     Crow[n] = c;
   }
@@ -103,7 +103,7 @@ __global__ void line_coeffs_kernel(DevParams P, int32_t K, const double2* __rest
   for (int n = lane; n < P.Lp; n += 32) {
     double2 v;
     if (n == 0) v = a;
-    else if (n < P.L) v = cmul(a, line_factor(P.v_all[(int64_t)(n - 1) * P.kk + j], P.E));
+    else if (n < P.L) v = cmul(a, line_factor(P.v_all[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
     else v = make_double2(0.0, 0.0);
     Crow[n] = v;
   }

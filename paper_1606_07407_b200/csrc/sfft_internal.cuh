@@ -115,7 +115,25 @@ struct DevParams {
   int32_t i8_estride;          // >= kk + 16, multiple of 4
   int32_t lines_log;           // launch flag: the lines hold samples in discrete-log order (int8 exp-sum)
   int64_t i8_tstride;          // >= p_stride + 8 (bulk copies round the table up to 16 bytes)
+  // line sharding: shard line_g of line_G holds line 0 and the shifted lines of reduced axes
+  // [line_lo, line_lo + L - 1); its decode is split into a local test (records) and a commit after the
+  // all-gather of the records.  Unsharded plans: line_G = 1, line_lo = 0, L = r + 1, no records.
+  int32_t line_lo, line_G, line_g;
+  int32_t line_split;          // 1: two-phase decode (records + exchange + commit), also at line_G = 1
+  int32_t rec_words;           // int64 words per signal record: rec_fw flag words (int32 pairs) + (Lmax - 1) k coordinates
+  int32_t rec_fw;              // (k + 1) / 2
+  int64_t* rec_send;           // [batch][rec_words] this shard's records
+  const int64_t* rec_recv;     // [line_G][batch][rec_words] all shards' records (all-gather result)
+  int32_t* rec_cand;           // [batch][k] candidate bins of the local phase (identical on every shard)
+  int32_t* rec_nc;             // [batch] candidate count
 };
+
+// reduced axes [lo, hi) of line shard g of G over r axes (contiguous, sizes differ by at most one; shard 0 largest)
+__host__ __device__ inline void line_shard_range(int r, int G, int g, int* lo, int* hi) {
+  const int base = r / G, extra = r % G;
+  *lo = g * base + (g < extra ? g : extra);
+  *hi = *lo + base + (g < extra ? 1 : 0);
+}
 
 // balanced base-256 digits of X (|X| <= 127 * 256^(S-1)), most significant first (k_expsum_i8.cu, k_fft.cu)
 __device__ __forceinline__ void i8_digits(int64_t X, int S, int (&d)[8]) {
@@ -158,7 +176,9 @@ cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* fre
 cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, cudaStream_t st);
 // k_decode.cu
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st);
-cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st);
+// mode 0: whole decode; 1: local phase of a line shard (records); 2: commit after the record all-gather
+cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st,
+                          int mode = 0);
 // re-projection of the signals that switched fallback level (reading R23); freqs = the execute's input
 cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freqs, cudaStream_t st);
 cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,

@@ -411,3 +411,104 @@ def test_e2e_cta_pair_mode(S):
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                          cwd=os.path.dirname(GOLD_DIR.rstrip("/")).rsplit("/tests", 1)[0])
     assert out.returncode == 0 and "pair ok" in out.stdout, out.stderr[-2000:]
+
+
+# ------------------------------------------------------------------ line sharding
+def _shard_plans(S, c, G, blocks=None, **kw):
+    return [_plan(S, c, blocks, line_shards=G, line_rank=g, **kw) for g in range(G)]
+
+
+def _group_solve(S, plans, w, a):
+    wt, at = torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda()
+    sigs = [S.sfft_signal_expsum(p, wt, at) for p in plans]
+    return S.sfft_execute_group(plans, sigs)
+
+
+@pytest.mark.parametrize("name,tag,trials,G", [("c3", "primary", [0, 1], 2), ("c3", "primary", [2], 5),
+                                               ("c4", "primary", [0, 1], 3), ("c5", "primary", [0], 2),
+                                               ("c5", "alt", [0], 4), ("c2", "primary", range(8), 2)])
+@pytest.mark.parametrize("path", [0, 1])
+def test_e2e_line_shards_group_vs_golden_oracle(S, name, tag, trials, G, path):
+    """Line sharding: G shards each compute line 0 and their axes' lines, exchange per-candidate records
+    and commit the same registry update (sfft_execute_group: the shards on one GPU, the all-gather a device
+    copy).  The group call itself fails (ECORRUPT) unless every shard ends with a bitwise-identical registry;
+    sets, coefficients, the trace of signal 0 and the sample total equal the oracle's."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    blocks = c.blocks if tag == "primary" else c.alt_blocks
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    plans = _shard_plans(S, c, G, blocks, batch=len(trials), expsum_path=path)
+    r = plans[0].r
+    assert sum(p.L - 1 for p in plans) == r and plans[0].L >= plans[-1].L >= plans[0].L - 1
+    res = _group_solve(S, plans, w, a)
+    for i, t in enumerate(trials):
+        key = f"{tag}_{t}"
+        assert int(res.per_status[i]) == int(g[key + "_status"])
+        n = int(res.count[i])
+        assert n == int(g[key + "_count"])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        ra = g[key + "_a"]
+        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+    tr = g[f"{tag}_{trials[0]}_trace"]
+    rep = res.report
+    assert [rep.primes[i] for i in range(min(len(tr), 64))] == tr[:64, 1].tolist()
+    assert [rep.accepted[i] for i in range(min(len(tr), 64))] == tr[:64, 4].tolist()
+    assert rep.samples_used == sum(int(g[f"{tag}_{t}_samples"]) for t in trials)
+
+
+def test_e2e_line_shards_stall_fallback(S):
+    """Line shards through the tilt fallback (levels switch inside the commit, retilt per shard)."""
+    c = W.custom_config(4, 16, 8, (1, 1, 1, 1), structure="rectangles")
+    ws, as_ = [], []
+    for t in range(12):
+        try:
+            w, a = W.make_signal(c, t)
+        except AssertionError:
+            continue
+        ws.append(w)
+        as_.append(a)
+        if len(ws) == 6:
+            break
+    w, a = np.stack(ws).astype(np.int32), np.stack(as_)
+    plans = _shard_plans(S, c, 2, batch=len(ws), fallback_tilts=4)
+    res = _group_solve(S, plans, w, a)
+    P = O.params_for(c, n_fallback=4)
+    for i in range(len(ws)):
+        ref = O.solve(P, w[i], a[i])
+        assert int(res.per_status[i]) == ref.status
+        _check_against_oracle(res, i, ref.w, ref.a, ref.status)
+
+
+def test_e2e_line_shard_nccl_world1(S):
+    """The NCCL transport of line sharding (sfft_comm_init, ncclAllGather on the plan's stream) with one
+    rank: the two-phase decode and the record exchange through the library's NCCL, C3 at full size."""
+    c = W.CONFIGS["c3"]
+    g = _golden("c3")
+    trials = [0, 1]
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, batch=len(trials), line_shards=1, line_rank=0)
+    S.sfft_comm_init(plan, 1, 0, shard_mode=1, unique_id=S.sfft_comm_unique_id())
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for i, t in enumerate(trials):
+        key = f"primary_{t}"
+        n = int(res.count[i])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        ra = g[key + "_a"]
+        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+
+
+def test_line_shard_plan_errors(S):
+    c = W.CONFIGS["c2"]                       # r = 2
+    with pytest.raises(S.SfftError):
+        _plan(S, c, line_shards=3, line_rank=0)             # more shards than axes
+    with pytest.raises(S.SfftError):
+        _plan(S, c, line_shards=2, line_rank=2)
+    plans = _shard_plans(S, c, 2)
+    w, a = W.make_batch(c, [0])
+    with pytest.raises(S.SfftError):                         # a sharded plan alone has no exchange
+        S.solve(plans[0], torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    with pytest.raises(S.SfftError):                         # shard order must match the group
+        _group_solve(S, plans[::-1], w, a)

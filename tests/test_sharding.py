@@ -69,3 +69,56 @@ def test_gather_world2_gloo(n):
         p.join(120)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) is True
+
+
+# ------------------------------------------------------------------ line sharding host logic
+def test_line_shard_ranges_partition_axes():
+    """sfft_line_shard_range (C ABI, host): contiguous, disjoint, covering [0, r), sizes within one, shard 0
+    the largest (its line count fixes the tile shapes of every shard); G > r is rejected."""
+    import paper_1606_07407_b200 as S
+    for r in (1, 2, 3, 10, 20, 50, 500):
+        for G in (1, 2, 3, 4, 7, 8):
+            if G > r:
+                with pytest.raises(S.SfftError):
+                    S.sfft_line_shard_range(r, G, 0)
+                continue
+            rs = [S.sfft_line_shard_range(r, G, g) for g in range(G)]
+            assert rs[0][0] == 0 and rs[-1][1] == r
+            assert all(rs[g][1] == rs[g + 1][0] for g in range(G - 1))
+            sizes = [hi - lo for lo, hi in rs]
+            assert min(sizes) >= 1 and max(sizes) - min(sizes) <= 1 and sizes[0] == max(sizes)
+
+
+def _line_worker(rank, world, port, r, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1606_07407_b200 as S
+        # the communicator bootstrap of comm_init_line_shards: rank 0 draws the NCCL id, the group broadcasts it
+        obj = [S.sfft_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ids = [None] * world
+        dist.all_gather_object(ids, obj[0])
+        shards = [None] * world
+        dist.all_gather_object(shards, S.sfft_line_shard_range(r, world, rank))
+        if rank == 0:
+            axes = [a for lo, hi in shards for a in range(lo, hi)]
+            q.put(len(obj[0]) == 128 and all(i == ids[0] for i in ids) and axes == list(range(r)))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("r", [2, 51])
+def test_line_shard_bootstrap_world2_gloo(r):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_line_worker, args=(rk, 2, port, r, q)) for rk in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    assert all(p.exitcode == 0 for p in procs)
+    assert q.get(timeout=10) is True
