@@ -100,7 +100,7 @@ enum Buf {
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
-  B_RSEND, B_RRECV, B_RCAND, B_RNC,
+  B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -152,6 +152,8 @@ FftSize radix_plan(int M) {
   int S = M;
   for (int8_t R : s.radix) { sumq += S / R; S /= R; }
   s.smem = 16 * ((size_t)M + sumq + 2);
+  // the fused select of a line-0 CTA uses x[p ..) (p <= (M + 1) / 2): mag, cand, flag [p] + scratch[32]
+  s.smem = std::max(s.smem, 32 * (size_t)((M + 1) / 2) + 128);
   return s;
 }
 
@@ -228,11 +230,15 @@ void layout(sfft_plan_t* P) {
   sz[B_FILL] = 4 * T;
   sz[B_I8TLO] = P->i8_ok ? 8 * T * (2 * P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
-  const size_t G = (size_t)std::max(P->line_G, 0);
-  sz[B_RSEND] = G ? 8 * S * (size_t)P->rec_words : 0;
-  sz[B_RRECV] = G ? 8 * G * S * (size_t)P->rec_words : 0;
-  sz[B_RCAND] = G ? 4 * S * (size_t)P->k : 0;
-  sz[B_RNC] = G ? 4 * S : 0;
+  // decode records (fused FFT epilogue -> commit); line shards also receive every shard's records
+  sz[B_RSEND] = 8 * S * (size_t)P->rec_words;
+  sz[B_RRECV] = P->line_G > 0 ? 8 * (size_t)P->line_G * S * (size_t)P->rec_words : 0;
+  sz[B_RCAND] = 4 * S * (size_t)P->k;
+  sz[B_RNC] = 4 * S;
+  sz[B_RF0] = 16 * S * (size_t)P->k;
+  sz[B_SELRDY] = 4 * S;
+  sz[B_BINST] = 4 * S * ((size_t)P->p_stride + 1);
+  sz[B_BINORD] = 4 * S * (size_t)P->k;
   size_t o = 0;
   for (int b = 0; b < B_COUNT; ++b) {
     P->off[b] = o;
@@ -337,12 +343,14 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.line_split = P->line_G > 0;
   D.rec_words = P->rec_words;
   D.rec_fw = P->rec_fw;
-  if (P->line_G > 0) {
-    D.rec_send = ptr<int64_t>(P, B_RSEND);
-    D.rec_recv = ptr<int64_t>(P, B_RRECV);
-    D.rec_cand = ptr<int32_t>(P, B_RCAND);
-    D.rec_nc = ptr<int32_t>(P, B_RNC);
-  }
+  D.rec_send = ptr<int64_t>(P, B_RSEND);
+  D.rec_recv = P->line_G > 0 ? ptr<int64_t>(P, B_RRECV) : ptr<int64_t>(P, B_RSEND);   // unsharded: own records
+  D.rec_cand = ptr<int32_t>(P, B_RCAND);
+  D.rec_nc = ptr<int32_t>(P, B_RNC);
+  D.rec_f0 = ptr<double2>(P, B_RF0);
+  D.sel_ready = ptr<int32_t>(P, B_SELRDY);
+  D.bin_start = ptr<int32_t>(P, B_BINST);
+  D.bin_order = ptr<int32_t>(P, B_BINORD);
   return D;
 }
 
@@ -397,6 +405,8 @@ int ensure_ready(sfft_plan_t* P) {
     // empty per-prime table cache (slot_p = 0, slot_epoch = -1)
     CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SLOTP), 0, 4 * ((size_t)P->n_tslots + 1), P->stream));
     CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SLOTE), 0xFF, 4 * ((size_t)P->n_tslots + 1), P->stream));
+    // fused-decode publication stamps: never equal to an iteration stamp (those are >= 1)
+    CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SELRDY), 0xFF, 4 * (size_t)P->batch, P->stream));
     CUDA_TRY(P, cudaStreamSynchronize(P->stream));
     P->tables_ready = true;
   }
@@ -517,24 +527,23 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
     LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, it.max_p), it.max_p, it.n_active, it.ksplit,
                             ptr<double2>(P, B_PART), it.max_p, st));
   mark();
+  // FFT of every line with the fused select (line 0) / test + decode (lines n >= 1) epilogue -> records
   D.lines_log = it.use_i8 ? 1 : 0;
+  D.fuse_decode = 1;
+  D.it_epoch = P->epoch;
   LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M), it.big, it.ksplit,
                         ptr<double2>(P, B_PART), it.max_p, st));
   D.lines_log = 0;
+  D.fuse_decode = 0;
   mark();
-  D.i8_iter = it.use_i8 ? 1 : 0;
-  LAUNCH(P, launch_decode(D, iter, it.max_p, it.n_active, st, P->line_G > 0 ? 1 : 0));
-  D.i8_iter = 0;
   return SFFT_OK;
 }
 
 int iter_back(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, const sfft_signal_t* sig, int& launches) {
   cudaStream_t st = P->stream;
-  if (P->line_G > 0) {
-    D.i8_iter = it.use_i8 ? 1 : 0;
-    LAUNCH(P, launch_decode(D, iter, it.max_p, it.n_active, st, 2));
-    D.i8_iter = 0;
-  }
+  D.i8_iter = it.use_i8 ? 1 : 0;
+  LAUNCH(P, launch_decode_commit(D, iter, it.max_p, it.n_active, st));
+  D.i8_iter = 0;
   if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
     LAUNCH(P, launch_retilt(D, sig->batch, sig->freqs, st));
     if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch, P->k, st, true));
@@ -700,9 +709,9 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->line_lo = lo;
     P->L = 1 + (hi - lo);
     P->L_ref = 1 + (hi0 - lo0);
-    P->rec_fw = (k + 1) / 2;
-    P->rec_words = P->rec_fw + (P->L_ref - 1) * k;
   }
+  P->rec_fw = (k + 1) / 2;
+  P->rec_words = P->rec_fw + (P->L_ref - 1) * k;
   int64_t B = 1;
   int32_t off = 0;
   for (int q = 0; q < P->r; ++q) {

@@ -2,17 +2,17 @@
 // decode) and a7 (registry update), Algorithm 2 l.6-10 and l.18-34.
 //
 // setup_kernel  : k* = k - |R|, p = i-th prime >= max(2, c k*) (l.8, reading R10), m = i mod r (R9)
-// decode_kernel : one CTA per signal.
-//   1. select   : bins b with |F_0[b]| >= 1e-8 p, ascending b; if more than k* the k* largest (R5)
-//   2. decode   : one warp per candidate, lanes over the r shifted lines:
-//                 Eq. (42) |F_n[b]| / |F_0[b]| within tau of 1 for every n (ballot),
-//                 Eq. (41) v_n = round(Arg(F_n conj F_0) E / 2 pi) with the R12/R13 rejections
+// (the select of line 0 and the per-line collision test + decode run fused in the FFT epilogue, k_fft.cu)
+// decode_kernel<kDecCommit> : one CTA per signal.
+//   2. records  : candidates of line 0, pass flags ANDed over the lines (and line shards), coordinates
+//   2b.         : bin consistency (D_m v) = b mod p (R13)
 //   3. compact  : accepted candidates in ascending b (block prefix sum)
 //   4. registry : R[v] += F_0[b]/p (R14) through an open-addressing hash of the r-long key,
 //                 new entries appended in ascending-b order (deterministic), their C rows
 //                 (-a e^{2 pi i v_n / E}) written for the next iteration's residual; prune (R15)
 //   5. state    : |R|, stall counter (R16), samples (R18), status
-#include "sfft_internal.cuh"
+// decode_kernel<kDecStage> : teacher-forced stage entry point (select + test + decode of given lines).
+#include "decode_common.cuh"
 
 namespace sfft {
 
@@ -57,34 +57,6 @@ cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-// ------------------------------------------------------------------ block helpers
-// exclusive prefix sum over the block; returns the exclusive value, *total gets the sum
-__device__ int block_excl_scan(int v, int* scratch, int* total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int x = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) scratch[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    int t = lane < nw ? scratch[lane] : 0;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, t, o);
-      if (lane >= o) t += y;
-    }
-    if (lane < nw) scratch[lane] = t;       // inclusive warp-prefix
-  }
-  __syncthreads();
-  const int before = warp > 0 ? scratch[warp - 1] : 0;
-  *total = scratch[nw - 1];
-  __syncthreads();
-  return before + x - v;
-}
-
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
@@ -104,23 +76,25 @@ size_t decode_smem_bytes(const DevParams& P, int32_t max_p) {
   return sizeof(double) * (size_t)max_p + sizeof(int) * (2 * (size_t)max_p + 2 * (size_t)P.k + 64);
 }
 
-// MODE 0: the whole decode.  Line sharding splits it: MODE 1 (local) runs steps 0-2 on this
-// shard's lines and writes the per-candidate record (pass flag over the local lines, decoded coordinates of
-// the local axes); MODE 2 (commit), after the all-gather, ANDs the flags of every shard, unpacks the
-// coordinates and runs steps 2b-5.  Line 0 is local to every shard and computed by the same kernels, so the
-// candidate list and F_0 are bitwise identical on all shards and every shard applies the same registry update.
-enum { kDecFull = 0, kDecLocal = 1, kDecCommit = 2 };
+// kDecStage  : teacher-forced entry point -- select, test and decode the caller's lines F, output the accepted.
+// kDecCommit : execute -- the fused FFT epilogue (k_fft.cu) selected the candidates of line 0 and tested every
+//              line (records: pass flag, decoded coordinates); the flags of every line shard are ANDed, the
+//              coordinates unpacked, then steps 2b-5 (bin consistency, accepted list, registry, state).  With
+//              line sharding the records of all shards arrive by the all-gather; line 0 is
+//              computed identically on every shard, so every shard applies the same registry update.
+enum { kDecStage = 0, kDecCommit = 1 };
 
-template <bool STAGE, int MODE>
+template <int MODE>
 __global__ void __launch_bounds__(kDecodeThreads)
 decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, int64_t* out_v,
               double2* out_a, int32_t* out_counts) {
+  constexpr bool STAGE = MODE == kDecStage;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = P.active[blockIdx.x];
   const int p = P.st_p[s], m = P.st_m[s];
   const int nR = P.st_nR[s];
   const int kstar = STAGE ? kstar_stage : P.k - nR;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = blockDim.x >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = P.r;
   const int lvl = STAGE ? 0 : P.st_lvl[s];
   const int64_t Ev = P.lvl_E[lvl];
@@ -134,148 +108,25 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   int* found = accl + P.k;
   int* scratch = found + P.k;
 
-  double2* Fw = P.lines + (int64_t)s * P.L * P.p_stride;        // line n at F + n * p_stride
+  const double2* F = P.lines + (int64_t)s * P.L * P.p_stride;   // line n at F + n * p_stride
   int64_t* accv = P.acc_v + (int64_t)s * r * P.k;               // [r][k], column = candidate index
-  const double2* F = Fw;
-  const double floor_abs = P.floor_rel * (double)p;
-
-  // ---- 0. bin-domain residual (literal == 0): the lines hold DFT_p(f) only; add the registry's
-  //      bins p * sum_{e: v_{e,m} = b mod p} C_reg[e][n] (Eq. (3) applied to g, which is synthesised
-  //      from R, not sampled: reading R18).  Entries of a bin are summed in ascending e (stable
-  //      counting sort), so the result is deterministic.
   int nc = 0, total = 0;
-  if (MODE != kDecCommit) {
-  if (!STAGE && !P.literal && nR > 0) {
-    int* cnt = cand;                                   // [p] entries per bin
-    int* pos = flag;                                   // [p] running end of each bin
-    int* order = accl;                                 // [nR] entries sorted by bin
-    const int2* ug = P.u_all + (int64_t)s * P.kk + P.k;
-    for (int b = tid; b < p; b += blockDim.x) cnt[b] = 0;
+  if (STAGE) {
+    // ---- 1. select (ascending b) ----
+    nc = select_candidates([&](int b) { return F[b]; }, p, kstar, P.floor_rel * (double)p, cand, mag, flag, scratch);
+    // ---- 2. collision test + decode, flat over (candidate, shifted line) pairs (4 in flight per thread);
+    //      a failing pair clears its candidate's flag (benign race: all writers store 0) ----
+    for (int ci = tid; ci < nc; ci += blockDim.x) flag[ci] = 1;
     __syncthreads();
-    for (int e = tid; e < nR; e += blockDim.x) atomicAdd(&cnt[ug[e].x], 1);
-    __syncthreads();
-    {
-      const int per = (p + blockDim.x - 1) / blockDim.x;
-      const int b0 = tid * per, b1 = min(p, b0 + per);
-      int c0 = 0;
-      for (int b = b0; b < b1; ++b) c0 += cnt[b];
-      int tot;
-      int run = block_excl_scan(c0, scratch, &tot);
-      for (int b = b0; b < b1; ++b) { pos[b] = run; run += cnt[b]; }
-      __syncthreads();
-    }
-    if (warp == 0) {                                   // stable placement, 32 entries at a time
-      for (int e0 = 0; e0 < nR; e0 += 32) {
-        const int e = e0 + lane;
-        const int b = e < nR ? ug[e].x : -1 - lane;
-        const unsigned peers = __match_any_sync(0xffffffffu, b);
-        const int rank = __popc(peers & ((1u << lane) - 1u));
-        int base = 0;
-        if (e < nR) base = pos[b];
-        __syncwarp();
-        if (e < nR) {
-          order[base + rank] = e;
-          if (rank == __popc(peers) - 1) pos[b] = base + rank + 1;
-        }
-        __syncwarp();
-      }
-    }
-    __syncthreads();
-    const double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
-    const double pd = (double)p;
-    // one warp per (bin, 32-line chunk): lanes along the lines -> coalesced reads of the C rows
-    const int nchunk = (P.L + 31) >> 5;
-    for (int task = warp; task < p * nchunk; task += nwarps) {
-      const int b = task / nchunk, n = (task - b * nchunk) * 32 + lane;
-      const int c = cnt[b];
-      if (!c) continue;
-      const int end = pos[b];
-      double2 acc = make_double2(0.0, 0.0);
-      if (n < P.L) {
-        int q = end - c;
-        for (; q + 4 <= end; q += 4) {
-          double2 v[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) v[u] = Creg[(int64_t)order[q + u] * P.Lp + n];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) { acc.x += v[u].x; acc.y += v[u].y; }
-        }
-        for (; q < end; ++q) {
-          const double2 v = Creg[(int64_t)order[q] * P.Lp + n];
-          acc.x += v.x;
-          acc.y += v.y;
-        }
-        double2* Fn = Fw + (int64_t)n * P.p_stride;
-        const double2 f = Fn[b];
-        Fn[b] = make_double2(f.x + pd * acc.x, f.y + pd * acc.y);
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---- 1. select (ascending b): coalesced sweep, ballot + block prefix per 1024-bin round ----
-  for (int b0 = 0; b0 < p; b0 += blockDim.x) {
-    const int b = b0 + tid;
-    double mg = 0.0;
-    bool fl = false;
-    if (b < p) {
-      const double2 f = F[b];
-      mg = hypot(f.x, f.y);
-      fl = mg >= floor_abs;
-    }
-    int round_total;
-    const int pos = block_excl_scan(fl ? 1 : 0, scratch, &round_total);
-    if (fl) { cand[total + pos] = b; mag[total + pos] = mg; }
-    total += round_total;
-  }
-  __syncthreads();
-  nc = total;
-  if (nc > kstar) {
-    // keep the k* largest |F_0| (ties -> smaller b), preserve ascending order
-    for (int i = tid; i < nc; i += blockDim.x) {
-      const double mi = mag[i];
-      const int bi = cand[i];
-      int rank = 0;
-      for (int j = 0; j < nc; ++j) rank += (mag[j] > mi) || (mag[j] == mi && cand[j] < bi);
-      flag[i] = rank < kstar;
-    }
-    __syncthreads();
-    const int per = (nc + blockDim.x - 1) / blockDim.x;
-    const int i0 = tid * per, i1 = min(nc, i0 + per);
-    int c2 = 0;
-    int keep_b[32];
-    int nk = 0;
-    for (int i = i0; i < i1; ++i) c2 += flag[i];
-    int pos2 = block_excl_scan(c2, scratch, &total);
-    // stash own survivors in registers (per <= 7 since p <= 7168 and blockDim = 1024)
-    for (int i = i0; i < i1 && nk < 32; ++i)
-      if (flag[i]) keep_b[nk++] = cand[i];
-    __syncthreads();
-    for (int t = 0; t < nk; ++t) cand[pos2 + t] = keep_b[t];
-    __syncthreads();
-    nc = total;
-  }
-
-  // ---- 2. collision test + decode, flat over (candidate, shifted line) pairs ----
-  // Every pair is independent: thread t takes pairs t, t + blockDim, ... (4 in flight for latency hiding);
-  // a pair failing Eq. (42) or the rounding / range checks clears its candidate's flag (benign race: all
-  // writers store 0).  The decisions are those of a per-candidate loop: ok = AND over n of the same
-  // per-line tests.
-  const double twopi = 6.283185307179586476925286766559;
-  for (int ci = tid; ci < nc; ci += blockDim.x) flag[ci] = 1;
-  __syncthreads();
-  {
-    const int nl = P.L - 1;                               // local shifted lines (= r unsharded)
-    int64_t* sendv = MODE == kDecLocal ? P.rec_send + (int64_t)s * P.rec_words + P.rec_fw : nullptr;
-    const int tot = nc * nl;
+    const int tot = nc * r;
     for (int t0 = tid; t0 < tot; t0 += 4 * blockDim.x) {
       double2 fv[4], f0[4];
       int ci[4], n[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int t = t0 + u * blockDim.x;
-        ci[u] = t < tot ? t / nl : 0;
-        n[u] = t < tot ? t - ci[u] * nl : -1;
+        ci[u] = t < tot ? t / r : 0;
+        n[u] = t < tot ? t - ci[u] * r : -1;
         const int b = cand[ci[u]];
         f0[u] = F[b];
         fv[u] = n[u] >= 0 ? F[(int64_t)(1 + n[u]) * P.p_stride + b] : make_double2(0.0, 0.0);
@@ -283,38 +134,16 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (n[u] < 0) continue;
-        const double mag0 = hypot(f0[u].x, f0[u].y);
-        const double rho = hypot(fv[u].x, fv[u].y) / mag0;      // Eq. (42)
-        bool good = fabs(rho - 1.0) < P.tol;
-        if (good) {
-          // q = F_n conj(F_0), written without contraction to mirror the plain formula
-          const double qr = __dadd_rn(__dmul_rn(fv[u].x, f0[u].x), __dmul_rn(fv[u].y, f0[u].y));
-          const double qi = __dsub_rn(__dmul_rn(fv[u].y, f0[u].x), __dmul_rn(fv[u].x, f0[u].y));
-          const double x = __ddiv_rn(__dmul_rn(atan2(qi, qr), (double)Ev), twopi);    // Eq. (41)
-          const double xr = rint(x);
-          good = fabs(x - xr) <= P.round_tol;
-          const int64_t v = (int64_t)xr;
-          const int ng = P.line_lo + n[u];                 // reduced axis of the line
-          if (P.extra & 1) good = good && v >= lo_v[ng] && v <= hi_v[ng];
-          if (MODE == kDecLocal) sendv[(int64_t)n[u] * P.k + ci[u]] = v;
-          else accv[(int64_t)ng * P.k + ci[u]] = v;
-        }
-        if (!good) flag[ci[u]] = 0;
+        int64_t v = 0;
+        if (test_decode(f0[u], fv[u], P.tol, Ev, P.round_tol, P.extra & 1, lo_v[n[u]], hi_v[n[u]], &v))
+          accv[(int64_t)n[u] * P.k + ci[u]] = v;
+        else
+          flag[ci[u]] = 0;
       }
     }
-  }
-  __syncthreads();
-  if (MODE == kDecLocal) {
-    int32_t* sendf = reinterpret_cast<int32_t*>(P.rec_send + (int64_t)s * P.rec_words);
-    for (int ci = tid; ci < nc; ci += blockDim.x) {
-      sendf[ci] = flag[ci];
-      P.rec_cand[(int64_t)s * P.k + ci] = cand[ci];
-    }
-    if (tid == 0) P.rec_nc[s] = nc;
-    return;
-  }
+    __syncthreads();
   } else {
-    // ---- commit: candidates of the local phase, flags ANDed over the shards, coordinates unpacked ----
+    // ---- commit: candidates of line 0, flags ANDed over the line shards, coordinates unpacked ----
     nc = P.rec_nc[s];
     for (int ci = tid; ci < nc; ci += blockDim.x) {
       cand[ci] = P.rec_cand[(int64_t)s * P.k + ci];
@@ -642,13 +471,12 @@ cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freq
   return cudaGetLastError();
 }
 
-cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st, int mode) {
+cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st) {
   const size_t smem = decode_smem_bytes(P, max_p);
-  auto kern = mode == kDecLocal ? decode_kernel<false, kDecLocal>
-            : mode == kDecCommit ? decode_kernel<false, kDecCommit> : decode_kernel<false, kDecFull>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(decode_kernel<kDecCommit>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (n_active > 0) kern<<<n_active, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
+  if (n_active > 0)
+    decode_kernel<kDecCommit><<<n_active, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -656,10 +484,10 @@ cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_
                                 double* acc_a, int32_t* counts, cudaStream_t st) {
   const int max_p = (int)P.p_stride;
   const size_t smem = decode_smem_bytes(P, max_p);
-  cudaError_t e = cudaFuncSetAttribute(decode_kernel<true, kDecFull>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(decode_kernel<kDecStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  decode_kernel<true, kDecFull><<<1, kDecodeThreads, smem, st>>>(P, 0, kstar, acc_b, acc_v,
-                                                        reinterpret_cast<double2*>(acc_a), counts);
+  decode_kernel<kDecStage><<<1, kDecodeThreads, smem, st>>>(P, 0, kstar, acc_b, acc_v,
+                                                            reinterpret_cast<double2*>(acc_a), counts);
   return cudaGetLastError();
 }
 

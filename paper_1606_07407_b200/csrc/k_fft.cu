@@ -13,6 +13,7 @@
 // the in-place decimation-in-time inverse returns natural order: no permutation pass.
 // Twiddles e^{-2 pi i q/M} = T_hi[q >> 7] * T_lo[q & 127], two small tables in shared memory.
 #include "fft_consts.cuh"
+#include "decode_common.cuh"
 #include "sfft_internal.cuh"
 
 namespace sfft {
@@ -510,6 +511,46 @@ __global__ void terms_kernel(DevParams P) {
   }
   // the FP64 exp-sum stages the phases in 16-byte pairs: the partner of the last term must be a valid index
   if (threadIdx.x == 0 && (K & 1)) ug[K] = make_int2(0, 0);
+  // registry entries grouped by their bin u_e (bin-domain residual, reading R21): counting sort, stable in e
+  const int nR = P.st_nR[s];
+  if (P.literal || nR == 0) return;
+  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end
+  __shared__ int scratch[32];
+  int32_t* bstart = P.bin_start + (int64_t)s * (P.p_stride + 1);
+  int32_t* border = P.bin_order + (int64_t)s * P.k;
+  const int2* ur = ug + P.k;
+  for (int b = threadIdx.x; b < p; b += blockDim.x) cnt[b] = 0;
+  __syncthreads();                                   // also orders this block's ug writes before the reads below
+  for (int e = threadIdx.x; e < nR; e += blockDim.x) atomicAdd(&cnt[ur[e].x], 1);
+  __syncthreads();
+  {
+    const int per = (p + blockDim.x - 1) / blockDim.x;
+    const int b0 = threadIdx.x * per, b1 = min(p, b0 + per);
+    int c0 = 0;
+    for (int b = b0; b < b1; ++b) c0 += cnt[b];
+    int tot;
+    int run = block_excl_scan(c0, scratch, &tot);
+    for (int b = b0; b < b1; ++b) { const int c = cnt[b]; bstart[b] = run; cnt[b] = run; run += c; }
+    if (threadIdx.x == 0) bstart[p] = nR;
+    __syncthreads();
+  }
+  if (threadIdx.x < 32) {                            // stable placement, 32 entries at a time
+    const int lane = threadIdx.x;
+    for (int e0 = 0; e0 < nR; e0 += 32) {
+      const int e = e0 + lane;
+      const int b = e < nR ? ur[e].x : -1 - lane;
+      const unsigned peers = __match_any_sync(0xffffffffu, b);
+      const int rank = __popc(peers & ((1u << lane) - 1u));
+      int base = 0;
+      if (e < nR) base = cnt[b];
+      __syncwarp();
+      if (e < nR) {
+        border[base + rank] = e;
+        if (rank == __popc(peers) - 1) cnt[b] = base + rank + 1;
+      }
+      __syncwarp();
+    }
+  }
 }
 
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
@@ -555,12 +596,117 @@ __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
 }
 
+// ---- fused decode epilogue: no HBM round trip of the lines n >= 1 ----
+// line-0 CTA: F_0[b] = chirp[b] conv[b] + registry bins (reading R21), written to the line (the commit reads
+// a = F_0[b] / p) and kept in shared memory; select (a5) the candidates, publish them with F_0 at the
+// candidates and pass flags = 1, then release sel_ready[s] = it_epoch
+__device__ void fused_select(const DevParams& P, int s, int p, double2* x, const double2* __restrict__ ch,
+                             double2* line) {
+  const int tid = threadIdx.x;
+  const int nR = P.st_nR[s];
+  const bool resid = !P.literal && nR > 0;
+  const double pd = (double)p;
+  const int32_t* bstart = P.bin_start + (int64_t)s * (P.p_stride + 1);
+  const int32_t* border = P.bin_order + (int64_t)s * P.k;
+  const double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+  for (int b0 = tid; b0 < p; b0 += 4 * blockDim.x) {
+    double2 c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = b0 + u * blockDim.x;
+      c[u] = b < p ? __ldg(ch + b) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = b0 + u * blockDim.x;
+      if (b < p) {
+        double2 f = cmulx(x[b], c[u]);
+        if (resid) f = add_bin_residual(f, bstart, border, Creg, P.Lp, 0, b, pd);
+        x[b] = f;
+        line[b] = f;
+      }
+    }
+  }
+  __syncthreads();
+  // x[p ..) is free after the transform: mag[p] double, cand[p], flag[p], scratch[32] (smem budget: radix_plan)
+  double* mag = reinterpret_cast<double*>(x + p);
+  int* cand = reinterpret_cast<int*>(mag + p);
+  int* flag = cand + p;
+  int* scratch = flag + p;
+  const int nc = select_candidates([&](int b) { return x[b]; }, p, P.k - nR, P.floor_rel * pd, cand, mag, flag,
+                                   scratch);
+  int32_t* sendf = reinterpret_cast<int32_t*>(P.rec_send + (int64_t)s * P.rec_words);
+  for (int ci = tid; ci < nc; ci += blockDim.x) {
+    const int b = cand[ci];
+    P.rec_cand[(int64_t)s * P.k + ci] = b;
+    P.rec_f0[(int64_t)s * P.k + ci] = x[b];
+    sendf[ci] = 1;
+  }
+  if (tid == 0) P.rec_nc[s] = nc;
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.sel_ready + s), "r"(P.it_epoch) : "memory");
+  }
+}
+
+// line-n CTA (n >= 1 local line): after the line-0 CTA of the signal published, test + decode (a6) every
+// candidate on this line: F_n[b] = chirp[b] conv[b] + registry bins, Eq. (42) ratio and Eq. (41) decode;
+// a pass writes v into the record, a failure clears the candidate's flag (benign race: all writers store 0)
+__device__ void fused_test(const DevParams& P, int s, int p, int n, const double2* x, const double2* __restrict__ ch) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    int v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(P.sel_ready + s) : "memory");
+      if (v == P.it_epoch) break;
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  const int nR = P.st_nR[s];
+  const bool resid = !P.literal && nR > 0;
+  const double pd = (double)p;
+  const int32_t* bstart = P.bin_start + (int64_t)s * (P.p_stride + 1);
+  const int32_t* border = P.bin_order + (int64_t)s * P.k;
+  const double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+  const int lvl = P.st_lvl[s];
+  const int64_t Ev = P.lvl_E[lvl];
+  const int ng = P.line_lo + n - 1;                       // reduced axis of the line
+  const int64_t lo = P.lvl_lo[(int64_t)lvl * P.r + ng], hi = P.lvl_hi[(int64_t)lvl * P.r + ng];
+  const int nc = *(volatile const int32_t*)(P.rec_nc + s);
+  const int32_t* cand = P.rec_cand + (int64_t)s * P.k;
+  const double2* f0s = P.rec_f0 + (int64_t)s * P.k;
+  int32_t* sendf = reinterpret_cast<int32_t*>(P.rec_send + (int64_t)s * P.rec_words);
+  int64_t* sendv = P.rec_send + (int64_t)s * P.rec_words + P.rec_fw + (int64_t)(n - 1) * P.k;
+  for (int ci = tid; ci < nc; ci += blockDim.x) {
+    const int b = cand[ci];
+    double2 f = cmulx(x[b], __ldg(ch + b));
+    if (resid) f = add_bin_residual(f, bstart, border, Creg, P.Lp, n, b, pd);
+    int64_t v = 0;
+    if (test_decode(f0s[ci], f, P.tol, Ev, P.round_tol, P.extra & 1, lo, hi, &v)) sendv[ci] = v;
+    else sendf[ci] = 0;
+  }
+}
+
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
 template <bool BIG>
 __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4)
 pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int slot = blockIdx.x / n_lines, n = blockIdx.x % n_lines;
+  // fused decode: CTAs [0, n_signals) are the line-0 CTAs (they select and publish the candidates), the
+  // rest line n >= 1 of each signal; they wait for their signal's line-0 CTA, which has a lower block index
+  // (already resident or finished when a later block starts: the forward-progress argument of decoupled
+  // look-back scans)
+  int slot, n;
+  if (P.fuse_decode) {
+    const int na = (int)gridDim.x / n_lines;
+    if ((int)blockIdx.x < na) { slot = blockIdx.x; n = 0; }
+    else { const int t = blockIdx.x - na; slot = t / (n_lines - 1); n = 1 + t % (n_lines - 1); }
+  } else {
+    slot = blockIdx.x / n_lines;
+    n = blockIdx.x % n_lines;
+  }
   const int s = P.active[slot];
   const int p = P.st_p[s];
   const int fi = P.st_M[s];
@@ -639,6 +785,11 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   fft_dif<BIG>(P, x, fi, tb, 1);
   fft_mid<BIG>(P, x, fi, P.V + (int64_t)tslot * P.M_stride);
   fft_dit<BIG>(P, x, fi, tb, 1);
+  if (P.fuse_decode) {
+    if (n == 0) fused_select(P, s, p, x, ch, line);
+    else fused_test(P, s, p, n, x, ch);
+    return;
+  }
   // F[b] = w[b] * (conv)[b]: 4 chirp loads in flight per thread (the chirp is L2-resident, latency-bound)
   for (int b0 = threadIdx.x; b0 < p; b0 += 4 * blockDim.x) {
     double2 c[4];
@@ -669,7 +820,7 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   kern<<<n_signals, threads, smem, st>>>(P, direct ? 1 : 0);
-  terms_kernel<<<n_signals, 256, 0, st>>>(P);
+  terms_kernel<<<n_signals, 256, sizeof(int) * (size_t)P.p_stride, st>>>(P);
   return cudaGetLastError();
 }
 

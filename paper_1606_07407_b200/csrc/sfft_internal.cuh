@@ -126,6 +126,14 @@ struct DevParams {
   const int64_t* rec_recv;     // [line_G][batch][rec_words] all shards' records (all-gather result)
   int32_t* rec_cand;           // [batch][k] candidate bins of the local phase (identical on every shard)
   int32_t* rec_nc;             // [batch] candidate count
+  double2* rec_f0;             // [batch][k] F_0 at the candidates (residual included)
+  // fused FFT epilogue: line-0 CTAs select the candidates and publish them
+  // (sel_ready[s] = it_epoch, release); line-n CTAs wait for it (acquire), then test + decode their line
+  int32_t fuse_decode;         // launch flag of pfft_kernel (0: write the lines, stage entry point)
+  int32_t it_epoch;            // iteration stamp (plan-wide counter, never repeats within a plan)
+  int32_t* sel_ready;          // [batch]
+  int32_t* bin_start;          // [batch][p_stride + 1] registry entries of bin b: bin_order[bin_start[b] .. [b+1])
+  int32_t* bin_order;          // [batch][k] registry entry indices grouped by bin, ascending e within a bin
 };
 
 // reduced axes [lo, hi) of line shard g of G over r axes (contiguous, sizes differ by at most one; shard 0 largest)
@@ -176,9 +184,8 @@ cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* fre
 cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, cudaStream_t st);
 // k_decode.cu
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st);
-// mode 0: whole decode; 1: local phase of a line shard (records); 2: commit after the record all-gather
-cudaError_t launch_decode(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st,
-                          int mode = 0);
+// commit of an iteration: the records of the fused FFT epilogue (all line shards) -> registry update, state
+cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st);
 // re-projection of the signals that switched fallback level (reading R23); freqs = the execute's input
 cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freqs, cudaStream_t st);
 cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,
