@@ -147,6 +147,27 @@ FftSize radix_plan(int M) {
   std::vector<int> rs;
   for (int x = M; x > 1; x /= choice[x]) rs.push_back(choice[x]);
   std::sort(rs.begin(), rs.end(), [](int a, int b) { return a > b; });
+  // SFFT_FFT_PLAN="M:r1,r2,...;..." overrides the radices of size M (tuning experiments; order as given)
+  if (const char* env = getenv("SFFT_FFT_PLAN")) {
+    const std::string spec(env), key = std::to_string(M) + ":";
+    size_t at = 0;
+    while ((at = spec.find(key, at)) != std::string::npos && at > 0 && spec[at - 1] != ';') at += key.size();
+    if (at != std::string::npos) {
+      std::vector<int> ov;
+      int prod = 1;
+      bool ok = true;
+      size_t i = at + key.size();
+      while (i < spec.size() && spec[i] != ';') {
+        const int R = atoi(spec.c_str() + i);
+        ok = ok && R >= 2 && R <= rmax && std::find(std::begin(kRad), std::end(kRad), R) != std::end(kRad);
+        ov.push_back(R);
+        prod *= R;
+        while (i < spec.size() && spec[i] != ',' && spec[i] != ';') ++i;
+        if (i < spec.size() && spec[i] == ',') ++i;
+      }
+      if (ok && prod == M) rs = ov;
+    }
+  }
   for (int R : rs) s.radix.push_back((int8_t)R);
   size_t sumq = 0;
   int S = M;
@@ -1243,6 +1264,12 @@ int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int64_t* v_o
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }
+
+#ifdef SFFT_FFT_PROF
+SFFT_API int sfft_debug_fft_prof(unsigned long long* out, int reset) {
+  return sfft::fft_prof_read(out, reset != 0) == cudaSuccess ? SFFT_OK : SFFT_ECUDA;
+}
+#endif
 
 int sfft_line_shard_range(int32_t r, int32_t G, int32_t g, int32_t* lo, int32_t* hi) {
   if (!lo || !hi || r < 1 || G < 1 || G > r || g < 0 || g >= G) return SFFT_EINVAL;

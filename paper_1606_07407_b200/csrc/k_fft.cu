@@ -132,8 +132,22 @@ __device__ __forceinline__ void dft_small(double2 (&x)[R]) {
       for (int k1 = 0; k1 < A; ++k1) {
         const int q = (n2 * k1) % R;
         double2 t = u[k1];
-        if (q != 0) {
-          const double c = C[q], s = INV ? S[q] : -S[q];      // e^{-+ 2 pi i q / R}
+        // e^{-+ 2 pi i q / R}; quarter and half turns and odd eighths are done without full products
+        if (q == 0) {
+        } else if (2 * q == R) {
+          t = make_double2(-t.x, -t.y);
+        } else if (4 * q == R) {
+          t = mul_mi<INV>(t);
+        } else if (4 * q == 3 * R) {
+          t = mul_mi<!INV>(t);
+        } else if (8 * q == R || 8 * q == 3 * R || 8 * q == 5 * R || 8 * q == 7 * R) {
+          const double h = 0.70710678118654752440;                // (c, s) = (+-h, +-h)
+          const double c = (8 * q == R || 8 * q == 7 * R) ? h : -h;
+          const double sn = (8 * q < 4 * R) ? -h : h;             // forward sine sign: -sin(2 pi q / R)
+          const double s = INV ? -sn : sn;
+          t = c == s ? make_double2(c * (t.x - t.y), c * (t.x + t.y)) : make_double2(c * (t.x + t.y), c * (t.y - t.x));
+        } else {
+          const double c = C[q], s = INV ? S[q] : -S[q];
           t = make_double2(t.x * c - t.y * s, t.x * s + t.y * c);
         }
         x[B * k1 + n2] = t;
@@ -165,24 +179,32 @@ __device__ __forceinline__ void bfly_load(const double2* x, int base, int Q, dou
   for (int n = 0; n < R; ++n) v[n] = x[base + Q * n];
 }
 
+// w[k] = b^k for 1 <= k < R by a product tree: w[2^j] = w[2^(j-1)]^2, w[2^j + i] = w[2^j] w[i] -- the same
+// R - 2 products as a running power, dependency depth ceil(log2 R) instead of R - 2 (and error ~log2 k ulp)
+template <int R>
+__device__ __forceinline__ void twiddle_powers(double2 b, double2 (&w)[R]) {
+  w[0] = make_double2(1.0, 0.0);
+  if constexpr (R > 1) w[1] = b;
+#pragma unroll
+  for (int k = 2; k < R; ++k) {
+    int hi = 1;
+    while (2 * hi <= k) hi *= 2;
+    w[k] = hi == k ? cmulx(w[k / 2], w[k / 2]) : cmulx(w[hi], w[k - hi]);
+  }
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void bfly_finish(double2* x, int base, int Q, double2 b, double2 (&v)[R]) {
+  double2 w[R];
+  twiddle_powers<R>(b, w);
   if (!INV) {
     dft_small<R, false>(v);
     x[base] = v[0];
-    double2 w = b;
 #pragma unroll
-    for (int k = 1; k < R; ++k) {
-      x[base + Q * k] = cmulx(v[k], w);
-      if (k + 1 < R) w = cmulx(w, b);
-    }
+    for (int k = 1; k < R; ++k) x[base + Q * k] = cmulx(v[k], w[k]);
   } else {
-    double2 w = b;
 #pragma unroll
-    for (int k = 1; k < R; ++k) {
-      v[k] = cmulconj(v[k], w);
-      if (k + 1 < R) w = cmulx(w, b);
-    }
+    for (int k = 1; k < R; ++k) v[k] = cmulconj(v[k], w[k]);
     dft_small<R, true>(v);
 #pragma unroll
     for (int n = 0; n < R; ++n) x[base + Q * n] = v[n];
@@ -239,22 +261,35 @@ __device__ void load_twiddles(const DevParams& P, int fi, double2* tb) {
 // Fused middle of the Bluestein convolution: the last DIF pass (S = R, Q = 1: contiguous groups of
 // R, unit twiddles), the pointwise product with the kernel spectrum V and the first DIT pass (the
 // same groups) in registers -- three shared-memory sweeps replaced by one.
-template <int R>
+template <int R, bool BIG>
 __device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __restrict__ V) {
-  for (int g = threadIdx.x; g < M / R; g += blockDim.x) {
-    const int base = g * R;
-    double2 v[R], w[R];
+  // U groups per trip with all their loads (shared x, global V -- L2-resident) issued first: the V loads are
+  // latency-bound
+  constexpr int U = 1;
+  const int G = M / R;
+  for (int g0 = threadIdx.x; g0 < G; g0 += U * blockDim.x) {
+    double2 v[U][R], w[U][R];
 #pragma unroll
-    for (int k = 0; k < R; ++k) {
-      v[k] = x[base + k];
-      w[k] = __ldg(V + base + k);
+    for (int u = 0; u < U; ++u) {
+      const int g = g0 + u * blockDim.x;
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        v[u][k] = g < G ? x[g * R + k] : make_double2(0.0, 0.0);
+        w[u][k] = g < G ? __ldg(V + g * R + k) : make_double2(0.0, 0.0);
+      }
     }
-    dft_small<R, false>(v);
 #pragma unroll
-    for (int k = 0; k < R; ++k) v[k] = cmulx(v[k], w[k]);
-    dft_small<R, true>(v);
+    for (int u = 0; u < U; ++u) {
+      const int g = g0 + u * blockDim.x;
+      dft_small<R, false>(v[u]);
 #pragma unroll
-    for (int k = 0; k < R; ++k) x[base + k] = v[k];
+      for (int k = 0; k < R; ++k) v[u][k] = cmulx(v[u][k], w[u][k]);
+      dft_small<R, true>(v[u]);
+      if (g < G) {
+#pragma unroll
+        for (int k = 0; k < R; ++k) x[g * R + k] = v[u][k];
+      }
+    }
   }
 }
 
@@ -263,22 +298,22 @@ __device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* _
   const int M = P.fft_M[fi];
   const int R = P.fft_radix[fi * kMaxFftPasses + P.fft_npass[fi] - 1];
   switch (R) {
-    case 2: mid_loop<2>(x, M, V); break;
-    case 3: mid_loop<3>(x, M, V); break;
-    case 4: mid_loop<4>(x, M, V); break;
-    case 5: mid_loop<5>(x, M, V); break;
-    case 6: mid_loop<6>(x, M, V); break;
-    case 7: mid_loop<7>(x, M, V); break;
-    case 8: mid_loop<8>(x, M, V); break;
+    case 2: mid_loop<2, BIG>(x, M, V); break;
+    case 3: mid_loop<3, BIG>(x, M, V); break;
+    case 4: mid_loop<4, BIG>(x, M, V); break;
+    case 5: mid_loop<5, BIG>(x, M, V); break;
+    case 6: mid_loop<6, BIG>(x, M, V); break;
+    case 7: mid_loop<7, BIG>(x, M, V); break;
+    case 8: mid_loop<8, BIG>(x, M, V); break;
   }
   if constexpr (BIG) {
     switch (R) {
-      case 9: mid_loop<9>(x, M, V); break;
-      case 10: mid_loop<10>(x, M, V); break;
-      case 12: mid_loop<12>(x, M, V); break;
-      case 14: mid_loop<14>(x, M, V); break;
-      case 15: mid_loop<15>(x, M, V); break;
-      case 16: mid_loop<16>(x, M, V); break;
+      case 9: mid_loop<9, BIG>(x, M, V); break;
+      case 10: mid_loop<10, BIG>(x, M, V); break;
+      case 12: mid_loop<12, BIG>(x, M, V); break;
+      case 14: mid_loop<14, BIG>(x, M, V); break;
+      case 15: mid_loop<15, BIG>(x, M, V); break;
+      case 16: mid_loop<16, BIG>(x, M, V); break;
     }
   }
   __syncthreads();
@@ -689,11 +724,30 @@ __device__ void fused_test(const DevParams& P, int s, int p, int n, const double
   }
 }
 
+#ifdef SFFT_FFT_PROF
+// tuning builds only: cycles per phase summed over the CTAs of pfft_kernel (thread 0's clock)
+__device__ unsigned long long g_fft_prof[8];
+#define FFT_PROF_MARK(i)                                                     \
+  do {                                                                       \
+    __syncthreads();                                                         \
+    if (threadIdx.x == 0) {                                                  \
+      const long long t_ = clock64();                                        \
+      atomicAdd(&g_fft_prof[i], (unsigned long long)(t_ - prof_t0));         \
+      prof_t0 = t_;                                                          \
+    }                                                                        \
+  } while (0)
+#else
+#define FFT_PROF_MARK(i) do {} while (0)
+#endif
+
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
 template <bool BIG>
 __global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4)
 pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+#ifdef SFFT_FFT_PROF
+  long long prof_t0 = clock64();
+#endif
   // fused decode: CTAs [0, n_signals) are the line-0 CTAs (they select and publish the candidates), the
   // rest line n >= 1 of each signal; they wait for their signal's line-0 CTA, which has a lower block index
   // (already resident or finished when a later block starts: the forward-progress argument of decoupled
@@ -718,36 +772,35 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   const double2* ch = P.chirp + (int64_t)tslot * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
   if (P.lines_log) {
-    // the int8 exp-sum wrote the samples in discrete-log order: position f holds h = pw[f]
+    // the int8 exp-sum wrote the samples in discrete-log order: position f holds h = pw[f]; all of a
+    // thread's loads in flight (latency-bound phase), then the chirp products scattered
     const int32_t* pw = P.i8_pw + (int64_t)tslot * P.i8_tstride;
     const double2* chl = P.i8_chl + (int64_t)tslot * P.i8_tstride;
     const int n_slots = gridDim.x / n_lines;
-    for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
-    if (ksplit == 1) {
-      for (int f0 = threadIdx.x; f0 < p; f0 += 4 * blockDim.x) {   // coalesced loads, 4 in flight
-        double2 v[4], c[4];
-        int h[4];
+    for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);   // zero padding
+    constexpr int U = BIG ? 8 : 4;
+    for (int f0 = threadIdx.x; f0 < p; f0 += U * blockDim.x) {
+      double2 v[U], c[U];
+      int h[U];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int f = f0 + u * blockDim.x;
+      for (int u = 0; u < U; ++u) {
+        const int f = f0 + u * blockDim.x;
+        h[u] = f < p ? __ldg(pw + f) : -1;
+        c[u] = f < p ? __ldg(chl + f) : make_double2(0.0, 0.0);
+        if (ksplit == 1) {
           v[u] = f < p ? line[f] : make_double2(0.0, 0.0);
-          c[u] = f < p ? chl[f] : make_double2(0.0, 0.0);
-          h[u] = f < p ? pw[f] : -1;
+        } else {
+          v[u] = make_double2(0.0, 0.0);
+          for (int ks = 0; ks < ksplit && f < p; ++ks) {
+            const double2 t = part[(((int64_t)ks * n_slots + slot) * n_lines + n) * p_part + f];
+            v[u].x += t.x;
+            v[u].y += t.y;
+          }
         }
+      }
 #pragma unroll
-        for (int u = 0; u < 4; ++u)
-          if (h[u] >= 0) x[h[u]] = cmulx(v[u], c[u]);
-      }
-    } else {
-      for (int f = threadIdx.x; f < p; f += blockDim.x) {
-        double2 v = make_double2(0.0, 0.0);
-        for (int ks = 0; ks < ksplit; ++ks) {
-          const double2 t = part[(((int64_t)ks * n_slots + slot) * n_lines + n) * p_part + f];
-          v.x += t.x;
-          v.y += t.y;
-        }
-        x[pw[f]] = cmulx(v, chl[f]);
-      }
+      for (int u = 0; u < U; ++u)
+        if (h[u] >= 0) x[h[u]] = cmulx(v[u], c[u]);
     }
   } else if (ksplit == 1) {
     // 4 independent loads in flight per thread (latency-bound phase)
@@ -782,12 +835,17 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     }
   }
   __syncthreads();
+  FFT_PROF_MARK(0);
   fft_dif<BIG>(P, x, fi, tb, 1);
+  FFT_PROF_MARK(1);
   fft_mid<BIG>(P, x, fi, P.V + (int64_t)tslot * P.M_stride);
+  FFT_PROF_MARK(2);
   fft_dit<BIG>(P, x, fi, tb, 1);
+  FFT_PROF_MARK(3);
   if (P.fuse_decode) {
     if (n == 0) fused_select(P, s, p, x, ch, line);
     else fused_test(P, s, p, n, x, ch);
+    FFT_PROF_MARK(4);
     return;
   }
   // F[b] = w[b] * (conv)[b]: 4 chirp loads in flight per thread (the chirp is L2-resident, latency-bound)
@@ -804,7 +862,19 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
       if (b < p) line[b] = cmulx(x[b], c[u]);
     }
   }
+  FFT_PROF_MARK(4);
 }
+
+#ifdef SFFT_FFT_PROF
+cudaError_t fft_prof_read(unsigned long long* out, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_fft_prof, sizeof(unsigned long long) * 8);
+  if (e == cudaSuccess && reset) {
+    unsigned long long z[8] = {0};
+    e = cudaMemcpyToSymbol(g_fft_prof, z, sizeof z);
+  }
+  return e;
+}
+#endif
 
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
                             cudaStream_t st, int32_t epoch, bool direct) {

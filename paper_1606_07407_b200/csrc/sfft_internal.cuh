@@ -216,6 +216,9 @@ cudaError_t launch_i8_unpermute(const DevParams& P, int32_t p, double* out, cuda
 cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_p, int32_t n_signals, int32_t ksplit,
                              double2* part, int32_t p_part, int smem_optin, cudaStream_t st);
 // k_fft.cu
+#ifdef SFFT_FFT_PROF
+cudaError_t fft_prof_read(unsigned long long* out, bool reset);   // tuning builds only
+#endif
 // smem_bytes: 16 * max over the sizes in use of (M + sum of the per-pass base-twiddle counts)
 // per iteration: assign table slots to the active signals' primes (fills counted in ctrl[3]), compute the
 // tables of new primes (grid n_signals, CTAs beyond the fill count exit; direct = stage entry point: fill the
