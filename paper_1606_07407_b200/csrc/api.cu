@@ -134,7 +134,7 @@ FftSize radix_plan(int M) {
   // then descending order: the first (largest-Q) pass gets the largest radix -> fewest base twiddles
   // small sizes keep radices <= 8: with few butterflies per pass, wide radices idle most threads
   static const int kRad[] = {16, 15, 14, 12, 10, 9, 8, 7, 6, 5, 4, 3, 2};
-  const int rmax = M >= kFftBigM ? 16 : 8;
+  const int rmax = M >= fft_big_m() ? 16 : 8;
   FftSize s;
   s.M = M;
   std::vector<int> best(M + 1, 1 << 20), choice(M + 1, 0);
@@ -531,14 +531,14 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
       if (t < best - 1e-9) { best = t; it->ksplit = ks; }
     }
   }
-  it->big = it->max_M >= kFftBigM;
+  it->big = it->max_M >= fft_big_m();
   return SFFT_OK;
 }
 
 int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& launches,
                const std::function<int()>& mark) {
   cudaStream_t st = P->stream;
-  LAUNCH(P, launch_fft_prep(D, it.n_active, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M), it.big, st, ++P->epoch));
+  LAUNCH(P, launch_fft_prep(D, it.n_active, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto), it.big, st, ++P->epoch));
   launches += 2;   // tables_assign, terms
   mark();
   if (it.use_i8)
@@ -552,7 +552,7 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   D.lines_log = it.use_i8 ? 1 : 0;
   D.fuse_decode = 1;
   D.it_epoch = P->epoch;
-  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M), it.big, it.ksplit,
+  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto), it.big, it.ksplit,
                         ptr<double2>(P, B_PART), it.max_p, st));
   D.lines_log = 0;
   D.fuse_decode = 0;
@@ -1195,7 +1195,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   rc = set_signal0_state(P, D, (int)p, m, K - P->k);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M), P->fft[fi].M >= kFftBigM,
+  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M, P->fft[fi].smem_upto), P->fft[fi].M >= fft_big_m(),
                             P->stream, 0, true));
   if (P->i8_ok && i8_use_for(P, (int)p)) {
     D.i8_K = K;
@@ -1225,7 +1225,7 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   rc = set_signal0_state(P, D, (int)p, 0, 0);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M), big = P->fft[fi].M >= kFftBigM;
+  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M, P->fft[fi].smem_upto), big = P->fft[fi].M >= fft_big_m();
   LAUNCH(P, launch_fft_prep(D, 1, sm, th, big, P->stream, 0, true));
   LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, big, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));

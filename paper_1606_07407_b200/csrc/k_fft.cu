@@ -13,6 +13,9 @@
 // the in-place decimation-in-time inverse returns natural order: no permutation pass.
 // Twiddles e^{-2 pi i q/M} = T_hi[q >> 7] * T_lo[q & 127], two small tables in shared memory.
 #include "fft_consts.cuh"
+#include <algorithm>
+#include <cstdlib>
+
 #include "decode_common.cuh"
 #include "sfft_internal.cuh"
 
@@ -592,7 +595,7 @@ __global__ void terms_kernel(DevParams P) {
 // BIG: sizes >= 4096 whose plans use in-register radices up to 16 (512 threads, 128 registers);
 // small sizes use radices <= 8 with 64 registers so that several CTAs share an SM.
 template <bool BIG>
-__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4) fft_prep_kernel(DevParams P, int32_t direct) {
+__global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams P, int32_t direct) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int slot, p;
   if (direct) {
@@ -742,8 +745,9 @@ __device__ unsigned long long g_fft_prof[8];
 
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
 template <bool BIG>
-__global__ void __launch_bounds__(BIG ? 512 : 256, BIG ? 1 : 4)
-pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
+__global__ void __launch_bounds__(BIG ? 512 : 1024, 1)
+pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part,
+            int32_t ahead) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
 #ifdef SFFT_FFT_PROF
   long long prof_t0 = clock64();
@@ -760,6 +764,24 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   } else {
     slot = blockIdx.x / n_lines;
     n = blockIdx.x % n_lines;
+  }
+  // the block `ahead` positions later (it starts when a resident block retires) has its input line pulled into
+  // L2 now, so its load phase waits on L2 rather than HBM latency
+  if (threadIdx.x == 0 && ahead > 0 && ksplit == 1 && (int)blockIdx.x + ahead < (int)gridDim.x) {
+    const int b2 = blockIdx.x + ahead;
+    int slot2, n2;
+    if (P.fuse_decode) {
+      const int na = (int)gridDim.x / n_lines;
+      if (b2 < na) { slot2 = b2; n2 = 0; }
+      else { const int t = b2 - na; slot2 = t / (n_lines - 1); n2 = 1 + t % (n_lines - 1); }
+    } else {
+      slot2 = b2 / n_lines;
+      n2 = b2 % n_lines;
+    }
+    const int s2 = P.active[slot2];
+    const double2* src = P.lines + ((int64_t)s2 * n_lines + n2) * P.p_stride;
+    const uint32_t bytes = 16u * (uint32_t)P.st_p[s2];
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
   }
   const int s = P.active[slot];
   const int p = P.st_p[s];
@@ -901,7 +923,17 @@ cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, 
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;
-  if (grid > 0) kern<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part);
+  // resident blocks (the L2 prefetch distance)
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
+  const int ahead = getenv("SFFT_FFT_NOPREFETCH") ? 0 : n_sm * std::max(per_sm, 1);
+  if (grid > 0) kern<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part, ahead);
   return cudaGetLastError();
 }
 

@@ -4,6 +4,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <string>
 #include <vector>
@@ -229,9 +230,19 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
 #ifndef SFFT_FFT_BIGM
 #define SFFT_FFT_BIGM 8192
 #endif
-constexpr int kFftBigM = SFFT_FFT_BIGM;   // sizes >= this use radices up to 16 and the 512-thread variant (one CTA per SM); smaller sizes run two CTAs per SM
-inline int fft_threads(int M) {
-  const int cap = M >= kFftBigM ? 512 : 256;
+// sizes >= this use radices up to 16 and the 512-thread variant (128 registers, one CTA per SM); smaller sizes use
+// radices <= 8 with 64 registers (SFFT_FFT_BIGM overrides, tuning)
+inline int fft_big_m() {
+  static const int v = getenv("SFFT_FFT_BIGM") ? atoi(getenv("SFFT_FFT_BIGM")) : SFFT_FFT_BIGM;
+  return v;
+}
+// threads per FFT CTA: the 64-register variant fills the SM's 1024-thread register budget with as many CTAs as
+// shared memory allows (1024 / CTAs per SM threads each), but no more threads than ~M/6 butterflies need
+inline int fft_threads(int M, size_t smem) {
+  if (M >= fft_big_m()) return 512;
+  const size_t per_sm = 228 * 1024;
+  const int ctas = smem * 4 + 4096 <= per_sm ? 4 : smem * 2 + 2048 <= per_sm ? 2 : 1;
+  const int cap = getenv("SFFT_FFT_TCAP") ? atoi(getenv("SFFT_FFT_TCAP")) : 1024 / ctas;
   int t = ((M / 6 + 31) / 32) * 32;
   return t < 64 ? 64 : (t > cap ? cap : t);
 }
