@@ -12,6 +12,8 @@
 //                 (-a e^{2 pi i v_n / E}) written for the next iteration's residual; prune (R15)
 //   5. state    : |R|, stall counter (R16), samples (R18), status
 // decode_kernel<kDecStage> : teacher-forced stage entry point (select + test + decode of given lines).
+#include <algorithm>
+
 #include "decode_common.cuh"
 
 namespace sfft {
@@ -62,13 +64,20 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
   return z ^ (z >> 31);
 }
-
-__device__ __forceinline__ double2 line_factor_d(int64_t v, int64_t E) {
-  const int64_t q = mod_pos64(v, E);
-  double s, c;
-  sincospi(2.0 * (double)q / (double)E, &s, &c);
-  return make_double2(c, s);
+// registry key hash of the r-long coordinate vector: XOR over n of mix64(v_n ^ n * golden) -- order-free, so a
+// warp computes it with lanes along n (key_hash_warp) and a single thread with a plain loop (same value)
+__device__ __forceinline__ uint64_t key_term(int64_t v, int n) {
+  return mix64((uint64_t)v ^ ((uint64_t)(n + 1) * 0x9E3779B97F4A7C15ULL));
 }
+__device__ __forceinline__ uint64_t key_hash_warp(const int64_t* v, int64_t stride, int r, int lane) {
+  uint64_t h = 0;
+  for (int n = lane; n < r; n += 32) h ^= key_term(v[(int64_t)n * stride], n);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+  return h;
+}
+
+
 
 // ------------------------------------------------------------------ decode
 // dynamic smem: cand[p] int, flag[p] int, mag[p] double, accl[k] int, found[k] int, scratch[64] int
@@ -202,10 +211,37 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   uint64_t* khash = P.key_hash + (int64_t)s * P.k;
   int* htab = P.htab + (int64_t)s * P.H;
   const int Hm = P.H - 1;
-  for (int t = tid; t < na; t += blockDim.x) {
+  // 4a. lookup, warp per accepted candidate: key hash with lanes along the coordinates, linear probing,
+  //     full-key compare by ballot (the arrays of the select are free in the commit: mag -> hashes, flag -> new)
+  //     Short keys (r < 128) go thread per candidate instead (the same hash by a plain loop).
+  uint64_t* hsh = reinterpret_cast<uint64_t*>(mag);
+  const int nwarps = (int)(blockDim.x >> 5);
+  const bool wide = r >= 128;
+  if (!wide) {
+    for (int t = tid; t < na; t += blockDim.x) {
+      const int ci = accl[t];
+      uint64_t h = 0;
+      for (int n = 0; n < r; ++n) h ^= key_term(accv[(int64_t)n * P.k + ci], n);
+      int slot = (int)(h & (uint64_t)Hm);
+      int fe = -1;
+      for (;;) {
+        const int e1 = htab[slot];
+        if (e1 == 0) break;
+        const int e = e1 - 1;
+        if (khash[e] == h) {
+          bool eq = true;
+          for (int n = 0; n < r && eq; ++n) eq = vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+          if (eq) { fe = e; break; }
+        }
+        slot = (slot + 1) & Hm;
+      }
+      found[t] = fe;
+      hsh[t] = h;
+    }
+  }
+  for (int t = warp; wide && t < na; t += nwarps) {
     const int ci = accl[t];
-    uint64_t h = 0x9E3779B97F4A7C15ULL;
-    for (int n = 0; n < r; ++n) h = mix64(h ^ (uint64_t)accv[(int64_t)n * P.k + ci]);
+    const uint64_t h = key_hash_warp(accv + ci, P.k, r, lane);
     int slot = (int)(h & (uint64_t)Hm);
     int fe = -1;
     for (;;) {
@@ -214,14 +250,15 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
       const int e = e1 - 1;
       if (khash[e] == h) {
         bool eq = true;
-        for (int n = 0; n < r && eq; ++n) eq = vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
-        if (eq) { fe = e; break; }
+        for (int n = lane; n < r; n += 32) eq = eq && vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+        if (__all_sync(0xffffffffu, eq)) { fe = e; break; }
       }
       slot = (slot + 1) & Hm;
     }
-    found[t] = fe;
+    if (lane == 0) { found[t] = fe; hsh[t] = h; }
   }
   __syncthreads();
+  // 4b. R[v] += a for found keys; new keys get entries nR + rank in ascending-b order (deterministic)
   int n_new;
   {
     const int per = (na + blockDim.x - 1) / blockDim.x;
@@ -238,20 +275,35 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
       if (found[t] >= 0) {
         const int e = found[t];
         areg[e] = make_double2(areg[e].x + a.x, areg[e].y + a.y);
+        flag[t] = 0;
       } else {
         const int e = nR + rank++;
-        uint64_t h = 0x9E3779B97F4A7C15ULL;
-        for (int n = 0; n < r; ++n) {
-          const int64_t v = accv[(int64_t)n * P.k + ci];
-          vreg[(int64_t)n * P.kk + e] = v;
-          h = mix64(h ^ (uint64_t)v);
-        }
         areg[e] = a;
-        khash[e] = h;
-        int slot = (int)(h & (uint64_t)Hm);
-        while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+        khash[e] = hsh[t];
         found[t] = e;
+        flag[t] = 1;
       }
+    }
+  }
+  __syncthreads();
+  // 4c. new entries: key row and hash-table insert (warp per entry with lanes along the coordinates for long
+  //     keys, thread per entry otherwise)
+  if (!wide) {
+    for (int t = tid; t < na; t += blockDim.x) {
+      if (!flag[t]) continue;
+      const int ci = accl[t], e = found[t];
+      for (int n = 0; n < r; ++n) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
+      int slot = (int)(hsh[t] & (uint64_t)Hm);
+      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+    }
+  }
+  for (int t = warp; wide && t < na; t += nwarps) {
+    if (!flag[t]) continue;
+    const int ci = accl[t], e = found[t];
+    for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
+    if (lane == 0) {
+      int slot = (int)(hsh[t] & (uint64_t)Hm);
+      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
     }
   }
   __syncthreads();
@@ -259,17 +311,18 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
 
   // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}
   double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
-  for (int64_t w = tid; w < (int64_t)na * P.Lp; w += blockDim.x) {
-    const int t = (int)(w / P.Lp), n = (int)(w % P.Lp);
+  for (int t = warp; t < na; t += nwarps) {                        // warp per touched entry, lanes along the row
     const int e = found[t];
     const double2 a = areg[e];
-    double2 c;
-    if (n == 0) c = make_double2(-a.x, -a.y);
-    else if (n < P.L) {
-      const double2 lf = line_factor_d(vreg[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
-      c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
-    } else c = make_double2(0.0, 0.0);
-    Creg[(int64_t)e * P.Lp + n] = c;
+    for (int n = lane; n < P.Lp; n += 32) {
+      double2 c;
+      if (n == 0) c = make_double2(-a.x, -a.y);
+      else if (n < P.L) {
+        const double2 lf = line_factor_exact(vreg[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
+        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+      } else c = make_double2(0.0, 0.0);
+      Creg[(int64_t)e * P.Lp + n] = c;
+    }
   }
   // prune test (only touched entries can have changed)
   int small = 0;
@@ -383,7 +436,7 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
     __syncwarp();
     const double2 a = Cs[(int64_t)j * P.Lp];                       // column 0 = a_j
     for (int n = 1 + lane; n < P.L; n += 32) {
-      const double2 lf = line_factor_d(vs[(int64_t)(P.line_lo + n - 1) * kk + j], E);
+      const double2 lf = line_factor_exact(vs[(int64_t)(P.line_lo + n - 1) * kk + j], E);
       Cs[(int64_t)j * P.Lp + n] = make_double2(a.x * lf.x - a.y * lf.y, a.x * lf.y + a.y * lf.x);
     }
   }
@@ -427,11 +480,11 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
     int pos = block_excl_scan(c, scratch, &total);
     for (int e = e0; e < e1; ++e) {
       if (!keep[e]) continue;
-      uint64_t h = 0x9E3779B97F4A7C15ULL;
+      uint64_t h = 0;
       for (int n = 0; n < r; ++n) {
         const int64_t v = sv[(int64_t)n * P.k + e];
         vreg[(int64_t)n * kk + pos] = v;
-        h = mix64(h ^ (uint64_t)v);
+        h ^= key_term(v, n);
       }
       areg[pos] = sa[e];
       P.key_hash[(int64_t)s * P.k + pos] = h;
@@ -449,16 +502,17 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
     while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
   }
   double2* Creg = Cs + (int64_t)P.k * P.Lp;
-  for (int64_t w = tid; w < (int64_t)total * P.Lp; w += blockDim.x) {
-    const int e = (int)(w / P.Lp), n = (int)(w % P.Lp);
+  for (int e = warp; e < total; e += nwarps) {
     const double2 a = areg[e];
-    double2 c;
-    if (n == 0) c = make_double2(-a.x, -a.y);
-    else if (n < P.L) {
-      const double2 lf = line_factor_d(vreg[(int64_t)(P.line_lo + n - 1) * kk + e], E);
-      c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
-    } else c = make_double2(0.0, 0.0);
-    Creg[(int64_t)e * P.Lp + n] = c;
+    for (int n = lane; n < P.Lp; n += 32) {
+      double2 c;
+      if (n == 0) c = make_double2(-a.x, -a.y);
+      else if (n < P.L) {
+        const double2 lf = line_factor_exact(vreg[(int64_t)(P.line_lo + n - 1) * kk + e], E);
+        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+      } else c = make_double2(0.0, 0.0);
+      Creg[(int64_t)e * P.Lp + n] = c;
+    }
   }
   if (tid == 0) {
     P.st_nR[s] = total;
@@ -475,8 +529,11 @@ cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p
   const size_t smem = decode_smem_bytes(P, max_p);
   cudaError_t e = cudaFuncSetAttribute(decode_kernel<kDecCommit>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
+  // threads: ~8 (candidate, axis) records per thread (small problems: many short CTAs, e.g. C2's 1024 signals)
+  const long work = (long)P.k * (P.r + 1) / 8;
+  const int threads = (int)std::min<long>(kDecodeThreads, std::max<long>(128, (work + 31) / 32 * 32));
   if (n_active > 0)
-    decode_kernel<kDecCommit><<<n_active, kDecodeThreads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
+    decode_kernel<kDecCommit><<<n_active, threads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 

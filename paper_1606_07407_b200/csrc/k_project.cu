@@ -11,14 +11,6 @@
 
 namespace sfft {
 
-__device__ __forceinline__ double2 line_factor(int64_t v, int64_t E) {
-  // e^{2 pi i (v mod E)/E} via sincospi of the exactly reduced rational 2 (v mod E) / E
-  const int64_t q = mod_pos64(v, E);
-  double s, c;
-  sincospi(2.0 * (double)q / (double)E, &s, &c);
-  return make_double2(c, s);
-}
-
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
@@ -55,7 +47,7 @@ __global__ void project_kernel(DevParams P, int32_t batch, const int32_t* __rest
   for (int n = lane; n < P.Lp; n += 32) {
     double2 c;
     if (n == 0) c = a;
-    else if (n < P.L) c = cmul(a, line_factor(vs[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
+    else if (n < P.L) c = cmul(a, line_factor_exact(vs[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
     else c = make_double2(0.0, 0.0);
     Crow[n] = c;
   }
@@ -103,7 +95,7 @@ __global__ void line_coeffs_kernel(DevParams P, int32_t K, const double2* __rest
   for (int n = lane; n < P.Lp; n += 32) {
     double2 v;
     if (n == 0) v = a;
-    else if (n < P.L) v = cmul(a, line_factor(P.v_all[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
+    else if (n < P.L) v = cmul(a, line_factor_exact(P.v_all[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
     else v = make_double2(0.0, 0.0);
     Crow[n] = v;
   }

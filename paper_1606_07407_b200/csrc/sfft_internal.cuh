@@ -177,6 +177,19 @@ __host__ __device__ inline int64_t mod_pos64(int64_t x, int64_t m) {
   int64_t q = x % m;
   return q < 0 ? q + m : q;
 }
+// the same for the usual case |x| < m (decodable coordinates: the plan keeps every image inside (-E/2, E/2))
+// without a 64-bit division; falls back to mod_pos64 otherwise
+__host__ __device__ __forceinline__ int64_t mod_near64(int64_t x, int64_t m) {
+  const int64_t q = x < 0 ? x + m : x;
+  return (q >= 0 && q < m) ? q : mod_pos64(x, m);
+}
+// e^{2 pi i (v mod E)/E} via sincospi of the exactly reduced rational 2 (v mod E) / E (line factor of a shift)
+__device__ __forceinline__ double2 line_factor_exact(int64_t v, int64_t E) {
+  const int64_t q = mod_near64(v, E);
+  double s, c;
+  sincospi(2.0 * (double)q / (double)E, &s, &c);
+  return make_double2(c, s);
+}
 
 // ---- launchers (each .cu file) ----------------------------------------------------------
 // k_project.cu
