@@ -56,6 +56,9 @@ def parse():
                     help="signals: independent signal shards per rank (weak scaling, default); lines: every rank "
                          "solves the same signals and owns a shard of the shifted lines (strong scaling, NCCL "
                          "record all-gather per iteration, SURVEY 8(e))")
+    ap.add_argument("--table-cache", type=int, default=1024,
+                    help="per-prime table cache slots (plan option table_cache_slots; ~1 MB each): the steady state "
+                         "reuses the tables of every prime the workload visits")
     ap.add_argument("--expsum-path", type=int, default=0, choices=[0, 1, 2],
                     help="0 auto (int8 limbs on tcgen05 when available), 1 FP64 tensor/vector, 2 int8 limbs")
     return ap.parse_args()
@@ -186,7 +189,7 @@ def main():
     stream = torch.cuda.current_stream()
     plan = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, profile=True,
                         expsum_path=args.expsum_path, line_shards=world if lines else 0,
-                        line_rank=rank if lines else 0)
+                        line_rank=rank if lines else 0, table_cache_slots=args.table_cache)
     if lines:
         if world > 1:
             S.comm_init_line_shards(plan)
@@ -333,7 +336,7 @@ def main():
             "expsum_path": "int8 limbs on tcgen05" if n8 else "fp64",
             "config": {"workload": f"{cfg.name}: d={cfg.d} N={cfg.N} k={cfg.k} |a|~U[1,10], partition (2^50), "
                                    f"r={plan.r}, E=2^{int(np.log2(plan.E))}",
-                       "signals_per_gpu_per_step": T,
+                       "signals_per_gpu_per_step": T, "table_cache_slots": args.table_cache,
                        "parallelism": f"line shards x{world} (NCCL record all-gather)" if lines else f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
             "sample_evals_per_s": mult * samples / (ms_max / 1e3),

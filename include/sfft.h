@@ -80,6 +80,9 @@ typedef struct {
                                  its decode exchanges per-candidate records with the other shards every iteration
                                  (sfft_comm_init, or sfft_execute_group on one device).  1 <= G <= r. */
   int32_t line_rank;          /* shard index of this plan, 0 <= line_rank < line_shards [0] */
+  int32_t table_cache_slots;  /* per-prime table cache capacity (W_p roots, Bluestein chirp and kernel spectrum,
+                                 int8 root limbs: ~1 MB each, they depend on p only and are kept across iterations
+                                 and executes, least recently used evicted); 0 -> batch + 16, the minimum [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */

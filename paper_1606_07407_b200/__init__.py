@@ -45,7 +45,7 @@ class sfft_options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("profile", ctypes.c_int32),
                 ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32),
                 ("fallback_tilts", ctypes.c_int32), ("line_shards", ctypes.c_int32),
-                ("line_rank", ctypes.c_int32)]
+                ("line_rank", ctypes.c_int32), ("table_cache_slots", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -168,7 +168,8 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               bin_floor_rel: float = 1e-8, prune_floor: float = 1e-8, round_tol: float = 0.01,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
               stream=None, profile: bool = False, literal_residual: bool = False,
-              expsum_path: int = 0, fallback_tilts: int = 0, line_shards: int = 0, line_rank: int = 0) -> Plan:
+              expsum_path: int = 0, fallback_tilts: int = 0, line_shards: int = 0, line_rank: int = 0,
+              table_cache_slots: int = 0) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -187,6 +188,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.expsum_path = int(expsum_path)
     opt.fallback_tilts = int(fallback_tilts)
     opt.line_shards, opt.line_rank = int(line_shards), int(line_rank)
+    opt.table_cache_slots = int(table_cache_slots)
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)

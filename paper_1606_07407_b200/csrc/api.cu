@@ -26,6 +26,24 @@ struct sfft_signal_s {
   const double* coeffs;
 };
 
+namespace sfft {
+cudaError_t ensure_smem(const void* kern, size_t bytes) {
+  static std::vector<std::pair<std::pair<int, const void*>, size_t>> cache;   // (device, kernel) -> bytes set
+  int dev = 0;
+  cudaGetDevice(&dev);
+  for (auto& c : cache)
+    if (c.first.first == dev && c.first.second == kern) {
+      if (c.second >= bytes) return cudaSuccess;
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+      if (e == cudaSuccess) c.second = bytes;
+      return e;
+    }
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cache.push_back({{dev, kern}, bytes});
+  return e;
+}
+}  // namespace sfft
+
 namespace {
 
 struct FftSize {
@@ -89,6 +107,7 @@ struct sfft_plan_s {
   int32_t line_G = 0, line_g = 0, line_lo = 0, L_ref = 0;
   int32_t rec_words = 0, rec_fw = 0;
   void* nccl_comm = nullptr;   // ncclComm_t of sfft_comm_init (shard_mode 1)
+  cudaEvent_t ev_ctrl = nullptr;   // the per-iteration control read (iter_setup)
 };
 
 namespace {
@@ -391,6 +410,7 @@ int ensure_ready(sfft_plan_t* P) {
     P->tables_ready = false;
   }
   if (!P->h_ctrl) CUDA_TRY(P, cudaMallocHost(&P->h_ctrl, 64));
+  if (!P->ev_ctrl) CUDA_TRY(P, cudaEventCreateWithFlags(&P->ev_ctrl, cudaEventDisableTiming));
   if (!P->tables_ready) {
     std::vector<int32_t> fm, fn;
     std::vector<int8_t> fr(P->fft.size() * kMaxFftPasses, 0);
@@ -497,11 +517,20 @@ int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& lau
   return SFFT_OK;
 }
 
-int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launches) {
+int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launches, int n_bound) {
   cudaStream_t st = P->stream;
   LAUNCH(P, launch_setup(D, iter, st));
   CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(P, cudaStreamSynchronize(st));
+  CUDA_TRY(P, cudaEventRecord(P->ev_ctrl, st));
+  // the table prep needs no host decision: it is enqueued before the control read returns, sized for the
+  // previous iteration's active count and the largest FFT size (CTAs beyond the device-side counts exit), so
+  // the host round trip overlaps it
+  {
+    const FftSize& fb = P->fft.back();
+    LAUNCH(P, launch_fft_prep(D, n_bound, (int)fb.smem_upto, 512, 1, st, ++P->epoch));
+    launches += 2;   // tables_assign, terms
+  }
+  CUDA_TRY(P, cudaEventSynchronize(P->ev_ctrl));
   it->n_active = P->h_ctrl[0];
   it->max_p = P->h_ctrl[1];
   if (it->n_active == 0) return SFFT_OK;
@@ -538,8 +567,6 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
 int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& launches,
                const std::function<int()>& mark) {
   cudaStream_t st = P->stream;
-  LAUNCH(P, launch_fft_prep(D, it.n_active, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto), it.big, st, ++P->epoch));
-  launches += 2;   // tables_assign, terms
   mark();
   if (it.use_i8)
     LAUNCH(P, launch_expsum_i8(D, P->i8, it.max_p, it.n_active, it.ksplit, ptr<double2>(P, B_PART), it.max_p,
@@ -698,6 +725,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->expsum_path = opt->expsum_path;
     if (P->expsum_path < 0 || P->expsum_path > 2) return SFFT_EINVAL;
     if (opt->fallback_tilts < 0 || opt->fallback_tilts > 4) return SFFT_EINVAL;
+    if (opt->table_cache_slots < 0 || opt->table_cache_slots > (1 << 16)) return SFFT_EINVAL;
     if (opt->line_shards < 0 || (opt->line_shards > 0 && (opt->line_rank < 0 || opt->line_rank >= opt->line_shards)))
       return SFFT_EINVAL;
     P->line_G = opt->line_shards;
@@ -906,6 +934,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     return SFFT_ENOTSUP;
   if (8 * (size_t)k > (size_t)smem_optin) return SFFT_ENOTSUP;
   P->n_tslots = P->batch + 16;    // at most batch primes are live per iteration; the rest keeps recent primes
+  if (opt && opt->table_cache_slots > P->n_tslots) P->n_tslots = opt->table_cache_slots;
   layout(P.get());
   *out = P.release();
   return SFFT_OK;
@@ -941,6 +970,7 @@ void sfft_plan_destroy(sfft_plan_t* plan) {
   if (plan->nccl_comm && nccl_api().ok) nccl_api().comm_destroy(plan->nccl_comm);
   if (plan->ws_owned && plan->ws) cudaFree(plan->ws);
   if (plan->h_ctrl) cudaFreeHost(plan->h_ctrl);
+  if (plan->ev_ctrl) cudaEventDestroy(plan->ev_ctrl);
   for (cudaEvent_t e : plan->events) cudaEventDestroy(e);
   delete plan;
 }
@@ -989,9 +1019,11 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   int iter = 1;
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
   std::vector<size_t> it_marks, it_i8;
+  int n_bound = batch;
   for (; iter <= P->max_iter; ++iter) {
     IterPlan it;
-    if ((rc = iter_setup(P, D, iter, &it, launches))) return rc;
+    if ((rc = iter_setup(P, D, iter, &it, launches, n_bound))) return rc;
+    n_bound = it.n_active;
     if (it.n_active == 0) break;
     if (P->profile) it_marks.push_back(n_ev);
     mark();
@@ -1026,7 +1058,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
       cudaEventElapsedTime(&b, P->events[m0 + 1], P->events[m0 + 2]);
       cudaEventElapsedTime(&c, P->events[m0 + 2], P->events[m0 + 3]);
       cudaEventElapsedTime(&d, P->events[m0 + 3], P->events[m0 + 4]);
-      fprintf(stderr, "[sfft] iter %zu prep %.3f expsum %.3f pfft %.3f decode %.3f ms\n", it + 1, a, b, c, d);
+      float g = 0;       // from the previous mark (end of the last iteration / solve start) to this prep
+      cudaEventElapsedTime(&g, P->events[m0 - 1], P->events[m0]);
+      fprintf(stderr, "[sfft] iter %zu gap+setup %.3f prep %.3f expsum %.3f pfft %.3f decode %.3f ms\n", it + 1, g, a, b,
+              c, d);
     }
   }
   if (rep && P->profile && n_ev >= 2) {
@@ -1077,14 +1112,16 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
   }
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
   const size_t words = (size_t)batch * P0->rec_words;
+  int n_bound = batch;
   for (int iter = 1; iter <= P0->max_iter; ++iter) {
     std::vector<IterPlan> it(G);
     for (int g = 0; g < G; ++g) {
-      if ((rc = iter_setup(plans[g], D[g], iter, &it[g], launches))) return rc;
+      if ((rc = iter_setup(plans[g], D[g], iter, &it[g], launches, n_bound))) return rc;
       if (it[g].n_active != it[0].n_active || it[g].max_p != it[0].max_p)
         return fail(P0, SFFT_ECORRUPT, "line shards diverged at iteration %d", iter);
     }
     if (it[0].n_active == 0) break;
+    n_bound = it[0].n_active;
     for (int g = 0; g < G; ++g)
       if ((rc = iter_front(plans[g], D[g], iter, it[g], launches, nomark))) return rc;
     for (int g = 0; g < G; ++g)          // the all-gather: shard g's records into slot g of every shard

@@ -527,7 +527,7 @@ cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freq
 
 cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st) {
   const size_t smem = decode_smem_bytes(P, max_p);
-  cudaError_t e = cudaFuncSetAttribute(decode_kernel<kDecCommit>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(decode_kernel<kDecCommit>, smem);
   if (e != cudaSuccess) return e;
   // threads: ~8 (candidate, axis) records per thread (small problems: many short CTAs, e.g. C2's 1024 signals)
   const long work = (long)P.k * (P.r + 1) / 8;
@@ -541,7 +541,7 @@ cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_
                                 double* acc_a, int32_t* counts, cudaStream_t st) {
   const int max_p = (int)P.p_stride;
   const size_t smem = decode_smem_bytes(P, max_p);
-  cudaError_t e = cudaFuncSetAttribute(decode_kernel<kDecStage>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(decode_kernel<kDecStage>, smem);
   if (e != cudaSuccess) return e;
   decode_kernel<kDecStage><<<1, kDecodeThreads, smem, st>>>(P, 0, kstar, acc_b, acc_v,
                                                             reinterpret_cast<double2*>(acc_a), counts);

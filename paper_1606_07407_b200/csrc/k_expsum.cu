@@ -437,7 +437,7 @@ template <typename KernT, typename... Args>
 static cudaError_t launch_grid(KernT kern, const ExpsumShape& S, int32_t max_p, int32_t n_signals, const Split& sp,
                                cudaStream_t st, Args... args) {
   const size_t smem = expsum_smem(max_p, S.bn);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   if (sp.occ_out) return cudaOccupancyMaxActiveBlocksPerMultiprocessor(sp.occ_out, kern, S.warps * 32, smem);
   const int n_htiles = (max_p + S.bm - 1) / S.bm;

@@ -640,7 +640,7 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
                             : (A.prof ? expsum_i8_kernel<6, true, true> : expsum_i8_kernel<6, false, true>);
   else kern = c.S == 5 ? (A.prof ? expsum_i8_kernel<5, true, false> : expsum_i8_kernel<5, false, false>)
                        : (A.prof ? expsum_i8_kernel<6, true, false> : expsum_i8_kernel<6, false, false>);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   if (pair) {
     A.n_htiles = (max_p + 2 * kI8Rows - 1) / (2 * kI8Rows);            // 256-row tiles of the pair

@@ -530,7 +530,8 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
 }
 
 // ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
-__global__ void terms_kernel(DevParams P) {
+__global__ void terms_kernel(DevParams P, int32_t direct) {
+  if (!direct && (int)blockIdx.x >= P.ctrl[0]) return;   // grid sized before the host read n_active
   const int s = P.active[blockIdx.x];
   const int p = P.st_p[s];
   if (threadIdx.x == 0) P.st_M[s] = find_fft_index(P, p);
@@ -746,8 +747,7 @@ __device__ unsigned long long g_fft_prof[8];
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
 template <bool BIG>
 __global__ void __launch_bounds__(BIG ? 512 : 1024, 1)
-pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part,
-            int32_t ahead) {
+pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
 #ifdef SFFT_FFT_PROF
   long long prof_t0 = clock64();
@@ -764,24 +764,6 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   } else {
     slot = blockIdx.x / n_lines;
     n = blockIdx.x % n_lines;
-  }
-  // the block `ahead` positions later (it starts when a resident block retires) has its input line pulled into
-  // L2 now, so its load phase waits on L2 rather than HBM latency
-  if (threadIdx.x == 0 && ahead > 0 && ksplit == 1 && (int)blockIdx.x + ahead < (int)gridDim.x) {
-    const int b2 = blockIdx.x + ahead;
-    int slot2, n2;
-    if (P.fuse_decode) {
-      const int na = (int)gridDim.x / n_lines;
-      if (b2 < na) { slot2 = b2; n2 = 0; }
-      else { const int t = b2 - na; slot2 = t / (n_lines - 1); n2 = 1 + t % (n_lines - 1); }
-    } else {
-      slot2 = b2 / n_lines;
-      n2 = b2 % n_lines;
-    }
-    const int s2 = P.active[slot2];
-    const double2* src = P.lines + ((int64_t)s2 * n_lines + n2) * P.p_stride;
-    const uint32_t bytes = 16u * (uint32_t)P.st_p[s2];
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
   }
   const int s = P.active[slot];
   const int p = P.st_p[s];
@@ -903,16 +885,16 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
   if (n_signals <= 0) return cudaSuccess;
   if (!direct) {
     const size_t sm = sizeof(int) * (2 * (size_t)P.n_tslots + 4096);
-    cudaError_t e = cudaFuncSetAttribute(tables_assign_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = ensure_smem(tables_assign_kernel, sm);
     if (e != cudaSuccess) return e;
     tables_assign_kernel<<<1, 1024, sm, st>>>(P, epoch);
   }
   const size_t smem = (size_t)smem_bytes;
   auto kern = big ? fft_prep_kernel<true> : fft_prep_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   kern<<<n_signals, threads, smem, st>>>(P, direct ? 1 : 0);
-  terms_kernel<<<n_signals, 256, sizeof(int) * (size_t)P.p_stride, st>>>(P);
+  terms_kernel<<<n_signals, 256, sizeof(int) * (size_t)P.p_stride, st>>>(P, direct ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -920,20 +902,10 @@ cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, 
                         int32_t big, int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st) {
   const size_t smem = (size_t)smem_bytes;
   auto kern = big ? pfft_kernel<true> : pfft_kernel<false>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;
-  // resident blocks (the L2 prefetch distance)
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem);
-  const int ahead = getenv("SFFT_FFT_NOPREFETCH") ? 0 : n_sm * std::max(per_sm, 1);
-  if (grid > 0) kern<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part, ahead);
+  if (grid > 0) kern<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part);
   return cudaGetLastError();
 }
 

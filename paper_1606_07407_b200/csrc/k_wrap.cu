@@ -128,7 +128,7 @@ cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freq
   const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
   wrap_digits_kernel<<<blocks, 256, 0, st>>>(P, bad);
   const size_t smem = sizeof(unsigned long long) * (size_t)P.k;
-  e = cudaFuncSetAttribute(wrap_rank_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  e = ensure_smem(wrap_rank_kernel, smem);
   if (e != cudaSuccess) return e;
   wrap_rank_kernel<<<n_signals, 1024, smem, st>>>(P, perm);
   wrap_gather_kernel<<<blocks, 256, 0, st>>>(P, perm, bad, out_freqs, reinterpret_cast<double2*>(out_coeffs),

@@ -191,6 +191,12 @@ __device__ __forceinline__ double2 line_factor_exact(int64_t v, int64_t E) {
   return make_double2(c, s);
 }
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) only when the kernel's limit on this device is below `bytes`
+// (a host call per launch otherwise sits on the per-iteration critical path)
+cudaError_t ensure_smem(const void* kern, size_t bytes);
+template <class K>
+inline cudaError_t ensure_smem(K* kern, size_t bytes) { return ensure_smem(reinterpret_cast<const void*>(kern), bytes); }
+
 // ---- launchers (each .cu file) ----------------------------------------------------------
 // k_project.cu
 cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* freqs, const double* coeffs,

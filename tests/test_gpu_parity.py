@@ -512,3 +512,22 @@ def test_line_shard_plan_errors(S):
         S.solve(plans[0], torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
     with pytest.raises(S.SfftError):                         # shard order must match the group
         _group_solve(S, plans[::-1], w, a)
+
+
+@pytest.mark.parametrize("name,trials", [("c5", [0, 1]), ("c3", [0])])
+def test_table_cache_reuse_bitwise(S, name, trials):
+    """Per-prime tables cached across executes (table_cache_slots large enough that nothing is evicted): the
+    second execute reuses every prime's tables and must give bitwise the same result as the first and as a
+    plan with the minimum cache (tables recomputed every time)."""
+    c = W.CONFIGS[name]
+    w, a = W.make_batch(c, trials)
+    wt, at = torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda()
+    big = _plan(S, c, batch=len(trials), table_cache_slots=1024)
+    r1 = S.solve(big, wt, at)
+    r2 = S.solve(big, wt, at)
+    r0 = S.solve(_plan(S, c, batch=len(trials)), wt, at)
+    for r in (r2, r0):
+        assert torch.equal(r.count, r1.count) and torch.equal(r.per_status, r1.per_status)
+        assert torch.equal(r.freqs, r1.freqs)
+        assert torch.equal(torch.view_as_real(r.coeffs), torch.view_as_real(r1.coeffs))
+    assert r1.report.samples_used == r2.report.samples_used == r0.report.samples_used
