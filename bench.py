@@ -56,6 +56,7 @@ def parse():
                     help="signals: independent signal shards per rank (weak scaling, default); lines: every rank "
                          "solves the same signals and owns a shard of the shifted lines (strong scaling, NCCL "
                          "record all-gather per iteration, SURVEY 8(e))")
+    ap.add_argument("--latency-steps", type=int, default=20, help="single-signal solves timed for latency_single_solve")
     ap.add_argument("--table-cache", type=int, default=1024,
                     help="per-prime table cache slots (plan option table_cache_slots; ~1 MB each): the steady state "
                          "reuses the tables of every prime the workload visits")
@@ -318,6 +319,27 @@ def main():
         dist.all_reduce(ok_t, op=dist.ReduceOp.MIN)
     ok = bool(ok_t.item())
 
+    # single-solve latency: one signal per execute (trial 0 of this rank), device-resident inputs,
+    # CUDA events around each execute, median of the timed runs (not part of `value`)
+    lat = None
+    if args.latency_steps and not lines:
+        plan1 = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=1, expsum_path=args.expsum_path,
+                            table_cache_slots=args.table_cache)
+        sig1 = S.sfft_signal_expsum(plan1, w_d[:1].contiguous(), a_d[:1].contiguous())
+        outs1 = tuple(o[:1].clone() for o in outs)
+        for _ in range(2):
+            S.sfft_execute(plan1, sig1, outs1)
+        ts = []
+        for _ in range(args.latency_steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r1 = S.sfft_execute(plan1, sig1, outs1)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        lat = {"ms_median": sorted(ts)[len(ts) // 2], "ms_min": min(ts), "iterations": r1.report.iterations,
+               "signal": f"{cfg.name} trial {trials[0]}", "exact": bool(np.array_equal(outs1[0][0].cpu().numpy(), ws[0]))}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = args.cpu_threads or os.cpu_count() or 1
@@ -349,6 +371,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "modes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
+            "latency_single_solve": lat,
             "clocks": clocks.result() if clocks else None,
         }
         print(json.dumps(line), flush=True)

@@ -31,6 +31,7 @@ __device__ int ith_prime_at_least(const DevParams& P, int x, int i) {
 }
 
 __global__ void setup_kernel(DevParams P, int32_t iter) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= P.batch || P.st_status[s] != ST_RUN) return;
   const int nR = P.st_nR[s];
@@ -55,8 +56,7 @@ __global__ void setup_kernel(DevParams P, int32_t iter) {
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(P.ctrl, 0, sizeof(int32_t) * 4, st);
   if (e != cudaSuccess) return e;
-  setup_kernel<<<(P.batch + 255) / 256, 256, 0, st>>>(P, iter);
-  return cudaGetLastError();
+  return launch_pdl(setup_kernel, dim3((P.batch + 255) / 256), dim3(256), 0, st, P, iter);
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -97,6 +97,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kDecodeThreads)
 decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, int64_t* out_v,
               double2* out_a, int32_t* out_counts) {
+  pdl_wait();
   constexpr bool STAGE = MODE == kDecStage;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = P.active[blockIdx.x];
@@ -402,6 +403,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
 // are dropped) and tilted with the new one, order preserved; hashes, the hash table and the registry C
 // rows are rebuilt.  The level-local iteration counter restarts (Alg. 3 l.5).
 __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t* __restrict__ freqs) {
+  pdl_wait();
   const int s = blockIdx.x;
   if (!P.st_retilt[s]) return;
   __shared__ int scratch[64];
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
 }
 
 cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freqs, cudaStream_t st) {
-  if (P.n_levels > 1 && batch > 0) retilt_kernel<<<batch, 1024, 0, st>>>(P, freqs);
+  if (P.n_levels > 1 && batch > 0) return launch_pdl(retilt_kernel, dim3(batch), dim3(1024), 0, st, P, freqs);
   return cudaGetLastError();
 }
 
@@ -533,7 +535,8 @@ cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p
   const long work = (long)P.k * (P.r + 1) / 8;
   const int threads = (int)std::min<long>(kDecodeThreads, std::max<long>(128, (work + 31) / 32 * 32));
   if (n_active > 0)
-    decode_kernel<kDecCommit><<<n_active, threads, smem, st>>>(P, iter, 0, nullptr, nullptr, nullptr, nullptr);
+    return launch_pdl(decode_kernel<kDecCommit>, dim3(n_active), dim3(threads), smem, st, P, iter, 0, nullptr, nullptr,
+                      nullptr, nullptr);
   return cudaGetLastError();
 }
 

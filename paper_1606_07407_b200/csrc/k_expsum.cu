@@ -41,6 +41,7 @@ template <int TN, int TH, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 expsum_kernel(DevParams P, int32_t wn_count, int32_t n_htiles, int32_t n_ntiles, int32_t ksplit, double2* part,
               int32_t p_part) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int BN = TN * wn_count;
   const int WH = WARPS / wn_count;
@@ -303,6 +304,7 @@ __device__ __forceinline__ void dmma_group(StageF&& stage, const double2* sW, co
 template <int MB, int NB0, int NB1, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
 expsum_dmma_kernel(DevParams P, int32_t n_htiles, int32_t n_ntiles, int32_t ksplit, double2* part, int32_t p_part) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int WG = NB1 ? 2 : 1;
   constexpr int WPG = WARPS / WG;                               // warps per column group
@@ -443,8 +445,8 @@ static cudaError_t launch_grid(KernT kern, const ExpsumShape& S, int32_t max_p, 
   const int n_htiles = (max_p + S.bm - 1) / S.bm;
   const long grid = (long)n_signals * n_htiles * S.nt * sp.ksplit;
   if (grid <= 0) return cudaSuccess;
-  kern<<<(unsigned)grid, S.warps * 32, smem, st>>>(args..., n_htiles, S.nt, sp.ksplit, sp.part, sp.p_part);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3((unsigned)grid), dim3(S.warps * 32), smem, st, args..., n_htiles, S.nt, sp.ksplit,
+                    sp.part, sp.p_part);
 }
 
 template <int TN>

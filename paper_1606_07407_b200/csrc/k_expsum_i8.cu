@@ -52,6 +52,7 @@ constexpr int kI8StepTerms = 16;      // terms per K step (32 int8 K elements: r
 // sigma[s] >= every |Re C[j][n]|, |Im C[j][n]|: the line factors have unit modulus, so |C[j][n]| = |C[j][0]|
 // up to a few ulp; sigma = (1 + 1e-12) max_j |C[j][0]| (column 0 is the unshifted line, C[j][0] = a_j)
 __global__ void i8_sigma_kernel(DevParams P, int32_t K) {
+  pdl_wait();
   const int s = blockIdx.x;
   const double2* Cs = P.C_all + (int64_t)s * P.kk * P.Lp;
   double m = 0.0;
@@ -80,6 +81,7 @@ __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT
 // memory, every (column, K byte) value is split into its S digits in shared memory, and the S limb tiles
 // (contiguous in global memory) are written with 16-byte stores.
 __global__ void __launch_bounds__(256) i8_limbs_kernel(DevParams P, int32_t K, int32_t only_retilted) {
+  pdl_wait();
   __shared__ double2 cv[kI8StepTerms][48];                      // [term][line of the tile] (W <= 96)
   __shared__ __align__(16) uint8_t tiles[6 * 96 * 32];           // [limb][W * 32]
   const int NT = P.i8_NT, S = P.i8_S, ntiles = P.i8_ntiles, nks = P.i8_nks;
@@ -230,6 +232,7 @@ __device__ __forceinline__ int ring_slots(int W, int S) { return min(kI8MaxSlots
 // barriers through the cluster window; the commits are multicast to both CTAs.
 template <int S, bool PROF, bool PAIR>
 __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I8Args A, double2* part, int32_t n_tiles) {
+  pdl_wait();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* afull = reinterpret_cast<uint64_t*>(smem_raw);         // [kI8MaxSlots]
   uint64_t* aempty = afull + kI8MaxSlots;
@@ -589,7 +592,7 @@ int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st, bool only_retilted) {
   if (!only_retilted) i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);   // |a_j| do not change on a retilt
   const int64_t ctas = (int64_t)n_signals * P.i8_ntiles * ((K + kI8StepTerms - 1) / kI8StepTerms);
-  if (ctas > 0) i8_limbs_kernel<<<(unsigned)ctas, 256, 0, st>>>(P, K, only_retilted ? 1 : 0);
+  if (ctas > 0) return launch_pdl(i8_limbs_kernel, dim3((unsigned)ctas), dim3(256), 0, st, P, K, only_retilted ? 1 : 0);
   return cudaGetLastError();
 }
 
@@ -657,13 +660,15 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
     cfg.blockDim = dim3(kI8Threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute at[1];
+    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = pair ? 2 : 1;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     e = cudaLaunchKernelEx(&cfg, kern, P, A, part, (int32_t)tiles);
     if (e != cudaSuccess) return e;
   }

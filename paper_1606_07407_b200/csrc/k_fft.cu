@@ -458,6 +458,7 @@ __device__ void i8_log_tables(const DevParams& P, int slot, int p) {
 // Hits reuse their slot; the distinct missing primes get slots not used in this epoch (at most n_active slots
 // are in use, the cache has n_active + 16 or more), which are queued in fill[] for tables_fill.
 __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_t epoch) {
+  pdl_wait();
   extern __shared__ int sm[];
   int* sp = sm;                                      // [n_tslots] primes of the slots
   int* hkey = sp + P.n_tslots;                       // [2048] hash of missing primes
@@ -531,6 +532,7 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
 
 // ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
 __global__ void terms_kernel(DevParams P, int32_t direct) {
+  pdl_wait();
   if (!direct && (int)blockIdx.x >= P.ctrl[0]) return;   // grid sized before the host read n_active
   const int s = P.active[blockIdx.x];
   const int p = P.st_p[s];
@@ -597,6 +599,7 @@ __global__ void terms_kernel(DevParams P, int32_t direct) {
 // small sizes use radices <= 8 with 64 registers so that several CTAs share an SM.
 template <bool BIG>
 __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams P, int32_t direct) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   int slot, p;
   if (direct) {
@@ -748,6 +751,7 @@ __device__ unsigned long long g_fft_prof[8];
 template <bool BIG>
 __global__ void __launch_bounds__(BIG ? 512 : 1024, 1)
 pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
 #ifdef SFFT_FFT_PROF
   long long prof_t0 = clock64();
@@ -887,14 +891,17 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
     const size_t sm = sizeof(int) * (2 * (size_t)P.n_tslots + 4096);
     cudaError_t e = ensure_smem(tables_assign_kernel, sm);
     if (e != cudaSuccess) return e;
-    tables_assign_kernel<<<1, 1024, sm, st>>>(P, epoch);
+    e = launch_pdl(tables_assign_kernel, dim3(1), dim3(1024), sm, st, P, epoch);
+    if (e != cudaSuccess) return e;
   }
   const size_t smem = (size_t)smem_bytes;
   auto kern = big ? fft_prep_kernel<true> : fft_prep_kernel<false>;
   cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
-  kern<<<n_signals, threads, smem, st>>>(P, direct ? 1 : 0);
-  terms_kernel<<<n_signals, 256, sizeof(int) * (size_t)P.p_stride, st>>>(P, direct ? 1 : 0);
+  e = launch_pdl(kern, dim3(n_signals), dim3(threads), smem, st, P, direct ? 1 : 0);
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(terms_kernel, dim3(n_signals), dim3(256), sizeof(int) * (size_t)P.p_stride, st, P, direct ? 1 : 0);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -905,7 +912,7 @@ cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, 
   cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;
-  if (grid > 0) kern<<<(unsigned)grid, threads, smem, st>>>(P, n_lines, ksplit, part, p_part);
+  if (grid > 0) return launch_pdl(kern, dim3((unsigned)grid), dim3(threads), smem, st, P, n_lines, ksplit, part, p_part);
   return cudaGetLastError();
 }
 

@@ -197,6 +197,31 @@ cudaError_t ensure_smem(const void* kern, size_t bytes);
 template <class K>
 inline cudaError_t ensure_smem(K* kern, size_t bytes) { return ensure_smem(reinterpret_cast<const void*>(kern), bytes); }
 
+// Programmatic dependent launch for the per-iteration kernel chain: a kernel launched with launch_pdl may be
+// scheduled while its predecessor drains; every such kernel calls pdl_wait() before touching anything the
+// predecessor writes (griddepcontrol.wait returns immediately for a kernel launched without the attribute).
+// SFFT_NO_PDL=1 turns the attribute off (A/B).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+inline bool pdl_enabled() {
+  static const bool on = getenv("SFFT_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- launchers (each .cu file) ----------------------------------------------------------
 // k_project.cu
 cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* freqs, const double* coeffs,
