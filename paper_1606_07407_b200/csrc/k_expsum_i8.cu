@@ -232,7 +232,6 @@ __device__ __forceinline__ int ring_slots(int W, int S) { return min(kI8MaxSlots
 // barriers through the cluster window; the commits are multicast to both CTAs.
 template <int S, bool PROF, bool PAIR>
 __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I8Args A, double2* part, int32_t n_tiles) {
-  pdl_wait();
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   uint64_t* afull = reinterpret_cast<uint64_t*>(smem_raw);         // [kI8MaxSlots]
   uint64_t* aempty = afull + kI8MaxSlots;
@@ -278,6 +277,7 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
   if (PAIR) tc::cluster_sync();                                        // barriers of both CTAs initialised
   tc::fence_after_sync();
   const uint32_t tbase = *tslot;
+  pdl_wait();       // the prologue above (TMEM, barriers) overlaps the predecessor's tail; its data only from here
   // the leader's afull / accempty as seen from this CTA (cluster window), for the peer's arrivals
   const uint32_t afull_l = PAIR ? tc::mapa(afull, 0) : 0u, accempty_l = PAIR ? tc::mapa(accempty, 0) : 0u;
   // Peer arrivals of the generators / epilogue only signal completed TMEM stores / loads (tcgen05.wait::st /
