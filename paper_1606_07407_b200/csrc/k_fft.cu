@@ -214,40 +214,47 @@ __device__ __forceinline__ void bfly_finish(double2* x, int base, int Q, double2
   }
 }
 
-template <int R, bool INV>
-__device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double2* __restrict__ tb) {
+// ZT: the first DIF pass of a zero-padded input -- points at index >= nz are zero and are neither stored by
+// the load phase nor read here (the pass writes every point, so the buffer needs no zero fill)
+template <int R, bool INV, bool ZT = false>
+__device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double2* __restrict__ tb, int nz = 0) {
   const int Q = S / R;
   const int nb = M / R;
   for (int bi = threadIdx.x; bi < nb; bi += blockDim.x) {
     const int blk = bi / Q, n1 = bi - blk * Q;
     const int base = blk * S + n1;
     double2 v[R];
-    bfly_load<R, INV>(x, base, Q, v);
+    if (ZT) {
+#pragma unroll
+      for (int n = 0; n < R; ++n) v[n] = base + Q * n < nz ? x[base + Q * n] : make_double2(0.0, 0.0);
+    } else {
+      bfly_load<R, INV>(x, base, Q, v);
+    }
     bfly_finish<R, INV>(x, base, Q, tb[n1], v);
   }
 }
 
-template <bool INV, bool BIG>
-__device__ void fft_pass(double2* x, int M, int S, int R, const double2* tb) {
+template <bool INV, bool BIG, bool ZT = false>
+__device__ void fft_pass(double2* x, int M, int S, int R, const double2* tb, int nz = 0) {
   if constexpr (BIG) {
     switch (R) {
-      case 6: pass_loop<6, INV>(x, M, S, tb); __syncthreads(); return;
-      case 9: pass_loop<9, INV>(x, M, S, tb); __syncthreads(); return;
-      case 10: pass_loop<10, INV>(x, M, S, tb); __syncthreads(); return;
-      case 12: pass_loop<12, INV>(x, M, S, tb); __syncthreads(); return;
-      case 14: pass_loop<14, INV>(x, M, S, tb); __syncthreads(); return;
-      case 15: pass_loop<15, INV>(x, M, S, tb); __syncthreads(); return;
-      case 16: pass_loop<16, INV>(x, M, S, tb); __syncthreads(); return;
+      case 6: pass_loop<6, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
+      case 9: pass_loop<9, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
+      case 10: pass_loop<10, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
+      case 12: pass_loop<12, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
+      case 14: pass_loop<14, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
+      case 15: pass_loop<15, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
+      case 16: pass_loop<16, INV, ZT>(x, M, S, tb, nz); __syncthreads(); return;
     }
   }
   switch (R) {
-    case 2: pass_loop<2, INV>(x, M, S, tb); break;
-    case 3: pass_loop<3, INV>(x, M, S, tb); break;
-    case 4: pass_loop<4, INV>(x, M, S, tb); break;
-    case 5: pass_loop<5, INV>(x, M, S, tb); break;
-    case 6: pass_loop<6, INV>(x, M, S, tb); break;
-    case 7: pass_loop<7, INV>(x, M, S, tb); break;
-    case 8: pass_loop<8, INV>(x, M, S, tb); break;
+    case 2: pass_loop<2, INV, ZT>(x, M, S, tb, nz); break;
+    case 3: pass_loop<3, INV, ZT>(x, M, S, tb, nz); break;
+    case 4: pass_loop<4, INV, ZT>(x, M, S, tb, nz); break;
+    case 5: pass_loop<5, INV, ZT>(x, M, S, tb, nz); break;
+    case 6: pass_loop<6, INV, ZT>(x, M, S, tb, nz); break;
+    case 7: pass_loop<7, INV, ZT>(x, M, S, tb, nz); break;
+    case 8: pass_loop<8, INV, ZT>(x, M, S, tb, nz); break;
   }
   __syncthreads();
 }
@@ -324,7 +331,8 @@ __device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* _
 
 // forward DIF FFT, natural -> digit-reversed; tb = shared copy of this size's tables
 template <bool BIG>
-__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0) {
+// nz < M: only x[0, nz) holds data, the rest is implicit zero padding (never stored, see pass_loop ZT)
+__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0, int nz = -1) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -332,7 +340,8 @@ __device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* t
   int S = M;
   for (int ps = 0; ps < npass - skip_last; ++ps) {
     const int R = radix[ps];
-    fft_pass<false, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
+    if (ps == 0 && nz >= 0 && nz < M) fft_pass<false, BIG, true>(x, M, S, R, tb + (off[ps] - off[0]), nz);
+    else fft_pass<false, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
     S /= R;
   }
 }
@@ -785,7 +794,6 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     const int32_t* pw = P.i8_pw + (int64_t)tslot * P.i8_tstride;
     const double2* chl = P.i8_chl + (int64_t)tslot * P.i8_tstride;
     const int n_slots = gridDim.x / n_lines;
-    for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);   // zero padding
     constexpr int U = BIG ? 8 : 4;
     for (int f0 = threadIdx.x; f0 < p; f0 += U * blockDim.x) {
       double2 v[U], c[U];
@@ -812,7 +820,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     }
   } else if (ksplit == 1) {
     // 4 independent loads in flight per thread (latency-bound phase)
-    for (int q0 = threadIdx.x; q0 < M; q0 += 4 * blockDim.x) {
+    for (int q0 = threadIdx.x; q0 < p; q0 += 4 * blockDim.x) {
       double2 a[4], c[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
@@ -823,28 +831,27 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int q = q0 + u * blockDim.x;
-        if (q < M) x[q] = cmulx(a[u], c[u]);
+        if (q < p) x[q] = cmulx(a[u], c[u]);
       }
     }
   } else {
     // sum the exp-sum partials over the term splits in fixed order (deterministic)
     const int n_slots = gridDim.x / n_lines;
-    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+    for (int q = threadIdx.x; q < p; q += blockDim.x) {
       double2 v = make_double2(0.0, 0.0);
-      if (q < p) {
-        for (int ks = 0; ks < ksplit; ++ks) {
-          const double2 t = part[(((int64_t)ks * n_slots + slot) * n_lines + n) * p_part + q];
-          v.x += t.x;
-          v.y += t.y;
-        }
-        v = cmulx(v, ch[q]);
+      for (int ks = 0; ks < ksplit; ++ks) {
+        const double2 t = part[(((int64_t)ks * n_slots + slot) * n_lines + n) * p_part + q];
+        v.x += t.x;
+        v.y += t.y;
       }
-      x[q] = v;
+      x[q] = cmulx(v, ch[q]);
     }
   }
+  if (P.fft_npass[fi] <= 1)                           // a single-pass size has no DIF pass to treat the padding
+    for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
   __syncthreads();
   FFT_PROF_MARK(0);
-  fft_dif<BIG>(P, x, fi, tb, 1);
+  fft_dif<BIG>(P, x, fi, tb, 1, p);                   // x[p, M) is implicit zero padding
   FFT_PROF_MARK(1);
   fft_mid<BIG>(P, x, fi, P.V + (int64_t)tslot * P.M_stride);
   FFT_PROF_MARK(2);
