@@ -196,8 +196,8 @@ __device__ __forceinline__ void twiddle_powers(double2 b, double2 (&w)[R]) {
   }
 }
 
-template <int R, bool INV>
-__device__ __forceinline__ void bfly_finish(double2* x, int base, int Q, double2 b, double2 (&v)[R]) {
+template <int R, bool INV, bool ZT = false>
+__device__ __forceinline__ void bfly_finish(double2* x, int base, int Q, double2 b, double2 (&v)[R], int nz = 0) {
   double2 w[R];
   twiddle_powers<R>(b, w);
   if (!INV) {
@@ -210,12 +210,14 @@ __device__ __forceinline__ void bfly_finish(double2* x, int base, int Q, double2
     for (int k = 1; k < R; ++k) v[k] = cmulconj(v[k], w[k]);
     dft_small<R, true>(v);
 #pragma unroll
-    for (int n = 0; n < R; ++n) x[base + Q * n] = v[n];
+    for (int n = 0; n < R; ++n)
+      if (!ZT || base + Q * n < nz) x[base + Q * n] = v[n];   // ZT (last DIT pass): outputs >= nz are not needed
   }
 }
 
-// ZT: the first DIF pass of a zero-padded input -- points at index >= nz are zero and are neither stored by
-// the load phase nor read here (the pass writes every point, so the buffer needs no zero fill)
+// ZT, forward: the first DIF pass of a zero-padded input -- points at index >= nz are zero and are neither stored
+// by the load phase nor read here (the pass writes every point, so the buffer needs no zero fill).
+// ZT, inverse: the last DIT pass stores only the outputs below nz (the Bluestein result needs b < p)
 template <int R, bool INV, bool ZT = false>
 __device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double2* __restrict__ tb, int nz = 0) {
   const int Q = S / R;
@@ -224,13 +226,13 @@ __device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double
     const int blk = bi / Q, n1 = bi - blk * Q;
     const int base = blk * S + n1;
     double2 v[R];
-    if (ZT) {
+    if (ZT && !INV) {
 #pragma unroll
       for (int n = 0; n < R; ++n) v[n] = base + Q * n < nz ? x[base + Q * n] : make_double2(0.0, 0.0);
     } else {
       bfly_load<R, INV>(x, base, Q, v);
     }
-    bfly_finish<R, INV>(x, base, Q, tb[n1], v);
+    bfly_finish<R, INV, ZT && INV>(x, base, Q, tb[n1], v, nz);
   }
 }
 
@@ -347,7 +349,7 @@ __device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* t
 }
 // inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
 template <bool BIG>
-__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb, int skip_first = 0) {
+__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb, int skip_first = 0, int nz = -1) {
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -357,7 +359,8 @@ __device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* t
     const int R = radix[ps];
     S *= R;
     if (ps == npass - 1 && skip_first) continue;
-    fft_pass<true, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
+    if (ps == 0 && nz >= 0 && nz < M) fft_pass<true, BIG, true>(x, M, S, R, tb + (off[ps] - off[0]), nz);
+    else fft_pass<true, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
   }
 }
 
@@ -855,7 +858,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   FFT_PROF_MARK(1);
   fft_mid<BIG>(P, x, fi, P.V + (int64_t)tslot * P.M_stride);
   FFT_PROF_MARK(2);
-  fft_dit<BIG>(P, x, fi, tb, 1);
+  fft_dit<BIG>(P, x, fi, tb, 1, p);                   // only F[b], b < p, is used
   FFT_PROF_MARK(3);
   if (P.fuse_decode) {
     if (n == 0) fused_select(P, s, p, x, ch, line);
