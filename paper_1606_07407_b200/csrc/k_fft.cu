@@ -468,26 +468,47 @@ __device__ void i8_log_tables(const DevParams& P, int slot, int p) {
 
 // ---- table cache: slot assignment (one CTA) ----
 // Hits reuse their slot; the distinct missing primes get slots not used in this epoch (at most n_active slots
-// are in use, the cache has n_active + 16 or more), which are queued in fill[] for tables_fill.
+// are in use, the cache has n_active + 16 or more), which are queued in fill[] for tables_fill.  The primes of
+// the slots are looked up through a shared-memory hash map (prime -> slot) built at entry, O(1) per signal.
+__device__ __forceinline__ int tab_hash(int p, int mask) { return (int)(((uint32_t)p * 2654435761u) >> 7) & mask; }
+
 __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_t epoch) {
   pdl_wait();
   extern __shared__ int sm[];
-  int* sp = sm;                                      // [n_tslots] primes of the slots
-  int* hkey = sp + P.n_tslots;                       // [2048] hash of missing primes
+  const int C = P.n_tslots;
+  int HS = 2048;
+  while (HS < 2 * C) HS <<= 1;
+  const int hm = HS - 1;
+  int* mk = sm;                                      // [HS] map keys: prime of a slot (0 = empty)
+  int* mv = mk + HS;                                 // [HS] map values: slot
+  int* hkey = mv + HS;                               // [2048] hash of missing primes
   int* hidx = hkey + 2048;                           // [2048] their rank
+  int* ep = hidx + 2048;                             // [C] slot epochs (victim choice)
   __shared__ int n_miss, n_free;
   const int n_active = P.ctrl[0];
-  const int C = P.n_tslots;
-  for (int i = threadIdx.x; i < C; i += blockDim.x) sp[i] = P.slot_p[i];
+  for (int i = threadIdx.x; i < HS; i += blockDim.x) mk[i] = 0;
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) hkey[i] = 0;
   if (threadIdx.x == 0) { n_miss = 0; n_free = 0; }
   __syncthreads();
+  for (int i = threadIdx.x; i < C; i += blockDim.x) {
+    const int p = P.slot_p[i];
+    if (p == 0) continue;
+    int h = tab_hash(p, hm);
+    while (atomicCAS(&mk[h], 0, p) != 0) h = (h + 1) & hm;        // each prime occupies at most one slot
+    mv[h] = i;
+  }
+  __syncthreads();
+  auto lookup = [&](int p) -> int {
+    for (int h = tab_hash(p, hm);; h = (h + 1) & hm) {
+      const int k = mk[h];
+      if (k == p) return mv[h];
+      if (k == 0) return -1;
+    }
+  };
   for (int a = threadIdx.x; a < n_active; a += blockDim.x) {
     const int s = P.active[a];
     const int p = P.st_p[s];
-    int hit = -1;
-    for (int i = 0; i < C; ++i)
-      if (sp[i] == p) { hit = i; break; }
+    const int hit = lookup(p);
     if (hit >= 0) {
       P.st_slot[s] = hit;
       P.slot_epoch[hit] = epoch;
@@ -504,8 +525,7 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
   __syncthreads();
   // victims for the missing primes: least recently used first (empty slots have epoch -1), ties -> lower index;
   // warp 0 picks them one by one (deterministic; n_miss is 0 in the steady state)
-  if (threadIdx.x < 32) {
-    int* ep = hidx + 2048;                                     // [n_tslots] epochs, chosen slots marked
+  if (threadIdx.x < 32 && n_miss > 0) {
     for (int i = threadIdx.x; i < C; i += 32) ep[i] = P.slot_epoch[i];
     __syncwarp();
     int got = 0;
@@ -524,20 +544,26 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
     if (threadIdx.x == 0) n_free = got;
   }
   __syncthreads();
+  if (n_miss == 0) {
+    if (threadIdx.x == 0) P.ctrl[3] = 0;
+    return;
+  }
+  // the filled slots: new primes into the map (the victims' old primes are not looked up in this epoch)
   for (int h = threadIdx.x; h < 2048; h += blockDim.x) {
     const int p = hkey[h];
     if (p == 0 || hidx[h] >= n_free) continue;
     const int slot = P.fill[hidx[h]];
     P.slot_p[slot] = p;
     P.slot_epoch[slot] = epoch;
-    sp[slot] = p;
+    int g = tab_hash(p, hm);
+    while (atomicCAS(&mk[g], 0, p) != 0) g = (g + 1) & hm;
+    mv[g] = slot;
   }
   __syncthreads();
   for (int a = threadIdx.x; a < n_active; a += blockDim.x) {
     const int s = P.active[a];
-    const int p = P.st_p[s];
-    for (int i = 0; i < C; ++i)
-      if (sp[i] == p) { P.st_slot[s] = i; break; }
+    const int slot = lookup(P.st_p[s]);
+    if (slot >= 0) P.st_slot[s] = slot;
   }
   if (threadIdx.x == 0) P.ctrl[3] = min(n_miss, n_free);
 }
@@ -898,7 +924,9 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
                             cudaStream_t st, int32_t epoch, bool direct) {
   if (n_signals <= 0) return cudaSuccess;
   if (!direct) {
-    const size_t sm = sizeof(int) * (2 * (size_t)P.n_tslots + 4096);
+    size_t hs = 2048;
+    while (hs < 2 * (size_t)P.n_tslots) hs <<= 1;
+    const size_t sm = sizeof(int) * (2 * hs + 4096 + (size_t)P.n_tslots);
     cudaError_t e = ensure_smem(tables_assign_kernel, sm);
     if (e != cudaSuccess) return e;
     e = launch_pdl(tables_assign_kernel, dim3(1), dim3(1024), sm, st, P, epoch);
