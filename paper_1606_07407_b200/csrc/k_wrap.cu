@@ -2,8 +2,9 @@
 //   untilt every tilted pair: u = T^T v / hypo^2, rejecting non-integers (Alg. 3 l.38-39, reading R17)
 //   wrap every block by balanced digits: digit = ((u + N/2) mod N) - N/2, u <- (u - digit)/N
 //   canonical order: lexicographic by frequency vector.
-// Three kernels: digits (one warp per registry entry, lanes over blocks), rank (one CTA per
-// signal; keys of the first two coordinates in shared memory, full compare only on ties), gather.
+// Three kernels: digits (one warp per registry entry, lanes over blocks), rank (one CTA per signal; the rows
+// packed into fixed-width 64-bit chunks in shared memory, or keys of the first two coordinates with a full
+// compare on ties when they do not fit), gather.
 #include "sfft_internal.cuh"
 
 namespace sfft {
@@ -56,7 +57,46 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad) {
   if (__any_sync(0xffffffffu, err) && lane == 0) bad[s] = 1;
 }
 
-// rank of every entry in lexicographic order -> perm[s][rank] = entry
+// rank of every entry in lexicographic order -> perm[s][rank] = entry.  Rows packed into fixed-width 64-bit
+// chunks in shared memory (coordinate + N/2 in `bits` bits, `per` coordinates per chunk, most significant
+// first): chunk sequences compare like the rows, so every comparison is a few shared-memory loads
+__global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm, int bits, int per, int nch) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [nch][k]
+  const int s = blockIdx.x, tid = threadIdx.x;
+  const int nR = P.st_nR[s];
+  const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
+  const int64_t h2 = P.N / 2;
+  for (int i = tid; i < nch * nR; i += blockDim.x) {
+    const int c = i / nR, e = i - c * nR;
+    const int32_t* row = wt + (int64_t)e * P.d;
+    unsigned long long kv = 0;
+    for (int t = 0; t < per; ++t) {
+      const int l = c * per + t;
+      kv = (kv << bits) | (l < P.d ? (unsigned long long)(row[l] + h2) : 0ull);
+    }
+    key[(int64_t)c * P.k + e] = kv;
+  }
+  __syncthreads();
+  for (int e = tid; e < nR; e += blockDim.x) {
+    const unsigned long long ke = key[e];
+    int rank = 0;
+    for (int f = 0; f < nR; ++f) {
+      const unsigned long long kf = key[f];
+      if (kf < ke) ++rank;
+      else if (kf == ke && f != e) {
+        for (int c = 1; c < nch; ++c) {
+          const unsigned long long a = key[(int64_t)c * P.k + f], b = key[(int64_t)c * P.k + e];
+          if (a != b) { rank += a < b; break; }
+        }
+      }
+    }
+    perm[(int64_t)s * P.k + rank] = e;
+  }
+}
+
+// fallback when the packed rows do not fit in shared memory: keys of the first two coordinates, full
+// compare from global memory on ties
 __global__ void wrap_rank_kernel(DevParams P, int32_t* __restrict__ perm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [k]
@@ -127,10 +167,23 @@ cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freq
   const int64_t warps = (int64_t)n_signals * P.k;
   const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
   wrap_digits_kernel<<<blocks, 256, 0, st>>>(P, bad);
-  const size_t smem = sizeof(unsigned long long) * (size_t)P.k;
-  e = ensure_smem(wrap_rank_kernel, smem);
-  if (e != cudaSuccess) return e;
-  wrap_rank_kernel<<<n_signals, 1024, smem, st>>>(P, perm);
+  int bits = 1;
+  while (((int64_t)1 << bits) < P.N) ++bits;
+  const int per = 64 / bits, nch = (P.d + per - 1) / per;
+  const size_t psmem = sizeof(unsigned long long) * (size_t)nch * P.k;
+  int optin = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  if (psmem <= (size_t)optin) {
+    e = ensure_smem(wrap_rank_packed_kernel, psmem);
+    if (e != cudaSuccess) return e;
+    wrap_rank_packed_kernel<<<n_signals, 1024, psmem, st>>>(P, perm, bits, per, nch);
+  } else {
+    const size_t smem = sizeof(unsigned long long) * (size_t)P.k;
+    e = ensure_smem(wrap_rank_kernel, smem);
+    if (e != cudaSuccess) return e;
+    wrap_rank_kernel<<<n_signals, 1024, smem, st>>>(P, perm);
+  }
   wrap_gather_kernel<<<blocks, 256, 0, st>>>(P, perm, bad, out_freqs, reinterpret_cast<double2*>(out_coeffs),
                                              out_count, out_status);
   return cudaGetLastError();
