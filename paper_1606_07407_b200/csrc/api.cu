@@ -119,7 +119,7 @@ enum Buf {
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
-  B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD,
+  B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -268,6 +268,10 @@ void layout(sfft_plan_t* P) {
   sz[B_SLOTP] = 4 * T;
   sz[B_SLOTE] = 4 * T;
   sz[B_FILL] = 4 * T;
+  sz[B_FILLBY] = 4 * T;
+  sz[B_FILLEP] = 4 * T;
+  sz[B_SLOTRDY] = 4 * T;
+  sz[B_ASGRDY] = 4;
   sz[B_I8TLO] = P->i8_ok ? 8 * T * (2 * P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
   // decode records (fused FFT epilogue -> commit); line shards also receive every shard's records
@@ -362,6 +366,10 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.slot_p = ptr<int32_t>(P, B_SLOTP);
   D.slot_epoch = ptr<int32_t>(P, B_SLOTE);
   D.fill = ptr<int32_t>(P, B_FILL);
+  D.fill_by = ptr<int32_t>(P, B_FILLBY);
+  D.fill_ep = ptr<int32_t>(P, B_FILLEP);
+  D.slot_ready = ptr<int32_t>(P, B_SLOTRDY);
+  D.assign_ready = ptr<int32_t>(P, B_ASGRDY);
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
@@ -446,6 +454,9 @@ int ensure_ready(sfft_plan_t* P) {
     // empty per-prime table cache (slot_p = 0, slot_epoch = -1)
     CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SLOTP), 0, 4 * ((size_t)P->n_tslots + 1), P->stream));
     CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SLOTE), 0xFF, 4 * ((size_t)P->n_tslots + 1), P->stream));
+    for (int b : {B_FILLEP, B_SLOTRDY})
+      CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, b), 0xFF, 4 * ((size_t)P->n_tslots + 1), P->stream));
+    CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_ASGRDY), 0xFF, 4, P->stream));
     // fused-decode publication stamps: never equal to an iteration stamp (those are >= 1)
     CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SELRDY), 0xFF, 4 * (size_t)P->batch, P->stream));
     CUDA_TRY(P, cudaStreamSynchronize(P->stream));
@@ -527,8 +538,14 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
   // the host round trip overlaps it
   {
     const FftSize& fb = P->fft.back();
-    LAUNCH(P, launch_fft_prep(D, n_bound, (int)fb.smem_upto, 512, 1, st, ++P->epoch));
-    launches += 2;   // tables_assign, terms
+    // one combined kernel while the signals fit in one wave of its (largest-FFT) shared-memory footprint;
+    // beyond that the separate assign / fill / terms kernels keep the terms work at full occupancy
+    if (n_bound <= P->n_sm) {
+      LAUNCH(P, launch_prep_iter(D, n_bound, (int)fb.smem_upto, st, ++P->epoch));
+    } else {
+      LAUNCH(P, launch_fft_prep(D, n_bound, (int)fb.smem_upto, 512, 1, st, ++P->epoch));
+      launches += 2;   // tables_assign, terms
+    }
   }
   CUDA_TRY(P, cudaEventSynchronize(P->ev_ctrl));
   it->n_active = P->h_ctrl[0];

@@ -472,9 +472,10 @@ __device__ void i8_log_tables(const DevParams& P, int slot, int p) {
 // the slots are looked up through a shared-memory hash map (prime -> slot) built at entry, O(1) per signal.
 __device__ __forceinline__ int tab_hash(int p, int mask) { return (int)(((uint32_t)p * 2654435761u) >> 7) & mask; }
 
-__global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_t epoch) {
-  pdl_wait();
-  extern __shared__ int sm[];
+// sm: 2 HS + 2 * 2048 + C ints (HS = power of two >= max(2048, 2C)).  fillers: also record, for every slot
+// refilled in this epoch, the lowest active index whose signal uses the prime (the CTA that fills it in
+// prep_iter_kernel: every other user has a higher block index)
+__device__ void assign_slots(const DevParams& P, int32_t epoch, int* sm, bool fillers) {
   const int C = P.n_tslots;
   int HS = 2048;
   while (HS < 2 * C) HS <<= 1;
@@ -484,10 +485,11 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
   int* hkey = mv + HS;                               // [2048] hash of missing primes
   int* hidx = hkey + 2048;                           // [2048] their rank
   int* ep = hidx + 2048;                             // [C] slot epochs (victim choice)
+  int* hfill = ep + C;                               // [2048] lowest active index using the missing prime
   __shared__ int n_miss, n_free;
   const int n_active = P.ctrl[0];
   for (int i = threadIdx.x; i < HS; i += blockDim.x) mk[i] = 0;
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) hkey[i] = 0;
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) { hkey[i] = 0; hfill[i] = 0x7fffffff; }
   if (threadIdx.x == 0) { n_miss = 0; n_free = 0; }
   __syncthreads();
   for (int i = threadIdx.x; i < C; i += blockDim.x) {
@@ -520,6 +522,7 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
         if (old == p) break;
         h = (h + 1) & 2047;
       }
+      atomicMin(&hfill[h], a);
     }
   }
   __syncthreads();
@@ -555,6 +558,7 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
     const int slot = P.fill[hidx[h]];
     P.slot_p[slot] = p;
     P.slot_epoch[slot] = epoch;
+    if (fillers) { P.fill_by[slot] = hfill[h]; P.fill_ep[slot] = epoch; }
     int g = tab_hash(p, hm);
     while (atomicCAS(&mk[g], 0, p) != 0) g = (g + 1) & hm;
     mv[g] = slot;
@@ -568,11 +572,16 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
   if (threadIdx.x == 0) P.ctrl[3] = min(n_miss, n_free);
 }
 
-// ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
-__global__ void terms_kernel(DevParams P, int32_t direct) {
+__global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_t epoch) {
   pdl_wait();
-  if (!direct && (int)blockIdx.x >= P.ctrl[0]) return;   // grid sized before the host read n_active
-  const int s = P.active[blockIdx.x];
+  extern __shared__ int sm[];
+  assign_slots(P, epoch, sm, false);
+}
+
+
+// ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
+// cnt: >= p ints of shared memory; scratch: >= 32 ints
+__device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch) {
   const int p = P.st_p[s];
   if (threadIdx.x == 0) P.st_M[s] = find_fft_index(P, p);
   const int m = P.st_m[s];
@@ -593,8 +602,6 @@ __global__ void terms_kernel(DevParams P, int32_t direct) {
   // registry entries grouped by their bin u_e (bin-domain residual, reading R21): counting sort, stable in e
   const int nR = P.st_nR[s];
   if (P.literal || nR == 0) return;
-  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end
-  __shared__ int scratch[32];
   int32_t* bstart = P.bin_start + (int64_t)s * (P.p_stride + 1);
   int32_t* border = P.bin_order + (int64_t)s * P.k;
   const int2* ur = ug + P.k;
@@ -632,23 +639,21 @@ __global__ void terms_kernel(DevParams P, int32_t direct) {
   }
 }
 
+__global__ void terms_kernel(DevParams P, int32_t direct) {
+  pdl_wait();
+  if (!direct && (int)blockIdx.x >= P.ctrl[0]) return;   // grid sized before the host read n_active
+  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end
+  __shared__ int scratch[32];
+  terms_body(P, P.active[blockIdx.x], cnt, scratch);
+}
+
 // per active signal: expsum root table, Bluestein chirp and the kernel spectrum for its prime
 // BIG: sizes >= 4096 whose plans use in-register radices up to 16 (512 threads, 128 registers);
 // small sizes use radices <= 8 with 64 registers so that several CTAs share an SM.
+// tables of prime p into cache slot `slot`: W_p roots, Bluestein chirp, kernel spectrum V = DIF(conj chirp)/M,
+// int8 root tables in discrete-log order; smem: the FFT buffer of size M and its twiddles
 template <bool BIG>
-__global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams P, int32_t direct) {
-  pdl_wait();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  int slot, p;
-  if (direct) {
-    const int s = P.active[blockIdx.x];
-    slot = P.st_slot[s];
-    p = P.st_p[s];
-  } else {
-    if ((int)blockIdx.x >= P.ctrl[3]) return;
-    slot = P.fill[blockIdx.x];
-    p = P.slot_p[slot];
-  }
+__device__ void fill_tables(const DevParams& P, int slot, int p, unsigned char* smem_raw) {
   const int fi = find_fft_index(P, p);
   const int M = P.fft_M[fi];
   double2* x = reinterpret_cast<double2*>(smem_raw);
@@ -674,6 +679,72 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams
   const double inv = 1.0 / (double)M;
   double2* V = P.V + (int64_t)slot * P.M_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
+}
+
+// stage entry points (direct): the tables of every listed signal's prime; else the queued fills of the iteration
+template <bool BIG>
+__global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams P, int32_t direct) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  int slot, p;
+  if (direct) {
+    const int s = P.active[blockIdx.x];
+    slot = P.st_slot[s];
+    p = P.st_p[s];
+  } else {
+    if ((int)blockIdx.x >= P.ctrl[3]) return;
+    slot = P.fill[blockIdx.x];
+    p = P.slot_p[slot];
+  }
+  fill_tables<BIG>(P, slot, p, smem_raw);
+}
+
+// One kernel per iteration for the table prep (CTA per active-signal slot of the previous count): CTA 0 maps
+// the primes to cache slots and releases a stamp; every CTA then fills its prime's slot if it is the filler
+// (lowest active index using the prime) and releases the slot's stamp, or waits for that stamp (the filler
+// has a lower block index: resident or finished -- the decoupled look-back progress argument); then the
+// signal's terms.  Replaces tables_assign + fft_prep + terms launches.
+__device__ __forceinline__ void wait_stamp(const int32_t* flag, int32_t v) {
+  int got;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(flag) : "memory");
+    if (got == v) return;
+    __nanosleep(64);
+  }
+}
+__device__ __forceinline__ void release_stamp(int32_t* flag, int32_t v) {
+  __threadfence();
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
+}
+
+template <bool BIG>
+__global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParams P, int32_t epoch) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int scratch[32];
+  if (blockIdx.x == 0) {
+    assign_slots(P, epoch, reinterpret_cast<int*>(smem_raw), true);
+    __syncthreads();
+    if (threadIdx.x == 0) release_stamp(P.assign_ready, epoch);
+  } else if (threadIdx.x == 0) {
+    wait_stamp(P.assign_ready, epoch);
+  }
+  __syncthreads();
+  const int a = blockIdx.x;
+  if (a >= P.ctrl[0]) return;
+  const int s = P.active[a];
+  const int slot = P.st_slot[s];
+  if (P.fill_ep[slot] == epoch) {
+    if (P.fill_by[slot] == a) {
+      fill_tables<BIG>(P, slot, P.st_p[s], smem_raw);
+      __syncthreads();
+      if (threadIdx.x == 0) release_stamp(P.slot_ready + slot, epoch);
+    } else if (threadIdx.x == 0) {
+      wait_stamp(P.slot_ready + slot, epoch);
+    }
+    __syncthreads();
+  }
+  terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch);
 }
 
 // ---- fused decode epilogue: no HBM round trip of the lines n >= 1 ----
@@ -920,13 +991,25 @@ cudaError_t fft_prof_read(unsigned long long* out, bool reset) {
 }
 #endif
 
+cudaError_t launch_prep_iter(const DevParams& P, int32_t n_bound, int32_t smem_bytes, cudaStream_t st, int32_t epoch) {
+  if (n_bound <= 0) return cudaSuccess;
+  size_t hs = 2048;
+  while (hs < 2 * (size_t)P.n_tslots) hs <<= 1;
+  const size_t smem = std::max<size_t>((size_t)smem_bytes,
+                                       std::max(sizeof(int) * (2 * hs + 2 * 4096 + (size_t)P.n_tslots),
+                                                sizeof(int) * (size_t)P.p_stride));
+  cudaError_t e = ensure_smem(prep_iter_kernel<true>, smem);
+  if (e != cudaSuccess) return e;
+  return launch_pdl(prep_iter_kernel<true>, dim3(n_bound), dim3(512), smem, st, P, epoch);
+}
+
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
                             cudaStream_t st, int32_t epoch, bool direct) {
   if (n_signals <= 0) return cudaSuccess;
   if (!direct) {
     size_t hs = 2048;
     while (hs < 2 * (size_t)P.n_tslots) hs <<= 1;
-    const size_t sm = sizeof(int) * (2 * hs + 4096 + (size_t)P.n_tslots);
+    const size_t sm = sizeof(int) * (2 * hs + 2 * 4096 + (size_t)P.n_tslots);
     cudaError_t e = ensure_smem(tables_assign_kernel, sm);
     if (e != cudaSuccess) return e;
     e = launch_pdl(tables_assign_kernel, dim3(1), dim3(1024), sm, st, P, epoch);

@@ -87,6 +87,10 @@ struct DevParams {
   int32_t* slot_p;             // [n_tslots] prime held by the slot, 0 = empty
   int32_t* slot_epoch;         // [n_tslots] last iteration epoch that used the slot
   int32_t* fill;               // [n_tslots] slots to (re)compute this iteration, count in ctrl[3]
+  int32_t* fill_by;            // [n_tslots] active index of the CTA that refills the slot (prep_iter_kernel)
+  int32_t* fill_ep;            // [n_tslots] epoch in which the slot is refilled
+  int32_t* slot_ready;         // [n_tslots] epoch stamp released once the slot's tables are written
+  int32_t* assign_ready;       // [1] epoch stamp released after the slot assignment
   // stall fallback (reading R23): level 0 = the plan's own tilts and E, levels 1.. = fallback tilts
   int32_t n_levels, lvl_tmax;  // levels, tilt slots per level
   const int64_t* lvl_E;        // [n_levels]
@@ -268,6 +272,8 @@ cudaError_t fft_prof_read(unsigned long long* out, bool reset);   // tuning buil
 // per iteration: assign table slots to the active signals' primes (fills counted in ctrl[3]), compute the
 // tables of new primes (grid n_signals, CTAs beyond the fill count exit; direct = stage entry point: fill the
 // slot of every listed signal), then the per-signal term phases u_j / e_j and FFT size index
+// the per-iteration table prep in one launch (slot assignment, fills of new primes, terms; prep_iter_kernel)
+cudaError_t launch_prep_iter(const DevParams& P, int32_t n_bound, int32_t smem_bytes, cudaStream_t st, int32_t epoch);
 cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_bytes, int32_t threads, int32_t big,
                             cudaStream_t st, int32_t epoch, bool direct = false);
 // threads per FFT CTA for a size (more CTAs per SM for small M)
