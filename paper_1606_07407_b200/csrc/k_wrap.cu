@@ -67,8 +67,8 @@ __global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm,
   const int nR = P.st_nR[s];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
   const int64_t h2 = P.N / 2;
-  for (int i = tid; i < nch * nR; i += blockDim.x) {
-    const int c = i / nR, e = i - c * nR;
+  for (int i = tid; i < nch * nR; i += blockDim.x) {         // chunk index fastest: coalesced row reads
+    const int e = i / nch, c = i - e * nch;
     const int32_t* row = wt + (int64_t)e * P.d;
     unsigned long long kv = 0;
     for (int t = 0; t < per; ++t) {
