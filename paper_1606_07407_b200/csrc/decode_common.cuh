@@ -43,20 +43,22 @@ __device__ int select_candidates(F0 f0, int p, int kstar, double floor_abs, int*
                                  int* scratch) {
   const int tid = threadIdx.x;
   int total = 0;
-  for (int b0 = 0; b0 < p; b0 += blockDim.x) {
-    const int b = b0 + tid;
-    double mg = 0.0;
-    bool fl = false;
-    if (b < p) {
-      const double2 f = f0(b);
-      mg = hypot(f.x, f.y);
-      fl = mg >= floor_abs;
-    }
-    int round_total;
-    const int pos = block_excl_scan(fl ? 1 : 0, scratch, &round_total);
-    if (fl) { cand[total + pos] = b; mag[total + pos] = mg; }
-    total += round_total;
+  // thread t owns the contiguous bins [t per, (t + 1) per): flags in a register mask, one block scan
+  const int per = (p + blockDim.x - 1) / blockDim.x;     // <= 32
+  const int b0 = tid * per, b1 = min(p, b0 + per);
+  unsigned mask = 0u;
+  for (int b = b0; b < b1; ++b) {
+    const double2 f = f0(b);
+    if (hypot(f.x, f.y) >= floor_abs) mask |= 1u << (b - b0);
   }
+  int pos = block_excl_scan(__popc(mask), scratch, &total);
+  for (int b = b0; b < b1; ++b)
+    if (mask >> (b - b0) & 1u) {
+      const double2 f = f0(b);
+      cand[pos] = b;
+      mag[pos] = hypot(f.x, f.y);
+      ++pos;
+    }
   __syncthreads();
   int nc = total;
   if (nc > kstar) {
@@ -68,8 +70,8 @@ __device__ int select_candidates(F0 f0, int p, int kstar, double floor_abs, int*
       flag[i] = rank < kstar;
     }
     __syncthreads();
-    const int per = (nc + blockDim.x - 1) / blockDim.x;
-    const int i0 = tid * per, i1 = min(nc, i0 + per);
+    const int per2 = (nc + blockDim.x - 1) / blockDim.x;
+    const int i0 = tid * per2, i1 = min(nc, i0 + per2);
     int c2 = 0, keep_b[32], nk = 0;
     for (int i = i0; i < i1; ++i) c2 += flag[i];
     const int pos2 = block_excl_scan(c2, scratch, &total);

@@ -270,8 +270,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
     n_new = total;
     for (int t = t0; t < t1; ++t) {
       const int ci = accl[t];
-      const int b = cand[ci];
-      const double2 f0 = F[b];
+      const double2 f0 = P.rec_f0[(int64_t)s * P.k + ci];   // F_0 at the candidate (the FFT's line-0 CTA)
       const double2 a = make_double2(f0.x / (double)p, f0.y / (double)p);    // Eq. (7): a = F_0 / p
       if (found[t] >= 0) {
         const int e = found[t];

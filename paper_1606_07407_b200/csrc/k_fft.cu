@@ -748,9 +748,9 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
 }
 
 // ---- fused decode epilogue: no HBM round trip of the lines n >= 1 ----
-// line-0 CTA: F_0[b] = chirp[b] conv[b] + registry bins (reading R21), written to the line (the commit reads
-// a = F_0[b] / p) and kept in shared memory; select (a5) the candidates, publish them with F_0 at the
-// candidates and pass flags = 1, then release sel_ready[s] = it_epoch
+// line-0 CTA: F_0[b] = chirp[b] conv[b] + registry bins (reading R21), kept in shared memory; select (a5) the
+// candidates, publish them with F_0 at the candidates (the commit's a = F_0[b] / p) and pass flags = 1, then
+// release sel_ready[s] = it_epoch
 __device__ void fused_select(const DevParams& P, int s, int p, double2* x, const double2* __restrict__ ch,
                              double2* line) {
   const int tid = threadIdx.x;
@@ -774,7 +774,6 @@ __device__ void fused_select(const DevParams& P, int s, int p, double2* x, const
         double2 f = cmulx(x[b], c[u]);
         if (resid) f = add_bin_residual(f, bstart, border, Creg, P.Lp, 0, b, pd);
         x[b] = f;
-        line[b] = f;
       }
     }
   }
