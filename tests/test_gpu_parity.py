@@ -531,3 +531,21 @@ def test_table_cache_reuse_bitwise(S, name, trials):
         assert torch.equal(r.freqs, r1.freqs)
         assert torch.equal(torch.view_as_real(r.coeffs), torch.view_as_real(r1.coeffs))
     assert r1.report.samples_used == r2.report.samples_used == r0.report.samples_used
+
+
+@pytest.mark.parametrize("name,trials,G", [("c2", range(4), 2), ("c5", [0], 3)])
+def test_e2e_line_shards_literal_residual(S, name, trials, G):
+    """Line shards with the literal residual (registry terms sampled on every line, FP64 exp-sum)."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    plans = _shard_plans(S, c, G, batch=len(trials), literal_residual=True)
+    res = _group_solve(S, plans, w, a)
+    for i, t in enumerate(trials):
+        key = f"primary_{t}"
+        n = int(res.count[i])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        ra = g[key + "_a"]
+        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
