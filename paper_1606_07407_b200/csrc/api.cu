@@ -388,7 +388,6 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.line_lo = P->line_lo;
   D.line_G = std::max(P->line_G, 1);
   D.line_g = P->line_g;
-  D.line_split = P->line_G > 0;
   D.rec_words = P->rec_words;
   D.rec_fw = P->rec_fw;
   D.rec_send = ptr<int64_t>(P, B_RSEND);

@@ -17,7 +17,6 @@ namespace sfft {
 enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK, 1 PARTIAL, <0 error)
 
 constexpr int kMaxFftPasses = 24;
-constexpr int kFftThreads = 512;
 constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
 
@@ -124,7 +123,6 @@ struct DevParams {
   // [line_lo, line_lo + L - 1); its decode is split into a local test (records) and a commit after the
   // all-gather of the records.  Unsharded plans: line_G = 1, line_lo = 0, L = r + 1, no records.
   int32_t line_lo, line_G, line_g;
-  int32_t line_split;          // 1: two-phase decode (records + exchange + commit), also at line_G = 1
   int32_t rec_words;           // int64 words per signal record: rec_fw flag words (int32 pairs) + (Lmax - 1) k coordinates
   int32_t rec_fw;              // (k + 1) / 2
   int64_t* rec_send;           // [batch][rec_words] this shard's records
