@@ -1,6 +1,7 @@
 // api.cu -- the C ABI (include/sfft.h): plan, workspace, the host-side
 // iteration driver of Algorithm 2 and the stage entry points.
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
@@ -96,7 +97,9 @@ struct sfft_plan_s {
   bool ws_owned = false;
   bool tables_ready = false;
   size_t off[128] = {0};        // workspace offsets, indexed by Buf (static_assert below)
-  int32_t* h_ctrl = nullptr;   // pinned
+  int32_t* h_ctrl = nullptr;   // pinned, host-mapped: setup_kernel publishes the iteration's control values here
+  int32_t* h_ctrl_dev = nullptr;   // its device address
+  int32_t ctrl_seq = 0;
   bool profile = false;
   int32_t literal = 0;
   std::vector<cudaEvent_t> events;
@@ -235,7 +238,7 @@ void layout(sfft_plan_t* P) {
   sz[B_SAMPLES] = 8 * S;
   sz[B_CMACS] = 8 * S;
   sz[B_LOG] = 4 * 2 * kLogIters;
-  sz[B_CTRL] = 16;
+  sz[B_CTRL] = 32;
   sz[B_IN_F] = 4 * S * P->k * P->d;
   sz[B_IN_C] = 16 * S * P->k;
   sz[B_OUT_F] = 4 * S * P->k * P->d;
@@ -349,6 +352,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_cmacs_i8 = ptr<int64_t>(P, B_CMACS8);
   D.st_log = ptr<int32_t>(P, B_LOG);
   D.ctrl = ptr<int32_t>(P, B_CTRL);
+  D.h_ctrl_map = P->h_ctrl_dev;
   D.active = ptr<int32_t>(P, B_ACTIVE);
   D.n_levels = P->n_levels;
   D.lvl_tmax = P->lvl_tmax;
@@ -416,7 +420,11 @@ int ensure_ready(sfft_plan_t* P) {
     P->ws_owned = true;
     P->tables_ready = false;
   }
-  if (!P->h_ctrl) CUDA_TRY(P, cudaMallocHost(&P->h_ctrl, 64));
+  if (!P->h_ctrl) {
+    CUDA_TRY(P, cudaHostAlloc(reinterpret_cast<void**>(&P->h_ctrl), 64, cudaHostAllocMapped));
+    memset(P->h_ctrl, 0, 64);
+    CUDA_TRY(P, cudaHostGetDevicePointer(reinterpret_cast<void**>(&P->h_ctrl_dev), P->h_ctrl, 0));
+  }
   if (!P->ev_ctrl) CUDA_TRY(P, cudaEventCreateWithFlags(&P->ev_ctrl, cudaEventDisableTiming));
   if (!P->tables_ready) {
     std::vector<int32_t> fm, fn;
@@ -529,9 +537,8 @@ int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& lau
 
 int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launches, int n_bound) {
   cudaStream_t st = P->stream;
-  LAUNCH(P, launch_setup(D, iter, st));
-  CUDA_TRY(P, cudaMemcpyAsync(P->h_ctrl, D.ctrl, 16, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(P, cudaEventRecord(P->ev_ctrl, st));
+  const int32_t seq = ++P->ctrl_seq;
+  LAUNCH(P, launch_setup(D, iter, st, seq));
   // the table prep needs no host decision: it is enqueued before the control read returns, sized for the
   // previous iteration's active count and the largest FFT size (CTAs beyond the device-side counts exit), so
   // the host round trip overlaps it
@@ -546,7 +553,19 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
       launches += 2;   // tables_assign, terms
     }
   }
-  CUDA_TRY(P, cudaEventSynchronize(P->ev_ctrl));
+  // poll the host-mapped control block (published by setup's last CTA); a fault surfaces through the stream
+  {
+    volatile int32_t* hc = P->h_ctrl;
+    long spins = 0;
+    while (hc[3] != seq) {
+      if ((++spins & 1023) == 0) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaSuccess && q != cudaErrorNotReady) return fail(P, SFFT_ECUDA, "setup: %s", cudaGetErrorString(q));
+        if (q == cudaSuccess && hc[3] != seq) return fail(P, SFFT_ECUDA, "setup: control block not published");
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+  }
   it->n_active = P->h_ctrl[0];
   it->max_p = P->h_ctrl[1];
   if (it->n_active == 0) return SFFT_OK;

@@ -30,33 +30,50 @@ __device__ int ith_prime_at_least(const DevParams& P, int x, int i) {
   return idx < P.n_primes ? P.primes[idx] : -1;
 }
 
-__global__ void setup_kernel(DevParams P, int32_t iter) {
+__global__ void setup_kernel(DevParams P, int32_t iter, int32_t seq) {
   pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= P.batch || P.st_status[s] != ST_RUN) return;
-  const int nR = P.st_nR[s];
-  const int kstar = P.k - nR;
-  P.st_retilt[s] = 0;
-  const int il = P.st_il[s] + 1;                           // counter of the current level (= iter without a switch)
-  P.st_il[s] = il;
-  int p;
-  if (P.n_sched > 0) p = (int)P.sched[(il - 1) % P.n_sched];
-  else p = ith_prime_at_least(P, P.c * kstar, il);
-  if (p < 2 || p > P.p_cap) {
-    P.st_status[s] = SFFT_ENOTSUP;
-    return;
+  if (s < P.batch && P.st_status[s] == ST_RUN) {
+    const int nR = P.st_nR[s];
+    const int kstar = P.k - nR;
+    P.st_retilt[s] = 0;
+    const int il = P.st_il[s] + 1;                         // counter of the current level (= iter without a switch)
+    P.st_il[s] = il;
+    int p;
+    if (P.n_sched > 0) p = (int)P.sched[(il - 1) % P.n_sched];
+    else p = ith_prime_at_least(P, P.c * kstar, il);
+    if (p < 2 || p > P.p_cap) {
+      P.st_status[s] = SFFT_ENOTSUP;
+    } else {
+      P.st_p[s] = p;
+      P.st_m[s] = il % P.r;
+      P.active[atomicAdd(&P.ctrl[0], 1)] = s;
+      atomicMax(&P.ctrl[1], p);
+      atomicMax(&P.ctrl[2], P.k + (P.literal ? nR : 0));  // terms the exp-sum sums
+    }
   }
-  P.st_p[s] = p;
-  P.st_m[s] = il % P.r;
-  P.active[atomicAdd(&P.ctrl[0], 1)] = s;
-  atomicMax(&P.ctrl[1], p);
-  atomicMax(&P.ctrl[2], P.k + (P.literal ? nR : 0));        // terms the exp-sum sums
+  // the last CTA publishes (n_active, max p, max K, seq) to the host-mapped control block: the host polls it
+  // instead of a device-to-host copy and an event
+  if (P.h_ctrl_map == nullptr) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&P.ctrl[4], 1) == (int)gridDim.x - 1) {
+      volatile int32_t* c = P.ctrl;
+      volatile int32_t* h = P.h_ctrl_map;
+      h[0] = c[0];
+      h[1] = c[1];
+      h[2] = c[2];
+      __threadfence_system();
+      h[3] = seq;
+    }
+  }
 }
 
-cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(P.ctrl, 0, sizeof(int32_t) * 4, st);
+cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st, int32_t seq) {
+  cudaError_t e = cudaMemsetAsync(P.ctrl, 0, sizeof(int32_t) * 8, st);
   if (e != cudaSuccess) return e;
-  return launch_pdl(setup_kernel, dim3((P.batch + 255) / 256), dim3(256), 0, st, P, iter);
+  return launch_pdl(setup_kernel, dim3((P.batch + 255) / 256), dim3(256), 0, st, P, iter, seq);
 }
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {

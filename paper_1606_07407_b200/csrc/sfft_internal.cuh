@@ -77,7 +77,8 @@ struct DevParams {
   int64_t* st_cmacs_i8;        // [batch] cMACs of the iterations whose exp-sum ran on the int8-limb kernel
   int32_t i8_iter;             // decode launch: this iteration's exp-sum used the int8-limb kernel
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
-  int32_t* ctrl;               // [4]: n_active, max_p, max_K, flags
+  int32_t* ctrl;               // [8]: n_active, max_p, max_K, fills, setup CTAs done
+  int32_t* h_ctrl_map;         // host-mapped [4]: n_active, max_p, max_K, sequence (setup_kernel publishes)
   int32_t* active;             // [batch] indices of the signals still running this iteration
   // per-prime tables (W_tab, chirp, V, int8 root tables) live in a cache of slots keyed by p: they depend on p
   // only, like FFT twiddles; slot n_tslots is reserved for the stage entry points
@@ -230,7 +231,7 @@ cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* fre
                            cudaStream_t st);
 cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, cudaStream_t st);
 // k_decode.cu
-cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st);
+cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st, int32_t seq = 0);
 // commit of an iteration: the records of the fused FFT epilogue (all line shards) -> registry update, state
 cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st);
 // re-projection of the signals that switched fallback level (reading R23); freqs = the execute's input
