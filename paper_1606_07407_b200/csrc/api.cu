@@ -238,7 +238,7 @@ void layout(sfft_plan_t* P) {
   sz[B_SAMPLES] = 8 * S;
   sz[B_CMACS] = 8 * S;
   sz[B_LOG] = 4 * 2 * kLogIters;
-  sz[B_CTRL] = 32;
+  sz[B_CTRL] = 64;                              // two alternating control blocks of 8 ints
   sz[B_IN_F] = 4 * S * P->k * P->d;
   sz[B_IN_C] = 16 * S * P->k;
   sz[B_OUT_F] = 4 * S * P->k * P->d;
@@ -526,6 +526,7 @@ struct IterPlan {
 // a1 (projection, term rows) and the int8 limbs of the signal terms, once per solve
 int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& launches) {
   cudaStream_t st = P->stream;
+  CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_CTRL), 0, 64, st));   // both control blocks
   LAUNCH(P, launch_project(D, sig->batch, sig->freqs, sig->coeffs, st));
   launches += 1;   // init_state_kernel
   if (P->i8_ok) {
@@ -538,6 +539,8 @@ int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& lau
 int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launches, int n_bound) {
   cudaStream_t st = P->stream;
   const int32_t seq = ++P->ctrl_seq;
+  D.ctrl = ptr<int32_t>(P, B_CTRL) + 8 * (seq & 1);
+  D.ctrl_next = ptr<int32_t>(P, B_CTRL) + 8 * ((seq + 1) & 1);
   LAUNCH(P, launch_setup(D, iter, st, seq));
   // the table prep needs no host decision: it is enqueued before the control read returns, sized for the
   // previous iteration's active count and the largest FFT size (CTAs beyond the device-side counts exit), so

@@ -70,9 +70,8 @@ __global__ void setup_kernel(DevParams P, int32_t iter, int32_t seq) {
   }
 }
 
+// P.ctrl must be zero: it alternates between two blocks, the previous iteration's prep kernel cleared this one
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st, int32_t seq) {
-  cudaError_t e = cudaMemsetAsync(P.ctrl, 0, sizeof(int32_t) * 8, st);
-  if (e != cudaSuccess) return e;
   return launch_pdl(setup_kernel, dim3((P.batch + 255) / 256), dim3(256), 0, st, P, iter, seq);
 }
 

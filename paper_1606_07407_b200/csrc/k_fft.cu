@@ -488,6 +488,7 @@ __device__ void assign_slots(const DevParams& P, int32_t epoch, int* sm, bool fi
   int* hfill = ep + C;                               // [2048] lowest active index using the missing prime
   __shared__ int n_miss, n_free;
   const int n_active = P.ctrl[0];
+  if (P.ctrl_next && threadIdx.x < 8) P.ctrl_next[threadIdx.x] = 0;   // the next iteration's control block
   for (int i = threadIdx.x; i < HS; i += blockDim.x) mk[i] = 0;
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) { hkey[i] = 0; hfill[i] = 0x7fffffff; }
   if (threadIdx.x == 0) { n_miss = 0; n_free = 0; }

@@ -77,7 +77,8 @@ struct DevParams {
   int64_t* st_cmacs_i8;        // [batch] cMACs of the iterations whose exp-sum ran on the int8-limb kernel
   int32_t i8_iter;             // decode launch: this iteration's exp-sum used the int8-limb kernel
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
-  int32_t* ctrl;               // [8]: n_active, max_p, max_K, fills, setup CTAs done
+  int32_t* ctrl;               // [8]: n_active, max_p, max_K, fills, setup CTAs done (this iteration's block)
+  int32_t* ctrl_next;          // [8]: the next iteration's block, cleared by the table prep
   int32_t* h_ctrl_map;         // host-mapped [4]: n_active, max_p, max_K, sequence (setup_kernel publishes)
   int32_t* active;             // [batch] indices of the signals still running this iteration
   // per-prime tables (W_tab, chirp, V, int8 root tables) live in a cache of slots keyed by p: they depend on p
