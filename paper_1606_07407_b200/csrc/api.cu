@@ -122,7 +122,7 @@ enum Buf {
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
-  B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY,
+  B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY, B_SPINERR,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -275,6 +275,7 @@ void layout(sfft_plan_t* P) {
   sz[B_FILLEP] = 4 * T;
   sz[B_SLOTRDY] = 4 * T;
   sz[B_ASGRDY] = 4;
+  sz[B_SPINERR] = 4;
   sz[B_I8TLO] = P->i8_ok ? 8 * T * (2 * P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
   // decode records (fused FFT epilogue -> commit); line shards also receive every shard's records
@@ -374,6 +375,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.fill_ep = ptr<int32_t>(P, B_FILLEP);
   D.slot_ready = ptr<int32_t>(P, B_SLOTRDY);
   D.assign_ready = ptr<int32_t>(P, B_ASGRDY);
+  D.spin_err = ptr<int32_t>(P, B_SPINERR);
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
@@ -527,6 +529,7 @@ struct IterPlan {
 int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& launches) {
   cudaStream_t st = P->stream;
   CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_CTRL), 0, 64, st));   // both control blocks
+  CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SPINERR), 0, 4, st));
   LAUNCH(P, launch_project(D, sig->batch, sig->freqs, sig->coeffs, st));
   launches += 1;   // init_state_kernel
   if (P->i8_ok) {
@@ -642,7 +645,9 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
                  int32_t last_iter, int launches, int32_t n_expsum, int32_t n_expsum_i8, int* worst_out) {
   cudaStream_t st = P->stream;
   std::vector<int32_t> hs(batch);
+  int32_t spin_err = 0;
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(P, cudaMemcpyAsync(&spin_err, D.spin_err, 4, cudaMemcpyDeviceToHost, st));
   std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
   std::vector<int32_t> hlog(2 * kLogIters);
   if (rep) {
@@ -652,6 +657,7 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
     CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
   }
   CUDA_TRY(P, cudaStreamSynchronize(st));
+  if (spin_err) return fail(P, SFFT_ECUDA, "a cross-CTA stamp wait timed out (block scheduling assumption)");
   int worst = SFFT_OK, n_ok = 0, n_part = 0, n_err = 0;
   for (int s = 0; s < batch; ++s) {
     const int v = hs[s];

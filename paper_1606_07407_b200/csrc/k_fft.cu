@@ -466,6 +466,29 @@ __device__ void i8_log_tables(const DevParams& P, int slot, int p) {
   }
 }
 
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// spin until *flag == v; after 2 s (the scheduling assumption failed) flag the plan's error word and go on
+// instead of hanging the GPU -- the execute then fails with SFFT_ECUDA
+__device__ __forceinline__ void wait_stamp(const int32_t* flag, int32_t v, int32_t* err, int ns = 64) {
+  int got;
+  long long t0 = 0;
+  for (int it = 0;; ++it) {
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(flag) : "memory");
+    if (got == v) return;
+    if ((it & 255) == 0) {
+      const long long t = global_ns();
+      if (it == 0) t0 = t;
+      else if (t - t0 > 2000000000ll) { atomicExch(err, 1); return; }
+    }
+    __nanosleep(ns);
+  }
+}
+
+
 // ---- table cache: slot assignment (one CTA) ----
 // Hits reuse their slot; the distinct missing primes get slots not used in this epoch (at most n_active slots
 // are in use, the cache has n_active + 16 or more), which are queued in fill[] for tables_fill.  The primes of
@@ -705,14 +728,6 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams
 // (lowest active index using the prime) and releases the slot's stamp, or waits for that stamp (the filler
 // has a lower block index: resident or finished -- the decoupled look-back progress argument); then the
 // signal's terms.  Replaces tables_assign + fft_prep + terms launches.
-__device__ __forceinline__ void wait_stamp(const int32_t* flag, int32_t v) {
-  int got;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(flag) : "memory");
-    if (got == v) return;
-    __nanosleep(64);
-  }
-}
 __device__ __forceinline__ void release_stamp(int32_t* flag, int32_t v) {
   __threadfence();
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(flag), "r"(v) : "memory");
@@ -728,7 +743,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
     __syncthreads();
     if (threadIdx.x == 0) release_stamp(P.assign_ready, epoch);
   } else if (threadIdx.x == 0) {
-    wait_stamp(P.assign_ready, epoch);
+    wait_stamp(P.assign_ready, epoch, P.spin_err);
   }
   __syncthreads();
   const int a = blockIdx.x;
@@ -741,12 +756,13 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
       __syncthreads();
       if (threadIdx.x == 0) release_stamp(P.slot_ready + slot, epoch);
     } else if (threadIdx.x == 0) {
-      wait_stamp(P.slot_ready + slot, epoch);
+      wait_stamp(P.slot_ready + slot, epoch, P.spin_err);
     }
     __syncthreads();
   }
   terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch);
 }
+
 
 // ---- fused decode epilogue: no HBM round trip of the lines n >= 1 ----
 // line-0 CTA: F_0[b] = chirp[b] conv[b] + registry bins (reading R21), kept in shared memory; select (a5) the
@@ -807,12 +823,7 @@ __device__ void fused_select(const DevParams& P, int s, int p, double2* x, const
 __device__ void fused_test(const DevParams& P, int s, int p, int n, const double2* x, const double2* __restrict__ ch) {
   const int tid = threadIdx.x;
   if (tid == 0) {
-    int v;
-    for (;;) {
-      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(P.sel_ready + s) : "memory");
-      if (v == P.it_epoch) break;
-      __nanosleep(256);
-    }
+    wait_stamp(P.sel_ready + s, P.it_epoch, P.spin_err, 256);
   }
   __syncthreads();
   const int nR = P.st_nR[s];

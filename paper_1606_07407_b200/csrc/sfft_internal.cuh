@@ -92,6 +92,7 @@ struct DevParams {
   int32_t* fill_ep;            // [n_tslots] epoch in which the slot is refilled
   int32_t* slot_ready;         // [n_tslots] epoch stamp released once the slot's tables are written
   int32_t* assign_ready;       // [1] epoch stamp released after the slot assignment
+  int32_t* spin_err;           // [1] set when a stamp wait timed out (the execute fails instead of hanging)
   // stall fallback (reading R23): level 0 = the plan's own tilts and E, levels 1.. = fallback tilts
   int32_t n_levels, lvl_tmax;  // levels, tilt slots per level
   const int64_t* lvl_E;        // [n_levels]
