@@ -2,6 +2,7 @@
 // iteration driver of Algorithm 2 and the stage entry points.
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
@@ -563,11 +564,15 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
   {
     volatile int32_t* hc = P->h_ctrl;
     long spins = 0;
+    std::chrono::steady_clock::time_point t0;
     while (hc[3] != seq) {
       if ((++spins & 1023) == 0) {
         const cudaError_t q = cudaStreamQuery(st);
         if (q != cudaSuccess && q != cudaErrorNotReady) return fail(P, SFFT_ECUDA, "setup: %s", cudaGetErrorString(q));
         if (q == cudaSuccess && hc[3] != seq) return fail(P, SFFT_ECUDA, "setup: control block not published");
+        if (spins == 1024) t0 = std::chrono::steady_clock::now();
+        else if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
+          return fail(P, SFFT_ECUDA, "setup: no control block after 120 s");
       }
     }
     std::atomic_thread_fence(std::memory_order_acquire);
