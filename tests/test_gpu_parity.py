@@ -549,3 +549,20 @@ def test_e2e_line_shards_literal_residual(S, name, trials, G):
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ra = g[key + "_a"]
         assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+
+
+@pytest.mark.parametrize("path", [0, 1])
+def test_e2e_max_fft_size_vs_oracle(S, path):
+    """Maximum sizes: k = p_max // 5 makes the first prime the largest one the plan supports (its Bluestein
+    size is the largest FFT that fits a CTA's shared memory); both exp-sum paths, against the oracle."""
+    probe = _plan(S, W.custom_config(10, 65536, 4, (2, 2, 2, 2, 2), cfg=70))
+    k = probe.p_max // 5
+    c = W.custom_config(10, 65536, k, (2, 2, 2, 2, 2), cfg=70)
+    plan = _plan(S, c, batch=2, expsum_path=path)
+    w, a = W.make_batch(c, [0, 1])
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    assert probe.p_max - 5 <= res.report.primes[0] <= probe.p_max
+    for i in range(2):
+        ref = O.solve(O.params_for(c), w[i], a[i])
+        _check_against_oracle(res, i, ref.w, ref.a, ref.status)
+        assert ref.status == O.OK
