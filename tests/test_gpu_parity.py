@@ -566,3 +566,22 @@ def test_e2e_max_fft_size_vs_oracle(S, path):
         ref = O.solve(O.params_for(c), w[i], a[i])
         _check_against_oracle(res, i, ref.w, ref.a, ref.status)
         assert ref.status == O.OK
+
+
+def test_e2e_degenerate_zero_coefficients(S):
+    """Degenerate inputs: modes with a zero coefficient are invisible, so |R| never reaches k and the solve
+    ends by the stall rule with PARTIAL; all-zero signal (nothing to find).  GPU == oracle (sets, status)."""
+    c = W.custom_config(3, 4096, 40, (2, 1), cfg=71)
+    w, a = W.make_batch(c, [0, 1, 2])
+    a = a.copy()
+    a[0, [3, 17, 29]] = 0.0              # three silent modes
+    a[1, :] = 0.0                        # nothing at all
+    plan = _plan(S, c, batch=3)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    P = O.params_for(c)
+    for i in range(3):
+        ref = O.solve(P, w[i], a[i])
+        _check_against_oracle(res, i, ref.w, ref.a, ref.status)
+    assert int(res.per_status[0]) == O.PARTIAL and int(res.count[0]) == 37
+    assert int(res.per_status[1]) == O.PARTIAL and int(res.count[1]) == 0
+    assert int(res.per_status[2]) == O.OK
