@@ -104,6 +104,8 @@ typedef struct {
   int32_t i8_limbs, n_expsum_i8;
   int64_t cmacs_i8;
   float ms_expsum_i8;
+  int32_t fallback_used;       /* signals that switched to a tilt level of the stall fallback (R23) */
+  float ms_total;              /* when profiling: device time of the whole execute (CUDA events) */
 } sfft_report;
 
 typedef struct sfft_plan_s sfft_plan_t;

@@ -654,8 +654,9 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(P, cudaMemcpyAsync(&spin_err, D.spin_err, 4, cudaMemcpyDeviceToHost, st));
   std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
-  std::vector<int32_t> hlog(2 * kLogIters);
+  std::vector<int32_t> hlog(2 * kLogIters), hlvl(batch);
   if (rep) {
+    CUDA_TRY(P, cudaMemcpyAsync(hlvl.data(), D.st_lvl, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
@@ -673,7 +674,12 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   *worst_out = worst;
   if (rep) {
     memset(rep, 0, sizeof *rep);
-    for (int s = 0; s < batch; ++s) { rep->samples_used += hsamp[s]; rep->cmacs += hcm[s]; rep->cmacs_i8 += hcm8[s]; }
+    for (int s = 0; s < batch; ++s) {
+      rep->samples_used += hsamp[s];
+      rep->cmacs += hcm[s];
+      rep->cmacs_i8 += hcm8[s];
+      rep->fallback_used += hlvl[s] > 0;
+    }
     rep->i8_limbs = P->i8_ok ? P->i8.S : 0;
     rep->n_expsum_i8 = n_expsum_i8;
     rep->iterations = last_iter;
@@ -1130,6 +1136,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     rep->ms_fft = ff;
     rep->ms_decode = fd;
     rep->ms_other = tot - fx - ff - fd;
+    rep->ms_total = tot;
   }
   return worst;
 }

@@ -389,6 +389,10 @@ def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trial
             wc, _ = W.canonical_sort(w[i], a[i])
             assert np.array_equal(ref.w, wc)
     assert res.report.samples_used == samples
+    if n_fb == 0:
+        assert res.report.fallback_used == 0
+    elif structure == "rectangles":                       # rectangles never resolve untilted
+        assert 0 < res.report.fallback_used <= len(used)
 
 
 def test_e2e_cta_pair_mode(S):
