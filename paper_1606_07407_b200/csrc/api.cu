@@ -508,8 +508,11 @@ int i8_ksplit(const sfft_plan_t* P, int max_p, int n_active) {
   double best = 1e30;
   for (int ks = 1; ks <= ks_max; ++ks) {
     if (ks > 1 && (size_t)ks * n_active * P->L_ref * (size_t)max_p * 16 > kPartBytes) break;
+    // a tile's epilogue (accumulator drain + stores, ~10 % of a full-K tile, measured with SFFT_I8_PROF) does
+    // not shrink with its K range; splits also write ks partial lines that the FFT sums
+    static const double e = getenv("SFFT_I8_EPI") ? atof(getenv("SFFT_I8_EPI")) : 0.10;
     const double waves = std::ceil((double)blocks * ks / W);
-    const double t = waves / ks * (ks > 1 ? 1.03 : 1.0) + 0.02 * ks;   // per-CTA prologue (tables)
+    const double t = waves * (1.0 / ks + e) * (ks > 1 ? 1.03 : 1.0) + 0.02 * ks;
     if (t < best - 1e-9) { best = t; ksplit = ks; }
   }
   return ksplit;
