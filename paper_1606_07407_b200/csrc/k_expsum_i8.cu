@@ -651,8 +651,10 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   const long tiles = (long)n_signals * A.n_htiles * c.ntiles * ksplit;
   int n_sm = 148;
   cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, 0);
-  A.chunk = getenv("SFFT_I8_CHUNK") ? std::max(1, atoi(getenv("SFFT_I8_CHUNK"))) : 4;
   const long units = pair ? n_sm / 2 : n_sm;                            // persistent CTAs (pairs)
+  // chunks of consecutive tiles per CTA visit keep a signal's root table in the CTA (measured, C3 / C4 / C5:
+  // 2 tiles when the columns span several n-tiles, one tile otherwise; 4 and more lengthen the tail)
+  A.chunk = getenv("SFFT_I8_CHUNK") ? std::max(1, atoi(getenv("SFFT_I8_CHUNK"))) : (c.ntiles >= 2 ? 2 : 1);
   const long grid = std::min<long>((tiles + A.chunk - 1) / A.chunk, units) * (pair ? 2 : 1);
   if (grid > 0) {
     cudaLaunchConfig_t cfg = {};
