@@ -604,8 +604,9 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
     double best = 1e30;
     for (int ks = 1; ks <= ks_max; ++ks) {
       if (ks > 1 && (size_t)ks * it->n_active * P->L_ref * (size_t)it->max_p * 16 > kPartBytes) break;
+      static const double e = getenv("SFFT_FP64_EPI") ? atof(getenv("SFFT_FP64_EPI")) : 0.0;
       const double waves = std::ceil((double)blocks * ks / W);
-      const double t = waves / ks * (ks > 1 ? 1.03 : 1.0);
+      const double t = waves * (1.0 / ks + e) * (ks > 1 ? 1.03 : 1.0);
       if (t < best - 1e-9) { best = t; it->ksplit = ks; }
     }
   }
