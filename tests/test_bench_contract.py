@@ -48,3 +48,15 @@ def test_our_arm_c1():
     assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
     assert d["gpu_launches"] > 0
     assert d["latency_single_solve"]["exact"] is True
+
+
+@pytest.mark.gpu
+def test_our_arm_line_shards_c3_world1():
+    """--shard lines at one rank: the plan is a line shard with the NCCL record all-gather (world 1)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    d = _run(["--config", "c3", "--shard", "lines", "--steps", "2", "--warmup", "3", "--e2e-steps", "1",
+              "--latency-steps", "0", "--no-cpu-baseline", "--batch", "4"])
+    assert d["scaling"] == "strong" and d["verified_exact_recovery"] is True
+    assert "line shards x1" in d["config"]["parallelism"]
