@@ -179,16 +179,20 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
       flag[ci] = f;
     }
     __syncthreads();
-    for (int g = 0; g < P.line_G; ++g) {
-      int glo, ghi;
-      line_shard_range(r, P.line_G, g, &glo, &ghi);
-      const int64_t* rv = P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words + P.rec_fw;
-      for (int t = tid; t < (ghi - glo) * nc; t += blockDim.x) {
-        const int nn = t / nc, ci = t - nn * nc;
-        if (flag[ci]) accv[(int64_t)(glo + nn) * P.k + ci] = rv[(int64_t)nn * P.k + ci];
+    if (P.line_G == 1) {
+      // one shard holds every axis: its record already is the [r][k] coordinate array
+      accv = const_cast<int64_t*>(P.rec_recv) + (int64_t)s * P.rec_words + P.rec_fw;   // read-only below
+    } else {
+      for (int g = 0; g < P.line_G; ++g) {
+        int glo, ghi;
+        line_shard_range(r, P.line_G, g, &glo, &ghi);
+        const int64_t* rv = P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words + P.rec_fw;
+        for (int nn = 0; nn < ghi - glo; ++nn)
+          for (int ci = tid; ci < nc; ci += blockDim.x)
+            if (flag[ci]) accv[(int64_t)(glo + nn) * P.k + ci] = rv[(int64_t)nn * P.k + ci];
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   if (P.extra & 2) {
     for (int ci = tid; ci < nc; ci += blockDim.x)
