@@ -629,7 +629,7 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   D.lines_log = it.use_i8 ? 1 : 0;
   D.fuse_decode = 1;
   D.it_epoch = P->epoch;
-  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto), it.big, it.ksplit,
+  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto, (int64_t)it.n_active * P->L), it.big, it.ksplit,
                         ptr<double2>(P, B_PART), it.max_p, st));
   D.lines_log = 0;
   D.fuse_decode = 0;
@@ -1292,7 +1292,7 @@ int sfft_stage_expsum(sfft_plan_t* plan, int32_t K, const int64_t* v, const doub
   rc = set_signal0_state(P, D, (int)p, m, K - P->k);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M, P->fft[fi].smem_upto), P->fft[fi].M >= fft_big_m(),
+  LAUNCH(P, launch_fft_prep(D, 1, (int)P->fft[fi].smem_upto, fft_threads(P->fft[fi].M, P->fft[fi].smem_upto, P->L), P->fft[fi].M >= fft_big_m(),
                             P->stream, 0, true));
   if (P->i8_ok && i8_use_for(P, (int)p)) {
     D.i8_K = K;
@@ -1322,7 +1322,7 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   rc = set_signal0_state(P, D, (int)p, 0, 0);
   if (rc) return rc;
   const int fi = fft_index_host(P, (int)p);
-  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M, P->fft[fi].smem_upto), big = P->fft[fi].M >= fft_big_m();
+  const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M, P->fft[fi].smem_upto, n_lines), big = P->fft[fi].M >= fft_big_m();
   LAUNCH(P, launch_fft_prep(D, 1, sm, th, big, P->stream, 0, true));
   LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, big, 1, nullptr, 0, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));

@@ -6,6 +6,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <string>
 #include <vector>
 
@@ -289,12 +290,17 @@ inline int fft_big_m() {
 }
 // threads per FFT CTA: the 64-register variant fills the SM's 1024-thread register budget with as many CTAs as
 // shared memory allows (1024 / CTAs per SM threads each), but no more threads than ~M/6 butterflies need
-inline int fft_threads(int M, size_t smem) {
+inline int fft_threads(int M, size_t smem, int64_t n_ctas) {
   if (M >= fft_big_m()) return 512;
   const size_t per_sm = 228 * 1024;
   const int ctas = smem * 4 + 4096 <= per_sm ? 4 : smem * 2 + 2048 <= per_sm ? 2 : 1;
   const int cap = getenv("SFFT_FFT_TCAP") ? atoi(getenv("SFFT_FFT_TCAP")) : 1024 / ctas;
-  int t = ((M / 6 + 31) / 32) * 32;
+  // ~M/6 threads; small sizes (M <= 2048) over many lines (>= 4096 CTAs) run better as more, smaller CTAs
+  // per SM: ~M/12 (measured: C4 -6 %, C2 -1 %; with few CTAs, as in C5's later iterations, M/12 is slower)
+  static const int tdiv_env = getenv("SFFT_FFT_TDIV") ? std::max(1, atoi(getenv("SFFT_FFT_TDIV"))) : 0;
+  static const int64_t cta_min = getenv("SFFT_FFT_TDIV_CTAS") ? atoll(getenv("SFFT_FFT_TDIV_CTAS")) : 4096;
+  const int tdiv = tdiv_env ? tdiv_env : (M <= 2048 && n_ctas >= cta_min ? 12 : 6);
+  int t = ((M / tdiv + 31) / 32) * 32;
   return t < 64 ? 64 : (t > cap ? cap : t);
 }
 cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads, int32_t big,
