@@ -75,6 +75,7 @@ struct sfft_plan_s {
   double tol = 1e-6, floor_rel = 1e-8, prune = 1e-8, round_tol = 0.01;
   // tables
   std::vector<int32_t> primes;
+  std::vector<int32_t> prime_tab;   // device copy: the primes, then pfirst[x] = index of the first prime >= x
   int32_t p_cap = 0;
   int64_t p_stride = 0, M_stride = 0;
   std::vector<FftSize> fft;
@@ -218,7 +219,7 @@ void layout(sfft_plan_t* P) {
   sz[B_TILTS] = 8 * std::max<size_t>(P->tilts.size(), 1);
   sz[B_AXT] = 4 * (size_t)P->r;
   sz[B_SCHED] = 8 * std::max<size_t>(P->sched.size(), 1);
-  sz[B_PRIMES] = 4 * P->primes.size();
+  sz[B_PRIMES] = 4 * P->prime_tab.size();
   sz[B_FFTM] = 4 * P->fft.size();
   sz[B_FFTR] = (size_t)kMaxFftPasses * P->fft.size();
   sz[B_FFTN] = 4 * P->fft.size();
@@ -323,6 +324,8 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.sched = ptr<int64_t>(P, B_SCHED);
   D.primes = ptr<int32_t>(P, B_PRIMES);
   D.n_primes = (int32_t)P->primes.size();
+  D.pfirst = D.primes + P->primes.size();
+  D.n_pfirst = (int32_t)(P->prime_tab.size() - P->primes.size());
   D.fft_M = ptr<int32_t>(P, B_FFTM);
   D.fft_radix = ptr<int8_t>(P, B_FFTR);
   D.fft_npass = ptr<int32_t>(P, B_FFTN);
@@ -448,7 +451,7 @@ int ensure_ready(sfft_plan_t* P) {
     CUDA_TRY(P, up(B_TILTS, P->tilts.data(), 8 * P->tilts.size()));
     CUDA_TRY(P, up(B_AXT, P->axis_tilt.data(), 4 * P->axis_tilt.size()));
     CUDA_TRY(P, up(B_SCHED, P->sched.data(), 8 * P->sched.size()));
-    CUDA_TRY(P, up(B_PRIMES, P->primes.data(), 4 * P->primes.size()));
+    CUDA_TRY(P, up(B_PRIMES, P->prime_tab.data(), 4 * P->prime_tab.size()));
     CUDA_TRY(P, up(B_FFTM, fm.data(), 4 * fm.size()));
     CUDA_TRY(P, up(B_FFTR, fr.data(), fr.size()));
     CUDA_TRY(P, up(B_FFTN, fn.data(), 4 * fn.size()));
@@ -962,6 +965,13 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
       for (long y = (long)x * x; y <= lim; y += x) comp[y] = 1;
     }
     P->p_cap = P->primes.back();
+    // the setup kernel's lookup of the i-th prime >= x: two loads instead of a binary search
+    P->prime_tab = P->primes;
+    size_t j = 0;
+    for (int x = 0; x <= lim + 1; ++x) {
+      while (j < P->primes.size() && P->primes[j] < x) ++j;
+      P->prime_tab.push_back((int32_t)j);
+    }
   }
   if (primes && n_primes > 0) {
     for (int i = 0; i < n_primes; ++i) {

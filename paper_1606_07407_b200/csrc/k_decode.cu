@@ -21,12 +21,8 @@ namespace sfft {
 // ------------------------------------------------------------------ setup
 __device__ int ith_prime_at_least(const DevParams& P, int x, int i) {
   if (x < 2) x = 2;
-  int lo = 0, hi = P.n_primes;            // first index with primes[idx] >= x
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (P.primes[mid] >= x) hi = mid; else lo = mid + 1;
-  }
-  const int idx = lo + i - 1;
+  if (x >= P.n_pfirst) return -1;          // beyond the largest prime
+  const int idx = P.pfirst[x] + i - 1;     // first index with primes[idx] >= x, then the i-th
   return idx < P.n_primes ? P.primes[idx] : -1;
 }
 

@@ -604,9 +604,24 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
 
 
 // ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
-// cnt: >= p ints of shared memory; scratch: >= 32 ints
-__device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch) {
+// cnt: >= p + k ints of shared memory; scratch: >= 32 ints.  phases: kTermsU (u_j and the bin sort; needs no
+// table slot) | kTermsE (e_j, from the slot's discrete-log table; alone, it reads back this block's u_j)
+constexpr int kTermsU = 1, kTermsE = 2;
+__device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, int phases = kTermsU | kTermsE) {
   const int p = P.st_p[s];
+  if (!(phases & kTermsU)) {
+    if (P.i8_S <= 0) return;
+    const int K = P.k + P.st_nR[s];
+    const int Kp = (K + 15) & ~15;
+    const int2* ug = P.u_all + (int64_t)s * P.kk;
+    const int64_t base = (int64_t)P.st_slot[s] * P.i8_tstride;
+    int32_t* eg = P.i8_elog + (int64_t)s * P.i8_estride;
+    for (int j = threadIdx.x; j < Kp; j += blockDim.x) {
+      const int u = j < K ? ug[j].x : 0;
+      eg[j] = u ? P.i8_dlog[base + u] : -1;
+    }
+    return;
+  }
   if (threadIdx.x == 0) P.st_M[s] = find_fft_index(P, p);
   const int m = P.st_m[s];
   const int K = P.k + P.st_nR[s];
@@ -614,10 +629,12 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch) {
   int2* ug = P.u_all + (int64_t)s * P.kk;
   const int Kp = (K + 15) & ~15;
   const int64_t base = (int64_t)P.st_slot[s] * P.i8_tstride;
-  int32_t* eg = P.i8_S > 0 ? P.i8_elog + (int64_t)s * P.i8_estride : nullptr;
+  int32_t* eg = P.i8_S > 0 && (phases & kTermsE) ? P.i8_elog + (int64_t)s * P.i8_estride : nullptr;
+  int* ub = cnt + p;                                 // [nR] bins of the registry entries (smem copy)
   for (int j = threadIdx.x; j < (eg ? Kp : K); j += blockDim.x) {
     const int u = j < K ? (int)mod_pos64(vm[j], p) : 0;
     if (j < K) ug[j] = make_int2(u, (8 * u) % p);
+    if (j >= P.k && j < K) ub[j - P.k] = u;
     // e_j: -1 for u_j = 0 and for the padding up to a multiple of 16 (reading R22)
     if (eg) eg[j] = u ? P.i8_dlog[base + u] : -1;
   }
@@ -628,10 +645,9 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch) {
   if (P.literal || nR == 0) return;
   int32_t* bstart = P.bin_start + (int64_t)s * (P.p_stride + 1);
   int32_t* border = P.bin_order + (int64_t)s * P.k;
-  const int2* ur = ug + P.k;
   for (int b = threadIdx.x; b < p; b += blockDim.x) cnt[b] = 0;
-  __syncthreads();                                   // also orders this block's ug writes before the reads below
-  for (int e = threadIdx.x; e < nR; e += blockDim.x) atomicAdd(&cnt[ur[e].x], 1);
+  __syncthreads();
+  for (int e = threadIdx.x; e < nR; e += blockDim.x) atomicAdd(&cnt[ub[e]], 1);
   __syncthreads();
   {
     const int per = (p + blockDim.x - 1) / blockDim.x;
@@ -648,7 +664,7 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch) {
     const int lane = threadIdx.x;
     for (int e0 = 0; e0 < nR; e0 += 32) {
       const int e = e0 + lane;
-      const int b = e < nR ? ur[e].x : -1 - lane;
+      const int b = e < nR ? ub[e] : -1 - lane;
       const unsigned peers = __match_any_sync(0xffffffffu, b);
       const int rank = __popc(peers & ((1u << lane) - 1u));
       int base = 0;
@@ -666,7 +682,7 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch) {
 __global__ void terms_kernel(DevParams P, int32_t direct) {
   pdl_wait();
   if (!direct && (int)blockIdx.x >= P.ctrl[0]) return;   // grid sized before the host read n_active
-  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end
+  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end; [nR] bins
   __shared__ int scratch[32];
   terms_body(P, P.active[blockIdx.x], cnt, scratch);
 }
@@ -738,17 +754,19 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int scratch[32];
-  if (blockIdx.x == 0) {
+  // CTA 0 assigns the slots; meanwhile the others do the slot-independent half of their terms
+  const int a = blockIdx.x;
+  if (a == 0) {
     assign_slots(P, epoch, reinterpret_cast<int*>(smem_raw), true);
     __syncthreads();
     if (threadIdx.x == 0) release_stamp(P.assign_ready, epoch);
-  } else if (threadIdx.x == 0) {
-    wait_stamp(P.assign_ready, epoch, P.spin_err);
+    __syncthreads();
   }
-  __syncthreads();
-  const int a = blockIdx.x;
   if (a >= P.ctrl[0]) return;
   const int s = P.active[a];
+  terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch, kTermsU);
+  if (a > 0 && threadIdx.x == 0) wait_stamp(P.assign_ready, epoch, P.spin_err);
+  __syncthreads();
   const int slot = P.st_slot[s];
   if (P.fill_ep[slot] == epoch) {
     if (P.fill_by[slot] == a) {
@@ -760,7 +778,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
     }
     __syncthreads();
   }
-  terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch);
+  terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch, kTermsE);
 }
 
 
@@ -1008,7 +1026,7 @@ cudaError_t launch_prep_iter(const DevParams& P, int32_t n_bound, int32_t smem_b
   while (hs < 2 * (size_t)P.n_tslots) hs <<= 1;
   const size_t smem = std::max<size_t>((size_t)smem_bytes,
                                        std::max(sizeof(int) * (2 * hs + 2 * 4096 + (size_t)P.n_tslots),
-                                                sizeof(int) * (size_t)P.p_stride));
+                                                sizeof(int) * ((size_t)P.p_stride + P.k)));
   cudaError_t e = ensure_smem(prep_iter_kernel<true>, smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(prep_iter_kernel<true>, dim3(n_bound), dim3(512), smem, st, P, epoch);
@@ -1032,7 +1050,9 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
   if (e != cudaSuccess) return e;
   e = launch_pdl(kern, dim3(n_signals), dim3(threads), smem, st, P, direct ? 1 : 0);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(terms_kernel, dim3(n_signals), dim3(256), sizeof(int) * (size_t)P.p_stride, st, P, direct ? 1 : 0);
+  e = ensure_smem(terms_kernel, sizeof(int) * ((size_t)P.p_stride + P.k));
+  if (e != cudaSuccess) return e;
+  e = launch_pdl(terms_kernel, dim3(n_signals), dim3(256), sizeof(int) * ((size_t)P.p_stride + P.k), st, P, direct ? 1 : 0);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }

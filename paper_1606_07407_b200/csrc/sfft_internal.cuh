@@ -45,6 +45,8 @@ struct DevParams {
   const int64_t* sched;        // [n_sched] explicit primes or null
   const int32_t* primes;       // sorted primes <= p_cap
   int32_t n_primes;
+  const int32_t* pfirst;       // [n_pfirst] index of the first prime >= x (x < n_pfirst; beyond: none)
+  int32_t n_pfirst;
   const int32_t* fft_M;        // [n_fft] allowed Bluestein sizes, ascending
   const int8_t* fft_radix;     // [n_fft][kMaxFftPasses]
   const int32_t* fft_npass;    // [n_fft]
