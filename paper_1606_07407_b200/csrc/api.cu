@@ -277,7 +277,7 @@ void layout(sfft_plan_t* P) {
   sz[B_FILLEP] = 4 * T;
   sz[B_SLOTRDY] = 4 * T;
   sz[B_ASGRDY] = 4;
-  sz[B_SPINERR] = 4;
+  sz[B_SPINERR] = 4 * (1 + S);        // [0] stamp-wait timeout flag, [1 + s] fused-commit arrival counters
   sz[B_I8TLO] = P->i8_ok ? 8 * T * (2 * P->p_stride + 8) : 0;
   sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
   // decode records (fused FFT epilogue -> commit); line shards also receive every shard's records
@@ -380,6 +380,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.slot_ready = ptr<int32_t>(P, B_SLOTRDY);
   D.assign_ready = ptr<int32_t>(P, B_ASGRDY);
   D.spin_err = ptr<int32_t>(P, B_SPINERR);
+  D.commit_cnt = ptr<int32_t>(P, B_SPINERR) + 1;
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
     D.i8_K = P->k;
@@ -530,13 +531,14 @@ const bool g_sync_launches = getenv("SFFT_SYNC") != nullptr;
 struct IterPlan {
   int n_active = 0, max_p = 0, fi = 0, max_M = 0, ksplit = 1, big = 0;
   bool use_i8 = false;
+  bool fuse_commit = false;   // the commit runs in the last FFT CTA of each signal (no commit launch)
 };
 
 // a1 (projection, term rows) and the int8 limbs of the signal terms, once per solve
 int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& launches) {
   cudaStream_t st = P->stream;
   CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_CTRL), 0, 64, st));   // both control blocks
-  CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SPINERR), 0, 4, st));
+  CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SPINERR), 0, 4 * (1 + (size_t)P->batch), st));
   LAUNCH(P, launch_project(D, sig->batch, sig->freqs, sig->coeffs, st));
   launches += 1;   // init_state_kernel
   if (P->i8_ok) {
@@ -614,6 +616,11 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
     }
   }
   it->big = it->max_M >= fft_big_m();
+  // fused commit (opt-in, SFFT_FUSE_COMMIT=1; measured slower: the commit then runs with the FFT's thread count
+  // on the tail of the launch -- C3 +4 %, C4 +44 %, C5 -0.7 %): unsharded lines only (line shards commit after
+  // the record all-gather), and the commit's shared memory must fit in the FFT's
+  static const bool fc = getenv("SFFT_FUSE_COMMIT") && atoi(getenv("SFFT_FUSE_COMMIT")) != 0;
+  it->fuse_commit = fc && P->line_G == 0 && decode_smem_bytes(D, it->max_p) <= P->fft[it->fi].smem_upto;
   return SFFT_OK;
 }
 
@@ -632,19 +639,26 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   D.lines_log = it.use_i8 ? 1 : 0;
   D.fuse_decode = 1;
   D.it_epoch = P->epoch;
+  D.fuse_commit = it.fuse_commit ? 1 : 0;
+  D.cur_iter = iter;
+  D.i8_iter = it.use_i8 ? 1 : 0;
   LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto, (int64_t)it.n_active * P->L), it.big, it.ksplit,
                         ptr<double2>(P, B_PART), it.max_p, st));
   D.lines_log = 0;
   D.fuse_decode = 0;
+  D.fuse_commit = 0;
+  D.i8_iter = 0;
   mark();
   return SFFT_OK;
 }
 
 int iter_back(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, const sfft_signal_t* sig, int& launches) {
   cudaStream_t st = P->stream;
-  D.i8_iter = it.use_i8 ? 1 : 0;
-  LAUNCH(P, launch_decode_commit(D, iter, it.max_p, it.n_active, st));
-  D.i8_iter = 0;
+  if (!it.fuse_commit) {
+    D.i8_iter = it.use_i8 ? 1 : 0;
+    LAUNCH(P, launch_decode_commit(D, iter, it.max_p, it.n_active, st));
+    D.i8_iter = 0;
+  }
   if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
     LAUNCH(P, launch_retilt(D, sig->batch, sig->freqs, st));
     if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch, P->k, st, true));

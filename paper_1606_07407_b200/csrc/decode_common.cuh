@@ -120,4 +120,275 @@ __device__ __forceinline__ double2 add_bin_residual(double2 f, const int32_t* bs
   return make_double2(__dadd_rn(f.x, __dmul_rn(pd, acc.x)), __dadd_rn(f.y, __dmul_rn(pd, acc.y)));
 }
 
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+// registry key hash of the r-long coordinate vector: XOR over n of mix64(v_n ^ n * golden) -- order-free, so a
+// warp computes it with lanes along n (key_hash_warp) and a single thread with a plain loop (same value)
+__device__ __forceinline__ uint64_t key_term(int64_t v, int n) {
+  return mix64((uint64_t)v ^ ((uint64_t)(n + 1) * 0x9E3779B97F4A7C15ULL));
+}
+__device__ __forceinline__ uint64_t key_hash_warp(const int64_t* v, int64_t stride, int r, int lane) {
+  uint64_t h = 0;
+  for (int n = lane; n < r; n += 32) h ^= key_term(v[(int64_t)n * stride], n);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) h ^= __shfl_xor_sync(0xffffffffu, h, o);
+  return h;
+}
+
+// a7 commit of one signal (steps 2-5 of decode_kernel<kDecCommit>, k_decode.cu): candidates of line 0 and the
+// pass flags / coordinates of every line from the records, bin consistency, accepted list, registry update
+// (hash lookup, R[v] += a, new entries and their C rows, prune) and the signal's state.  Runs in the commit
+// kernel (one CTA per signal) or, fused, in the last FFT CTA of the signal to finish (k_fft.cu).
+// smem: decode_smem_bytes(P, p); any blockDim that is a multiple of 32.
+static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t iter, int s, unsigned char* smem_raw) {
+  const int p = P.st_p[s], m = P.st_m[s];
+  const int nR = P.st_nR[s];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int r = P.r;
+  const int lvl = P.st_lvl[s];
+  const int64_t Ev = P.lvl_E[lvl];
+  double* mag = reinterpret_cast<double*>(smem_raw);
+  int* cand = reinterpret_cast<int*>(mag + p);
+  int* flag = cand + p;
+  int* accl = flag + p;
+  int* found = accl + P.k;
+  int* scratch = found + P.k;
+  int64_t* accv = P.acc_v + (int64_t)s * r * P.k;               // [r][k], column = candidate index
+  int nc = 0, total = 0;
+  // ---- commit: candidates of line 0, flags ANDed over the line shards, coordinates unpacked ----
+  nc = P.rec_nc[s];
+  for (int ci = tid; ci < nc; ci += blockDim.x) {
+    cand[ci] = P.rec_cand[(int64_t)s * P.k + ci];
+    int f = 1;
+    for (int g = 0; g < P.line_G; ++g)
+      f &= reinterpret_cast<const int32_t*>(P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words)[ci];
+    flag[ci] = f;
+  }
+  __syncthreads();
+  if (P.line_G == 1) {
+    // one shard holds every axis: its record already is the [r][k] coordinate array
+    accv = const_cast<int64_t*>(P.rec_recv) + (int64_t)s * P.rec_words + P.rec_fw;   // read-only below
+  } else {
+    for (int g = 0; g < P.line_G; ++g) {
+      int glo, ghi;
+      line_shard_range(r, P.line_G, g, &glo, &ghi);
+      const int64_t* rv = P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words + P.rec_fw;
+      for (int nn = 0; nn < ghi - glo; ++nn)
+        for (int ci = tid; ci < nc; ci += blockDim.x)
+          if (flag[ci]) accv[(int64_t)(glo + nn) * P.k + ci] = rv[(int64_t)nn * P.k + ci];
+    }
+    __syncthreads();
+  }
+  if (P.extra & 2) {
+    for (int ci = tid; ci < nc; ci += blockDim.x)
+      if (flag[ci] && mod_pos64(accv[(int64_t)m * P.k + ci], p) != cand[ci]) flag[ci] = 0;
+    __syncthreads();
+  }
+
+  // ---- 3. accepted list in ascending b ----
+  {
+    const int per = (nc + blockDim.x - 1) / blockDim.x;
+    const int i0 = tid * per, i1 = min(nc, i0 + per);
+    int c3 = 0;
+    for (int i = i0; i < i1; ++i) c3 += flag[i];
+    int pos3 = block_excl_scan(c3, scratch, &total);
+    for (int i = i0; i < i1; ++i)
+      if (flag[i]) accl[pos3++] = i;
+    __syncthreads();
+  }
+  const int na = total;
+
+  // ---- 4. registry update: R[v] += a ----
+  int64_t* vreg = P.v_all + (int64_t)s * r * P.kk + P.k;   // column e = registry entry e
+  double2* areg = P.a_reg + (int64_t)s * P.k;
+  uint64_t* khash = P.key_hash + (int64_t)s * P.k;
+  int* htab = P.htab + (int64_t)s * P.H;
+  const int Hm = P.H - 1;
+  // 4a. lookup, warp per accepted candidate: key hash with lanes along the coordinates, linear probing,
+  //     full-key compare by ballot (the arrays of the select are free in the commit: mag -> hashes, flag -> new)
+  //     Short keys (r < 128) go thread per candidate instead (the same hash by a plain loop).
+  uint64_t* hsh = reinterpret_cast<uint64_t*>(mag);
+  const int nwarps = (int)(blockDim.x >> 5);
+  const bool wide = r >= 128;
+  if (!wide) {
+    for (int t = tid; t < na; t += blockDim.x) {
+      const int ci = accl[t];
+      uint64_t h = 0;
+      for (int n = 0; n < r; ++n) h ^= key_term(accv[(int64_t)n * P.k + ci], n);
+      int slot = (int)(h & (uint64_t)Hm);
+      int fe = -1;
+      for (;;) {
+        const int e1 = htab[slot];
+        if (e1 == 0) break;
+        const int e = e1 - 1;
+        if (khash[e] == h) {
+          bool eq = true;
+          for (int n = 0; n < r && eq; ++n) eq = vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+          if (eq) { fe = e; break; }
+        }
+        slot = (slot + 1) & Hm;
+      }
+      found[t] = fe;
+      hsh[t] = h;
+    }
+  }
+  for (int t = warp; wide && t < na; t += nwarps) {
+    const int ci = accl[t];
+    const uint64_t h = key_hash_warp(accv + ci, P.k, r, lane);
+    int slot = (int)(h & (uint64_t)Hm);
+    int fe = -1;
+    for (;;) {
+      const int e1 = htab[slot];
+      if (e1 == 0) break;
+      const int e = e1 - 1;
+      if (khash[e] == h) {
+        bool eq = true;
+        for (int n = lane; n < r; n += 32) eq = eq && vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+        if (__all_sync(0xffffffffu, eq)) { fe = e; break; }
+      }
+      slot = (slot + 1) & Hm;
+    }
+    if (lane == 0) { found[t] = fe; hsh[t] = h; }
+  }
+  __syncthreads();
+  // 4b. R[v] += a for found keys; new keys get entries nR + rank in ascending-b order (deterministic)
+  int n_new;
+  {
+    const int per = (na + blockDim.x - 1) / blockDim.x;
+    const int t0 = tid * per, t1 = min(na, t0 + per);
+    int c4 = 0;
+    for (int t = t0; t < t1; ++t) c4 += found[t] < 0;
+    int rank = block_excl_scan(c4, scratch, &total);
+    n_new = total;
+    for (int t = t0; t < t1; ++t) {
+      const int ci = accl[t];
+      const double2 f0 = P.rec_f0[(int64_t)s * P.k + ci];   // F_0 at the candidate (the FFT's line-0 CTA)
+      const double2 a = make_double2(f0.x / (double)p, f0.y / (double)p);    // Eq. (7): a = F_0 / p
+      if (found[t] >= 0) {
+        const int e = found[t];
+        areg[e] = make_double2(areg[e].x + a.x, areg[e].y + a.y);
+        flag[t] = 0;
+      } else {
+        const int e = nR + rank++;
+        areg[e] = a;
+        khash[e] = hsh[t];
+        found[t] = e;
+        flag[t] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  // 4c. new entries: key row and hash-table insert (warp per entry with lanes along the coordinates for long
+  //     keys, thread per entry otherwise)
+  if (!wide) {
+    for (int t = tid; t < na; t += blockDim.x) {
+      if (!flag[t]) continue;
+      const int ci = accl[t], e = found[t];
+      for (int n = 0; n < r; ++n) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
+      int slot = (int)(hsh[t] & (uint64_t)Hm);
+      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+    }
+  }
+  for (int t = warp; wide && t < na; t += nwarps) {
+    if (!flag[t]) continue;
+    const int ci = accl[t], e = found[t];
+    for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
+    if (lane == 0) {
+      int slot = (int)(hsh[t] & (uint64_t)Hm);
+      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+    }
+  }
+  __syncthreads();
+  const int nR_new = nR + n_new;
+
+  // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}
+  double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+  for (int t = warp; t < na; t += nwarps) {                        // warp per touched entry, lanes along the row
+    const int e = found[t];
+    const double2 a = areg[e];
+    for (int n = lane; n < P.Lp; n += 32) {
+      double2 c;
+      if (n == 0) c = make_double2(-a.x, -a.y);
+      else if (n < P.L) {
+        const double2 lf = line_factor_exact(vreg[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
+        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+      } else c = make_double2(0.0, 0.0);
+      Creg[(int64_t)e * P.Lp + n] = c;
+    }
+  }
+  // prune test (only touched entries can have changed)
+  int small = 0;
+  for (int t = tid; t < na; t += blockDim.x) {
+    const double2 a = areg[found[t]];
+    small |= hypot(a.x, a.y) < P.prune;
+  }
+  const int any_small = __syncthreads_or(small);
+  int nR_final = nR_new;
+  if (any_small) {
+    // rare path: order-preserving compaction by warp 0, then rebuild the hash table
+    if (warp == 0) {
+      int wpos = 0;
+      for (int e = 0; e < nR_new; ++e) {
+        const double2 a = areg[e];
+        const bool keep = !(hypot(a.x, a.y) < P.prune);
+        if (keep) {
+          if (wpos != e) {
+            for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + wpos] = vreg[(int64_t)n * P.kk + e];
+            for (int n = lane; n < P.Lp; n += 32) Creg[(int64_t)wpos * P.Lp + n] = Creg[(int64_t)e * P.Lp + n];
+            if (lane == 0) { areg[wpos] = a; khash[wpos] = khash[e]; }
+          }
+          ++wpos;
+        }
+        __syncwarp();
+      }
+      if (lane == 0) scratch[0] = wpos;
+    }
+    __syncthreads();
+    nR_final = scratch[0];
+    for (int i = tid; i < P.H; i += blockDim.x) htab[i] = 0;
+    __syncthreads();
+    for (int e = tid; e < nR_final; e += blockDim.x) {
+      int slot = (int)(khash[e] & (uint64_t)Hm);
+      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+    }
+    __syncthreads();
+  }
+
+  // ---- 5. state ----
+  if (tid == 0) {
+    const int K = P.k + (P.literal ? nR : 0);
+    P.st_nR[s] = nR_final;
+    int stall = na == 0 ? P.st_stall[s] + 1 : 0;
+    P.st_samples[s] += (int64_t)(r + 1) * p;              // f evaluations of all shards (reading C22)
+    P.st_cmacs[s] += (int64_t)P.L * p * K;
+    if (P.i8_iter) P.st_cmacs_i8[s] += (int64_t)P.L * p * K;
+    P.st_iters[s] = iter;
+    if (s == 0 && iter <= kLogIters) {
+      P.st_log[2 * (iter - 1)] = p;
+      P.st_log[2 * (iter - 1) + 1] = na;
+    }
+    int st = ST_RUN;
+    if (nR_final >= P.k) {
+      st = SFFT_OK;
+    } else if (stall >= P.stall_limit) {
+      // C19 / R23: no progress for stall_limit iterations -> next tilt level (Alg. 3) if another iteration may run
+      if (lvl + 1 < P.n_levels && iter < P.max_iter) {
+        P.st_lvl[s] = lvl + 1;
+        P.st_retilt[s] = 1;
+        stall = 0;
+      } else {
+        st = SFFT_PARTIAL;
+      }
+    } else if (iter >= P.max_iter) {
+      st = SFFT_PARTIAL;
+    }
+    P.st_stall[s] = stall;
+    P.st_status[s] = st;
+  }
+}
+
+
 }  // namespace sfft

@@ -990,6 +990,22 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     if (n == 0) fused_select(P, s, p, x, ch, line);
     else fused_test(P, s, p, n, x, ch);
     FFT_PROF_MARK(4);
+    if (P.fuse_commit) {
+      // the last of the signal's n_lines CTAs to arrive commits it (a7): every thread fences its record
+      // writes, thread 0 counts the arrival; the last one resets the counter for the next iteration
+      __shared__ int last;
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        last = atomicAdd(P.commit_cnt + s, 1) == n_lines - 1;
+        if (last) {
+          P.commit_cnt[s] = 0;
+          __threadfence();
+        }
+      }
+      __syncthreads();
+      if (last) commit_signal(P, P.cur_iter, s, smem_raw);
+    }
     return;
   }
   // F[b] = w[b] * (conv)[b]: 4 chirp loads in flight per thread (the chirp is L2-resident, latency-bound)

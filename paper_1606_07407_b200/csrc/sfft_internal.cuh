@@ -140,6 +140,9 @@ struct DevParams {
   // (sel_ready[s] = it_epoch, release); line-n CTAs wait for it (acquire), then test + decode their line
   int32_t fuse_decode;         // launch flag of pfft_kernel (0: write the lines, stage entry point)
   int32_t it_epoch;            // iteration stamp (plan-wide counter, never repeats within a plan)
+  int32_t fuse_commit;         // pfft launch flag: the last CTA of a signal to finish runs its commit (a7)
+  int32_t cur_iter;            // the iteration of that launch (the commit's state / log)
+  int32_t* commit_cnt;         // [batch] arrival counters of the fused commit (reset by the last CTA)
   int32_t* sel_ready;          // [batch]
   int32_t* bin_start;          // [batch][p_stride + 1] registry entries of bin b: bin_order[bin_start[b] .. [b+1])
   int32_t* bin_order;          // [batch][k] registry entry indices grouped by bin, ascending e within a bin

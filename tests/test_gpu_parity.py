@@ -395,12 +395,11 @@ def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trial
         assert 0 < res.report.fallback_used <= len(used)
 
 
-def test_e2e_cta_pair_mode(S):
-    """The CTA-pair (tcgen05.mma.cta_group::2, M = 256) variant of the int8 exp-sum (opt-in, SFFT_I8_PAIR=1)
-    gives the same sets and coefficients as the oracle (full size, C3 and C5 seeds)."""
+def _opt_in_parity(env_var, cases):
+    """Full-size parity of an opt-in code path selected by an environment knob read once per process."""
     import subprocess, sys
     code = ("import numpy as np, torch, hashlib, oracle as O, workloads as W, paper_1606_07407_b200 as S\n"
-            "for name, tr in (('c3', [0, 1]), ('c5', [0])):\n"
+            "for name, tr in %r:\n" % (cases,) +
             "    c = W.CONFIGS[name]; g = np.load('tests/golden/oracle_%s.npz' % name)\n"
             "    w, a = W.make_batch(c, tr)\n"
             "    plan = S.sfft_plan(c.d, c.N, c.k, blocks=c.blocks, batch=len(tr))\n"
@@ -410,11 +409,23 @@ def test_e2e_cta_pair_mode(S):
             "        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())\n"
             "        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[k + '_w_sha256'])\n"
             "        ra = g[k + '_a']; assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max()\n"
-            "print('pair ok')\n")
-    env = dict(os.environ, SFFT_I8_PAIR="1")
+            "print('opt-in ok')\n")
+    env = dict(os.environ, **{env_var: "1"})
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                          cwd=os.path.dirname(GOLD_DIR.rstrip("/")).rsplit("/tests", 1)[0])
-    assert out.returncode == 0 and "pair ok" in out.stdout, out.stderr[-2000:]
+    assert out.returncode == 0 and "opt-in ok" in out.stdout, out.stderr[-2000:]
+
+
+def test_e2e_cta_pair_mode(S):
+    """The CTA-pair (tcgen05.mma.cta_group::2, M = 256) variant of the int8 exp-sum (opt-in, SFFT_I8_PAIR=1)
+    gives the same sets and coefficients as the oracle (full size, C3 and C5 seeds)."""
+    _opt_in_parity("SFFT_I8_PAIR", (("c3", [0, 1]), ("c5", [0])))
+
+
+def test_e2e_fused_commit(S):
+    """The registry commit run by the last FFT CTA of each signal (opt-in, SFFT_FUSE_COMMIT=1) gives the same
+    sets and coefficients as the oracle (full size: C3, C4 with its long keys, C5 with its tilt fallback)."""
+    _opt_in_parity("SFFT_FUSE_COMMIT", (("c3", [0, 1]), ("c4", [0]), ("c5", [0, 1])))
 
 
 # ------------------------------------------------------------------ line sharding (SURVEY 8(e))
