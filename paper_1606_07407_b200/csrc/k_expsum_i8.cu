@@ -80,11 +80,13 @@ __host__ __device__ __forceinline__ int i8_tile_width(int nt, int ntiles, int NT
 // One CTA per (signal, n-tile, K step): the 16 terms x W/2 lines of C are read coalesced into shared
 // memory, every (column, K byte) value is split into its S digits in shared memory, and the S limb tiles
 // (contiguous in global memory) are written with 16-byte stores.
+template <int S>
 __global__ void __launch_bounds__(256) i8_limbs_kernel(DevParams P, int32_t K, int32_t only_retilted) {
   pdl_wait();
-  __shared__ double2 cv[kI8StepTerms][48];                      // [term][line of the tile] (W <= 96)
+  // [term][line of the tile] (W <= 96); row stride 49 x 16 B: the terms a warp reads share banks only 2-way
+  __shared__ double2 cv[kI8StepTerms][49];
   __shared__ __align__(16) uint8_t tiles[6 * 96 * 32];           // [limb][W * 32]
-  const int NT = P.i8_NT, S = P.i8_S, ntiles = P.i8_ntiles, nks = P.i8_nks;
+  const int NT = P.i8_NT, ntiles = P.i8_ntiles, nks = P.i8_nks;
   const int nkt = (K + kI8StepTerms - 1) / kI8StepTerms;        // steps in use (layout stride stays nks)
   const int cols = (ntiles - 1) * NT + P.i8_NT_last;
   int b = blockIdx.x;
@@ -103,17 +105,35 @@ __global__ void __launch_bounds__(256) i8_limbs_kernel(DevParams P, int32_t K, i
   }
   __syncthreads();
   const double q = 127.0 * ldexp(1.0, 8 * (S - 1)) / P.i8_sigma[s];
-  for (int i = threadIdx.x; i < W * 32; i += blockDim.x) {
-    const int col = i >> 5, kp = i & 31;                          // output column, K byte of the step
-    const double2 c = cv[kp >> 1][col >> 1];
-    const bool a_im = kp & 1, im_out = col & 1;                   // row 2j+1 multiplies Im W; column 2n+1 is Im s_n
-    const double v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
-    int dg[8];
-    i8_digits(llrint(v * q), S, dg);
-    // CTA pairs: column halves [0, W/2) and [W/2, W) are separate K-major tiles (one per CTA of the pair)
-    const int hw = P.i8_pair ? W / 2 : W, half = col / hw, cc = col - half * hw;
-    const int off = half * S * hw * 32 + (cc >> 3) * 256 + (kp >> 4) * 128 + (cc & 7) * 16 + (kp & 15);
-    for (int t = 0; t < S; ++t) tiles[t * hw * 32 + off] = (uint8_t)dg[t];
+  // CTA pairs: column halves [0, W/2) and [W/2, W) are separate K-major tiles (one per CTA of the pair)
+  const int hw = P.i8_pair ? W / 2 : W;
+  uint32_t* tw = reinterpret_cast<uint32_t*>(tiles);
+  // thread item: output column col, K bytes 4 k4 .. 4 k4 + 3 (terms 2 k4, 2 k4 + 1; re / im rows) -> one
+  // 32-bit word per limb
+  for (int i = threadIdx.x; i < W * 8; i += blockDim.x) {
+    const int col = i >> 3, k4 = i & 7;
+    const bool im_out = col & 1;                                  // column 2n+1 is Im s_n
+    uint32_t word[S];
+#pragma unroll
+    for (int t = 0; t < S; ++t) word[t] = 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int kp = 4 * k4 + u;
+      const double2 c = cv[kp >> 1][col >> 1];
+      const bool a_im = kp & 1;                                   // row 2j+1 multiplies Im W
+      const double v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
+      int64_t X = llrint(v * q);
+#pragma unroll
+      for (int t = S - 1; t >= 0; --t) {                          // balanced base-256 digits (i8_digits)
+        const int64_t r = ((X + 128) & 255) - 128;
+        word[t] |= (uint32_t)(uint8_t)(int8_t)r << (8 * u);
+        X = (X - r) >> 8;
+      }
+    }
+    const int half = col / hw, cc = col - half * hw, kp0 = 4 * k4;
+    const int off = half * S * hw * 32 + (cc >> 3) * 256 + (kp0 >> 4) * 128 + (cc & 7) * 16 + (kp0 & 15);
+#pragma unroll
+    for (int t = 0; t < S; ++t) tw[(t * hw * 32 + off) >> 2] = word[t];
   }
   __syncthreads();
   int8_t* base = P.i8_B + (int64_t)s * nks * S * 32 * cols + (int64_t)nt * nks * S * NT * 32 + (int64_t)ks * S * W * 32;
@@ -592,7 +612,10 @@ int i8_blocks(const I8Config& c, int32_t max_p, int32_t n_signals) {
 cudaError_t launch_i8_prepare(const DevParams& P, int32_t n_signals, int32_t K, cudaStream_t st, bool only_retilted) {
   if (!only_retilted) i8_sigma_kernel<<<n_signals, 256, 0, st>>>(P, K);   // |a_j| do not change on a retilt
   const int64_t ctas = (int64_t)n_signals * P.i8_ntiles * ((K + kI8StepTerms - 1) / kI8StepTerms);
-  if (ctas > 0) return launch_pdl(i8_limbs_kernel, dim3((unsigned)ctas), dim3(256), 0, st, P, K, only_retilted ? 1 : 0);
+  if (ctas > 0) {
+    auto kern = P.i8_S == 6 ? i8_limbs_kernel<6> : i8_limbs_kernel<5>;      // i8_limbs_for: S is 5 or 6
+    return launch_pdl(kern, dim3((unsigned)ctas), dim3(256), 0, st, P, K, only_retilted ? 1 : 0);
+  }
   return cudaGetLastError();
 }
 
