@@ -15,39 +15,50 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
 
-// one warp per (signal, term)
-__global__ void project_kernel(DevParams P, int32_t batch, const int32_t* __restrict__ freqs,
-                               const double2* __restrict__ coeffs) {
+// one warp per (signal, term); the term's r reduced coordinates stay in shared memory (tilts, line factors)
+// and are written to v_all once.  Dynamic smem: 8 r bytes per warp (SMEM = false for very long keys: v_all
+// itself, stride kk).
+template <bool SMEM>
+__global__ void __launch_bounds__(256) project_kernel(DevParams P, int32_t batch, const int32_t* __restrict__ freqs,
+                                                      const double2* __restrict__ coeffs) {
+  extern __shared__ int64_t vsm_all[];
   const int lane = threadIdx.x & 31;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   if (gw >= (int64_t)batch * P.k) return;
   const int s = (int)(gw / P.k), j = (int)(gw % P.k);
-  const int32_t* w = freqs + ((int64_t)s * P.k + j) * P.d;
   int64_t* vs = P.v_all + (int64_t)s * P.r * P.kk;
+  const int64_t vstr = SMEM ? 1 : P.kk;
+  int64_t* vsm = SMEM ? vsm_all + (int64_t)(threadIdx.x >> 5) * P.r : vs + j;
+  const int32_t* w = freqs + ((int64_t)s * P.k + j) * P.d;
   for (int q = lane; q < P.r; q += 32) {
     const int off = P.block_off[q], dq = P.block_dims[q];
     int64_t acc = 0, pw = 1;
-    for (int t = 0; t < dq; ++t) {
-      acc += (int64_t)__ldg(w + off + t) * pw;
-      pw *= P.N;
+    int t = 0;
+    for (; t + 2 <= dq; t += 2) {                       // two independent loads in flight
+      const int64_t w0 = __ldg(w + off + t), w1 = __ldg(w + off + t + 1);
+      acc += w0 * pw + w1 * (pw * P.N);
+      pw *= P.N * P.N;
     }
-    vs[(int64_t)q * P.kk + j] = acc;
+    if (t < dq) acc += (int64_t)__ldg(w + off + t) * pw;
+    vsm[q * vstr] = acc;
   }
   __syncwarp();
   for (int t = lane; t < P.n_tilts; t += 32) {
     const int64_t* T = P.tilts + 5 * t;
     const int64_t a0 = T[0], a1 = T[1], b = T[2], h = T[3];
-    const int64_t u0 = vs[a0 * P.kk + j], u1 = vs[a1 * P.kk + j];
-    vs[a0 * P.kk + j] = b * u0 - h * u1;
-    vs[a1 * P.kk + j] = h * u0 + b * u1;
+    const int64_t u0 = vsm[a0 * vstr], u1 = vsm[a1 * vstr];
+    vsm[a0 * vstr] = b * u0 - h * u1;
+    vsm[a1 * vstr] = h * u0 + b * u1;
   }
   __syncwarp();
+  if (SMEM)
+    for (int q = lane; q < P.r; q += 32) vs[(int64_t)q * P.kk + j] = vsm[q];
   const double2 a = coeffs[(int64_t)s * P.k + j];
   double2* Crow = P.C_all + ((int64_t)s * P.kk + j) * P.Lp;
   for (int n = lane; n < P.Lp; n += 32) {
     double2 c;
     if (n == 0) c = a;
-    else if (n < P.L) c = cmul(a, line_factor_exact(vs[(int64_t)(P.line_lo + n - 1) * P.kk + j], P.E));
+    else if (n < P.L) c = cmul(a, line_factor_exact(vsm[(int64_t)(P.line_lo + n - 1) * vstr], P.E));
     else c = make_double2(0.0, 0.0);
     Crow[n] = c;
   }
@@ -81,7 +92,16 @@ cudaError_t launch_project(const DevParams& P, int32_t batch, const int32_t* fre
   const int64_t warps = (int64_t)batch * P.k;
   const int threads = 256;
   const int64_t blocks = (warps * 32 + threads - 1) / threads;
-  project_kernel<<<(unsigned)blocks, threads, 0, st>>>(P, batch, freqs, reinterpret_cast<const double2*>(coeffs));
+  const size_t smem = sizeof(int64_t) * (size_t)(threads / 32) * P.r;
+  if (smem <= 160 * 1024) {
+    e = ensure_smem(project_kernel<true>, smem);
+    if (e != cudaSuccess) return e;
+    project_kernel<true><<<(unsigned)blocks, threads, smem, st>>>(P, batch, freqs,
+                                                                  reinterpret_cast<const double2*>(coeffs));
+  } else {
+    project_kernel<false><<<(unsigned)blocks, threads, 0, st>>>(P, batch, freqs,
+                                                                reinterpret_cast<const double2*>(coeffs));
+  }
   return cudaGetLastError();
 }
 
