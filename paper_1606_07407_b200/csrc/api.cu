@@ -1146,6 +1146,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
       fprintf(stderr, "[sfft] iter %zu gap+setup %.3f prep %.3f expsum %.3f pfft %.3f decode %.3f ms\n", it + 1, g, a, b,
               c, d);
     }
+    float w = 0, b0 = 0;
+    cudaEventElapsedTime(&w, P->events[n_ev - 2], P->events[n_ev - 1]);
+    if (!it_marks.empty()) cudaEventElapsedTime(&b0, P->events[0], P->events[it_marks[0]]);
+    fprintf(stderr, "[sfft] begin+iter1 setup %.3f wrap %.3f ms\n", b0, w);
   }
   if (rep && P->profile && n_ev >= 2) {
     auto el = [&](size_t a, size_t b) {

@@ -2,9 +2,11 @@
 //   untilt every tilted pair: u = T^T v / hypo^2, rejecting non-integers (Alg. 3 l.38-39, reading R17)
 //   wrap every block by balanced digits: digit = ((u + N/2) mod N) - N/2, u <- (u - digit)/N
 //   canonical order: lexicographic by frequency vector.
-// Three kernels: digits (one warp per registry entry, lanes over blocks), rank (one CTA per signal; the rows
-// packed into fixed-width 64-bit chunks in shared memory, or keys of the first two coordinates with a full
-// compare on ties when they do not fit), gather.
+// Three kernels: digits (lanes over the blocks of a registry entry), rank (one CTA per signal: a bitonic sort of
+// the rows packed into 64-bit chunks in shared memory, or an O(k^2) ranking by keys of the first two coordinates
+// with a full compare on ties when they do not fit), gather.
+#include <algorithm>
+
 #include "sfft_internal.cuh"
 
 namespace sfft {
@@ -18,9 +20,11 @@ __device__ __forceinline__ int64_t floordiv(int64_t x, int64_t N, double invN) {
   return q;
 }
 
-__global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+// G lanes (a power of two <= 32, >= r when r <= 32) per registry entry, lanes over the blocks
+__global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(gt & (G - 1));
+  const int64_t gw = gt / G;
   if (gw >= (int64_t)P.batch * P.k) return;
   const int s = (int)(gw / P.k), e = (int)(gw % P.k);
   if (e >= P.st_nR[s]) return;
@@ -32,7 +36,7 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad) {
   const int lvl = P.st_lvl[s];
   const int32_t* axt = P.lvl_axt + (int64_t)lvl * P.r;
   const int64_t* tl = P.lvl_tilts + (int64_t)lvl * P.lvl_tmax * 5;
-  for (int q = lane; q < P.r; q += 32) {
+  for (int q = lane; q < P.r; q += G) {
     int64_t u = vreg[(int64_t)q * P.kk + e];
     const int at = axt[q];
     if (at >= 0) {
@@ -54,15 +58,17 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad) {
       u = qn;                                          // (u - digit) / N
     }
   }
-  if (__any_sync(0xffffffffu, err) && lane == 0) bad[s] = 1;
+  if (err) bad[s] = 1;
 }
 
-// rank of every entry in lexicographic order -> perm[s][rank] = entry.  Rows packed into fixed-width 64-bit
-// chunks in shared memory (coordinate + N/2 in `bits` bits, `per` coordinates per chunk, most significant
-// first): chunk sequences compare like the rows, so every comparison is a few shared-memory loads
+// lexicographic order of the entries -> perm[s][rank] = entry.  Rows packed into fixed-width 64-bit chunks in
+// shared memory (coordinate + N/2 in `bits` bits, `per` coordinates per chunk, most significant first): chunk
+// sequences compare like the rows.  A bitonic sort of the entry indices (a power of two >= nR slots, padding
+// sorts last; equal rows -- only possible for entries flagged bad -- by index) replaces the O(k^2) ranking.
 __global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm, int bits, int per, int nch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [nch][k]
+  int* ord = reinterpret_cast<int*>(key + (size_t)nch * P.k);                     // [power of two >= k]
   const int s = blockIdx.x, tid = threadIdx.x;
   const int nR = P.st_nR[s];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
@@ -77,22 +83,31 @@ __global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm,
     }
     key[(int64_t)c * P.k + e] = kv;
   }
+  int n = 1;
+  while (n < nR) n <<= 1;
+  for (int i = tid; i < n; i += blockDim.x) ord[i] = i < nR ? i : 0x7fffffff;
   __syncthreads();
-  for (int e = tid; e < nR; e += blockDim.x) {
-    const unsigned long long ke = key[e];
-    int rank = 0;
-    for (int f = 0; f < nR; ++f) {
-      const unsigned long long kf = key[f];
-      if (kf < ke) ++rank;
-      else if (kf == ke && f != e) {
-        for (int c = 1; c < nch; ++c) {
-          const unsigned long long a = key[(int64_t)c * P.k + f], b = key[(int64_t)c * P.k + e];
-          if (a != b) { rank += a < b; break; }
-        }
-      }
+  auto less = [&](int a, int b) -> bool {                    // row a before row b
+    if (b == 0x7fffffff) return a != 0x7fffffff;
+    if (a == 0x7fffffff) return false;
+    for (int c = 0; c < nch; ++c) {
+      const unsigned long long ka = key[(int64_t)c * P.k + a], kb = key[(int64_t)c * P.k + b];
+      if (ka != kb) return ka < kb;
     }
-    perm[(int64_t)s * P.k + rank] = e;
+    return a < b;
+  };
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int i = tid; i < (n >> 1); i += blockDim.x) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const int a = ord[lo], b = ord[hi];
+        const bool up = (lo & size) == 0;
+        if (up ? less(b, a) : less(a, b)) { ord[lo] = b; ord[hi] = a; }
+      }
+      __syncthreads();
+    }
   }
+  for (int i = tid; i < nR; i += blockDim.x) perm[(int64_t)s * P.k + i] = ord[i];
 }
 
 // fallback when the packed rows do not fit in shared memory: keys of the first two coordinates, full
@@ -128,12 +143,14 @@ __global__ void wrap_rank_kernel(DevParams P, int32_t* __restrict__ perm) {
   }
 }
 
-// one warp per output row: coalesced copy of the d-vector, coefficient, counts and status
+// G lanes (a power of two <= 32, >= d when d <= 32) per output row: coalesced copy of the d-vector,
+// coefficient, counts and status
 __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm, const int32_t* __restrict__ bad,
                                    int32_t* __restrict__ out_freqs, double2* __restrict__ out_coeffs,
-                                   int32_t* __restrict__ out_count, int32_t* __restrict__ out_status) {
-  const int lane = threadIdx.x & 31;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+                                   int32_t* __restrict__ out_count, int32_t* __restrict__ out_status, int G) {
+  const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(gt & (G - 1));
+  const int64_t gw = gt / G;
   if (gw >= (int64_t)P.batch * P.k) return;
   const int s = (int)(gw / P.k), i = (int)(gw % P.k);
   const int nR = P.st_nR[s];
@@ -141,10 +158,10 @@ __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm
   if (i < nR) {
     const int e = perm[(int64_t)s * P.k + i];
     const int32_t* src = P.wtmp + ((int64_t)s * P.k + e) * P.d;
-    for (int l = lane; l < P.d; l += 32) of[l] = src[l];
+    for (int l = lane; l < P.d; l += G) of[l] = src[l];
     if (lane == 0) out_coeffs[(int64_t)s * P.k + i] = P.a_reg[(int64_t)s * P.k + e];
   } else {
-    for (int l = lane; l < P.d; l += 32) of[l] = 0;
+    for (int l = lane; l < P.d; l += G) of[l] = 0;
     if (lane == 0) out_coeffs[(int64_t)s * P.k + i] = make_double2(0.0, 0.0);
   }
   if (i == 0 && lane == 0) {
@@ -165,27 +182,35 @@ cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freq
   cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int32_t) * n_signals, st);
   if (e != cudaSuccess) return e;
   const int64_t warps = (int64_t)n_signals * P.k;
-  const unsigned blocks = (unsigned)((warps * 32 + 255) / 256);
-  wrap_digits_kernel<<<blocks, 256, 0, st>>>(P, bad);
+  int G = 1;
+  while (G < 32 && G < P.r) G <<= 1;
+  wrap_digits_kernel<<<(unsigned)((warps * G + 255) / 256), 256, 0, st>>>(P, bad, G);
   int bits = 1;
   while (((int64_t)1 << bits) < P.N) ++bits;
   const int per = 64 / bits, nch = (P.d + per - 1) / per;
-  const size_t psmem = sizeof(unsigned long long) * (size_t)nch * P.k;
+  int n2 = 1;
+  while (n2 < P.k) n2 <<= 1;
+  const size_t psmem = sizeof(unsigned long long) * (size_t)nch * P.k + sizeof(int) * (size_t)n2;
   int optin = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (psmem <= (size_t)optin) {
     e = ensure_smem(wrap_rank_packed_kernel, psmem);
     if (e != cudaSuccess) return e;
-    wrap_rank_packed_kernel<<<n_signals, 1024, psmem, st>>>(P, perm, bits, per, nch);
+    // threads: the sort's n2 / 2 compare-exchanges, or ~8 packed chunks each for the build if more
+    const int want = std::max(n2 / 2, (int)(((int64_t)nch * P.k + 7) / 8));
+    const int threads = std::min(1024, std::max(64, (want + 31) / 32 * 32));
+    wrap_rank_packed_kernel<<<n_signals, threads, psmem, st>>>(P, perm, bits, per, nch);
   } else {
     const size_t smem = sizeof(unsigned long long) * (size_t)P.k;
     e = ensure_smem(wrap_rank_kernel, smem);
     if (e != cudaSuccess) return e;
     wrap_rank_kernel<<<n_signals, 1024, smem, st>>>(P, perm);
   }
-  wrap_gather_kernel<<<blocks, 256, 0, st>>>(P, perm, bad, out_freqs, reinterpret_cast<double2*>(out_coeffs),
-                                             out_count, out_status);
+  int Gd = 1;
+  while (Gd < 32 && Gd < P.d) Gd <<= 1;
+  wrap_gather_kernel<<<(unsigned)((warps * Gd + 255) / 256), 256, 0, st>>>(
+      P, perm, bad, out_freqs, reinterpret_cast<double2*>(out_coeffs), out_count, out_status, Gd);
   return cudaGetLastError();
 }
 
