@@ -284,10 +284,23 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   // 4c. new entries: key row and hash-table insert (warp per entry with lanes along the coordinates for long
   //     keys, thread per entry otherwise)
   if (!wide) {
-    for (int t = tid; t < na; t += blockDim.x) {
+    // key rows: items (entry, 8 axes) with the entries along the threads (coalesced record reads), the
+    // 8 loads of an item issued before its stores
+    const int rch = (r + 7) / 8;
+    for (int it = tid; it < na * rch; it += blockDim.x) {
+      const int t = it % na, n0 = (it / na) * 8;
       if (!flag[t]) continue;
       const int ci = accl[t], e = found[t];
-      for (int n = 0; n < r; ++n) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
+      int64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = n0 + u < r ? accv[(int64_t)(n0 + u) * P.k + ci] : 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (n0 + u < r) vreg[(int64_t)(n0 + u) * P.kk + e] = v[u];
+    }
+    for (int t = tid; t < na; t += blockDim.x) {
+      if (!flag[t]) continue;
+      const int e = found[t];
       int slot = (int)(hsh[t] & (uint64_t)Hm);
       while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
     }
@@ -304,19 +317,47 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   __syncthreads();
   const int nR_new = nR + n_new;
 
-  // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}
+  // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}.  Items
+  // (entry, 8 lines) with the entries along the threads; v from the record (a touched entry's key equals
+  // its candidate's coordinates), coalesced, the 8 loads of an item in flight together
   double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
-  for (int t = warp; t < na; t += nwarps) {                        // warp per touched entry, lanes along the row
-    const int e = found[t];
+  const int lch = (P.Lp + 7) / 8;
+  const bool by_items = 2 * na * lch >= (int)blockDim.x;  // else too few items: warp per entry, lanes along the row
+  for (int t = warp; !by_items && t < na; t += nwarps) {
+    const int e = found[t], ci = accl[t];
     const double2 a = areg[e];
     for (int n = lane; n < P.Lp; n += 32) {
       double2 c;
       if (n == 0) c = make_double2(-a.x, -a.y);
       else if (n < P.L) {
-        const double2 lf = line_factor_exact(vreg[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
+        const double2 lf = line_factor_exact(accv[(int64_t)(P.line_lo + n - 1) * P.k + ci], Ev);
         c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
       } else c = make_double2(0.0, 0.0);
       Creg[(int64_t)e * P.Lp + n] = c;
+    }
+  }
+  for (int it = tid; by_items && it < na * lch; it += blockDim.x) {
+    const int t = it % na, n0 = (it / na) * 8;
+    const int e = found[t], ci = accl[t];
+    const double2 a = areg[e];
+    int64_t v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u;
+      v[u] = (n >= 1 && n < P.L) ? accv[(int64_t)(P.line_lo + n - 1) * P.k + ci] : 0;
+    }
+    double2* row = Creg + (int64_t)e * P.Lp;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int n = n0 + u;
+      if (n >= P.Lp) break;
+      double2 c;
+      if (n == 0) c = make_double2(-a.x, -a.y);
+      else if (n < P.L) {
+        const double2 lf = line_factor_exact(v[u], Ev);
+        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+      } else c = make_double2(0.0, 0.0);
+      row[n] = c;
     }
   }
   // prune test (only touched entries can have changed)
