@@ -247,6 +247,19 @@ def test_e2e_edge_cases(S):
             _check_against_oracle(res, i, ref.w, ref.a, ref.status)
 
 
+def test_e2e_very_long_keys(S):
+    """r = 3000 one-dimensional blocks (d = 3000): the projection keeps v in v_all instead of shared memory
+    (8 r bytes per warp > 160 KB), long-key commit, 3001 lines per signal."""
+    c = W.custom_config(3000, 16, 3, (1,) * 3000, cfg=72)
+    trials = list(range(2))
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, batch=len(trials))
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for i in trials:
+        ref = O.solve(O.params_for(c), w[i], a[i])
+        _check_against_oracle(res, i, ref.w, ref.a, ref.status)
+
+
 def test_e2e_paper_config_small(S):
     """PAPER.md:422 (N=20, d1=5, d=100), non-power-of-two E = 2 * 20^5."""
     c = W.paper_config(100, 16)
