@@ -122,13 +122,13 @@ __global__ void __launch_bounds__(256) i8_limbs_kernel(DevParams P, int32_t K, i
       const double2 c = cv[kp >> 1][col >> 1];
       const bool a_im = kp & 1;                                   // row 2j+1 multiplies Im W
       const double v = im_out ? (a_im ? c.x : c.y) : (a_im ? -c.y : c.x);
-      int64_t X = llrint(v * q);
+      // balanced base-256 digits of X (i8_digits, most significant first): X + sum_t 128 * 256^t has the plain
+      // base-256 digits r_t + 128 (|X| <= 127 * 256^(S-1)), so limb t is byte S-1-t of it with the top bit
+      // flipped -- the same bytes as the digit loop, without its 64-bit arithmetic per digit
+      const uint64_t Y = (uint64_t)llrint(v * q) + 0x8080808080808080ull;
 #pragma unroll
-      for (int t = S - 1; t >= 0; --t) {                          // balanced base-256 digits (i8_digits)
-        const int64_t r = ((X + 128) & 255) - 128;
-        word[t] |= (uint32_t)(uint8_t)(int8_t)r << (8 * u);
-        X = (X - r) >> 8;
-      }
+      for (int t = 0; t < S; ++t)
+        word[t] |= (((uint32_t)(Y >> (8 * (S - 1 - t))) & 255u) ^ 128u) << (8 * u);
     }
     const int half = col / hw, cc = col - half * hw, kp0 = 4 * k4;
     const int off = half * S * hw * 32 + (cc >> 3) * 256 + (kp0 >> 4) * 128 + (cc & 7) * 16 + (kp0 & 15);

@@ -32,6 +32,7 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G
   int32_t* row = P.wtmp + ((int64_t)s * P.k + e) * P.d;
   const int64_t N = P.N, h2 = N / 2;
   const double invN = 1.0 / (double)N;
+  const int lgN = (N & (N - 1)) == 0 ? __ffsll(N) - 1 : -1;
   int err = 0;
   const int lvl = P.st_lvl[s];
   const int32_t* axt = P.lvl_axt + (int64_t)lvl * P.r;
@@ -51,11 +52,20 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G
     int64_t geo = 0, pw = 1;
     for (int t = 0; t < dq; ++t) { geo += pw; pw *= N; }
     if (u < -h2 * geo || u > (h2 - 1) * geo) { err = 1; u = 0; }
-    for (int t = 0; t < dq; ++t) {
-      const int64_t x = u + h2;
-      const int64_t qn = floordiv(x, N, invN);
-      row[off + t] = (int32_t)(x - qn * N - h2);      // balanced digit
-      u = qn;                                          // (u - digit) / N
+    if (lgN >= 0) {
+      // N = 2^lgN: floor division is an arithmetic shift, the remainder a mask (same digits)
+      for (int t = 0; t < dq; ++t) {
+        const int64_t x = u + h2;
+        row[off + t] = (int32_t)((x & (N - 1)) - h2);  // balanced digit
+        u = x >> lgN;                                  // (u - digit) / N
+      }
+    } else {
+      for (int t = 0; t < dq; ++t) {
+        const int64_t x = u + h2;
+        const int64_t qn = floordiv(x, N, invN);
+        row[off + t] = (int32_t)(x - qn * N - h2);    // balanced digit
+        u = qn;                                        // (u - digit) / N
+      }
     }
   }
   if (err) bad[s] = 1;
