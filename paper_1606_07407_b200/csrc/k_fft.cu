@@ -604,20 +604,23 @@ __global__ void __launch_bounds__(1024) tables_assign_kernel(DevParams P, int32_
 
 
 // ---- per-signal term phases of the iteration: u_j = v_{j,m} mod p, 8 u_j mod p, e_j = log_g u_j ----
-// cnt: >= p + k ints of shared memory; scratch: >= 32 ints.  phases: kTermsU (u_j and the bin sort; needs no
-// table slot) | kTermsE (e_j, from the slot's discrete-log table; alone, it reads back this block's u_j)
+// cnt: >= p + 3k ints of shared memory; scratch: >= 32 ints.  phases: kTermsU (u_j and the bin sort; needs no
+// table slot; u_j also kept in cnt[p + k ..)) | kTermsE (e_j, from the slot's discrete-log table; alone, it
+// reads u_j from shared memory, or back from u_all when `u_smem` is false -- the table fill reused the smem)
 constexpr int kTermsU = 1, kTermsE = 2;
-__device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, int phases = kTermsU | kTermsE) {
+__device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, int phases = kTermsU | kTermsE,
+                           bool u_smem = false) {
   const int p = P.st_p[s];
   if (!(phases & kTermsU)) {
     if (P.i8_S <= 0) return;
     const int K = P.k + P.st_nR[s];
     const int Kp = (K + 15) & ~15;
     const int2* ug = P.u_all + (int64_t)s * P.kk;
+    const int* us = cnt + p + P.k;
     const int64_t base = (int64_t)P.st_slot[s] * P.i8_tstride;
     int32_t* eg = P.i8_elog + (int64_t)s * P.i8_estride;
     for (int j = threadIdx.x; j < Kp; j += blockDim.x) {
-      const int u = j < K ? ug[j].x : 0;
+      const int u = j < K ? (u_smem ? us[j] : ug[j].x) : 0;
       eg[j] = u ? P.i8_dlog[base + u] : -1;
     }
     return;
@@ -631,9 +634,10 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, in
   const int64_t base = (int64_t)P.st_slot[s] * P.i8_tstride;
   int32_t* eg = P.i8_S > 0 && (phases & kTermsE) ? P.i8_elog + (int64_t)s * P.i8_estride : nullptr;
   int* ub = cnt + p;                                 // [nR] bins of the registry entries (smem copy)
+  int* us = cnt + p + P.k;                           // [K] u_j (smem copy for a later kTermsE pass)
   for (int j = threadIdx.x; j < (eg ? Kp : K); j += blockDim.x) {
     const int u = j < K ? (int)mod_pos64(vm[j], p) : 0;
-    if (j < K) ug[j] = make_int2(u, (8 * u) % p);
+    if (j < K) { ug[j] = make_int2(u, (8 * u) % p); us[j] = u; }
     if (j >= P.k && j < K) ub[j - P.k] = u;
     // e_j: -1 for u_j = 0 and for the padding up to a multiple of 16 (reading R22)
     if (eg) eg[j] = u ? P.i8_dlog[base + u] : -1;
@@ -682,7 +686,7 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, in
 __global__ void terms_kernel(DevParams P, int32_t direct) {
   pdl_wait();
   if (!direct && (int)blockIdx.x >= P.ctrl[0]) return;   // grid sized before the host read n_active
-  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end; [nR] bins
+  extern __shared__ int cnt[];                       // [p]: entries per bin, then the running end; [nR] bins; [K] u
   __shared__ int scratch[32];
   terms_body(P, P.active[blockIdx.x], cnt, scratch);
 }
@@ -768,8 +772,10 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
   if (a > 0 && threadIdx.x == 0) wait_stamp(P.assign_ready, epoch, P.spin_err);
   __syncthreads();
   const int slot = P.st_slot[s];
+  bool filled = false;
   if (P.fill_ep[slot] == epoch) {
     if (P.fill_by[slot] == a) {
+      filled = true;                                 // the FFT buffer overwrites the smem copy of u_j
       fill_tables<BIG>(P, slot, P.st_p[s], smem_raw);
       __syncthreads();
       if (threadIdx.x == 0) release_stamp(P.slot_ready + slot, epoch);
@@ -778,7 +784,7 @@ __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) prep_iter_kernel(DevParam
     }
     __syncthreads();
   }
-  terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch, kTermsE);
+  terms_body(P, s, reinterpret_cast<int*>(smem_raw), scratch, kTermsE, !filled);
 }
 
 
@@ -1042,7 +1048,7 @@ cudaError_t launch_prep_iter(const DevParams& P, int32_t n_bound, int32_t smem_b
   while (hs < 2 * (size_t)P.n_tslots) hs <<= 1;
   const size_t smem = std::max<size_t>((size_t)smem_bytes,
                                        std::max(sizeof(int) * (2 * hs + 2 * 4096 + (size_t)P.n_tslots),
-                                                sizeof(int) * ((size_t)P.p_stride + P.k)));
+                                                sizeof(int) * ((size_t)P.p_stride + 3 * (size_t)P.k)));
   cudaError_t e = ensure_smem(prep_iter_kernel<true>, smem);
   if (e != cudaSuccess) return e;
   return launch_pdl(prep_iter_kernel<true>, dim3(n_bound), dim3(512), smem, st, P, epoch);
@@ -1066,9 +1072,10 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
   if (e != cudaSuccess) return e;
   e = launch_pdl(kern, dim3(n_signals), dim3(threads), smem, st, P, direct ? 1 : 0);
   if (e != cudaSuccess) return e;
-  e = ensure_smem(terms_kernel, sizeof(int) * ((size_t)P.p_stride + P.k));
+  e = ensure_smem(terms_kernel, sizeof(int) * ((size_t)P.p_stride + 3 * (size_t)P.k));
   if (e != cudaSuccess) return e;
-  e = launch_pdl(terms_kernel, dim3(n_signals), dim3(256), sizeof(int) * ((size_t)P.p_stride + P.k), st, P, direct ? 1 : 0);
+  e = launch_pdl(terms_kernel, dim3(n_signals), dim3(256), sizeof(int) * ((size_t)P.p_stride + 3 * (size_t)P.k), st, P,
+                 direct ? 1 : 0);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
