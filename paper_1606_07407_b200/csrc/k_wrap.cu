@@ -157,7 +157,8 @@ __global__ void wrap_rank_kernel(DevParams P, int32_t* __restrict__ perm) {
 // coefficient, counts and status
 __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm, const int32_t* __restrict__ bad,
                                    int32_t* __restrict__ out_freqs, double2* __restrict__ out_coeffs,
-                                   int32_t* __restrict__ out_count, int32_t* __restrict__ out_status, int G) {
+                                   int32_t* __restrict__ out_count, int32_t* __restrict__ out_status, int G,
+                                   int vec) {
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(gt & (G - 1));
   const int64_t gw = gt / G;
@@ -168,7 +169,13 @@ __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm
   if (i < nR) {
     const int e = perm[(int64_t)s * P.k + i];
     const int32_t* src = P.wtmp + ((int64_t)s * P.k + e) * P.d;
-    for (int l = lane; l < P.d; l += G) of[l] = src[l];
+    if (vec) {                                          // 16-byte rows, 16-byte aligned output: int4 copies
+      const int4* s4 = reinterpret_cast<const int4*>(src);
+      int4* o4 = reinterpret_cast<int4*>(of);
+      for (int l = lane; l < (P.d >> 2); l += G) o4[l] = s4[l];
+    } else {
+      for (int l = lane; l < P.d; l += G) of[l] = src[l];
+    }
     if (lane == 0) out_coeffs[(int64_t)s * P.k + i] = P.a_reg[(int64_t)s * P.k + e];
   } else {
     for (int l = lane; l < P.d; l += G) of[l] = 0;
@@ -218,9 +225,12 @@ cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freq
     wrap_rank_kernel<<<n_signals, 1024, smem, st>>>(P, perm);
   }
   int Gd = 1;
-  while (Gd < 32 && Gd < P.d) Gd <<= 1;
+  // int4 copies when every row is 16-byte aligned (d % 4 == 0 and an aligned caller buffer)
+  const int vec = (P.d & 3) == 0 && (reinterpret_cast<uintptr_t>(out_freqs) & 15) == 0;
+  const int dw = vec ? P.d / 4 : P.d;                  // copy words per row
+  while (Gd < 32 && Gd < dw) Gd <<= 1;
   wrap_gather_kernel<<<(unsigned)((warps * Gd + 255) / 256), 256, 0, st>>>(
-      P, perm, bad, out_freqs, reinterpret_cast<double2*>(out_coeffs), out_count, out_status, Gd);
+      P, perm, bad, out_freqs, reinterpret_cast<double2*>(out_coeffs), out_count, out_status, Gd, vec);
   return cudaGetLastError();
 }
 
