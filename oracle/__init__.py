@@ -23,6 +23,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "sfft_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
+TRACE_COLS = 8      # ORACLE_TRACE_COLS (sfft_oracle.h)
 OK, PARTIAL, EINVAL, EPRECISION, ECORRUPT, ENOMEM = 0, 1, -1, -2, -4, -6
 
 
@@ -80,8 +81,9 @@ def lib():
         L.oracle_fallback_tilts.argtypes = [i32, i32, vp]
         L.oracle_fallback_tilts.restype = i32
         L.oracle_solve.argtypes = [ctypes.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, i32, vp]
+        L.oracle_solve_raw.argtypes = [ctypes.POINTER(_Params), vp, vp, vp, vp, vp]
         L.oracle_solve_batch.argtypes = [ctypes.POINTER(_Params), i32, vp, vp, vp, vp, vp, vp, vp,
-                                         vp, i32]
+                                         vp, i32, vp]
         _lib = L
     return _lib
 
@@ -282,7 +284,8 @@ class SolveResult:
     a: np.ndarray          # complex128 [count]
     samples: int
     iterations: int
-    trace: np.ndarray      # int64 [iterations, 5] = (i, p, m, n_candidates, n_accepted)
+    trace: np.ndarray      # int64 [iterations, TRACE_COLS] = (i, p, m, n_candidates, n_accepted,
+    #                        n_nonempty before the k* cap, n_accumulated, n_pruned)
 
 
 def solve(P: Params, w: np.ndarray, a: np.ndarray, trace_cap: int = 1000) -> SolveResult:
@@ -295,7 +298,7 @@ def solve(P: Params, w: np.ndarray, a: np.ndarray, trace_cap: int = 1000) -> Sol
     cnt = np.zeros(1, np.int32)
     samples = np.zeros(1, np.int64)
     iters = np.zeros(1, np.int32)
-    trace = np.zeros((trace_cap, 5), np.int64)
+    trace = np.zeros((trace_cap, TRACE_COLS), np.int64)
     s = P.c_struct()
     st = lib().oracle_solve(ctypes.byref(s), _p(w), _p(a.view(np.float64)), _p(out_w),
                             _p(out_a.view(np.float64)), _p(cnt), _p(samples), _p(iters),
@@ -306,9 +309,22 @@ def solve(P: Params, w: np.ndarray, a: np.ndarray, trace_cap: int = 1000) -> Sol
                        trace[:min(it, trace_cap)].copy())
 
 
-def solve_batch(P: Params, w: np.ndarray, a: np.ndarray, n_threads: int = 0):
+def solve_raw(P: Params, w: np.ndarray, a: np.ndarray):
+    """Debugging aid: (status, registry keys int64 [n, r], coefficients complex128 [n]) before the wrap."""
+    w = np.ascontiguousarray(w, dtype=np.int32)
+    a = np.ascontiguousarray(a, dtype=np.complex128)
+    rv = np.zeros((P.k, P.r), np.int64)
+    ra = np.zeros(P.k, np.complex128)
+    n = np.zeros(1, np.int32)
+    s = P.c_struct()
+    st = lib().oracle_solve_raw(ctypes.byref(s), _p(w), _p(a.view(np.float64)), _p(rv), _p(ra.view(np.float64)),
+                                _p(n))
+    return st, rv[:int(n[0])].copy(), ra[:int(n[0])].copy()
+
+
+def solve_batch(P: Params, w: np.ndarray, a: np.ndarray, n_threads: int = 0, times: bool = False):
     """Independent signals over host threads: returns (status[T], w[T,k,d], a[T,k], count[T],
-    samples[T], iterations[T])."""
+    samples[T], iterations[T]) and, with times=True, ns int64 [T, 2] = (solve wall ns, sampling ns)."""
     w = np.ascontiguousarray(w, dtype=np.int32)
     a = np.ascontiguousarray(a, dtype=np.complex128)
     T = w.shape[0]
@@ -321,8 +337,11 @@ def solve_batch(P: Params, w: np.ndarray, a: np.ndarray, n_threads: int = 0):
     status = np.zeros(T, np.int32)
     if n_threads <= 0:
         n_threads = os.cpu_count() or 1
+    ns = np.zeros((T, 2), np.int64) if times else None
     s = P.c_struct()
     lib().oracle_solve_batch(ctypes.byref(s), T, _p(w), _p(a.view(np.float64)), _p(out_w),
                              _p(out_a.view(np.float64)), _p(cnt), _p(samples), _p(iters),
-                             _p(status), n_threads)
+                             _p(status), n_threads, _p(ns))
+    if times:
+        return status, out_w, out_a, cnt, samples, iters, ns
     return status, out_w, out_a, cnt, samples, iters

@@ -10,12 +10,14 @@
  * Scalar double / int64 arithmetic, direct O(p^2) DFT, linear-search registry.
  * Compiled with -O2 and WITHOUT -ffast-math.
  */
+#define _POSIX_C_SOURCE 200809L
 #include "sfft_oracle.h"
 
 #include <math.h>
 #include <pthread.h>
 #include <stdlib.h>
 #include <string.h>
+#include <time.h>
 
 #ifndef M_PI
 #define M_PI 3.14159265358979323846
@@ -312,7 +314,7 @@ void oracle_dft(int64_t p, const double* s, double* F) {
 
 typedef struct { double mag; int64_t b; } cand_t;
 
-static int cand_cmp_mag(const void* x, const void* y) {   /* |F_0| descending, ties -> smaller b (C6) */
+static int cand_cmp_mag(const void* x, const void* y) {   /* |F_0|^2 descending, ties -> smaller b (C6) */
   const cand_t* a = (const cand_t*)x;
   const cand_t* b = (const cand_t*)y;
   if (a->mag > b->mag) return -1;
@@ -328,15 +330,28 @@ static int cand_cmp_b(const void* x, const void* y) {
 int32_t oracle_decode(const oracle_params* P, int64_t E, const int64_t* lo, const int64_t* hi,
                       int64_t p, int32_t m, int32_t kstar, const double* F,
                       int32_t* n_cand, int32_t* acc_b, int64_t* acc_v, double* acc_a) {
+  return oracle_decode_ex(P, E, lo, hi, p, m, kstar, F, n_cand, NULL, acc_b, acc_v, acc_a);
+}
+
+int32_t oracle_decode_ex(const oracle_params* P, int64_t E, const int64_t* lo, const int64_t* hi,
+                         int64_t p, int32_t m, int32_t kstar, const double* F,
+                         int32_t* n_cand, int32_t* n_nonempty, int32_t* acc_b, int64_t* acc_v, double* acc_a) {
   const int32_t r = P->r;
   const double* F0 = F;
-  /* select (C5, C18): bins with |F_0[b]| >= floor * p, at most the k* largest */
+  /* select (C5, C18): bins with |F_0[b]| >= floor * p, at most the k* largest.  The magnitude is compared as
+   * |F_0|^2 = Re^2 + Im^2, each operation rounded once (reading R5: a plain formula, so that the k* cap and
+   * its ties are decided identically by any implementation that is handed the same bins) */
   cand_t* cand = (cand_t*)malloc(sizeof(cand_t) * (size_t)p);
   int32_t nc = 0;
+  const double floor_abs = P->bin_floor_rel * (double)p;
+  const double floor2 = floor_abs * floor_abs;
   for (int64_t b = 0; b < p; ++b) {
-    double mag = hypot(F0[2 * b], F0[2 * b + 1]);
-    if (mag >= P->bin_floor_rel * (double)p) { cand[nc].mag = mag; cand[nc].b = b; ++nc; }
+    const double re = F0[2 * b], im = F0[2 * b + 1];
+    const double re2 = re * re, im2 = im * im;
+    const double mag2 = re2 + im2;
+    if (mag2 >= floor2) { cand[nc].mag = mag2; cand[nc].b = b; ++nc; }
   }
+  if (n_nonempty) *n_nonempty = nc;
   if (nc > kstar) {
     qsort(cand, (size_t)nc, sizeof(cand_t), cand_cmp_mag);   /* SORT (Alg. 2 l.18) */
     nc = kstar;
@@ -465,9 +480,51 @@ static void tilt_all(const oracle_params* L, int64_t* u) {
   }
 }
 
+static int64_t now_ns(void) {
+  struct timespec ts;
+  clock_gettime(CLOCK_MONOTONIC, &ts);
+  return (int64_t)ts.tv_sec * 1000000000 + ts.tv_nsec;
+}
+
 int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int32_t* out_w,
                  double* out_a, int32_t* out_count, int64_t* out_samples, int32_t* out_iters,
                  int32_t trace_cap, int64_t* trace) {
+  return oracle_solve_timed(P, w, a, out_w, out_a, out_count, out_samples, out_iters, trace_cap, trace, NULL);
+}
+
+/* ns[0] = wall time of the solve, ns[1] = the part spent sampling f - g (Alg. 2 l.13-14); the paper's
+ * "main part" timing excludes the sampling */
+static int solve_impl(const oracle_params* P, const int32_t* w, const double* a, int32_t* out_w,
+                      double* out_a, int32_t* out_count, int64_t* out_samples, int32_t* out_iters,
+                      int32_t trace_cap, int64_t* trace, int64_t* ns, int64_t* raw_v, double* raw_a,
+                      int32_t* raw_n);
+
+int oracle_solve_timed(const oracle_params* P, const int32_t* w, const double* a, int32_t* out_w,
+                       double* out_a, int32_t* out_count, int64_t* out_samples, int32_t* out_iters,
+                       int32_t trace_cap, int64_t* trace, int64_t* ns) {
+  return solve_impl(P, w, a, out_w, out_a, out_count, out_samples, out_iters, trace_cap, trace, ns, NULL, NULL,
+                    NULL);
+}
+
+/* debugging aid: the registry R itself (reduced keys [<=k][r] and coefficients, insertion order after prunes)
+ * at the end of the loop, before the wrap */
+int oracle_solve_raw(const oracle_params* P, const int32_t* w, const double* a, int64_t* raw_v, double* raw_a,
+                     int32_t* raw_n) {
+  int32_t* ow = (int32_t*)malloc(sizeof(int32_t) * (size_t)P->k * P->d);
+  double* oa = (double*)malloc(sizeof(double) * 2 * (size_t)P->k);
+  int32_t cnt = 0;
+  int st = solve_impl(P, w, a, ow, oa, &cnt, NULL, NULL, 0, NULL, NULL, raw_v, raw_a, raw_n);
+  free(ow);
+  free(oa);
+  return st;
+}
+
+static int solve_impl(const oracle_params* P, const int32_t* w, const double* a, int32_t* out_w,
+                      double* out_a, int32_t* out_count, int64_t* out_samples, int32_t* out_iters,
+                      int32_t trace_cap, int64_t* trace, int64_t* ns, int64_t* raw_v, double* raw_a,
+                      int32_t* raw_n) {
+  const int64_t t_start = now_ns();
+  int64_t t_sampling = 0;
   const int32_t r = P->r, k = P->k, d = P->d;
   int64_t E;
   int64_t* lo = (int64_t*)malloc(sizeof(int64_t) * (size_t)r);
@@ -525,20 +582,23 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
     double* s = (double*)malloc(sizeof(double) * 2 * (size_t)p);
     /* l.11-17: sample the unshifted line and the r shifted lines, DFT each */
     for (int32_t line = 0; line <= r; ++line) {
+      const int64_t t0 = now_ns();
       oracle_sample_line(K, r, tv, tc, p, m, line - 1, E, s);
+      t_sampling += now_ns() - t0;
       oracle_dft(p, s, F + (size_t)line * 2 * p);
     }
     free(s);
     samples += (int64_t)(r + 1) * p;                          /* f evaluations only (C22) */
     /* l.18-32 */
-    int32_t ncand = 0;
-    int32_t na = oracle_decode(P, E, lo, hi, p, m, kstar, F, &ncand, acc_b, acc_v, acc_a);
+    int32_t ncand = 0, nnonempty = 0, n_accum = 0;
+    int32_t na = oracle_decode_ex(P, E, lo, hi, p, m, kstar, F, &ncand, &nnonempty, acc_b, acc_v, acc_a);
     /* l.30: R <- R u (w~, a), accumulating (C16), in ascending b */
     for (int32_t t = 0; t < na; ++t) {
       int32_t e = registry_find(&R, acc_v + (size_t)t * r);
       if (e >= 0) {
         R.a[2 * e] += acc_a[2 * t];
         R.a[2 * e + 1] += acc_a[2 * t + 1];
+        ++n_accum;
       } else {
         if (R.n >= R.cap) {   /* cannot happen with the k* cap; kept for safety */
           R.cap *= 2;
@@ -564,10 +624,12 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
       }
       ++keep;
     }
+    const int32_t n_pruned = R.n - keep;
     R.n = keep;
     if (trace && it <= trace_cap) {
-      int64_t* T = trace + (size_t)(it - 1) * 5;
+      int64_t* T = trace + (size_t)(it - 1) * ORACLE_TRACE_COLS;
       T[0] = it; T[1] = p; T[2] = m; T[3] = ncand; T[4] = na;
+      T[5] = nnonempty; T[6] = n_accum; T[7] = n_pruned;
     }
     stall = (na == 0) ? stall + 1 : 0;
     ++i;                                                        /* l.34 */
@@ -611,6 +673,11 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
     }
   }
   if (R.n == k) status = ORACLE_OK;
+  if (raw_n) {
+    *raw_n = R.n;
+    memcpy(raw_v, R.v, sizeof(int64_t) * (size_t)R.n * r);
+    memcpy(raw_a, R.a, sizeof(double) * 2 * (size_t)R.n);
+  }
 
   /* l.36: untilt (C20) and wrap back to d dimensions, then canonical order */
   int32_t* wt = (int32_t*)malloc(sizeof(int32_t) * (size_t)(R.n > 0 ? R.n : 1) * d);
@@ -643,6 +710,7 @@ int oracle_solve(const oracle_params* P, const int32_t* w, const double* a, int3
   free(u); free(idx_of); free(refs); free(wt);
   free(F); free(acc_a); free(acc_v); free(acc_b); free(tc); free(tv);
   free(R.a); free(R.v); free(vf); free(hi); free(lo); free(tbuf);
+  if (ns) { ns[0] = now_ns() - t_start; ns[1] = t_sampling; }
   return status;
 }
 
@@ -657,6 +725,7 @@ typedef struct {
   const int32_t* w; const double* a;
   int32_t* out_w; double* out_a; int32_t* out_count; int64_t* out_samples; int32_t* out_iters;
   int32_t* out_status;
+  int64_t* out_ns;
 } batch_ctx;
 
 static void* batch_worker(void* arg) {
@@ -667,10 +736,11 @@ static void* batch_worker(void* arg) {
     int32_t s = C->next++;
     pthread_mutex_unlock(&C->lock);
     if (s >= C->batch) break;
-    int st = oracle_solve(C->P, C->w + (size_t)s * k * d, C->a + (size_t)s * 2 * k,
-                          C->out_w + (size_t)s * k * d, C->out_a + (size_t)s * 2 * k,
-                          C->out_count + s, C->out_samples ? C->out_samples + s : NULL,
-                          C->out_iters ? C->out_iters + s : NULL, 0, NULL);
+    int st = oracle_solve_timed(C->P, C->w + (size_t)s * k * d, C->a + (size_t)s * 2 * k,
+                                C->out_w + (size_t)s * k * d, C->out_a + (size_t)s * 2 * k,
+                                C->out_count + s, C->out_samples ? C->out_samples + s : NULL,
+                                C->out_iters ? C->out_iters + s : NULL, 0, NULL,
+                                C->out_ns ? C->out_ns + 2 * (size_t)s : NULL);
     C->out_status[s] = st;
   }
   return NULL;
@@ -678,12 +748,12 @@ static void* batch_worker(void* arg) {
 
 int oracle_solve_batch(const oracle_params* P, int32_t batch, const int32_t* w, const double* a,
                        int32_t* out_w, double* out_a, int32_t* out_count, int64_t* out_samples,
-                       int32_t* out_iters, int32_t* out_status, int32_t n_threads) {
+                       int32_t* out_iters, int32_t* out_status, int32_t n_threads, int64_t* out_ns) {
   batch_ctx C;
   memset(&C, 0, sizeof(C));
   C.P = P; C.batch = batch; C.next = 0;
   C.w = w; C.a = a; C.out_w = out_w; C.out_a = out_a; C.out_count = out_count;
-  C.out_samples = out_samples; C.out_iters = out_iters; C.out_status = out_status;
+  C.out_samples = out_samples; C.out_iters = out_iters; C.out_status = out_status; C.out_ns = out_ns;
   pthread_mutex_init(&C.lock, NULL);
   if (n_threads < 1) n_threads = 1;
   if (n_threads > batch) n_threads = batch > 0 ? batch : 1;

@@ -94,18 +94,37 @@ void oracle_dft(int64_t p, const double* s /*[p][2]*/, double* F /*[p][2]*/);
 int32_t oracle_decode(const oracle_params* P, int64_t E, const int64_t* lo, const int64_t* hi,
                       int64_t p, int32_t m, int32_t kstar, const double* F,
                       int32_t* n_cand, int32_t* acc_b, int64_t* acc_v, double* acc_a);
+/* the same, *n_nonempty (nullable) receiving the number of bins above the floor BEFORE the k* cap */
+int32_t oracle_decode_ex(const oracle_params* P, int64_t E, const int64_t* lo, const int64_t* hi,
+                         int64_t p, int32_t m, int32_t kstar, const double* F,
+                         int32_t* n_cand, int32_t* n_nonempty, int32_t* acc_b, int64_t* acc_v, double* acc_a);
 
 /* ---- the whole of Algorithm 2 for one signal ----
  * out_w [k][d] int32 (canonical lexicographic order), out_a [k][2], out_count.
- * trace [trace_cap][5] = (i, p, m, n_candidates, n_accepted) per iteration. */
+ * trace [trace_cap][ORACLE_TRACE_COLS] per iteration = (i, p, m, n_candidates (after the k* cap),
+ * n_accepted, n_nonempty (bins above the floor before the cap), n_accumulated (accepted keys already in R,
+ * l.30 R[v] += a), n_pruned (entries removed by l.33)). */
+#define ORACLE_TRACE_COLS 8
 int oracle_solve(const oracle_params* P, const int32_t* w /*[k][d]*/, const double* a /*[k][2]*/,
                  int32_t* out_w, double* out_a, int32_t* out_count, int64_t* out_samples,
                  int32_t* out_iters, int32_t trace_cap, int64_t* trace);
 
-/* Independent signals spread over n_threads host threads (one solve per thread at a time). */
+/* The same, ns (nullable) [2] = wall ns of the solve and ns spent sampling (the "main part" of P:461-463
+ * is the difference). */
+int oracle_solve_timed(const oracle_params* P, const int32_t* w, const double* a, int32_t* out_w,
+                       double* out_a, int32_t* out_count, int64_t* out_samples, int32_t* out_iters,
+                       int32_t trace_cap, int64_t* trace, int64_t* ns);
+
+/* Debugging aid: the registry (reduced keys raw_v [<=k][r], raw_a [<=k][2], *raw_n entries) at the end of the
+ * loop, before the wrap; returns the solve status. */
+int oracle_solve_raw(const oracle_params* P, const int32_t* w, const double* a, int64_t* raw_v, double* raw_a,
+                     int32_t* raw_n);
+
+/* Independent signals spread over n_threads host threads (one solve per thread at a time).
+ * out_ns (nullable) [batch][2]: per-signal oracle_solve_timed times. */
 int oracle_solve_batch(const oracle_params* P, int32_t batch, const int32_t* w, const double* a,
                        int32_t* out_w, double* out_a, int32_t* out_count, int64_t* out_samples,
-                       int32_t* out_iters, int32_t* out_status, int32_t n_threads);
+                       int32_t* out_iters, int32_t* out_status, int32_t n_threads, int64_t* out_ns);
 
 #ifdef __cplusplus
 }

@@ -474,3 +474,75 @@ def test_stall_fallback_keeps_found_modes():
     # after the switch the first prime is the first prime >= c k* with k* = k - (modes kept), not c k
     sw = r0.trace.shape[0]
     assert r1.trace[sw, 1] == O.ith_prime_at_least(5 * (12 - r0.w.shape[0]), 1)
+
+
+# ------------------------------------------------------------------ Alg. 2 decision branches: cap, accumulate, prune
+def _cap_fixture(E):
+    """Hand-made bins of one p = 11 iteration (r = 1): singletons at b = 3, 5, 9 with |F_0| = 33, 22, 22 EXACTLY
+    (F_0 = 33, 22, 22i: the two 22s are an exact magnitude tie), shifted line F_1[b] = F_0[b] e^{2 pi i v/E}
+    (Eq. (4)) with v = 3, 5, -2 (v = b mod 11)."""
+    p = 11
+    F = np.zeros((2, p), np.complex128)
+    for b, f0, v in ((3, 33.0, 3), (5, 22.0, 5), (9, 22.0j, -2)):
+        F[0, b] = f0
+        F[1, b] = f0 * cmath.exp(2j * math.pi * v / E)
+    return p, F
+
+
+def test_select_cap_keeps_largest_ties_to_smaller_b():
+    """Alg. 2 l.18 SORT with readings C5/C6: when more than k* bins are non-empty only the k* largest
+    |F_0| are examined, ties going to the smaller b; the examined bins are then processed in ascending b.
+    Fails if the cap keeps the smallest bins, breaks ties towards the larger b, or does not bind."""
+    P = O.Params(d=1, N=16, k=3, blocks=(1,))
+    E, lo, hi = O.prepare(P)
+    p, F = _cap_fixture(E)
+    nc, acc_b, acc_v, acc_a = O.decode(P, E, lo, hi, p, 0, 3, F)
+    assert nc == 3 and acc_b.tolist() == [3, 5, 9] and acc_v[:, 0].tolist() == [3, 5, -2]
+    nc, acc_b, acc_v, acc_a = O.decode(P, E, lo, hi, p, 0, 2, F)
+    assert nc == 2 and acc_b.tolist() == [3, 5] and acc_v[:, 0].tolist() == [3, 5]    # 22 vs 22i: smaller b
+    assert abs(acc_a[0] - 3.0) < 1e-15 and abs(acc_a[1] - 2.0) < 1e-15               # a = F_0 / p (Eq. (7))
+    nc, acc_b, _, _ = O.decode(P, E, lo, hi, p, 0, 1, F)
+    assert nc == 1 and acc_b.tolist() == [3]
+    # swap the tie's phases: still the smaller b wins; make b = 9 strictly larger: it is kept instead of b = 5
+    F2 = F.copy()
+    F2[:, 9] *= (22.0 + 1e-9) / 22.0
+    _, acc_b, _, _ = O.decode(P, E, lo, hi, p, 0, 2, F2)
+    assert acc_b.tolist() == [3, 9]
+
+
+# Workloads that force false accepts (SURVEY NEXT-row pins of Alg. 2 l.30 / l.33): tau = 0.5 and round_tol = 0.5
+# let collided bins pass Eq. (42), extra_checks = 0 drops the range and bin-consistency rejections.  A false entry
+# puts a spurious mode -a' at v' into the residual; a later iteration finds it isolated, decodes v' again and the
+# accumulation R[v'] += -a' cancels it to rounding, which the prune removes.  The wrong residual also holds more
+# non-empty bins than k*, so the cap binds.  Seeds listed here are ones where the oracle ends with the exact
+# input spectrum (seeds where a false entry survives to |R| = k exist too: the method then returns a wrong set,
+# which the GPU must reproduce -- tests/test_gpu_parity.py).
+FFA_CASES = [((2, 128, 40, (1, 1)), (7, 14, 19, 26, 32)), ((3, 32, 30, (1, 1, 1)), (13, 27, 29)),
+             ((3, 16, 20, (2, 1)), (6, 7, 36))]
+FFA_PARAMS = dict(tol=0.5, round_tol=0.5, extra_checks=0, max_iter=60)
+
+
+def ffa_config(d, N, k, blocks):
+    return W.custom_config(d, N, k, blocks, cfg=81, rho="uniform1_10")
+
+
+@pytest.mark.parametrize("case,seeds", FFA_CASES)
+def test_forced_false_accepts_accumulate_prune_exact(case, seeds):
+    """Alg. 2 l.30 'R <- R u (w, a)' read as R[v] += a (C16) and l.33 prune (C17): with forced false accepts
+    the oracle still ends with the brute-force dense DFT's spectrum, and its trace shows the k* cap binding,
+    keys found again (accumulated) and entries pruned.  Replacing instead of accumulating leaves the spurious
+    entry with a non-zero coefficient (never pruned, so the set is wrong); dropping the prune keeps it too."""
+    d, N, k, blocks = case
+    c = ffa_config(d, N, k, blocks)
+    for t in seeds:
+        w, a = W.make_signal(c, t)
+        res = O.solve(O.params_for(c, **FFA_PARAMS), w, a)
+        wb, ab = _brute_force_modes(w, a, N)
+        assert res.status == O.OK, t
+        assert res.w.shape == wb.shape and np.array_equal(res.w, wb), t
+        assert np.all(np.abs(res.a - ab) <= 1e-10 * np.abs(ab)), t
+        tr = res.trace
+        assert (tr[:, 5] > tr[:, 3]).any(), t           # more non-empty bins than k*: the cap bound
+        assert (tr[:, 3] == np.minimum(tr[:, 5], k - np.concatenate([[0], np.cumsum(tr[:-1, 4] - tr[:-1, 6]
+                                                                                   - tr[:-1, 7])]))).all(), t
+        assert tr[:, 6].sum() > 0 and tr[:, 7].sum() > 0, t
