@@ -5,14 +5,16 @@ One *step* = one complete solve (all iterations of Algorithm 2
 SURVEY 8(a)) of a batch of independent synthetic signals of BASELINE.json's metric configuration
 (configs[2]: d=100, N=65536, k=1000, |a| ~ U[1,10]) -- per GPU (weak scaling over signal shards).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c1..c5]
 
-N>1 runs under torchrun (one rank per GPU, NCCL).  Rank 0 prints ONE JSON line.  The oracle
+N>1 runs one rank per GPU over NCCL: under torchrun as the driver launches it, or -- when WORLD_SIZE is unset --
+bench.py re-executes itself under torch.distributed.run with N ranks.  Rank 0 prints ONE JSON line.  The oracle
 (oracle/, test infrastructure) is executed only by the cpu_baseline leg and by --impl reference.
 """
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -67,12 +69,40 @@ def parse():
                          "solves the same signals and owns a shard of the shifted lines (strong scaling, NCCL "
                          "record all-gather per iteration, SURVEY 8(e))")
     ap.add_argument("--latency-steps", type=int, default=20, help="single-signal solves timed for latency_single_solve")
-    ap.add_argument("--table-cache", type=int, default=1024,
-                    help="per-prime table cache slots (plan option table_cache_slots; ~1 MB each): the steady state "
-                         "reuses the tables of every prime the workload visits")
+    ap.add_argument("--table-cache", type=int, default=0,
+                    help="per-prime table cache slots (plan option table_cache_slots; ~1 MB each); 0 = the plan "
+                         "default (batch + 16)")
     ap.add_argument("--expsum-path", type=int, default=0, choices=[0, 1, 2],
                     help="0 auto (int8 limbs on tcgen05 when available), 1 FP64 tensor/vector, 2 int8 limbs")
+    ap.add_argument("--fp64-steps", type=int, default=-1,
+                    help="steps of the FP64-path sub-measurement (fp64_path object; -1 = --steps, 0 = skip)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / reduction check without a GPU: gloo ranks, a fake solve (tests only)")
     return ap.parse_args()
+
+
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def maybe_self_launch(args) -> None:
+    """--gpus N > 1 without torchrun: re-execute this script under torch.distributed.run with N local ranks (one
+    per GPU), so a plain `python bench.py --gpus N` measures N GPUs.  Fails loudly when fewer GPUs are visible."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return
+    if not args.dry_run:
+        import torch
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.exit(f"bench.py: --gpus {args.gpus} but only {have} CUDA device(s) visible")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
 
 
 # ------------------------------------------------------------------ clocks (nvidia-smi during the timed region)
@@ -129,16 +159,40 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ oracle legs (CPU)
-def oracle_throughput(cfg, n_threads, trials):
-    """The oracle as it stands, one solve per host thread: recovered modes/s on this host."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def oracle_run(cfg, n_threads, n_signals):
+    """The oracle as it stands, one solve per host thread, n_signals = a multiple of n_threads (balanced rounds).
+    Returns the cpu_baseline object (value = recovered modes/s on this host) and the wall time."""
     import oracle as O
+    trials = list(range(n_signals))
     w, a = W.make_batch(cfg, trials)
     P = O.params_for(cfg)
     t = time.perf_counter()
-    status, ow, oa, cnt, samples, _ = O.solve_batch(P, w, a, n_threads=n_threads)
+    status, _, _, cnt, samples, _, ns = O.solve_batch(P, w, a, n_threads=n_threads, times=True)
     dt = time.perf_counter() - t
     assert (status == 0).all()
-    return int(cnt.sum()) / dt, dt, int(samples.sum())
+    rounds = max(1, n_signals // n_threads)
+    solve_s = ns[:, 0] / 1e9
+    main_s = (ns[:, 0] - ns[:, 1]) / 1e9
+    obj = {"value": int(cnt.sum()) / dt, "unit": "modes/s", "cores": n_threads, "kind": "oracle",
+           "sample": f"{n_signals} {cfg.name} signals (trials 0..{n_signals - 1}), {rounds} round(s) of one oracle "
+                     f"solve per host thread ({n_threads} threads), {dt:.1f} s wall",
+           "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+           "s_per_solve_single_core": float(np.mean(solve_s)),
+           "main_part_s_per_solve": float(np.mean(main_s)),
+           "main_part_note": "solve time minus the sampling of f - g (Alg. 2 l.13-14), the paper's 'CPU TICKS' "
+                             "excludes sampling (PAPER.md:461-463)",
+           "sample_evals_per_s": float(samples.sum()) / dt}
+    return obj, dt
 
 
 def run_reference(args, rank, world):
@@ -147,37 +201,83 @@ def run_reference(args, rank, world):
         return
     cfg = W.CONFIGS[args.config]
     cores = args.cpu_threads or os.cpu_count() or 1
-    # A step is one signal's solve; the steps run concurrently, one per host thread (an oracle solve of C3 takes
-    # ~20 s on one core, so K sequential rounds would not finish in minutes).  The W warm-up steps run the same
-    # way, untimed.  At least `cores` signals are timed so that every host thread works.
+    # A step is one signal's solve; the steps run concurrently, one per host thread (an oracle C3 solve takes ~20 s
+    # on one core, so K sequential rounds would not finish in minutes).  The timed signals are a whole number of
+    # rounds of `cores` solves (balanced: every thread does the same number of solves), at least K of them; the W
+    # warm-up solves run the same way, untimed.
     if args.warmup:
-        oracle_throughput(cfg, min(cores, args.warmup), list(range(args.warmup)))
-    n = max(args.steps, cores)
-    trials = list(range(n))
-    _, dt, samp = oracle_throughput(cfg, cores, trials)
-    value = n * cfg.k / dt
-    times = [dt / args.steps] * args.steps
-    sample = (f"{n} {cfg.name} signals (trials 0..{n - 1}) solved concurrently, one solve per host thread "
-              f"({cores} threads), {dt:.1f} s wall; ms_per_step = wall / steps")
-    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "modes/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+        oracle_run(cfg, min(cores, args.warmup), min(cores, args.warmup))
+    rounds = max(1, -(-args.steps // cores))
+    n = rounds * cores
+    cb, dt = oracle_run(cfg, cores, n)
+    value = cb["value"]
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "modes/s",
+            "n_gpus": world if "WORLD_SIZE" in os.environ else args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded PCG64, PAPER.md:424 recipe)",
             "config": {"workload": workload_desc(cfg), "signals_timed": n, "host_threads": cores},
-            "sample_evals_per_s": samp / sum(times),
-            "cpu_baseline": {"value": value, "unit": "modes/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "sample_evals_per_s": cb["sample_evals_per_s"],
+            "cpu_baseline": cb,
             "e2e": {"value": value, "unit": "modes/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ launcher check without a GPU
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank plumbing of our arm (launcher, barriers, max-over-ranks time, MIN of the
+    verification flags, rank-0 printing) on gloo with a fake solve of fixed duration -- no GPU, no kernels."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    ms = 1.0 + rank                                         # rank-dependent: the max over ranks must win
+    t = torch.tensor([ms * args.steps], dtype=torch.float64)
+    ok = torch.tensor([1], dtype=torch.int32)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "value": world * 1.0 / (float(t.item()) / 1e3), "unit": "modes/s",
+                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": float(t.item()) / args.steps, "dry_run": True,
+                          "verified_exact_recovery": bool(ok.item())}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ our arm
+def time_steps(S, plan, sig, outs, steps, stream, flush, barrier):
+    """K steps bracketed by barrier + synchronize, CUDA events on the plan's stream around each execute, an L2
+    flush (not timed) before each.  Returns (total ms, reports)."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    reps = []
+    barrier()
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        res = S.sfft_execute(plan, sig, outs)
+        ev[i][1].record(stream)
+        reps.append(res.report)
+    torch.cuda.synchronize()
+    barrier()
+    return sum(a.elapsed_time(b) for a, b in ev), reps
+
+
 def main():
     args = parse()
+    maybe_self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.dry_run:
+        run_dry(args, rank, world)
         return
     import torch
     import torch.distributed as dist
@@ -198,14 +298,19 @@ def main():
     a_h = torch.from_numpy(a_np).pin_memory()
     w_d, a_d = w_h.cuda(), a_h.cuda()
     stream = torch.cuda.current_stream()
-    plan = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, profile=True,
-                        expsum_path=args.expsum_path, line_shards=world if lines else 0,
-                        line_rank=rank if lines else 0, table_cache_slots=args.table_cache)
-    if lines:
-        if world > 1:
-            S.comm_init_line_shards(plan)
-        else:
-            S.sfft_comm_init(plan, 1, 0, shard_mode=1, unique_id=S.sfft_comm_unique_id())
+
+    def make_plan(path, batch=T, profile=True, shard=True):
+        p = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=batch, profile=profile, expsum_path=path,
+                        line_shards=world if (lines and shard) else 0, line_rank=rank if (lines and shard) else 0,
+                        table_cache_slots=args.table_cache)
+        if lines and shard:
+            if world > 1:
+                S.comm_init_line_shards(p)
+            else:
+                S.sfft_comm_init(p, 1, 0, shard_mode=1, unique_id=S.sfft_comm_unique_id())
+        return p
+
+    plan = make_plan(args.expsum_path)
     sig = S.sfft_signal_expsum(plan, w_d, a_d)
     outs = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32, device="cuda"),
             torch.empty((T, cfg.k, 2), dtype=torch.float64, device="cuda"),
@@ -217,49 +322,42 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ws = np.stack([W.canonical_sort(w_np[i], a_np[i])[0] for i in range(T)])
+
+    def exact(o):
+        return bool((o[3] == 0).all().item()) and np.array_equal(o[0].cpu().numpy(), ws)
+
     for _ in range(args.warmup):
         S.sfft_execute(plan, sig, outs)
     torch.cuda.synchronize()
     # correctness of what we time: the recovered spectra equal the inputs (exact recovery)
-    ok = bool((outs[3] == 0).all().item())
-    ws = np.stack([W.canonical_sort(w_np[i], a_np[i])[0] for i in range(T)])
-    ok = ok and np.array_equal(outs[0].cpu().numpy(), ws)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    reps = []
+    ok = exact(outs)
     clocks = Clocks({local_rank} if world == 1 else set(range(world))) if rank == 0 else None
-    barrier()
-    torch.cuda.synchronize()
     if clocks:
         clocks.start()
-    for i in range(args.steps):
-        flush.zero_()                                   # L2 flush between timed steps (not timed)
-        ev[i][0].record(stream)
-        res = S.sfft_execute(plan, sig, outs)
-        ev[i][1].record(stream)
-        reps.append(res.report)
-    torch.cuda.synchronize()
-    barrier()
+    ms, reps = time_steps(S, plan, sig, outs, args.steps, stream, flush, barrier)
     if clocks:
         clocks.stop()
-    ms = sum(a.elapsed_time(b) for a, b in ev)
-    t_max = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms_max = float(t_max.item())
+    ok = ok and exact(outs)
+    ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
     modes_total = mult * T * cfg.k * args.steps
     value = modes_total / (ms_max / 1e3)
-    samples = sum(r.samples_used for r in reps)
-    cmacs = sum(r.cmacs for r in reps)
-    ms_exp = sum(r.ms_expsum for r in reps)
-    ms_fft = sum(r.ms_fft for r in reps)
-    ms_dec = sum(r.ms_decode for r in reps)
-    ms_oth = sum(r.ms_other for r in reps)
-    n_exp = sum(r.n_expsum for r in reps)
-    launches = sum(r.kernel_launches for r in reps)
-    cm8 = sum(r.cmacs_i8 for r in reps)
-    ms8 = sum(r.ms_expsum_i8 for r in reps)
-    n8 = sum(r.n_expsum_i8 for r in reps)
+
+    def tot(attr):
+        return sum(getattr(r, attr) for r in reps)
+
+    samples, cmacs = tot("samples_used"), tot("cmacs")
+    ms_exp, ms_fft, ms_dec, ms_oth = tot("ms_expsum"), tot("ms_fft"), tot("ms_decode"), tot("ms_other")
+    n_exp, launches = tot("n_expsum"), tot("kernel_launches")
+    cm8, ms8, n8 = tot("cmacs_i8"), tot("ms_expsum_i8"), tot("n_expsum_i8")
+    plogp = tot("fft_plogp")
     limbs = reps[0].i8_limbs if reps else 0
     peaks, peaks_src = measured_peaks()
     traffic, traffic_kernel = None, ""
@@ -275,14 +373,14 @@ def main():
         # int8-limb tensor-core exp-sum: per complex MAC of the method, 4 real MACs of the 2K x 2L
         # real GEMM times S (S + 1) / 2 limb products, 2 ops per MAC -- unpadded rows p and columns 2L
         ops = 2.0 * 4.0 * limbs * (limbs + 1) / 2.0 * cm8
-        peak = peaks.get("bf16_tflops_sustained", 1400.0) * INT8_PER_BF16
+        peak = peaks.get("bf16_tflops", 1654.1) * INT8_PER_BF16
         achieved = ops / (ms8 / 1e3) / 1e12
         roofline = {"bound": "tensor", "kernel": f"expsum_i8 (tcgen05.mma.kind::i8, {limbs} limbs, A in TMEM)",
                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
                     "traffic": traffic if traffic is not None and "i8" in traffic_kernel else None,
                     "unit_note": "int8 tera-ops/s (MAC = 2 ops)",
-                    "peak_source": f"{peaks_src} bf16_tflops_sustained x {INT8_PER_BF16} (nominal int8:bf16 ratio, "
-                                   "B200_PROFILING.md); kernel timed inside the step",
+                    "peak_source": f"{peaks_src} bf16_tflops (burst: the kernel runs in ms-long steps at max clock, "
+                                   f"see clocks) x {INT8_PER_BF16} (nominal int8:bf16 ratio, B200_PROFILING.md)",
                     "algorithmic_ops_per_launch": ops / n8, "avg_launch_ms": ms8 / n8,
                     "fp64_equivalent": {"achieved_tflops": 8.0 * cm8 / (ms8 / 1e3) / 1e12,
                                         "fp64_peak_tflops": FP64_PEAK_TFLOPS,
@@ -299,6 +397,41 @@ def main():
                     "avg_launch_ms": ms_exp / max(n_exp, 1)}
     if roofline.get("traffic") is not None:
         roofline["traffic_note"] = "DRAM bytes of the iteration-1 launch (ncu --set full, profiles/expsum_ncu.json)"
+    fft_gbs = 32.0 * samples / (ms_fft / 1e3) / 1e9 if ms_fft > 0 else None
+    fft_tf = 5.0 * plogp / (ms_fft / 1e3) / 1e12 if ms_fft > 0 else None
+    fft_roof = {"bound": "hbm", "kernel": "pfft (Bluestein, smem-resident; fused select / test / decode epilogue)",
+                "achieved": fft_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                "frac": fft_gbs / peaks.get("hbm_gbs") if fft_gbs else None, "traffic": None,
+                "algorithmic_bytes": "32 B per sample (read s, write F) = 32 * samples_used per step",
+                "fp64": {"achieved_tflops": fft_tf, "peak_tflops": FP64_PEAK_TFLOPS,
+                         "frac": fft_tf / FP64_PEAK_TFLOPS if fft_tf else None,
+                         "algorithmic_flops": "5 p log2 p per line of length p (radix-2 convention, report fft_plogp)"}}
+
+    # FP64 path (expsum_path = 1: DMMA exp-sum) on the same workload, timed the same way (north star: the sum kernel
+    # against the FP64 peak)
+    fp64 = None
+    fp64_steps = args.steps if args.fp64_steps < 0 else args.fp64_steps
+    if fp64_steps and (n8 or args.expsum_path == 2):
+        plan64 = make_plan(1)
+        sig64 = S.sfft_signal_expsum(plan64, w_d, a_d)
+        outs64 = tuple(torch.empty_like(o) for o in outs)
+        for _ in range(args.warmup):
+            S.sfft_execute(plan64, sig64, outs64)
+        ms64, reps64 = time_steps(S, plan64, sig64, outs64, fp64_steps, stream, flush, barrier)
+        ok64 = exact(outs64)
+        ms64 = max_over_ranks(ms64)
+        cm64 = sum(r.cmacs for r in reps64)
+        mse64 = sum(r.ms_expsum for r in reps64)
+        ach64 = 8.0 * cm64 / (mse64 / 1e3) / 1e12
+        fp64 = {"value": mult * T * cfg.k * fp64_steps / (ms64 / 1e3), "unit": "modes/s",
+                "ms_per_step": ms64 / fp64_steps, "steps": fp64_steps, "verified_exact_recovery": ok64,
+                "dtype": "f64", "kernel_ms_per_step": {"expsum": mse64 / fp64_steps,
+                                                       "fft": sum(r.ms_fft for r in reps64) / fp64_steps},
+                "roofline": {"bound": "alu", "kernel": "expsum_dmma (mma.sync.m8n8k4 f64, DMMA)",
+                             "achieved": ach64, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                             "frac": ach64 / FP64_PEAK_TFLOPS,
+                             "peak_source": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz (measured DMMA 37.1)"}}
+        del plan64, sig64, outs64
 
     # e2e: the public host-buffer call, H2D of the inputs and D2H of the result inside the timed region
     hout = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32).pin_memory(),
@@ -316,10 +449,8 @@ def main():
         t = time.perf_counter()
         S.sfft_solve_host(plan, w_h, a_h, hout)
         e_ms += (time.perf_counter() - t) * 1e3
-    e_t = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-    e2e_value = mult * T * cfg.k * args.e2e_steps / (float(e_t.item()) / 1e3) if args.e2e_steps else None
+    e_ms = max_over_ranks(e_ms)
+    e2e_value = mult * T * cfg.k * args.e2e_steps / (e_ms / 1e3) if args.e2e_steps else None
     h2d = w_h.numel() * 4 + a_h.numel() * 16
     d2h = hout[0].numel() * 4 + hout[1].numel() * 8 + hout[2].numel() * 4 + hout[3].numel() * 4
     if args.e2e_steps:
@@ -333,8 +464,7 @@ def main():
     # CUDA events around each execute, median of the timed runs (not part of `value`)
     lat = None
     if args.latency_steps and not lines:
-        plan1 = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=1, expsum_path=args.expsum_path,
-                            table_cache_slots=args.table_cache)
+        plan1 = make_plan(args.expsum_path, batch=1, profile=False, shard=False)
         sig1 = S.sfft_signal_expsum(plan1, w_d[:1].contiguous(), a_d[:1].contiguous())
         outs1 = tuple(o[:1].clone() for o in outs)
         for _ in range(2):
@@ -353,30 +483,31 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = args.cpu_threads or os.cpu_count() or 1
-        v, dt, _ = oracle_throughput(cfg, cores, list(range(cores)))
-        cpu = {"value": v, "unit": "modes/s", "cores": cores, "kind": "oracle",
-               "sample": f"{cores} {cfg.name} signals (trials 0..{cores - 1}), one oracle solve per host thread, "
-                         f"{dt:.1f} s wall"}
+        cpu, _ = oracle_run(cfg, cores, cores)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "modes/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong" if lines else "weak",
-            "vs_baseline": None, "dtype": "f64",
+            "vs_baseline": None,
+            "dtype": f"int8-limb S={limbs} exp-sum + f64" if n8 else "f64",
+            "dtype_note": ("exp-sum as exact int8 x int8 -> int32 limb products on tcgen05 combined in FP64 (reading "
+                           "R22); FFT, decode, registry in FP64 / int64" if n8 else "FP64 / int64 throughout"),
             "data": "synthetic (seeded PCG64 per PAPER.md:424 recipe; no dataset exists for this metric)",
             "expsum_path": "int8 limbs on tcgen05" if n8 else "fp64",
             "config": {"workload": workload_desc(cfg),
-                       "signals_per_gpu_per_step": T, "table_cache_slots": args.table_cache,
+                       "signals_per_gpu_per_step": T,
+                       "table_cache_slots": args.table_cache or f"plan default (batch + 16 = {T + 16})",
                        "parallelism": f"line shards x{world} (NCCL record all-gather)" if lines else f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
             "sample_evals_per_s": mult * samples / (ms_max / 1e3),
             "verified_exact_recovery": ok,
             "roofline": roofline,
+            "fft_roofline": fft_roof,
+            "fp64_path": fp64,
             "kernel_ms_per_step": {"expsum": ms_exp / args.steps, "fft": ms_fft / args.steps,
                                    "decode": ms_dec / args.steps, "other": ms_oth / args.steps},
-            "fft_hbm": {"achieved_gbs": 32.0 * samples / (ms_fft / 1e3) / 1e9, "peak_gbs": peaks.get("hbm_gbs"),
-                        "note": "32 B per sample (read s, write F); Bluestein work is FP64-bound"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "modes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,

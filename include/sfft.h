@@ -106,6 +106,8 @@ typedef struct {
   float ms_expsum_i8;
   int32_t fallback_used;       /* signals that switched to a tilt level of the stall fallback (R23) */
   float ms_total;              /* when profiling: device time of the whole execute (CUDA events) */
+  double fft_plogp;            /* sum over signals and iterations of L p log2(p): the prime-length DFTs' size,
+                                  5 fft_plogp = their algorithmic flops (radix-2 convention) */
 } sfft_report;
 
 typedef struct sfft_plan_s sfft_plan_t;

@@ -338,9 +338,11 @@ int32_t oracle_decode_ex(const oracle_params* P, int64_t E, const int64_t* lo, c
                          int32_t* n_cand, int32_t* n_nonempty, int32_t* acc_b, int64_t* acc_v, double* acc_a) {
   const int32_t r = P->r;
   const double* F0 = F;
-  /* select (C5, C18): bins with |F_0[b]| >= floor * p, at most the k* largest.  The magnitude is compared as
-   * |F_0|^2 = Re^2 + Im^2, each operation rounded once (reading R5: a plain formula, so that the k* cap and
-   * its ties are decided identically by any implementation that is handed the same bins) */
+  /* select (C5, C18): bins with |F_0[b]| >= floor * p, at most the k* largest.  The magnitude is |F_0|^2 =
+   * Re^2 + Im^2, each operation rounded once, and the k* cap ranks it rounded to 36 significant bits (reading
+   * R5): the bins carry ~1e-13 relative rounding error, so magnitudes that agree to ~1.5e-11 are ties (-> the
+   * smaller b, C6) -- e.g. a false entry's bin and the collided bin it was decoded from, equal in exact
+   * arithmetic -- and any implementation decides them as exact arithmetic would */
   cand_t* cand = (cand_t*)malloc(sizeof(cand_t) * (size_t)p);
   int32_t nc = 0;
   const double floor_abs = P->bin_floor_rel * (double)p;
@@ -349,7 +351,13 @@ int32_t oracle_decode_ex(const oracle_params* P, int64_t E, const int64_t* lo, c
     const double re = F0[2 * b], im = F0[2 * b + 1];
     const double re2 = re * re, im2 = im * im;
     const double mag2 = re2 + im2;
-    if (mag2 >= floor2) { cand[nc].mag = mag2; cand[nc].b = b; ++nc; }
+    if (mag2 >= floor2) {
+      int ex;
+      const double fr = frexp(mag2, &ex);
+      cand[nc].mag = ldexp(nearbyint(ldexp(fr, 36)), ex - 36);
+      cand[nc].b = b;
+      ++nc;
+    }
   }
   if (n_nonempty) *n_nonempty = nc;
   if (nc > kstar) {

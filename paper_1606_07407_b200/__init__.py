@@ -58,7 +58,7 @@ class sfft_report(ctypes.Structure):
                 ("ms_expsum", ctypes.c_float), ("ms_fft", ctypes.c_float), ("ms_decode", ctypes.c_float),
                 ("ms_other", ctypes.c_float), ("i8_limbs", ctypes.c_int32), ("n_expsum_i8", ctypes.c_int32),
                 ("cmacs_i8", ctypes.c_int64), ("ms_expsum_i8", ctypes.c_float),
-                ("fallback_used", ctypes.c_int32), ("ms_total", ctypes.c_float)]
+                ("fallback_used", ctypes.c_int32), ("ms_total", ctypes.c_float), ("fft_plogp", ctypes.c_double)]
 
 
 class SfftError(RuntimeError):
@@ -233,13 +233,47 @@ def _coeff_view(coeffs):
     return coeffs.contiguous()
 
 
+def _require(t, name: str, shape, dtype, cuda: bool = True, pinned_ok: bool = True):
+    """Argument check of the binding (the C ABI only sees raw pointers): raises ValueError, never asserts."""
+    if t is None:
+        raise ValueError(f"{name}: missing")
+    if tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name}: shape {tuple(t.shape)}, expected {tuple(shape)}")
+    if t.dtype != dtype:
+        raise ValueError(f"{name}: dtype {t.dtype}, expected {dtype}")
+    if cuda and not t.is_cuda:
+        raise ValueError(f"{name}: must be a CUDA tensor")
+    if not cuda and t.is_cuda:
+        raise ValueError(f"{name}: must be a host tensor")
+    if not t.is_contiguous():
+        raise ValueError(f"{name}: must be contiguous")
+
+
+def _check_outs(plan, out, B: int, cuda: bool):
+    torch = _torch()
+    if len(out) != 4:
+        raise ValueError("out: expected (freqs, coeffs, count, status)")
+    of, oc, on, os_ = out
+    _require(of, "out freqs", (B, plan.k, plan.d), torch.int32, cuda)
+    if oc is not None and oc.is_complex():
+        _require(oc, "out coeffs", (B, plan.k), torch.complex128, cuda)
+    else:
+        _require(oc, "out coeffs", (B, plan.k, 2), torch.float64, cuda)
+    _require(on, "out count", (B,), torch.int32, cuda)
+    _require(os_, "out status", (B,), torch.int32, cuda)
+
+
 def sfft_signal_expsum(plan: Plan, freqs, coeffs) -> Signal:
     """f(t) = sum_j a_j e^{2 pi i omega_j . t}: freqs int32 [B,k,d] and coeffs complex128 [B,k] on the GPU."""
     torch = _torch()
-    assert freqs.is_cuda and freqs.dtype == torch.int32 and freqs.is_contiguous()
-    c = _coeff_view(coeffs)
-    assert c.is_cuda and c.dtype == torch.float64
+    if freqs.dim() != 3:
+        raise ValueError(f"freqs: expected [batch, k, d], got shape {tuple(freqs.shape)}")
     batch = freqs.shape[0]
+    if batch < 1 or batch > plan.batch:
+        raise ValueError(f"freqs: batch {batch} outside [1, plan batch {plan.batch}]")
+    _require(freqs, "freqs", (batch, plan.k, plan.d), torch.int32)
+    c = _coeff_view(coeffs)
+    _require(c, "coeffs", (batch, plan.k, 2), torch.float64)
     h = ctypes.c_void_p()
     _check(lib().sfft_signal_expsum(plan.handle, batch, ctypes.c_void_p(freqs.data_ptr()),
                                     ctypes.c_void_p(c.data_ptr()), ctypes.byref(h)), plan.handle)
@@ -265,6 +299,7 @@ def sfft_execute(plan: Plan, sig: Signal, out=None) -> Result:
                torch.empty((B, plan.k, 2), dtype=torch.float64, device="cuda"),
                torch.empty((B,), dtype=torch.int32, device="cuda"),
                torch.empty((B,), dtype=torch.int32, device="cuda"))
+    _check_outs(plan, out, B, cuda=True)
     of, oc, on, os_ = out
     rep = sfft_report()
     rc = lib().sfft_execute(plan.handle, sig.handle, ctypes.c_void_p(of.data_ptr()), ctypes.c_void_p(oc.data_ptr()),
@@ -276,13 +311,20 @@ def sfft_execute(plan: Plan, sig: Signal, out=None) -> Result:
 def sfft_solve_host(plan: Plan, freqs, coeffs, out=None) -> Result:
     """End-to-end call with HOST tensors (pinned for full speed): H2D, solve, D2H inside the library."""
     torch = _torch()
+    if freqs.dim() != 3:
+        raise ValueError(f"freqs: expected [batch, k, d], got shape {tuple(freqs.shape)}")
     B = freqs.shape[0]
+    if B < 1 or B > plan.batch:
+        raise ValueError(f"freqs: batch {B} outside [1, plan batch {plan.batch}]")
+    _require(freqs, "freqs", (B, plan.k, plan.d), torch.int32, cuda=False)
     c = coeffs if not coeffs.is_complex() else torch.view_as_real(coeffs)
+    _require(c, "coeffs", (B, plan.k, 2), torch.float64, cuda=False)
     if out is None:
         out = (torch.empty((B, plan.k, plan.d), dtype=torch.int32).pin_memory(),
                torch.empty((B, plan.k, 2), dtype=torch.float64).pin_memory(),
                torch.empty((B,), dtype=torch.int32).pin_memory(),
                torch.empty((B,), dtype=torch.int32).pin_memory())
+    _check_outs(plan, out, B, cuda=False)
     of, oc, on, os_ = out
     rep = sfft_report()
     rc = lib().sfft_solve_host(plan.handle, B, ctypes.c_void_p(freqs.data_ptr()), ctypes.c_void_p(c.data_ptr()),
@@ -296,9 +338,13 @@ def sfft_solve_host(plan: Plan, freqs, coeffs, out=None) -> Result:
 def sfft_stage_expsum(plan: Plan, v, c, p: int, m: int):
     """Lines of one iteration: v int64 [r, K], c complex128 [K] (device) -> complex128 [L, p]."""
     torch = _torch()
+    if v.dim() != 2 or v.shape[0] != plan.r:
+        raise ValueError(f"v: expected [r={plan.r}, K], got shape {tuple(v.shape)}")
     K = v.shape[1]
     v = v.contiguous()
+    _require(v, "v", (plan.r, K), torch.int64)
     cc = _coeff_view(c)
+    _require(cc, "c", (K, 2), torch.float64)
     out = torch.empty((plan.L, p, 2), dtype=torch.float64, device="cuda")
     _check(lib().sfft_stage_expsum(plan.handle, K, ctypes.c_void_p(v.data_ptr()), ctypes.c_void_p(cc.data_ptr()),
                                    p, m, ctypes.c_void_p(out.data_ptr())), plan.handle)
@@ -308,8 +354,9 @@ def sfft_stage_expsum(plan: Plan, v, c, p: int, m: int):
 def sfft_stage_pfft(plan: Plan, x):
     """In-place DFT of every row of x (complex128 [n_lines, p], device); returns x."""
     torch = _torch()
+    if x.dim() != 2 or x.dtype != torch.complex128 or not x.is_cuda or not x.is_contiguous():
+        raise ValueError("x: expected a contiguous complex128 CUDA tensor [n_lines, p]")
     xr = torch.view_as_real(x)
-    assert xr.is_contiguous()
     _check(lib().sfft_stage_pfft(plan.handle, x.shape[0], x.shape[1], ctypes.c_void_p(xr.data_ptr())), plan.handle)
     return x
 
@@ -318,6 +365,7 @@ def sfft_stage_decode(plan: Plan, F, p: int, m: int, kstar: int):
     """Select + test + decode of one iteration: F complex128 [L, p] (device).
     Returns (n_candidates, bins int32 [na], v int64 [na, r], a complex128 [na]) on the device."""
     torch = _torch()
+    _require(F.contiguous(), "F", (plan.L, p), torch.complex128)
     Fr = torch.view_as_real(F.contiguous())
     acc_b = torch.zeros(kstar, dtype=torch.int32, device="cuda")
     acc_v = torch.zeros((plan.r, kstar), dtype=torch.int64, device="cuda")

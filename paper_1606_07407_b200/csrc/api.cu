@@ -125,6 +125,7 @@ enum Buf {
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
   B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY, B_SPINERR,
+  B_FFTW,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -258,6 +259,7 @@ void layout(sfft_plan_t* P) {
   sz[B_I8B] = P->i8_ok ? i8_limb_bytes(P->i8, (int)S) : 0;
   sz[B_I8SIG] = 8 * S;
   sz[B_CMACS8] = 8 * S;
+  sz[B_FFTW] = 8 * S;
   sz[B_LVLE] = 8 * (size_t)P->n_levels;
   sz[B_LVLLO] = 8 * (size_t)P->n_levels * P->r;
   sz[B_LVLHI] = 8 * (size_t)P->n_levels * P->r;
@@ -355,6 +357,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.st_samples = ptr<int64_t>(P, B_SAMPLES);
   D.st_cmacs = ptr<int64_t>(P, B_CMACS);
   D.st_cmacs_i8 = ptr<int64_t>(P, B_CMACS8);
+  D.st_fftw = ptr<double>(P, B_FFTW);
   D.st_log = ptr<int32_t>(P, B_LOG);
   D.ctrl = ptr<int32_t>(P, B_CTRL);
   D.h_ctrl_map = P->h_ctrl_dev;
@@ -675,12 +678,14 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(P, cudaMemcpyAsync(&spin_err, D.spin_err, 4, cudaMemcpyDeviceToHost, st));
   std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
+  std::vector<double> hfw(batch);
   std::vector<int32_t> hlog(2 * kLogIters), hlvl(batch);
   if (rep) {
     CUDA_TRY(P, cudaMemcpyAsync(hlvl.data(), D.st_lvl, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hfw.data(), D.st_fftw, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
   }
   CUDA_TRY(P, cudaStreamSynchronize(st));
@@ -699,6 +704,7 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
       rep->samples_used += hsamp[s];
       rep->cmacs += hcm[s];
       rep->cmacs_i8 += hcm8[s];
+      rep->fft_plogp += hfw[s];
       rep->fallback_used += hlvl[s] > 0;
     }
     rep->i8_limbs = P->i8_ok ? P->i8.S : 0;

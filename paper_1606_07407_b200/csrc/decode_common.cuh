@@ -34,8 +34,21 @@ __device__ __forceinline__ int block_excl_scan(int v, int* scratch, int* total) 
   return before + x - v;
 }
 
-// a5 select (Alg. 2 l.18, readings R5/R6): bins b < p with |F_0[b]| >= floor_abs in ascending b; if more than
-// kstar qualify, the kstar largest |F_0| (ties -> smaller b), still ascending.  f0(b) returns F_0[b].
+// |F|^2 = Re^2 + Im^2, every operation rounded once (no contraction): the select's magnitude (reading R5), the
+// same number as the oracle's for the same bin
+__device__ __forceinline__ double mag2_rn(double2 f) {
+  return __dadd_rn(__dmul_rn(f.x, f.x), __dmul_rn(f.y, f.y));
+}
+// the k* cap's ranking key (reading R5): |F|^2 rounded to 36 significant bits (round half to even), so that
+// magnitudes equal up to the bins' rounding error are ties -> smaller b, as in the oracle
+__device__ __forceinline__ double rank_key(double mag2) {
+  int ex;
+  const double fr = frexp(mag2, &ex);
+  return ldexp(rint(ldexp(fr, 36)), ex - 36);
+}
+
+// a5 select (Alg. 2 l.18, readings R5/R6): bins b < p with |F_0[b]|^2 >= floor_abs^2 in ascending b; if more than
+// kstar qualify, the kstar largest |F_0|^2 (ties -> smaller b), still ascending.  f0(b) returns F_0[b].
 // Shared memory: cand[p], mag[p], flag[p], scratch[>= 32].  Returns the candidate count (all threads).
 // Needs ceil(nc / blockDim) <= 32 (p <= 32 blockDim).
 template <class F0>
@@ -47,16 +60,15 @@ __device__ int select_candidates(F0 f0, int p, int kstar, double floor_abs, int*
   const int per = (p + blockDim.x - 1) / blockDim.x;     // <= 32
   const int b0 = tid * per, b1 = min(p, b0 + per);
   unsigned mask = 0u;
+  const double floor2 = __dmul_rn(floor_abs, floor_abs);
   for (int b = b0; b < b1; ++b) {
-    const double2 f = f0(b);
-    if (hypot(f.x, f.y) >= floor_abs) mask |= 1u << (b - b0);
+    if (mag2_rn(f0(b)) >= floor2) mask |= 1u << (b - b0);
   }
   int pos = block_excl_scan(__popc(mask), scratch, &total);
   for (int b = b0; b < b1; ++b)
     if (mask >> (b - b0) & 1u) {
-      const double2 f = f0(b);
       cand[pos] = b;
-      mag[pos] = hypot(f.x, f.y);
+      mag[pos] = rank_key(mag2_rn(f0(b)));
       ++pos;
     }
   __syncthreads();
@@ -254,13 +266,47 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
     if (lane == 0) { found[t] = fe; hsh[t] = h; }
   }
   __syncthreads();
+  // 4a'. without the bin-consistency check (extra_checks bit 1 off) two accepted candidates of one iteration can
+  //      decode to the same key; Alg. 2 l.30 processes them in ascending b, so the first creates the entry and
+  //      the later ones accumulate into it.  A key absent from R is marked a duplicate of the FIRST earlier
+  //      accepted candidate with the same key (found = -2 - t'); so is a key of R found twice (its += a would
+  //      race in 4b).  With the check on, equal keys have equal
+  //      v_m mod p = b, so distinct candidates never collide and this pass is skipped.
+  bool any_dup = false;
+  if (!(P.extra & 2)) {
+    int dup_local = 0;
+    for (int t = tid; t < na; t += blockDim.x) {
+      int dup = -1;
+      if (found[t] >= 0) {                              // an existing key found twice: serialise its += a
+        for (int t2 = 0; t2 < t && dup < 0; ++t2)
+          if (found[t2] == found[t]) dup = t2;
+      } else {
+        const int ci = accl[t];
+        for (int t2 = 0; t2 < t && dup < 0; ++t2) {
+          if (found[t2] >= 0 || hsh[t2] != hsh[t]) continue;
+          const int c2 = accl[t2];
+          bool eq = true;
+          for (int n = 0; n < r && eq; ++n) eq = accv[(int64_t)n * P.k + c2] == accv[(int64_t)n * P.k + ci];
+          if (eq) dup = t2;
+        }
+      }
+      flag[t] = dup;
+      dup_local |= dup >= 0;
+    }
+    any_dup = __syncthreads_or(dup_local) != 0;
+    if (any_dup) {
+      for (int t = tid; t < na; t += blockDim.x)
+        if (flag[t] >= 0) found[t] = -2 - flag[t];
+      __syncthreads();
+    }
+  }
   // 4b. R[v] += a for found keys; new keys get entries nR + rank in ascending-b order (deterministic)
   int n_new;
   {
     const int per = (na + blockDim.x - 1) / blockDim.x;
     const int t0 = tid * per, t1 = min(na, t0 + per);
     int c4 = 0;
-    for (int t = t0; t < t1; ++t) c4 += found[t] < 0;
+    for (int t = t0; t < t1; ++t) c4 += found[t] == -1;
     int rank = block_excl_scan(c4, scratch, &total);
     n_new = total;
     for (int t = t0; t < t1; ++t) {
@@ -271,16 +317,30 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
         const int e = found[t];
         areg[e] = make_double2(areg[e].x + a.x, areg[e].y + a.y);
         flag[t] = 0;
-      } else {
+      } else if (found[t] == -1) {
         const int e = nR + rank++;
         areg[e] = a;
         khash[e] = hsh[t];
         found[t] = e;
         flag[t] = 1;
+      } else {
+        flag[t] = 0;                                      // duplicate: accumulated below, in ascending b
       }
     }
   }
   __syncthreads();
+  if (any_dup) {
+    if (tid == 0)
+      for (int t = 0; t < na; ++t) {
+        if (found[t] >= -1) continue;
+        const int e = found[-2 - found[t]];             // the entry its first occurrence created
+        const int ci = accl[t];
+        const double2 f0 = P.rec_f0[(int64_t)s * P.k + ci];
+        areg[e] = make_double2(areg[e].x + f0.x / (double)p, areg[e].y + f0.y / (double)p);
+        found[t] = e;
+      }
+    __syncthreads();
+  }
   // 4c. new entries: key row and hash-table insert (warp per entry with lanes along the coordinates for long
   //     keys, thread per entry otherwise)
   if (!wide) {
@@ -406,6 +466,7 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
     P.st_samples[s] += (int64_t)(r + 1) * p;              // f evaluations of all shards (reading C22)
     P.st_cmacs[s] += (int64_t)P.L * p * K;
     if (P.i8_iter) P.st_cmacs_i8[s] += (int64_t)P.L * p * K;
+    P.st_fftw[s] += (double)P.L * p * log2((double)p);
     P.st_iters[s] = iter;
     if (s == 0 && iter <= kLogIters) {
       P.st_log[2 * (iter - 1)] = p;

@@ -9,8 +9,10 @@
 // base-256 digits x_0 .. x_{S-1} (x_0 most significant, every digit in [-128, 127], |x_0| <= 127),
 // so x = sum_s x_s 256^-s / 127 up to the rounding of X.  A line coefficient component y (of a
 // signal whose largest coefficient component is sigma) is Y = rint(y / sigma * 127 * 256^(S-1)) split
-// the same way.  Every limb product x_s y_t is an exact int8 x int8 -> int32 product and the int32
-// sums over 2K operands (|sum| <= 2K * 127 * 128 < 2^31 for K < 65000) are exact, so
+// the same way.  Every limb product x_s y_t is an exact int8 x int8 -> int32 product.  Accumulator w
+// sums the w + 1 <= S limb pairs (s, w - s) over the 2K real operands, |Acc_w| <= S * 2K * 128 * 128,
+// so the int32 sums are exact while S * 2K * 2^14 < 2^31, i.e. K < 10922 terms at S = 6 (13107 at
+// S = 5); i8_configure refuses larger k (the FP64 path runs, or expsum_path = 2 gets ENOTSUP).  Then
 //
 //   s = sigma / 127^2 * sum_{w < S} 256^-w * Acc_w,   Acc_w = sum_{s + t = w} sum_j x_s(h, j) y_t(j, n)
 //
@@ -534,10 +536,10 @@ __global__ void __launch_bounds__(kI8Threads, 1) expsum_i8_kernel(DevParams P, I
 }
 
 // ------------------------------------------------------------------ host side
-// Limb count from the decode budget: the int8 path keeps |x - round(x)| of the
-// Eq. (41) decode below ~1e-3 and coefficient errors below ~1e-11 relative.
+// Limb count (reading R22): S = 6 keeps every sample within the stage-parity bar 1e-12 sum |c| of
+// SURVEY 4 layer 5 (measured; S = 5 missed it for short lines, K = 6: 8e-12 vs 6e-12) and coefficient errors
+// ~1e-14 relative; FP64 roots cannot feed more than E = 2^36 (the Eq. (41) decode then needs the FP64 path).
 int i8_limbs_for(int64_t E) {
-  if (E <= ((int64_t)1 << 28)) return 5;
   if (E <= ((int64_t)1 << 36)) return 6;
   return 0;   // beyond what FP64 roots can feed: use the FP64 tensor (DMMA) path
 }
@@ -550,6 +552,8 @@ bool i8_configure(int L, int64_t E, int k, I8Config* out) {
   I8Config c{};
   c.S = i8_limbs_for(E);
   if (c.S == 0 || getenv("SFFT_NO_I8")) return false;
+  // exact int32 accumulation (header): S * 2K * 2^14 < 2^31 for the K = k signal terms of a line
+  if ((int64_t)c.S * 2 * k * 16384 >= ((int64_t)1 << 31)) return false;
   const int N2 = 2 * L;
   // very few lines (2L <= 16): one N = 16 MMA per limb product is mostly padding and the A generation
   // dominates; the FP64 kernels are faster there (measured on C2, L = 3) unless forced (expsum_path = 2)

@@ -60,3 +60,12 @@ def test_our_arm_line_shards_c3_world1():
               "--latency-steps", "0", "--no-cpu-baseline", "--batch", "4"])
     assert d["scaling"] == "strong" and d["verified_exact_recovery"] is True
     assert "line shards x1" in d["config"]["parallelism"]
+
+
+def test_self_launch_dry_run_world2():
+    """`python bench.py --gpus 2` without torchrun re-executes itself under torch.distributed.run with two ranks
+    (here on gloo with a fake solve, --dry-run): one JSON line from rank 0, n_gpus = 2, the time the max over
+    ranks (rank r fakes 1 + r ms per step)."""
+    d = _run(["--dry-run", "--gpus", "2", "--steps", "3", "--warmup", "1"], timeout=300)
+    assert d["n_gpus"] == 2 and d["dry_run"] is True and d["verified_exact_recovery"] is True
+    assert abs(d["ms_per_step"] - 2.0) < 1e-9

@@ -58,19 +58,20 @@ def test_stage_expsum_vs_oracle(S, name, blocks, p, m, path):
                               torch.from_numpy(cc).cuda(), p, m).cpu().numpy()
     r = len(blocks)
     scale = np.abs(cc).sum()
+    bar = 1e-12 * scale                        # SURVEY 4 layer 5: relative error <= 1e-12 against sum |c|
+    bound = bar
     if path == 2:
-        # int8 limbs: every root / coefficient component is held to 256^-S (rounding of the fixed-point
-        # value, <= 1.008 * 256^-S, plus the dropped limb products of weight >= S, <= (S + 1) * 256^-S)
-        # relative to 1 / sigma; 4 real products per complex term -> a worst-case bound per sample
-        nl = 5 if E <= 2 ** 28 else 6
+        # int8 limbs (R22): the worst case per sample is K * 4 * (S + 3) * 256^-S * sigma (rounding of every
+        # fixed-point root / coefficient component, <= 1.008 * 256^-S, plus the dropped limb products of weight
+        # >= S, <= (S + 1) * 256^-S, relative to sigma; 4 real products per complex term).  Documented, and
+        # checked; the measured error must also meet the survey's bar.
+        nl = 6                                 # i8_limbs_for: S = 6 for every E <= 2^36
         sigma = np.abs(np.concatenate([cc.real, cc.imag])).max()
         bound = len(cc) * 4 * (nl + 3) * 256.0 ** -nl * sigma
-    else:
-        bound = 1e-12 * scale
     for n in [-1] + list(range(r)):
         ref = O.sample_line(vv, cc, p, m, n, E)
         err = np.abs(got[n + 1] - ref).max()
-        assert err <= bound, (n, err, bound)
+        assert err <= bar and err <= bound, (n, err, bar, bound)
 
 
 @pytest.mark.parametrize("p", [2, 3, 5, 7, 11, 23, 101, 503, 1009, 2503, 5003])
@@ -145,6 +146,12 @@ def test_stage_project_vs_oracle(S, name, blocks, tilts):
 
 
 # ------------------------------------------------------------------ end-to-end parity
+def _coef_ok(got, ref):
+    """North star: coefficients within 1e-9 relative, per element (|a_j| >= 1e-8 after the prune, C17)."""
+    got, ref = np.asarray(got), np.asarray(ref)
+    return got.shape == ref.shape and bool(np.all(np.abs(got - ref) <= 1e-9 * np.abs(ref)))
+
+
 def _check_against_oracle(res, i, ref_w, ref_a, ref_status=O.OK):
     st = int(res.per_status[i])
     assert st == ref_status, (i, st)
@@ -153,7 +160,7 @@ def _check_against_oracle(res, i, ref_w, ref_a, ref_status=O.OK):
     ga = res.coeffs[i, :n].cpu().numpy()
     assert n == ref_w.shape[0] and np.array_equal(gw, ref_w), i
     if n:
-        assert np.abs(ga - ref_a).max() <= 1e-9 * np.abs(ref_a).max(), i
+        assert _coef_ok(ga, ref_a), i
 
 
 @pytest.mark.parametrize("blocks", [(1, 1), (2,)])
@@ -199,7 +206,7 @@ def test_e2e_full_size_vs_golden_oracle(S, name, tag, trials):
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ga = res.coeffs[i, :n].cpu().numpy()
         ra = g[key + "_a"]
-        assert np.abs(ga - ra).max() <= 1e-9 * np.abs(ra).max(), key
+        assert _coef_ok(ga, ra), key
         ws, _ = W.canonical_sort(w[i], a[i])
         assert np.array_equal(gw, ws)                         # exact recovery of the input
     # iteration trace of signal 0 and the total sample count
@@ -333,7 +340,7 @@ def test_e2e_poisoned_workspace(S, name, trials):
         gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ra = g[key + "_a"]
-        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+        assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), ra), key
 
 
 @pytest.mark.parametrize("name,trials", [("c2", range(8)), ("c3", range(2)), ("c5", range(2))])
@@ -356,7 +363,7 @@ def test_e2e_literal_residual_mode(S, name, trials):
             gw = np.ascontiguousarray(r.freqs[i, :n].cpu().numpy())
             assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), (key, lit)
             ra = g[key + "_a"]
-            assert np.abs(r.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), (key, lit)
+            assert _coef_ok(r.coeffs[i, :n].cpu().numpy(), ra), (key, lit)
     assert np.array_equal(res[True][0], res[False][0]) and res[True][3:] == res[False][3:]
     assert np.abs(res[True][1] - res[False][1]).max() <= 1e-12 * np.abs(res[True][1]).max()
 
@@ -397,7 +404,7 @@ def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trial
         assert n == ref.w.shape[0]
         assert np.array_equal(res.freqs[i, :n].cpu().numpy(), ref.w), i
         if n:
-            assert np.abs(res.coeffs[i, :n].cpu().numpy() - ref.a).max() <= 1e-9 * np.abs(ref.a).max()
+            assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), ref.a)
         if n_fb and ref.status == O.OK:
             wc, _ = W.canonical_sort(w[i], a[i])
             assert np.array_equal(ref.w, wc)
@@ -421,7 +428,7 @@ def _opt_in_parity(env_var, cases):
             "        k = 'primary_%d' % t; n = int(res.count[i])\n"
             "        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())\n"
             "        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[k + '_w_sha256'])\n"
-            "        ra = g[k + '_a']; assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max()\n"
+            "        ra = g[k + '_a']; assert np.all(np.abs(res.coeffs[i, :n].cpu().numpy() - ra) <= 1e-9 * np.abs(ra))\n"
             "print('opt-in ok')\n")
     env = dict(os.environ, **{env_var: "1"})
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
@@ -478,7 +485,7 @@ def test_e2e_line_shards_group_vs_golden_oracle(S, name, tag, trials, G, path):
         gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ra = g[key + "_a"]
-        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+        assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), ra), key
     tr = g[f"{tag}_{trials[0]}_trace"]
     rep = res.report
     assert [rep.primes[i] for i in range(min(len(tr), 64))] == tr[:64, 1].tolist()
@@ -525,7 +532,7 @@ def test_e2e_line_shard_nccl_world1(S):
         gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ra = g[key + "_a"]
-        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+        assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), ra), key
 
 
 def test_line_shard_plan_errors(S):
@@ -576,7 +583,7 @@ def test_e2e_line_shards_literal_residual(S, name, trials, G):
         gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
         assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
         ra = g[key + "_a"]
-        assert np.abs(res.coeffs[i, :n].cpu().numpy() - ra).max() <= 1e-9 * np.abs(ra).max(), key
+        assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), ra), key
 
 
 @pytest.mark.parametrize("path", [0, 1])
@@ -613,3 +620,74 @@ def test_e2e_degenerate_zero_coefficients(S):
     assert int(res.per_status[0]) == O.PARTIAL and int(res.count[0]) == 37
     assert int(res.per_status[1]) == O.PARTIAL and int(res.count[1]) == 0
     assert int(res.per_status[2]) == O.OK
+
+
+# ------------------------------------------------------------------ Alg. 2 decision branches: cap, accumulate, prune
+def test_stage_decode_cap_binds(S):
+    """a5 with the k* cap binding (Alg. 2 l.18, readings C5/C6): the hand-made exact-tie fixture of the oracle
+    pins (keep the k* largest |F_0|, ties -> smaller b) and DFT bins of a real iteration with k* below the number
+    of non-empty bins; candidates, accepted bins, coordinates and coefficients equal the oracle's."""
+    from test_oracle_pins import _cap_fixture
+    P = O.Params(d=1, N=16, k=3, blocks=(1,))
+    E, lo, hi = O.prepare(P)
+    p, F = _cap_fixture(E)
+    plan = S.sfft_plan(1, 16, 3, blocks=(1,))
+    for kstar in (3, 2, 1):
+        nc, ob, ov, oa = O.decode(P, E, lo, hi, p, 0, kstar, F)
+        gnc, gb, gv, ga = S.sfft_stage_decode(plan, torch.from_numpy(F).cuda(), p, 0, kstar)
+        assert gnc == nc and np.array_equal(gb.cpu().numpy(), ob) and np.array_equal(gv.cpu().numpy(), ov)
+        assert np.array_equal(ga.cpu().numpy(), oa)
+    c = W.CONFIGS["c2"]
+    w, a = W.make_signal(c, 0)
+    Pc = O.params_for(c)
+    E, lo, hi = O.prepare(Pc)
+    v = O.project(Pc, w)
+    p, m = 503, 1
+    F = np.stack([O.dft(O.sample_line(v, a, p, m, n, E)) for n in [-1, 0, 1]])
+    nonempty = int((np.abs(F[0]) >= 1e-8 * p).sum())
+    plan = _plan(S, c)
+    for kstar in (nonempty // 2, nonempty - 1, 7):
+        nc, ob, ov, oa = O.decode(Pc, E, lo, hi, p, m, kstar, F)
+        assert nc == kstar < nonempty
+        gnc, gb, gv, ga = S.sfft_stage_decode(plan, torch.from_numpy(F).cuda(), p, m, kstar)
+        assert gnc == nc and np.array_equal(gb.cpu().numpy(), ob) and np.array_equal(gv.cpu().numpy(), ov)
+        assert np.all(np.abs(ga.cpu().numpy() - oa) <= 1e-15 * np.abs(oa))
+
+
+@pytest.mark.parametrize("ci", range(3))
+@pytest.mark.parametrize("extra", [0, 1, 2])
+@pytest.mark.parametrize("path", [1, 2])
+def test_e2e_forced_false_accepts_vs_oracle(S, ci, extra, path):
+    """Alg. 2 l.30 accumulate (C16), l.33 prune (C17) and the k* cap (C5/C6) end to end: tau = 0.5, round_tol
+    = 0.5 and the bin-consistency check off force false accepts (the oracle pins' workloads, 40 seeds each,
+    including seeds that end PARTIAL, ECORRUPT or with a wrong set).  Per signal: status, set bit-exact,
+    coefficients per element within 1e-9 relative, sample count; trace of signal 0."""
+    from test_oracle_pins import FFA_CASES, FFA_PARAMS, ffa_config
+    (d, N, k, blocks), _ = FFA_CASES[ci]
+    c = ffa_config(d, N, k, blocks)
+    trials = list(range(40))
+    w, a = W.make_batch(c, trials)
+    kw = dict(FFA_PARAMS, extra_checks=extra)
+    plan = _plan(S, c, batch=len(trials), expsum_path=path, **kw)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    P = O.params_for(c, **kw)
+    st, ow, oa, cnt, samples, _ = O.solve_batch(P, w, a)
+    n_acc = n_pr = 0
+    for i in trials:
+        assert int(res.per_status[i]) == int(st[i]), (i, int(res.per_status[i]), int(st[i]))
+        if st[i] == O.ECORRUPT:
+            continue                                      # wrap failed on both sides: no output defined
+        n = int(res.count[i])
+        assert n == int(cnt[i]), i
+        assert np.array_equal(res.freqs[i, :n].cpu().numpy(), ow[i, :n]), i
+        assert np.all(np.abs(res.coeffs[i, :n].cpu().numpy() - oa[i, :n]) <= 1e-9 * np.abs(oa[i, :n])), i
+    assert res.report.samples_used == int(samples.sum())
+    ref0 = O.solve(P, w[0], a[0])
+    nl = min(len(ref0.trace), 64)
+    assert [res.report.primes[j] for j in range(nl)] == ref0.trace[:nl, 1].tolist()
+    assert [res.report.accepted[j] for j in range(nl)] == ref0.trace[:nl, 4].tolist()
+    for i in trials[:12]:
+        tr = O.solve(P, w[i], a[i]).trace
+        n_acc += int(tr[:, 6].sum())
+        n_pr += int(tr[:, 7].sum())
+    assert n_acc > 0 and n_pr > 0                          # the branches ran

@@ -510,14 +510,14 @@ def test_select_cap_keeps_largest_ties_to_smaller_b():
     assert acc_b.tolist() == [3, 9]
 
 
-# Workloads that force false accepts (SURVEY NEXT-row pins of Alg. 2 l.30 / l.33): tau = 0.5 and round_tol = 0.5
-# let collided bins pass Eq. (42), extra_checks = 0 drops the range and bin-consistency rejections.  A false entry
+# Workloads that force false accepts (pins of Alg. 2 l.30 / l.33): tau = 0.5 and round_tol = 0.5 let collided bins
+# pass Eq. (42), extra_checks = 0 drops the range and bin-consistency rejections (2: bin consistency only).  A false entry
 # puts a spurious mode -a' at v' into the residual; a later iteration finds it isolated, decodes v' again and the
 # accumulation R[v'] += -a' cancels it to rounding, which the prune removes.  The wrong residual also holds more
 # non-empty bins than k*, so the cap binds.  Seeds listed here are ones where the oracle ends with the exact
 # input spectrum (seeds where a false entry survives to |R| = k exist too: the method then returns a wrong set,
 # which the GPU must reproduce -- tests/test_gpu_parity.py).
-FFA_CASES = [((2, 128, 40, (1, 1)), (7, 14, 19, 26, 32)), ((3, 32, 30, (1, 1, 1)), (13, 27, 29)),
+FFA_CASES = [((2, 128, 40, (1, 1)), (2, 7, 26, 32)), ((3, 32, 30, (1, 1, 1)), (13, 28, 29)),
              ((3, 16, 20, (2, 1)), (6, 7, 36))]
 FFA_PARAMS = dict(tol=0.5, round_tol=0.5, extra_checks=0, max_iter=60)
 
@@ -526,8 +526,9 @@ def ffa_config(d, N, k, blocks):
     return W.custom_config(d, N, k, blocks, cfg=81, rho="uniform1_10")
 
 
+@pytest.mark.parametrize("extra", [0, 2])
 @pytest.mark.parametrize("case,seeds", FFA_CASES)
-def test_forced_false_accepts_accumulate_prune_exact(case, seeds):
+def test_forced_false_accepts_accumulate_prune_exact(case, seeds, extra):
     """Alg. 2 l.30 'R <- R u (w, a)' read as R[v] += a (C16) and l.33 prune (C17): with forced false accepts
     the oracle still ends with the brute-force dense DFT's spectrum, and its trace shows the k* cap binding,
     keys found again (accumulated) and entries pruned.  Replacing instead of accumulating leaves the spurious
@@ -536,7 +537,7 @@ def test_forced_false_accepts_accumulate_prune_exact(case, seeds):
     c = ffa_config(d, N, k, blocks)
     for t in seeds:
         w, a = W.make_signal(c, t)
-        res = O.solve(O.params_for(c, **FFA_PARAMS), w, a)
+        res = O.solve(O.params_for(c, **dict(FFA_PARAMS, extra_checks=extra)), w, a)
         wb, ab = _brute_force_modes(w, a, N)
         assert res.status == O.OK, t
         assert res.w.shape == wb.shape and np.array_equal(res.w, wb), t
