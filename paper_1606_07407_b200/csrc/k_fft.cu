@@ -844,12 +844,12 @@ __device__ void fused_select(const DevParams& P, int s, int p, double2* x, const
 // line-n CTA (n >= 1 local line): after the line-0 CTA of the signal published, test + decode (a6) every
 // candidate on this line: F_n[b] = chirp[b] conv[b] + registry bins, Eq. (42) ratio and Eq. (41) decode;
 // a pass writes v into the record, a failure clears the candidate's flag (benign race: all writers store 0)
+__device__ __forceinline__ void fused_test_wait(const DevParams& P, int s) {
+  if (threadIdx.x == 0) wait_stamp(P.sel_ready + s, P.it_epoch, P.spin_err, 256);
+  __syncthreads();
+}
 __device__ void fused_test(const DevParams& P, int s, int p, int n, const double2* x, const double2* __restrict__ ch) {
   const int tid = threadIdx.x;
-  if (tid == 0) {
-    wait_stamp(P.sel_ready + s, P.it_epoch, P.spin_err, 256);
-  }
-  __syncthreads();
   const int nR = P.st_nR[s];
   const bool resid = !P.literal && nR > 0;
   const double pd = (double)p;
@@ -993,9 +993,15 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   fft_dit<BIG>(P, x, fi, tb, 1, p);                   // only F[b], b < p, is used
   FFT_PROF_MARK(3);
   if (P.fuse_decode) {
-    if (n == 0) fused_select(P, s, p, x, ch, line);
-    else fused_test(P, s, p, n, x, ch);
-    FFT_PROF_MARK(4);
+    if (n == 0) {
+      fused_select(P, s, p, x, ch, line);
+      FFT_PROF_MARK(4);
+    } else {
+      fused_test_wait(P, s);
+      FFT_PROF_MARK(5);
+      fused_test(P, s, p, n, x, ch);
+      FFT_PROF_MARK(6);
+    }
     if (P.fuse_commit) {
       // the last of the signal's n_lines CTAs to arrive commits it (a7): every thread fences its record
       // writes, thread 0 counts the arrival; the last one resets the counter for the next iteration

@@ -1,0 +1,7 @@
+# FFT phase cycle counters (SFFT_FFT_PROF tuning build) for C3 / C4 / C5
+cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
+TAG=${1:-r2f}
+python paper_1606_07407_b200/build.py --out=paper_1606_07407_b200/libsfft_prof.so -DSFFT_FFT_PROF > gpurun_out/${TAG}_build.log 2>&1
+for c in "c3 1" c3 "c4 1" c4 c5 c2; do
+  PYTHONPATH=. SFFT_LIB_PATH=paper_1606_07407_b200/libsfft_prof.so timeout 300 python tools/fft_phases_solve.py $c >> gpurun_out/${TAG}_phases.log 2>&1
+done

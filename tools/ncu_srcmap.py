@@ -14,13 +14,16 @@ import subprocess
 import sys
 
 
-def ncu_rows(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
+def ncu_rows(rep, kernel=None):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv"]
+    if kernel:
+        cmd += ["--kernel-name", "regex:" + re.escape(kernel.split("<")[0])]
+    out = subprocess.run(cmd, capture_output=True, text=True).stdout
     r = csv.reader(out.splitlines())
     next(r)
     hdr = next(r)
     iw, isrc = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
-    return [(int(x[iw]), x[isrc]) for x in r]
+    return [(int(x[iw]) if x[iw] else 0, x[isrc]) for x in r if len(x) > max(iw, isrc)]
 
 
 def sass_lines(cubin, kernel):
@@ -50,7 +53,7 @@ def sass_lines(cubin, kernel):
 def main():
     rep, cubin, kernel = sys.argv[1:4]
     top = int(sys.argv[4]) if len(sys.argv) > 4 else 30
-    rows = ncu_rows(rep)
+    rows = ncu_rows(rep, sys.argv[5] if len(sys.argv) > 5 else kernel)   # argv[5]: function-name filter for ncu
     fn, ins = sass_lines(cubin, kernel)
     if len(ins) != len(rows):
         print(f"warning: {len(rows)} ncu rows vs {len(ins)} disassembled instructions ({fn})")
