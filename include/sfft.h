@@ -70,10 +70,13 @@ typedef struct {
   int32_t expsum_path;        /* exp-sum arithmetic: 0 auto, 1 FP64 (DMMA / DFMA), 2 exact int8-limb products on
                                  the tcgen05 tensor cores combined in FP64 (needs
                                  literal_residual = 0 and E <= 2^36) [0: int8 limbs when available] */
-  int32_t fallback_tilts;     /* stall fallback (Algorithm 3; reading R23): after stall_limit
-                                 zero-accept iterations switch to the next of up to 4 tilt levels -- Pythagorean
-                                 triples (3,4,5), (5,12,13), (8,15,17), (7,24,25) on disjoint reduced-axis pairs --
-                                 keeping the modes found (mapped exactly); 0 = stop with PARTIAL [0] */
+  int32_t fallback_tilts;     /* stall fallback (Algorithm 3; readings R23 / R24): after
+                                 stall_limit zero-accept iterations switch to the next of up to 67 tilt levels --
+                                 levels 1-4: Pythagorean triples (3,4,5), (5,12,13), (8,15,17), (7,24,25) on
+                                 fixed disjoint reduced-axis pairs; levels 5..: the rounds of a round robin over a
+                                 seeded order of the axes (every pair tilted once after r - 1 rounds) -- keeping the
+                                 modes found (mapped exactly); 0 = stop with PARTIAL; values past the last
+                                 non-empty level are clamped [0] */
   int32_t line_shards;        /* line sharding: 0 = this plan holds every line [0]; G >= 1 = the
                                  plan is shard line_rank of G: it computes line 0 and the shifted lines of reduced
                                  axes [lo, hi) (contiguous, sizes differ by at most one, shard 0 the largest), and

@@ -80,6 +80,8 @@ def lib():
         L.oracle_decode.restype = i32
         L.oracle_fallback_tilts.argtypes = [i32, i32, vp]
         L.oracle_fallback_tilts.restype = i32
+        L.oracle_axis_order.argtypes = [i32, i32, vp]
+        L.oracle_axis_order.restype = None
         L.oracle_solve.argtypes = [ctypes.POINTER(_Params), vp, vp, vp, vp, vp, vp, vp, i32, vp]
         L.oracle_solve_raw.argtypes = [ctypes.POINTER(_Params), vp, vp, vp, vp, vp]
         L.oracle_solve_batch.argtypes = [ctypes.POINTER(_Params), i32, vp, vp, vp, vp, vp, vp, vp,
@@ -198,8 +200,18 @@ def ith_prime_at_least(x: int, i: int = 1) -> int:
 
 
 # ---------------------------------------------------------------- plan quantities
+MAX_FALLBACK = 67   # ORACLE_MAX_FALLBACK
+
+
+def axis_order(r: int, seed: int = 1):
+    """Seeded axis order of the round-robin fallback levels (reading R24)."""
+    pi = np.zeros(max(r, 1), np.int32)
+    lib().oracle_axis_order(r, seed, _p(pi))
+    return pi[:r].tolist()
+
+
 def fallback_tilts(r: int, level: int):
-    """Tilts of stall-fallback level `level` >= 1 (reading R23): list of (axis0, axis1, base, height, hypo)."""
+    """Tilts of stall-fallback level `level` >= 1 (readings R23 / R24): list of (axis0, axis1, base, height, hypo)."""
     out = np.zeros((max(r // 2, 1), 5), np.int64)
     n = lib().oracle_fallback_tilts(r, level, _p(out))
     return [tuple(int(x) for x in row) for row in out[:n]]

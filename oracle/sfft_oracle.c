@@ -438,8 +438,48 @@ static int row_cmp(const void* x, const void* y) {
 
 static const int64_t kFallbackTriples[4][3] = {{3, 4, 5}, {5, 12, 13}, {8, 15, 17}, {7, 24, 25}};
 
+static uint64_t splitmix64_fin(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+void oracle_axis_order(int32_t r, int32_t seed, int32_t* pi) {
+  for (int32_t i = 0; i < r; ++i) pi[i] = i;
+  for (int32_t i = r - 1; i >= 1; --i) {
+    const uint64_t c = (uint64_t)seed * 0x9E3779B97F4A7C15ULL + (uint64_t)(r - i) * 0xD1B54A32D192ED03ULL;
+    const int32_t j = (int32_t)(splitmix64_fin(c) % (uint64_t)(i + 1));
+    const int32_t t = pi[i];
+    pi[i] = pi[j];
+    pi[j] = t;
+  }
+}
+
 int32_t oracle_fallback_tilts(int32_t r, int32_t lvl, int64_t* out) {
-  if (lvl < 1 || lvl > 4) return 0;
+  if (lvl < 1 || lvl > ORACLE_MAX_FALLBACK) return 0;
+  if (lvl > 4) {
+    /* R24: "randomizing the order of the dimensions", applied to the axes the tilt pairs up: the rounds of
+     * a round robin over a seeded order of the axes, every pair tilted once over n - 1 levels */
+    const int32_t j = lvl - 5;
+    const int32_t n = r + (r & 1);
+    if (r < 2 || j >= n - 1) return 0;
+    const int64_t* T = kFallbackTriples[j % 4];
+    int32_t* pi = (int32_t*)malloc(sizeof(int32_t) * (size_t)r);
+    int32_t* a = (int32_t*)malloc(sizeof(int32_t) * (size_t)n);
+    oracle_axis_order(r, 1, pi);
+    a[0] = 0;
+    for (int32_t i = 1; i < n; ++i) a[i] = 1 + (i - 1 + j) % (n - 1);   /* slots 1..n-1 rotated by j */
+    int32_t cnt = 0;
+    for (int32_t i = 0; i < n / 2; ++i) {
+      const int32_t x = a[i], y = a[n - 1 - i];
+      if (x >= r || y >= r) continue;                                  /* the padding slot of an odd r */
+      int64_t* o = out + 5 * cnt++;
+      o[0] = pi[x]; o[1] = pi[y]; o[2] = T[0]; o[3] = T[1]; o[4] = T[2];
+    }
+    free(a);
+    free(pi);
+    return cnt;
+  }
   const int64_t* T = kFallbackTriples[lvl - 1];
   /* disjoint pairs (q, q + s): level 1 s = 1 from axis 0, level 2 s = 1 from axis 1 (r >= 3), level 3 s = 2,
    * level 4 s = 3 -- for r <= 4 every axis pair is tilted at some level ("randomizing the order
@@ -649,7 +689,7 @@ static int solve_impl(const oracle_params* P, const int32_t* w, const double* a,
       oracle_params Ln;
       int64_t* tn = (int64_t*)malloc(sizeof(int64_t) * 5 * (size_t)(r / 2 + 1));
       int64_t En;
-      if (lvl + 1 > P->n_fallback || lvl + 1 > 4 || !level_params(P, lvl + 1, &Ln, tn) ||
+      if (lvl + 1 > P->n_fallback || lvl + 1 > ORACLE_MAX_FALLBACK || !level_params(P, lvl + 1, &Ln, tn) ||
           oracle_prepare(&Ln, &En, lo, hi) != ORACLE_OK) {
         free(tn);
         break;

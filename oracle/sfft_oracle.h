@@ -41,14 +41,25 @@ typedef struct {
   int32_t extra_checks;      /* bit0 range check, bit1 bin consistency (C15) */
   int32_t n_primes;          /* explicit prime schedule p_i = primes[(i-1) mod n] */
   const int64_t* primes;     /* NULL -> i-th prime >= max(2, c k*) (Alg. 2 l.8) */
-  int32_t n_fallback;        /* stall fallback (reading R23): up to 4 tilt levels, Pythagorean triples
-                                (3,4,5), (5,12,13), (8,15,17), (7,24,25) on disjoint reduced-axis pairs */
+  int32_t n_fallback;        /* stall fallback (readings R23 / R24): up to ORACLE_MAX_FALLBACK levels;
+                                1-4 tilt fixed axis pairs with the Pythagorean triples (3,4,5), (5,12,13),
+                                (8,15,17), (7,24,25); 5.. tilt the pairs of a seeded random order of the axes */
 } oracle_params;
 
-/* Tilts of fallback level lvl in 1..4 (reading R23): triple lvl-1 of the schedule on disjoint reduced-axis
- * pairs (q, q + s): level 1 (0,1),(2,3),...; level 2 (1,2),(3,4),... (r >= 3); level 3 stride 2 (0,2),(1,3),
- * (4,6),...; level 4 stride 3.  Writes out [r/2][5]; returns the number of tilts (0 when r < 2). */
+#define ORACLE_MAX_FALLBACK 67
+
+/* Tilts of fallback level lvl in 1..ORACLE_MAX_FALLBACK (readings R23 / R24).  Levels 1-4: triple lvl-1 on the
+ * disjoint reduced-axis pairs (q, q + s): level 1 (0,1),(2,3),...; level 2 (1,2),(3,4),... (r >= 3); level 3
+ * stride 2 (0,2),(1,3),(4,6),...; level 4 stride 3.  Levels 5.. ("randomizing the order of the dimensions",
+ * P:293, reading R24): round j = lvl - 5 of the circle-method round robin over the seeded axis order
+ * pi = oracle_axis_order(r, 1) -- n = r rounded up to even slots, slot 0 fixed, slots 1..n-1 rotated by j, pairs
+ * (a[i], a[n-1-i]) for i < n/2 mapped through pi (a pair with the padding slot is skipped) -- with triple j mod 4:
+ * the n - 1 rounds tilt every pair of axes exactly once.  Writes out [r/2][5]; returns the number of tilts (0 when
+ * r < 2 or the level is past the last round). */
 int32_t oracle_fallback_tilts(int32_t r, int32_t lvl, int64_t* out);
+/* The seeded axis order: Fisher-Yates from i = r-1 down to 1, j = z_i mod (i + 1), with z_i = the splitmix64
+ * finaliser of the counter c_i = seed * 0x9E3779B97F4A7C15 + (r - i) * 0xD1B54A32D192ED03 (mod 2^64). */
+void oracle_axis_order(int32_t r, int32_t seed, int32_t* pi);
 
 enum { ORACLE_OK = 0, ORACLE_PARTIAL = 1, ORACLE_EINVAL = -1, ORACLE_EPRECISION = -2,
        ORACLE_ECORRUPT = -4, ORACLE_ENOMEM = -6 };

@@ -806,7 +806,7 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->literal = opt->literal_residual != 0;
     P->expsum_path = opt->expsum_path;
     if (P->expsum_path < 0 || P->expsum_path > 2) return SFFT_EINVAL;
-    if (opt->fallback_tilts < 0 || opt->fallback_tilts > 4) return SFFT_EINVAL;
+    if (opt->fallback_tilts < 0 || opt->fallback_tilts > kMaxFallbackLevels) return SFFT_EINVAL;
     if (opt->table_cache_slots < 0 || opt->table_cache_slots > (1 << 16)) return SFFT_EINVAL;
     if (opt->line_shards < 0 || (opt->line_shards > 0 && (opt->line_rank < 0 || opt->line_rank >= opt->line_shards)))
       return SFFT_EINVAL;
@@ -893,21 +893,44 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   for (int q = 0; q < P->r; ++q)
     if (2 * P->hi[q] >= P->E || -2 * P->lo[q] > P->E) return SFFT_EINVAL;
   if (P->stall_limit <= 0) P->stall_limit = std::max(2 * P->r, 16);
-  // fallback levels (reading R23): level 0 = this plan; level l >= 1 = Pythagorean triple l-1 on the disjoint
+  // fallback levels: level 0 = this plan; level l in 1..4 (reading R23) = Pythagorean triple l-1 on the disjoint
   // reduced-axis pairs (q, q + s) -- s = 1 from axis 0 (l = 1), s = 1 from axis 1 (l = 2, r >= 3), s = 2 (l = 3),
-  // s = 3 (l = 4) -- with E = 2 B (base + height) (reading R2); the schedule stops at the first empty level
+  // s = 3 (l = 4); level l >= 5 (reading R24, "randomizing the order of the dimensions") = round l - 5 of
+  // the circle-method round robin over a seeded order of the axes, triple (l - 5) mod 4, so that the r - 1 (r
+  // even) rounds tilt every pair of axes once; E = 2 B (base + height) (reading R2); the schedule stops at the
+  // first empty level
   {
     static const int64_t kTri[4][3] = {{3, 4, 5}, {5, 12, 13}, {8, 15, 17}, {7, 24, 25}};
     const int n_fb = opt ? opt->fallback_tilts : 0;
     std::vector<std::vector<int64_t>> lt(1, P->tilts);
     std::vector<int64_t> lE(1, P->E);
+    // seeded axis order (Fisher-Yates driven by a splitmix64 counter; reading R24)
+    std::vector<int> order(P->r);
+    for (int i = 0; i < P->r; ++i) order[i] = i;
+    for (int i = P->r - 1; i >= 1; --i) {
+      uint64_t z = 1ull * 0x9E3779B97F4A7C15ull + (uint64_t)(P->r - i) * 0xD1B54A32D192ED03ull;
+      z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+      z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+      z ^= z >> 31;
+      std::swap(order[i], order[(int)(z % (uint64_t)(i + 1))]);
+    }
     for (int l = 1; l <= n_fb; ++l) {
-      const int64_t* T = kTri[l - 1];
-      const int st = l <= 2 ? 1 : l - 1;
-      const int off = (l == 2 && P->r >= 3) ? 1 : 0;
+      const int64_t* T = kTri[l <= 4 ? l - 1 : (l - 5) % 4];
       std::vector<int64_t> ts;
-      for (int b = off; b < P->r; b += 2 * st)
-        for (int i = 0; i < st && b + i + st < P->r; ++i) ts.insert(ts.end(), {b + i, b + i + st, T[0], T[1], T[2]});
+      if (l <= 4) {
+        const int st = l <= 2 ? 1 : l - 1;
+        const int off = (l == 2 && P->r >= 3) ? 1 : 0;
+        for (int b = off; b < P->r; b += 2 * st)
+          for (int i = 0; i < st && b + i + st < P->r; ++i) ts.insert(ts.end(), {b + i, b + i + st, T[0], T[1], T[2]});
+      } else {
+        const int j = l - 5, n = P->r + (P->r & 1);       // round j over n slots (one padding slot when r is odd)
+        if (j < n - 1)
+          for (int i = 0; i < n / 2; ++i) {
+            const int x = i == 0 ? 0 : 1 + (i - 1 + j) % (n - 1);
+            const int y = 1 + (n - 2 - i + j) % (n - 1);    // slot n-1-i after the rotation
+            if (x < P->r && y < P->r) ts.insert(ts.end(), {order[x], order[y], T[0], T[1], T[2]});
+          }
+      }
       if (ts.empty()) break;
       const int64_t El = 2 * B * (T[0] + T[1]);
       if (El > ((int64_t)1 << 42)) break;

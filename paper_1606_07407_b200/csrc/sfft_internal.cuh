@@ -20,6 +20,7 @@ enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK,
 constexpr int kMaxFftPasses = 24;
 constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
+constexpr int kMaxFallbackLevels = 67;   // sfft_options.fallback_tilts: 4 fixed-stride tilt levels + 63 round-robin rounds
 
 // Everything a kernel needs, passed by value (kernel parameter space).
 struct DevParams {

@@ -372,7 +372,8 @@ def test_e2e_literal_residual_mode(S, name, trials):
 @pytest.mark.parametrize("d,N,k,blocks,structure,n_fb,trials", [
     (2, 16, 8, (1, 1), "rectangles", 4, 12), (2, 64, 12, (1, 1), "rect_mix", 1, 12),
     (3, 16, 16, (1, 1, 1), "rect_mix", 4, 8), (4, 16, 8, (1, 1, 1, 1), "rectangles", 4, 8),
-    (4, 8, 8, (2, 2), "rect_mix", 2, 8), (2, 16, 8, (1, 1), "rectangles", 0, 4)])
+    (4, 8, 8, (2, 2), "rect_mix", 2, 8), (2, 16, 8, (1, 1), "rectangles", 0, 4),
+    (8, 16, 8, (1,) * 8, "rect_far", 67, 4), (20, 4096, 16, (1,) * 20, "rect_far", 67, 2)])
 @pytest.mark.parametrize("path", [0, 1])
 def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trials, path):
     """Worst-case rectangles stall; the tilt fallback (Alg. 3 after a stall) recovers them.
@@ -411,7 +412,7 @@ def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trial
     assert res.report.samples_used == samples
     if n_fb == 0:
         assert res.report.fallback_used == 0
-    elif structure == "rectangles":                       # rectangles never resolve untilted
+    elif structure in ("rectangles", "rect_far"):         # rectangles never resolve untilted
         assert 0 < res.report.fallback_used <= len(used)
 
 

@@ -547,3 +547,43 @@ def test_forced_false_accepts_accumulate_prune_exact(case, seeds, extra):
         assert (tr[:, 3] == np.minimum(tr[:, 5], k - np.concatenate([[0], np.cumsum(tr[:-1, 4] - tr[:-1, 6]
                                                                                    - tr[:-1, 7])]))).all(), t
         assert tr[:, 6].sum() > 0 and tr[:, 7].sum() > 0, t
+
+
+# ------------------------------------------------------------------ randomized axis order (reading R24)
+def test_round_robin_levels_cover_every_axis_pair():
+    """Levels 5.. tilt the pairs of the circle-method round robin over a seeded axis order: disjoint pairs per
+    level, r - 1 rounds (r even; r for odd r), every pair of axes exactly once, then the schedule ends."""
+    for r in range(2, 11):
+        pi = O.axis_order(r)
+        assert sorted(pi) == list(range(r))
+        n = r + (r & 1)
+        seen = []
+        for j in range(n - 1):
+            ts = O.fallback_tilts(r, 5 + j)
+            axes = [x for t in ts for x in t[:2]]
+            assert len(axes) == len(set(axes)) and len(ts) == r // 2
+            tri = [(3, 4, 5), (5, 12, 13), (8, 15, 17), (7, 24, 25)][j % 4]
+            assert all(tuple(t[2:]) == tri for t in ts)
+            seen += [tuple(sorted(t[:2])) for t in ts]
+        assert sorted(seen) == [(i, j) for i in range(r) for j in range(i + 1, r)]
+        assert O.fallback_tilts(r, 5 + n - 1) == []
+
+
+@pytest.mark.parametrize("d,N,k,seeds,brute", [(6, 8, 8, range(3), True), (8, 16, 8, range(3), False),
+                                                (20, 16, 8, range(2), False)])
+def test_far_apart_rectangles_need_the_round_robin(d, N, k, seeds, brute):
+    """Rectangles on axes at least 4 apart are never tilted by the fixed-stride levels 1-4: the solve stalls
+    through them and ends PARTIAL; with the round-robin levels some level tilts their pair and the solve
+    recovers the input spectrum exactly -- for d = 6, N = 8 also the brute-force dense DFT's."""
+    c = W.custom_config(d, N, k, (1,) * d, cfg=85, structure="rect_far")
+    for t in seeds:
+        w, a = W.make_signal(c, t)
+        r4 = O.solve(O.params_for(c, n_fallback=4), w, a)
+        assert r4.status == O.PARTIAL, t
+        rr = O.solve(O.params_for(c, n_fallback=O.MAX_FALLBACK), w, a)
+        ws, as_ = W.canonical_sort(w, a)
+        assert rr.status == O.OK and np.array_equal(rr.w, ws), t
+        assert np.all(np.abs(rr.a - as_) <= 1e-12 * np.abs(as_)), t
+        if brute:
+            wb, ab = _brute_force_modes(w, a, N)
+            assert np.array_equal(rr.w, wb) and np.all(np.abs(rr.a - ab) <= 1e-10 * np.abs(ab))

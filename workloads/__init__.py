@@ -18,7 +18,8 @@ Recipe (DESIGN.md "Input recipe"):
     base vector ~ integers(-N/2, N/2, d), an axis alpha ~ integers(0, d) and
     k/G distinct values on that axis (choice(N, k/G, replace=False) - N/2).
   * "rectangles" (SURVEY NEXT #2, P:119 / P:213): axis-aligned 2x2 rectangles
-    in a random pair of coordinates, the paper's worst case.
+    in a random pair of coordinates, the paper's worst case; "rect_far": the same
+    with the two coordinates at least 4 axes apart.
 
 Arrays: omega int32 [k, d] (C-contiguous), a complex128 [k].
 """
@@ -116,13 +117,16 @@ def _collinear_rows(rng: np.random.Generator, N: int, k: int, d: int, groups: in
     return w
 
 
-def _rectangle_rows(rng: np.random.Generator, N: int, k: int, d: int) -> np.ndarray:
-    """k/4 axis-aligned rectangles: 4 modes sharing all but two coordinates."""
+def _rectangle_rows(rng: np.random.Generator, N: int, k: int, d: int, min_gap: int = 0) -> np.ndarray:
+    """k/4 axis-aligned rectangles: 4 modes sharing all but two coordinates; min_gap > 0: the two
+    coordinates are at least min_gap axes apart (pairs the fixed-stride tilt levels never tilt)."""
     assert k % 4 == 0 and d >= 2
     rows = []
     for _ in range(k // 4):
         base = rng.integers(-N // 2, N // 2, size=d, dtype=np.int64)
         i, j = rng.choice(d, size=2, replace=False)
+        while min_gap and abs(int(i) - int(j)) < min_gap:
+            i, j = rng.choice(d, size=2, replace=False)
         xi = rng.choice(N, size=2, replace=False) - N // 2
         xj = rng.choice(N, size=2, replace=False) - N // 2
         for a in xi:
@@ -162,6 +166,8 @@ def make_signal(c: Config, trial: int = 0, seed: Optional[int] = None) -> Tuple[
         w = _rectangle_rows(rng, c.N, c.k, c.d)
     elif c.structure == "rect_mix":
         w = _rect_mix_rows(rng, c.N, c.k, c.d)
+    elif c.structure == "rect_far":
+        w = _rectangle_rows(rng, c.N, c.k, c.d, min_gap=4)
     else:
         raise ValueError(c.structure)
     theta = rng.random(c.k)
@@ -191,11 +197,3 @@ def canonical_sort(w: np.ndarray, a: np.ndarray) -> Tuple[np.ndarray, np.ndarray
         return w, a
     order = np.lexsort(w.T[::-1])
     return w[order], a[order]
-
-
-def shard_trials(n_trials: int, world: int, rank: int) -> List[int]:
-    """Contiguous block of trial indices owned by `rank` (signal sharding)."""
-    per = (n_trials + world - 1) // world
-    lo = min(n_trials, rank * per)
-    hi = min(n_trials, lo + per)
-    return list(range(lo, hi))
