@@ -70,8 +70,8 @@ def parse():
                          "record all-gather per iteration, SURVEY 8(e))")
     ap.add_argument("--latency-steps", type=int, default=20, help="single-signal solves timed for latency_single_solve")
     ap.add_argument("--table-cache", type=int, default=0,
-                    help="per-prime table cache slots (plan option table_cache_slots; ~1 MB each); 0 = the plan "
-                         "default (batch + 16)")
+                    help="per-prime table cache slots (plan option table_cache_slots; ~0.8 MB each); 0 = the plan "
+                         "default max(batch + 16, 512)")
     ap.add_argument("--expsum-path", type=int, default=0, choices=[0, 1, 2],
                     help="0 auto (int8 limbs on tcgen05 when available), 1 FP64 tensor/vector, 2 int8 limbs")
     ap.add_argument("--fp64-steps", type=int, default=-1,
@@ -310,7 +310,9 @@ def main():
                 S.sfft_comm_init(p, 1, 0, shard_mode=1, unique_id=S.sfft_comm_unique_id())
         return p
 
-    plan = make_plan(args.expsum_path)
+    # the timed plan runs without per-kernel events (they cost ~30 us per iteration: C5's 72 iterations lose 14 %);
+    # a second, profiled plan on the same signals gives the per-kernel-class times of the roofline
+    plan = make_plan(args.expsum_path, profile=False)
     sig = S.sfft_signal_expsum(plan, w_d, a_d)
     outs = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32, device="cuda"),
             torch.empty((T, cfg.k, 2), dtype=torch.float64, device="cuda"),
@@ -342,10 +344,19 @@ def main():
     clocks = Clocks({local_rank} if world == 1 else set(range(world))) if rank == 0 else None
     if clocks:
         clocks.start()
-    ms, reps = time_steps(S, plan, sig, outs, args.steps, stream, flush, barrier)
+    ms, reps_timed = time_steps(S, plan, sig, outs, args.steps, stream, flush, barrier)
     if clocks:
         clocks.stop()
     ok = ok and exact(outs)
+    # kernel-class breakdown (profile = 1: CUDA events around every kernel class on the plan's stream), same steps
+    plan_prof = make_plan(args.expsum_path, profile=True)
+    sig_prof = S.sfft_signal_expsum(plan_prof, w_d, a_d)
+    outs_prof = tuple(torch.empty_like(o) for o in outs)
+    for _ in range(args.warmup):
+        S.sfft_execute(plan_prof, sig_prof, outs_prof)
+    ms_prof, reps = time_steps(S, plan_prof, sig_prof, outs_prof, args.steps, stream, flush, barrier)
+    ok = ok and exact(outs_prof)
+    del plan_prof, sig_prof, outs_prof
     ms_max = max_over_ranks(ms)
     ms_step = ms_max / args.steps
     modes_total = mult * T * cfg.k * args.steps
@@ -356,7 +367,8 @@ def main():
 
     samples, cmacs = tot("samples_used"), tot("cmacs")
     ms_exp, ms_fft, ms_dec, ms_oth = tot("ms_expsum"), tot("ms_fft"), tot("ms_decode"), tot("ms_other")
-    n_exp, launches = tot("n_expsum"), tot("kernel_launches")
+    n_exp = tot("n_expsum")
+    launches = sum(r.kernel_launches for r in reps_timed)      # our kernels inside the timed region
     cm8, ms8, n8 = tot("cmacs_i8"), tot("ms_expsum_i8"), tot("n_expsum_i8")
     plogp = tot("fft_plogp")
     limbs = reps[0].i8_limbs if reps else 0
@@ -499,7 +511,7 @@ def main():
             "expsum_path": "int8 limbs on tcgen05" if n8 else "fp64",
             "config": {"workload": workload_desc(cfg),
                        "signals_per_gpu_per_step": T,
-                       "table_cache_slots": args.table_cache or f"plan default (batch + 16 = {T + 16})",
+                       "table_cache_slots": args.table_cache or f"plan default max(batch + 16, 512) = {max(T + 16, 512)}",
                        "parallelism": f"line shards x{world} (NCCL record all-gather)" if lines else f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
             "sample_evals_per_s": mult * samples / (ms_max / 1e3),
@@ -508,7 +520,10 @@ def main():
             "fft_roofline": fft_roof,
             "fp64_path": fp64,
             "kernel_ms_per_step": {"expsum": ms_exp / args.steps, "fft": ms_fft / args.steps,
-                                   "decode": ms_dec / args.steps, "other": ms_oth / args.steps},
+                                   "decode": ms_dec / args.steps, "other": ms_oth / args.steps,
+                                   "profiled_step": ms_prof / args.steps,
+                                   "note": "per-kernel-class CUDA events of a profiled plan (same signals, same steps); "
+                                           "ms_per_step / value come from an unprofiled plan"},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "modes/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,

@@ -85,7 +85,16 @@ typedef struct {
   int32_t line_rank;          /* shard index of this plan, 0 <= line_rank < line_shards [0] */
   int32_t table_cache_slots;  /* per-prime table cache capacity (W_p roots, Bluestein chirp and kernel spectrum,
                                  int8 root limbs: ~1 MB each, they depend on p only and are kept across iterations
-                                 and executes, least recently used evicted); 0 -> batch + 16, the minimum [0] */
+                                 and executes, least recently used evicted); 0 -> max(batch + 16, 512); n > 0 ->
+                                 max(batch + 16, n) (batch + 16 is the minimum: every live prime has a slot) [0] */
+  int32_t line_exchange;      /* how line shards exchange their per-candidate records every iteration: 0 = an
+                                 all-gather after the FFT (ncclAllGather through sfft_comm_init, device copies in
+                                 sfft_execute_group); 1 = fused into the FFT epilogue: every record word is stored
+                                 straight into the receive buffer of every shard (peer memory over NVLink: CUDA IPC
+                                 mappings from sfft_comm_peer_handle / sfft_comm_init_peers, plain pointers in
+                                 sfft_execute_group) and per-(shard, line, signal) stamps released at system scope
+                                 tell the commit that a shard's lines are in -- no separate collective.  At most 8
+                                 shards [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */
@@ -220,6 +229,18 @@ SFFT_API int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int
  * else the system one); without it the call fails with SFFT_ENCCL.  All ranks must call it together
  * (ncclCommInitRank is collective).  The communicator is destroyed with the plan.
  */
+/*
+ * Fused record exchange (sfft_options.line_exchange = 1) across processes / GPUs of one node:
+ *   sfft_comm_peer_handle -- allocates this shard's exchange buffer (receive records [line_shards][batch][words]
+ *                            + stamps; cudaMalloc, owned by the plan) and writes its cudaIpcMemHandle_t (64 bytes)
+ *                            to out (host)
+ *   sfft_comm_init_peers  -- collective over the line shards: handles = host [nranks][64] bytes of every rank's
+ *                            handle (all-gathered by the caller, e.g. torch.distributed); opens the peers' buffers
+ *                            (cudaIpcOpenMemHandle) so that this plan's FFT epilogue stores into them.  nranks =
+ *                            line_shards, rank = line_rank; one rank (nranks = 1) uses its own buffer.
+ */
+SFFT_API int sfft_comm_peer_handle(sfft_plan_t* plan, void* out);
+SFFT_API int sfft_comm_init_peers(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* handles);
 SFFT_API int sfft_comm_init(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* nccl_unique_id,
                    int32_t shard_mode);
 /* Reduced axes [lo, hi) of line shard g of G over r axes (host, no device needed): contiguous, sizes

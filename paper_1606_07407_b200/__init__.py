@@ -26,7 +26,7 @@ EXPORTS = (
     "sfft_plan_destroy", "sfft_signal_expsum", "sfft_signal_destroy", "sfft_execute",
     "sfft_solve_host", "sfft_stage_expsum", "sfft_stage_pfft", "sfft_stage_decode",
     "sfft_stage_project", "sfft_comm_init", "sfft_comm_unique_id", "sfft_execute_group",
-    "sfft_line_shard_range", "sfft_strerror",
+    "sfft_line_shard_range", "sfft_comm_peer_handle", "sfft_comm_init_peers", "sfft_strerror",
     "sfft_last_error", "sfft_version",
 )
 
@@ -45,7 +45,8 @@ class sfft_options(ctypes.Structure):
                 ("stream", ctypes.c_void_p), ("profile", ctypes.c_int32),
                 ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32),
                 ("fallback_tilts", ctypes.c_int32), ("line_shards", ctypes.c_int32),
-                ("line_rank", ctypes.c_int32), ("table_cache_slots", ctypes.c_int32)]
+                ("line_rank", ctypes.c_int32), ("table_cache_slots", ctypes.c_int32),
+                ("line_exchange", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -96,6 +97,8 @@ def lib() -> ctypes.CDLL:
         L.sfft_stage_project.argtypes = [vp, vp, vp]
         L.sfft_comm_init.argtypes = [vp, i32, i32, vp, i32]
         L.sfft_comm_unique_id.argtypes = [vp]
+        L.sfft_comm_peer_handle.argtypes = [vp, vp]
+        L.sfft_comm_init_peers.argtypes = [vp, i32, i32, vp]
         L.sfft_line_shard_range.argtypes = [i32, i32, i32, vp, vp]
         L.sfft_execute_group.argtypes = [vp, vp, i32, vp, vp, vp, vp, vp]
         L.sfft_strerror.argtypes = [ctypes.c_int]
@@ -170,7 +173,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
               stream=None, profile: bool = False, literal_residual: bool = False,
               expsum_path: int = 0, fallback_tilts: int = 0, line_shards: int = 0, line_rank: int = 0,
-              table_cache_slots: int = 0) -> Plan:
+              table_cache_slots: int = 0, line_exchange: int = 0) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -190,6 +193,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.fallback_tilts = int(fallback_tilts)
     opt.line_shards, opt.line_rank = int(line_shards), int(line_rank)
     opt.table_cache_slots = int(table_cache_slots)
+    opt.line_exchange = int(line_exchange)
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)
@@ -426,11 +430,40 @@ def sfft_execute_group(plans: Sequence[Plan], sigs: Sequence[Signal], out=None) 
     return Result(rc, of, torch.view_as_complex(oc), on, os_, rep)
 
 
-def comm_init_line_shards(plan: Plan, group=None) -> None:
-    """Line sharding over a torch.distributed group: rank 0 draws the NCCL id, the group broadcasts it
-    (broadcast_object_list), every rank initialises the plan's communicator (collective)."""
+def sfft_comm_peer_handle(plan: Plan) -> bytes:
+    """64-byte CUDA IPC handle of this shard's record-exchange buffer (plans with line_exchange = 1)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(lib().sfft_comm_peer_handle(plan.handle, buf), plan.handle)
+    return buf.raw
+
+
+def sfft_comm_init_peers(plan: Plan, nranks: int, rank: int, handles: Sequence[bytes]) -> int:
+    """Open the other shards' exchange buffers (collective over the line shards; handles of all ranks in rank
+    order, 64 bytes each)."""
+    if len(handles) != nranks or any(len(h) != 64 for h in handles):
+        raise ValueError("handles: one 64-byte handle per rank")
+    blob = ctypes.create_string_buffer(b"".join(handles), 64 * nranks)
+    return _check(lib().sfft_comm_init_peers(plan.handle, nranks, rank, blob), plan.handle)
+
+
+def exchange_handles(local: bytes, group=None) -> list:
+    """All-gather one opaque byte string per rank over a torch.distributed group (CPU-testable with gloo)."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, local, group=group)
+    return out
+
+
+def comm_init_line_shards(plan: Plan, group=None, exchange: int = 0) -> None:
+    """Line sharding over a torch.distributed group.  exchange 0: rank 0 draws the NCCL id, the group broadcasts it
+    (broadcast_object_list), every rank initialises the plan's communicator (collective).  exchange 1 (plans with
+    line_exchange = 1): the ranks all-gather the CUDA IPC handles of their exchange buffers and open each other's,
+    so the FFT epilogue stores the records into every shard's memory directly."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if exchange == 1:
+        sfft_comm_init_peers(plan, world, rank, exchange_handles(sfft_comm_peer_handle(plan), group))
+        return
     obj = [sfft_comm_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0, group=group)
     sfft_comm_init(plan, world, rank, shard_mode=1, unique_id=obj[0])

@@ -112,6 +112,15 @@ struct sfft_plan_s {
   int32_t line_G = 0, line_g = 0, line_lo = 0, L_ref = 0;
   int32_t rec_words = 0, rec_fw = 0;
   void* nccl_comm = nullptr;   // ncclComm_t of sfft_comm_init (shard_mode 1)
+  // fused record exchange (line_exchange = 1): this shard's buffer (receive records [G][batch][rec_words] + stamps
+  // [G][L_ref][batch]) and the G shards' buffers as mapped here (own one included)
+  int32_t line_exchange = 0;
+  void* peer_buf = nullptr;
+  size_t peer_bytes = 0, peer_stamp_off = 0;
+  std::vector<void*> peer_ptr;
+  std::vector<bool> peer_opened;   // opened with cudaIpcOpenMemHandle (closed at destroy)
+  bool peer_ready = false;
+  int32_t peer_epoch = 0;
   cudaEvent_t ev_ctrl = nullptr;   // the per-iteration control read (iter_setup)
 };
 
@@ -406,6 +415,18 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.rec_fw = P->rec_fw;
   D.rec_send = ptr<int64_t>(P, B_RSEND);
   D.rec_recv = P->line_G > 0 ? ptr<int64_t>(P, B_RRECV) : ptr<int64_t>(P, B_RSEND);   // unsharded: own records
+  D.L_ref = P->L_ref;
+  D.peer_mode = 0;
+  if (P->line_exchange == 1 && P->peer_ready) {
+    D.peer_mode = 1;
+    D.peer_epoch = P->peer_epoch;
+    D.rec_recv = static_cast<int64_t*>(P->peer_buf);
+    D.stamp_local = reinterpret_cast<int32_t*>(static_cast<char*>(P->peer_buf) + P->peer_stamp_off);
+    for (int h = 0; h < P->line_G; ++h) {
+      D.peer_recv[h] = static_cast<int64_t*>(P->peer_ptr[h]);
+      D.peer_stamp[h] = reinterpret_cast<int32_t*>(static_cast<char*>(P->peer_ptr[h]) + P->peer_stamp_off);
+    }
+  }
   D.rec_cand = ptr<int32_t>(P, B_RCAND);
   D.rec_nc = ptr<int32_t>(P, B_RNC);
   D.rec_f0 = ptr<double2>(P, B_RF0);
@@ -413,6 +434,21 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.bin_start = ptr<int32_t>(P, B_BINST);
   D.bin_order = ptr<int32_t>(P, B_BINORD);
   return D;
+}
+
+// the fused exchange's buffer of this shard (cudaMalloc'ed separately from the workspace so that it can be shared
+// through a CUDA IPC handle): receive records [G][batch][rec_words] int64, then stamps [G][L_ref][batch] int32
+int ensure_peer_buf(sfft_plan_t* P) {
+  if (P->peer_buf) return SFFT_OK;
+  CUDA_TRY(P, cudaSetDevice(P->device));
+  const size_t rec = 8 * (size_t)P->line_G * P->batch * (size_t)P->rec_words;
+  P->peer_stamp_off = align_up(rec, 256);
+  P->peer_bytes = P->peer_stamp_off + 4 * (size_t)P->line_G * P->L_ref * (size_t)P->batch;
+  cudaError_t e = cudaMalloc(&P->peer_buf, P->peer_bytes);
+  if (e != cudaSuccess) return fail(P, SFFT_ENOMEM, "cudaMalloc(%zu) for the record exchange: %s", P->peer_bytes,
+                                    cudaGetErrorString(e));
+  CUDA_TRY(P, cudaMemset(P->peer_buf, 0, P->peer_bytes));   // stamps 0: the exchange epochs start at 1
+  return SFFT_OK;
 }
 
 int ensure_ready(sfft_plan_t* P) {
@@ -645,6 +681,7 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   D.fuse_commit = it.fuse_commit ? 1 : 0;
   D.cur_iter = iter;
   D.i8_iter = it.use_i8 ? 1 : 0;
+  if (D.peer_mode) D.peer_epoch = ++P->peer_epoch;   // the same sequence on every shard (one per iteration)
   LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto, (int64_t)it.n_active * P->L), it.big, it.ksplit,
                         ptr<double2>(P, B_PART), it.max_p, st));
   D.lines_log = 0;
@@ -812,6 +849,9 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
       return SFFT_EINVAL;
     P->line_G = opt->line_shards;
     P->line_g = opt->line_shards > 0 ? opt->line_rank : 0;
+    if (opt->line_exchange < 0 || opt->line_exchange > 1) return SFFT_EINVAL;
+    if (opt->line_exchange == 1 && (opt->line_shards < 1 || opt->line_shards > kMaxPeers)) return SFFT_EINVAL;
+    P->line_exchange = opt->line_exchange;
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -1045,8 +1085,11 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   if (8 * (size_t)P->p_stride + 4 * (2 * (size_t)P->p_stride + 2 * (size_t)k + 64) > (size_t)smem_optin)
     return SFFT_ENOTSUP;
   if (8 * (size_t)k > (size_t)smem_optin) return SFFT_ENOTSUP;
-  P->n_tslots = P->batch + 16;    // at most batch primes are live per iteration; the rest keeps recent primes
-  if (opt && opt->table_cache_slots > P->n_tslots) P->n_tslots = opt->table_cache_slots;
+  // at most batch primes are live per iteration; the rest keeps recent primes, so that repeated executes (and later
+  // iterations revisiting a prime) reuse their tables -- like FFT twiddle tables, they depend on p only (~0.8 MB
+  // per slot at p_cap ~ 7056)
+  P->n_tslots = std::max(P->batch + 16, kDefaultTableSlots);
+  if (opt && opt->table_cache_slots > 0) P->n_tslots = std::max(P->batch + 16, (int)opt->table_cache_slots);
   layout(P.get());
   *out = P.release();
   return SFFT_OK;
@@ -1080,6 +1123,9 @@ int sfft_plan_info(const sfft_plan_t* plan, int64_t* E, int32_t* r, int32_t* L, 
 void sfft_plan_destroy(sfft_plan_t* plan) {
   if (!plan) return;
   if (plan->nccl_comm && nccl_api().ok) nccl_api().comm_destroy(plan->nccl_comm);
+  for (size_t h = 0; h < plan->peer_opened.size(); ++h)
+    if (plan->peer_opened[h] && plan->peer_ptr[h]) cudaIpcCloseMemHandle(plan->peer_ptr[h]);
+  if (plan->peer_buf) cudaFree(plan->peer_buf);
   if (plan->ws_owned && plan->ws) cudaFree(plan->ws);
   if (plan->h_ctrl) cudaFreeHost(plan->h_ctrl);
   if (plan->ev_ctrl) cudaEventDestroy(plan->ev_ctrl);
@@ -1106,7 +1152,9 @@ void sfft_signal_destroy(sfft_signal_t* sig) { delete sig; }
 int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs, double* out_coeffs,
                  int32_t* out_count, int32_t* out_status, sfft_report* rep) {
   if (!plan || !sig || sig->plan != plan || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
-  if (plan->line_G > 1 && !plan->nccl_comm)
+  if (plan->line_exchange == 1 && !plan->peer_ready)
+    return fail(plan, SFFT_EINVAL, "fused record exchange needs sfft_comm_init_peers or sfft_execute_group");
+  if (plan->line_exchange == 0 && plan->line_G > 1 && !plan->nccl_comm)
     return fail(plan, SFFT_EINVAL, "line-sharded plan (%d shards) needs sfft_comm_init or sfft_execute_group", plan->line_G);
   int rc = ensure_ready(plan);
   if (rc) return rc;
@@ -1140,7 +1188,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     if (P->profile) it_marks.push_back(n_ev);
     mark();
     if ((rc = iter_front(P, D, iter, it, launches, mark))) return rc;
-    if (P->line_G > 0) {
+    if (P->line_G > 0 && !D.peer_mode) {
       // line sharding: all-gather of this shard's records (one rank: a device copy), then the commit
       const size_t words = (size_t)batch * P->rec_words;
       if (P->nccl_comm) {
@@ -1220,6 +1268,23 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
   }
   cudaStream_t st = P0->stream;
   const int32_t batch = sigs[0]->batch;
+  // fused record exchange: every shard's FFT epilogue stores into the buffers of all shards of the group (plain
+  // device pointers, the same code path as the IPC mappings across GPUs)
+  const bool fused = P0->line_exchange == 1;
+  for (int g = 0; g < G; ++g)
+    if ((plans[g]->line_exchange == 1) != fused) return fail(P0, SFFT_EINVAL, "shards disagree on line_exchange");
+  if (fused) {
+    for (int g = 0; g < G; ++g) {
+      const int rc0 = ensure_peer_buf(plans[g]);
+      if (rc0) return rc0;
+    }
+    for (int g = 0; g < G; ++g) {
+      plans[g]->peer_ptr.assign(G, nullptr);
+      plans[g]->peer_opened.assign(G, false);
+      for (int h = 0; h < G; ++h) plans[g]->peer_ptr[h] = plans[h]->peer_buf;
+      plans[g]->peer_ready = true;
+    }
+  }
   std::vector<DevParams> D(G);
   int launches = 0, rc;
   auto nomark = []() -> int { return 0; };
@@ -1241,7 +1306,7 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
     n_bound = it[0].n_active;
     for (int g = 0; g < G; ++g)
       if ((rc = iter_front(plans[g], D[g], iter, it[g], launches, nomark))) return rc;
-    for (int g = 0; g < G; ++g)          // the all-gather: shard g's records into slot g of every shard
+    for (int g = 0; g < G && !fused; ++g)   // the all-gather: shard g's records into slot g of every shard
       for (int h = 0; h < G; ++h)
         CUDA_TRY(P0, cudaMemcpyAsync(ptr<int64_t>(plans[h], B_RRECV) + (size_t)g * words, ptr<int64_t>(plans[g], B_RSEND),
                                      8 * words, cudaMemcpyDeviceToDevice, st));
@@ -1441,6 +1506,46 @@ int sfft_comm_unique_id(void* out) {
   NcclUid id;
   if (n.get_unique_id(&id) != 0) return SFFT_ENCCL;
   memcpy(out, id.internal, sizeof id.internal);
+  return SFFT_OK;
+}
+
+int sfft_comm_peer_handle(sfft_plan_t* plan, void* out) {
+  if (!plan || !out) return SFFT_EINVAL;
+  if (plan->line_exchange != 1) return fail(plan, SFFT_EINVAL, "plan has line_exchange = 0");
+  int rc = ensure_peer_buf(plan);
+  if (rc) return rc;
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(plan, cudaIpcGetMemHandle(&h, plan->peer_buf));
+  static_assert(sizeof h == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(out, &h, sizeof h);
+  return SFFT_OK;
+}
+
+int sfft_comm_init_peers(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* handles) {
+  if (!plan || !handles || nranks < 1 || rank < 0 || rank >= nranks) return SFFT_EINVAL;
+  if (plan->line_exchange != 1) return fail(plan, SFFT_EINVAL, "plan has line_exchange = 0");
+  if (plan->line_G != nranks || plan->line_g != rank)
+    return fail(plan, SFFT_EINVAL, "plan is line shard %d of %d, peer rank %d of %d", plan->line_g, plan->line_G, rank,
+                nranks);
+  if (plan->peer_ready) return fail(plan, SFFT_EINVAL, "peers already initialised");
+  int rc = ensure_peer_buf(plan);
+  if (rc) return rc;
+  plan->peer_ptr.assign(nranks, nullptr);
+  plan->peer_opened.assign(nranks, false);
+  for (int h = 0; h < nranks; ++h) {
+    if (h == rank) {
+      plan->peer_ptr[h] = plan->peer_buf;
+      continue;
+    }
+    cudaIpcMemHandle_t ih;
+    memcpy(&ih, static_cast<const char*>(handles) + 64 * (size_t)h, sizeof ih);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(plan, SFFT_ECUDA, "cudaIpcOpenMemHandle(rank %d): %s", h, cudaGetErrorString(e));
+    plan->peer_ptr[h] = p;
+    plan->peer_opened[h] = true;
+  }
+  plan->peer_ready = true;
   return SFFT_OK;
 }
 

@@ -150,6 +150,65 @@ __device__ __forceinline__ uint64_t key_hash_warp(const int64_t* v, int64_t stri
   return h;
 }
 
+// fused record exchange (line_exchange = 1): the FFT epilogue of shard g stores the word into every shard's copy of
+// its record (receive slot g); flags are int32 words at the record start, coordinates int64 words after rec_fw
+__device__ __forceinline__ int64_t peer_rec_off(const DevParams& P, int s) {
+  return ((int64_t)P.line_g * P.batch + s) * P.rec_words;
+}
+__device__ __forceinline__ void peer_put_flag(const DevParams& P, int s, int ci, int32_t v) {
+  const int64_t off = peer_rec_off(P, s);
+  for (int h = 0; h < P.line_G; ++h) reinterpret_cast<int32_t*>(P.peer_recv[h] + off)[ci] = v;
+}
+__device__ __forceinline__ void peer_put_coord(const DevParams& P, int s, int n, int ci, int64_t v) {
+  const int64_t off = peer_rec_off(P, s) + P.rec_fw + (int64_t)(n - 1) * P.k + ci;
+  for (int h = 0; h < P.line_G; ++h) P.peer_recv[h][off] = v;
+}
+// after a CTA's record stores: system-scope release of its (shard, local line, signal) stamp on every shard
+__device__ __forceinline__ void peer_release_line(const DevParams& P, int s, int n) {
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int64_t idx = ((int64_t)P.line_g * P.L_ref + n) * P.batch + s;
+    for (int h = 0; h < P.line_G; ++h)
+      asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(P.peer_stamp[h] + idx), "r"(P.peer_epoch) : "memory");
+  }
+}
+// the commit of signal s waits until every line of every shard released this iteration's stamp (acquire, system
+// scope); a peer that never arrives flags spin_err after 2 s instead of hanging the GPU
+__device__ __forceinline__ void peer_wait_lines(const DevParams& P, int s) {
+  int total = 0;
+  for (int g = 0; g < P.line_G; ++g) {
+    int lo, hi;
+    line_shard_range(P.r, P.line_G, g, &lo, &hi);
+    total += 1 + (hi - lo);
+  }
+  for (int t = threadIdx.x; t < total; t += blockDim.x) {
+    int g = 0, n = t;
+    for (;; ++g) {
+      int lo, hi;
+      line_shard_range(P.r, P.line_G, g, &lo, &hi);
+      if (n < 1 + (hi - lo)) break;
+      n -= 1 + (hi - lo);
+    }
+    const int32_t* f = P.stamp_local + ((int64_t)g * P.L_ref + n) * P.batch + s;
+    long long t0 = 0;
+    for (int it = 0;; ++it) {
+      int got;
+      asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(got) : "l"(f) : "memory");
+      if (got == P.peer_epoch) break;
+      if ((it & 255) == 0) {
+        long long now;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+        if (it == 0) t0 = now;
+        else if (now - t0 > 2000000000ll) { atomicExch(P.spin_err, 1); break; }
+      }
+      __nanosleep(128);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+}
+
 // a7 commit of one signal (steps 2-5 of decode_kernel<kDecCommit>, k_decode.cu): candidates of line 0 and the
 // pass flags / coordinates of every line from the records, bin consistency, accepted list, registry update
 // (hash lookup, R[v] += a, new entries and their C rows, prune) and the signal's state.  Runs in the commit
@@ -170,6 +229,7 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   int* scratch = found + P.k;
   int64_t* accv = P.acc_v + (int64_t)s * r * P.k;               // [r][k], column = candidate index
   int nc = 0, total = 0;
+  if (P.peer_mode) peer_wait_lines(P, s);        // the records of every shard's lines are in (fused exchange)
   // ---- commit: candidates of line 0, flags ANDed over the line shards, coordinates unpacked ----
   nc = P.rec_nc[s];
   for (int ci = tid; ci < nc; ci += blockDim.x) {

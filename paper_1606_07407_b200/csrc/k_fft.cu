@@ -831,13 +831,20 @@ __device__ void fused_select(const DevParams& P, int s, int p, double2* x, const
     const int b = cand[ci];
     P.rec_cand[(int64_t)s * P.k + ci] = b;
     P.rec_f0[(int64_t)s * P.k + ci] = x[b];
-    sendf[ci] = 1;
+    if (P.peer_mode) peer_put_flag(P, s, ci, 1);
+    else sendf[ci] = 1;
   }
   if (tid == 0) P.rec_nc[s] = nc;
+  // fused exchange: the flags just stored in the peers' memory must land before the line-n CTAs' clears, which
+  // follow their acquire of sel_ready -- every thread fences at system scope, the release is system scope
+  if (P.peer_mode) __threadfence_system();
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.sel_ready + s), "r"(P.it_epoch) : "memory");
+    if (P.peer_mode)
+      asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(P.sel_ready + s), "r"(P.it_epoch) : "memory");
+    else
+      asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(P.sel_ready + s), "r"(P.it_epoch) : "memory");
   }
 }
 
@@ -870,8 +877,14 @@ __device__ void fused_test(const DevParams& P, int s, int p, int n, const double
     double2 f = cmulx(x[b], __ldg(ch + b));
     if (resid) f = add_bin_residual(f, bstart, border, Creg, P.Lp, n, b, pd);
     int64_t v = 0;
-    if (test_decode(f0s[ci], f, P.tol, Ev, P.round_tol, P.extra & 1, lo, hi, &v)) sendv[ci] = v;
-    else sendf[ci] = 0;
+    const bool pass = test_decode(f0s[ci], f, P.tol, Ev, P.round_tol, P.extra & 1, lo, hi, &v);
+    if (P.peer_mode) {
+      if (pass) peer_put_coord(P, s, n, ci, v);
+      else peer_put_flag(P, s, ci, 0);
+    } else {
+      if (pass) sendv[ci] = v;
+      else sendf[ci] = 0;
+    }
   }
 }
 
@@ -1002,6 +1015,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
       fused_test(P, s, p, n, x, ch);
       FFT_PROF_MARK(6);
     }
+    if (P.peer_mode) peer_release_line(P, s, n);
     if (P.fuse_commit) {
       // the last of the signal's n_lines CTAs to arrive commits it (a7): every thread fences its record
       // writes, thread 0 counts the arrival; the last one resets the counter for the next iteration

@@ -21,6 +21,8 @@ constexpr int kMaxFftPasses = 24;
 constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
 constexpr int kMaxFallbackLevels = 67;   // sfft_options.fallback_tilts: 4 fixed-stride tilt levels + 63 round-robin rounds
+constexpr int kDefaultTableSlots = 512;  // per-prime table cache slots when sfft_options.table_cache_slots = 0
+constexpr int kMaxPeers = 8;             // line shards of a fused record exchange (one node)
 
 // Everything a kernel needs, passed by value (kernel parameter space).
 struct DevParams {
@@ -146,6 +148,16 @@ struct DevParams {
   int32_t cur_iter;            // the iteration of that launch (the commit's state / log)
   int32_t* commit_cnt;         // [batch] arrival counters of the fused commit (reset by the last CTA)
   int32_t* sel_ready;          // [batch]
+  // fused record exchange (sfft_options.line_exchange = 1): the FFT epilogue stores its record words straight into
+  // the receive buffer of every shard (peer memory: CUDA IPC mappings across GPUs, plain pointers on one device)
+  // and releases a per-(shard, local line, signal) stamp = peer_epoch on every shard; the commit acquires all
+  // r + G stamps of its signal instead of waiting for a separate all-gather
+  int32_t peer_mode;
+  int32_t peer_epoch;          // iteration stamp of the exchange (the same sequence on every shard, starts at 1)
+  int64_t* peer_recv[kMaxPeers];   // receive buffer [line_G][batch][rec_words] of shard h
+  int32_t* peer_stamp[kMaxPeers];  // stamps [line_G][L_ref][batch] of shard h
+  int32_t* stamp_local;        // this shard's own stamps (the commit waits on them)
+  int32_t L_ref;               // lines of shard 0 (the largest shard; the stamp row stride)
   int32_t* bin_start;          // [batch][p_stride + 1] registry entries of bin b: bin_order[bin_start[b] .. [b+1])
   int32_t* bin_order;          // [batch][k] registry entry indices grouped by bin, ascending e within a bin
 };

@@ -494,6 +494,53 @@ def test_e2e_line_shards_group_vs_golden_oracle(S, name, tag, trials, G, path):
     assert rep.samples_used == sum(int(g[f"{tag}_{t}_samples"]) for t in trials)
 
 
+@pytest.mark.parametrize("name,tag,trials,G", [("c3", "primary", [0, 1], 2), ("c3", "primary", [2], 5),
+                                               ("c4", "primary", [0, 1], 3), ("c5", "alt", [0], 4),
+                                               ("c2", "primary", range(8), 2)])
+def test_e2e_line_shards_fused_exchange(S, name, tag, trials, G):
+    """Fused record exchange (line_exchange = 1): every shard's FFT epilogue stores its records straight into the
+    receive buffers of all shards and releases per-(shard, line, signal) stamps that the commit acquires -- no
+    separate all-gather (sfft_execute_group: the shards' buffers are plain pointers on one device, the same stores
+    as over NVLink).  Same bars as the all-gather variant."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    blocks = c.blocks if tag == "primary" else c.alt_blocks
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    plans = _shard_plans(S, c, G, blocks, batch=len(trials), line_exchange=1)
+    res = _group_solve(S, plans, w, a)
+    for i, t in enumerate(trials):
+        key = f"{tag}_{t}"
+        assert int(res.per_status[i]) == int(g[key + "_status"])
+        n = int(res.count[i])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), g[key + "_a"]), key
+    assert res.report.samples_used == sum(int(g[f"{tag}_{t}_samples"]) for t in trials)
+
+
+def test_e2e_line_shard_fused_exchange_world1(S):
+    """The fused exchange through the public bootstrap at one rank: sfft_comm_peer_handle + sfft_comm_init_peers
+    (own buffer), C3 at full size; a plan without the bootstrap is refused."""
+    c = W.CONFIGS["c3"]
+    g = _golden("c3")
+    trials = [0, 1]
+    w, a = W.make_batch(c, trials)
+    plan = _plan(S, c, batch=len(trials), line_shards=1, line_rank=0, line_exchange=1)
+    with pytest.raises(S.SfftError):
+        S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    S.sfft_comm_init_peers(plan, 1, 0, [S.sfft_comm_peer_handle(plan)])
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for i, t in enumerate(trials):
+        key = f"primary_{t}"
+        n = int(res.count[i])
+        gw = np.ascontiguousarray(res.freqs[i, :n].cpu().numpy())
+        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+        assert _coef_ok(res.coeffs[i, :n].cpu().numpy(), g[key + "_a"]), key
+    res2 = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())     # stamps carry across executes
+    assert torch.equal(res2.freqs, res.freqs)
+
+
 def test_e2e_line_shards_stall_fallback(S):
     """Line shards through the tilt fallback (levels switch inside the commit, retilt per shard)."""
     c = W.custom_config(4, 16, 8, (1, 1, 1, 1), structure="rectangles")
@@ -508,13 +555,14 @@ def test_e2e_line_shards_stall_fallback(S):
         if len(ws) == 6:
             break
     w, a = np.stack(ws).astype(np.int32), np.stack(as_)
-    plans = _shard_plans(S, c, 2, batch=len(ws), fallback_tilts=4)
-    res = _group_solve(S, plans, w, a)
     P = O.params_for(c, n_fallback=4)
-    for i in range(len(ws)):
-        ref = O.solve(P, w[i], a[i])
-        assert int(res.per_status[i]) == ref.status
-        _check_against_oracle(res, i, ref.w, ref.a, ref.status)
+    for exchange in (0, 1):
+        plans = _shard_plans(S, c, 2, batch=len(ws), fallback_tilts=4, line_exchange=exchange)
+        res = _group_solve(S, plans, w, a)
+        for i in range(len(ws)):
+            ref = O.solve(P, w[i], a[i])
+            assert int(res.per_status[i]) == ref.status
+            _check_against_oracle(res, i, ref.w, ref.a, ref.status)
 
 
 def test_e2e_line_shard_nccl_world1(S):
@@ -561,7 +609,7 @@ def test_table_cache_reuse_bitwise(S, name, trials):
     big = _plan(S, c, batch=len(trials), table_cache_slots=1024)
     r1 = S.solve(big, wt, at)
     r2 = S.solve(big, wt, at)
-    r0 = S.solve(_plan(S, c, batch=len(trials)), wt, at)
+    r0 = S.solve(_plan(S, c, batch=len(trials), table_cache_slots=1), wt, at)    # minimum cache: batch + 16
     for r in (r2, r0):
         assert torch.equal(r.count, r1.count) and torch.equal(r.per_status, r1.per_status)
         assert torch.equal(r.freqs, r1.freqs)

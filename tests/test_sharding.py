@@ -122,3 +122,34 @@ def test_line_shard_bootstrap_world2_gloo(r):
         p.join(180)
     assert all(p.exitcode == 0 for p in procs)
     assert q.get(timeout=10) is True
+
+
+def _peer_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1606_07407_b200 as S
+        # the handle exchange of comm_init_line_shards(exchange=1): every rank contributes its 64-byte CUDA IPC
+        # handle, every rank receives all of them in rank order (stand-in bytes here: no GPU)
+        mine = bytes([rank + 1]) * 64
+        got = S.exchange_handles(mine)
+        q.put((rank, got == [bytes([g + 1]) * 64 for g in range(world)]))
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_peer_handle_exchange_world2_gloo():
+    """Fused record exchange bootstrap (line_exchange = 1): the all-gather of the ranks' IPC handles."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(rk, 2, port, q)) for rk in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(180)
+    assert all(p.exitcode == 0 for p in procs)
+    res = dict(q.get(timeout=10) for _ in range(2))
+    assert res == {0: True, 1: True}

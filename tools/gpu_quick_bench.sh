@@ -11,6 +11,6 @@ import json,glob
 for f in sorted(glob.glob("gpurun_out/${TAG}_bench_*.json")):
     try:
         d=json.loads(open(f).read().strip().splitlines()[-1])
-        print(f, round(d['value']/1e6,3), 'M/s', round(d['ms_per_step'],3), 'ms', 'frac', round(d['roofline']['frac'],3), 'kms', {k: round(v,3) for k,v in d['kernel_ms_per_step'].items()}, 'exact', d['verified_exact_recovery'])
+        print(f, round(d['value']/1e6,3), 'M/s', round(d['ms_per_step'],3), 'ms', 'frac', round(d['roofline']['frac'],3), 'kms', {k: round(v,3) for k,v in d['kernel_ms_per_step'].items() if isinstance(v, float)}, 'exact', d['verified_exact_recovery'])
     except Exception as e: print(f, 'ERR', e)
 PY
