@@ -68,6 +68,9 @@ def parse():
                     help="signals: independent signal shards per rank (weak scaling, default); lines: every rank "
                          "solves the same signals and owns a shard of the shifted lines (strong scaling, NCCL "
                          "record all-gather per iteration, SURVEY 8(e))")
+    ap.add_argument("--exchange", default="allgather", choices=["allgather", "fused"],
+                    help="--shard lines: records all-gathered after the FFT (NCCL) or stored into every shard's memory "
+                         "by the FFT epilogue itself (line_exchange = 1, CUDA IPC peer mappings)")
     ap.add_argument("--latency-steps", type=int, default=20, help="single-signal solves timed for latency_single_solve")
     ap.add_argument("--table-cache", type=int, default=0,
                     help="per-prime table cache slots (plan option table_cache_slots; ~0.8 MB each); 0 = the plan "
@@ -300,12 +303,15 @@ def main():
     stream = torch.cuda.current_stream()
 
     def make_plan(path, batch=T, profile=True, shard=True):
+        fused = lines and shard and args.exchange == "fused"
         p = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=batch, profile=profile, expsum_path=path,
                         line_shards=world if (lines and shard) else 0, line_rank=rank if (lines and shard) else 0,
-                        table_cache_slots=args.table_cache)
+                        table_cache_slots=args.table_cache, line_exchange=1 if fused else 0)
         if lines and shard:
             if world > 1:
-                S.comm_init_line_shards(p)
+                S.comm_init_line_shards(p, exchange=1 if fused else 0)
+            elif fused:
+                S.sfft_comm_init_peers(p, 1, 0, [S.sfft_comm_peer_handle(p)])
             else:
                 S.sfft_comm_init(p, 1, 0, shard_mode=1, unique_id=S.sfft_comm_unique_id())
         return p
@@ -512,7 +518,9 @@ def main():
             "config": {"workload": workload_desc(cfg),
                        "signals_per_gpu_per_step": T,
                        "table_cache_slots": args.table_cache or f"plan default max(batch + 16, 512) = {max(T + 16, 512)}",
-                       "parallelism": f"line shards x{world} (NCCL record all-gather)" if lines else f"signal shards x{world}",
+                       "parallelism": (f"line shards x{world} (" + ("records stored into every shard's memory by the FFT "
+                                       "epilogue, CUDA IPC peer mappings" if args.exchange == "fused" else
+                                       "NCCL record all-gather") + ")") if lines else f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
             "sample_evals_per_s": mult * samples / (ms_max / 1e3),
             "verified_exact_recovery": ok,

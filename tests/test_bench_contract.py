@@ -60,6 +60,9 @@ def test_our_arm_line_shards_c3_world1():
               "--latency-steps", "0", "--no-cpu-baseline", "--batch", "4"])
     assert d["scaling"] == "strong" and d["verified_exact_recovery"] is True
     assert "line shards x1" in d["config"]["parallelism"]
+    d = _run(["--config", "c3", "--shard", "lines", "--exchange", "fused", "--steps", "2", "--warmup", "3",
+              "--e2e-steps", "1", "--latency-steps", "0", "--no-cpu-baseline", "--batch", "4", "--fp64-steps", "0"])
+    assert d["verified_exact_recovery"] is True and "CUDA IPC" in d["config"]["parallelism"]
 
 
 def test_self_launch_dry_run_world2():
