@@ -740,3 +740,26 @@ def test_e2e_forced_false_accepts_vs_oracle(S, ci, extra, path):
         n_acc += int(tr[:, 6].sum())
         n_pr += int(tr[:, 7].sum())
     assert n_acc > 0 and n_pr > 0                          # the branches ran
+
+
+@pytest.mark.parametrize("name,T", [("c3", 100), ("c5", 100), ("c2", 1024), ("c4", 100)])
+def test_e2e_bench_launch_configuration(S, name, T):
+    """The launch configuration bench.py times (BASELINE sizes, the config's full trial batch in one execute): the
+    golden oracle's seeds bit-exact (sets) and within 1e-9 per coefficient; every one of the T signals recovers its
+    input spectrum exactly with coefficients within 1e-9 of the input's."""
+    c = W.CONFIGS[name]
+    g = _golden(name)
+    w, a = W.make_batch(c, range(T))
+    plan = _plan(S, c, batch=T)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    assert res.status == S.SFFT_OK
+    gw_all, ga_all, gn = res.freqs.cpu().numpy(), res.coeffs.cpu().numpy(), res.count.cpu().numpy()
+    for t in range(T):
+        key = f"primary_{t}"
+        if key + "_status" in g.files:
+            n = int(gn[t])
+            assert hashlib.sha256(np.ascontiguousarray(gw_all[t, :n]).tobytes()).digest() == bytes(g[key + "_w_sha256"])
+            assert _coef_ok(ga_all[t, :n], g[key + "_a"]), key
+        ws, as_ = W.canonical_sort(w[t], a[t])
+        assert int(gn[t]) == c.k and np.array_equal(gw_all[t], ws), t
+        assert _coef_ok(ga_all[t], as_), t
