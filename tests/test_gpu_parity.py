@@ -290,14 +290,19 @@ def test_determinism(S):
     assert torch.equal(f1, r2.freqs) and torch.equal(torch.view_as_real(c1), torch.view_as_real(r2.coeffs))
 
 
-def test_solve_host_matches_device(S):
+@pytest.mark.parametrize("T", [4, 17])
+def test_solve_host_matches_device(S, T):
+    """The host-buffer entry point (T >= 8: two chunks whose copies overlap the other chunk's solve) gives bitwise
+    the device path's result and the same aggregate report."""
     c = W.CONFIGS["c2"]
-    w, a = W.make_batch(c, range(4))
-    plan = _plan(S, c, batch=4)
+    w, a = W.make_batch(c, range(T))
+    plan = _plan(S, c, batch=T)
     rd = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
     fd, cd = rd.freqs.cpu(), rd.coeffs.cpu()
     rh = S.sfft_solve_host(plan, torch.from_numpy(w).pin_memory(), torch.from_numpy(a).pin_memory())
     assert torch.equal(fd, rh.freqs) and torch.equal(torch.view_as_real(cd), torch.view_as_real(rh.coeffs))
+    assert torch.equal(rd.count.cpu(), rh.count) and torch.equal(rd.per_status.cpu(), rh.per_status)
+    assert rh.report.samples_used == rd.report.samples_used and rh.status == rd.status
 
 
 def test_error_codes(S):
