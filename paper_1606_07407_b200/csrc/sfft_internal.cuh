@@ -313,7 +313,8 @@ inline int fft_threads(int M, size_t smem, int64_t n_ctas) {
   if (M >= fft_big_m()) return 512;
   const size_t per_sm = 228 * 1024;
   const int ctas = smem * 4 + 4096 <= per_sm ? 4 : smem * 2 + 2048 <= per_sm ? 2 : 1;
-  const int cap = getenv("SFFT_FFT_TCAP") ? atoi(getenv("SFFT_FFT_TCAP")) : 1024 / ctas;
+  // (two CTAs per SM: 256 threads measured ~2 % faster than 512 on C5's M ~ 5100 lines; 768 / 1024 much slower)
+  const int cap = getenv("SFFT_FFT_TCAP") ? atoi(getenv("SFFT_FFT_TCAP")) : (ctas == 2 ? 256 : 1024 / ctas);
   // ~M/6 threads; small sizes (M <= 2048) over many lines (>= 4096 CTAs) run better as more, smaller CTAs
   // per SM: ~M/12 (measured: C4 -6 %, C2 -1 %; with few CTAs, as in C5's later iterations, M/12 is slower)
   static const int tdiv_env = getenv("SFFT_FFT_TDIV") ? std::max(1, atoi(getenv("SFFT_FFT_TDIV"))) : 0;
