@@ -23,7 +23,13 @@ def ncu_rows(rep, kernel=None):
     next(r)
     hdr = next(r)
     iw, isrc = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
-    return [(int(x[iw]) if x[iw] else 0, x[isrc]) for x in r if len(x) > max(iw, isrc)]
+    rows = []
+    for x in r:                                   # several launches: the first launch's listing only
+        if x and x[0] in ("Kernel Name", "Address"):
+            break
+        if len(x) > max(iw, isrc):
+            rows.append((int(x[iw]) if x[iw] else 0, x[isrc]))
+    return rows
 
 
 def sass_lines(cubin, kernel):
