@@ -85,6 +85,7 @@ struct sfft_plan_s {
   ExpsumShape shape{};
   I8Config i8{};
   bool i8_ok = false;          // int8-limb tensor-core exp-sum available for this plan
+  bool fs_ok = false;          // fused sampling in the FFT CTA for short lines (FP64 plans, L_ref <= kFusedMaxL)
   int32_t expsum_path = 0;     // sfft_options.expsum_path
   // stall fallback levels (reading R23): level 0 = the plan's own tilts / E
   int32_t n_levels = 1, lvl_tmax = 1;
@@ -134,7 +135,7 @@ enum Buf {
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
   B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY, B_SPINERR,
-  B_FFTW,
+  B_FFTW, B_DLROOT,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -276,10 +277,12 @@ void layout(sfft_plan_t* P) {
   sz[B_LVLNT] = 4 * (size_t)P->n_levels;
   sz[B_LVLAXT] = 4 * (size_t)P->n_levels * P->r;
   for (int b : {B_STLVL, B_STIL, B_STRT}) sz[b] = 4 * S;
-  sz[B_I8PW] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
-  sz[B_I8DLOG] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
-  sz[B_I8ELOG] = P->i8_ok ? 4 * S * align_up((size_t)P->kk + 16, 4) : 0;
-  sz[B_I8CHL] = P->i8_ok ? 16 * T * (2 * P->p_stride + 8) : 0;
+  const bool logt = P->i8_ok || P->fs_ok;   // discrete-log tables: the int8 exp-sum and the fused sampling
+  sz[B_I8PW] = logt ? 4 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_I8DLOG] = logt ? 4 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_I8ELOG] = logt ? 4 * S * align_up((size_t)P->kk + 16, 4) : 0;
+  sz[B_I8CHL] = logt ? 16 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_DLROOT] = P->fs_ok ? 16 * T * (2 * P->p_stride + 8) : 0;
   sz[B_STSLOT] = 4 * S;
   sz[B_SLOTP] = 4 * T;
   sz[B_SLOTE] = 4 * T;
@@ -401,6 +404,9 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_sigma = ptr<double>(P, B_I8SIG);
     D.i8_tlo = ptr<uint2>(P, B_I8TLO);
     D.i8_thi = ptr<uint32_t>(P, B_I8THI);
+  }
+  if (P->i8_ok || P->fs_ok) {
+    D.log_tables = 1;
     D.i8_tstride = 2 * P->p_stride + 8;   // the root table holds T twice (discrete-log rows, no wrap)
     D.i8_pw = ptr<int32_t>(P, B_I8PW);
     D.i8_dlog = ptr<int32_t>(P, B_I8DLOG);
@@ -408,6 +414,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_estride = (int32_t)align_up((size_t)P->kk + 16, 4);   // rows 16-byte aligned for the bulk copies
     D.i8_chl = ptr<double2>(P, B_I8CHL);
   }
+  if (P->fs_ok) D.dl_root = ptr<double2>(P, B_DLROOT);
   D.line_lo = P->line_lo;
   D.line_G = std::max(P->line_G, 1);
   D.line_g = P->line_g;
@@ -570,6 +577,8 @@ const bool g_sync_launches = getenv("SFFT_SYNC") != nullptr;
 struct IterPlan {
   int n_active = 0, max_p = 0, fi = 0, max_M = 0, ksplit = 1, big = 0;
   bool use_i8 = false;
+  bool fused = false;         // samples computed in the FFT CTAs (no exp-sum launch), fused_smem bytes per CTA
+  size_t fused_smem = 0;
   bool fuse_commit = false;   // the commit runs in the last FFT CTA of each signal (no commit launch)
 };
 
@@ -636,6 +645,10 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
   const ExpsumShape shp = expsum_for_p(P->shape, it->max_p);
   it->use_i8 = P->i8_ok && i8_use_for(P, it->max_p);
   it->ksplit = 1;
+  if (P->fs_ok) {
+    it->fused_smem = P->fft[it->fi].smem_upto + 16 * (2 * (size_t)it->max_p + 4) + 20 * (size_t)P->k + 256;
+    it->fused = it->fused_smem <= (size_t)P->smem_optin;
+  }
   if (it->use_i8) {
     it->ksplit = i8_ksplit(P, it->max_p, it->n_active);
   } else {
@@ -667,7 +680,9 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
                const std::function<int()>& mark) {
   cudaStream_t st = P->stream;
   mark();
-  if (it.use_i8)
+  if (it.fused) {
+    // no exp-sum launch: the FFT CTAs sample their lines (the mark pair stays for the profile's bookkeeping)
+  } else if (it.use_i8)
     LAUNCH(P, launch_expsum_i8(D, P->i8, it.max_p, it.n_active, it.ksplit, ptr<double2>(P, B_PART), it.max_p,
                                P->smem_optin, st));
   else
@@ -682,8 +697,12 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   D.cur_iter = iter;
   D.i8_iter = it.use_i8 ? 1 : 0;
   if (D.peer_mode) D.peer_epoch = ++P->peer_epoch;   // the same sequence on every shard (one per iteration)
-  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)P->fft[it.fi].smem_upto, fft_threads(it.max_M, P->fft[it.fi].smem_upto, (int64_t)it.n_active * P->L), it.big, it.ksplit,
-                        ptr<double2>(P, B_PART), it.max_p, st));
+  D.fused_sample = it.fused ? 1 : 0;
+  if (it.fused) D.lines_log = 0;
+  const size_t fsm = it.fused ? it.fused_smem : P->fft[it.fi].smem_upto;
+  LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)fsm, fft_threads(it.max_M, fsm, (int64_t)it.n_active * P->L), it.big,
+                        it.fused ? 1 : it.ksplit, ptr<double2>(P, B_PART), it.max_p, st));
+  D.fused_sample = 0;
   D.lines_log = 0;
   D.fuse_decode = 0;
   D.fuse_commit = 0;
@@ -1080,6 +1099,9 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     P->i8_ok = i8_configure(P->L_ref, *std::max_element(P->lvl_E.begin(), P->lvl_E.end()), P->k, &P->i8);
   if (P->i8_ok && P->i8.small_l && P->expsum_path == 0) P->i8_ok = false;
   if (P->expsum_path == 2 && !P->i8_ok) return SFFT_ENOTSUP;
+  // short lines on the FP64 path: each FFT CTA samples its own line (NEXT #3 fusion); SFFT_NO_FUSED_LINES=1 keeps
+  // the separate exp-sum launch (A/B, parity)
+  P->fs_ok = P->expsum_path == 0 && !P->i8_ok && !P->literal && P->L_ref <= kFusedMaxL && !getenv("SFFT_NO_FUSED_LINES");
   // shared-memory budgets of the other kernels
   if (16 * ((size_t)P->p_stride + 2) + 2 * 16 * 16 * (size_t)P->shape.bn + 256 > (size_t)smem_optin) return SFFT_ENOTSUP;
   if (8 * (size_t)P->p_stride + 4 * (2 * (size_t)P->p_stride + 2 * (size_t)k + 64) > (size_t)smem_optin)

@@ -446,23 +446,32 @@ __device__ void i8_log_tables(const DevParams& P, int slot, int p) {
     P.i8_chl[base + f] = chirp_value(x, p);
     double sn, cs;
     sincospi(2.0 * (double)x / (double)p, &sn, &cs);   // W_p[x] = e^{+2 pi i x / p}, exact rational argument
-    uint2 lo;
-    uint32_t hi;
-    i8_root_entry(cs, sn, P.i8_S, lo, hi);
-    P.i8_tlo[base + f] = lo;
-    P.i8_thi[base + f] = hi;
-    P.i8_tlo[base + n1 + f] = lo;
-    P.i8_thi[base + n1 + f] = hi;
+    if (P.i8_S > 0) {
+      uint2 lo;
+      uint32_t hi;
+      i8_root_entry(cs, sn, P.i8_S, lo, hi);
+      P.i8_tlo[base + f] = lo;
+      P.i8_thi[base + f] = hi;
+      P.i8_tlo[base + n1 + f] = lo;
+      P.i8_thi[base + n1 + f] = hi;
+    }
+    if (P.dl_root) {
+      P.dl_root[base + f] = make_double2(cs, sn);
+      P.dl_root[base + n1 + f] = make_double2(cs, sn);
+    }
     x = mulmod32(x, g, (uint32_t)p);
   }
   if (threadIdx.x == 0) {
-    uint2 lo;
-    uint32_t hi;
-    i8_root_entry(1.0, 0.0, P.i8_S, lo, hi);
+    if (P.i8_S > 0) {
+      uint2 lo;
+      uint32_t hi;
+      i8_root_entry(1.0, 0.0, P.i8_S, lo, hi);
+      P.i8_tlo[base + 2 * n1] = lo;
+      P.i8_thi[base + 2 * n1] = hi;
+    }
+    if (P.dl_root) P.dl_root[base + 2 * n1] = make_double2(1.0, 0.0);
     P.i8_pw[base + n1] = 0;
     P.i8_chl[base + n1] = chirp_value(0, p);
-    P.i8_tlo[base + 2 * n1] = lo;
-    P.i8_thi[base + 2 * n1] = hi;
   }
 }
 
@@ -612,7 +621,7 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, in
                            bool u_smem = false) {
   const int p = P.st_p[s];
   if (!(phases & kTermsU)) {
-    if (P.i8_S <= 0) return;
+    if (!P.log_tables) return;
     const int K = P.k + P.st_nR[s];
     const int Kp = (K + 15) & ~15;
     const int2* ug = P.u_all + (int64_t)s * P.kk;
@@ -632,7 +641,7 @@ __device__ void terms_body(const DevParams& P, int s, int* cnt, int* scratch, in
   int2* ug = P.u_all + (int64_t)s * P.kk;
   const int Kp = (K + 15) & ~15;
   const int64_t base = (int64_t)P.st_slot[s] * P.i8_tstride;
-  int32_t* eg = P.i8_S > 0 && (phases & kTermsE) ? P.i8_elog + (int64_t)s * P.i8_estride : nullptr;
+  int32_t* eg = P.log_tables && (phases & kTermsE) ? P.i8_elog + (int64_t)s * P.i8_estride : nullptr;
   int* ub = cnt + p;                                 // [nR] bins of the registry entries (smem copy)
   int* us = cnt + p + P.k;                           // [K] u_j (smem copy for a later kTermsE pass)
   for (int j = threadIdx.x; j < (eg ? Kp : K); j += blockDim.x) {
@@ -717,7 +726,7 @@ __device__ void fill_tables(const DevParams& P, int slot, int p, unsigned char* 
     x[q] = vq;
     if (q > 0) x[M - q] = vq;
   }
-  if (P.i8_S > 0) i8_log_tables(P, slot, p);
+  if (P.log_tables) i8_log_tables(P, slot, p);
   __syncthreads();
   fft_dif<BIG>(P, x, fi, tb);
   const double inv = 1.0 / (double)M;
@@ -936,7 +945,50 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   const int tslot = P.st_slot[s];                     // table slot of the signal's prime
   const double2* ch = P.chirp + (int64_t)tslot * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
-  if (P.lines_log) {
+  if (P.fused_sample) {
+    // NEXT #3 fusion: this CTA samples its own line (Alg. 2 l.13-14; Eq. (41)) -- s_n[h] = sum_j C[j][n] W_p^{h u_j}
+    // with rows f in discrete-log order (h = g^f, root of (f, j) = dl_root[f + e_j], W_p[0] = 1 for e_j < 0 and
+    // for the h = 0 row) -- and multiplies by the chirp into the FFT buffer; the samples never leave shared memory.
+    // shared memory after the FFT buffer and its twiddles: roots [2(p - 1) + 1], C column [K], e_j [K]
+    const int K = P.k;
+    const int ntw = P.fft_tw_off[fi * kMaxFftPasses + P.fft_npass[fi]] - P.fft_tw_off[fi * kMaxFftPasses];
+    double2* sroot = tb + ((ntw + 1) & ~1);
+    const int nroot = 2 * (p - 1) + 1;
+    double2* scol = sroot + ((nroot + 1) & ~1);
+    int* se = reinterpret_cast<int*>(scol + K);
+    const double2* rsrc = P.dl_root + (int64_t)tslot * P.i8_tstride;
+    for (int q = threadIdx.x; q < nroot; q += blockDim.x) sroot[q] = rsrc[q];
+    const double2* Cs = P.C_all + (int64_t)s * P.kk * P.Lp + n;
+    const int32_t* eg = P.i8_elog + (int64_t)s * P.i8_estride;
+    for (int j = threadIdx.x; j < K; j += blockDim.x) {
+      scol[j] = Cs[(int64_t)j * P.Lp];
+      se[j] = eg[j];
+    }
+    __syncthreads();
+    const int32_t* pw = P.i8_pw + (int64_t)tslot * P.i8_tstride;
+    const double2* chl = P.i8_chl + (int64_t)tslot * P.i8_tstride;
+    const int one = 2 * (p - 1);
+    // two rows per thread and trip share the broadcast loads of e_j and C[j][n]; the h = 0 row (f = p - 1, every
+    // root 1) takes the table's W_p[0] entry through e = -1 semantics: its index is forced to `one`
+    for (int f0 = threadIdx.x; f0 < p; f0 += 2 * blockDim.x) {
+      const int f1 = f0 + blockDim.x;
+      const bool z0 = f0 == p - 1, z1 = f1 == p - 1, v1 = f1 < p;
+      double ar0 = 0.0, ai0 = 0.0, ar1 = 0.0, ai1 = 0.0;
+#pragma unroll 4
+      for (int j = 0; j < K; ++j) {
+        const int e = se[j];
+        const double2 c = scol[j];
+        const double2 w0 = sroot[(e < 0 || z0) ? one : f0 + e];
+        const double2 w1 = sroot[(e < 0 || z1 || !v1) ? one : f1 + e];
+        ar0 = fma(c.x, w0.x, fma(-c.y, w0.y, ar0));
+        ai0 = fma(c.x, w0.y, fma(c.y, w0.x, ai0));
+        ar1 = fma(c.x, w1.x, fma(-c.y, w1.y, ar1));
+        ai1 = fma(c.x, w1.y, fma(c.y, w1.x, ai1));
+      }
+      x[__ldg(pw + f0)] = cmulx(make_double2(ar0, ai0), __ldg(chl + f0));
+      if (v1) x[__ldg(pw + f1)] = cmulx(make_double2(ar1, ai1), __ldg(chl + f1));
+    }
+  } else if (P.lines_log) {
     // the int8 exp-sum wrote the samples in discrete-log order: position f holds h = pw[f]; all of a
     // thread's loads in flight (latency-bound phase), then the chirp products scattered
     const int32_t* pw = P.i8_pw + (int64_t)tslot * P.i8_tstride;

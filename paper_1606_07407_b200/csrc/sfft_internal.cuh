@@ -23,6 +23,7 @@ constexpr int kLogIters = 64;
 constexpr int kMaxFallbackLevels = 67;   // sfft_options.fallback_tilts: 4 fixed-stride tilt levels + 63 round-robin rounds
 constexpr int kDefaultTableSlots = 512;  // per-prime table cache slots when sfft_options.table_cache_slots = 0
 constexpr int kMaxPeers = 8;             // line shards of a fused record exchange (one node)
+constexpr int kFusedMaxL = 8;            // lines per signal up to which FP64 plans sample inside the FFT CTAs
 
 // Everything a kernel needs, passed by value (kernel parameter space).
 struct DevParams {
@@ -128,6 +129,12 @@ struct DevParams {
   int32_t* i8_elog;            // [batch][i8_estride] e_j of the iteration's terms
   int32_t i8_estride;          // >= kk + 16, multiple of 4
   int32_t lines_log;           // launch flag: the lines hold samples in discrete-log order (int8 exp-sum)
+  // fused sampling for short lines (plans whose exp-sum runs on the FP64 kernels with few lines):
+  // the FFT CTA of (signal, line n) computes its own samples s_n in shared memory -- rows in discrete-log order,
+  // root of (f, j) = dl_root[f + e_j] (FP64, the i8 tables' layout) -- so the lines never reach HBM
+  int32_t log_tables;          // the discrete-log tables (i8_pw, i8_dlog, i8_chl, e_j in i8_elog) are built
+  double2* dl_root;            // [n_tslots][i8_tstride] W_p[g^f] twice + W_p[0] (FP64), or null
+  int32_t fused_sample;        // pfft launch flag: compute the samples in the FFT CTA (no exp-sum launch)
   int64_t i8_tstride;          // >= p_stride + 8 (bulk copies round the table up to 16 bytes)
   // line sharding: shard line_g of line_G holds line 0 and the shifted lines of reduced axes
   // [line_lo, line_lo + L - 1); its decode is split into a local test (records) and a commit after the

@@ -448,6 +448,13 @@ def test_e2e_cta_pair_mode(S):
     _opt_in_parity("SFFT_I8_PAIR", (("c3", [0, 1]), ("c5", [0])))
 
 
+def test_e2e_separate_expsum_for_short_lines(S):
+    """Short-line FP64 plans sample inside the FFT CTAs by default (NEXT #3 fusion, `fused_sample`); with
+    SFFT_NO_FUSED_LINES=1 the separate exp-sum kernel writes the lines to HBM first.  Both meet the oracle bars
+    (C1 and C2 golden seeds, full size); the default path is covered by every other C1 / C2 test."""
+    _opt_in_parity("SFFT_NO_FUSED_LINES", (("c2", list(range(16))), ("c1", list(range(16)))))
+
+
 def test_e2e_fused_commit(S):
     """The registry commit run by the last FFT CTA of each signal (opt-in, SFFT_FUSE_COMMIT=1) gives the same
     sets and coefficients as the oracle (full size: C3, C4 with its long keys, C5 with its tilt fallback)."""
