@@ -377,6 +377,7 @@ def main():
     launches = sum(r.kernel_launches for r in reps_timed)      # our kernels inside the timed region
     cm8, ms8, n8 = tot("cmacs_i8"), tot("ms_expsum_i8"), tot("n_expsum_i8")
     plogp = tot("fft_plogp")
+    mlogm = tot("fft_mlogm")
     limbs = reps[0].i8_limbs if reps else 0
     peaks, peaks_src = measured_peaks()
     traffic, traffic_kernel = None, ""
@@ -424,7 +425,12 @@ def main():
                 "algorithmic_bytes": "32 B per sample (read s, write F) = 32 * samples_used per step",
                 "fp64": {"achieved_tflops": fft_tf, "peak_tflops": FP64_PEAK_TFLOPS,
                          "frac": fft_tf / FP64_PEAK_TFLOPS if fft_tf else None,
-                         "algorithmic_flops": "5 p log2 p per line of length p (radix-2 convention, report fft_plogp)"}}
+                         "algorithmic_flops": "5 p log2 p per line of length p (radix-2 convention, report fft_plogp)"},
+                "executed_fp64": {"tflops": 10.0 * mlogm / (ms_fft / 1e3) / 1e12 if ms_fft > 0 else None,
+                                  "frac": 10.0 * mlogm / (ms_fft / 1e3) / 1e12 / FP64_PEAK_TFLOPS if ms_fft > 0 else None,
+                                  "note": "Bluestein: a forward and an inverse FFT of size M >= 2p - 1 per line, 5 M log2 M "
+                                          "flops each (report fft_mlogm); the transform is bound by shared-memory "
+                                          "sweeps and FP64 latency at one 161 KB line per SM (DESIGN.md 8)"}}
 
     # FP64 path (expsum_path = 1: DMMA exp-sum) on the same workload, timed the same way (north star: the sum kernel
     # against the FP64 peak)

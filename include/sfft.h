@@ -120,6 +120,7 @@ typedef struct {
   float ms_total;              /* when profiling: device time of the whole execute (CUDA events) */
   double fft_plogp;            /* sum over signals and iterations of L p log2(p): the prime-length DFTs' size,
                                   5 fft_plogp = their algorithmic flops (radix-2 convention) */
+  double fft_mlogm;            /* the same for the Bluestein sizes M run: 2 x 5 fft_mlogm ~ the executed FFT flops */
 } sfft_report;
 
 typedef struct sfft_plan_s sfft_plan_t;

@@ -59,7 +59,8 @@ class sfft_report(ctypes.Structure):
                 ("ms_expsum", ctypes.c_float), ("ms_fft", ctypes.c_float), ("ms_decode", ctypes.c_float),
                 ("ms_other", ctypes.c_float), ("i8_limbs", ctypes.c_int32), ("n_expsum_i8", ctypes.c_int32),
                 ("cmacs_i8", ctypes.c_int64), ("ms_expsum_i8", ctypes.c_float),
-                ("fallback_used", ctypes.c_int32), ("ms_total", ctypes.c_float), ("fft_plogp", ctypes.c_double)]
+                ("fallback_used", ctypes.c_int32), ("ms_total", ctypes.c_float), ("fft_plogp", ctypes.c_double),
+                ("fft_mlogm", ctypes.c_double)]
 
 
 class SfftError(RuntimeError):

@@ -269,7 +269,7 @@ void layout(sfft_plan_t* P) {
   sz[B_I8B] = P->i8_ok ? i8_limb_bytes(P->i8, (int)S) : 0;
   sz[B_I8SIG] = 8 * S;
   sz[B_CMACS8] = 8 * S;
-  sz[B_FFTW] = 8 * S;
+  sz[B_FFTW] = 16 * S;
   sz[B_LVLE] = 8 * (size_t)P->n_levels;
   sz[B_LVLLO] = 8 * (size_t)P->n_levels * P->r;
   sz[B_LVLHI] = 8 * (size_t)P->n_levels * P->r;
@@ -734,14 +734,14 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(P, cudaMemcpyAsync(&spin_err, D.spin_err, 4, cudaMemcpyDeviceToHost, st));
   std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
-  std::vector<double> hfw(batch);
+  std::vector<double> hfw(2 * (size_t)batch);
   std::vector<int32_t> hlog(2 * kLogIters), hlvl(batch);
   if (rep) {
     CUDA_TRY(P, cudaMemcpyAsync(hlvl.data(), D.st_lvl, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hfw.data(), D.st_fftw, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hfw.data(), D.st_fftw, 16 * (size_t)batch, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
   }
   CUDA_TRY(P, cudaStreamSynchronize(st));
@@ -760,7 +760,8 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
       rep->samples_used += hsamp[s];
       rep->cmacs += hcm[s];
       rep->cmacs_i8 += hcm8[s];
-      rep->fft_plogp += hfw[s];
+      rep->fft_plogp += hfw[2 * s];
+      rep->fft_mlogm += hfw[2 * s + 1];
       rep->fallback_used += hlvl[s] > 0;
     }
     rep->i8_limbs = P->i8_ok ? P->i8.S : 0;

@@ -526,7 +526,11 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
     P.st_samples[s] += (int64_t)(r + 1) * p;              // f evaluations of all shards (reading C22)
     P.st_cmacs[s] += (int64_t)P.L * p * K;
     if (P.i8_iter) P.st_cmacs_i8[s] += (int64_t)P.L * p * K;
-    P.st_fftw[s] += (double)P.L * p * log2((double)p);
+    P.st_fftw[2 * s] += (double)P.L * p * log2((double)p);
+    {
+      const double Mb = (double)P.fft_M[P.st_M[s]];        // the Bluestein size the FFT ran
+      P.st_fftw[2 * s + 1] += (double)P.L * Mb * log2(Mb);
+    }
     P.st_iters[s] = iter;
     if (s == 0 && iter <= kLogIters) {
       P.st_log[2 * (iter - 1)] = p;

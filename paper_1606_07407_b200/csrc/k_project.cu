@@ -77,7 +77,8 @@ __global__ void init_state_kernel(DevParams P, int32_t batch) {
   P.st_samples[s] = 0;
   P.st_cmacs[s] = 0;
   P.st_cmacs_i8[s] = 0;
-  P.st_fftw[s] = 0.0;
+  P.st_fftw[2 * s] = 0.0;
+  P.st_fftw[2 * s + 1] = 0.0;
   P.st_lvl[s] = 0;
   P.st_il[s] = 0;
   P.st_retilt[s] = 0;

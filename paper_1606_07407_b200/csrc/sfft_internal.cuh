@@ -82,7 +82,7 @@ struct DevParams {
   int64_t* st_samples;         // [batch]
   int64_t* st_cmacs;           // [batch]
   int64_t* st_cmacs_i8;        // [batch] cMACs of the iterations whose exp-sum ran on the int8-limb kernel
-  double* st_fftw;             // [batch] sum over iterations of L p log2(p) (this plan's FFT lines)
+  double* st_fftw;             // [batch][2] sums over iterations of L p log2(p) and L M log2(M) (Bluestein sizes)
   int32_t i8_iter;             // decode launch: this iteration's exp-sum used the int8-limb kernel
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [8]: n_active, max_p, max_K, fills, setup CTAs done (this iteration's block)
