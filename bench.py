@@ -406,6 +406,16 @@ def main():
                                         "fp64_peak_tflops": FP64_PEAK_TFLOPS,
                                         "ratio": 8.0 * cm8 / (ms8 / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
                                         "note": "8 flop per complex MAC of the exp-sum vs the FP64 pipe peak"}}
+    elif tot("n_fused_sample") > 0:
+        # short lines: the sampling runs inside the FFT CTAs (fused_sample) -- the sampling's FP64 flops over the
+        # fused kernel's whole time (which also holds the FFT and the decode epilogue): a lower bound of its rate
+        achieved = 8.0 * cmacs / (ms_fft / 1e3) / 1e12
+        roofline = {"bound": "alu", "kernel": "pfft with fused sampling (FP64; the exp-sum inside the FFT CTAs)",
+                    "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                    "traffic": None,
+                    "peak_source": "derived 148 SM x 64 FP64 FMA/clk x 2 x 1.965 GHz; measured DMMA 37.1, DFMA 33.6",
+                    "note": "8 flop per (sample, term) complex MAC over the fused sample + FFT + decode kernel's time",
+                    "fused_iterations": tot("n_fused_sample")}
     else:
         achieved = 8.0 * cmacs / (ms_exp / 1e3) / 1e12
         roofline = {"bound": "alu", "kernel": "expsum (FP64 tensor pipe: mma.sync f64 / DMMA)", "achieved": achieved,
@@ -520,7 +530,8 @@ def main():
             "dtype_note": ("exp-sum as exact int8 x int8 -> int32 limb products on tcgen05 combined in FP64 (reading "
                            "R22); FFT, decode, registry in FP64 / int64" if n8 else "FP64 / int64 throughout"),
             "data": "synthetic (seeded PCG64 per PAPER.md:424 recipe; no dataset exists for this metric)",
-            "expsum_path": "int8 limbs on tcgen05" if n8 else "fp64",
+            "expsum_path": ("int8 limbs on tcgen05" if n8 else
+                            "fp64, fused into the FFT CTAs" if tot("n_fused_sample") else "fp64"),
             "config": {"workload": workload_desc(cfg),
                        "signals_per_gpu_per_step": T,
                        "table_cache_slots": args.table_cache or f"plan default max(batch + 16, 512) = {max(T + 16, 512)}",

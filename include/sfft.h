@@ -121,6 +121,8 @@ typedef struct {
   double fft_plogp;            /* sum over signals and iterations of L p log2(p): the prime-length DFTs' size,
                                   5 fft_plogp = their algorithmic flops (radix-2 convention) */
   double fft_mlogm;            /* the same for the Bluestein sizes M run: 2 x 5 fft_mlogm ~ the executed FFT flops */
+  int32_t n_fused_sample;      /* iterations whose sampling ran inside the FFT CTAs (no exp-sum launch; its time is
+                                  in ms_fft) */
 } sfft_report;
 
 typedef struct sfft_plan_s sfft_plan_t;

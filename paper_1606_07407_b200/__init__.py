@@ -60,7 +60,7 @@ class sfft_report(ctypes.Structure):
                 ("ms_other", ctypes.c_float), ("i8_limbs", ctypes.c_int32), ("n_expsum_i8", ctypes.c_int32),
                 ("cmacs_i8", ctypes.c_int64), ("ms_expsum_i8", ctypes.c_float),
                 ("fallback_used", ctypes.c_int32), ("ms_total", ctypes.c_float), ("fft_plogp", ctypes.c_double),
-                ("fft_mlogm", ctypes.c_double)]
+                ("fft_mlogm", ctypes.c_double), ("n_fused_sample", ctypes.c_int32)]
 
 
 class SfftError(RuntimeError):

@@ -86,6 +86,7 @@ struct sfft_plan_s {
   I8Config i8{};
   bool i8_ok = false;          // int8-limb tensor-core exp-sum available for this plan
   bool fs_ok = false;          // fused sampling in the FFT CTA for short lines (FP64 plans, L_ref <= kFusedMaxL)
+  int32_t n_fused_iters = 0;   // iterations of the current execute whose sampling ran inside the FFT (report)
   int32_t expsum_path = 0;     // sfft_options.expsum_path
   // stall fallback levels (reading R23): level 0 = the plan's own tilts / E
   int32_t n_levels = 1, lvl_tmax = 1;
@@ -682,6 +683,7 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   mark();
   if (it.fused) {
     // no exp-sum launch: the FFT CTAs sample their lines (the mark pair stays for the profile's bookkeeping)
+    ++P->n_fused_iters;
   } else if (it.use_i8)
     LAUNCH(P, launch_expsum_i8(D, P->i8, it.max_p, it.n_active, it.ksplit, ptr<double2>(P, B_PART), it.max_p,
                                P->smem_optin, st));
@@ -773,6 +775,7 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
     for (int i = 0; i < rep->n_iter_logged; ++i) { rep->primes[i] = hlog[2 * i]; rep->accepted[i] = hlog[2 * i + 1]; }
     rep->kernel_launches = launches;
     rep->n_expsum = n_expsum;
+    rep->n_fused_sample = P->n_fused_iters;
   }
   return SFFT_OK;
 }
@@ -1198,6 +1201,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     return cudaEventRecord(P->events[n_ev++], st) == cudaSuccess ? 0 : -1;
   };
   mark();
+  P->n_fused_iters = 0;
   if ((rc = solve_begin(P, D, sig, launches))) return rc;
   int iter = 1;
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
@@ -1311,6 +1315,7 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
   std::vector<DevParams> D(G);
   int launches = 0, rc;
   auto nomark = []() -> int { return 0; };
+  for (int g = 0; g < G; ++g) plans[g]->n_fused_iters = 0;
   for (int g = 0; g < G; ++g) {
     D[g] = dev_params(plans[g], batch);
     if ((rc = solve_begin(plans[g], D[g], sigs[g], launches))) return rc;
