@@ -775,3 +775,37 @@ def test_e2e_bench_launch_configuration(S, name, T):
         ws, as_ = W.canonical_sort(w[t], a[t])
         assert int(gn[t]) == c.k and np.array_equal(gw_all[t], ws), t
         assert _coef_ok(ga_all[t], as_), t
+
+
+def test_binding_validates_arguments(S):
+    """The C ABI sees raw pointers only, so the binding checks shapes / dtypes / devices / contiguity of the signal
+    and of caller-supplied outputs (ValueError, never an out-of-bounds launch): an empty batch, a batch beyond the
+    plan, the wrong k or d, host tensors, wrong dtypes, non-contiguous and mis-shaped outputs."""
+    c = W.CONFIGS["c2"]
+    plan = _plan(S, c, batch=4)
+    w, a = W.make_batch(c, range(4))
+    wd, ad = torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda()
+    bad_inputs = [(wd[:0], ad[:0]),                                   # empty batch
+                  (torch.cat([wd, wd]), torch.cat([ad, ad])),         # more signals than the plan holds
+                  (wd[:, :50].contiguous(), ad[:, :50].contiguous()),  # k mismatch
+                  (wd[:, :, :2].contiguous(), ad),                    # d mismatch
+                  (torch.from_numpy(w), ad),                          # host tensor
+                  (wd.to(torch.int64), ad),                           # dtype
+                  (wd.transpose(1, 2).contiguous().transpose(1, 2), ad)]   # non-contiguous
+    for fw, fa in bad_inputs:
+        with pytest.raises(ValueError):
+            S.sfft_signal_expsum(plan, fw, fa)
+    sig = S.sfft_signal_expsum(plan, wd, ad)
+    good = (torch.empty((4, c.k, c.d), dtype=torch.int32, device="cuda"),
+            torch.empty((4, c.k, 2), dtype=torch.float64, device="cuda"),
+            torch.empty((4,), dtype=torch.int32, device="cuda"), torch.empty((4,), dtype=torch.int32, device="cuda"))
+    for i, bad in [(0, torch.empty((4, c.k, c.d + 1), dtype=torch.int32, device="cuda")),
+                   (1, torch.empty((4, c.k, 2), dtype=torch.float32, device="cuda")),
+                   (2, torch.empty((3,), dtype=torch.int32, device="cuda")),
+                   (3, torch.empty((4,), dtype=torch.int32))]:
+        outs = list(good)
+        outs[i] = bad
+        with pytest.raises(ValueError):
+            S.sfft_execute(plan, sig, tuple(outs))
+    res = S.sfft_execute(plan, sig, good)
+    assert res.status == S.SFFT_OK
