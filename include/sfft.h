@@ -191,6 +191,23 @@ SFFT_API int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* fr
                     int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
                     sfft_report* rep);
 
+/*
+ * sfft_solve_host_batches -- n_batches consecutive batches of `batch` signals each, HOST buffers, with the
+ * transfers overlapped with the solves: the H2D of batch i + 1 and the D2H of batch i - 1 run on two
+ * library-owned non-blocking streams while batch i is solved on the plan's stream (two device input / output
+ * sets; the second one is allocated on the first call, 2 * batch * k * (4 d + 16) + 16 * batch bytes).
+ * Each batch is an independent sfft_execute (the same results as sfft_solve_host batch by batch).
+ *   freqs  host int32 [n_batches][batch][k][d], coeffs host double [n_batches][batch][k][2]
+ *   out_*  host [n_batches][...] with the per-batch shapes of sfft_execute; out_status nullable
+ *   rep    host, nullable, [n_batches] reports
+ * Pinned (page-locked) host buffers are required for the overlap (pageable ones work, serialised).  Returns after
+ * the last result is on the host: a hard error of any batch at once, else the first SFFT_ENOTSUP /
+ * SFFT_ECORRUPT, else SFFT_PARTIAL if any batch returned it, else SFFT_OK.
+ */
+SFFT_API int sfft_solve_host_batches(sfft_plan_t* plan, int32_t n_batches, int32_t batch, const int32_t* freqs,
+                                     const double* coeffs, int32_t* out_freqs, double* out_coeffs, int32_t* out_count,
+                                     int32_t* out_status, sfft_report* rep);
+
 /* ---- stage entry points (teacher-forced parity of single steps; same kernels as execute) ---- */
 
 /*

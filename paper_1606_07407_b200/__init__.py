@@ -24,7 +24,7 @@ SFFT_ECUDA, SFFT_ENOMEM, SFFT_ENCCL, SFFT_ENOTSUP = -5, -6, -7, -8
 EXPORTS = (
     "sfft_plan", "sfft_plan_workspace_size", "sfft_plan_set_workspace", "sfft_plan_info",
     "sfft_plan_destroy", "sfft_signal_expsum", "sfft_signal_destroy", "sfft_execute",
-    "sfft_solve_host", "sfft_stage_expsum", "sfft_stage_pfft", "sfft_stage_decode",
+    "sfft_solve_host", "sfft_solve_host_batches", "sfft_stage_expsum", "sfft_stage_pfft", "sfft_stage_decode",
     "sfft_stage_project", "sfft_comm_init", "sfft_comm_unique_id", "sfft_execute_group",
     "sfft_line_shard_range", "sfft_comm_peer_handle", "sfft_comm_init_peers", "sfft_strerror",
     "sfft_last_error", "sfft_version",
@@ -92,6 +92,7 @@ def lib() -> ctypes.CDLL:
         L.sfft_signal_destroy.restype = None
         L.sfft_execute.argtypes = [vp, vp, vp, vp, vp, vp, vp]
         L.sfft_solve_host.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp, vp]
+        L.sfft_solve_host_batches.argtypes = [vp, i32, i32, vp, vp, vp, vp, vp, vp, vp]
         L.sfft_stage_expsum.argtypes = [vp, i32, vp, vp, i64, i32, vp]
         L.sfft_stage_pfft.argtypes = [vp, i32, i64, vp]
         L.sfft_stage_decode.argtypes = [vp, i64, i32, i32, vp, vp, vp, vp, vp]
@@ -337,6 +338,44 @@ def sfft_solve_host(plan: Plan, freqs, coeffs, out=None) -> Result:
                                ctypes.c_void_p(on.data_ptr()), ctypes.c_void_p(os_.data_ptr()), ctypes.byref(rep))
     _check(rc, plan.handle, ok=(SFFT_OK, SFFT_PARTIAL, SFFT_ENOTSUP, SFFT_ECORRUPT))
     return Result(rc, of, torch.view_as_complex(oc), on, os_, rep)
+
+
+def sfft_solve_host_batches(plan: Plan, freqs, coeffs, out=None):
+    """n_batches batches of HOST tensors (pinned for the overlap): freqs int32 [n_batches, batch, k, d], coeffs
+    complex128 [n_batches, batch, k] (or float64 [..., 2]).  The library overlaps the H2D / D2H of neighbouring
+    batches with each solve.  Returns (status, out_freqs, out_coeffs, out_count, out_status, [reports])."""
+    torch = _torch()
+    if freqs.dim() != 4:
+        raise ValueError(f"freqs: expected [n_batches, batch, k, d], got shape {tuple(freqs.shape)}")
+    nb, B = freqs.shape[0], freqs.shape[1]
+    if nb < 1:
+        raise ValueError("freqs: no batches")
+    if B < 1 or B > plan.batch:
+        raise ValueError(f"freqs: batch {B} outside [1, plan batch {plan.batch}]")
+    _require(freqs, "freqs", (nb, B, plan.k, plan.d), torch.int32, cuda=False)
+    c = coeffs if not coeffs.is_complex() else torch.view_as_real(coeffs)
+    _require(c, "coeffs", (nb, B, plan.k, 2), torch.float64, cuda=False)
+    if out is None:
+        out = (torch.empty((nb, B, plan.k, plan.d), dtype=torch.int32).pin_memory(),
+               torch.empty((nb, B, plan.k, 2), dtype=torch.float64).pin_memory(),
+               torch.empty((nb, B), dtype=torch.int32).pin_memory(),
+               torch.empty((nb, B), dtype=torch.int32).pin_memory())
+    if len(out) != 4:
+        raise ValueError("out: expected (freqs, coeffs, count, status)")
+    of, oc, on, os_ = out
+    oc = oc if not oc.is_complex() else torch.view_as_real(oc)
+    _require(of, "out freqs", (nb, B, plan.k, plan.d), torch.int32, cuda=False)
+    _require(oc, "out coeffs", (nb, B, plan.k, 2), torch.float64, cuda=False)
+    _require(on, "out count", (nb, B), torch.int32, cuda=False)
+    if os_ is not None:
+        _require(os_, "out status", (nb, B), torch.int32, cuda=False)
+    reps = (sfft_report * nb)()
+    rc = lib().sfft_solve_host_batches(plan.handle, nb, B, ctypes.c_void_p(freqs.data_ptr()),
+                                       ctypes.c_void_p(c.data_ptr()), ctypes.c_void_p(of.data_ptr()),
+                                       ctypes.c_void_p(oc.data_ptr()), ctypes.c_void_p(on.data_ptr()),
+                                       ctypes.c_void_p(_ptr(os_)), ctypes.cast(reps, ctypes.c_void_p))
+    _check(rc, plan.handle, ok=(SFFT_OK, SFFT_PARTIAL, SFFT_ENOTSUP, SFFT_ECORRUPT))
+    return rc, of, torch.view_as_complex(oc), on, os_, list(reps)
 
 
 # ------------------------------------------------------------------ stage entry points

@@ -124,6 +124,11 @@ struct sfft_plan_s {
   bool peer_ready = false;
   int32_t peer_epoch = 0;
   cudaEvent_t ev_ctrl = nullptr;   // the per-iteration control read (iter_setup)
+  // sfft_solve_host_batches: the second device input / output set, the H2D and D2H streams and their events
+  void* pipe_buf = nullptr;
+  size_t pipe_bytes = 0;
+  cudaStream_t pipe_st[2] = {nullptr, nullptr};
+  cudaEvent_t pipe_ev[6] = {};    // [set] inputs landed, [2 + set] solve done, [4 + set] outputs copied out
 };
 
 namespace {
@@ -1156,6 +1161,11 @@ void sfft_plan_destroy(sfft_plan_t* plan) {
   if (plan->h_ctrl) cudaFreeHost(plan->h_ctrl);
   if (plan->ev_ctrl) cudaEventDestroy(plan->ev_ctrl);
   for (cudaEvent_t e : plan->events) cudaEventDestroy(e);
+  if (plan->pipe_buf) cudaFree(plan->pipe_buf);
+  for (cudaStream_t s : plan->pipe_st)
+    if (s) cudaStreamDestroy(s);
+  for (cudaEvent_t e : plan->pipe_ev)
+    if (e) cudaEventDestroy(e);
   delete plan;
 }
 
@@ -1409,6 +1419,80 @@ int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, cons
     CUDA_TRY(P, cudaMemcpyAsync(out_status, ptr<int32_t>(P, B_OUT_S), 4 * (size_t)batch, cudaMemcpyDeviceToHost, P->stream));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return st;
+}
+
+int sfft_solve_host_batches(sfft_plan_t* plan, int32_t n_batches, int32_t batch, const int32_t* freqs,
+                            const double* coeffs, int32_t* out_freqs, double* out_coeffs, int32_t* out_count,
+                            int32_t* out_status, sfft_report* rep) {
+  if (!plan || n_batches < 1 || !freqs || !coeffs || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
+  if (batch < 1 || batch > plan->batch) return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch);
+  int rc = ensure_ready(plan);
+  if (rc) return rc;
+  sfft_plan_t* P = plan;
+  const size_t nf = 4 * (size_t)batch * P->k * P->d, nc = 16 * (size_t)batch * P->k, ns = 4 * (size_t)batch;
+  // the second input / output set (the first is the workspace's, shared with sfft_solve_host), 256-B aligned parts
+  const size_t a_nf = align_up(nf, 256), a_nc = align_up(nc, 256), a_ns = align_up(ns, 256);
+  const size_t set_bytes = 2 * a_nf + 2 * a_nc + 2 * a_ns;
+  if (P->pipe_bytes < set_bytes) {
+    if (P->pipe_buf) cudaFree(P->pipe_buf);
+    P->pipe_buf = nullptr;
+    P->pipe_bytes = 0;
+    const cudaError_t e = cudaMalloc(&P->pipe_buf, set_bytes);
+    if (e != cudaSuccess) return fail(P, SFFT_ENOMEM, "cudaMalloc(%zu) for the batch pipeline: %s", set_bytes,
+                                      cudaGetErrorString(e));
+    P->pipe_bytes = set_bytes;
+  }
+  for (cudaStream_t& s : P->pipe_st)
+    if (!s) CUDA_TRY(P, cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : P->pipe_ev)
+    if (!e) CUDA_TRY(P, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  struct Set { int32_t* f; double* c; int32_t* of; double* oc; int32_t* on; int32_t* os; };
+  char* pb = static_cast<char*>(P->pipe_buf);
+  const Set sets[2] = {
+      {ptr<int32_t>(P, B_IN_F), ptr<double>(P, B_IN_C), ptr<int32_t>(P, B_OUT_F), ptr<double>(P, B_OUT_C),
+       ptr<int32_t>(P, B_OUT_N), ptr<int32_t>(P, B_OUT_S)},
+      {reinterpret_cast<int32_t*>(pb), reinterpret_cast<double*>(pb + a_nf), reinterpret_cast<int32_t*>(pb + a_nf + a_nc),
+       reinterpret_cast<double*>(pb + 2 * a_nf + a_nc), reinterpret_cast<int32_t*>(pb + 2 * a_nf + 2 * a_nc),
+       reinterpret_cast<int32_t*>(pb + 2 * a_nf + 2 * a_nc + a_ns)}};
+  cudaStream_t h2d = P->pipe_st[0], d2h = P->pipe_st[1];
+  // H2D of batch i into set i & 1 once the solve of batch i - 2 (the set's previous user) has finished
+  auto load = [&](int i) -> int {
+    const Set& s = sets[i & 1];
+    if (i >= 2) CUDA_TRY(P, cudaStreamWaitEvent(h2d, P->pipe_ev[2 + (i & 1)], 0));
+    CUDA_TRY(P, cudaMemcpyAsync(s.f, reinterpret_cast<const char*>(freqs) + i * nf, nf, cudaMemcpyHostToDevice, h2d));
+    CUDA_TRY(P, cudaMemcpyAsync(s.c, reinterpret_cast<const char*>(coeffs) + i * nc, nc, cudaMemcpyHostToDevice, h2d));
+    CUDA_TRY(P, cudaEventRecord(P->pipe_ev[i & 1], h2d));
+    return SFFT_OK;
+  };
+  if ((rc = load(0))) return rc;
+  if (n_batches > 1 && (rc = load(1))) return rc;
+  int result = SFFT_OK;
+  for (int i = 0; i < n_batches; ++i) {
+    const Set& s = sets[i & 1];
+    CUDA_TRY(P, cudaStreamWaitEvent(P->stream, P->pipe_ev[i & 1], 0));              // inputs of batch i landed
+    if (i >= 2) CUDA_TRY(P, cudaStreamWaitEvent(P->stream, P->pipe_ev[4 + (i & 1)], 0));  // outputs of i - 2 read out
+    sfft_signal_t sig{P, batch, s.f, s.c};
+    const int st = sfft_execute(P, &sig, s.of, s.oc, s.on, s.os, rep ? rep + i : nullptr);
+    if (st < 0 && st != SFFT_ENOTSUP && st != SFFT_ECORRUPT) {
+      cudaStreamSynchronize(h2d);
+      cudaStreamSynchronize(d2h);
+      return st;
+    }
+    if (st < 0 && result >= 0) result = st;
+    else if (st > 0 && result == SFFT_OK) result = st;
+    CUDA_TRY(P, cudaEventRecord(P->pipe_ev[2 + (i & 1)], P->stream));
+    CUDA_TRY(P, cudaStreamWaitEvent(d2h, P->pipe_ev[2 + (i & 1)], 0));
+    CUDA_TRY(P, cudaMemcpyAsync(reinterpret_cast<char*>(out_freqs) + i * nf, s.of, nf, cudaMemcpyDeviceToHost, d2h));
+    CUDA_TRY(P, cudaMemcpyAsync(reinterpret_cast<char*>(out_coeffs) + i * nc, s.oc, nc, cudaMemcpyDeviceToHost, d2h));
+    CUDA_TRY(P, cudaMemcpyAsync(reinterpret_cast<char*>(out_count) + i * ns, s.on, ns, cudaMemcpyDeviceToHost, d2h));
+    if (out_status)
+      CUDA_TRY(P, cudaMemcpyAsync(reinterpret_cast<char*>(out_status) + i * ns, s.os, ns, cudaMemcpyDeviceToHost, d2h));
+    CUDA_TRY(P, cudaEventRecord(P->pipe_ev[4 + (i & 1)], d2h));
+    if (i + 2 < n_batches && (rc = load(i + 2))) return rc;
+  }
+  CUDA_TRY(P, cudaStreamSynchronize(d2h));
+  CUDA_TRY(P, cudaStreamSynchronize(P->stream));
+  return result;
 }
 
 // ---------------------------------------------------------------- stage entry points

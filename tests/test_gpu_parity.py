@@ -292,8 +292,8 @@ def test_determinism(S):
 
 @pytest.mark.parametrize("T", [4, 17])
 def test_solve_host_matches_device(S, T):
-    """The host-buffer entry point (T >= 8: two chunks whose copies overlap the other chunk's solve) gives bitwise
-    the device path's result and the same aggregate report."""
+    """The host-buffer entry point gives bitwise the device path's result and the same aggregate report (a batch of
+    4 and a ragged 17)."""
     c = W.CONFIGS["c2"]
     w, a = W.make_batch(c, range(T))
     plan = _plan(S, c, batch=T)
@@ -303,6 +303,37 @@ def test_solve_host_matches_device(S, T):
     assert torch.equal(fd, rh.freqs) and torch.equal(torch.view_as_real(cd), torch.view_as_real(rh.coeffs))
     assert torch.equal(rd.count.cpu(), rh.count) and torch.equal(rd.per_status.cpu(), rh.per_status)
     assert rh.report.samples_used == rd.report.samples_used and rh.status == rd.status
+
+
+@pytest.mark.parametrize("name,T,nb", [("c2", 8, 1), ("c2", 5, 4), ("c3", 2, 3)])
+def test_solve_host_batches_matches_per_batch(S, name, T, nb):
+    """sfft_solve_host_batches (nb batches of T signals, the transfers of neighbouring batches overlapping each
+    solve on two extra streams and a second device buffer set) gives, batch by batch, bitwise the results, counts,
+    statuses and reports of separate device executes; distinct signals per batch so a batch routed to the wrong
+    buffer set fails."""
+    c = W.CONFIGS[name]
+    ws, as_ = zip(*(W.make_batch(c, range(b * T, (b + 1) * T)) for b in range(nb)))
+    plan = _plan(S, c, batch=T)
+    wb = torch.from_numpy(np.stack(ws)).pin_memory()
+    ab = torch.from_numpy(np.stack(as_)).pin_memory()
+    rc, of, oc, on, os_, reps = S.sfft_solve_host_batches(plan, wb, ab)
+    assert len(reps) == nb
+    for b in range(nb):
+        rd = S.solve(plan, torch.from_numpy(ws[b]).cuda(), torch.from_numpy(as_[b]).cuda())
+        assert torch.equal(rd.freqs.cpu(), of[b])
+        assert torch.equal(torch.view_as_real(rd.coeffs.cpu()), torch.view_as_real(oc[b]))
+        assert torch.equal(rd.count.cpu(), on[b]) and torch.equal(rd.per_status.cpu(), os_[b])
+        assert reps[b].samples_used == rd.report.samples_used and reps[b].iterations == rd.report.iterations
+        for i in range(T):                                     # exact recovery
+            assert np.array_equal(of[b][i].numpy(), W.canonical_sort(ws[b][i], as_[b][i])[0])
+    assert rc == S.SFFT_OK
+    # a second call reuses the buffers; a pageable (unpinned) input still gives the same results
+    rc2, of2, oc2, _, _, _ = S.sfft_solve_host_batches(plan, torch.from_numpy(np.stack(ws)), ab)
+    assert rc2 == rc and torch.equal(of2, of) and torch.equal(torch.view_as_real(oc2), torch.view_as_real(oc))
+    with pytest.raises(ValueError):
+        S.sfft_solve_host_batches(plan, wb[0], ab[0])          # not [n_batches, batch, k, d]
+    with pytest.raises(ValueError):
+        S.sfft_solve_host_batches(plan, wb.cuda(), ab)         # device tensor
 
 
 def test_error_codes(S):
