@@ -141,7 +141,7 @@ enum Buf {
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
   B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY, B_SPINERR,
-  B_FFTW, B_DLROOT,
+  B_FFTW, B_DLROOT, B_CROWI, B_CROWL,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -289,6 +289,8 @@ void layout(sfft_plan_t* P) {
   sz[B_I8ELOG] = logt ? 4 * S * align_up((size_t)P->kk + 16, 4) : 0;
   sz[B_I8CHL] = logt ? 16 * T * (2 * P->p_stride + 8) : 0;
   sz[B_DLROOT] = P->fs_ok ? 16 * T * (2 * P->p_stride + 8) : 0;
+  sz[B_CROWI] = 16 * S * (size_t)((P->k + 31) / 32) * ((P->Lp + 15) / 16);
+  sz[B_CROWL] = 4 * S * (size_t)P->k;
   sz[B_STSLOT] = 4 * S;
   sz[B_SLOTP] = 4 * T;
   sz[B_SLOTE] = 4 * T;
@@ -421,6 +423,9 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
     D.i8_chl = ptr<double2>(P, B_I8CHL);
   }
   if (P->fs_ok) D.dl_root = ptr<double2>(P, B_DLROOT);
+  D.crow_nl = (P->Lp + 15) / 16;
+  D.crow_items = ptr<int4>(P, B_CROWI);
+  D.crow_list = ptr<int32_t>(P, B_CROWL);
   D.line_lo = P->line_lo;
   D.line_G = std::max(P->line_G, 1);
   D.line_g = P->line_g;
@@ -718,12 +723,30 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   return SFFT_OK;
 }
 
+// the C rows of the touched entries in the GPU-wide crow kernel when few signals are active (the commit grid
+// leaves most SMs idle: single solves) and their rows are long: k* L >= 8192 elements per signal with k* ~ p / c
+// (C3 / C4 / C5 first iterations).  Batched steps keep the rows in the commit CTAs, which already spread over the
+// SMs: there the extra launch per iteration measured slower (C5 14.16 -> 14.53 ms, C4 2.59 -> 2.61 ms);
+// single solves gain (C3 0.667 -> 0.632 ms, C4 0.446 -> 0.412 ms).  SFFT_CROW=0/1 forces the choice.
+bool crow_on(const sfft_plan_t* P, const IterPlan& it) {
+  static const int env = getenv("SFFT_CROW") ? atoi(getenv("SFFT_CROW")) : -1;
+  if (env >= 0) return env != 0;
+  return 4L * it.n_active <= P->n_sm && (long)(it.max_p / std::max(P->c, 1)) * P->L >= 8192;
+}
+
 int iter_back(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, const sfft_signal_t* sig, int& launches) {
   cudaStream_t st = P->stream;
   if (!it.fuse_commit) {
     D.i8_iter = it.use_i8 ? 1 : 0;
+    D.crow_mode = crow_on(P, it) ? 1 : 0;
     LAUNCH(P, launch_decode_commit(D, iter, it.max_p, it.n_active, st));
     D.i8_iter = 0;
+    if (D.crow_mode) {
+      // one CTA per work item of the largest iteration (every signal touching k entries), at most 8 per SM
+      const long items = (long)it.n_active * ((P->k + 31) / 32) * D.crow_nl;
+      LAUNCH(P, launch_crow(D, (int)std::min<long>(items, 8L * P->n_sm), st));
+      D.crow_mode = 0;
+    }
   }
   if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
     LAUNCH(P, launch_retilt(D, sig->batch, sig->freqs, st));

@@ -332,22 +332,58 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   //      accepted candidate with the same key (found = -2 - t'); so is a key of R found twice (its += a would
   //      race in 4b).  With the check on, equal keys have equal
   //      v_m mod p = b, so distinct candidates never collide and this pass is skipped.
+  //      The first occurrence comes from a table of key-hash groups (open addressing over the freed cand array,
+  //      slot = 1 + the smallest t of the group by atomicMin); a group whose smallest t holds a different key
+  //      (a 64-bit hash collision) falls back to the scan over every earlier t.
   bool any_dup = false;
   if (!(P.extra & 2)) {
+    int* gtab = cand;                                   // p ints; p >= c k* >= 2 na
+    int tsz = 1;
+    while (2 * tsz <= p) tsz *= 2;
+    const int gm = tsz - 1;
+    for (int i = tid; i < tsz; i += blockDim.x) gtab[i] = 0;
+    __syncthreads();
+    for (int t = tid; t < na; t += blockDim.x) {
+      const uint64_t h = hsh[t];
+      int slot = (int)((h ^ (h >> 32)) & (uint64_t)gm);
+      for (;;) {
+        int o = reinterpret_cast<volatile int*>(gtab)[slot];
+        if (o == 0) {
+          o = atomicCAS(&gtab[slot], 0, t + 1);
+          if (o == 0) break;
+        }
+        if (hsh[o - 1] == h) {                          // every occupant of a slot has this slot's hash
+          atomicMin(&gtab[slot], t + 1);
+          break;
+        }
+        slot = (slot + 1) & gm;
+      }
+    }
+    __syncthreads();
     int dup_local = 0;
     for (int t = tid; t < na; t += blockDim.x) {
+      const uint64_t h = hsh[t];
+      int slot = (int)((h ^ (h >> 32)) & (uint64_t)gm);
+      while (hsh[gtab[slot] - 1] != h) slot = (slot + 1) & gm;
+      const int first = gtab[slot] - 1;
       int dup = -1;
-      if (found[t] >= 0) {                              // an existing key found twice: serialise its += a
-        for (int t2 = 0; t2 < t && dup < 0; ++t2)
-          if (found[t2] == found[t]) dup = t2;
-      } else {
-        const int ci = accl[t];
-        for (int t2 = 0; t2 < t && dup < 0; ++t2) {
-          if (found[t2] >= 0 || hsh[t2] != hsh[t]) continue;
-          const int c2 = accl[t2];
-          bool eq = true;
-          for (int n = 0; n < r && eq; ++n) eq = accv[(int64_t)n * P.k + c2] == accv[(int64_t)n * P.k + ci];
-          if (eq) dup = t2;
+      if (first != t) {
+        const int ci = accl[t], c1 = accl[first];
+        bool eq = found[first] == found[t];
+        if (eq && found[t] < 0)
+          for (int n = 0; n < r && eq; ++n) eq = accv[(int64_t)n * P.k + c1] == accv[(int64_t)n * P.k + ci];
+        if (eq) dup = first;
+        else if (found[t] >= 0) {                       // hash collision: the scan (an existing key found twice)
+          for (int t2 = 0; t2 < t && dup < 0; ++t2)
+            if (found[t2] == found[t]) dup = t2;
+        } else {
+          for (int t2 = 0; t2 < t && dup < 0; ++t2) {
+            if (found[t2] >= 0 || hsh[t2] != h) continue;
+            const int c2 = accl[t2];
+            bool e2 = true;
+            for (int n = 0; n < r && e2; ++n) e2 = accv[(int64_t)n * P.k + c2] == accv[(int64_t)n * P.k + ci];
+            if (e2) dup = t2;
+          }
         }
       }
       flag[t] = dup;
@@ -437,49 +473,6 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   __syncthreads();
   const int nR_new = nR + n_new;
 
-  // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}.  Items
-  // (entry, 8 lines) with the entries along the threads; v from the record (a touched entry's key equals
-  // its candidate's coordinates), coalesced, the 8 loads of an item in flight together
-  double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
-  const int lch = (P.Lp + 7) / 8;
-  const bool by_items = 2 * na * lch >= (int)blockDim.x;  // else too few items: warp per entry, lanes along the row
-  for (int t = warp; !by_items && t < na; t += nwarps) {
-    const int e = found[t], ci = accl[t];
-    const double2 a = areg[e];
-    for (int n = lane; n < P.Lp; n += 32) {
-      double2 c;
-      if (n == 0) c = make_double2(-a.x, -a.y);
-      else if (n < P.L) {
-        const double2 lf = line_factor_exact(accv[(int64_t)(P.line_lo + n - 1) * P.k + ci], Ev);
-        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
-      } else c = make_double2(0.0, 0.0);
-      Creg[(int64_t)e * P.Lp + n] = c;
-    }
-  }
-  for (int it = tid; by_items && it < na * lch; it += blockDim.x) {
-    const int t = it % na, n0 = (it / na) * 8;
-    const int e = found[t], ci = accl[t];
-    const double2 a = areg[e];
-    int64_t v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u;
-      v[u] = (n >= 1 && n < P.L) ? accv[(int64_t)(P.line_lo + n - 1) * P.k + ci] : 0;
-    }
-    double2* row = Creg + (int64_t)e * P.Lp;
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int n = n0 + u;
-      if (n >= P.Lp) break;
-      double2 c;
-      if (n == 0) c = make_double2(-a.x, -a.y);
-      else if (n < P.L) {
-        const double2 lf = line_factor_exact(v[u], Ev);
-        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
-      } else c = make_double2(0.0, 0.0);
-      row[n] = c;
-    }
-  }
   // prune test (only touched entries can have changed)
   int small = 0;
   for (int t = tid; t < na; t += blockDim.x) {
@@ -487,9 +480,63 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
     small |= hypot(a.x, a.y) < P.prune;
   }
   const int any_small = __syncthreads_or(small);
+  double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+  if (P.crow_mode && !any_small) {
+    // the rows go to crow_kernel (GPU-wide): the touched entries in ascending b and this signal's work items
+    for (int t = tid; t < na; t += blockDim.x) P.crow_list[(int64_t)s * P.k + t] = found[t];
+    const int nit = ((na + 31) / 32) * P.crow_nl;
+    if (tid == 0) scratch[0] = nit > 0 ? atomicAdd(&P.ctrl[5], nit) : 0;
+    __syncthreads();
+    const int base = scratch[0];
+    for (int i = tid; i < nit; i += blockDim.x) P.crow_items[base + i] = make_int4(s, i / P.crow_nl, i % P.crow_nl, na);
+  } else {
+    // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}.  Items
+    // (entry, 8 lines) with the entries along the threads; v from the record (a touched entry's key equals
+    // its candidate's coordinates), coalesced, the 8 loads of an item in flight together
+    const int lch = (P.Lp + 7) / 8;
+    const bool by_items = 2 * na * lch >= (int)blockDim.x;  // else too few items: warp per entry, lanes along the row
+    for (int t = warp; !by_items && t < na; t += nwarps) {
+      const int e = found[t], ci = accl[t];
+      const double2 a = areg[e];
+      for (int n = lane; n < P.Lp; n += 32) {
+        double2 c;
+        if (n == 0) c = make_double2(-a.x, -a.y);
+        else if (n < P.L) {
+          const double2 lf = line_factor_exact(accv[(int64_t)(P.line_lo + n - 1) * P.k + ci], Ev);
+          c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+        } else c = make_double2(0.0, 0.0);
+        Creg[(int64_t)e * P.Lp + n] = c;
+      }
+    }
+    for (int it = tid; by_items && it < na * lch; it += blockDim.x) {
+      const int t = it % na, n0 = (it / na) * 8;
+      const int e = found[t], ci = accl[t];
+      const double2 a = areg[e];
+      int64_t v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int n = n0 + u;
+        v[u] = (n >= 1 && n < P.L) ? accv[(int64_t)(P.line_lo + n - 1) * P.k + ci] : 0;
+      }
+      double2* row = Creg + (int64_t)e * P.Lp;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int n = n0 + u;
+        if (n >= P.Lp) break;
+        double2 c;
+        if (n == 0) c = make_double2(-a.x, -a.y);
+        else if (n < P.L) {
+          const double2 lf = line_factor_exact(v[u], Ev);
+          c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+        } else c = make_double2(0.0, 0.0);
+        row[n] = c;
+      }
+    }
+  }
   int nR_final = nR_new;
   if (any_small) {
     // rare path: order-preserving compaction by warp 0, then rebuild the hash table
+    __syncthreads();                                    // the C rows above are in before warp 0 moves them
     if (warp == 0) {
       int wpos = 0;
       for (int e = 0; e < nR_new; ++e) {

@@ -327,6 +327,53 @@ cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p
   return cudaGetLastError();
 }
 
+// C rows of the entries this iteration's commits touched (DevParams::crow_mode): work item = 32 touched entries
+// (lanes) x 16 lines (4 warps x 4 lines), C[k+e][0] = -a_e, C[k+e][n] = -a_e e^{2 pi i (v_{e,n} mod E)/E} (the
+// commit's own formula, line_factor_exact), staged in shared memory and stored as 256-B row segments.  The items
+// are counted in ctrl[5] of the iteration's control block (zeroed by the previous iteration's table prep, which
+// clears the next block; this iteration's prep clears the other one).
+__global__ void __launch_bounds__(128) crow_kernel(DevParams P) {
+  pdl_wait();
+  __shared__ double2 tile[32][17];
+  __shared__ int ent[32];
+  const int n_items = P.ctrl[5];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int w = blockIdx.x; w < n_items; w += gridDim.x) {
+    const int4 item = P.crow_items[w];
+    const int s = item.x, t0 = item.y * 32, n0 = item.z * 16, na = item.w;
+    const int64_t Ev = P.lvl_E[P.st_lvl[s]];           // the commit's level (a level switch touches no entry)
+    const int t = t0 + lane;
+    const int e = t < na ? P.crow_list[(int64_t)s * P.k + t] : -1;
+    if (warp == 0) ent[lane] = e;
+    double2 a = make_double2(0.0, 0.0);
+    if (e >= 0) a = P.a_reg[(int64_t)s * P.k + e];
+    const int64_t* vreg = P.v_all + (int64_t)s * P.r * P.kk + P.k;
+    for (int j = warp; j < 16; j += 4) {
+      const int n = n0 + j;
+      double2 c = make_double2(0.0, 0.0);
+      if (e >= 0 && n == 0) c = make_double2(-a.x, -a.y);
+      else if (e >= 0 && n < P.L) {
+        const double2 lf = line_factor_exact(vreg[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
+        c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+      }
+      tile[lane][j] = c;
+    }
+    __syncthreads();
+    double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+    for (int i = threadIdx.x; i < 32 * 16; i += 128) {
+      const int row = i >> 4, col = i & 15;
+      const int n = n0 + col, ee = ent[row];
+      if (ee >= 0 && n < P.Lp) Creg[(int64_t)ee * P.Lp + n] = tile[row][col];
+    }
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_crow(const DevParams& P, int32_t grid, cudaStream_t st) {
+  if (grid < 1) return cudaGetLastError();
+  return launch_pdl(crow_kernel, dim3(grid), dim3(128), 0, st, P);
+}
+
 cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,
                                 double* acc_a, int32_t* counts, cudaStream_t st) {
   const int max_p = (int)P.p_stride;

@@ -154,6 +154,13 @@ struct DevParams {
   int32_t fuse_commit;         // pfft launch flag: the last CTA of a signal to finish runs its commit (a7)
   int32_t cur_iter;            // the iteration of that launch (the commit's state / log)
   int32_t* commit_cnt;         // [batch] arrival counters of the fused commit (reset by the last CTA)
+  // C rows of the entries an iteration touched, spread over the GPU (crow_kernel, k_decode.cu) instead of in the
+  // commit CTA: the commit lists the touched entries and appends work items (32 entries x 16 lines) counted in
+  // ctrl[5]
+  int32_t crow_mode;           // launch flag of the commit kernel (0: the commit writes the rows itself)
+  int32_t crow_nl;             // 16-line chunks per row, ceil(Lp / 16)
+  int4* crow_items;            // [batch * ceil(k / 32) * crow_nl] (signal, entry chunk, line chunk, touched count)
+  int32_t* crow_list;          // [batch][k] touched entry indices of the iteration, ascending b
   int32_t* sel_ready;          // [batch]
   // fused record exchange (sfft_options.line_exchange = 1): the FFT epilogue stores its record words straight into
   // the receive buffer of every shard (peer memory: CUDA IPC mappings across GPUs, plain pointers on one device)
@@ -215,11 +222,18 @@ __host__ __device__ __forceinline__ int64_t mod_near64(int64_t x, int64_t m) {
   const int64_t q = x < 0 ? x + m : x;
   return (q >= 0 && q < m) ? q : mod_pos64(x, m);
 }
-// e^{2 pi i (v mod E)/E} via sincospi of the exactly reduced rational 2 (v mod E) / E (line factor of a shift)
+// e^{2 pi i (v mod E)/E} via sincospi of the exactly reduced rational 2 (v mod E) / E (line factor of a shift).
+// E a power of two 2^t (every plan whose N is one): 2q / E = q * 2^(1-t) exactly, a multiply instead of the FP64
+// division -- the same double bit for bit
 __device__ __forceinline__ double2 line_factor_exact(int64_t v, int64_t E) {
   const int64_t q = mod_near64(v, E);
   double s, c;
-  sincospi(2.0 * (double)q / (double)E, &s, &c);
+  if ((E & (E - 1)) == 0) {
+    const int t = 63 - __clzll((unsigned long long)E);
+    sincospi((double)q * __longlong_as_double((long long)(1024 - t) << 52), &s, &c);
+  } else {
+    sincospi(2.0 * (double)q / (double)E, &s, &c);
+  }
   return make_double2(c, s);
 }
 
@@ -263,6 +277,8 @@ cudaError_t launch_line_coeffs(const DevParams& P, int32_t K, const double* c, c
 cudaError_t launch_setup(const DevParams& P, int32_t iter, cudaStream_t st, int32_t seq = 0);
 // commit of an iteration: the records of the fused FFT epilogue (all line shards) -> registry update, state
 cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st);
+// the C rows listed by this iteration's commits (P.crow_mode); grid = CTAs looping over the work items
+cudaError_t launch_crow(const DevParams& P, int32_t grid, cudaStream_t st);
 // re-projection of the signals that switched fallback level (reading R23); freqs = the execute's input
 cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freqs, cudaStream_t st);
 cudaError_t launch_stage_decode(const DevParams& P, int32_t kstar, int32_t* acc_b, int64_t* acc_v,

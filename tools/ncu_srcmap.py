@@ -22,7 +22,8 @@ def ncu_rows(rep, kernel=None):
     r = csv.reader(out.splitlines())
     next(r)
     hdr = next(r)
-    iw, isrc = hdr.index("Warp Stall Sampling (All Samples)"), hdr.index("Source")
+    col = __import__("os").environ.get("SRCMAP_COL", "Warp Stall Sampling (All Samples)")   # or "Instructions Executed"
+    iw, isrc = hdr.index(col), hdr.index("Source")
     rows = []
     for x in r:                                   # several launches: the first launch's listing only
         if x and x[0] in ("Kernel Name", "Address"):
