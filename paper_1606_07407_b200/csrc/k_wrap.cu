@@ -2,9 +2,9 @@
 //   untilt every tilted pair: u = T^T v / hypo^2, rejecting non-integers (Alg. 3 l.38-39, reading R17)
 //   wrap every block by balanced digits: digit = ((u + N/2) mod N) - N/2, u <- (u - digit)/N
 //   canonical order: lexicographic by frequency vector.
-// Three kernels: digits (lanes over the blocks of a registry entry), rank (one CTA per signal: a bitonic sort of
-// the rows packed into 64-bit chunks in shared memory, or an O(k^2) ranking by keys of the first two coordinates
-// with a full compare on ties when they do not fit), gather.
+// Three kernels: digits (lanes over the blocks of a registry entry), rank (one CTA per signal: a bitonic sort by
+// the rows' first coordinates packed into a 64-bit key in shared memory, ties ordered by the full rows; an O(k^2)
+// ranking when the keys do not fit), gather.
 #include <algorithm>
 
 #include "sfft_internal.cuh"
@@ -71,51 +71,98 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G
   if (err) bad[s] = 1;
 }
 
-// lexicographic order of the entries -> perm[s][rank] = entry.  Rows packed into fixed-width 64-bit chunks in
-// shared memory (coordinate + N/2 in `bits` bits, `per` coordinates per chunk, most significant first): chunk
-// sequences compare like the rows.  A bitonic sort of the entry indices (a power of two >= nR slots, padding
-// sorts last; equal rows -- only possible for entries flagged bad -- by index) replaces the O(k^2) ranking.
-__global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm, int bits, int per, int nch) {
+// lexicographic order of the entries -> perm[s][rank] = entry.  Rows packed into fixed-width 64-bit chunks
+// (coordinate + N/2 in `bits` bits, `per` coordinates per chunk, most significant first): chunk sequences compare
+// like the rows.  A bitonic sort of the entry indices (a power of two >= nR slots, padding last) first by chunk 0
+// and the index -- random rows never tie there, so one chunk per row is built; when some rows tie on chunk 0
+// (structured spectra, e.g. C5's collinear groups) the other chunks are built (`nchs` = nch chunks fit in shared
+// memory) and the sort reruns on the whole rows; equal rows (entries flagged bad) stay by index.  Without room for
+// the other chunks, runs of equal chunk 0 are insertion-sorted by the full rows from global memory.
+__global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm, int bits, int per, int nch,
+                                        int nchs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [nch][k]
-  int* ord = reinterpret_cast<int*>(key + (size_t)nch * P.k);                     // [power of two >= k]
+  unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [nchs][k]
+  int* ord = reinterpret_cast<int*>(key + (size_t)nchs * P.k);                   // [power of two >= k]
+  __shared__ int any_tie;
   const int s = blockIdx.x, tid = threadIdx.x;
   const int nR = P.st_nR[s];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
   const int64_t h2 = P.N / 2;
-  for (int i = tid; i < nch * nR; i += blockDim.x) {         // chunk index fastest: coalesced row reads
-    const int e = i / nch, c = i - e * nch;
-    const int32_t* row = wt + (int64_t)e * P.d;
-    unsigned long long kv = 0;
-    for (int t = 0; t < per; ++t) {
-      const int l = c * per + t;
-      kv = (kv << bits) | (l < P.d ? (unsigned long long)(row[l] + h2) : 0ull);
+  auto build = [&](int c0, int c1) {                         // chunks [c0, c1) of every row, chunk index fastest
+    const int nc = c1 - c0;
+    for (int i = tid; i < nc * nR; i += blockDim.x) {
+      const int e = i / nc, c = c0 + (i - e * nc);
+      const int32_t* row = wt + (int64_t)e * P.d;
+      unsigned long long kv = 0;
+      for (int t = 0; t < per; ++t) {
+        const int l = c * per + t;
+        kv = (kv << bits) | (l < P.d ? (unsigned long long)(row[l] + h2) : 0ull);
+      }
+      key[(int64_t)c * P.k + e] = kv;
     }
-    key[(int64_t)c * P.k + e] = kv;
-  }
+  };
+  build(0, 1);
   int n = 1;
   while (n < nR) n <<= 1;
   for (int i = tid; i < n; i += blockDim.x) ord[i] = i < nR ? i : 0x7fffffff;
+  if (tid == 0) any_tie = 0;
   __syncthreads();
-  auto less = [&](int a, int b) -> bool {                    // row a before row b
-    if (b == 0x7fffffff) return a != 0x7fffffff;
-    if (a == 0x7fffffff) return false;
-    for (int c = 0; c < nch; ++c) {
-      const unsigned long long ka = key[(int64_t)c * P.k + a], kb = key[(int64_t)c * P.k + b];
-      if (ka != kb) return ka < kb;
-    }
-    return a < b;
-  };
-  for (int size = 2; size <= n; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int i = tid; i < (n >> 1); i += blockDim.x) {
-        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
-        const int a = ord[lo], b = ord[hi];
-        const bool up = (lo & size) == 0;
-        if (up ? less(b, a) : less(a, b)) { ord[lo] = b; ord[hi] = a; }
+  auto sort = [&](int ncmp) {
+    auto less = [&](int a, int b) -> bool {                  // chunks [0, ncmp) then index: a before b
+      if (b == 0x7fffffff) return a != 0x7fffffff;
+      if (a == 0x7fffffff) return false;
+      for (int c = 0; c < ncmp; ++c) {
+        const unsigned long long ka = key[(int64_t)c * P.k + a], kb = key[(int64_t)c * P.k + b];
+        if (ka != kb) return ka < kb;
       }
-      __syncthreads();
+      return a < b;
+    };
+    for (int size = 2; size <= n; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int i = tid; i < (n >> 1); i += blockDim.x) {
+          const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+          const int a = ord[lo], b = ord[hi];
+          const bool up = (lo & size) == 0;
+          if (up ? less(b, a) : less(a, b)) { ord[lo] = b; ord[hi] = a; }
+        }
+        __syncthreads();
+      }
     }
+  };
+  sort(1);
+  if (nch > 1) {
+    int tie = 0;
+    for (int i = tid; i + 1 < nR; i += blockDim.x) tie |= key[ord[i]] == key[ord[i + 1]];
+    if (tie) any_tie = 1;
+    __syncthreads();
+    if (any_tie && nchs == nch) {
+      build(1, nch);
+      __syncthreads();
+      sort(nch);
+    } else if (any_tie) {
+      // a thread per run of equal chunk 0 (the run's first slot); the runs are disjoint, and a key compare
+      // against a slot another thread is permuting reads the same key whichever entry it finds there
+      auto row_less = [&](int a, int b) -> bool {            // full rows, then index
+        const int32_t* ra = wt + (int64_t)a * P.d;
+        const int32_t* rb = wt + (int64_t)b * P.d;
+        for (int l = 0; l < P.d; ++l)
+          if (ra[l] != rb[l]) return ra[l] < rb[l];
+        return a < b;
+      };
+      for (int i = tid; i + 1 < nR; i += blockDim.x) {
+        const unsigned long long ki = key[ord[i]];
+        if ((i > 0 && key[ord[i - 1]] == ki) || key[ord[i + 1]] != ki) continue;
+        int j = i + 1;
+        while (j < nR && key[ord[j]] == ki) ++j;
+        for (int x = i + 1; x < j; ++x) {
+          const int v = ord[x];
+          int y = x - 1;
+          while (y >= i && row_less(v, ord[y])) { ord[y + 1] = ord[y]; --y; }
+          ord[y + 1] = v;
+        }
+      }
+    }
+    __syncthreads();
   }
   for (int i = tid; i < nR; i += blockDim.x) perm[(int64_t)s * P.k + i] = ord[i];
 }
@@ -207,17 +254,20 @@ cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freq
   const int per = 64 / bits, nch = (P.d + per - 1) / per;
   int n2 = 1;
   while (n2 < P.k) n2 <<= 1;
-  const size_t psmem = sizeof(unsigned long long) * (size_t)nch * P.k + sizeof(int) * (size_t)n2;
+  // every chunk in shared memory when it fits (the tie rerun needs them), else chunk 0 only
+  const size_t full = sizeof(unsigned long long) * (size_t)nch * P.k + sizeof(int) * (size_t)n2;
+  const size_t one = sizeof(unsigned long long) * (size_t)P.k + sizeof(int) * (size_t)n2;
   int optin = 0, dev = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const int nchs = full <= (size_t)optin ? nch : 1;
+  const size_t psmem = nchs == nch ? full : one;
   if (psmem <= (size_t)optin) {
     e = ensure_smem(wrap_rank_packed_kernel, psmem);
     if (e != cudaSuccess) return e;
-    // threads: the sort's n2 / 2 compare-exchanges, or ~8 packed chunks each for the build if more
-    const int want = std::max(n2 / 2, (int)(((int64_t)nch * P.k + 7) / 8));
-    const int threads = std::min(1024, std::max(64, (want + 31) / 32 * 32));
-    wrap_rank_packed_kernel<<<n_signals, threads, psmem, st>>>(P, perm, bits, per, nch);
+    // threads: the sort's n2 / 2 compare-exchanges
+    const int threads = std::min(1024, std::max(64, (n2 / 2 + 31) / 32 * 32));
+    wrap_rank_packed_kernel<<<n_signals, threads, psmem, st>>>(P, perm, bits, per, nch, nchs);
   } else {
     const size_t smem = sizeof(unsigned long long) * (size_t)P.k;
     e = ensure_smem(wrap_rank_kernel, smem);

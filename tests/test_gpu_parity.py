@@ -584,6 +584,32 @@ def test_e2e_line_shard_fused_exchange_world1(S):
     assert torch.equal(res2.freqs, res.freqs)
 
 
+@pytest.mark.parametrize("d,N,k,blocks,per,T", [(12, 64, 16, (1,) * 12, 10, 8),
+                                                 (1000, 4096, 160, (2,) * 500, 5, 2)])
+def test_e2e_wrap_order_ties_in_packed_prefix(S, d, N, k, blocks, per, T):
+    """a8 canonical order when rows share the first 64-bit chunk of their packed rows (`per` coordinates), ordered
+    by the full rows -- d = 12, N = 64: collinear groups varying one axis (tied when that axis is >= per), the rank
+    kernel's rerun over every chunk in shared memory; d = 1000, k = 160: uniform rows whose groups of 8 share
+    their first 8 coordinates, 200 chunks x 160 rows do not fit in shared memory, the per-run insertion pass over
+    the rows in global memory.  The output equals the lexicographic sort of the truth."""
+    c = W.custom_config(d, N, k, blocks, structure="collinear", groups=4)
+    if d == 12:
+        w, a = W.make_batch(c, range(T))
+    else:
+        rng = np.random.Generator(np.random.PCG64(1606))
+        w = rng.integers(-N // 2, N // 2, size=(T, k, d)).astype(np.int32)
+        for g in range(0, k, 8):
+            w[:, g:g + 8, :8] = w[:, g:g + 1, :8]
+        a = np.exp(2j * np.pi * rng.random((T, k)))
+    tied = sum(len({tuple(r[:per]) for r in wt}) < len(wt) for wt in w)
+    assert tied >= 1                                        # the fixture exercises the tie pass
+    plan = _plan(S, c, batch=T)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    for t in range(T):
+        assert int(res.per_status[t]) == S.SFFT_OK
+        assert np.array_equal(res.freqs[t].cpu().numpy(), W.canonical_sort(w[t], a[t])[0])
+
+
 def test_e2e_line_shards_stall_fallback(S):
     """Line shards through the tilt fallback (levels switch inside the commit, retilt per shard)."""
     c = W.custom_config(4, 16, 8, (1, 1, 1, 1), structure="rectangles")
