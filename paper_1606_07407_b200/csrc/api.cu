@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <dlfcn.h>
+#include <immintrin.h>
 #include <functional>
 #include <memory>
 #include <new>
@@ -627,16 +628,24 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
       launches += 2;   // tables_assign, terms
     }
   }
-  // poll the host-mapped control block (published by setup's last CTA); a fault surfaces through the stream
+  // poll the host-mapped control block (one 16-byte store of setup's last CTA, read as one aligned 16-byte load:
+  // accepted when its check word carries this sequence number); a fault surfaces through the stream
+  int32_t cv[4];
   {
-    volatile int32_t* hc = P->h_ctrl;
+    auto snap = [&]() {
+      std::atomic_signal_fence(std::memory_order_seq_cst);
+      const __m128i x = _mm_load_si128(reinterpret_cast<const __m128i*>(P->h_ctrl));
+      _mm_storeu_si128(reinterpret_cast<__m128i*>(cv), x);
+      std::atomic_signal_fence(std::memory_order_seq_cst);
+      return (uint32_t)cv[3] == ((uint32_t)seq ^ ctrl_mix((uint32_t)cv[0], (uint32_t)cv[1], (uint32_t)cv[2]));
+    };
     long spins = 0;
     std::chrono::steady_clock::time_point t0;
-    while (hc[3] != seq) {
+    while (!snap()) {
       if ((++spins & 1023) == 0) {
         const cudaError_t q = cudaStreamQuery(st);
         if (q != cudaSuccess && q != cudaErrorNotReady) return fail(P, SFFT_ECUDA, "setup: %s", cudaGetErrorString(q));
-        if (q == cudaSuccess && hc[3] != seq) return fail(P, SFFT_ECUDA, "setup: control block not published");
+        if (q == cudaSuccess && !snap()) return fail(P, SFFT_ECUDA, "setup: control block not published");
         if (spins == 1024) t0 = std::chrono::steady_clock::now();
         else if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(120))
           return fail(P, SFFT_ECUDA, "setup: no control block after 120 s");
@@ -644,13 +653,13 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
     }
     std::atomic_thread_fence(std::memory_order_acquire);
   }
-  it->n_active = P->h_ctrl[0];
-  it->max_p = P->h_ctrl[1];
+  it->n_active = cv[0];
+  it->max_p = cv[1];
   if (it->n_active == 0) return SFFT_OK;
   it->fi = fft_index_host(P, it->max_p);
   if (it->fi < 0) return fail(P, SFFT_ENOTSUP, "p=%d beyond FFT table", it->max_p);
   it->max_M = P->fft[it->fi].M;
-  const int max_K = P->h_ctrl[2];
+  const int max_K = cv[2];
   // term split when the (signal x h-tile x n-tile) grid cannot fill the GPU (late iterations); computed
   // from shard 0's line count so that every line shard sums line 0 in the same order
   const ExpsumShape shp = expsum_for_p(P->shape, it->max_p);

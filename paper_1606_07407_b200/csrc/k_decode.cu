@@ -48,20 +48,18 @@ __global__ void setup_kernel(DevParams P, int32_t iter, int32_t seq) {
       atomicMax(&P.ctrl[2], P.k + (P.literal ? nR : 0));  // terms the exp-sum sums
     }
   }
-  // the last CTA publishes (n_active, max p, max K, seq) to the host-mapped control block: the host polls it
-  // instead of a device-to-host copy and an event
+  // the last CTA publishes (n_active, max p, max K, check word) to the host-mapped control block in one 16-byte
+  // store: the host polls it instead of a device-to-host copy and an event (ctrl_mix: no system-scope fence)
   if (P.h_ctrl_map == nullptr) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     if (atomicAdd(&P.ctrl[4], 1) == (int)gridDim.x - 1) {
       volatile int32_t* c = P.ctrl;
-      volatile int32_t* h = P.h_ctrl_map;
-      h[0] = c[0];
-      h[1] = c[1];
-      h[2] = c[2];
-      __threadfence_system();
-      h[3] = seq;
+      const int32_t v0 = c[0], v1 = c[1], v2 = c[2];
+      const int32_t chk = (int32_t)((uint32_t)seq ^ ctrl_mix((uint32_t)v0, (uint32_t)v1, (uint32_t)v2));
+      asm volatile("st.volatile.global.v4.s32 [%0], {%1, %2, %3, %4};" ::"l"(P.h_ctrl_map), "r"(v0), "r"(v1), "r"(v2),
+                   "r"(chk) : "memory");
     }
   }
 }

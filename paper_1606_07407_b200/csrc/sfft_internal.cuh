@@ -87,7 +87,7 @@ struct DevParams {
   int32_t* st_log;             // [kLogIters][2] (p, accepted) of signal 0
   int32_t* ctrl;               // [8]: n_active, max_p, max_K, fills, setup CTAs done (this iteration's block)
   int32_t* ctrl_next;          // [8]: the next iteration's block, cleared by the table prep
-  int32_t* h_ctrl_map;         // host-mapped [4]: n_active, max_p, max_K, sequence (setup_kernel publishes)
+  int32_t* h_ctrl_map;         // host-mapped [4]: n_active, max_p, max_K, sequence ^ ctrl_mix (setup_kernel)
   int32_t* active;             // [batch] indices of the signals still running this iteration
   // per-prime tables (W_tab, chirp, V, int8 root tables) live in a cache of slots keyed by p: they depend on p
   // only, like FFT twiddles; slot n_tslots is reserved for the stage entry points
@@ -210,6 +210,18 @@ struct I8Config {
   int small_l;   // 1: auto mode prefers the FP64 kernels (2L <= 16)
   int pair;      // 1: CTA-pair kernel (every tile width >= 32)
 };
+
+// check word of the host-mapped control block: one 16-byte store publishes (n_active, max_p, max_K,
+// seq ^ ctrl_mix(n_active, max_p, max_K)) without a system-scope fence; the host accepts a 16-byte snapshot only when
+// its check word matches the sequence number it waits for (a stale block carries an older sequence; a torn one
+// fails the check)
+__host__ __device__ inline uint32_t ctrl_mix(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t h = 0x27D4EB2Fu ^ (a * 0x9E3779B1u);
+  h = (h ^ (h >> 15)) * 0x85EBCA77u + b;
+  h = (h ^ (h >> 13)) * 0xC2B2AE3Du + c;
+  h = (h ^ (h >> 16)) * 0x9E3779B1u;
+  return h ^ (h >> 15);
+}
 
 // ---- device helpers ----------------------------------------------------------------------
 __host__ __device__ inline int64_t mod_pos64(int64_t x, int64_t m) {
