@@ -49,7 +49,7 @@ class _Params(ctypes.Structure):
         ("max_iter", ctypes.c_int32), ("stall_limit", ctypes.c_int32),
         ("extra_checks", ctypes.c_int32),
         ("n_primes", ctypes.c_int32), ("primes", ctypes.POINTER(ctypes.c_int64)),
-        ("n_fallback", ctypes.c_int32),
+        ("n_fallback", ctypes.c_int32), ("n_spec", ctypes.c_int32),
     ]
 
 
@@ -114,6 +114,7 @@ class Params:
     extra_checks: int = 3
     primes: Optional[Sequence[int]] = None
     n_fallback: int = 0
+    n_spec: int = 0
     _keep: list = field(default_factory=list, repr=False)
 
     def c_struct(self) -> _Params:
@@ -135,6 +136,7 @@ class Params:
         s.n_primes = 0 if primes is None else primes.size
         s.primes = None if primes is None else primes.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))
         s.n_fallback = self.n_fallback
+        s.n_spec = self.n_spec
         return s
 
     @property

@@ -599,21 +599,22 @@ static int solve_impl(const oracle_params* P, const int32_t* w, const double* a,
   /* terms of the residual f - g: k signal modes then the registry with negated coefficients */
   int64_t* tv = (int64_t*)malloc(sizeof(int64_t) * (size_t)2 * k * r);
   double* tc = (double*)malloc(sizeof(double) * 2 * (size_t)2 * k);
-  int32_t* acc_b = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);
-  int64_t* acc_v = (int64_t*)malloc(sizeof(int64_t) * (size_t)k * r);
-  double* acc_a = (double*)malloc(sizeof(double) * 2 * (size_t)k);
   double* F = NULL;
   int64_t Fcap = 0;
 
   int64_t samples = 0;
   int32_t i = 1, it = 1, stall = 0, status = ORACLE_PARTIAL;   /* i: Alg. 2/3 counter of the level, it: total */
+  const int32_t G = P->n_spec > 1 ? P->n_spec : 1;            /* reading R26: primes per iteration */
+  int32_t* touch = (int32_t*)malloc(sizeof(int32_t) * (size_t)k);   /* set that last updated entry e this iteration */
+  int32_t* set_b = (int32_t*)malloc(sizeof(int32_t) * (size_t)G * k);
+  int64_t* set_v = (int64_t*)malloc(sizeof(int64_t) * (size_t)G * k * r);
+  double* set_a = (double*)malloc(sizeof(double) * 2 * (size_t)G * k);
+  int32_t* set_n = (int32_t*)malloc(sizeof(int32_t) * (size_t)G);
   while (R.n < k && it <= P->max_iter) {                        /* Alg. 2 l.6 */
     int32_t kstar = k - R.n;                                  /* l.7 */
-    int64_t p = (P->n_primes > 0 && P->primes)
-                    ? P->primes[(i - 1) % P->n_primes]
-                    : oracle_ith_prime_at_least((int64_t)P->c * kstar, i);   /* l.8 (C11) */
-    int32_t m = i % r;                                         /* l.9, 0-based (C10) */
-    /* l.10: g from the registry; residual terms */
+    int64_t p0 = 0;
+    int32_t m0 = 0;
+    /* l.10: g from the registry; residual terms (one snapshot of R for every prime of the iteration) */
     memcpy(tv, vf, sizeof(int64_t) * (size_t)k * r);
     for (int32_t j = 0; j < k; ++j) { tc[2 * j] = a[2 * j]; tc[2 * j + 1] = a[2 * j + 1]; }
     for (int32_t e = 0; e < R.n; ++e) {
@@ -622,45 +623,63 @@ static int solve_impl(const oracle_params* P, const int32_t* w, const double* a,
       tc[2 * (k + e) + 1] = -R.a[2 * e + 1];
     }
     int32_t K = k + R.n;
-    if ((r + 1) * p > Fcap) {
-      Fcap = (int64_t)(r + 1) * p;
-      free(F);
-      F = (double*)malloc(sizeof(double) * 2 * (size_t)Fcap);
+    int32_t ncand = 0, nnonempty = 0, n_accum = 0, na = 0;
+    for (int32_t g = 0; g < G; ++g) {
+      const int32_t ig = (i - 1) * G + g + 1;                  /* prime counter of this prime (G = 1: i) */
+      int64_t p = (P->n_primes > 0 && P->primes)
+                      ? P->primes[(ig - 1) % P->n_primes]
+                      : oracle_ith_prime_at_least((int64_t)P->c * kstar, ig);   /* l.8 (C11) */
+      int32_t m = ig % r;                                      /* l.9, 0-based (C10) */
+      if (g == 0) { p0 = p; m0 = m; }
+      if ((r + 1) * p > Fcap) {
+        Fcap = (int64_t)(r + 1) * p;
+        free(F);
+        F = (double*)malloc(sizeof(double) * 2 * (size_t)Fcap);
+      }
+      double* s = (double*)malloc(sizeof(double) * 2 * (size_t)p);
+      /* l.11-17: sample the unshifted line and the r shifted lines, DFT each */
+      for (int32_t line = 0; line <= r; ++line) {
+        const int64_t t0 = now_ns();
+        oracle_sample_line(K, r, tv, tc, p, m, line - 1, E, s);
+        t_sampling += now_ns() - t0;
+        oracle_dft(p, s, F + (size_t)line * 2 * p);
+      }
+      free(s);
+      samples += (int64_t)(r + 1) * p;                        /* f evaluations only (C22) */
+      /* l.18-32 */
+      int32_t nc1 = 0, nn1 = 0;
+      set_n[g] = oracle_decode_ex(P, E, lo, hi, p, m, kstar, F, &nc1, &nn1, set_b + (size_t)g * k,
+                                  set_v + (size_t)g * k * r, set_a + (size_t)g * 2 * k);
+      ncand += nc1;
+      nnonempty += nn1;
+      na += set_n[g];
     }
-    double* s = (double*)malloc(sizeof(double) * 2 * (size_t)p);
-    /* l.11-17: sample the unshifted line and the r shifted lines, DFT each */
-    for (int32_t line = 0; line <= r; ++line) {
-      const int64_t t0 = now_ns();
-      oracle_sample_line(K, r, tv, tc, p, m, line - 1, E, s);
-      t_sampling += now_ns() - t0;
-      oracle_dft(p, s, F + (size_t)line * 2 * p);
-    }
-    free(s);
-    samples += (int64_t)(r + 1) * p;                          /* f evaluations only (C22) */
-    /* l.18-32 */
-    int32_t ncand = 0, nnonempty = 0, n_accum = 0;
-    int32_t na = oracle_decode_ex(P, E, lo, hi, p, m, kstar, F, &ncand, &nnonempty, acc_b, acc_v, acc_a);
-    /* l.30: R <- R u (w~, a), accumulating (C16), in ascending b */
-    for (int32_t t = 0; t < na; ++t) {
-      int32_t e = registry_find(&R, acc_v + (size_t)t * r);
-      if (e >= 0) {
-        R.a[2 * e] += acc_a[2 * t];
-        R.a[2 * e + 1] += acc_a[2 * t + 1];
-        ++n_accum;
-      } else {
-        if (R.n >= R.cap) {   /* cannot happen with the k* cap; kept for safety */
-          R.cap *= 2;
-          R.v = (int64_t*)realloc(R.v, sizeof(int64_t) * (size_t)R.cap * r);
-          R.a = (double*)realloc(R.a, sizeof(double) * 2 * (size_t)R.cap);
-          tv = (int64_t*)realloc(tv, sizeof(int64_t) * (size_t)(k + R.cap) * r);
-          tc = (double*)realloc(tc, sizeof(double) * 2 * (size_t)(k + R.cap));
+    /* l.30: R <- R u (w~, a), accumulating (C16), in ascending b; the sets in prime order, a key that an earlier
+     * set of this iteration already updated is skipped (R26: that prime saw the same residual) */
+    for (int32_t e = 0; e < k; ++e) touch[e] = -1;
+    for (int32_t g = 0; g < G; ++g) {
+      const int64_t* acc_v = set_v + (size_t)g * k * r;
+      const double* acc_a = set_a + (size_t)g * 2 * k;
+      for (int32_t t = 0; t < set_n[g]; ++t) {
+        int32_t e = registry_find(&R, acc_v + (size_t)t * r);
+        if (e >= 0) {
+          if (touch[e] >= 0 && touch[e] < g) continue;
+          R.a[2 * e] += acc_a[2 * t];
+          R.a[2 * e + 1] += acc_a[2 * t + 1];
+          touch[e] = g;
+          ++n_accum;
+        } else {
+          if (R.n >= k) continue;         /* capacity k (only false accepts of several primes can reach it) */
+          memcpy(R.v + (size_t)R.n * r, acc_v + (size_t)t * r, sizeof(int64_t) * (size_t)r);
+          R.a[2 * R.n] = acc_a[2 * t];
+          R.a[2 * R.n + 1] = acc_a[2 * t + 1];
+          touch[R.n] = g;
+          ++R.n;
         }
-        memcpy(R.v + (size_t)R.n * r, acc_v + (size_t)t * r, sizeof(int64_t) * (size_t)r);
-        R.a[2 * R.n] = acc_a[2 * t];
-        R.a[2 * R.n + 1] = acc_a[2 * t + 1];
-        ++R.n;
       }
     }
+    const int64_t p = p0;
+    const int32_t m = m0;
     /* l.33: prune small coefficients (C17), order-preserving */
     int32_t keep = 0;
     for (int32_t e = 0; e < R.n; ++e) {
@@ -756,7 +775,7 @@ static int solve_impl(const oracle_params* P, const int32_t* w, const double* a,
   if (out_iters) *out_iters = it - 1;
 
   free(u); free(idx_of); free(refs); free(wt);
-  free(F); free(acc_a); free(acc_v); free(acc_b); free(tc); free(tv);
+  free(F); free(set_a); free(set_v); free(set_b); free(set_n); free(touch); free(tc); free(tv);
   free(R.a); free(R.v); free(vf); free(hi); free(lo); free(tbuf);
   if (ns) { ns[0] = now_ns() - t_start; ns[1] = t_sampling; }
   return status;

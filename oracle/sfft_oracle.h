@@ -44,6 +44,10 @@ typedef struct {
   int32_t n_fallback;        /* stall fallback (readings R23 / R24): up to ORACLE_MAX_FALLBACK levels;
                                 1-4 tilt fixed axis pairs with the Pythagorean triples (3,4,5), (5,12,13),
                                 (8,15,17), (7,24,25); 5.. tilt the pairs of a seeded random order of the axes */
+  int32_t n_spec;            /* multi-prime speculation (reading R26): 0 / 1 = Alg. 2 as
+                                written; G > 1: iteration i runs the G primes of counters (i-1) G + 1 .. i G against
+                                the same residual and merges their accepted bins in prime order, a key already
+                                updated by an earlier prime of the iteration being skipped */
 } oracle_params;
 
 #define ORACLE_MAX_FALLBACK 67

@@ -587,3 +587,59 @@ def test_far_apart_rectangles_need_the_round_robin(d, N, k, seeds, brute):
         if brute:
             wb, ab = _brute_force_modes(w, a, N)
             assert np.array_equal(rr.w, wb) and np.all(np.abs(rr.a - ab) <= 1e-10 * np.abs(ab))
+
+
+# ------------------------------------------------------------------ multi-prime speculation (NEXT #3, reading R26)
+@pytest.mark.parametrize("name,trials", [("c1", range(40)), ("c2", range(3))])
+def test_speculation_exact_and_fewer_iterations(name, trials):
+    """Reading R26: G primes per iteration against one snapshot of the registry, merged in prime order.  Noiseless
+    inputs are still recovered exactly -- a key two primes of one iteration both isolate is counted once
+    (double counting would leave 2 a_j); G = 1 is Alg. 2 itself (identical trace); the iterations never exceed
+    G = 1's."""
+    c = W.CONFIGS[name]
+    for t in trials:
+        w, a = W.make_signal(c, t)
+        ws, as_ = W.canonical_sort(w, a)
+        base = O.solve(O.params_for(c), w, a)
+        one = O.solve(O.params_for(c, n_spec=1), w, a)
+        assert np.array_equal(base.trace, one.trace) and base.samples == one.samples
+        for G in (2, 3, 4):
+            res = O.solve(O.params_for(c, n_spec=G), w, a)
+            assert res.status == O.OK, (name, t, G)
+            assert np.array_equal(res.w, ws)
+            assert np.abs(res.a - as_).max() <= 1e-12 * np.abs(as_).max(), (name, t, G)
+            assert res.iterations <= base.iterations, (name, t, G)
+
+
+def test_speculation_two_primes_isolating_one_mode_count_it_once():
+    """k = 1: both primes of iteration 1 isolate the single mode; the merge keeps one entry with a_0 (not 2 a_0),
+    one iteration, f evaluated on both primes' lines."""
+    c = W.custom_config(3, 64, 1, (1, 1, 1), cfg=82)
+    for t in range(10):
+        w, a = W.make_signal(c, t)
+        res = O.solve(O.params_for(c, n_spec=2), w, a)
+        assert res.status == O.OK and res.iterations == 1
+        assert np.array_equal(res.w, w) and abs(res.a[0] - a[0]) <= 1e-12 * abs(a[0])
+        assert res.trace[0, 4] == 2 and res.trace[0, 6] == 0       # two accepted bins, no accumulation
+        assert res.samples == 4 * (5 + 7)                           # primes 5 and 7 (counters 1, 2 from c k* = 5)
+
+
+SPEC_FFA_CASE, SPEC_FFA_SEEDS = (3, 32, 30, (1, 1, 1)), (2, 13, 15, 27, 36)
+
+
+def test_speculation_forced_false_accepts_exact():
+    """R26 with forced false accepts (keys re-found and accumulated, entries pruned): on these seeds the G = 2
+    schedule ends with the brute-force dense DFT's spectrum (on others the false entries fill R to k first, as
+    they can under Alg. 2 itself); its trace shows accumulations and prunes.  (A key re-found inside one prime's
+    own set -- R25, kept accumulating -- did not occur on 240 seeds of the three FFA cases, so the same-set
+    distinction of the merge is not observable here.)"""
+    d, N, k, blocks = SPEC_FFA_CASE
+    c = ffa_config(d, N, k, blocks)
+    for t in SPEC_FFA_SEEDS:
+        w, a = W.make_signal(c, t)
+        wb, ab = _brute_force_modes(w, a, N)
+        res = O.solve(O.params_for(c, **dict(FFA_PARAMS, n_spec=2)), w, a)
+        assert res.status == O.OK, t
+        assert res.w.shape == wb.shape and np.array_equal(res.w, wb), t
+        assert np.all(np.abs(res.a - ab) <= 1e-10 * np.abs(ab)), t
+        assert res.trace[:, 6].sum() > 0 and res.trace[:, 7].sum() > 0, t
