@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--config", default="c3", choices=sorted(W.CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="signals per GPU per step (default: config trials)")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--spec-primes", type=int, nargs="*", default=[2, 4, 8],
+                    help="single-solve latency also with G-prime speculation (reading R26) for each G")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--shard", default="signals", choices=["signals", "lines"],
@@ -548,6 +550,28 @@ def main():
             ts.append(e0.elapsed_time(e1))
         lat = {"ms_median": sorted(ts)[len(ts) // 2], "ms_min": min(ts), "iterations": r1.report.iterations,
                "signal": f"{cfg.name} trial {trials[0]}", "exact": bool(np.array_equal(outs1[0][0].cpu().numpy(), ws[0]))}
+        del plan1, sig1
+        # multi-prime speculation (DESIGN reading R26, sfft_options.spec_primes = G): G primes per iteration in G
+        # slots of one plan, merged in prime order -- fewer iterations for the same signal
+        lat["speculation"] = {}
+        for G in args.spec_primes:
+            planG = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=1, expsum_path=args.expsum_path,
+                                spec_primes=G)
+            sigG = S.sfft_signal_expsum(planG, w_d[:1].contiguous(), a_d[:1].contiguous())
+            for _ in range(2):
+                S.sfft_execute(planG, sigG, outs1)
+            tg = []
+            for _ in range(args.latency_steps):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                rg = S.sfft_execute(planG, sigG, outs1)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tg.append(e0.elapsed_time(e1))
+            lat["speculation"][f"G{G}"] = {"ms_median": sorted(tg)[len(tg) // 2], "iterations": rg.report.iterations,
+                                           "samples": rg.report.samples_used,
+                                           "exact": bool(np.array_equal(outs1[0][0].cpu().numpy(), ws[0]))}
+            del planG, sigG
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

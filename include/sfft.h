@@ -95,6 +95,13 @@ typedef struct {
                                  sfft_execute_group) and per-(shard, line, signal) stamps released at system scope
                                  tell the commit that a shard's lines are in -- no separate collective.  At most 8
                                  shards [0] */
+  int32_t spec_primes;        /* multi-prime speculation (reading R26): G primes per
+                                 iteration, the prime counters (i-1) G + 1 .. i G of Alg. 2 l.8, all sampled
+                                 against the same registry and merged in prime order, a key that an earlier prime of
+                                 the iteration updated being skipped.  Fewer, wider iterations (single-signal
+                                 latency); noiseless signals are recovered exactly, the trace differs from Alg. 2.
+                                 Each signal occupies G plan slots (workspace ~G x).  0 / 1 = Alg. 2 as written;
+                                 at most 16; not with line shards, fused commit or literal_residual [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */

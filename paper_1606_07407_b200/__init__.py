@@ -46,7 +46,7 @@ class sfft_options(ctypes.Structure):
                 ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32),
                 ("fallback_tilts", ctypes.c_int32), ("line_shards", ctypes.c_int32),
                 ("line_rank", ctypes.c_int32), ("table_cache_slots", ctypes.c_int32),
-                ("line_exchange", ctypes.c_int32)]
+                ("line_exchange", ctypes.c_int32), ("spec_primes", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -175,7 +175,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
               stream=None, profile: bool = False, literal_residual: bool = False,
               expsum_path: int = 0, fallback_tilts: int = 0, line_shards: int = 0, line_rank: int = 0,
-              table_cache_slots: int = 0, line_exchange: int = 0) -> Plan:
+              table_cache_slots: int = 0, line_exchange: int = 0, spec_primes: int = 0) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -196,6 +196,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.line_shards, opt.line_rank = int(line_shards), int(line_rank)
     opt.table_cache_slots = int(table_cache_slots)
     opt.line_exchange = int(line_exchange)
+    opt.spec_primes = int(spec_primes)
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)

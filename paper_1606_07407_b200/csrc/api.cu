@@ -125,6 +125,7 @@ struct sfft_plan_s {
   bool peer_ready = false;
   int32_t peer_epoch = 0;
   cudaEvent_t ev_ctrl = nullptr;   // the per-iteration control read (iter_setup)
+  int32_t spec_G = 1;              // multi-prime speculation (R26): slots per signal; batch counts slots
   // sfft_solve_host_batches: the second device input / output set, the H2D and D2H streams and their events
   void* pipe_buf = nullptr;
   size_t pipe_bytes = 0;
@@ -142,7 +143,7 @@ enum Buf {
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
   B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY, B_SPINERR,
-  B_FFTW, B_DLROOT, B_CROWI, B_CROWL,
+  B_FFTW, B_DLROOT, B_CROWI, B_CROWL, B_SPECT,
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
@@ -292,6 +293,7 @@ void layout(sfft_plan_t* P) {
   sz[B_DLROOT] = P->fs_ok ? 16 * T * (2 * P->p_stride + 8) : 0;
   sz[B_CROWI] = 16 * S * (size_t)((P->k + 31) / 32) * ((P->Lp + 15) / 16);
   sz[B_CROWL] = 4 * S * (size_t)P->k;
+  sz[B_SPECT] = P->spec_G > 1 ? 4 * S * (size_t)P->k : 0;
   sz[B_STSLOT] = 4 * S;
   sz[B_SLOTP] = 4 * T;
   sz[B_SLOTE] = 4 * T;
@@ -404,6 +406,8 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.slot_ready = ptr<int32_t>(P, B_SLOTRDY);
   D.assign_ready = ptr<int32_t>(P, B_ASGRDY);
   D.spin_err = ptr<int32_t>(P, B_SPINERR);
+  D.spec_G = 1;                              // sfft_execute sets the plan's G (stage entry points run single slots)
+  D.spec_touch = P->spec_G > 1 ? ptr<int32_t>(P, B_SPECT) : nullptr;
   D.commit_cnt = ptr<int32_t>(P, B_SPINERR) + 1;
   if (P->i8_ok) {
     D.i8_S = P->i8.S; D.i8_NT = P->i8.NT; D.i8_NT_last = P->i8.NT_last; D.i8_ntiles = P->i8.ntiles; D.i8_nks = P->i8.nks;
@@ -599,10 +603,13 @@ int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& lau
   cudaStream_t st = P->stream;
   CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_CTRL), 0, 64, st));   // both control blocks
   CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SPINERR), 0, 4 * (1 + (size_t)P->batch), st));
-  LAUNCH(P, launch_project(D, sig->batch, sig->freqs, sig->coeffs, st));
+  const int slots = sig->batch * D.spec_G;   // R26: G slots per signal, the projection maps slot -> signal
+  if (D.spec_G > 1)
+    CUDA_TRY(P, cudaMemsetAsync(D.spec_touch, 0, 4 * (size_t)slots * P->k, st));
+  LAUNCH(P, launch_project(D, slots, sig->freqs, sig->coeffs, st));
   launches += 1;   // init_state_kernel
   if (P->i8_ok) {
-    LAUNCH(P, launch_i8_prepare(D, sig->batch, P->k, st));
+    LAUNCH(P, launch_i8_prepare(D, slots, P->k, st));
     launches += 1;   // sigma + limbs
   }
   return SFFT_OK;
@@ -692,7 +699,7 @@ int iter_setup(sfft_plan_t* P, DevParams& D, int iter, IterPlan* it, int& launch
   // on the tail of the launch -- C3 +4 %, C4 +44 %, C5 -0.7 %): unsharded lines only (line shards commit after
   // the record all-gather), and the commit's shared memory must fit in the FFT's
   static const bool fc = getenv("SFFT_FUSE_COMMIT") && atoi(getenv("SFFT_FUSE_COMMIT")) != 0;
-  it->fuse_commit = fc && P->line_G == 0 && decode_smem_bytes(D, it->max_p) <= P->fft[it->fi].smem_upto;
+  it->fuse_commit = fc && P->line_G == 0 && P->spec_G == 1 && decode_smem_bytes(D, it->max_p) <= P->fft[it->fi].smem_upto;
   return SFFT_OK;
 }
 
@@ -758,8 +765,8 @@ int iter_back(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, const 
     }
   }
   if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
-    LAUNCH(P, launch_retilt(D, sig->batch, sig->freqs, st));
-    if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch, P->k, st, true));
+    LAUNCH(P, launch_retilt(D, sig->batch * D.spec_G, sig->freqs, st));
+    if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch * D.spec_G, P->k, st, true));
   }
   return SFFT_OK;
 }
@@ -772,15 +779,17 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   int32_t spin_err = 0;
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(P, cudaMemcpyAsync(&spin_err, D.spin_err, 4, cudaMemcpyDeviceToHost, st));
-  std::vector<int64_t> hsamp(batch), hcm(batch), hcm8(batch);
-  std::vector<double> hfw(2 * (size_t)batch);
-  std::vector<int32_t> hlog(2 * kLogIters), hlvl(batch);
+  const int G = std::max(1, (int)D.spec_G);
+  const size_t slots = (size_t)batch * G;       // per-slot counters (R26: G slots per signal, all summed)
+  std::vector<int64_t> hsamp(slots), hcm(slots), hcm8(slots);
+  std::vector<double> hfw(2 * slots);
+  std::vector<int32_t> hlog(2 * kLogIters), hlvl(slots);
   if (rep) {
-    CUDA_TRY(P, cudaMemcpyAsync(hlvl.data(), D.st_lvl, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(P, cudaMemcpyAsync(hfw.data(), D.st_fftw, 16 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hlvl.data(), D.st_lvl, 4 * slots, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hsamp.data(), D.st_samples, 8 * slots, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hcm.data(), D.st_cmacs, 8 * slots, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hcm8.data(), D.st_cmacs_i8, 8 * slots, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(P, cudaMemcpyAsync(hfw.data(), D.st_fftw, 16 * slots, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(P, cudaMemcpyAsync(hlog.data(), D.st_log, 4 * 2 * kLogIters, cudaMemcpyDeviceToHost, st));
   }
   CUDA_TRY(P, cudaStreamSynchronize(st));
@@ -795,13 +804,13 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   *worst_out = worst;
   if (rep) {
     memset(rep, 0, sizeof *rep);
-    for (int s = 0; s < batch; ++s) {
+    for (size_t s = 0; s < slots; ++s) {
       rep->samples_used += hsamp[s];
       rep->cmacs += hcm[s];
       rep->cmacs_i8 += hcm8[s];
       rep->fft_plogp += hfw[2 * s];
       rep->fft_mlogm += hfw[2 * s + 1];
-      rep->fallback_used += hlvl[s] > 0;
+      rep->fallback_used += (s % G == 0) && hlvl[s] > 0;
     }
     rep->i8_limbs = P->i8_ok ? P->i8.S : 0;
     rep->n_expsum_i8 = n_expsum_i8;
@@ -912,6 +921,15 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     if (opt->line_exchange < 0 || opt->line_exchange > 1) return SFFT_EINVAL;
     if (opt->line_exchange == 1 && (opt->line_shards < 1 || opt->line_shards > kMaxPeers)) return SFFT_EINVAL;
     P->line_exchange = opt->line_exchange;
+    if (opt->spec_primes < 0 || opt->spec_primes > 16) return SFFT_EINVAL;
+    if (opt->spec_primes > 1) {
+      // R26: G slots per signal (each its own prime and registry copy); not with line shards (their records are
+      // per line, not per prime), the literal residual or an explicit batch of slots beyond 2^20
+      if (opt->line_shards > 0 || opt->literal_residual || (int64_t)P->batch * opt->spec_primes > (1 << 20))
+        return SFFT_EINVAL;
+      P->spec_G = opt->spec_primes;
+      P->batch *= P->spec_G;
+    }
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
   const double log2N = std::log2((double)N);
@@ -1204,7 +1222,8 @@ void sfft_plan_destroy(sfft_plan_t* plan) {
 int sfft_signal_expsum(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, const double* coeffs,
                        sfft_signal_t** out) {
   if (!plan || !out || !freqs || !coeffs) return SFFT_EINVAL;
-  if (batch < 1 || batch > plan->batch) return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch);
+  if (batch < 1 || batch > plan->batch / plan->spec_G)
+    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_G);
   sfft_signal_t* s = new (std::nothrow) sfft_signal_t();
   if (!s) return SFFT_ENOMEM;
   s->plan = plan;
@@ -1228,8 +1247,9 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   if (rc) return rc;
   sfft_plan_t* P = plan;
   cudaStream_t st = P->stream;
-  const int32_t batch = sig->batch;
-  DevParams D = dev_params(P, batch);
+  const int32_t batch = sig->batch;                 // signals; slots = batch G (R26)
+  DevParams D = dev_params(P, batch * P->spec_G);
+  D.spec_G = P->spec_G;
   int launches = 0;
   // profiling: event marks on the stream, 5 per iteration (prep | expsum | pfft | decode)
   size_t n_ev = 0;
@@ -1248,7 +1268,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   int iter = 1;
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
   std::vector<size_t> it_marks, it_i8;
-  int n_bound = batch;
+  int n_bound = batch * P->spec_G;
   for (; iter <= P->max_iter; ++iter) {
     IterPlan it;
     if ((rc = iter_setup(P, D, iter, &it, launches, n_bound))) return rc;
@@ -1433,7 +1453,8 @@ int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, cons
                     int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
                     sfft_report* rep) {
   if (!plan || !freqs || !coeffs || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
-  if (batch < 1 || batch > plan->batch) return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch);
+  if (batch < 1 || batch > plan->batch / plan->spec_G)
+    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_G);
   int rc = ensure_ready(plan);
   if (rc) return rc;
   sfft_plan_t* P = plan;
@@ -1457,7 +1478,8 @@ int sfft_solve_host_batches(sfft_plan_t* plan, int32_t n_batches, int32_t batch,
                             const double* coeffs, int32_t* out_freqs, double* out_coeffs, int32_t* out_count,
                             int32_t* out_status, sfft_report* rep) {
   if (!plan || n_batches < 1 || !freqs || !coeffs || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
-  if (batch < 1 || batch > plan->batch) return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch);
+  if (batch < 1 || batch > plan->batch / plan->spec_G)
+    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_G);
   int rc = ensure_ready(plan);
   if (rc) return rc;
   sfft_plan_t* P = plan;

@@ -209,87 +209,127 @@ __device__ __forceinline__ void peer_wait_lines(const DevParams& P, int s) {
   __syncthreads();
 }
 
+// multi-prime speculation (reading R26): tag of the set that updated a registry entry this iteration, and whether
+// set gs must skip entry e (an earlier set of the same iteration updated it); never for G = 1
+__device__ __forceinline__ int32_t spec_tag(int32_t iter, int gs) { return (iter << 4) | gs; }
+__device__ __forceinline__ bool spec_skip(const DevParams& P, int s, int e, int32_t iter, int gs) {
+  if (P.spec_G <= 1) return false;
+  const int32_t t = P.spec_touch[(int64_t)s * P.k + e];
+  return (t >> 4) == iter && (t & 15) < gs;
+}
+
 // a7 commit of one signal (steps 2-5 of decode_kernel<kDecCommit>, k_decode.cu): candidates of line 0 and the
 // pass flags / coordinates of every line from the records, bin consistency, accepted list, registry update
 // (hash lookup, R[v] += a, new entries and their C rows, prune) and the signal's state.  Runs in the commit
 // kernel (one CTA per signal) or, fused, in the last FFT CTA of the signal to finish (k_fft.cu).
 // smem: decode_smem_bytes(P, p); any blockDim that is a multiple of 32.
+template <bool SPEC>   // SPEC: spec_G > 1 (R26); false compiles the single-set commit of Alg. 2
 static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t iter, int s, unsigned char* smem_raw) {
-  const int p = P.st_p[s], m = P.st_m[s];
-  const int nR = P.st_nR[s];
+  // multi-prime speculation (reading R26, spec_G > 1): slots s0 .. s0 + G - 1 hold one signal, each with its own
+  // prime of the iteration and its own copy of the registry; every slot merges all G record sets in prime order
+  // into its copy (so the copies stay identical), skipping keys an earlier set of the iteration updated
+  const int G = SPEC ? P.spec_G : 1;
+  const int s0 = s - s % G;
+  const int p_own = P.st_p[s];
+  const int nR0 = P.st_nR[s];
+  int nR = nR0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int r = P.r;
   const int lvl = P.st_lvl[s];
   const int64_t Ev = P.lvl_E[lvl];
-  double* mag = reinterpret_cast<double*>(smem_raw);
-  int* cand = reinterpret_cast<int*>(mag + p);
-  int* flag = cand + p;
-  int* accl = flag + p;
+  double* mag = reinterpret_cast<double*>(smem_raw);             // arrays of >= k* entries: p >= c k* for every set
+  int* cand = reinterpret_cast<int*>(mag + p_own);
+  int* flag = cand + p_own;
+  int* accl = flag + p_own;
   int* found = accl + P.k;
   int* scratch = found + P.k;
   int64_t* accv = P.acc_v + (int64_t)s * r * P.k;               // [r][k], column = candidate index
   int nc = 0, total = 0;
   if (P.peer_mode) peer_wait_lines(P, s);        // the records of every shard's lines are in (fused exchange)
-  // ---- commit: candidates of line 0, flags ANDed over the line shards, coordinates unpacked ----
-  nc = P.rec_nc[s];
-  for (int ci = tid; ci < nc; ci += blockDim.x) {
-    cand[ci] = P.rec_cand[(int64_t)s * P.k + ci];
-    int f = 1;
-    for (int g = 0; g < P.line_G; ++g)
-      f &= reinterpret_cast<const int32_t*>(P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words)[ci];
-    flag[ci] = f;
-  }
-  __syncthreads();
-  if (P.line_G == 1) {
-    // one shard holds every axis: its record already is the [r][k] coordinate array
-    accv = const_cast<int64_t*>(P.rec_recv) + (int64_t)s * P.rec_words + P.rec_fw;   // read-only below
-  } else {
-    for (int g = 0; g < P.line_G; ++g) {
-      int glo, ghi;
-      line_shard_range(r, P.line_G, g, &glo, &ghi);
-      const int64_t* rv = P.rec_recv + ((int64_t)g * P.batch + s) * P.rec_words + P.rec_fw;
-      for (int nn = 0; nn < ghi - glo; ++nn)
-        for (int ci = tid; ci < nc; ci += blockDim.x)
-          if (flag[ci]) accv[(int64_t)(glo + nn) * P.k + ci] = rv[(int64_t)nn * P.k + ci];
+  int na_all = 0, nR_final = nR0;
+  for (int gs = 0; gs < G; ++gs) {
+    const int sr = s0 + gs;                               // the slot whose prime's records this set holds
+    const int p = P.st_p[sr], m = P.st_m[sr];
+    // ---- commit: candidates of line 0, flags ANDed over the line shards, coordinates unpacked ----
+    nc = P.rec_nc[sr];
+    for (int ci = tid; ci < nc; ci += blockDim.x) {
+      cand[ci] = P.rec_cand[(int64_t)sr * P.k + ci];
+      int f = 1;
+      for (int g = 0; g < P.line_G; ++g)
+        f &= reinterpret_cast<const int32_t*>(P.rec_recv + ((int64_t)g * P.batch + sr) * P.rec_words)[ci];
+      flag[ci] = f;
     }
     __syncthreads();
-  }
-  if (P.extra & 2) {
-    for (int ci = tid; ci < nc; ci += blockDim.x)
-      if (flag[ci] && mod_pos64(accv[(int64_t)m * P.k + ci], p) != cand[ci]) flag[ci] = 0;
-    __syncthreads();
-  }
+    if (P.line_G == 1) {
+      // one shard holds every axis: its record already is the [r][k] coordinate array
+      accv = const_cast<int64_t*>(P.rec_recv) + (int64_t)sr * P.rec_words + P.rec_fw;   // read-only below
+    } else {
+      for (int g = 0; g < P.line_G; ++g) {
+        int glo, ghi;
+        line_shard_range(r, P.line_G, g, &glo, &ghi);
+        const int64_t* rv = P.rec_recv + ((int64_t)g * P.batch + sr) * P.rec_words + P.rec_fw;
+        for (int nn = 0; nn < ghi - glo; ++nn)
+          for (int ci = tid; ci < nc; ci += blockDim.x)
+            if (flag[ci]) accv[(int64_t)(glo + nn) * P.k + ci] = rv[(int64_t)nn * P.k + ci];
+      }
+      __syncthreads();
+    }
+    if (P.extra & 2) {
+      for (int ci = tid; ci < nc; ci += blockDim.x)
+        if (flag[ci] && mod_pos64(accv[(int64_t)m * P.k + ci], p) != cand[ci]) flag[ci] = 0;
+      __syncthreads();
+    }
 
-  // ---- 3. accepted list in ascending b ----
-  {
-    const int per = (nc + blockDim.x - 1) / blockDim.x;
-    const int i0 = tid * per, i1 = min(nc, i0 + per);
-    int c3 = 0;
-    for (int i = i0; i < i1; ++i) c3 += flag[i];
-    int pos3 = block_excl_scan(c3, scratch, &total);
-    for (int i = i0; i < i1; ++i)
-      if (flag[i]) accl[pos3++] = i;
-    __syncthreads();
-  }
-  const int na = total;
+    // ---- 3. accepted list in ascending b ----
+    {
+      const int per = (nc + blockDim.x - 1) / blockDim.x;
+      const int i0 = tid * per, i1 = min(nc, i0 + per);
+      int c3 = 0;
+      for (int i = i0; i < i1; ++i) c3 += flag[i];
+      int pos3 = block_excl_scan(c3, scratch, &total);
+      for (int i = i0; i < i1; ++i)
+        if (flag[i]) accl[pos3++] = i;
+      __syncthreads();
+    }
+    const int na = total;
 
-  // ---- 4. registry update: R[v] += a ----
-  int64_t* vreg = P.v_all + (int64_t)s * r * P.kk + P.k;   // column e = registry entry e
-  double2* areg = P.a_reg + (int64_t)s * P.k;
-  uint64_t* khash = P.key_hash + (int64_t)s * P.k;
-  int* htab = P.htab + (int64_t)s * P.H;
-  const int Hm = P.H - 1;
-  // 4a. lookup, warp per accepted candidate: key hash with lanes along the coordinates, linear probing,
-  //     full-key compare by ballot (the arrays of the select are free in the commit: mag -> hashes, flag -> new)
-  //     Short keys (r < 128) go thread per candidate instead (the same hash by a plain loop).
-  uint64_t* hsh = reinterpret_cast<uint64_t*>(mag);
-  const int nwarps = (int)(blockDim.x >> 5);
-  const bool wide = r >= 128;
-  if (!wide) {
-    for (int t = tid; t < na; t += blockDim.x) {
+    // ---- 4. registry update: R[v] += a ----
+    int64_t* vreg = P.v_all + (int64_t)s * r * P.kk + P.k;   // column e = registry entry e
+    double2* areg = P.a_reg + (int64_t)s * P.k;
+    uint64_t* khash = P.key_hash + (int64_t)s * P.k;
+    int* htab = P.htab + (int64_t)s * P.H;
+    const int Hm = P.H - 1;
+    // 4a. lookup, warp per accepted candidate: key hash with lanes along the coordinates, linear probing,
+    //     full-key compare by ballot (the arrays of the select are free in the commit: mag -> hashes, flag -> new)
+    //     Short keys (r < 128) go thread per candidate instead (the same hash by a plain loop).
+    uint64_t* hsh = reinterpret_cast<uint64_t*>(mag);
+    const int nwarps = (int)(blockDim.x >> 5);
+    const bool wide = r >= 128;
+    if (!wide) {
+      for (int t = tid; t < na; t += blockDim.x) {
+        const int ci = accl[t];
+        uint64_t h = 0;
+        for (int n = 0; n < r; ++n) h ^= key_term(accv[(int64_t)n * P.k + ci], n);
+        int slot = (int)(h & (uint64_t)Hm);
+        int fe = -1;
+        for (;;) {
+          const int e1 = htab[slot];
+          if (e1 == 0) break;
+          const int e = e1 - 1;
+          if (khash[e] == h) {
+            bool eq = true;
+            for (int n = 0; n < r && eq; ++n) eq = vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+            if (eq) { fe = e; break; }
+          }
+          slot = (slot + 1) & Hm;
+        }
+        found[t] = fe;
+        hsh[t] = h;
+      }
+    }
+    for (int t = warp; wide && t < na; t += nwarps) {
       const int ci = accl[t];
-      uint64_t h = 0;
-      for (int n = 0; n < r; ++n) h ^= key_term(accv[(int64_t)n * P.k + ci], n);
+      const uint64_t h = key_hash_warp(accv + ci, P.k, r, lane);
       int slot = (int)(h & (uint64_t)Hm);
       int fe = -1;
       for (;;) {
@@ -298,276 +338,319 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
         const int e = e1 - 1;
         if (khash[e] == h) {
           bool eq = true;
-          for (int n = 0; n < r && eq; ++n) eq = vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
-          if (eq) { fe = e; break; }
+          for (int n = lane; n < r; n += 32) eq = eq && vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
+          if (__all_sync(0xffffffffu, eq)) { fe = e; break; }
         }
         slot = (slot + 1) & Hm;
       }
-      found[t] = fe;
-      hsh[t] = h;
-    }
-  }
-  for (int t = warp; wide && t < na; t += nwarps) {
-    const int ci = accl[t];
-    const uint64_t h = key_hash_warp(accv + ci, P.k, r, lane);
-    int slot = (int)(h & (uint64_t)Hm);
-    int fe = -1;
-    for (;;) {
-      const int e1 = htab[slot];
-      if (e1 == 0) break;
-      const int e = e1 - 1;
-      if (khash[e] == h) {
-        bool eq = true;
-        for (int n = lane; n < r; n += 32) eq = eq && vreg[(int64_t)n * P.kk + e] == accv[(int64_t)n * P.k + ci];
-        if (__all_sync(0xffffffffu, eq)) { fe = e; break; }
-      }
-      slot = (slot + 1) & Hm;
-    }
-    if (lane == 0) { found[t] = fe; hsh[t] = h; }
-  }
-  __syncthreads();
-  // 4a'. without the bin-consistency check (extra_checks bit 1 off) two accepted candidates of one iteration can
-  //      decode to the same key; Alg. 2 l.30 processes them in ascending b, so the first creates the entry and
-  //      the later ones accumulate into it.  A key absent from R is marked a duplicate of the FIRST earlier
-  //      accepted candidate with the same key (found = -2 - t'); so is a key of R found twice (its += a would
-  //      race in 4b).  With the check on, equal keys have equal
-  //      v_m mod p = b, so distinct candidates never collide and this pass is skipped.
-  //      The first occurrence comes from a table of key-hash groups (open addressing over the freed cand array,
-  //      slot = 1 + the smallest t of the group by atomicMin); a group whose smallest t holds a different key
-  //      (a 64-bit hash collision) falls back to the scan over every earlier t.
-  bool any_dup = false;
-  if (!(P.extra & 2)) {
-    int* gtab = cand;                                   // p ints; p >= c k* >= 2 na
-    int tsz = 1;
-    while (2 * tsz <= p) tsz *= 2;
-    const int gm = tsz - 1;
-    for (int i = tid; i < tsz; i += blockDim.x) gtab[i] = 0;
-    __syncthreads();
-    for (int t = tid; t < na; t += blockDim.x) {
-      const uint64_t h = hsh[t];
-      int slot = (int)((h ^ (h >> 32)) & (uint64_t)gm);
-      for (;;) {
-        int o = reinterpret_cast<volatile int*>(gtab)[slot];
-        if (o == 0) {
-          o = atomicCAS(&gtab[slot], 0, t + 1);
-          if (o == 0) break;
-        }
-        if (hsh[o - 1] == h) {                          // every occupant of a slot has this slot's hash
-          atomicMin(&gtab[slot], t + 1);
-          break;
-        }
-        slot = (slot + 1) & gm;
-      }
+      if (lane == 0) { found[t] = fe; hsh[t] = h; }
     }
     __syncthreads();
-    int dup_local = 0;
-    for (int t = tid; t < na; t += blockDim.x) {
-      const uint64_t h = hsh[t];
-      int slot = (int)((h ^ (h >> 32)) & (uint64_t)gm);
-      while (hsh[gtab[slot] - 1] != h) slot = (slot + 1) & gm;
-      const int first = gtab[slot] - 1;
-      int dup = -1;
-      if (first != t) {
-        const int ci = accl[t], c1 = accl[first];
-        bool eq = found[first] == found[t];
-        if (eq && found[t] < 0)
-          for (int n = 0; n < r && eq; ++n) eq = accv[(int64_t)n * P.k + c1] == accv[(int64_t)n * P.k + ci];
-        if (eq) dup = first;
-        else if (found[t] >= 0) {                       // hash collision: the scan (an existing key found twice)
-          for (int t2 = 0; t2 < t && dup < 0; ++t2)
-            if (found[t2] == found[t]) dup = t2;
-        } else {
-          for (int t2 = 0; t2 < t && dup < 0; ++t2) {
-            if (found[t2] >= 0 || hsh[t2] != h) continue;
-            const int c2 = accl[t2];
-            bool e2 = true;
-            for (int n = 0; n < r && e2; ++n) e2 = accv[(int64_t)n * P.k + c2] == accv[(int64_t)n * P.k + ci];
-            if (e2) dup = t2;
+    // 4a'. without the bin-consistency check (extra_checks bit 1 off) two accepted candidates of one iteration can
+    //      decode to the same key; Alg. 2 l.30 processes them in ascending b, so the first creates the entry and
+    //      the later ones accumulate into it.  A key absent from R is marked a duplicate of the FIRST earlier
+    //      accepted candidate with the same key (found = -2 - t'); so is a key of R found twice (its += a would
+    //      race in 4b).  With the check on, equal keys have equal
+    //      v_m mod p = b, so distinct candidates never collide and this pass is skipped.
+    //      The first occurrence comes from a table of key-hash groups (open addressing over the freed cand array,
+    //      slot = 1 + the smallest t of the group by atomicMin); a group whose smallest t holds a different key
+    //      (a 64-bit hash collision) falls back to the scan over every earlier t.
+    bool any_dup = false;
+    if (!(P.extra & 2)) {
+      int* gtab = cand;                                   // p_own ints; p_own >= c k* >= 2 na
+      int tsz = 1;
+      while (2 * tsz <= p_own) tsz *= 2;
+      const int gm = tsz - 1;
+      for (int i = tid; i < tsz; i += blockDim.x) gtab[i] = 0;
+      __syncthreads();
+      for (int t = tid; t < na; t += blockDim.x) {
+        const uint64_t h = hsh[t];
+        int slot = (int)((h ^ (h >> 32)) & (uint64_t)gm);
+        for (;;) {
+          int o = reinterpret_cast<volatile int*>(gtab)[slot];
+          if (o == 0) {
+            o = atomicCAS(&gtab[slot], 0, t + 1);
+            if (o == 0) break;
+          }
+          if (hsh[o - 1] == h) {                          // every occupant of a slot has this slot's hash
+            atomicMin(&gtab[slot], t + 1);
+            break;
+          }
+          slot = (slot + 1) & gm;
+        }
+      }
+      __syncthreads();
+      int dup_local = 0;
+      for (int t = tid; t < na; t += blockDim.x) {
+        const uint64_t h = hsh[t];
+        int slot = (int)((h ^ (h >> 32)) & (uint64_t)gm);
+        while (hsh[gtab[slot] - 1] != h) slot = (slot + 1) & gm;
+        const int first = gtab[slot] - 1;
+        int dup = -1;
+        if (first != t) {
+          const int ci = accl[t], c1 = accl[first];
+          bool eq = found[first] == found[t];
+          if (eq && found[t] < 0)
+            for (int n = 0; n < r && eq; ++n) eq = accv[(int64_t)n * P.k + c1] == accv[(int64_t)n * P.k + ci];
+          if (eq) dup = first;
+          else if (found[t] >= 0) {                       // hash collision: the scan (an existing key found twice)
+            for (int t2 = 0; t2 < t && dup < 0; ++t2)
+              if (found[t2] == found[t]) dup = t2;
+          } else {
+            for (int t2 = 0; t2 < t && dup < 0; ++t2) {
+              if (found[t2] >= 0 || hsh[t2] != h) continue;
+              const int c2 = accl[t2];
+              bool e2 = true;
+              for (int n = 0; n < r && e2; ++n) e2 = accv[(int64_t)n * P.k + c2] == accv[(int64_t)n * P.k + ci];
+              if (e2) dup = t2;
+            }
           }
         }
+        flag[t] = dup;
+        dup_local |= dup >= 0;
       }
-      flag[t] = dup;
-      dup_local |= dup >= 0;
+      any_dup = __syncthreads_or(dup_local) != 0;
+      if (any_dup) {
+        for (int t = tid; t < na; t += blockDim.x)
+          if (flag[t] >= 0) found[t] = -2 - flag[t];
+        __syncthreads();
+      }
     }
-    any_dup = __syncthreads_or(dup_local) != 0;
+    // 4b. R[v] += a for found keys; new keys get entries nR + rank in ascending-b order (deterministic)
+    int n_new;
+    {
+      const int per = (na + blockDim.x - 1) / blockDim.x;
+      const int t0 = tid * per, t1 = min(na, t0 + per);
+      int c4 = 0;
+      for (int t = t0; t < t1; ++t) c4 += found[t] == -1;
+      int rank = block_excl_scan(c4, scratch, &total);
+      n_new = min(total, P.k - nR);
+      for (int t = t0; t < t1; ++t) {
+        const int ci = accl[t];
+        const double2 f0 = P.rec_f0[(int64_t)sr * P.k + ci];   // F_0 at the candidate (the FFT's line-0 CTA)
+        const double2 a = make_double2(f0.x / (double)p, f0.y / (double)p);    // Eq. (7): a = F_0 / p
+        if (found[t] >= 0) {
+          const int e = found[t];
+          if (!(SPEC && spec_skip(P, s, e, iter, gs))) {
+            areg[e] = make_double2(areg[e].x + a.x, areg[e].y + a.y);
+            if (SPEC) P.spec_touch[(int64_t)s * P.k + e] = spec_tag(iter, gs);
+          }
+          flag[t] = 0;
+        } else if (found[t] == -1) {
+          const int e = nR + rank++;
+          if (e >= P.k) {                                   // capacity k (R26: several primes' false accepts)
+            flag[t] = 0;
+            continue;
+          }
+          areg[e] = a;
+          khash[e] = hsh[t];
+          if (SPEC) P.spec_touch[(int64_t)s * P.k + e] = spec_tag(iter, gs);
+          found[t] = e;
+          flag[t] = 1;
+        } else {
+          flag[t] = 0;                                      // duplicate: accumulated below, in ascending b
+        }
+      }
+    }
+    __syncthreads();
     if (any_dup) {
-      for (int t = tid; t < na; t += blockDim.x)
-        if (flag[t] >= 0) found[t] = -2 - flag[t];
+      if (tid == 0)
+        for (int t = 0; t < na; ++t) {
+          if (found[t] >= -1) continue;
+          const int e = found[-2 - found[t]];             // the entry its first occurrence created
+          found[t] = e;
+          if (e < 0 || (SPEC && spec_skip(P, s, e, iter, gs))) continue;   // first occurrence dropped / key of an earlier set
+          const int ci = accl[t];
+          const double2 f0 = P.rec_f0[(int64_t)sr * P.k + ci];
+          areg[e] = make_double2(areg[e].x + f0.x / (double)p, areg[e].y + f0.y / (double)p);
+          found[t] = e;
+        }
       __syncthreads();
     }
-  }
-  // 4b. R[v] += a for found keys; new keys get entries nR + rank in ascending-b order (deterministic)
-  int n_new;
-  {
-    const int per = (na + blockDim.x - 1) / blockDim.x;
-    const int t0 = tid * per, t1 = min(na, t0 + per);
-    int c4 = 0;
-    for (int t = t0; t < t1; ++t) c4 += found[t] == -1;
-    int rank = block_excl_scan(c4, scratch, &total);
-    n_new = total;
-    for (int t = t0; t < t1; ++t) {
-      const int ci = accl[t];
-      const double2 f0 = P.rec_f0[(int64_t)s * P.k + ci];   // F_0 at the candidate (the FFT's line-0 CTA)
-      const double2 a = make_double2(f0.x / (double)p, f0.y / (double)p);    // Eq. (7): a = F_0 / p
-      if (found[t] >= 0) {
+    // 4c. new entries: key row and hash-table insert (warp per entry with lanes along the coordinates for long
+    //     keys, thread per entry otherwise)
+    if (!wide) {
+      // key rows: items (entry, 8 axes) with the entries along the threads (coalesced record reads), the
+      // 8 loads of an item issued before its stores
+      const int rch = (r + 7) / 8;
+      for (int it = tid; it < na * rch; it += blockDim.x) {
+        const int t = it % na, n0 = (it / na) * 8;
+        if (!flag[t]) continue;
+        const int ci = accl[t], e = found[t];
+        int64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = n0 + u < r ? accv[(int64_t)(n0 + u) * P.k + ci] : 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (n0 + u < r) vreg[(int64_t)(n0 + u) * P.kk + e] = v[u];
+      }
+      for (int t = tid; t < na; t += blockDim.x) {
+        if (!flag[t]) continue;
         const int e = found[t];
-        areg[e] = make_double2(areg[e].x + a.x, areg[e].y + a.y);
-        flag[t] = 0;
-      } else if (found[t] == -1) {
-        const int e = nR + rank++;
-        areg[e] = a;
-        khash[e] = hsh[t];
-        found[t] = e;
-        flag[t] = 1;
-      } else {
-        flag[t] = 0;                                      // duplicate: accumulated below, in ascending b
+        int slot = (int)(hsh[t] & (uint64_t)Hm);
+        while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
       }
     }
-  }
-  __syncthreads();
-  if (any_dup) {
-    if (tid == 0)
-      for (int t = 0; t < na; ++t) {
-        if (found[t] >= -1) continue;
-        const int e = found[-2 - found[t]];             // the entry its first occurrence created
-        const int ci = accl[t];
-        const double2 f0 = P.rec_f0[(int64_t)s * P.k + ci];
-        areg[e] = make_double2(areg[e].x + f0.x / (double)p, areg[e].y + f0.y / (double)p);
-        found[t] = e;
-      }
-    __syncthreads();
-  }
-  // 4c. new entries: key row and hash-table insert (warp per entry with lanes along the coordinates for long
-  //     keys, thread per entry otherwise)
-  if (!wide) {
-    // key rows: items (entry, 8 axes) with the entries along the threads (coalesced record reads), the
-    // 8 loads of an item issued before its stores
-    const int rch = (r + 7) / 8;
-    for (int it = tid; it < na * rch; it += blockDim.x) {
-      const int t = it % na, n0 = (it / na) * 8;
+    for (int t = warp; wide && t < na; t += nwarps) {
       if (!flag[t]) continue;
       const int ci = accl[t], e = found[t];
-      int64_t v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = n0 + u < r ? accv[(int64_t)(n0 + u) * P.k + ci] : 0;
-#pragma unroll
-      for (int u = 0; u < 8; ++u)
-        if (n0 + u < r) vreg[(int64_t)(n0 + u) * P.kk + e] = v[u];
+      for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
+      if (lane == 0) {
+        int slot = (int)(hsh[t] & (uint64_t)Hm);
+        while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+      }
     }
-    for (int t = tid; t < na; t += blockDim.x) {
-      if (!flag[t]) continue;
-      const int e = found[t];
-      int slot = (int)(hsh[t] & (uint64_t)Hm);
-      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
-    }
-  }
-  for (int t = warp; wide && t < na; t += nwarps) {
-    if (!flag[t]) continue;
-    const int ci = accl[t], e = found[t];
-    for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + e] = accv[(int64_t)n * P.k + ci];
-    if (lane == 0) {
-      int slot = (int)(hsh[t] & (uint64_t)Hm);
-      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
-    }
-  }
-  __syncthreads();
-  const int nR_new = nR + n_new;
+    __syncthreads();
+    const int nR_new = nR + n_new;
 
-  // prune test (only touched entries can have changed)
-  int small = 0;
-  for (int t = tid; t < na; t += blockDim.x) {
-    const double2 a = areg[found[t]];
-    small |= hypot(a.x, a.y) < P.prune;
-  }
-  const int any_small = __syncthreads_or(small);
-  double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
-  if (P.crow_mode && !any_small) {
-    // the rows go to crow_kernel (GPU-wide): the touched entries in ascending b and this signal's work items
-    for (int t = tid; t < na; t += blockDim.x) P.crow_list[(int64_t)s * P.k + t] = found[t];
-    const int nit = ((na + 31) / 32) * P.crow_nl;
-    if (tid == 0) scratch[0] = nit > 0 ? atomicAdd(&P.ctrl[5], nit) : 0;
-    __syncthreads();
-    const int base = scratch[0];
-    for (int i = tid; i < nit; i += blockDim.x) P.crow_items[base + i] = make_int4(s, i / P.crow_nl, i % P.crow_nl, na);
-  } else {
-    // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}.  Items
-    // (entry, 8 lines) with the entries along the threads; v from the record (a touched entry's key equals
-    // its candidate's coordinates), coalesced, the 8 loads of an item in flight together
-    const int lch = (P.Lp + 7) / 8;
-    const bool by_items = 2 * na * lch >= (int)blockDim.x;  // else too few items: warp per entry, lanes along the row
-    for (int t = warp; !by_items && t < na; t += nwarps) {
-      const int e = found[t], ci = accl[t];
-      const double2 a = areg[e];
-      for (int n = lane; n < P.Lp; n += 32) {
-        double2 c;
-        if (n == 0) c = make_double2(-a.x, -a.y);
-        else if (n < P.L) {
-          const double2 lf = line_factor_exact(accv[(int64_t)(P.line_lo + n - 1) * P.k + ci], Ev);
-          c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
-        } else c = make_double2(0.0, 0.0);
-        Creg[(int64_t)e * P.Lp + n] = c;
-      }
+    // prune test (only touched entries can have changed): after the last set, over every set's touched entries
+    const bool last = gs == G - 1;
+    int small = 0;
+    for (int t = tid; !SPEC && t < na; t += blockDim.x) {
+      if (found[t] < 0) continue;
+      const double2 a = areg[found[t]];
+      small |= hypot(a.x, a.y) < P.prune;
     }
-    for (int it = tid; by_items && it < na * lch; it += blockDim.x) {
-      const int t = it % na, n0 = (it / na) * 8;
-      const int e = found[t], ci = accl[t];
+    for (int e = tid; SPEC && last && e < nR_new; e += blockDim.x) {
+      if (P.spec_touch[(int64_t)s * P.k + e] >> 4 != iter) continue;
       const double2 a = areg[e];
-      int64_t v[8];
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int n = n0 + u;
-        v[u] = (n >= 1 && n < P.L) ? accv[(int64_t)(P.line_lo + n - 1) * P.k + ci] : 0;
-      }
-      double2* row = Creg + (int64_t)e * P.Lp;
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int n = n0 + u;
-        if (n >= P.Lp) break;
-        double2 c;
-        if (n == 0) c = make_double2(-a.x, -a.y);
-        else if (n < P.L) {
-          const double2 lf = line_factor_exact(v[u], Ev);
-          c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
-        } else c = make_double2(0.0, 0.0);
-        row[n] = c;
-      }
+      small |= hypot(a.x, a.y) < P.prune;
     }
-  }
-  int nR_final = nR_new;
-  if (any_small) {
-    // rare path: order-preserving compaction by warp 0, then rebuild the hash table
-    __syncthreads();                                    // the C rows above are in before warp 0 moves them
-    if (warp == 0) {
-      int wpos = 0;
-      for (int e = 0; e < nR_new; ++e) {
-        const double2 a = areg[e];
-        const bool keep = !(hypot(a.x, a.y) < P.prune);
-        if (keep) {
-          if (wpos != e) {
-            for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + wpos] = vreg[(int64_t)n * P.kk + e];
-            for (int n = lane; n < P.Lp; n += 32) Creg[(int64_t)wpos * P.Lp + n] = Creg[(int64_t)e * P.Lp + n];
-            if (lane == 0) { areg[wpos] = a; khash[wpos] = khash[e]; }
+    const int any_small = __syncthreads_or(small);
+    double2* Creg = P.C_all + ((int64_t)s * P.kk + P.k) * P.Lp;
+    if (SPEC) {
+      // R26: the rows of every set's touched entries once, after the last set, from the registry's key rows
+      // (crow_kernel over a list in ascending entry order, or here when a prune follows / few rows)
+      if (last) {
+        const int per = (nR_new + blockDim.x - 1) / blockDim.x;
+        const int e0 = tid * per, e1 = min(nR_new, e0 + per);
+        int ct = 0;
+        for (int e = e0; e < e1; ++e) ct += P.spec_touch[(int64_t)s * P.k + e] >> 4 == iter;
+        int tt = 0;
+        int pos = block_excl_scan(ct, scratch, &tt);
+        __syncthreads();
+        int* tl = accl;                                   // free after the last set: the touched list
+        for (int e = e0; e < e1; ++e)
+          if (P.spec_touch[(int64_t)s * P.k + e] >> 4 == iter) tl[pos++] = e;
+        __syncthreads();
+        if (P.crow_mode && !any_small) {
+          for (int t = tid; t < tt; t += blockDim.x) P.crow_list[(int64_t)s * P.k + t] = tl[t];
+          const int nit = ((tt + 31) / 32) * P.crow_nl;
+          if (tid == 0) scratch[0] = nit > 0 ? atomicAdd(&P.ctrl[5], nit) : 0;
+          __syncthreads();
+          const int base = scratch[0];
+          for (int i = tid; i < nit; i += blockDim.x)
+            P.crow_items[base + i] = make_int4(s, i / P.crow_nl, i % P.crow_nl, tt);
+        } else {
+          const int64_t* vk = P.v_all + (int64_t)s * r * P.kk + P.k;
+          for (int it = tid; it < tt * P.Lp; it += blockDim.x) {
+            const int t = it % tt, n = it / tt;
+            const int e = tl[t];
+            const double2 a = areg[e];
+            double2 c = make_double2(0.0, 0.0);
+            if (n == 0) c = make_double2(-a.x, -a.y);
+            else if (n < P.L) {
+              const double2 lf = line_factor_exact(vk[(int64_t)(P.line_lo + n - 1) * P.kk + e], Ev);
+              c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+            }
+            Creg[(int64_t)e * P.Lp + n] = c;
           }
-          ++wpos;
         }
-        __syncwarp();
       }
-      if (lane == 0) scratch[0] = wpos;
+    } else if (P.crow_mode && !any_small) {
+      // the rows go to crow_kernel (GPU-wide): the touched entries in ascending b and this signal's work items
+      for (int t = tid; t < na; t += blockDim.x) P.crow_list[(int64_t)s * P.k + t] = found[t];
+      const int nit = ((na + 31) / 32) * P.crow_nl;
+      if (tid == 0) scratch[0] = nit > 0 ? atomicAdd(&P.ctrl[5], nit) : 0;
+      __syncthreads();
+      const int base = scratch[0];
+      for (int i = tid; i < nit; i += blockDim.x) P.crow_items[base + i] = make_int4(s, i / P.crow_nl, i % P.crow_nl, na);
+    } else {
+      // C rows of touched entries: C[k+e][0] = -a_e, C[k+e][1+n] = -a_e e^{2 pi i (v_{e,n} mod E)/E}.  Items
+      // (entry, 8 lines) with the entries along the threads; v from the record (a touched entry's key equals
+      // its candidate's coordinates), coalesced, the 8 loads of an item in flight together
+      const int lch = (P.Lp + 7) / 8;
+      const bool by_items = 2 * na * lch >= (int)blockDim.x;  // else too few items: warp per entry, lanes along the row
+      for (int t = warp; !by_items && t < na; t += nwarps) {
+        const int e = found[t], ci = accl[t];
+        if (e < 0) continue;                                // dropped (capacity)
+        const double2 a = areg[e];
+        for (int n = lane; n < P.Lp; n += 32) {
+          double2 c;
+          if (n == 0) c = make_double2(-a.x, -a.y);
+          else if (n < P.L) {
+            const double2 lf = line_factor_exact(accv[(int64_t)(P.line_lo + n - 1) * P.k + ci], Ev);
+            c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+          } else c = make_double2(0.0, 0.0);
+          Creg[(int64_t)e * P.Lp + n] = c;
+        }
+      }
+      for (int it = tid; by_items && it < na * lch; it += blockDim.x) {
+        const int t = it % na, n0 = (it / na) * 8;
+        const int e = found[t], ci = accl[t];
+        if (e < 0) continue;                                // dropped (capacity)
+        const double2 a = areg[e];
+        int64_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int n = n0 + u;
+          v[u] = (n >= 1 && n < P.L) ? accv[(int64_t)(P.line_lo + n - 1) * P.k + ci] : 0;
+        }
+        double2* row = Creg + (int64_t)e * P.Lp;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int n = n0 + u;
+          if (n >= P.Lp) break;
+          double2 c;
+          if (n == 0) c = make_double2(-a.x, -a.y);
+          else if (n < P.L) {
+            const double2 lf = line_factor_exact(v[u], Ev);
+            c = make_double2(-(a.x * lf.x - a.y * lf.y), -(a.x * lf.y + a.y * lf.x));
+          } else c = make_double2(0.0, 0.0);
+          row[n] = c;
+        }
+      }
     }
-    __syncthreads();
-    nR_final = scratch[0];
-    for (int i = tid; i < P.H; i += blockDim.x) htab[i] = 0;
-    __syncthreads();
-    for (int e = tid; e < nR_final; e += blockDim.x) {
-      int slot = (int)(khash[e] & (uint64_t)Hm);
-      while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+    nR_final = nR_new;
+    if (any_small) {
+      // rare path: order-preserving compaction by warp 0, then rebuild the hash table
+      __syncthreads();                                    // the C rows above are in before warp 0 moves them
+      if (warp == 0) {
+        int wpos = 0;
+        for (int e = 0; e < nR_new; ++e) {
+          const double2 a = areg[e];
+          const bool keep = !(hypot(a.x, a.y) < P.prune);
+          if (keep) {
+            if (wpos != e) {
+              for (int n = lane; n < r; n += 32) vreg[(int64_t)n * P.kk + wpos] = vreg[(int64_t)n * P.kk + e];
+              for (int n = lane; n < P.Lp; n += 32) Creg[(int64_t)wpos * P.Lp + n] = Creg[(int64_t)e * P.Lp + n];
+              if (lane == 0) { areg[wpos] = a; khash[wpos] = khash[e]; }
+            }
+            ++wpos;
+          }
+          __syncwarp();
+        }
+        if (lane == 0) scratch[0] = wpos;
+      }
+      __syncthreads();
+      nR_final = scratch[0];
+      for (int i = tid; i < P.H; i += blockDim.x) htab[i] = 0;
+      __syncthreads();
+      for (int e = tid; e < nR_final; e += blockDim.x) {
+        int slot = (int)(khash[e] & (uint64_t)Hm);
+        while (atomicCAS(&htab[slot], 0, e + 1) != 0) slot = (slot + 1) & Hm;
+      }
+      __syncthreads();
     }
+    nR = nR_final;
+    na_all += na;
     __syncthreads();
   }
+  const int p = p_own, na = na_all;
 
   // ---- 5. state ----
   if (tid == 0) {
-    const int K = P.k + (P.literal ? nR : 0);
+    const int K = P.k + (P.literal ? nR0 : 0);
     P.st_nR[s] = nR_final;
     int stall = na == 0 ? P.st_stall[s] + 1 : 0;
     P.st_samples[s] += (int64_t)(r + 1) * p;              // f evaluations of all shards (reading C22)

@@ -35,14 +35,16 @@ __global__ void setup_kernel(DevParams P, int32_t iter, int32_t seq) {
     P.st_retilt[s] = 0;
     const int il = P.st_il[s] + 1;                         // counter of the current level (= iter without a switch)
     P.st_il[s] = il;
+    // prime counter: il (Alg. 2 l.8); with G-prime speculation (R26) slot s takes counter (il - 1) G + s % G + 1
+    const int ic = P.spec_G > 1 ? (il - 1) * P.spec_G + s % P.spec_G + 1 : il;
     int p;
-    if (P.n_sched > 0) p = (int)P.sched[(il - 1) % P.n_sched];
-    else p = ith_prime_at_least(P, P.c * kstar, il);
+    if (P.n_sched > 0) p = (int)P.sched[(ic - 1) % P.n_sched];
+    else p = ith_prime_at_least(P, P.c * kstar, ic);
     if (p < 2 || p > P.p_cap) {
       P.st_status[s] = SFFT_ENOTSUP;
     } else {
       P.st_p[s] = p;
-      P.st_m[s] = il % P.r;
+      P.st_m[s] = ic % P.r;
       P.active[atomicAdd(&P.ctrl[0], 1)] = s;
       atomicMax(&P.ctrl[1], p);
       atomicMax(&P.ctrl[2], P.k + (P.literal ? nR : 0));  // terms the exp-sum sums
@@ -81,7 +83,9 @@ size_t decode_smem_bytes(const DevParams& P, int32_t max_p) {
 //              coordinates unpacked, then steps 2b-5 (bin consistency, accepted list, registry, state).  With
 //              line sharding the records of all shards arrive by the all-gather; line 0 is
 //              computed identically on every shard, so every shard applies the same registry update.
-enum { kDecStage = 0, kDecCommit = 1 };
+// kDecCommitSpec : the same with multi-prime speculation (R26: G record sets merged per slot), a separate
+//              instantiation so that the single-set commit keeps its register budget.
+enum { kDecStage = 0, kDecCommit = 1, kDecCommitSpec = 2 };
 
 template <int MODE>
 __global__ void __launch_bounds__(kDecodeThreads)
@@ -92,7 +96,7 @@ decode_kernel(DevParams P, int32_t iter, int32_t kstar_stage, int32_t* out_b, in
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int s = P.active[blockIdx.x];
   if (!STAGE) {
-    commit_signal(P, iter, s, smem_raw);
+    commit_signal<MODE == kDecCommitSpec>(P, iter, s, smem_raw);
     return;
   }
   const int p = P.st_p[s], m = P.st_m[s];
@@ -203,7 +207,7 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
   double2* Cs = P.C_all + (int64_t)s * kk * P.Lp;
   // 1. signal terms (warp per term)
   for (int j = warp; j < P.k; j += nwarps) {
-    const int32_t* w = freqs + ((int64_t)s * P.k + j) * P.d;
+    const int32_t* w = freqs + ((int64_t)(P.spec_G > 1 ? s / P.spec_G : s) * P.k + j) * P.d;   // input of slot s
     for (int q = lane; q < r; q += 32) {
       const int off = P.block_off[q], dq = P.block_dims[q];
       int64_t acc = 0, pw = 1;
@@ -314,14 +318,14 @@ cudaError_t launch_retilt(const DevParams& P, int32_t batch, const int32_t* freq
 
 cudaError_t launch_decode_commit(const DevParams& P, int32_t iter, int32_t max_p, int32_t n_active, cudaStream_t st) {
   const size_t smem = decode_smem_bytes(P, max_p);
-  cudaError_t e = ensure_smem(decode_kernel<kDecCommit>, smem);
+  const auto kern = P.spec_G > 1 ? decode_kernel<kDecCommitSpec> : decode_kernel<kDecCommit>;
+  cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   // threads: ~8 (candidate, axis) records per thread (small problems: many short CTAs, e.g. C2's 1024 signals)
   const long work = (long)P.k * (P.r + 1) / 8;
   const int threads = (int)std::min<long>(kDecodeThreads, std::max<long>(128, (work + 31) / 32 * 32));
   if (n_active > 0)
-    return launch_pdl(decode_kernel<kDecCommit>, dim3(n_active), dim3(threads), smem, st, P, iter, 0, nullptr, nullptr,
-                      nullptr, nullptr);
+    return launch_pdl(kern, dim3(n_active), dim3(threads), smem, st, P, iter, 0, nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 

@@ -1082,7 +1082,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
         }
       }
       __syncthreads();
-      if (last) commit_signal(P, P.cur_iter, s, smem_raw);
+      if (last) commit_signal<false>(P, P.cur_iter, s, smem_raw);   // not with R26 (api.cu)
     }
     return;
   }

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(256) project_kernel(DevParams P, int32_t batch
   int64_t* vs = P.v_all + (int64_t)s * P.r * P.kk;
   const int64_t vstr = SMEM ? 1 : P.kk;
   int64_t* vsm = SMEM ? vsm_all + (int64_t)(threadIdx.x >> 5) * P.r : vs + j;
-  const int32_t* w = freqs + ((int64_t)s * P.k + j) * P.d;
+  const int si = P.spec_G > 1 ? s / P.spec_G : s;              // the input signal of slot s (R26)
+  const int32_t* w = freqs + ((int64_t)si * P.k + j) * P.d;
   for (int q = lane; q < P.r; q += 32) {
     const int off = P.block_off[q], dq = P.block_dims[q];
     int64_t acc = 0, pw = 1;
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) project_kernel(DevParams P, int32_t batch
   __syncwarp();
   if (SMEM)
     for (int q = lane; q < P.r; q += 32) vs[(int64_t)q * P.kk + j] = vsm[q];
-  const double2 a = coeffs[(int64_t)s * P.k + j];
+  const double2 a = coeffs[(int64_t)si * P.k + j];
   double2* Crow = P.C_all + ((int64_t)s * P.kk + j) * P.Lp;
   for (int n = lane; n < P.Lp; n += 32) {
     double2 c;

@@ -25,16 +25,17 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(gt & (G - 1));
   const int64_t gw = gt / G;
-  if (gw >= (int64_t)P.batch * P.k) return;
+  if (gw >= (int64_t)(P.batch / P.spec_G) * P.k) return;   // signals (R26: P.batch counts G slots each)
   const int s = (int)(gw / P.k), e = (int)(gw % P.k);
-  if (e >= P.st_nR[s]) return;
-  const int64_t* vreg = P.v_all + (int64_t)s * P.r * P.kk + P.k;
+  const int sl = s * P.spec_G;                         // the signal's (first) slot (R26: G identical copies)
+  if (e >= P.st_nR[sl]) return;
+  const int64_t* vreg = P.v_all + (int64_t)sl * P.r * P.kk + P.k;
   int32_t* row = P.wtmp + ((int64_t)s * P.k + e) * P.d;
   const int64_t N = P.N, h2 = N / 2;
   const double invN = 1.0 / (double)N;
   const int lgN = (N & (N - 1)) == 0 ? __ffsll(N) - 1 : -1;
   int err = 0;
-  const int lvl = P.st_lvl[s];
+  const int lvl = P.st_lvl[sl];
   const int32_t* axt = P.lvl_axt + (int64_t)lvl * P.r;
   const int64_t* tl = P.lvl_tilts + (int64_t)lvl * P.lvl_tmax * 5;
   for (int q = lane; q < P.r; q += G) {
@@ -85,7 +86,7 @@ __global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm,
   int* ord = reinterpret_cast<int*>(key + (size_t)nchs * P.k);                   // [power of two >= k]
   __shared__ int any_tie;
   const int s = blockIdx.x, tid = threadIdx.x;
-  const int nR = P.st_nR[s];
+  const int nR = P.st_nR[s * P.spec_G];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
   const int64_t h2 = P.N / 2;
   auto build = [&](int c0, int c1) {                         // chunks [c0, c1) of every row, chunk index fastest
@@ -173,7 +174,7 @@ __global__ void wrap_rank_kernel(DevParams P, int32_t* __restrict__ perm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [k]
   const int s = blockIdx.x, tid = threadIdx.x;
-  const int nR = P.st_nR[s];
+  const int nR = P.st_nR[s * P.spec_G];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
   const int64_t h2 = P.N / 2;
   for (int e = tid; e < nR; e += blockDim.x) {
@@ -209,9 +210,10 @@ __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(gt & (G - 1));
   const int64_t gw = gt / G;
-  if (gw >= (int64_t)P.batch * P.k) return;
+  if (gw >= (int64_t)(P.batch / P.spec_G) * P.k) return;   // signals (R26: P.batch counts G slots each)
   const int s = (int)(gw / P.k), i = (int)(gw % P.k);
-  const int nR = P.st_nR[s];
+  const int sl = s * P.spec_G;
+  const int nR = P.st_nR[sl];
   int32_t* of = out_freqs + ((int64_t)s * P.k + i) * P.d;
   if (i < nR) {
     const int e = perm[(int64_t)s * P.k + i];
@@ -223,18 +225,18 @@ __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm
     } else {
       for (int l = lane; l < P.d; l += G) of[l] = src[l];
     }
-    if (lane == 0) out_coeffs[(int64_t)s * P.k + i] = P.a_reg[(int64_t)s * P.k + e];
+    if (lane == 0) out_coeffs[(int64_t)s * P.k + i] = P.a_reg[(int64_t)sl * P.k + e];
   } else {
     for (int l = lane; l < P.d; l += G) of[l] = 0;
     if (lane == 0) out_coeffs[(int64_t)s * P.k + i] = make_double2(0.0, 0.0);
   }
   if (i == 0 && lane == 0) {
-    int status = P.st_status[s];
+    int status = P.st_status[sl];
     if (status == ST_RUN) status = SFFT_PARTIAL;
     if (bad[s]) status = SFFT_ECORRUPT;
     out_count[s] = nR;
     if (out_status) out_status[s] = status;
-    P.st_status[s] = status;
+    P.st_status[sl] = status;
   }
 }
 

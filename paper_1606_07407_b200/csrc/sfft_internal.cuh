@@ -158,6 +158,10 @@ struct DevParams {
   // commit CTA: the commit lists the touched entries and appends work items (32 entries x 16 lines) counted in
   // ctrl[5]
   int32_t crow_mode;           // launch flag of the commit kernel (0: the commit writes the rows itself)
+  // multi-prime speculation (reading R26): slot s holds signal s / spec_G with the prime of counter
+  // (i - 1) spec_G + s % spec_G + 1; the commit merges the spec_G sibling slots' records
+  int32_t spec_G;              // 1 = Alg. 2 as written
+  int32_t* spec_touch;         // [slots][k] (iteration << 4) | set of the last update of entry e
   int32_t crow_nl;             // 16-line chunks per row, ceil(Lp / 16)
   int4* crow_items;            // [batch * ceil(k / 32) * crow_nl] (signal, entry chunk, line chunk, touched count)
   int32_t* crow_list;          // [batch][k] touched entry indices of the iteration, ascending b

@@ -217,6 +217,70 @@ def test_e2e_full_size_vs_golden_oracle(S, name, tag, trials):
     assert rep.samples_used == sum(int(g[f"{tag}_{t}_samples"]) for t in trials)
 
 
+# ------------------------------------------------------------------ multi-prime speculation (NEXT #3, reading R26)
+@pytest.mark.parametrize("name,T,G", [("c1", 20, 2), ("c1", 20, 3), ("c2", 8, 2), ("c2", 8, 4), ("c2", 3, 16)])
+def test_e2e_speculation_vs_live_oracle(S, name, T, G):
+    """spec_primes = G: G slots per signal, each with its own prime of the iteration and registry copy, every
+    commit merging the G record sets in prime order -- against the oracle's R26 schedule (n_spec = G): statuses,
+    sets, coefficients, the f evaluations summed over every prime, the iteration count and signal 0's trace (first
+    prime and accepted bins of all primes per iteration)."""
+    c = W.CONFIGS[name]
+    w, a = W.make_batch(c, range(T))
+    plan = _plan(S, c, batch=T, spec_primes=G)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    samples, iters = 0, 0
+    for i in range(T):
+        ref = O.solve(O.params_for(c, n_spec=G), w[i], a[i])
+        assert int(res.per_status[i]) == ref.status == O.OK, i
+        _check_against_oracle(res, i, ref.w, ref.a)
+        samples += ref.samples
+        iters = max(iters, ref.iterations)
+        if i == 0:
+            tr = ref.trace
+            rep = res.report
+            assert [rep.primes[j] for j in range(min(len(tr), 64))] == tr[:64, 1].tolist()
+            assert [rep.accepted[j] for j in range(min(len(tr), 64))] == tr[:64, 4].tolist()
+    assert res.report.samples_used == samples and res.report.iterations == iters
+
+
+@pytest.mark.parametrize("name,t,G", [("c3", 0, 2), ("c3", 1, 4), ("c5", 0, 4), ("c4", 0, 2), ("c4", 1, 8)])
+@pytest.mark.parametrize("path", [0, 1])
+def test_e2e_speculation_full_size_vs_golden_oracle(S, name, t, G, path):
+    """R26 at BASELINE sizes (int8-limb and FP64 exp-sum) against tests/golden/oracle_spec.npz (written by
+    tests/golden/make_spec_golden.py from oracle/ only): set (SHA-256), coefficients, samples, trace; and exact
+    recovery of the input."""
+    c = W.CONFIGS[name]
+    g = np.load(os.path.join(GOLD_DIR, "oracle_spec.npz"))
+    key = f"{name}_{t}_G{G}"
+    w, a = W.make_batch(c, [t])
+    plan = _plan(S, c, batch=1, spec_primes=G, expsum_path=path)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    assert int(res.per_status[0]) == int(g[key + "_status"]) == S.SFFT_OK
+    n = int(res.count[0])
+    gw = np.ascontiguousarray(res.freqs[0, :n].cpu().numpy())
+    assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[key + "_w_sha256"]), key
+    assert _coef_ok(res.coeffs[0, :n].cpu().numpy(), g[key + "_a"]), key
+    assert np.array_equal(gw, W.canonical_sort(w[0], a[0])[0])
+    tr = g[key + "_trace"]
+    rep = res.report
+    assert rep.samples_used == int(g[key + "_samples"]) and rep.iterations == len(tr)
+    assert [rep.primes[j] for j in range(min(len(tr), 64))] == tr[:64, 1].tolist()
+    assert [rep.accepted[j] for j in range(min(len(tr), 64))] == tr[:64, 4].tolist()
+
+
+def test_speculation_options_validated(S):
+    c = W.CONFIGS["c2"]
+    for kw in (dict(spec_primes=17), dict(spec_primes=-1), dict(spec_primes=2, line_shards=2, line_rank=0),
+               dict(spec_primes=2, literal_residual=True)):
+        with pytest.raises(S.SfftError) as e:
+            _plan(S, c, batch=2, **kw)
+        assert e.value.status == S.SFFT_EINVAL
+    plan = _plan(S, c, batch=2, spec_primes=4)
+    w, a = W.make_batch(c, range(3))
+    with pytest.raises(ValueError):                         # 3 signals in a 2-signal plan (8 slots inside)
+        S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+
+
 def test_e2e_tilted_rectangle_and_fig2(S):
     """Static tilt (Eq. (27)) recovers the axis-aligned worst case; explicit prime schedule."""
     w = np.array([[[1, 1], [1, 2], [2, 1], [2, 2]]], np.int32)
