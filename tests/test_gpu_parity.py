@@ -268,6 +268,38 @@ def test_e2e_speculation_full_size_vs_golden_oracle(S, name, t, G, path):
     assert [rep.accepted[j] for j in range(min(len(tr), 64))] == tr[:64, 4].tolist()
 
 
+@pytest.mark.parametrize("d,N,k,blocks,structure,n_fb,trials", [
+    (2, 16, 8, (1, 1), "rectangles", 4, 12), (3, 16, 16, (1, 1, 1), "rect_mix", 4, 8),
+    (8, 16, 8, (1,) * 8, "rect_far", 67, 4)])
+@pytest.mark.parametrize("G", [2, 3])
+def test_e2e_speculation_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trials, G):
+    """R26 through the stall fallback (R23 / R24): the G slots of a signal stall together (their registries are
+    identical), switch level together and restart the prime counter; against the oracle's n_spec + n_fallback
+    schedule: statuses, sets, coefficients, sample totals, and the input spectrum recovered."""
+    c = W.custom_config(d, N, k, blocks, structure=structure)
+    ws, as_ = [], []
+    for t in range(trials * 2):
+        try:
+            w, a = W.make_signal(c, t)
+        except AssertionError:
+            continue
+        ws.append(w)
+        as_.append(a)
+        if len(ws) == trials:
+            break
+    w, a = np.stack(ws).astype(np.int32), np.stack(as_)
+    plan = _plan(S, c, batch=len(ws), fallback_tilts=n_fb, spec_primes=G)
+    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())
+    samples = 0
+    for i in range(len(ws)):
+        ref = O.solve(O.params_for(c, n_fallback=n_fb, n_spec=G), w[i], a[i])
+        samples += ref.samples
+        assert int(res.per_status[i]) == ref.status == O.OK, i
+        _check_against_oracle(res, i, ref.w, ref.a)
+        assert np.array_equal(ref.w, W.canonical_sort(w[i], a[i])[0])
+    assert res.report.samples_used == samples and res.report.fallback_used > 0
+
+
 def test_speculation_options_validated(S):
     c = W.CONFIGS["c2"]
     for kw in (dict(spec_primes=17), dict(spec_primes=-1), dict(spec_primes=2, line_shards=2, line_rank=0),
