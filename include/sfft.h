@@ -102,6 +102,11 @@ typedef struct {
                                  latency); noiseless signals are recovered exactly, the trace differs from Alg. 2.
                                  Each signal occupies G plan slots (workspace ~G x).  0 / 1 = Alg. 2 as written;
                                  at most 16; not with line shards, fused commit or literal_residual [0] */
+  int32_t spec_distributed;   /* with spec_primes = G > 1: 1 = the G primes on G ranks (GPUs), this plan being rank
+                                 spec_rank with one slot per signal; every iteration the ranks all-gather their
+                                 records (sfft_comm_init shard_mode 2, or sfft_execute_group on one device) and
+                                 apply the same merge, so their registries stay identical [0] */
+  int32_t spec_rank;          /* 0 <= spec_rank < spec_primes when spec_distributed [0] */
 } sfft_options;
 
 /* Per-execute report (host struct). Aggregates over the batch. */
@@ -251,6 +256,11 @@ SFFT_API int sfft_stage_project(sfft_plan_t* plan, const sfft_signal_t* sig, int
  * and decodes the candidates of line 0 on them, all-gathers the per-candidate records (pass flag over
  * its lines, decoded coordinates of its axes: batch * ((k+1)/2 + (Lmax-1) k) int64 words per rank) with
  * ncclAllGather on the plan's stream, and applies the identical registry update (Alg. 2 l.20-33).
+ * Distributed multi-prime speculation (shard_mode 2, reading R26): the plan must have been created
+ * with spec_primes = nranks, spec_distributed = 1, spec_rank = rank; every iteration each rank samples, transforms
+ * and decodes its own prime of the iteration, the ranks all-gather their records (flags, coordinates and a tail
+ * of candidate count, p, m, candidate bins and F_0 there: batch * ((k+1)/2 + r k + 2 + (k+1)/2 + 2k) int64 words
+ * per rank) and every rank merges the nranks sets in rank (prime) order into its identical registry.
  *   nccl_unique_id  host, 128 bytes from sfft_comm_unique_id on rank 0, broadcast by the caller
  * NCCL is loaded at run time (dlopen "libnccl.so.2": the copy already in the process, e.g. torch's,
  * else the system one); without it the call fails with SFFT_ENCCL.  All ranks must call it together

@@ -46,7 +46,8 @@ class sfft_options(ctypes.Structure):
                 ("literal_residual", ctypes.c_int32), ("expsum_path", ctypes.c_int32),
                 ("fallback_tilts", ctypes.c_int32), ("line_shards", ctypes.c_int32),
                 ("line_rank", ctypes.c_int32), ("table_cache_slots", ctypes.c_int32),
-                ("line_exchange", ctypes.c_int32), ("spec_primes", ctypes.c_int32)]
+                ("line_exchange", ctypes.c_int32), ("spec_primes", ctypes.c_int32),
+                ("spec_distributed", ctypes.c_int32), ("spec_rank", ctypes.c_int32)]
 
 
 class sfft_report(ctypes.Structure):
@@ -175,7 +176,8 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
               max_iter: int = 1000, stall_limit: int = 0, extra_checks: int = 3,
               stream=None, profile: bool = False, literal_residual: bool = False,
               expsum_path: int = 0, fallback_tilts: int = 0, line_shards: int = 0, line_rank: int = 0,
-              table_cache_slots: int = 0, line_exchange: int = 0, spec_primes: int = 0) -> Plan:
+              table_cache_slots: int = 0, line_exchange: int = 0, spec_primes: int = 0,
+              spec_distributed: int = 0, spec_rank: int = 0) -> Plan:
     """sfft_plan(d, N, k, primes, tilts, eps) of include/sfft.h; workspace from torch on the current device."""
     torch = _torch()
     L = lib()
@@ -197,6 +199,7 @@ def sfft_plan(d: int, N: int, k: int, primes: Optional[Sequence[int]] = None,
     opt.table_cache_slots = int(table_cache_slots)
     opt.line_exchange = int(line_exchange)
     opt.spec_primes = int(spec_primes)
+    opt.spec_distributed, opt.spec_rank = int(spec_distributed), int(spec_rank)
     pr = None
     if primes is not None:
         pr = (ctypes.c_int64 * len(primes))(*primes)
@@ -452,7 +455,8 @@ def sfft_comm_unique_id() -> bytes:
 
 
 def sfft_execute_group(plans: Sequence[Plan], sigs: Sequence[Signal], out=None) -> Result:
-    """Line-sharded solve of len(plans) shards on ONE device (include/sfft.h sfft_execute_group)."""
+    """Line-sharded solve of len(plans) shards, or the ranks of a distributed speculation (spec_distributed plans),
+    on ONE device (include/sfft.h sfft_execute_group)."""
     torch = _torch()
     n = len(plans)
     B, p0 = sigs[0].batch, plans[0]
@@ -493,6 +497,16 @@ def exchange_handles(local: bytes, group=None) -> list:
     out = [None] * dist.get_world_size(group)
     dist.all_gather_object(out, local, group=group)
     return out
+
+
+def comm_init_spec_ranks(plan: Plan, group=None) -> None:
+    """Distributed multi-prime speculation (R26) over a torch.distributed group: rank 0 draws the NCCL id, the group
+    broadcasts it, every rank initialises the plan's communicator (shard_mode 2, collective)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [sfft_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    sfft_comm_init(plan, world, rank, shard_mode=2, unique_id=obj[0])
 
 
 def comm_init_line_shards(plan: Plan, group=None, exchange: int = 0) -> None:

@@ -125,7 +125,9 @@ struct sfft_plan_s {
   bool peer_ready = false;
   int32_t peer_epoch = 0;
   cudaEvent_t ev_ctrl = nullptr;   // the per-iteration control read (iter_setup)
-  int32_t spec_G = 1;              // multi-prime speculation (R26): slots per signal; batch counts slots
+  int32_t spec_G = 1;              // multi-prime speculation (R26): primes (record sets) per iteration
+  int32_t spec_slots = 1;          // slots per signal on this GPU (G, or 1 distributed); batch counts slots
+  int32_t spec_dist = 0, spec_rank = 0, spec_tail = 0;
   // sfft_solve_host_batches: the second device input / output set, the H2D and D2H streams and their events
   void* pipe_buf = nullptr;
   size_t pipe_bytes = 0;
@@ -307,7 +309,8 @@ void layout(sfft_plan_t* P) {
   sz[B_I8THI] = P->i8_ok ? 4 * T * (2 * P->p_stride + 8) : 0;
   // decode records (fused FFT epilogue -> commit); line shards also receive every shard's records
   sz[B_RSEND] = 8 * S * (size_t)P->rec_words;
-  sz[B_RRECV] = P->line_G > 0 ? 8 * (size_t)P->line_G * S * (size_t)P->rec_words : 0;
+  sz[B_RRECV] = P->line_G > 0 ? 8 * (size_t)P->line_G * S * (size_t)P->rec_words
+                : P->spec_dist ? 8 * (size_t)P->spec_G * S * (size_t)P->rec_words : 0;
   sz[B_RCAND] = 4 * S * (size_t)P->k;
   sz[B_RNC] = 4 * S;
   sz[B_RF0] = 16 * S * (size_t)P->k;
@@ -407,6 +410,10 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.assign_ready = ptr<int32_t>(P, B_ASGRDY);
   D.spin_err = ptr<int32_t>(P, B_SPINERR);
   D.spec_G = 1;                              // sfft_execute sets the plan's G (stage entry points run single slots)
+  D.spec_slots = 1;
+  D.spec_dist = P->spec_dist;
+  D.spec_rank = P->spec_rank;
+  D.spec_tail = P->spec_tail;
   D.spec_touch = P->spec_G > 1 ? ptr<int32_t>(P, B_SPECT) : nullptr;
   D.commit_cnt = ptr<int32_t>(P, B_SPINERR) + 1;
   if (P->i8_ok) {
@@ -437,7 +444,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.rec_words = P->rec_words;
   D.rec_fw = P->rec_fw;
   D.rec_send = ptr<int64_t>(P, B_RSEND);
-  D.rec_recv = P->line_G > 0 ? ptr<int64_t>(P, B_RRECV) : ptr<int64_t>(P, B_RSEND);   // unsharded: own records
+  D.rec_recv = P->line_G > 0 || P->spec_dist ? ptr<int64_t>(P, B_RRECV) : ptr<int64_t>(P, B_RSEND);   // unsharded: own
   D.L_ref = P->L_ref;
   D.peer_mode = 0;
   if (P->line_exchange == 1 && P->peer_ready) {
@@ -603,7 +610,7 @@ int solve_begin(sfft_plan_t* P, DevParams& D, const sfft_signal_t* sig, int& lau
   cudaStream_t st = P->stream;
   CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_CTRL), 0, 64, st));   // both control blocks
   CUDA_TRY(P, cudaMemsetAsync(ptr<int32_t>(P, B_SPINERR), 0, 4 * (1 + (size_t)P->batch), st));
-  const int slots = sig->batch * D.spec_G;   // R26: G slots per signal, the projection maps slot -> signal
+  const int slots = sig->batch * D.spec_slots;   // R26: G slots per signal, the projection maps slot -> signal
   if (D.spec_G > 1)
     CUDA_TRY(P, cudaMemsetAsync(D.spec_touch, 0, 4 * (size_t)slots * P->k, st));
   LAUNCH(P, launch_project(D, slots, sig->freqs, sig->coeffs, st));
@@ -765,8 +772,8 @@ int iter_back(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, const 
     }
   }
   if (P->n_levels > 1) {                 // signals that switched fallback level (reading R23)
-    LAUNCH(P, launch_retilt(D, sig->batch * D.spec_G, sig->freqs, st));
-    if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch * D.spec_G, P->k, st, true));
+    LAUNCH(P, launch_retilt(D, sig->batch * D.spec_slots, sig->freqs, st));
+    if (P->i8_ok) LAUNCH(P, launch_i8_prepare(D, sig->batch * D.spec_slots, P->k, st, true));
   }
   return SFFT_OK;
 }
@@ -779,7 +786,7 @@ int solve_report(sfft_plan_t* P, const DevParams& D, int32_t batch, const int32_
   int32_t spin_err = 0;
   CUDA_TRY(P, cudaMemcpyAsync(hs.data(), ostat, 4 * (size_t)batch, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(P, cudaMemcpyAsync(&spin_err, D.spin_err, 4, cudaMemcpyDeviceToHost, st));
-  const int G = std::max(1, (int)D.spec_G);
+  const int G = std::max(1, (int)D.spec_slots);
   const size_t slots = (size_t)batch * G;       // per-slot counters (R26: G slots per signal, all summed)
   std::vector<int64_t> hsamp(slots), hcm(slots), hcm8(slots);
   std::vector<double> hfw(2 * slots);
@@ -922,13 +929,18 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
     if (opt->line_exchange == 1 && (opt->line_shards < 1 || opt->line_shards > kMaxPeers)) return SFFT_EINVAL;
     P->line_exchange = opt->line_exchange;
     if (opt->spec_primes < 0 || opt->spec_primes > 16) return SFFT_EINVAL;
+    if (opt->spec_distributed && (opt->spec_primes < 2 || opt->spec_rank < 0 || opt->spec_rank >= opt->spec_primes))
+      return SFFT_EINVAL;
     if (opt->spec_primes > 1) {
-      // R26: G slots per signal (each its own prime and registry copy); not with line shards (their records are
-      // per line, not per prime), the literal residual or an explicit batch of slots beyond 2^20
+      // R26: G slots per signal (each its own prime and registry copy) or one per rank; not with line shards (their
+      // records are per line, not per prime), the literal residual or an explicit batch of slots beyond 2^20
       if (opt->line_shards > 0 || opt->literal_residual || (int64_t)P->batch * opt->spec_primes > (1 << 20))
         return SFFT_EINVAL;
       P->spec_G = opt->spec_primes;
-      P->batch *= P->spec_G;
+      P->spec_dist = opt->spec_distributed ? 1 : 0;
+      P->spec_rank = P->spec_dist ? opt->spec_rank : 0;
+      P->spec_slots = P->spec_dist ? 1 : P->spec_G;
+      P->batch *= P->spec_slots;
     }
   }
   // partition: explicit, or uniform largest d1 | d with N^d1 <= 2^40
@@ -961,6 +973,10 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   }
   P->rec_fw = (k + 1) / 2;
   P->rec_words = P->rec_fw + (P->L_ref - 1) * k;
+  if (P->spec_dist) {            // R26 distributed: + (nc, p, m) header, candidate bins, F_0 at them
+    P->spec_tail = P->rec_words;
+    P->rec_words += 2 + (k + 1) / 2 + 2 * k;
+  }
   int64_t B = 1;
   int32_t off = 0;
   for (int q = 0; q < P->r; ++q) {
@@ -1222,8 +1238,8 @@ void sfft_plan_destroy(sfft_plan_t* plan) {
 int sfft_signal_expsum(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, const double* coeffs,
                        sfft_signal_t** out) {
   if (!plan || !out || !freqs || !coeffs) return SFFT_EINVAL;
-  if (batch < 1 || batch > plan->batch / plan->spec_G)
-    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_G);
+  if (batch < 1 || batch > plan->batch / plan->spec_slots)
+    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_slots);
   sfft_signal_t* s = new (std::nothrow) sfft_signal_t();
   if (!s) return SFFT_ENOMEM;
   s->plan = plan;
@@ -1243,13 +1259,17 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
     return fail(plan, SFFT_EINVAL, "fused record exchange needs sfft_comm_init_peers or sfft_execute_group");
   if (plan->line_exchange == 0 && plan->line_G > 1 && !plan->nccl_comm)
     return fail(plan, SFFT_EINVAL, "line-sharded plan (%d shards) needs sfft_comm_init or sfft_execute_group", plan->line_G);
+  if (plan->spec_dist && !plan->nccl_comm)
+    return fail(plan, SFFT_EINVAL, "distributed speculation (%d ranks) needs sfft_comm_init or sfft_execute_group",
+                plan->spec_G);
   int rc = ensure_ready(plan);
   if (rc) return rc;
   sfft_plan_t* P = plan;
   cudaStream_t st = P->stream;
   const int32_t batch = sig->batch;                 // signals; slots = batch G (R26)
-  DevParams D = dev_params(P, batch * P->spec_G);
+  DevParams D = dev_params(P, batch * P->spec_slots);
   D.spec_G = P->spec_G;
+  D.spec_slots = P->spec_slots;
   int launches = 0;
   // profiling: event marks on the stream, 5 per iteration (prep | expsum | pfft | decode)
   size_t n_ev = 0;
@@ -1268,7 +1288,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   int iter = 1;
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
   std::vector<size_t> it_marks, it_i8;
-  int n_bound = batch * P->spec_G;
+  int n_bound = batch * P->spec_slots;
   for (; iter <= P->max_iter; ++iter) {
     IterPlan it;
     if ((rc = iter_setup(P, D, iter, &it, launches, n_bound))) return rc;
@@ -1286,6 +1306,10 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
         CUDA_TRY(P, cudaMemcpyAsync(ptr<int64_t>(P, B_RRECV), ptr<int64_t>(P, B_RSEND), 8 * words,
                                     cudaMemcpyDeviceToDevice, st));
       }
+    } else if (P->spec_dist) {
+      // R26 distributed: every rank's records (with their tails) to every rank; the commits merge them in rank order
+      if ((rc = nccl_allgather(P, ptr<int64_t>(P, B_RSEND), ptr<int64_t>(P, B_RRECV), (size_t)batch * P->rec_words)))
+        return rc;
     }
     if ((rc = iter_back(P, D, iter, it, sig, launches))) return rc;
     ++n_expsum;
@@ -1346,10 +1370,14 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
   sfft_plan_t* P0 = plans[0];
   if (!P0) return SFFT_EINVAL;
   const int G = n_plans;
+  const bool spec = P0->spec_dist != 0;      // R26 distributed: plans = the G ranks of one speculation
   for (int g = 0; g < G; ++g) {
     sfft_plan_t* P = plans[g];
     if (!P || !sigs[g] || sigs[g]->plan != P) return SFFT_EINVAL;
-    if (P->line_G != G || P->line_g != g) return fail(P0, SFFT_EINVAL, "plan %d is not line shard %d of %d", g, g, G);
+    if (spec && (!P->spec_dist || P->spec_G != G || P->spec_rank != g))
+      return fail(P0, SFFT_EINVAL, "plan %d is not speculation rank %d of %d", g, g, G);
+    if (!spec && (P->line_G != G || P->line_g != g))
+      return fail(P0, SFFT_EINVAL, "plan %d is not line shard %d of %d", g, g, G);
     if (P->stream != P0->stream || P->device != P0->device) return fail(P0, SFFT_EINVAL, "shards must share device and stream");
     if (P->k != P0->k || P->r != P0->r || P->d != P0->d || sigs[g]->batch != sigs[0]->batch) return SFFT_EINVAL;
     const int rc = ensure_ready(P);
@@ -1380,6 +1408,7 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
   for (int g = 0; g < G; ++g) plans[g]->n_fused_iters = 0;
   for (int g = 0; g < G; ++g) {
     D[g] = dev_params(plans[g], batch);
+    D[g].spec_G = plans[g]->spec_G;
     if ((rc = solve_begin(plans[g], D[g], sigs[g], launches))) return rc;
   }
   int32_t last_iter = 0, n_expsum = 0, n_expsum_i8 = 0;
@@ -1389,8 +1418,8 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
     std::vector<IterPlan> it(G);
     for (int g = 0; g < G; ++g) {
       if ((rc = iter_setup(plans[g], D[g], iter, &it[g], launches, n_bound))) return rc;
-      if (it[g].n_active != it[0].n_active || it[g].max_p != it[0].max_p)
-        return fail(P0, SFFT_ECORRUPT, "line shards diverged at iteration %d", iter);
+      if (it[g].n_active != it[0].n_active || (!spec && it[g].max_p != it[0].max_p))   // ranks: own primes
+        return fail(P0, SFFT_ECORRUPT, "shards diverged at iteration %d", iter);
     }
     if (it[0].n_active == 0) break;
     n_bound = it[0].n_active;
@@ -1437,13 +1466,18 @@ int sfft_execute_group(sfft_plan_t* const* plans, const sfft_signal_t* const* si
   launches += 2;
   int worst = 0;
   if ((rc = solve_report(P, D[0], batch, ostat, rep, last_iter, launches, n_expsum, n_expsum_i8, &worst))) return rc;
-  if (rep) {            // exp-sum work of every shard
+  if (rep) {            // exp-sum work of every shard (and, for speculation ranks, their own primes' samples)
     for (int g = 1; g < G; ++g) {
-      std::vector<int64_t> hcm(batch), hcm8(batch);
+      std::vector<int64_t> hcm(batch), hcm8(batch), hsm(batch);
       CUDA_TRY(P0, cudaMemcpyAsync(hcm.data(), D[g].st_cmacs, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(P0, cudaMemcpyAsync(hcm8.data(), D[g].st_cmacs_i8, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(P0, cudaMemcpyAsync(hsm.data(), D[g].st_samples, 8 * (size_t)batch, cudaMemcpyDeviceToHost, st));
       CUDA_TRY(P0, cudaStreamSynchronize(st));
-      for (int s = 0; s < batch; ++s) { rep->cmacs += hcm[s]; rep->cmacs_i8 += hcm8[s]; }
+      for (int s = 0; s < batch; ++s) {
+        rep->cmacs += hcm[s];
+        rep->cmacs_i8 += hcm8[s];
+        if (spec) rep->samples_used += hsm[s];
+      }
     }
   }
   return worst;
@@ -1453,8 +1487,8 @@ int sfft_solve_host(sfft_plan_t* plan, int32_t batch, const int32_t* freqs, cons
                     int32_t* out_freqs, double* out_coeffs, int32_t* out_count, int32_t* out_status,
                     sfft_report* rep) {
   if (!plan || !freqs || !coeffs || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
-  if (batch < 1 || batch > plan->batch / plan->spec_G)
-    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_G);
+  if (batch < 1 || batch > plan->batch / plan->spec_slots)
+    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_slots);
   int rc = ensure_ready(plan);
   if (rc) return rc;
   sfft_plan_t* P = plan;
@@ -1478,8 +1512,8 @@ int sfft_solve_host_batches(sfft_plan_t* plan, int32_t n_batches, int32_t batch,
                             const double* coeffs, int32_t* out_freqs, double* out_coeffs, int32_t* out_count,
                             int32_t* out_status, sfft_report* rep) {
   if (!plan || n_batches < 1 || !freqs || !coeffs || !out_freqs || !out_coeffs || !out_count) return SFFT_EINVAL;
-  if (batch < 1 || batch > plan->batch / plan->spec_G)
-    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_G);
+  if (batch < 1 || batch > plan->batch / plan->spec_slots)
+    return fail(plan, SFFT_EDIM, "batch %d outside [1, %d]", batch, plan->batch / plan->spec_slots);
   int rc = ensure_ready(plan);
   if (rc) return rc;
   sfft_plan_t* P = plan;
@@ -1718,10 +1752,12 @@ int sfft_comm_init_peers(sfft_plan_t* plan, int32_t nranks, int32_t rank, const 
 int sfft_comm_init(sfft_plan_t* plan, int32_t nranks, int32_t rank, const void* nccl_unique_id, int32_t shard_mode) {
   if (!plan || nranks < 1 || rank < 0 || rank >= nranks) return SFFT_EINVAL;
   if (shard_mode == 0) return SFFT_OK;   // signal sharding: independent solves, no communicator
-  if (shard_mode != 1 || !nccl_unique_id) return SFFT_EINVAL;
-  if (plan->line_G != nranks || plan->line_g != rank)
+  if ((shard_mode != 1 && shard_mode != 2) || !nccl_unique_id) return SFFT_EINVAL;
+  if (shard_mode == 1 && (plan->line_G != nranks || plan->line_g != rank))
     return fail(plan, SFFT_EINVAL, "plan is line shard %d of %d, communicator rank %d of %d", plan->line_g,
                 plan->line_G, rank, nranks);
+  if (shard_mode == 2 && (!plan->spec_dist || plan->spec_G != nranks || plan->spec_rank != rank))
+    return fail(plan, SFFT_EINVAL, "plan is not speculation rank %d of %d", rank, nranks);
   if (plan->nccl_comm) return fail(plan, SFFT_EINVAL, "communicator already initialised");
   const NcclApi& n = nccl_api();
   if (!n.ok) return fail(plan, SFFT_ENCCL, "libnccl.so.2 not loadable");

@@ -229,7 +229,7 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   // prime of the iteration and its own copy of the registry; every slot merges all G record sets in prime order
   // into its copy (so the copies stay identical), skipping keys an earlier set of the iteration updated
   const int G = SPEC ? P.spec_G : 1;
-  const int s0 = s - s % G;
+  const int s0 = SPEC && !P.spec_dist ? s - s % G : s;
   const int p_own = P.st_p[s];
   const int nR0 = P.st_nR[s];
   int nR = nR0;
@@ -248,21 +248,32 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
   if (P.peer_mode) peer_wait_lines(P, s);        // the records of every shard's lines are in (fused exchange)
   int na_all = 0, nR_final = nR0;
   for (int gs = 0; gs < G; ++gs) {
-    const int sr = s0 + gs;                               // the slot whose prime's records this set holds
-    const int p = P.st_p[sr], m = P.st_m[sr];
+    // the set: this slot's own records (Alg. 2), a sibling slot's (R26 on one GPU) or rank gs's from the
+    // all-gathered records with their tail (R26 distributed)
+    const int sr = SPEC && !P.spec_dist ? s0 + gs : s;
+    const int64_t* sbase = SPEC && P.spec_dist ? P.rec_recv + ((int64_t)gs * P.batch + s) * P.rec_words
+                                               : P.rec_recv + (int64_t)sr * P.rec_words;
+    const int32_t* stail = reinterpret_cast<const int32_t*>(sbase + P.spec_tail);
+    const bool dist = SPEC && P.spec_dist;
+    const int p = dist ? stail[1] : P.st_p[sr], m = dist ? stail[2] : P.st_m[sr];
+    const int32_t* cand_src = dist ? stail + 4 : P.rec_cand + (int64_t)sr * P.k;
+    const double* f0_src = dist ? reinterpret_cast<const double*>(sbase + P.spec_tail + 2 + (P.k + 1) / 2)
+                                : reinterpret_cast<const double*>(P.rec_f0 + (int64_t)sr * P.k);
     // ---- commit: candidates of line 0, flags ANDed over the line shards, coordinates unpacked ----
-    nc = P.rec_nc[sr];
+    nc = dist ? stail[0] : P.rec_nc[sr];
     for (int ci = tid; ci < nc; ci += blockDim.x) {
-      cand[ci] = P.rec_cand[(int64_t)sr * P.k + ci];
+      cand[ci] = cand_src[ci];
       int f = 1;
-      for (int g = 0; g < P.line_G; ++g)
-        f &= reinterpret_cast<const int32_t*>(P.rec_recv + ((int64_t)g * P.batch + sr) * P.rec_words)[ci];
+      if (SPEC) f = reinterpret_cast<const int32_t*>(sbase)[ci];
+      else
+        for (int g = 0; g < P.line_G; ++g)
+          f &= reinterpret_cast<const int32_t*>(P.rec_recv + ((int64_t)g * P.batch + sr) * P.rec_words)[ci];
       flag[ci] = f;
     }
     __syncthreads();
-    if (P.line_G == 1) {
+    if (SPEC || P.line_G == 1) {
       // one shard holds every axis: its record already is the [r][k] coordinate array
-      accv = const_cast<int64_t*>(P.rec_recv) + (int64_t)sr * P.rec_words + P.rec_fw;   // read-only below
+      accv = const_cast<int64_t*>(sbase) + P.rec_fw;   // read-only below
     } else {
       for (int g = 0; g < P.line_G; ++g) {
         int glo, ghi;
@@ -427,7 +438,7 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
       n_new = min(total, P.k - nR);
       for (int t = t0; t < t1; ++t) {
         const int ci = accl[t];
-        const double2 f0 = P.rec_f0[(int64_t)sr * P.k + ci];   // F_0 at the candidate (the FFT's line-0 CTA)
+        const double2 f0 = make_double2(f0_src[2 * ci], f0_src[2 * ci + 1]);   // F_0 at the candidate (the FFT's line-0 CTA)
         const double2 a = make_double2(f0.x / (double)p, f0.y / (double)p);    // Eq. (7): a = F_0 / p
         if (found[t] >= 0) {
           const int e = found[t];
@@ -461,7 +472,7 @@ static __device__ __forceinline__ void commit_signal(const DevParams& P, int32_t
           found[t] = e;
           if (e < 0 || (SPEC && spec_skip(P, s, e, iter, gs))) continue;   // first occurrence dropped / key of an earlier set
           const int ci = accl[t];
-          const double2 f0 = P.rec_f0[(int64_t)sr * P.k + ci];
+          const double2 f0 = make_double2(f0_src[2 * ci], f0_src[2 * ci + 1]);
           areg[e] = make_double2(areg[e].x + f0.x / (double)p, areg[e].y + f0.y / (double)p);
           found[t] = e;
         }

@@ -36,7 +36,7 @@ __global__ void setup_kernel(DevParams P, int32_t iter, int32_t seq) {
     const int il = P.st_il[s] + 1;                         // counter of the current level (= iter without a switch)
     P.st_il[s] = il;
     // prime counter: il (Alg. 2 l.8); with G-prime speculation (R26) slot s takes counter (il - 1) G + s % G + 1
-    const int ic = P.spec_G > 1 ? (il - 1) * P.spec_G + s % P.spec_G + 1 : il;
+    const int ic = P.spec_G <= 1 ? il : (il - 1) * P.spec_G + (P.spec_dist ? P.spec_rank : s % P.spec_G) + 1;
     int p;
     if (P.n_sched > 0) p = (int)P.sched[(ic - 1) % P.n_sched];
     else p = ith_prime_at_least(P, P.c * kstar, ic);
@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(1024) retilt_kernel(DevParams P, const int32_t
   double2* Cs = P.C_all + (int64_t)s * kk * P.Lp;
   // 1. signal terms (warp per term)
   for (int j = warp; j < P.k; j += nwarps) {
-    const int32_t* w = freqs + ((int64_t)(P.spec_G > 1 ? s / P.spec_G : s) * P.k + j) * P.d;   // input of slot s
+    const int32_t* w = freqs + ((int64_t)(P.spec_slots > 1 ? s / P.spec_slots : s) * P.k + j) * P.d;   // slot's input
     for (int q = lane; q < r; q += 32) {
       const int off = P.block_off[q], dq = P.block_dims[q];
       int64_t acc = 0, pw = 1;

@@ -836,14 +836,30 @@ __device__ void fused_select(const DevParams& P, int s, int p, double2* x, const
   const int nc = select_candidates([&](int b) { return x[b]; }, p, P.k - nR, P.floor_rel * pd, cand, mag, flag,
                                    scratch);
   int32_t* sendf = reinterpret_cast<int32_t*>(P.rec_send + (int64_t)s * P.rec_words);
+  // distributed speculation (R26): the record's tail carries (nc, p, m), the bins and F_0 at them for the ranks
+  int64_t* tail = P.spec_dist ? P.rec_send + (int64_t)s * P.rec_words + P.spec_tail : nullptr;
   for (int ci = tid; ci < nc; ci += blockDim.x) {
     const int b = cand[ci];
     P.rec_cand[(int64_t)s * P.k + ci] = b;
     P.rec_f0[(int64_t)s * P.k + ci] = x[b];
     if (P.peer_mode) peer_put_flag(P, s, ci, 1);
     else sendf[ci] = 1;
+    if (tail) {
+      reinterpret_cast<int32_t*>(tail + 2)[ci] = b;
+      double* f0t = reinterpret_cast<double*>(tail + 2 + (P.k + 1) / 2);
+      f0t[2 * ci] = x[b].x;
+      f0t[2 * ci + 1] = x[b].y;
+    }
   }
-  if (tid == 0) P.rec_nc[s] = nc;
+  if (tid == 0) {
+    P.rec_nc[s] = nc;
+    if (tail) {
+      int32_t* h = reinterpret_cast<int32_t*>(tail);
+      h[0] = nc;
+      h[1] = p;
+      h[2] = P.st_m[s];
+    }
+  }
   // fused exchange: the flags just stored in the peers' memory must land before the line-n CTAs' clears, which
   // follow their acquire of sel_ready -- every thread fences at system scope, the release is system scope
   if (P.peer_mode) __threadfence_system();

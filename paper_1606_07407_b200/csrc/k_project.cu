@@ -29,7 +29,7 @@ __global__ void __launch_bounds__(256) project_kernel(DevParams P, int32_t batch
   int64_t* vs = P.v_all + (int64_t)s * P.r * P.kk;
   const int64_t vstr = SMEM ? 1 : P.kk;
   int64_t* vsm = SMEM ? vsm_all + (int64_t)(threadIdx.x >> 5) * P.r : vs + j;
-  const int si = P.spec_G > 1 ? s / P.spec_G : s;              // the input signal of slot s (R26)
+  const int si = P.spec_slots > 1 ? s / P.spec_slots : s;      // the input signal of slot s (R26)
   const int32_t* w = freqs + ((int64_t)si * P.k + j) * P.d;
   for (int q = lane; q < P.r; q += 32) {
     const int off = P.block_off[q], dq = P.block_dims[q];

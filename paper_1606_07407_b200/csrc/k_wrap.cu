@@ -25,9 +25,9 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(gt & (G - 1));
   const int64_t gw = gt / G;
-  if (gw >= (int64_t)(P.batch / P.spec_G) * P.k) return;   // signals (R26: P.batch counts G slots each)
+  if (gw >= (int64_t)(P.batch / P.spec_slots) * P.k) return;   // signals (R26: P.batch counts G slots each)
   const int s = (int)(gw / P.k), e = (int)(gw % P.k);
-  const int sl = s * P.spec_G;                         // the signal's (first) slot (R26: G identical copies)
+  const int sl = s * P.spec_slots;                         // the signal's (first) slot (R26: G identical copies)
   if (e >= P.st_nR[sl]) return;
   const int64_t* vreg = P.v_all + (int64_t)sl * P.r * P.kk + P.k;
   int32_t* row = P.wtmp + ((int64_t)s * P.k + e) * P.d;
@@ -86,7 +86,7 @@ __global__ void wrap_rank_packed_kernel(DevParams P, int32_t* __restrict__ perm,
   int* ord = reinterpret_cast<int*>(key + (size_t)nchs * P.k);                   // [power of two >= k]
   __shared__ int any_tie;
   const int s = blockIdx.x, tid = threadIdx.x;
-  const int nR = P.st_nR[s * P.spec_G];
+  const int nR = P.st_nR[s * P.spec_slots];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
   const int64_t h2 = P.N / 2;
   auto build = [&](int c0, int c1) {                         // chunks [c0, c1) of every row, chunk index fastest
@@ -174,7 +174,7 @@ __global__ void wrap_rank_kernel(DevParams P, int32_t* __restrict__ perm) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned long long* key = reinterpret_cast<unsigned long long*>(smem_raw);    // [k]
   const int s = blockIdx.x, tid = threadIdx.x;
-  const int nR = P.st_nR[s * P.spec_G];
+  const int nR = P.st_nR[s * P.spec_slots];
   const int32_t* wt = P.wtmp + (int64_t)s * P.k * P.d;
   const int64_t h2 = P.N / 2;
   for (int e = tid; e < nR; e += blockDim.x) {
@@ -210,9 +210,9 @@ __global__ void wrap_gather_kernel(DevParams P, const int32_t* __restrict__ perm
   const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = (int)(gt & (G - 1));
   const int64_t gw = gt / G;
-  if (gw >= (int64_t)(P.batch / P.spec_G) * P.k) return;   // signals (R26: P.batch counts G slots each)
+  if (gw >= (int64_t)(P.batch / P.spec_slots) * P.k) return;   // signals (R26: P.batch counts G slots each)
   const int s = (int)(gw / P.k), i = (int)(gw % P.k);
-  const int sl = s * P.spec_G;
+  const int sl = s * P.spec_slots;
   const int nR = P.st_nR[sl];
   int32_t* of = out_freqs + ((int64_t)s * P.k + i) * P.d;
   if (i < nR) {

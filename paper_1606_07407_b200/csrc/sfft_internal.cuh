@@ -158,9 +158,14 @@ struct DevParams {
   // commit CTA: the commit lists the touched entries and appends work items (32 entries x 16 lines) counted in
   // ctrl[5]
   int32_t crow_mode;           // launch flag of the commit kernel (0: the commit writes the rows itself)
-  // multi-prime speculation (reading R26): slot s holds signal s / spec_G with the prime of counter
-  // (i - 1) spec_G + s % spec_G + 1; the commit merges the spec_G sibling slots' records
+  // multi-prime speculation (reading R26): G primes per iteration, the commit merging G record sets.  On one GPU
+  // (spec_slots = G) slot s holds signal s / G with the prime of counter (i - 1) G + s % G + 1 and the sets are the
+  // sibling slots'; distributed (spec_dist, spec_slots = 1) rank spec_rank holds counter (i - 1) G + spec_rank + 1
+  // and the sets arrive by the all-gather of every rank's records, whose tail (word spec_tail) carries the
+  // candidate count, p, m, the candidate bins and F_0 there
   int32_t spec_G;              // 1 = Alg. 2 as written
+  int32_t spec_slots;          // slots per signal on this GPU (G, or 1 when distributed)
+  int32_t spec_dist, spec_rank, spec_tail;
   int32_t* spec_touch;         // [slots][k] (iteration << 4) | set of the last update of entry e
   int32_t crow_nl;             // 16-line chunks per row, ceil(Lp / 16)
   int4* crow_items;            // [batch * ceil(k / 32) * crow_nl] (signal, entry chunk, line chunk, touched count)

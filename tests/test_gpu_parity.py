@@ -300,10 +300,44 @@ def test_e2e_speculation_stall_fallback_vs_oracle(S, d, N, k, blocks, structure,
     assert res.report.samples_used == samples and res.report.fallback_used > 0
 
 
+@pytest.mark.parametrize("name,trials,G,path", [("c2", range(8), 2, 0), ("c2", range(4), 3, 0), ("c3", [0], 2, 0),
+                                                ("c3", [1], 4, 1), ("c5", [0], 4, 0)])
+def test_e2e_speculation_distributed_ranks(S, name, trials, G, path):
+    """R26 distributed: G plans, rank g sampling only its own prime of each iteration, the ranks' records (with the
+    tail of candidate count, p, m, bins, F_0) all-gathered and merged in rank order by every rank
+    (sfft_execute_group: the ranks on one GPU, the all-gather device copies; the call fails unless every rank's
+    registry is bitwise identical).  Equals the one-GPU speculation (G slots per signal) -- sets, per-signal
+    statuses, iterations, samples bit for bit; coefficients within 1e-9 (iterations on the FP64 exp-sum, small
+    primes included, split their terms by the number of active slots, so the summation order differs) -- and
+    recovers the input."""
+    c = W.CONFIGS[name]
+    trials = list(trials)
+    w, a = W.make_batch(c, trials)
+    wd, ad = torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda()
+    plans = [_plan(S, c, batch=len(trials), spec_primes=G, spec_distributed=1, spec_rank=g, expsum_path=path)
+             for g in range(G)]
+    sigs = [S.sfft_signal_expsum(p, wd, ad) for p in plans]
+    res = S.sfft_execute_group(plans, sigs)
+    ref = S.solve(_plan(S, c, batch=len(trials), spec_primes=G, expsum_path=path), wd, ad)
+    assert torch.equal(res.freqs, ref.freqs) and torch.equal(res.count, ref.count)
+    for i in range(len(trials)):
+        assert _coef_ok(res.coeffs[i].cpu().numpy(), ref.coeffs[i].cpu().numpy())
+    assert torch.equal(res.per_status, ref.per_status) and res.status == ref.status == S.SFFT_OK
+    assert res.report.iterations == ref.report.iterations
+    assert res.report.samples_used == ref.report.samples_used
+    assert [res.report.primes[i] for i in range(res.report.n_iter_logged)] == \
+        [ref.report.primes[i] for i in range(ref.report.n_iter_logged)]
+    for i in range(len(trials)):
+        assert np.array_equal(res.freqs[i].cpu().numpy(), W.canonical_sort(w[i], a[i])[0])
+    with pytest.raises(S.SfftError):                        # a rank alone has no communicator
+        S.solve(plans[0], wd, ad)
+
+
 def test_speculation_options_validated(S):
     c = W.CONFIGS["c2"]
     for kw in (dict(spec_primes=17), dict(spec_primes=-1), dict(spec_primes=2, line_shards=2, line_rank=0),
-               dict(spec_primes=2, literal_residual=True)):
+               dict(spec_primes=2, literal_residual=True), dict(spec_primes=1, spec_distributed=1),
+               dict(spec_primes=2, spec_distributed=1, spec_rank=2)):
         with pytest.raises(S.SfftError) as e:
             _plan(S, c, batch=2, **kw)
         assert e.value.status == S.SFFT_EINVAL
