@@ -72,6 +72,62 @@ __global__ void wrap_digits_kernel(DevParams P, int32_t* __restrict__ bad, int G
   if (err) bad[s] = 1;
 }
 
+// The same digits with coalesced traffic: a CTA takes 32 entries of one signal, lanes along the entries (the reads
+// vreg[q][e0 + lane] of one block q are one 256-B segment), warps along the blocks; the digit rows are staged in
+// shared memory (row stride dp = d | 1 words: conflict-free) and stored as whole rows.  Used for rows up to ~380
+// coordinates (48 KB of tile).
+__global__ void __launch_bounds__(256) wrap_digits_tiled_kernel(DevParams P, int32_t* __restrict__ bad, int dp) {
+  extern __shared__ int32_t rows[];                      // [32][dp]
+  const int s = blockIdx.y, e0 = blockIdx.x * 32;
+  const int sl = s * P.spec_slots;
+  const int nR = P.st_nR[sl];
+  if (e0 >= nR) return;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int e = e0 + lane;
+  const bool live = e < nR;
+  const int64_t* vreg = P.v_all + (int64_t)sl * P.r * P.kk + P.k;
+  const int64_t N = P.N, h2 = N / 2;
+  const double invN = 1.0 / (double)N;
+  const int lgN = (N & (N - 1)) == 0 ? __ffsll(N) - 1 : -1;
+  const int lvl = P.st_lvl[sl];
+  const int32_t* axt = P.lvl_axt + (int64_t)lvl * P.r;
+  const int64_t* tl = P.lvl_tilts + (int64_t)lvl * P.lvl_tmax * 5;
+  int32_t* row = rows + lane * dp;
+  int err = 0;
+  for (int q = warp; q < P.r; q += nw) {
+    int64_t u = live ? vreg[(int64_t)q * P.kk + e] : 0;
+    const int at = axt[q];
+    if (at >= 0 && live) {
+      const int64_t* T = tl + 5 * (at >> 1);
+      const int64_t v0 = vreg[T[0] * P.kk + e], v1 = vreg[T[1] * P.kk + e];
+      const int64_t b = T[2], h = T[3], c2 = T[4] * T[4];
+      const int64_t num = (at & 1) ? (-h * v0 + b * v1) : (b * v0 + h * v1);
+      if (num % c2 != 0) { err = 1; u = 0; }
+      else u = num / c2;
+    }
+    const int dq = P.block_dims[q], off = P.block_off[q];
+    int64_t geo = 0, pw = 1;
+    for (int t = 0; t < dq; ++t) { geo += pw; pw *= N; }
+    if (live && (u < -h2 * geo || u > (h2 - 1) * geo)) { err = 1; u = 0; }
+    for (int t = 0; t < dq; ++t) {
+      const int64_t x = u + h2;
+      int64_t qn;
+      if (lgN >= 0) qn = x >> lgN;
+      else qn = floordiv(x, N, invN);
+      row[off + t] = (int32_t)(x - qn * N - h2);         // balanced digit
+      u = qn;                                            // (u - digit) / N
+    }
+  }
+  if (err) bad[s] = 1;
+  __syncthreads();
+  const int nrow = min(32, nR - e0);
+  int32_t* out = P.wtmp + ((int64_t)s * P.k + e0) * P.d;
+  for (int i = threadIdx.x; i < nrow * P.d; i += blockDim.x) {
+    const int rr = i / P.d, c = i - rr * P.d;
+    out[i] = rows[rr * dp + c];
+  }
+}
+
 // lexicographic order of the entries -> perm[s][rank] = entry.  Rows packed into fixed-width 64-bit chunks
 // (coordinate + N/2 in `bits` bits, `per` coordinates per chunk, most significant first): chunk sequences compare
 // like the rows.  A bitonic sort of the entry indices (a power of two >= nR slots, padding last) first by chunk 0
@@ -250,7 +306,17 @@ cudaError_t launch_wrap(const DevParams& P, int32_t n_signals, int32_t* out_freq
   const int64_t warps = (int64_t)n_signals * P.k;
   int G = 1;
   while (G < 32 && G < P.r) G <<= 1;
-  wrap_digits_kernel<<<(unsigned)((warps * G + 255) / 256), 256, 0, st>>>(P, bad, G);
+  const int dp = P.d | 1;
+  const size_t tsm = sizeof(int32_t) * 32 * (size_t)dp;
+  // tiles while several CTAs share an SM (C3, d = 100: wrap 0.133 -> 0.123 ms); long rows (C4, d = 1000: 128 KB
+  // per tile, one CTA per SM) measured 0.12 ms slower than the lane-group kernel
+  if (tsm <= 48 * 1024 && !getenv("SFFT_WRAP_LANES")) {
+    e = ensure_smem(wrap_digits_tiled_kernel, tsm);
+    if (e != cudaSuccess) return e;
+    wrap_digits_tiled_kernel<<<dim3((unsigned)((P.k + 31) / 32), (unsigned)n_signals), 256, tsm, st>>>(P, bad, dp);
+  } else {
+    wrap_digits_kernel<<<(unsigned)((warps * G + 255) / 256), 256, 0, st>>>(P, bad, G);
+  }
   int bits = 1;
   while (((int64_t)1 << bits) < P.N) ++bits;
   const int per = 64 / bits, nch = (P.d + per - 1) / per;
