@@ -66,10 +66,12 @@ def parse():
                     help="single-solve latency also with G-prime speculation (reading R26) for each G")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
-    ap.add_argument("--shard", default="signals", choices=["signals", "lines"],
+    ap.add_argument("--shard", default="signals", choices=["signals", "lines", "spec"],
                     help="signals: independent signal shards per rank (weak scaling, default); lines: every rank "
                          "solves the same signals and owns a shard of the shifted lines (strong scaling, NCCL "
-                         "record all-gather per iteration, SURVEY 8(e))")
+                         "record all-gather per iteration, SURVEY 8(e)); spec: every rank solves the same signals "
+                         "with its own prime of each iteration, records all-gathered and merged in rank order "
+                         "(multi-prime speculation, DESIGN reading R26; world 1 = Alg. 2)")
     ap.add_argument("--exchange", default="allgather", choices=["allgather", "fused"],
                     help="--shard lines: records all-gathered after the FFT (NCCL) or stored into every shard's memory "
                          "by the FFT epilogue itself (line_exchange = 1, CUDA IPC peer mappings)")
@@ -294,7 +296,8 @@ def main():
     from paper_1606_07407_b200.shard import shard_indices
     cfg = W.CONFIGS[args.config]
     T = args.batch or cfg.trials
-    lines = args.shard == "lines"
+    spec = args.shard == "spec" and world > 1
+    lines = args.shard == "lines" or spec              # every rank solves the same signals
     mult = 1 if lines else world                        # signal sets solved per step across the job
     # signal shards: each rank its own independent signals; line shards: every rank the same signals
     trials = list(range(T)) if lines else shard_indices(world * T, world, rank)
@@ -305,6 +308,12 @@ def main():
     stream = torch.cuda.current_stream()
 
     def make_plan(path, batch=T, profile=True, shard=True):
+        if spec and shard:
+            p = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=batch, profile=profile, expsum_path=path,
+                            table_cache_slots=args.table_cache, spec_primes=world, spec_distributed=1,
+                            spec_rank=rank)
+            S.comm_init_spec_ranks(p)
+            return p
         fused = lines and shard and args.exchange == "fused"
         p = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=batch, profile=profile, expsum_path=path,
                         line_shards=world if (lines and shard) else 0, line_rank=rank if (lines and shard) else 0,
@@ -593,7 +602,9 @@ def main():
             "config": {"workload": workload_desc(cfg),
                        "signals_per_gpu_per_step": T,
                        "table_cache_slots": args.table_cache or f"plan default max(batch + 16, 512) = {max(T + 16, 512)}",
-                       "parallelism": (f"line shards x{world} (" + ("records stored into every shard's memory by the FFT "
+                       "parallelism": (f"prime-speculation ranks x{world} (one prime of each iteration per rank, NCCL "
+                                       "record all-gather, merge in rank order)" if spec else
+                                       f"line shards x{world} (" + ("records stored into every shard's memory by the FFT "
                                        "epilogue, CUDA IPC peer mappings" if args.exchange == "fused" else
                                        "NCCL record all-gather") + ")") if lines else f"signal shards x{world}",
                        "l2": "256 MB L2 flush between timed steps; per-step working set > 1 GB"},
