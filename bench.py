@@ -489,8 +489,12 @@ def main():
     if args.spec_primes and not lines and args.spec_steps:
         spec_b = {}
         for G in args.spec_primes:
-            planG = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, expsum_path=args.expsum_path,
-                                table_cache_slots=args.table_cache, spec_primes=G)
+            try:
+                planG = S.sfft_plan(cfg.d, cfg.N, cfg.k, blocks=cfg.blocks, batch=T, expsum_path=args.expsum_path,
+                                    table_cache_slots=args.table_cache, spec_primes=G)
+            except S.SfftError as e:          # e.g. C2: 1024 signals x 8 slots beyond the slot-assignment bound
+                spec_b[f"G{G}"] = {"unsupported": str(e)}
+                continue
             sigG = S.sfft_signal_expsum(planG, w_d, a_d)
             outsG = tuple(torch.empty_like(o) for o in outs)
             for _ in range(args.warmup):

@@ -39,7 +39,8 @@ typedef enum {
   SFFT_ECUDA = -5,
   SFFT_ENOMEM = -6,
   SFFT_ENCCL = -7,
-  SFFT_ENOTSUP = -8        /* prime larger than the FFT size table supports */
+  SFFT_ENOTSUP = -8        /* prime larger than the FFT size table supports; or (sfft_plan) more than ~8000 slots
+                              (batch x spec_primes, or table_cache_slots) for the slot assignment's hash map */
 } sfft_status;
 
 /* Eq. (25)/(27) tilt of the reduced-axis pair (axis0, axis1): sin = height/hypo, cos = base/hypo.

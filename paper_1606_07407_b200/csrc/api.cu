@@ -888,7 +888,7 @@ const char* sfft_strerror(int s) {
     case SFFT_ECUDA: return "CUDA error";
     case SFFT_ENOMEM: return "out of device memory";
     case SFFT_ENCCL: return "NCCL error";
-    case SFFT_ENOTSUP: return "prime beyond the supported FFT size";
+    case SFFT_ENOTSUP: return "not supported (prime beyond the FFT size table, or more plan slots than the slot assignment holds)";
   }
   return "unknown status";
 }
@@ -1187,6 +1187,13 @@ int sfft_plan(int32_t d, int64_t N, int32_t k, const int64_t* primes, int32_t n_
   // per slot at p_cap ~ 7056)
   P->n_tslots = std::max(P->batch + 16, kDefaultTableSlots);
   if (opt && opt->table_cache_slots > 0) P->n_tslots = std::max(P->batch + 16, (int)opt->table_cache_slots);
+  {
+    // the slot assignment keeps a prime -> slot hash map of >= 2 n_tslots entries in one CTA's shared memory
+    // (k_fft.cu assign_slots): about 8000 slots (signals x spec_primes, or table_cache_slots) at most
+    size_t hs = 2048;
+    while (hs < 2 * (size_t)P->n_tslots) hs <<= 1;
+    if (sizeof(int) * (2 * hs + 2 * 4096 + (size_t)P->n_tslots) > (size_t)smem_optin) return SFFT_ENOTSUP;
+  }
   layout(P.get());
   *out = P.release();
   return SFFT_OK;

@@ -341,6 +341,9 @@ def test_speculation_options_validated(S):
         with pytest.raises(S.SfftError) as e:
             _plan(S, c, batch=2, **kw)
         assert e.value.status == S.SFFT_EINVAL
+    with pytest.raises(S.SfftError) as e:                   # 8192 slots: beyond the slot-assignment hash map
+        _plan(S, c, batch=1024, spec_primes=8)
+    assert e.value.status == S.SFFT_ENOTSUP
     plan = _plan(S, c, batch=2, spec_primes=4)
     w, a = W.make_batch(c, range(3))
     with pytest.raises(ValueError):                         # 3 signals in a 2-signal plan (8 slots inside)
