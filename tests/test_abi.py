@@ -32,7 +32,7 @@ def test_library_builds_and_exports_every_declared_symbol():
     for n in _declared():
         assert hasattr(L, n)
     assert S.sfft_version().startswith("sfft sm_100a")
-    assert S.strerror(S.SFFT_ENOTSUP).startswith("prime")
+    assert "prime" in S.strerror(S.SFFT_ENOTSUP)
 
 
 def test_library_is_sm100a_sass():
