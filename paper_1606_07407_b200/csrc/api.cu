@@ -174,6 +174,20 @@ bool is_7smooth(int x) {
   return x == 1;
 }
 
+// FP64 + shared-memory instructions of one radix-R butterfly (dft_small in registers, R - 2 twiddle powers and
+// R - 1 twiddle products, R loads and stores); the fused middle has no twiddles but two DFTs and the V product
+double fft_dft_cost(int R) {
+  switch (R) {
+    case 2: return 4; case 3: return 14; case 4: return 16; case 5: return 36; case 7: return 66; case 8: return 52;
+    case 6: return 48; case 9: return 100; case 10: return 108; case 12: return 128; case 14: return 184;
+    case 15: return 210; case 16: return 188;
+  }
+  return 16.0 * R;
+}
+double fft_bfly_cost(int R, bool mid) {
+  return mid ? 2 * fft_dft_cost(R) + 4 * R + 3 * R : fft_dft_cost(R) + 8 * R - 12 + 2 * R;
+}
+
 FftSize radix_plan(int M) {
   // fewest passes with in-register radices {16,15,14,12,10,9,8,7,6,5,4,3,2} (DP over 2^a 3^b 5^c 7^d),
   // then descending order: the first (largest-Q) pass gets the largest radix -> fewest base twiddles
@@ -192,6 +206,45 @@ FftSize radix_plan(int M) {
   std::vector<int> rs;
   for (int x = M; x > 1; x /= choice[x]) rs.push_back(choice[x]);
   std::sort(rs.begin(), rs.end(), [](int a, int b) { return a > b; });
+  // warp-local plans (pfft_kernel's pass_loop_w): when the launch's warp count W divides M, the first pass takes
+  // radix W (one block-wide pass) and the rest of the plan -- run by each warp on its own M / W points -- is chosen
+  // for lane efficiency: a radix-R pass costs ceil(Mw / R / 32) warp trips of ~fft_bfly_cost(R) instructions
+  const int W = M >= fft_big_m() ? 16 : fft_threads(M, 16 * ((size_t)M + M / 4), 0) / 32;
+  if (!getenv("SFFT_FFT_NO_WLPLAN") && M >= kFftWlMinM && W >= 2 && M % W == 0 && M / W > 1 &&
+      std::find(std::begin(kRad), std::end(kRad), W) != std::end(kRad) && W <= rmax) {
+    const int Mw = M / W;
+    // cost[x][last]: cheapest plan of x points whose last (fused middle) radix is `last` (0: plan of 1)
+    std::vector<double> best_w(Mw + 1, 1e30);
+    std::vector<int> pick(Mw + 1, 0);
+    // middle radix first: the plan of Mw = (passes) x (middle); passes run twice (DIF, DIT), the middle once
+    // + ~40 instructions per warp trip (indices, loop, base twiddle) and ~150 cycles of dependent latency per pass
+    auto trips = [&](int R) { return (double)((Mw / R + 31) / 32); };
+    constexpr double kTrip = 40.0, kPass = 150.0;
+    best_w[1] = 0.0;
+    for (int x = 2; x <= Mw; ++x) {
+      if (Mw % x) continue;
+      for (int R : kRad)
+        if (R <= rmax && x % R == 0 && best_w[x / R] < 1e29) {
+          const double c = best_w[x / R] + 2.0 * (trips(R) * (fft_bfly_cost(R, false) + kTrip) + kPass);
+          if (c < best_w[x]) { best_w[x] = c; pick[x] = R; }
+        }
+    }
+    double bc = 1e30;
+    int bm = 0;
+    for (int R : kRad)
+      if (R <= rmax && Mw % R == 0 && best_w[Mw / R] < 1e29) {
+        const double c = best_w[Mw / R] + trips(R) * (fft_bfly_cost(R, true) + kTrip) + kPass;
+        if (c < bc) { bc = c; bm = R; }
+      }
+    if (bm > 0 && (int)rs.size() > 0) {
+      std::vector<int> sub;
+      for (int x = Mw / bm; x > 1; x /= pick[x]) sub.push_back(pick[x]);
+      std::sort(sub.begin(), sub.end(), [](int a, int b) { return a > b; });
+      rs.assign(1, W);
+      rs.insert(rs.end(), sub.begin(), sub.end());
+      rs.push_back(bm);
+    }
+  }
   // SFFT_FFT_PLAN="M:r1,r2,...;..." overrides the radices of size M (tuning experiments; order as given)
   if (const char* env = getenv("SFFT_FFT_PLAN")) {
     const std::string spec(env), key = std::to_string(M) + ":";
@@ -328,6 +381,12 @@ void layout(sfft_plan_t* P) {
 template <typename T>
 T* ptr(const sfft_plan_t* P, int b) {
   return reinterpret_cast<T*>(static_cast<char*>(P->ws) + P->off[b]);
+}
+
+// warp-local FFT passes for a launch whose largest size is M (SFFT_FFT_NO_WL=1: block-wide passes only)
+bool fft_wl_for(int M) {
+  static const bool no_wl = getenv("SFFT_FFT_NO_WL") != nullptr;
+  return !no_wl && M >= kFftWlMinM;
 }
 
 DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
@@ -736,7 +795,7 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   if (it.fused) D.lines_log = 0;
   const size_t fsm = it.fused ? it.fused_smem : P->fft[it.fi].smem_upto;
   LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)fsm, fft_threads(it.max_M, fsm, (int64_t)it.n_active * P->L), it.big,
-                        it.fused ? 1 : it.ksplit, ptr<double2>(P, B_PART), it.max_p, st));
+                        it.fused ? 1 : it.ksplit, ptr<double2>(P, B_PART), it.max_p, st, fft_wl_for(it.max_M) && !it.fused));
   D.fused_sample = 0;
   D.lines_log = 0;
   D.fuse_decode = 0;
@@ -1653,7 +1712,7 @@ int sfft_stage_pfft(sfft_plan_t* plan, int32_t n_lines, int64_t p, double* x) {
   const int fi = fft_index_host(P, (int)p);
   const int sm = (int)P->fft[fi].smem_upto, th = fft_threads(P->fft[fi].M, P->fft[fi].smem_upto, n_lines), big = P->fft[fi].M >= fft_big_m();
   LAUNCH(P, launch_fft_prep(D, 1, sm, th, big, P->stream, 0, true));
-  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, big, 1, nullptr, 0, P->stream));
+  LAUNCH(P, launch_pfft(D, 1, n_lines, sm, th, big, 1, nullptr, 0, P->stream, fft_wl_for(P->fft[fi].M)));
   CUDA_TRY(P, cudaStreamSynchronize(P->stream));
   return SFFT_OK;
 }

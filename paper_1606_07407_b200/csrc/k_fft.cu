@@ -236,6 +236,64 @@ __device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double
   }
 }
 
+// Warp-local pass: after the first passes of a DIF FFT the array splits into independent blocks (the butterflies
+// of a pass with span S only touch one aligned block of S points).  Once the leading radices' product is a multiple
+// of the warp count W, warp w owns the contiguous region [w Mw, (w + 1) Mw), Mw = M / W, and runs the remaining
+// passes on it with __syncwarp only: the same butterflies with the same twiddles as pass_loop (bitwise identical
+// results), no block barrier, and warps drift out of phase so that one warp's shared-memory loads / stores overlap
+// another's FP64 butterflies.
+template <int R, bool INV>
+__device__ __forceinline__ void pass_loop_w(double2* xw, int Mw, int S, const double2* __restrict__ tb) {
+  const int Q = S / R;
+  const int nb = Mw / R;
+  for (int bi = threadIdx.x & 31; bi < nb; bi += 32) {
+    const int blk = bi / Q, n1 = bi - blk * Q;
+    const int base = blk * S + n1;
+    double2 v[R];
+    bfly_load<R, INV>(xw, base, Q, v);
+    bfly_finish<R, INV>(xw, base, Q, tb[n1], v);
+  }
+  __syncwarp();
+}
+
+template <bool INV, bool BIG>
+__device__ void fft_pass_w(double2* xw, int Mw, int S, int R, const double2* tb) {
+  if constexpr (BIG) {
+    switch (R) {
+      case 9: pass_loop_w<9, INV>(xw, Mw, S, tb); return;
+      case 10: pass_loop_w<10, INV>(xw, Mw, S, tb); return;
+      case 12: pass_loop_w<12, INV>(xw, Mw, S, tb); return;
+      case 14: pass_loop_w<14, INV>(xw, Mw, S, tb); return;
+      case 15: pass_loop_w<15, INV>(xw, Mw, S, tb); return;
+      case 16: pass_loop_w<16, INV>(xw, Mw, S, tb); return;
+    }
+  }
+  switch (R) {
+    case 2: pass_loop_w<2, INV>(xw, Mw, S, tb); break;
+    case 3: pass_loop_w<3, INV>(xw, Mw, S, tb); break;
+    case 4: pass_loop_w<4, INV>(xw, Mw, S, tb); break;
+    case 5: pass_loop_w<5, INV>(xw, Mw, S, tb); break;
+    case 6: pass_loop_w<6, INV>(xw, Mw, S, tb); break;
+    case 7: pass_loop_w<7, INV>(xw, Mw, S, tb); break;
+    case 8: pass_loop_w<8, INV>(xw, Mw, S, tb); break;
+  }
+}
+
+// first pass index from which every pass is warp-local: the smallest ps >= 1 whose leading radix product
+// R_0 ... R_{ps-1} is a multiple of the warp count (npass: none)
+__device__ __forceinline__ int warp_local_from(const DevParams& P, int fi) {
+  if (blockDim.x & 31) return kMaxFftPasses;
+  const int W = blockDim.x >> 5;
+  const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
+  const int npass = P.fft_npass[fi];
+  int prod = radix[0];
+  for (int ps = 1; ps < npass; ++ps) {
+    if (prod % W == 0) return ps;
+    prod *= radix[ps];
+  }
+  return kMaxFftPasses;
+}
+
 template <bool INV, bool BIG, bool ZT = false>
 __device__ void fft_pass(double2* x, int M, int S, int R, const double2* tb, int nz = 0) {
   if constexpr (BIG) {
@@ -274,16 +332,24 @@ __device__ void load_twiddles(const DevParams& P, int fi, double2* tb) {
 // R, unit twiddles), the pointwise product with the kernel spectrum V and the first DIT pass (the
 // same groups) in registers -- three shared-memory sweeps replaced by one.
 template <int R, bool BIG>
-__device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __restrict__ V) {
+__device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __restrict__ V, const bool wl) {
   // U groups per trip with all their loads (shared x, global V -- L2-resident) issued first: the V loads are
-  // latency-bound
+  // latency-bound.  wl: warp w runs the groups of its region [w M/W, (w + 1) M/W) (warp-local passes)
   constexpr int U = 1;
-  const int G = M / R;
-  for (int g0 = threadIdx.x; g0 < G; g0 += U * blockDim.x) {
+  int G = M / R, t0 = threadIdx.x, step = blockDim.x;
+  if (wl) {
+    const int Mw = M / (int)(blockDim.x >> 5), w = threadIdx.x >> 5;
+    x += w * Mw;
+    V += w * Mw;
+    G = Mw / R;
+    t0 = threadIdx.x & 31;
+    step = 32;
+  }
+  for (int g0 = t0; g0 < G; g0 += U * step) {
     double2 v[U][R], w[U][R];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int g = g0 + u * blockDim.x;
+      const int g = g0 + u * step;
 #pragma unroll
       for (int k = 0; k < R; ++k) {
         v[u][k] = g < G ? x[g * R + k] : make_double2(0.0, 0.0);
@@ -292,7 +358,7 @@ __device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __res
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int g = g0 + u * blockDim.x;
+      const int g = g0 + u * step;
       dft_small<R, false>(v[u]);
 #pragma unroll
       for (int k = 0; k < R; ++k) v[u][k] = cmulx(v[u][k], w[u][k]);
@@ -305,36 +371,42 @@ __device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __res
   }
 }
 
-template <bool BIG>
-__device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* __restrict__ V) {
+template <bool BIG, bool WL = false>
+__device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* __restrict__ V, bool wl = false) {
+  if constexpr (!WL) wl = false;
   const int M = P.fft_M[fi];
   const int R = P.fft_radix[fi * kMaxFftPasses + P.fft_npass[fi] - 1];
   switch (R) {
-    case 2: mid_loop<2, BIG>(x, M, V); break;
-    case 3: mid_loop<3, BIG>(x, M, V); break;
-    case 4: mid_loop<4, BIG>(x, M, V); break;
-    case 5: mid_loop<5, BIG>(x, M, V); break;
-    case 6: mid_loop<6, BIG>(x, M, V); break;
-    case 7: mid_loop<7, BIG>(x, M, V); break;
-    case 8: mid_loop<8, BIG>(x, M, V); break;
+    case 2: mid_loop<2, BIG>(x, M, V, wl); break;
+    case 3: mid_loop<3, BIG>(x, M, V, wl); break;
+    case 4: mid_loop<4, BIG>(x, M, V, wl); break;
+    case 5: mid_loop<5, BIG>(x, M, V, wl); break;
+    case 6: mid_loop<6, BIG>(x, M, V, wl); break;
+    case 7: mid_loop<7, BIG>(x, M, V, wl); break;
+    case 8: mid_loop<8, BIG>(x, M, V, wl); break;
   }
   if constexpr (BIG) {
     switch (R) {
-      case 9: mid_loop<9, BIG>(x, M, V); break;
-      case 10: mid_loop<10, BIG>(x, M, V); break;
-      case 12: mid_loop<12, BIG>(x, M, V); break;
-      case 14: mid_loop<14, BIG>(x, M, V); break;
-      case 15: mid_loop<15, BIG>(x, M, V); break;
-      case 16: mid_loop<16, BIG>(x, M, V); break;
+      case 9: mid_loop<9, BIG>(x, M, V, wl); break;
+      case 10: mid_loop<10, BIG>(x, M, V, wl); break;
+      case 12: mid_loop<12, BIG>(x, M, V, wl); break;
+      case 14: mid_loop<14, BIG>(x, M, V, wl); break;
+      case 15: mid_loop<15, BIG>(x, M, V, wl); break;
+      case 16: mid_loop<16, BIG>(x, M, V, wl); break;
     }
   }
-  __syncthreads();
+  if (wl) __syncwarp();
+  else __syncthreads();
 }
 
 // forward DIF FFT, natural -> digit-reversed; tb = shared copy of this size's tables
-template <bool BIG>
+template <bool BIG, bool WL = false>
 // nz < M: only x[0, nz) holds data, the rest is implicit zero padding (never stored, see pass_loop ZT)
-__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0, int nz = -1) {
+// WL: passes >= wl are warp-local (pass_loop_w); a warp-local last pass ends with a block barrier unless the
+// caller continues on the warp's own region (skip_last: the fused middle)
+__device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0, int nz = -1,
+                        int wl = kMaxFftPasses) {
+  if constexpr (!WL) wl = kMaxFftPasses;
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -343,13 +415,20 @@ __device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* t
   for (int ps = 0; ps < npass - skip_last; ++ps) {
     const int R = radix[ps];
     if (ps == 0 && nz >= 0 && nz < M) fft_pass<false, BIG, true>(x, M, S, R, tb + (off[ps] - off[0]), nz);
-    else fft_pass<false, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
+    else if (WL && ps >= wl) {
+      const int Mw = M / (int)(blockDim.x >> 5);
+      fft_pass_w<false, BIG>(x + (threadIdx.x >> 5) * Mw, Mw, S, R, tb + (off[ps] - off[0]));
+    } else fft_pass<false, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
     S /= R;
   }
+  if (WL && !skip_last && npass - 1 >= wl) __syncthreads();
 }
 // inverse (unnormalised, x M) DIT FFT, digit-reversed -> natural
-template <bool BIG>
-__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb, int skip_first = 0, int nz = -1) {
+template <bool BIG, bool WL = false>
+// WL: passes >= wl are warp-local (they come first in DIT order); a block barrier follows the last of them
+__device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* tb, int skip_first = 0, int nz = -1,
+                        int wl = kMaxFftPasses) {
+  if constexpr (!WL) wl = kMaxFftPasses;
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
@@ -359,8 +438,12 @@ __device__ void fft_dit(const DevParams& P, double2* x, int fi, const double2* t
     const int R = radix[ps];
     S *= R;
     if (ps == npass - 1 && skip_first) continue;
+    if (WL && ps == wl - 1) __syncthreads();         // the first block-wide pass after the warp-local ones
     if (ps == 0 && nz >= 0 && nz < M) fft_pass<true, BIG, true>(x, M, S, R, tb + (off[ps] - off[0]), nz);
-    else fft_pass<true, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
+    else if (WL && ps >= wl) {
+      const int Mw = M / (int)(blockDim.x >> 5);
+      fft_pass_w<true, BIG>(x + (threadIdx.x >> 5) * Mw, Mw, S, R, tb + (off[ps] - off[0]));
+    } else fft_pass<true, BIG>(x, M, S, R, tb + (off[ps] - off[0]));
   }
 }
 
@@ -930,8 +1013,9 @@ __device__ unsigned long long g_fft_prof[8];
 #endif
 
 // one block per (signal, line): F = Bluestein DFT_p(s), in place in `lines`
-template <bool BIG>
-__global__ void __launch_bounds__(BIG ? 512 : 1024, 1)
+// WL small sizes (M < fft_big_m) launch with at most 256 threads (two CTAs per SM, 128 registers)
+template <bool BIG, bool WL>
+__global__ void __launch_bounds__(BIG ? 512 : (WL ? 256 : 1024), BIG ? 1 : (WL ? 2 : 1))
 pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restrict__ part, int32_t p_part) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1067,11 +1151,19 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     for (int q = p + threadIdx.x; q < M; q += blockDim.x) x[q] = make_double2(0.0, 0.0);
   __syncthreads();
   FFT_PROF_MARK(0);
-  fft_dif<BIG>(P, x, fi, tb, 1, p);                   // x[p, M) is implicit zero padding
+  // warp-local from pass wl on (the middle included), unless disabled or the middle would not be warp-local
+  // (WL instantiation: launched when the iteration's largest size qualifies; smaller sizes of the same launch fall
+  // back to block-wide passes)
+  int wl = kMaxFftPasses;
+  if constexpr (WL) {
+    wl = M >= kFftWlMinM ? warp_local_from(P, fi) : kMaxFftPasses;
+    if (wl > P.fft_npass[fi] - 1) wl = kMaxFftPasses;
+  }
+  fft_dif<BIG, WL>(P, x, fi, tb, 1, p, wl);           // x[p, M) is implicit zero padding
   FFT_PROF_MARK(1);
-  fft_mid<BIG>(P, x, fi, P.V + (int64_t)tslot * P.M_stride);
+  fft_mid<BIG, WL>(P, x, fi, P.V + (int64_t)tslot * P.M_stride, wl < kMaxFftPasses);
   FFT_PROF_MARK(2);
-  fft_dit<BIG>(P, x, fi, tb, 1, p);                   // only F[b], b < p, is used
+  fft_dit<BIG, WL>(P, x, fi, tb, 1, p, wl);           // only F[b], b < p, is used
   FFT_PROF_MARK(3);
   if (P.fuse_decode) {
     if (n == 0) {
@@ -1169,9 +1261,11 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
 }
 
 cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads,
-                        int32_t big, int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st) {
+                        int32_t big, int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st, bool wl) {
   const size_t smem = (size_t)smem_bytes;
-  auto kern = big ? pfft_kernel<true> : pfft_kernel<false>;
+  wl = wl && (big || threads <= 256);
+  auto kern = big ? (wl ? pfft_kernel<true, true> : pfft_kernel<true, false>)
+                  : (wl ? pfft_kernel<false, true> : pfft_kernel<false, false>);
   cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
   const long grid = (long)n_signals * n_lines;

@@ -18,6 +18,9 @@ namespace sfft {
 enum : int32_t { ST_RUN = 100 };   // final states use sfft_status values (0 OK, 1 PARTIAL, <0 error)
 
 constexpr int kMaxFftPasses = 24;
+// smallest FFT size whose passes run warp-local after the first (k_fft.cu pass_loop_w): smaller sizes run as
+// many short CTAs (C4's M = 1008 at 96 threads), where block-wide passes measured faster
+constexpr int kFftWlMinM = 4096;
 constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
 constexpr int kMaxFallbackLevels = 67;   // sfft_options.fallback_tilts: 4 fixed-stride tilt levels + 63 round-robin rounds
@@ -367,8 +370,9 @@ inline int fft_threads(int M, size_t smem, int64_t n_ctas) {
   int t = ((M / tdiv + 31) / 32) * 32;
   return t < 64 ? 64 : (t > cap ? cap : t);
 }
+// wl: warp-local passes once the leading radices split the line over the warps (pfft_kernel<., true>)
 cudaError_t launch_pfft(const DevParams& P, int32_t n_signals, int32_t n_lines, int32_t smem_bytes, int32_t threads, int32_t big,
-                        int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st);
+                        int32_t ksplit, const double2* part, int32_t p_part, cudaStream_t st, bool wl = false);
 cudaError_t launch_fft_twiddles(double2* tw, const int4* seg, int n_seg, cudaStream_t st);
 // k_wrap.cu
 // scratch: device int32 [n_signals * (k + 1)]
