@@ -210,7 +210,7 @@ FftSize radix_plan(int M) {
   // radix W (one block-wide pass) and the rest of the plan -- run by each warp on its own M / W points -- is chosen
   // for lane efficiency: a radix-R pass costs ceil(Mw / R / 32) warp trips of ~fft_bfly_cost(R) instructions
   const int W = M >= fft_big_m() ? 16 : fft_threads(M, 16 * ((size_t)M + M / 4), 0) / 32;
-  if (!getenv("SFFT_FFT_NO_WLPLAN") && M >= kFftWlMinM && W >= 2 && M % W == 0 && M / W > 1 &&
+  if (!getenv("SFFT_FFT_NO_WLPLAN") && M >= fft_wl_min() && W >= 2 && M % W == 0 && M / W > 1 &&
       std::find(std::begin(kRad), std::end(kRad), W) != std::end(kRad) && W <= rmax) {
     const int Mw = M / W;
     // cost[x][last]: cheapest plan of x points whose last (fused middle) radix is `last` (0: plan of 1)
@@ -386,7 +386,7 @@ T* ptr(const sfft_plan_t* P, int b) {
 // warp-local FFT passes for a launch whose largest size is M (SFFT_FFT_NO_WL=1: block-wide passes only)
 bool fft_wl_for(int M) {
   static const bool no_wl = getenv("SFFT_FFT_NO_WL") != nullptr;
-  return !no_wl && M >= kFftWlMinM;
+  return !no_wl && M >= fft_wl_min();
 }
 
 DevParams dev_params(const sfft_plan_t* P, int32_t batch) {

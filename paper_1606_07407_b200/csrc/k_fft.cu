@@ -1156,7 +1156,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   // back to block-wide passes)
   int wl = kMaxFftPasses;
   if constexpr (WL) {
-    wl = M >= kFftWlMinM ? warp_local_from(P, fi) : kMaxFftPasses;
+    wl = warp_local_from(P, fi);
     if (wl > P.fft_npass[fi] - 1) wl = kMaxFftPasses;
   }
   fft_dif<BIG, WL>(P, x, fi, tb, 1, p, wl);           // x[p, M) is implicit zero padding

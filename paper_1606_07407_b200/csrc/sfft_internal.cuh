@@ -21,6 +21,10 @@ constexpr int kMaxFftPasses = 24;
 // smallest FFT size whose passes run warp-local after the first (k_fft.cu pass_loop_w): smaller sizes run as
 // many short CTAs (C4's M = 1008 at 96 threads), where block-wide passes measured faster
 constexpr int kFftWlMinM = 4096;
+inline int fft_wl_min() {   // SFFT_FFT_WL_MIN: tuning override of kFftWlMinM (host decisions: plans, launches)
+  static const int v = getenv("SFFT_FFT_WL_MIN") ? atoi(getenv("SFFT_FFT_WL_MIN")) : kFftWlMinM;
+  return v;
+}
 constexpr int kDecodeThreads = 1024;
 constexpr int kLogIters = 64;
 constexpr int kMaxFallbackLevels = 67;   // sfft_options.fallback_tilts: 4 fixed-stride tilt levels + 63 round-robin rounds
