@@ -999,3 +999,32 @@ def test_binding_validates_arguments(S):
             S.sfft_execute(plan, sig, tuple(outs))
     res = S.sfft_execute(plan, sig, good)
     assert res.status == S.SFFT_OK
+
+
+def test_fft_warp_local_passes_bitwise(S):
+    """Warp-local FFT passes (pfft_kernel<., true>, k_fft.cu pass_loop_w) run the same butterflies with the same
+    twiddles as the block-wide passes, only assigned to warps by region: under one radix plan
+    (SFFT_FFT_NO_WLPLAN=1 in both processes) the stage FFT of the BIG (M = 10080, 16 warps) and the small
+    (M = 5040, 8 warps) sizes is bitwise identical with and without them (SFFT_FFT_NO_WL=1)."""
+    import subprocess, sys
+    code = ("import numpy as np, torch, hashlib, workloads as W, paper_1606_07407_b200 as S\n"
+            "c = W.CONFIGS['c3']; plan = S.sfft_plan(c.d, c.N, c.k, blocks=c.blocks)\n"
+            "for p, n in ((5003, 40), (2503, 40)):\n"
+            "    rng = np.random.default_rng(p)\n"
+            "    x = torch.from_numpy(rng.standard_normal((n, p)) + 1j * rng.standard_normal((n, p))).cuda()\n"
+            "    S.sfft_stage_pfft(plan, x)\n"
+            "    print(p, hashlib.sha256(x.cpu().numpy().tobytes()).hexdigest())\n")
+    root = os.path.dirname(GOLD_DIR.rstrip("/")).rsplit("/tests", 1)[0]
+    outs = []
+    for extra in ({}, {"SFFT_FFT_NO_WL": "1"}):
+        env = dict(os.environ, SFFT_FFT_NO_WLPLAN="1", **extra)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300, cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(r.stdout.split())
+    assert len(outs[0]) == 4 and outs[0] == outs[1], outs
+
+
+def test_e2e_block_wide_fft_passes(S):
+    """The block-wide FFT passes alone (SFFT_FFT_NO_WL=1: no warp-local plans or launches) against the golden
+    oracle at full size (C3 and C5 seeds)."""
+    _opt_in_parity("SFFT_FFT_NO_WL", (("c3", [0, 1]), ("c5", [0])))
