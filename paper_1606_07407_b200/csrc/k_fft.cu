@@ -822,17 +822,20 @@ template <bool BIG>
 __global__ void __launch_bounds__(BIG ? 512 : 1024, 1) fft_prep_kernel(DevParams P, int32_t direct) {
   pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  int slot, p;
   if (direct) {
     const int s = P.active[blockIdx.x];
-    slot = P.st_slot[s];
-    p = P.st_p[s];
-  } else {
-    if ((int)blockIdx.x >= P.ctrl[3]) return;
-    slot = P.fill[blockIdx.x];
-    p = P.slot_p[slot];
+    fill_tables<BIG>(P, P.st_slot[s], P.st_p[s], smem_raw);
+    return;
   }
-  fill_tables<BIG>(P, slot, p, smem_raw);
+  // the queued fills of this iteration (a device-side count, usually 0 once the cache is warm): a grid of at most
+  // one wave of these large-smem CTAs loops over them -- a grid of one CTA per active signal would spend several
+  // waves of empty CTAs (C2, 1024 signals: ~20 us per iteration)
+  const int n_fill = P.ctrl[3];
+  for (int f = blockIdx.x; f < n_fill; f += gridDim.x) {
+    const int slot = P.fill[f];
+    fill_tables<BIG>(P, slot, P.slot_p[slot], smem_raw);
+    __syncthreads();
+  }
 }
 
 // One kernel per iteration for the table prep (CTA per active-signal slot of the previous count): CTA 0 maps
@@ -1250,7 +1253,13 @@ cudaError_t launch_fft_prep(const DevParams& P, int32_t n_signals, int32_t smem_
   auto kern = big ? fft_prep_kernel<true> : fft_prep_kernel<false>;
   cudaError_t e = ensure_smem(kern, smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(kern, dim3(n_signals), dim3(threads), smem, st, P, direct ? 1 : 0);
+  int n_sm = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int fill_grid = direct ? n_signals : std::min(n_signals, n_sm);   // queued fills: one wave, looping
+  e = launch_pdl(kern, dim3(fill_grid), dim3(threads), smem, st, P, direct ? 1 : 0);
   if (e != cudaSuccess) return e;
   e = ensure_smem(terms_kernel, sizeof(int) * ((size_t)P.p_stride + 3 * (size_t)P.k));
   if (e != cudaSuccess) return e;
