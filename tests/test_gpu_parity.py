@@ -1028,3 +1028,14 @@ def test_e2e_block_wide_fft_passes(S):
     """The block-wide FFT passes alone (SFFT_FFT_NO_WL=1: no warp-local plans or launches) against the golden
     oracle at full size (C3 and C5 seeds)."""
     _opt_in_parity("SFFT_FFT_NO_WL", (("c3", [0, 1]), ("c5", [0])))
+
+
+def test_int8_accumulator_guard(S):
+    """The int8-limb exp-sum's int32 sums are exact while S * 2K * 2^14 < 2^31 (k_expsum_i8.cu header; K < 10923
+    terms at S = 6): an explicit prime schedule lets k pass the prime-table check, so the plan itself must refuse
+    the int8 path beyond the bound -- ENOTSUP when it is forced (expsum_path = 2), the FP64 exp-sum otherwise."""
+    with pytest.raises(S.SfftError) as e:
+        S.sfft_plan(3, 4096, 11000, primes=[6733], blocks=(2, 1), expsum_path=2)
+    assert e.value.status == S.SFFT_ENOTSUP
+    S.sfft_plan(3, 4096, 11000, primes=[6733], blocks=(2, 1))            # auto: falls back to the FP64 exp-sum
+    S.sfft_plan(3, 4096, 10000, primes=[6733], blocks=(2, 1), expsum_path=2)   # inside the bound: int8 allowed
