@@ -61,7 +61,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c3", choices=sorted(W.CONFIGS))
     ap.add_argument("--batch", type=int, default=0, help="signals per GPU per step (default: config trials)")
-    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--e2e-steps", type=int, default=-1,
+                    help="steps of the end-to-end (host-buffer) legs; -1 = --steps (0 = skip)")
     ap.add_argument("--spec-primes", type=int, nargs="*", default=[2, 4, 8],
                     help="single-solve latency (and, with --spec-steps, the batched step) also with G-prime "
                          "speculation (reading R26) for each G")
@@ -523,7 +524,7 @@ def main():
     # (1) sfft_solve_host_batches: the K steps' batches in one call, the library overlapping each step's transfers
     # with its neighbours' solves (the headline e2e); (2) sfft_solve_host once per step (copies serialised with the
     # solve, L2 flushed between steps), reported alongside
-    ne = args.e2e_steps
+    ne = args.steps if args.e2e_steps < 0 else args.e2e_steps
     e2e_value = e2e_serial = None
     hout = (torch.empty((T, cfg.k, cfg.d), dtype=torch.int32).pin_memory(),
             torch.empty((T, cfg.k, 2), dtype=torch.float64).pin_memory(),
