@@ -54,6 +54,7 @@ struct FftSize {
   std::vector<int8_t> radix;
   size_t smem = 0;        // 16 * (M + sum_passes S/R): data + base twiddles
   size_t smem_upto = 0;   // max smem over all sizes <= M (launch size when max M is this one)
+  int vw = 0;             // warp count of the warp-local plan (the table fill also stores V warp-blocked, k_fft.cu)
 };
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
@@ -139,7 +140,7 @@ namespace {
 
 enum Buf {
   B_BLOCKS, B_BOFF, B_LO, B_HI, B_TILTS, B_AXT, B_SCHED, B_PRIMES, B_FFTM, B_FFTR, B_FFTN,
-  B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
+  B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_VB, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
@@ -243,6 +244,7 @@ FftSize radix_plan(int M) {
       rs.assign(1, W);
       rs.insert(rs.end(), sub.begin(), sub.end());
       rs.push_back(bm);
+      s.vw = W;
     }
   }
   // SFFT_FFT_PLAN="M:r1,r2,...;..." overrides the radices of size M (tuning experiments; order as given)
@@ -263,7 +265,10 @@ FftSize radix_plan(int M) {
         while (i < spec.size() && spec[i] != ',' && spec[i] != ';') ++i;
         if (i < spec.size() && spec[i] == ',') ++i;
       }
-      if (ok && prod == M) rs = ov;
+      if (ok && prod == M) {
+        rs = ov;
+        if (s.vw && (rs[0] % s.vw != 0 || (M / s.vw) % rs.back() != 0)) s.vw = 0;
+      }
     }
   }
   for (int R : rs) s.radix.push_back((int8_t)R);
@@ -304,6 +309,7 @@ void layout(sfft_plan_t* P) {
   sz[B_WTAB] = 16 * T * P->p_stride;
   sz[B_CHIRP] = 16 * T * P->p_stride;
   sz[B_V] = 16 * T * P->M_stride;
+  sz[B_VB] = P->fft.back().M >= kFftWlMinM ? 16 * T * P->M_stride : 0;   // V warp-blocked (k_fft.cu mid_loop)
   sz[B_AREG] = 16 * S * P->k;
   sz[B_KHASH] = 8 * S * P->k;
   sz[B_HTAB] = 4 * S * P->H;
@@ -426,6 +432,7 @@ DevParams dev_params(const sfft_plan_t* P, int32_t batch) {
   D.W_tab = ptr<double2>(P, B_WTAB);
   D.chirp = ptr<double2>(P, B_CHIRP);
   D.V = ptr<double2>(P, B_V);
+  D.VB = P->fft.back().M >= kFftWlMinM ? ptr<double2>(P, B_VB) : nullptr;
   D.a_reg = ptr<double2>(P, B_AREG);
   D.key_hash = ptr<uint64_t>(P, B_KHASH);
   D.htab = ptr<int32_t>(P, B_HTAB);
@@ -568,6 +575,7 @@ int ensure_ready(sfft_plan_t* P) {
       fm.push_back(P->fft[i].M);
       fn.push_back((int32_t)P->fft[i].radix.size());
       for (size_t j = 0; j < P->fft[i].radix.size(); ++j) fr[i * kMaxFftPasses + j] = P->fft[i].radix[j];
+      fr[i * kMaxFftPasses + kFftVwSlot] = (int8_t)P->fft[i].vw;   // after the last pass (npass < kMaxFftPasses)
     }
     auto up = [&](int b, const void* src, size_t n) -> cudaError_t {
       if (n == 0) return cudaSuccess;

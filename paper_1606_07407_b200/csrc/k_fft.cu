@@ -332,10 +332,32 @@ __device__ void load_twiddles(const DevParams& P, int fi, double2* tb) {
 // R, unit twiddles), the pointwise product with the kernel spectrum V and the first DIT pass (the
 // same groups) in registers -- three shared-memory sweeps replaced by one.
 template <int R, bool BIG>
-__device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __restrict__ V, const bool wl) {
+__device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __restrict__ V, const bool wl,
+                                         const double2* __restrict__ VB = nullptr) {
   // U groups per trip with all their loads (shared x, global V -- L2-resident) issued first: the V loads are
-  // latency-bound.  wl: warp w runs the groups of its region [w M/W, (w + 1) M/W) (warp-local passes)
+  // latency-bound.  wl: warp w runs the groups of its region [w M/W, (w + 1) M/W) (warp-local passes); VB: the
+  // spectrum blocked for this warp count, so that the lanes' loads of element k are consecutive (coalesced)
   constexpr int U = 1;
+  if (VB) {
+    const int Mw = M / (int)(blockDim.x >> 5), w = threadIdx.x >> 5, Gw = Mw / R;
+    x += w * Mw;
+    VB += w * Mw;
+    for (int g = threadIdx.x & 31; g < Gw; g += 32) {
+      double2 v[R], wv[R];
+#pragma unroll
+      for (int k = 0; k < R; ++k) {
+        v[k] = x[g * R + k];
+        wv[k] = __ldg(VB + k * Gw + g);
+      }
+      dft_small<R, false>(v);
+#pragma unroll
+      for (int k = 0; k < R; ++k) v[k] = cmulx(v[k], wv[k]);
+      dft_small<R, true>(v);
+#pragma unroll
+      for (int k = 0; k < R; ++k) x[g * R + k] = v[k];
+    }
+    return;
+  }
   int G = M / R, t0 = threadIdx.x, step = blockDim.x;
   if (wl) {
     const int Mw = M / (int)(blockDim.x >> 5), w = threadIdx.x >> 5;
@@ -372,27 +394,30 @@ __device__ __forceinline__ void mid_loop(double2* x, int M, const double2* __res
 }
 
 template <bool BIG, bool WL = false>
-__device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* __restrict__ V, bool wl = false) {
+__device__ void fft_mid(const DevParams& P, double2* x, int fi, const double2* __restrict__ V, bool wl = false,
+                        const double2* __restrict__ VB = nullptr) {
   if constexpr (!WL) wl = false;
   const int M = P.fft_M[fi];
   const int R = P.fft_radix[fi * kMaxFftPasses + P.fft_npass[fi] - 1];
+  // the blocked copy only when this launch's warp count is the plan's (the fill blocked it for that count)
+  if (!WL || !wl || P.fft_radix[fi * kMaxFftPasses + kFftVwSlot] != (int)(blockDim.x >> 5)) VB = nullptr;
   switch (R) {
-    case 2: mid_loop<2, BIG>(x, M, V, wl); break;
-    case 3: mid_loop<3, BIG>(x, M, V, wl); break;
-    case 4: mid_loop<4, BIG>(x, M, V, wl); break;
-    case 5: mid_loop<5, BIG>(x, M, V, wl); break;
-    case 6: mid_loop<6, BIG>(x, M, V, wl); break;
-    case 7: mid_loop<7, BIG>(x, M, V, wl); break;
-    case 8: mid_loop<8, BIG>(x, M, V, wl); break;
+    case 2: mid_loop<2, BIG>(x, M, V, wl, VB); break;
+    case 3: mid_loop<3, BIG>(x, M, V, wl, VB); break;
+    case 4: mid_loop<4, BIG>(x, M, V, wl, VB); break;
+    case 5: mid_loop<5, BIG>(x, M, V, wl, VB); break;
+    case 6: mid_loop<6, BIG>(x, M, V, wl, VB); break;
+    case 7: mid_loop<7, BIG>(x, M, V, wl, VB); break;
+    case 8: mid_loop<8, BIG>(x, M, V, wl, VB); break;
   }
   if constexpr (BIG) {
     switch (R) {
-      case 9: mid_loop<9, BIG>(x, M, V, wl); break;
-      case 10: mid_loop<10, BIG>(x, M, V, wl); break;
-      case 12: mid_loop<12, BIG>(x, M, V, wl); break;
-      case 14: mid_loop<14, BIG>(x, M, V, wl); break;
-      case 15: mid_loop<15, BIG>(x, M, V, wl); break;
-      case 16: mid_loop<16, BIG>(x, M, V, wl); break;
+      case 9: mid_loop<9, BIG>(x, M, V, wl, VB); break;
+      case 10: mid_loop<10, BIG>(x, M, V, wl, VB); break;
+      case 12: mid_loop<12, BIG>(x, M, V, wl, VB); break;
+      case 14: mid_loop<14, BIG>(x, M, V, wl, VB); break;
+      case 15: mid_loop<15, BIG>(x, M, V, wl, VB); break;
+      case 16: mid_loop<16, BIG>(x, M, V, wl, VB); break;
     }
   }
   if (wl) __syncwarp();
@@ -815,6 +840,16 @@ __device__ void fill_tables(const DevParams& P, int slot, int p, unsigned char* 
   const double inv = 1.0 / (double)M;
   double2* V = P.V + (int64_t)slot * P.M_stride;
   for (int q = threadIdx.x; q < M; q += blockDim.x) V[q] = cscale(x[q], inv);
+  const int vw = P.fft_radix[fi * kMaxFftPasses + kFftVwSlot];
+  if (vw && P.VB) {
+    // warp-blocked copy for the warp-local middle (kFftVwSlot): element k of group g of warp region w
+    const int R = P.fft_radix[fi * kMaxFftPasses + P.fft_npass[fi] - 1], Mt = M / vw, Gt = Mt / R;
+    double2* VB = P.VB + (int64_t)slot * P.M_stride;
+    for (int q = threadIdx.x; q < M; q += blockDim.x) {
+      const int w = q / Mt, rr = q - w * Mt, g = rr / R, k = rr - g * R;
+      VB[w * Mt + k * Gt + g] = cscale(x[q], inv);
+    }
+  }
 }
 
 // stage entry points (direct): the tables of every listed signal's prime; else the queued fills of the iteration
@@ -1164,7 +1199,8 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   }
   fft_dif<BIG, WL>(P, x, fi, tb, 1, p, wl);           // x[p, M) is implicit zero padding
   FFT_PROF_MARK(1);
-  fft_mid<BIG, WL>(P, x, fi, P.V + (int64_t)tslot * P.M_stride, wl < kMaxFftPasses);
+  fft_mid<BIG, WL>(P, x, fi, P.V + (int64_t)tslot * P.M_stride, wl < kMaxFftPasses,
+                   P.VB ? P.VB + (int64_t)tslot * P.M_stride : nullptr);
   FFT_PROF_MARK(2);
   fft_dit<BIG, WL>(P, x, fi, tb, 1, p, wl);           // only F[b], b < p, is used
   FFT_PROF_MARK(3);

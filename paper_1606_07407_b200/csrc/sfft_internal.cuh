@@ -21,6 +21,9 @@ constexpr int kMaxFftPasses = 24;
 // smallest FFT size whose passes run warp-local after the first (k_fft.cu pass_loop_w): smaller sizes run as
 // many short CTAs (C4's M = 1008 at 96 threads), where block-wide passes measured faster
 constexpr int kFftWlMinM = 4096;
+// fft_radix[fi][kFftVwSlot]: W of a warp-local plan, whose kernel spectrum is also stored warp-blocked in VB (middle
+// group g of warp region w, element k at w Mw + k G + g, G = Mw / R: lanes read consecutive entries), 0: none
+constexpr int kFftVwSlot = kMaxFftPasses - 1;
 inline int fft_wl_min() {   // SFFT_FFT_WL_MIN: tuning override of kFftWlMinM (host decisions: plans, launches)
   static const int v = getenv("SFFT_FFT_WL_MIN") ? atoi(getenv("SFFT_FFT_WL_MIN")) : kFftWlMinM;
   return v;
@@ -72,6 +75,7 @@ struct DevParams {
   double2* W_tab;              // [batch][p_stride]   e^{+2 pi i q/p}
   double2* chirp;              // [batch][p_stride]   e^{-pi i (q^2 mod 2p)/p}
   double2* V;                  // [batch][M_stride]   DIF spectrum of the Bluestein kernel / M
+  double2* VB;                 // [slots][M_stride]  the same, warp-blocked for the warp-local middle (kFftVwSlot)
   double2* a_reg;              // [batch][k]
   uint64_t* key_hash;          // [batch][k]
   int32_t* htab;               // [batch][H]  entry index + 1, 0 = empty
