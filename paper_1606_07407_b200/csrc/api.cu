@@ -140,13 +140,14 @@ namespace {
 
 enum Buf {
   B_BLOCKS, B_BOFF, B_LO, B_HI, B_TILTS, B_AXT, B_SCHED, B_PRIMES, B_FFTM, B_FFTR, B_FFTN,
-  B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_VB, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
+  B_VALL, B_CALL, B_LINES, B_WTAB, B_CHIRP, B_V, B_AREG, B_KHASH, B_HTAB, B_ACCV, B_ACCA, B_WTMP,
   B_STATUS, B_NR, B_P, B_M, B_MI, B_STALL, B_ITERS, B_SAMPLES, B_CMACS, B_LOG, B_CTRL,
   B_IN_F, B_IN_C, B_OUT_F, B_OUT_C, B_OUT_N, B_OUT_S, B_STAGE, B_ACTIVE, B_PART, B_TWOFF, B_TW, B_TWSEG, B_UALL,
   B_WRAPS, B_I8B, B_I8SIG, B_CMACS8, B_LVLE, B_LVLLO, B_LVLHI, B_LVLT, B_LVLNT, B_LVLAXT, B_STLVL, B_STIL,
   B_STRT, B_I8PW, B_I8DLOG, B_I8ELOG, B_I8CHL, B_STSLOT, B_SLOTP, B_SLOTE, B_FILL, B_I8TLO, B_I8THI,
   B_RSEND, B_RRECV, B_RCAND, B_RNC, B_RF0, B_SELRDY, B_BINST, B_BINORD, B_FILLBY, B_FILLEP, B_SLOTRDY, B_ASGRDY, B_SPINERR,
   B_FFTW, B_DLROOT, B_CROWI, B_CROWL, B_SPECT,
+  B_VB,                   // last: adding it left every other buffer's offset unchanged
   B_COUNT
 };
 static_assert(B_COUNT <= 128, "sfft_plan_s::off is too small for the workspace buffer list");
