@@ -802,10 +802,15 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
   if (D.peer_mode) D.peer_epoch = ++P->peer_epoch;   // the same sequence on every shard (one per iteration)
   D.fused_sample = it.fused ? 1 : 0;
   if (it.fused) D.lines_log = 0;
+  // first DIF pass gathering the discrete-log line (no load sweep) up to this FFT size (0: off); measured
+  // (profiles/r02_experiments.md): C4's M = 1008 FFT -2 %, C3's 10080 / 2016-point lines slower (dependent gathers)
+  static const int gather_max_M = getenv("SFFT_FFT_GATHER") ? atoi(getenv("SFFT_FFT_GATHER")) : 1024;
+  D.fused_load = gather_max_M;
   const size_t fsm = it.fused ? it.fused_smem : P->fft[it.fi].smem_upto;
   LAUNCH(P, launch_pfft(D, it.n_active, P->L, (int)fsm, fft_threads(it.max_M, fsm, (int64_t)it.n_active * P->L), it.big,
                         it.fused ? 1 : it.ksplit, ptr<double2>(P, B_PART), it.max_p, st, fft_wl_for(it.max_M) && !it.fused));
   D.fused_sample = 0;
+  D.fused_load = 0;
   D.lines_log = 0;
   D.fuse_decode = 0;
   D.fuse_commit = 0;

@@ -236,6 +236,30 @@ __device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double
   }
 }
 
+// First DIF pass fused with the load of a discrete-log line (int8 exp-sum iterations, ksplit = 1): the butterfly
+// of base n1 gathers its inputs h = n1 + Q n < p straight from the line (position f = log_g h, the h = 0 row at
+// f = p - 1) times the chirp -- the same products as the load phase's x[h] = line[f] chirp[h] followed by the ZT
+// first pass (chirp[h] = chl[f]: one chirp_value), without the scattered shared-memory sweep and its barrier.
+template <int R>
+__device__ __forceinline__ void pass_loop_gather(double2* x, int M, int p, const double2* __restrict__ tb,
+                                                 const double2* __restrict__ line, const double2* __restrict__ ch,
+                                                 const int32_t* __restrict__ dlog) {
+  const int Q = M / R;
+  for (int n1 = threadIdx.x; n1 < Q; n1 += blockDim.x) {
+    int f[R];
+#pragma unroll
+    for (int n = 0; n < R; ++n) {
+      const int h = n1 + Q * n;
+      f[n] = h < p ? (h ? __ldg(dlog + h) : p - 1) : -1;
+    }
+    double2 v[R];
+#pragma unroll
+    for (int n = 0; n < R; ++n)
+      v[n] = f[n] >= 0 ? cmulx(line[f[n]], __ldg(ch + n1 + Q * n)) : make_double2(0.0, 0.0);
+    bfly_finish<R, false>(x, n1, Q, tb[n1], v);
+  }
+}
+
 // Warp-local pass: after the first passes of a DIF FFT the array splits into independent blocks (the butterflies
 // of a pass with span S only touch one aligned block of S points).  Once the leading radices' product is a multiple
 // of the warp count W, warp w owns the contiguous region [w Mw, (w + 1) Mw), Mw = M / W, and runs the remaining
@@ -315,6 +339,35 @@ __device__ void fft_pass(double2* x, int M, int S, int R, const double2* tb, int
     case 6: pass_loop<6, INV, ZT>(x, M, S, tb, nz); break;
     case 7: pass_loop<7, INV, ZT>(x, M, S, tb, nz); break;
     case 8: pass_loop<8, INV, ZT>(x, M, S, tb, nz); break;
+  }
+  __syncthreads();
+}
+
+template <bool BIG>
+__device__ void fft_first_gather(const DevParams& P, double2* x, int fi, const double2* tb, int p,
+                                 const double2* __restrict__ line, const double2* __restrict__ ch,
+                                 const int32_t* __restrict__ dlog) {
+  const int M = P.fft_M[fi];
+  const int R = P.fft_radix[fi * kMaxFftPasses];
+  if constexpr (BIG) {
+    switch (R) {
+      case 6: pass_loop_gather<6>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+      case 9: pass_loop_gather<9>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+      case 10: pass_loop_gather<10>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+      case 12: pass_loop_gather<12>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+      case 14: pass_loop_gather<14>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+      case 15: pass_loop_gather<15>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+      case 16: pass_loop_gather<16>(x, M, p, tb, line, ch, dlog); __syncthreads(); return;
+    }
+  }
+  switch (R) {
+    case 2: pass_loop_gather<2>(x, M, p, tb, line, ch, dlog); break;
+    case 3: pass_loop_gather<3>(x, M, p, tb, line, ch, dlog); break;
+    case 4: pass_loop_gather<4>(x, M, p, tb, line, ch, dlog); break;
+    case 5: pass_loop_gather<5>(x, M, p, tb, line, ch, dlog); break;
+    case 6: pass_loop_gather<6>(x, M, p, tb, line, ch, dlog); break;
+    case 7: pass_loop_gather<7>(x, M, p, tb, line, ch, dlog); break;
+    case 8: pass_loop_gather<8>(x, M, p, tb, line, ch, dlog); break;
   }
   __syncthreads();
 }
@@ -429,15 +482,17 @@ template <bool BIG, bool WL = false>
 // nz < M: only x[0, nz) holds data, the rest is implicit zero padding (never stored, see pass_loop ZT)
 // WL: passes >= wl are warp-local (pass_loop_w); a warp-local last pass ends with a block barrier unless the
 // caller continues on the warp's own region (skip_last: the fused middle)
+// ps0 = 1: the first pass already ran (fft_first_gather)
 __device__ void fft_dif(const DevParams& P, double2* x, int fi, const double2* tb, int skip_last = 0, int nz = -1,
-                        int wl = kMaxFftPasses) {
+                        int wl = kMaxFftPasses, int ps0 = 0) {
   if constexpr (!WL) wl = kMaxFftPasses;
   const int M = P.fft_M[fi];
   const int8_t* radix = P.fft_radix + fi * kMaxFftPasses;
   const int32_t* off = P.fft_tw_off + fi * kMaxFftPasses;
   const int npass = P.fft_npass[fi];
   int S = M;
-  for (int ps = 0; ps < npass - skip_last; ++ps) {
+  for (int ps = 0; ps < ps0; ++ps) S /= radix[ps];
+  for (int ps = ps0; ps < npass - skip_last; ++ps) {
     const int R = radix[ps];
     if (ps == 0 && nz >= 0 && nz < M) fft_pass<false, BIG, true>(x, M, S, R, tb + (off[ps] - off[0]), nz);
     else if (WL && ps >= wl) {
@@ -1083,6 +1138,7 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
   const int tslot = P.st_slot[s];                     // table slot of the signal's prime
   const double2* ch = P.chirp + (int64_t)tslot * P.p_stride;
   double2* line = P.lines + ((int64_t)s * n_lines + n) * P.p_stride;
+  const bool gather_first = M <= P.fused_load && P.lines_log && !P.fused_sample && ksplit == 1 && P.fft_npass[fi] >= 2;
   if (P.fused_sample) {
     // NEXT #3 fusion: this CTA samples its own line (Alg. 2 l.13-14; Eq. (41)) -- s_n[h] = sum_j C[j][n] W_p^{h u_j}
     // with rows f in discrete-log order (h = g^f, root of (f, j) = dl_root[f + e_j], W_p[0] = 1 for e_j < 0 and
@@ -1126,6 +1182,8 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
       x[__ldg(pw + f0)] = cmulx(make_double2(ar0, ai0), __ldg(chl + f0));
       if (v1) x[__ldg(pw + f1)] = cmulx(make_double2(ar1, ai1), __ldg(chl + f1));
     }
+  } else if (gather_first) {
+    // the first DIF pass gathers the line itself (below)
   } else if (P.lines_log) {
     // the int8 exp-sum wrote the samples in discrete-log order: position f holds h = pw[f]; all of a
     // thread's loads in flight (latency-bound phase), then the chirp products scattered
@@ -1197,7 +1255,8 @@ pfft_kernel(DevParams P, int32_t n_lines, int32_t ksplit, const double2* __restr
     wl = warp_local_from(P, fi);
     if (wl > P.fft_npass[fi] - 1) wl = kMaxFftPasses;
   }
-  fft_dif<BIG, WL>(P, x, fi, tb, 1, p, wl);           // x[p, M) is implicit zero padding
+  if (gather_first) fft_first_gather<BIG>(P, x, fi, tb, p, line, ch, P.i8_dlog + (int64_t)tslot * P.i8_tstride);
+  fft_dif<BIG, WL>(P, x, fi, tb, 1, p, wl, gather_first ? 1 : 0);   // x[p, M) is implicit zero padding
   FFT_PROF_MARK(1);
   fft_mid<BIG, WL>(P, x, fi, P.V + (int64_t)tslot * P.M_stride, wl < kMaxFftPasses,
                    P.VB ? P.VB + (int64_t)tslot * P.M_stride : nullptr);

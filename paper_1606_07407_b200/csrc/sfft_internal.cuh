@@ -146,6 +146,7 @@ struct DevParams {
   int32_t log_tables;          // the discrete-log tables (i8_pw, i8_dlog, i8_chl, e_j in i8_elog) are built
   double2* dl_root;            // [n_tslots][i8_tstride] W_p[g^f] twice + W_p[0] (FP64), or null
   int32_t fused_sample;        // pfft launch flag: compute the samples in the FFT CTA (no exp-sum launch)
+  int32_t fused_load;          // pfft launch: largest FFT size whose first DIF pass gathers its discrete-log line
   int64_t i8_tstride;          // >= p_stride + 8 (bulk copies round the table up to 16 bytes)
   // line sharding: shard line_g of line_G holds line 0 and the shifted lines of reduced axes
   // [line_lo, line_lo + L - 1); its decode is split into a local test (records) and a commit after the
