@@ -238,8 +238,9 @@ __device__ __forceinline__ void pass_loop(double2* x, int M, int S, const double
 
 // First DIF pass fused with the load of a discrete-log line (int8 exp-sum iterations, ksplit = 1): the butterfly
 // of base n1 gathers its inputs h = n1 + Q n < p straight from the line (position f = log_g h, the h = 0 row at
-// f = p - 1) times the chirp -- the same products as the load phase's x[h] = line[f] chirp[h] followed by the ZT
-// first pass (chirp[h] = chl[f]: one chirp_value), without the scattered shared-memory sweep and its barrier.
+// f = p - 1) times the chirp -- the products of the load phase's x[h] = line[f] chirp[h] (chirp[h] = chl[f]: one
+// chirp_value) followed by the ZT first pass, up to the FMA contraction of the product into the butterfly, without
+// the scattered shared-memory sweep and its barrier.
 template <int R>
 __device__ __forceinline__ void pass_loop_gather(double2* x, int M, int p, const double2* __restrict__ tb,
                                                  const double2* __restrict__ line, const double2* __restrict__ ch,

@@ -585,7 +585,7 @@ def test_e2e_stall_fallback_vs_oracle(S, d, N, k, blocks, structure, n_fb, trial
         assert 0 < res.report.fallback_used <= len(used)
 
 
-def _opt_in_parity(env_var, cases):
+def _opt_in_parity(env_var, cases, value="1"):
     """Full-size parity of an opt-in code path selected by an environment knob read once per process."""
     import subprocess, sys
     code = ("import numpy as np, torch, hashlib, oracle as O, workloads as W, paper_1606_07407_b200 as S\n"
@@ -600,7 +600,7 @@ def _opt_in_parity(env_var, cases):
             "        assert hashlib.sha256(gw.tobytes()).digest() == bytes(g[k + '_w_sha256'])\n"
             "        ra = g[k + '_a']; assert np.all(np.abs(res.coeffs[i, :n].cpu().numpy() - ra) <= 1e-9 * np.abs(ra))\n"
             "print('opt-in ok')\n")
-    env = dict(os.environ, **{env_var: "1"})
+    env = dict(os.environ, **{env_var: value})
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
                          cwd=os.path.dirname(GOLD_DIR.rstrip("/")).rsplit("/tests", 1)[0])
     assert out.returncode == 0 and "opt-in ok" in out.stdout, out.stderr[-2000:]
@@ -1022,6 +1022,48 @@ def test_fft_warp_local_passes_bitwise(S):
         assert r.returncode == 0, r.stderr[-2000:]
         outs.append(r.stdout.split())
     assert len(outs[0]) == 4 and outs[0] == outs[1], outs
+
+
+def test_fft_gather_first_pass_same_products(S):
+    """The first DIF pass that gathers its discrete-log line itself (k_fft.cu pass_loop_gather, default for FFT sizes
+    up to SFFT_FFT_GATHER = 1024) forms the products x[h] = line[log_g h] * chirp[h] of the load sweep and runs the
+    same butterflies -- only the compiler's FMA contraction of the product into the butterfly differs (measured: C4
+    not bitwise): solves of C4 (M = 1008) and C3 (10080-point first iteration, small later ones) with it off (0), at
+    the default and for every size give identical counts and frequencies and coefficients within 1e-12 relative."""
+    import subprocess, sys
+    code = ("import numpy as np, torch, workloads as W, paper_1606_07407_b200 as S, sys\n"
+            "out = {}\n"
+            "for name in ('c4', 'c3'):\n"
+            "    c = W.CONFIGS[name]; w, a = W.make_batch(c, [0, 1])\n"
+            "    plan = S.sfft_plan(c.d, c.N, c.k, blocks=c.blocks, batch=2)\n"
+            "    res = S.solve(plan, torch.from_numpy(w).cuda(), torch.from_numpy(a).cuda())\n"
+            "    out[name + '_n'] = res.count.cpu().numpy(); out[name + '_w'] = res.freqs.cpu().numpy()\n"
+            "    out[name + '_a'] = res.coeffs.cpu().numpy()\n"
+            "np.savez(sys.argv[1], **out)\n")
+    root = os.path.dirname(GOLD_DIR.rstrip("/")).rsplit("/tests", 1)[0]
+    import tempfile
+    runs = []
+    with tempfile.TemporaryDirectory() as td:
+        for val in ("0", "1024", "16384"):
+            f = os.path.join(td, "g%s.npz" % val)
+            r = subprocess.run([sys.executable, "-c", code, f], env=dict(os.environ, SFFT_FFT_GATHER=val),
+                               capture_output=True, text=True, timeout=300, cwd=root)
+            assert r.returncode == 0, r.stderr[-2000:]
+            runs.append(dict(np.load(f)))
+    base = runs[0]
+    for other in runs[1:]:
+        for name in ("c4", "c3"):
+            n = base[name + "_n"]
+            assert np.array_equal(n, other[name + "_n"]) and np.array_equal(base[name + "_w"], other[name + "_w"])
+            for i, ni in enumerate(n):
+                ra, ga = base[name + "_a"][i, :ni], other[name + "_a"][i, :ni]
+                assert np.all(np.abs(ga - ra) <= 1e-12 * np.abs(ra)), (name, i)
+
+
+def test_e2e_fft_gather_every_size(S):
+    """The gathering first pass at every FFT size (SFFT_FFT_GATHER=16384) against the golden oracle at full size
+    (C3, C4, C5 seeds)."""
+    _opt_in_parity("SFFT_FFT_GATHER", (("c3", [0, 1]), ("c4", [0]), ("c5", [0])), value="16384")
 
 
 def test_e2e_block_wide_fft_passes(S):
