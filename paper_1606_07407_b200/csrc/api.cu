@@ -13,8 +13,29 @@
 #include <functional>
 #include <memory>
 #include <new>
+#include <nvtx3/nvToolsExt.h>
 
 #include "sfft_internal.cuh"
+
+// NVTX ranges around the solve, its iterations and their kernel classes (layer 8: tracing).
+// Off unless SFFT_NVTX=1: the header-only NVTX3 stubs cost nothing once resolved, but the default path stays
+// exactly the timed one.  Ranges bracket the host's launches (tools correlate them with the kernels).
+namespace {
+inline bool nvtx_on() {
+  static const bool on = getenv("SFFT_NVTX") && atoi(getenv("SFFT_NVTX")) != 0;
+  return on;
+}
+struct NvtxRange {
+  bool on;
+  explicit NvtxRange(const char* name) : on(nvtx_on()) { if (on) nvtxRangePushA(name); }
+  NvtxRange(const char* fmt, int v) : on(nvtx_on()) {
+    if (on) { char b[48]; snprintf(b, sizeof b, fmt, v); nvtxRangePushA(b); }
+  }
+  ~NvtxRange() { if (on) nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+}  // namespace
 
 using namespace sfft;
 
@@ -782,16 +803,20 @@ int iter_front(sfft_plan_t* P, DevParams& D, int iter, const IterPlan& it, int& 
                const std::function<int()>& mark) {
   cudaStream_t st = P->stream;
   mark();
-  if (it.fused) {
-    // no exp-sum launch: the FFT CTAs sample their lines (the mark pair stays for the profile's bookkeeping)
-    ++P->n_fused_iters;
-  } else if (it.use_i8)
-    LAUNCH(P, launch_expsum_i8(D, P->i8, it.max_p, it.n_active, it.ksplit, ptr<double2>(P, B_PART), it.max_p,
-                               P->smem_optin, st));
-  else
-    LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, it.max_p), it.max_p, it.n_active, it.ksplit,
-                            ptr<double2>(P, B_PART), it.max_p, st));
+  {
+    NvtxRange nv_x(it.fused ? "sfft expsum (fused into pfft)" : it.use_i8 ? "sfft expsum_i8" : "sfft expsum_dmma");
+    if (it.fused) {
+      // no exp-sum launch: the FFT CTAs sample their lines (the mark pair stays for the profile's bookkeeping)
+      ++P->n_fused_iters;
+    } else if (it.use_i8)
+      LAUNCH(P, launch_expsum_i8(D, P->i8, it.max_p, it.n_active, it.ksplit, ptr<double2>(P, B_PART), it.max_p,
+                                 P->smem_optin, st));
+    else
+      LAUNCH(P, launch_expsum(D, expsum_for_p(P->shape, it.max_p), it.max_p, it.n_active, it.ksplit,
+                              ptr<double2>(P, B_PART), it.max_p, st));
+  }
   mark();
+  NvtxRange nv_f("sfft pfft + select / test / decode");
   // FFT of every line with the fused select (line 0) / test + decode (lines n >= 1) epilogue -> records
   D.lines_log = it.use_i8 ? 1 : 0;
   D.fuse_decode = 1;
@@ -1346,6 +1371,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   if (rc) return rc;
   sfft_plan_t* P = plan;
   cudaStream_t st = P->stream;
+  NvtxRange nv_solve("sfft_execute");
   const int32_t batch = sig->batch;                 // signals; slots = batch G (R26)
   DevParams D = dev_params(P, batch * P->spec_slots);
   D.spec_G = P->spec_G;
@@ -1370,6 +1396,7 @@ int sfft_execute(sfft_plan_t* plan, const sfft_signal_t* sig, int32_t* out_freqs
   std::vector<size_t> it_marks, it_i8;
   int n_bound = batch * P->spec_slots;
   for (; iter <= P->max_iter; ++iter) {
+    NvtxRange nv_it("sfft iteration %d", iter);
     IterPlan it;
     if ((rc = iter_setup(P, D, iter, &it, launches, n_bound))) return rc;
     n_bound = it.n_active;

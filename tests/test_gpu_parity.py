@@ -625,6 +625,13 @@ def test_e2e_fused_commit(S):
     _opt_in_parity("SFFT_FUSE_COMMIT", (("c3", [0, 1]), ("c4", [0]), ("c5", [0, 1])))
 
 
+def test_e2e_nvtx_ranges(S):
+    """SFFT_NVTX=1 pushes NVTX ranges around the solve, its iterations and their kernel classes (SURVEY section 4,
+    layer 8).  With no tool attached the header-only NVTX3 stubs must leave the results untouched: golden-oracle
+    parity of an int8-path (C3), an FP64-path (C2, fused sampling) and a fallback (C5) workload."""
+    _opt_in_parity("SFFT_NVTX", (("c3", [0, 1]), ("c2", [0, 1, 2]), ("c5", [0])))
+
+
 # ------------------------------------------------------------------ line sharding (SURVEY 8(e))
 def _shard_plans(S, c, G, blocks=None, **kw):
     return [_plan(S, c, blocks, line_shards=G, line_rank=g, **kw) for g in range(G)]
