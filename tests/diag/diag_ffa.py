@@ -1,9 +1,9 @@
 """Diagnostic (GPU box): forced-false-accept workloads, GPU vs oracle per seed -- solo (batch 1) and batched --
-first divergent iteration of the (p, accepted) trace.  Usage: python tools/diag_ffa.py [ci] [extra] [path]"""
+first divergent iteration of the (p, accepted) trace.  Usage: python tests/diag/diag_ffa.py [ci] [extra] [path]"""
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402

@@ -1,9 +1,9 @@
 """Diagnostic (GPU box): registry after t iterations, GPU vs oracle, for one forced-false-accept seed.
-Usage: python tools/diag_ffa2.py ci extra path seed t0 t1"""
+Usage: python tests/diag/diag_ffa2.py ci extra path seed t0 t1"""
 import os
 import sys
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import numpy as np  # noqa: E402
