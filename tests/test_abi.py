@@ -56,6 +56,22 @@ def test_product_path_has_no_oracle_reference():
                 assert "import oracle" not in txt and "sfft_oracle" not in txt and "liboracle" not in txt, f
 
 
+def test_oracle_is_reached_only_from_tests_smoke_and_the_bench_baseline():
+    """Outside tests/ only `__graft_entry__` (build of the checker, smoke) and bench.py's `oracle_run` (the
+    cpu_baseline leg / the reference arm) import the oracle; tools/, workloads/ and the package never do."""
+    import re
+    pat = re.compile(r"^\s*(import oracle|from oracle)\b", re.M)
+    for sub in ("tools", "workloads", "paper_1606_07407_b200"):
+        for dirpath, _, files in os.walk(os.path.join(ROOT, sub)):
+            for f in files:
+                if f.endswith(".py"):
+                    assert not pat.search(open(os.path.join(dirpath, f)).read()), os.path.join(sub, f)
+    bench = open(os.path.join(ROOT, "bench.py")).read()
+    hits = [m.start() for m in pat.finditer(bench)]
+    assert len(hits) == 1
+    assert bench.rfind("\ndef ", 0, hits[0]) == bench.find("\ndef oracle_run(")
+
+
 def test_binding_raises_without_cuda():
     import torch
     if torch.cuda.is_available():
