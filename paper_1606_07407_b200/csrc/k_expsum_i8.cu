@@ -646,7 +646,9 @@ cudaError_t launch_expsum_i8(const DevParams& P, const I8Config& c, int32_t max_
   A.n_slots = n_signals;
   A.dbg = getenv("SFFT_I8_DBG") ? atoi(getenv("SFFT_I8_DBG")) : 0;
   A.nap = getenv("SFFT_I8_NAP") ? atoi(getenv("SFFT_I8_NAP")) : 256;
-  A.gnap = getenv("SFFT_I8_GNAP") ? atoi(getenv("SFFT_I8_GNAP")) : 0;
+  // generators sleep 64 ns between polls of a full A ring instead of spinning (their polls compete with the
+  // gathers of the generators that do have a slot; C3 / C5 exp-sum -0.5 % / -0.6 %, profiles/r02_experiments.md)
+  A.gnap = getenv("SFFT_I8_GNAP") ? atoi(getenv("SFFT_I8_GNAP")) : 64;
   A.relaxed = getenv("SFFT_I8_RELAXED") ? atoi(getenv("SFFT_I8_RELAXED")) : 0;
   static long long* prof_buf = nullptr;
   if (getenv("SFFT_I8_PROF")) {
